@@ -1,0 +1,1102 @@
+/*
+ * mpg_oracle.c -- TEST INFRASTRUCTURE ONLY.
+ *
+ * A plain, slow, single-threaded CPU oracle of the batched manifold walk of
+ * Fan et al., "Manifold Path Guiding for Importance Sampling Specular Chains"
+ * (arXiv 2311.12818).  It computes in fp64 (reading R24) except the seed
+ * arithmetic, which is fp32 without contraction (reading R23), and follows the
+ * algorithm step by step in the paper's order:
+ *   light sample x_L            PAPER.md:337  (§5.1 "x_L by uniformly sampling all emitters")
+ *   seed chain sampling         PAPER.md:395-421 (§5.4 init, Eq. 8), :501-512 (Eq. 13, alpha=0.5)
+ *   deduction recursion         PAPER.md:374-380 (Eq. 6)
+ *   manifold walk               PAPER.md:240-243 (Newton + reprojection), :362 (quadratic conv.)
+ *   throughput T = kappa G L    PAPER.md:229-237 (Eq. 2)
+ *   reciprocal probability      PAPER.md:582-591 (Eq. 15, trials reuse n)
+ *   sample weight w = T <1/P>   PAPER.md:427-432 (Eq. 9), estimator Eq. 3 (:267-277)
+ *   guide tables                PAPER.md:434-466 (Eqs. 10-11) as the BASELINE.json histogram
+ * Every choice the paper leaves open is a numbered reading (R1..R27) in
+ * DESIGN.md §3; the code cites them as [Rn].
+ *
+ * It shares no code, header, table or constant generator with the CUDA
+ * library under paper_2311_12818_b200/csrc; neither includes the other.  Only
+ * tests/, __graft_entry__.smoke() and bench.py's cpu_baseline may load it.
+ *
+ * Library primitives used as steps: dense LU with partial pivoting (the plain
+ * definition of "solve J d = -C"), a median-split BVH (an acceleration
+ * structure whose closest hit equals brute force; pinned in tests).
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define KMAX 8
+#define ST_CONVERGED 0
+#define ST_MAXITER 1
+#define ST_SEED_FAIL 2
+#define ST_BAD_SIDE 3
+#define ST_DEGENERATE 4
+#define ST_OCCLUDED 5
+
+/* ------------------------------------------------------------------------ */
+/* input records (mirrored by oracle/oracle.py ctypes)                       */
+/* ------------------------------------------------------------------------ */
+typedef struct {
+    int32_t kind, mat, tri_begin, tri_count; /* kind 0 sphere 1 quad 2 mesh; mat 0 conductor 1 dielectric 2 diffuse */
+    float eta_in, eta_out, reflectance, radius;
+    float center[3], origin[3], edge_u[3], edge_v[3];
+} orc_surface;
+
+typedef struct {
+    int32_t kind; /* 0 point, 1 quad area (one-sided along edge_u x edge_v) */
+    float emit;
+    float position[3], edge_u[3], edge_v[3];
+} orc_light;
+
+typedef struct {
+    int32_t mode;     /* 0 cap, 1 triangle, 2 guide-uv */
+    int32_t surf_id;
+    int32_t k;
+    uint32_t tau;     /* bit i = 1 <=> vertex i+1 is T */
+    float grid_origin[2], grid_extent[2];
+    int32_t cells_x, cells_y, bins_x, bins_y;
+    float uv_origin[2], uv_scale[2], uv_plane_y;
+    const uint64_t *prefix; /* [cells][bins] inclusive prefix sums of W' (orc_guide_tables) */
+} orc_seed_cfg;
+
+typedef struct {
+    int32_t max_iters;
+    int32_t trials;
+    uint32_t k_max;
+    int32_t pad;
+    double tol, beta0, same_chain_eps, ray_eps;
+    uint64_t seed, walk_id_base;
+} orc_opts;
+
+typedef struct {
+    int32_t status, iters;
+    uint32_t trials;
+    int32_t truncated;
+    double G, T, kappa, w;
+    double pos[KMAX][3];
+    int32_t prim[KMAX], surf[KMAX];
+    double xL[3];
+    double pdfL;
+    float target[3];
+    int32_t bin;
+    int64_t total_iters; /* Newton iterations over the primary and all trials */
+    int64_t attempts;    /* seed draws (primary + trials) */
+} orc_walk_out;
+
+/* ------------------------------------------------------------------------ */
+/* fp64 vectors                                                               */
+/* ------------------------------------------------------------------------ */
+typedef struct { double x, y, z; } v3;
+static v3 V(double x, double y, double z) { v3 r = {x, y, z}; return r; }
+static v3 vf(const float *f) { return V(f[0], f[1], f[2]); }
+static v3 add(v3 a, v3 b) { return V(a.x + b.x, a.y + b.y, a.z + b.z); }
+static v3 sub(v3 a, v3 b) { return V(a.x - b.x, a.y - b.y, a.z - b.z); }
+static v3 mul(v3 a, double s) { return V(a.x * s, a.y * s, a.z * s); }
+static double dot(v3 a, v3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
+static v3 cross(v3 a, v3 b) { return V(a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x); }
+static double len(v3 a) { return sqrt(dot(a, a)); }
+static v3 nrmz(v3 a) { return mul(a, 1.0 / len(a)); }
+static double vget(v3 a, int i) { return i == 0 ? a.x : (i == 1 ? a.y : a.z); }
+
+/* Orthonormal basis of a unit vector (Duff et al. 2017, "Building an
+ * Orthonormal Basis, Revisited") -- any basis is valid [R3,R4]. */
+static void onb(v3 n, v3 *b1, v3 *b2) {
+    double sign = copysign(1.0, n.z);
+    double a = -1.0 / (sign + n.z);
+    double b = n.x * n.y * a;
+    *b1 = V(1.0 + sign * n.x * n.x * a, sign * b, -sign * n.x);
+    *b2 = V(b, sign + n.y * n.y * a, -n.y);
+}
+
+/* ------------------------------------------------------------------------ */
+/* Philox4x32-10 (Salmon et al. 2011), key=(seed_lo,seed_hi),                 */
+/* counter=(walk_lo, walk_hi, purpose, trial)  [R2]                           */
+/* ------------------------------------------------------------------------ */
+void orc_philox(const uint32_t ctr_in[4], const uint32_t key_in[2], uint32_t out[4]) {
+    uint32_t c0 = ctr_in[0], c1 = ctr_in[1], c2 = ctr_in[2], c3 = ctr_in[3];
+    uint32_t k0 = key_in[0], k1 = key_in[1];
+    for (int r = 0; r < 10; r++) {
+        uint64_t p0 = (uint64_t)0xD2511F53u * c0;
+        uint64_t p1 = (uint64_t)0xCD9E8D57u * c2;
+        uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0;
+        uint32_t hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
+        uint32_t n0 = hi1 ^ c1 ^ k0, n1 = lo1, n2 = hi0 ^ c3 ^ k1, n3 = lo0;
+        c0 = n0; c1 = n1; c2 = n2; c3 = n3;
+        if (r < 9) { k0 += 0x9E3779B9u; k1 += 0xBB67AE85u; }
+    }
+    out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3;
+}
+
+void orc_philox_batch(const uint32_t *ctr, int64_t n, const uint32_t key[2], uint32_t *out) {
+    for (int64_t i = 0; i < n; i++) orc_philox(ctr + 4 * i, key, out + 4 * i);
+}
+
+static void draw(const orc_opts *o, uint64_t walk, uint32_t purpose, uint32_t trial, uint32_t out[4]) {
+    uint32_t ctr[4] = {(uint32_t)walk, (uint32_t)(walk >> 32), purpose, trial};
+    uint32_t key[2] = {(uint32_t)o->seed, (uint32_t)(o->seed >> 32)};
+    orc_philox(ctr, key, out);
+}
+
+/* u32 -> [0,1): (x>>8)*2^-24, exact [R2] */
+static float u01(uint32_t x) { return (float)(x >> 8) * (1.0f / 16777216.0f); }
+/* index in [0,m): floor(x*m/2^32), exact [R2] */
+static uint32_t uidx(uint32_t x, uint32_t m) { return (uint32_t)(((uint64_t)x * m) >> 32); }
+
+/* ------------------------------------------------------------------------ */
+/* scene                                                                      */
+/* ------------------------------------------------------------------------ */
+typedef struct { double lo[3], hi[3]; int32_t left, right, first, count; } bnode;
+
+typedef struct {
+    int n_surf, n_vert, n_tri, n_light;
+    orc_surface *surf;
+    orc_light *light;
+    double *P, *N; /* [n_vert*3] */
+    int32_t *I;    /* [n_tri*3] */
+    int32_t *TS;   /* [n_tri] */
+    int32_t *order;
+    bnode *nodes;
+    int n_nodes;
+    double extent;
+} orc_scene;
+
+static v3 vtx(const orc_scene *s, int i) { return V(s->P[3 * i], s->P[3 * i + 1], s->P[3 * i + 2]); }
+static v3 vnr(const orc_scene *s, int i) { return V(s->N[3 * i], s->N[3 * i + 1], s->N[3 * i + 2]); }
+
+static const double *g_cent; static int g_axis;
+static int cmp_cent(const void *a, const void *b) {
+    double ca = g_cent[3 * (*(const int32_t *)a) + g_axis], cb = g_cent[3 * (*(const int32_t *)b) + g_axis];
+    if (ca < cb) return -1;
+    if (ca > cb) return 1;
+    return (*(const int32_t *)a) - (*(const int32_t *)b);
+}
+
+static int build_node(orc_scene *s, const double *cent, int first, int count) {
+    int id = s->n_nodes++;
+    bnode *nd = &s->nodes[id];
+    for (int a = 0; a < 3; a++) { nd->lo[a] = 1e300; nd->hi[a] = -1e300; }
+    double clo[3] = {1e300, 1e300, 1e300}, chi[3] = {-1e300, -1e300, -1e300};
+    for (int j = first; j < first + count; j++) {
+        int t = s->order[j];
+        for (int c = 0; c < 3; c++) {
+            int vi = s->I[3 * t + c];
+            for (int a = 0; a < 3; a++) {
+                double v = s->P[3 * vi + a];
+                if (v < nd->lo[a]) nd->lo[a] = v;
+                if (v > nd->hi[a]) nd->hi[a] = v;
+            }
+        }
+        for (int a = 0; a < 3; a++) {
+            if (cent[3 * t + a] < clo[a]) clo[a] = cent[3 * t + a];
+            if (cent[3 * t + a] > chi[a]) chi[a] = cent[3 * t + a];
+        }
+    }
+    if (count <= 4) { nd->left = nd->right = -1; nd->first = first; nd->count = count; return id; }
+    int axis = 0;
+    for (int a = 1; a < 3; a++) if (chi[a] - clo[a] > chi[axis] - clo[axis]) axis = a;
+    g_cent = cent; g_axis = axis;
+    qsort(s->order + first, (size_t)count, sizeof(int32_t), cmp_cent); /* median split */
+    int half = count / 2;
+    int l = build_node(s, cent, first, half);
+    int r = build_node(s, cent, first + half, count - half);
+    nd = &s->nodes[id];
+    nd->left = l; nd->right = r; nd->first = first; nd->count = 0;
+    return id;
+}
+
+void orc_scene_destroy(void *h) {
+    orc_scene *s = (orc_scene *)h;
+    if (!s) return;
+    free(s->surf); free(s->light); free(s->P); free(s->N); free(s->I); free(s->TS); free(s->order); free(s->nodes);
+    free(s);
+}
+
+/* Copies everything; builds a median-split BVH over all mesh triangles. */
+void *orc_scene_create(const orc_surface *surf, int n_surf, const float *pos, const float *nrm, int n_vert,
+                       const int32_t *idx, const int32_t *tri_surf, int n_tri, const orc_light *light, int n_light) {
+    orc_scene *s = (orc_scene *)calloc(1, sizeof(orc_scene));
+    s->n_surf = n_surf; s->n_vert = n_vert; s->n_tri = n_tri; s->n_light = n_light;
+    s->surf = (orc_surface *)malloc(sizeof(orc_surface) * (size_t)(n_surf > 0 ? n_surf : 1));
+    memcpy(s->surf, surf, sizeof(orc_surface) * (size_t)n_surf);
+    s->light = (orc_light *)malloc(sizeof(orc_light) * (size_t)(n_light > 0 ? n_light : 1));
+    memcpy(s->light, light, sizeof(orc_light) * (size_t)n_light);
+    s->P = (double *)malloc(sizeof(double) * 3 * (size_t)(n_vert + 1));
+    s->N = (double *)malloc(sizeof(double) * 3 * (size_t)(n_vert + 1));
+    for (int i = 0; i < 3 * n_vert; i++) { s->P[i] = pos[i]; s->N[i] = nrm[i]; }
+    s->I = (int32_t *)malloc(sizeof(int32_t) * 3 * (size_t)(n_tri + 1));
+    s->TS = (int32_t *)malloc(sizeof(int32_t) * (size_t)(n_tri + 1));
+    memcpy(s->I, idx, sizeof(int32_t) * 3 * (size_t)n_tri);
+    memcpy(s->TS, tri_surf, sizeof(int32_t) * (size_t)n_tri);
+    s->order = (int32_t *)malloc(sizeof(int32_t) * (size_t)(n_tri + 1));
+    s->nodes = (bnode *)malloc(sizeof(bnode) * (size_t)(2 * n_tri + 2));
+    s->n_nodes = 0;
+    if (n_tri > 0) {
+        double *cent = (double *)malloc(sizeof(double) * 3 * (size_t)n_tri);
+        for (int t = 0; t < n_tri; t++) {
+            s->order[t] = t;
+            for (int a = 0; a < 3; a++)
+                cent[3 * t + a] = (s->P[3 * s->I[3 * t] + a] + s->P[3 * s->I[3 * t + 1] + a] + s->P[3 * s->I[3 * t + 2] + a]) / 3.0;
+        }
+        build_node(s, cent, 0, n_tri);
+        free(cent);
+    }
+    /* scene extent: bbox diagonal of all surfaces and lights [R10] */
+    double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+#define GROW(p) do { for (int a_ = 0; a_ < 3; a_++) { double q_ = vget((p), a_); if (q_ < lo[a_]) lo[a_] = q_; if (q_ > hi[a_]) hi[a_] = q_; } } while (0)
+    for (int i = 0; i < n_surf; i++) {
+        const orc_surface *f = &surf[i];
+        if (f->kind == 0) { v3 c = vf(f->center); GROW(sub(c, V(f->radius, f->radius, f->radius))); GROW(add(c, V(f->radius, f->radius, f->radius))); }
+        else if (f->kind == 1) { v3 o = vf(f->origin), u = vf(f->edge_u), w = vf(f->edge_v); GROW(o); GROW(add(o, u)); GROW(add(o, w)); GROW(add(add(o, u), w)); }
+        else for (int t = f->tri_begin; t < f->tri_begin + f->tri_count; t++) for (int c = 0; c < 3; c++) GROW(vtx(s, s->I[3 * t + c]));
+    }
+    for (int i = 0; i < n_light; i++) {
+        const orc_light *l = &light[i];
+        v3 c = vf(l->position);
+        if (l->kind == 1) {
+            v3 u = mul(vf(l->edge_u), 0.5), w = mul(vf(l->edge_v), 0.5);
+            GROW(add(add(c, u), w)); GROW(sub(sub(c, u), w)); GROW(add(sub(c, u), w)); GROW(sub(add(c, u), w));
+        } else GROW(c);
+    }
+#undef GROW
+    s->extent = len(sub(V(hi[0], hi[1], hi[2]), V(lo[0], lo[1], lo[2])));
+    return s;
+}
+
+double orc_scene_extent(const void *h) { return ((const orc_scene *)h)->extent; }
+
+/* ------------------------------------------------------------------------ */
+/* ray intersection: r(x, w) of Eq. 6 and V of Eq. 2          */
+/* ------------------------------------------------------------------------ */
+typedef struct { double t; int prim, surf; v3 p; } hit_t;
+
+/* Moller-Trumbore, double-sided; returns t or -1; u,v barycentric */
+static double tri_isect(v3 o, v3 d, v3 v0, v3 e1, v3 e2, double *pu, double *pv, int quad) {
+    v3 pvec = cross(d, e2);
+    double det = dot(e1, pvec);
+    if (det == 0.0) return -1.0;
+    double inv = 1.0 / det;
+    v3 tvec = sub(o, v0);
+    double u = dot(tvec, pvec) * inv;
+    if (u < 0.0 || u > 1.0) return -1.0;
+    v3 qvec = cross(tvec, e1);
+    double v = dot(d, qvec) * inv;
+    if (v < 0.0 || (quad ? v > 1.0 : u + v > 1.0)) return -1.0;
+    if (pu) *pu = u;
+    if (pv) *pv = v;
+    return dot(e2, qvec) * inv;
+}
+
+static int surf_is_specular(const orc_scene *s, int sid) { return s->surf[sid].mat != 2; }
+
+/* analytic surfaces, brute force; updates best if closer */
+static void isect_analytic(const orc_scene *s, v3 o, v3 d, double tmin, int spec_only, hit_t *best) {
+    for (int i = 0; i < s->n_surf; i++) {
+        const orc_surface *f = &s->surf[i];
+        if (spec_only && !surf_is_specular(s, i)) continue;
+        if (f->kind == 0) {
+            v3 oc = sub(o, vf(f->center));
+            double b = dot(oc, d), c = dot(oc, oc) - (double)f->radius * f->radius;
+            double disc = b * b - c;
+            if (disc < 0.0) continue;
+            double sq = sqrt(disc);
+            double ts[2] = {-b - sq, -b + sq};
+            for (int j = 0; j < 2; j++)
+                if (ts[j] > tmin && ts[j] < best->t) { best->t = ts[j]; best->prim = -1; best->surf = i; break; }
+        } else if (f->kind == 1) {
+            double t = tri_isect(o, d, vf(f->origin), vf(f->edge_u), vf(f->edge_v), NULL, NULL, 1);
+            if (t > tmin && t < best->t) { best->t = t; best->prim = -1; best->surf = i; }
+        }
+    }
+}
+
+static void isect_tri(const orc_scene *s, int t, v3 o, v3 d, double tmin, int spec_only, hit_t *best) {
+    int sid = s->TS[t];
+    if (spec_only && !surf_is_specular(s, sid)) return;
+    v3 v0 = vtx(s, s->I[3 * t]), v1 = vtx(s, s->I[3 * t + 1]), v2 = vtx(s, s->I[3 * t + 2]);
+    double th = tri_isect(o, d, v0, sub(v1, v0), sub(v2, v0), NULL, NULL, 0);
+    if (th > tmin && th < best->t) { best->t = th; best->prim = t; best->surf = sid; }
+}
+
+static int box_hit(const bnode *n, v3 o, v3 inv, double tmin, double tmax) {
+    double t0 = tmin, t1 = tmax;
+    for (int a = 0; a < 3; a++) {
+        double oa = vget(o, a), ia = vget(inv, a);
+        double ta = (n->lo[a] - oa) * ia, tb = (n->hi[a] - oa) * ia;
+        if (ta != ta) ta = -1e300; /* 0*inf */
+        if (tb != tb) tb = 1e300;
+        if (ta > tb) { double x = ta; ta = tb; tb = x; }
+        if (ta > t0) t0 = ta;
+        if (tb < t1) t1 = tb;
+        if (t0 > t1) return 0;
+    }
+    return 1;
+}
+
+/* closest hit with t in (tmin, tmax); use_bvh=0 is the brute-force pin */
+static hit_t closest(const orc_scene *s, v3 o, v3 d, double tmin, double tmax, int spec_only, int use_bvh) {
+    hit_t best; best.t = tmax; best.prim = -2; best.surf = -1; best.p = V(0, 0, 0);
+    isect_analytic(s, o, d, tmin, spec_only, &best);
+    if (s->n_tri > 0) {
+        if (!use_bvh) {
+            for (int t = 0; t < s->n_tri; t++) isect_tri(s, t, o, d, tmin, spec_only, &best);
+        } else {
+            v3 inv = V(1.0 / d.x, 1.0 / d.y, 1.0 / d.z);
+            int stack[128], sp = 0;
+            stack[sp++] = 0;
+            while (sp > 0) {
+                const bnode *n = &s->nodes[stack[--sp]];
+                if (!box_hit(n, o, inv, tmin, best.t)) continue;
+                if (n->left < 0) {
+                    for (int j = n->first; j < n->first + n->count; j++) isect_tri(s, s->order[j], o, d, tmin, spec_only, &best);
+                } else {
+                    stack[sp++] = n->left;
+                    stack[sp++] = n->right;
+                }
+            }
+        }
+    }
+    if (best.surf >= 0) best.p = add(o, mul(d, best.t));
+    return best;
+}
+
+/* ------------------------------------------------------------------------ */
+/* local geometry at a vertex                                                 */
+/* ------------------------------------------------------------------------ */
+typedef struct { v3 p; int prim, surf; } cvtx;
+
+/* geometric normal (outward [R9]) */
+static v3 geo_normal(const orc_scene *s, const cvtx *x) {
+    const orc_surface *f = &s->surf[x->surf];
+    if (f->kind == 0) return nrmz(sub(x->p, vf(f->center)));
+    if (f->kind == 1) return nrmz(cross(vf(f->edge_u), vf(f->edge_v)));
+    int t = x->prim;
+    v3 v0 = vtx(s, s->I[3 * t]), v1 = vtx(s, s->I[3 * t + 1]), v2 = vtx(s, s->I[3 * t + 2]);
+    return nrmz(cross(sub(v1, v0), sub(v2, v0)));
+}
+
+/* shading normal n_s and, for a tangent displacement v, its derivative d_v n_s.
+ * mesh: Phong interpolation n = n~/|n~|, n~ = sum b_j n_j (BASELINE.json configs[1]
+ * "interpolated vertex normals"); derivative from the barycentric gradient [R3]. */
+static v3 shading_normal(const orc_scene *s, const cvtx *x, int nv, const v3 *vs, v3 *dns) {
+    const orc_surface *f = &s->surf[x->surf];
+    if (f->kind == 0) {
+        v3 r = sub(x->p, vf(f->center));
+        double rl = len(r);
+        v3 n = mul(r, 1.0 / rl);
+        for (int j = 0; j < nv; j++) dns[j] = mul(sub(vs[j], mul(n, dot(n, vs[j]))), 1.0 / rl);
+        return n;
+    }
+    if (f->kind == 1) {
+        for (int j = 0; j < nv; j++) dns[j] = V(0, 0, 0);
+        return nrmz(cross(vf(f->edge_u), vf(f->edge_v)));
+    }
+    int t = x->prim;
+    int i0 = s->I[3 * t], i1 = s->I[3 * t + 1], i2 = s->I[3 * t + 2];
+    v3 v0 = vtx(s, i0), e1 = sub(vtx(s, i1), v0), e2 = sub(vtx(s, i2), v0);
+    v3 Ng = cross(e1, e2);
+    double nn = dot(Ng, Ng);
+    v3 r = sub(x->p, v0);
+    double b1 = dot(cross(r, e2), Ng) / nn, b2 = dot(cross(e1, r), Ng) / nn, b0 = 1.0 - b1 - b2;
+    v3 n0 = vnr(s, i0), n1 = vnr(s, i1), n2 = vnr(s, i2);
+    v3 nt = add(add(mul(n0, b0), mul(n1, b1)), mul(n2, b2));
+    double nl = len(nt);
+    v3 n = mul(nt, 1.0 / nl);
+    for (int j = 0; j < nv; j++) {
+        double db1 = dot(cross(vs[j], e2), Ng) / nn, db2 = dot(cross(e1, vs[j]), Ng) / nn;
+        v3 dnt = add(mul(sub(n1, n0), db1), mul(sub(n2, n0), db2));
+        dns[j] = mul(sub(dnt, mul(n, dot(n, dnt))), 1.0 / nl);
+    }
+    return n;
+}
+
+/* ------------------------------------------------------------------------ */
+/* specular constraint at vertex i (generalized half vector, [R1][R2])        */
+/* ------------------------------------------------------------------------ */
+typedef struct {
+    v3 wi, wo, h, n, s, t, ng, sg, tg;
+    double li, lo, eta_i, eta_o, hlen;
+    v3 dn[2]; /* d n_s along sg, tg */
+} cterm;
+
+/* returns 0 on a degenerate configuration */
+static int cterm_eval(const orc_scene *sc, v3 a, const cvtx *x, v3 b, int isT, cterm *c) {
+    const orc_surface *f = &sc->surf[x->surf];
+    v3 da = sub(a, x->p), db = sub(b, x->p);
+    c->li = len(da); c->lo = len(db);
+    if (!(c->li > 0.0) || !(c->lo > 0.0)) return 0;
+    c->wi = mul(da, 1.0 / c->li);
+    c->wo = mul(db, 1.0 / c->lo);
+    c->ng = geo_normal(sc, x);
+    onb(c->ng, &c->sg, &c->tg); /* step parameterization [R4] */
+    v3 vs[2] = {c->sg, c->tg};
+    c->n = shading_normal(sc, x, 2, vs, c->dn);
+    onb(c->n, &c->s, &c->t); /* constraint frame [R3] */
+    if (isT) {
+        int out = dot(c->wi, c->ng) > 0.0; /* media from the side of w_i [R9] */
+        c->eta_i = out ? f->eta_out : f->eta_in;
+        c->eta_o = out ? f->eta_in : f->eta_out;
+    } else {
+        c->eta_i = c->eta_o = 1.0;
+    }
+    v3 ht = add(mul(c->wi, c->eta_i), mul(c->wo, c->eta_o));
+    c->hlen = len(ht);
+    if (!(c->hlen > 0.0) || !isfinite(c->hlen)) return 0;
+    c->h = mul(ht, 1.0 / c->hlen);
+    return 1;
+}
+
+static void cterm_C(const cterm *c, double C[2]) { C[0] = dot(c->s, c->h); C[1] = dot(c->t, c->h); }
+
+/* dh for a change u of h~ : P_h u = (u - h(h.u))/|h~| */
+static v3 dh_of(const cterm *c, v3 u) { return mul(sub(u, mul(c->h, dot(c->h, u))), 1.0 / c->hlen); }
+/* P_i v, P_o v */
+static v3 Pi(const cterm *c, v3 v) { return mul(sub(v, mul(c->wi, dot(c->wi, v))), 1.0 / c->li); }
+static v3 Po(const cterm *c, v3 v) { return mul(sub(v, mul(c->wo, dot(c->wo, v))), 1.0 / c->lo); }
+
+/* dC/d(x_{i-1}) along v  (block L) */
+static void dC_da(const cterm *c, v3 v, double out[2]) {
+    v3 dh = dh_of(c, mul(Pi(c, v), c->eta_i));
+    out[0] = dot(c->s, dh); out[1] = dot(c->t, dh);
+}
+/* dC/d(x_{i+1}) along v  (block U, and D_L for the light) */
+static void dC_db(const cterm *c, v3 v, double out[2]) {
+    v3 dh = dh_of(c, mul(Po(c, v), c->eta_o));
+    out[0] = dot(c->s, dh); out[1] = dot(c->t, dh);
+}
+/* dC/d(x_i) along basis vector j (block D); frame moves by minimal rotation [R3] */
+static void dC_dp(const cterm *c, int j, double out[2]) {
+    v3 v = j == 0 ? c->sg : c->tg;
+    v3 u = sub(mul(Pi(c, v), -c->eta_i), mul(Po(c, v), c->eta_o));
+    v3 dh = dh_of(c, u);
+    double hn = dot(c->h, c->n);
+    out[0] = dot(c->s, dh) - hn * dot(c->s, c->dn[j]);
+    out[1] = dot(c->t, dh) - hn * dot(c->t, c->dn[j]);
+}
+
+/* whole chain: C (2k) and dense J (2k x 2k, row-major); returns 0 if degenerate */
+static int chain_system(const orc_scene *sc, int k, uint32_t tau, v3 xD, v3 xL, const cvtx *x, double *C, double *J,
+                        cterm *terms) {
+    int m = 2 * k;
+    if (J) memset(J, 0, sizeof(double) * (size_t)(m * m));
+    for (int i = 0; i < k; i++) {
+        v3 a = i == 0 ? xD : x[i - 1].p;
+        v3 b = i == k - 1 ? xL : x[i + 1].p;
+        if (!cterm_eval(sc, a, &x[i], b, (tau >> i) & 1u, &terms[i])) return 0;
+        cterm_C(&terms[i], C + 2 * i);
+    }
+    if (J) {
+        for (int i = 0; i < k; i++) {
+            double o2[2];
+            for (int j = 0; j < 2; j++) {
+                dC_dp(&terms[i], j, o2);
+                J[(2 * i) * m + 2 * i + j] = o2[0];
+                J[(2 * i + 1) * m + 2 * i + j] = o2[1];
+                if (i > 0) {
+                    v3 v = j == 0 ? terms[i - 1].sg : terms[i - 1].tg;
+                    dC_da(&terms[i], v, o2);
+                    J[(2 * i) * m + 2 * (i - 1) + j] = o2[0];
+                    J[(2 * i + 1) * m + 2 * (i - 1) + j] = o2[1];
+                }
+                if (i < k - 1) {
+                    v3 v = j == 0 ? terms[i + 1].sg : terms[i + 1].tg;
+                    dC_db(&terms[i], v, o2);
+                    J[(2 * i) * m + 2 * (i + 1) + j] = o2[0];
+                    J[(2 * i + 1) * m + 2 * (i + 1) + j] = o2[1];
+                }
+            }
+        }
+    }
+    for (int i = 0; i < m; i++) if (!isfinite(C[i])) return 0;
+    return 1;
+}
+
+/* dense LU with partial pivoting; solves A X = B for nr right-hand sides
+ * (B is m x nr row-major, overwritten by X). returns 0 if singular. */
+static int lu_solve(double *A, int m, double *B, int nr) {
+    for (int col = 0; col < m; col++) {
+        int piv = col;
+        for (int r = col + 1; r < m; r++) if (fabs(A[r * m + col]) > fabs(A[piv * m + col])) piv = r;
+        if (!(fabs(A[piv * m + col]) > 0.0)) return 0;
+        if (piv != col) {
+            for (int c = 0; c < m; c++) { double t = A[col * m + c]; A[col * m + c] = A[piv * m + c]; A[piv * m + c] = t; }
+            for (int c = 0; c < nr; c++) { double t = B[col * nr + c]; B[col * nr + c] = B[piv * nr + c]; B[piv * nr + c] = t; }
+        }
+        for (int r = col + 1; r < m; r++) {
+            double f = A[r * m + col] / A[col * m + col];
+            if (f == 0.0) continue;
+            for (int c = col; c < m; c++) A[r * m + c] -= f * A[col * m + c];
+            for (int c = 0; c < nr; c++) B[r * nr + c] -= f * B[col * nr + c];
+        }
+    }
+    for (int r = m - 1; r >= 0; r--) {
+        for (int c = 0; c < nr; c++) {
+            double acc = B[r * nr + c];
+            for (int j = r + 1; j < m; j++) acc -= A[r * m + j] * B[j * nr + c];
+            B[r * nr + c] = acc / A[r * m + r];
+        }
+    }
+    for (int i = 0; i < m * nr; i++) if (!isfinite(B[i])) return 0;
+    return 1;
+}
+
+/* ------------------------------------------------------------------------ */
+/* the manifold walk: Newton + sequential ray-traced reprojection [R5-R7]    */
+/* ------------------------------------------------------------------------ */
+static int newton(const orc_scene *sc, const orc_opts *o, int k, uint32_t tau, v3 xD, v3 xL, cvtx *x, int *iters,
+                  double eps, double *res_hist) {
+    double C[2 * KMAX], J[4 * KMAX * KMAX], D[2 * KMAX];
+    cterm terms[KMAX];
+    double beta = o->beta0;
+    int m = 2 * k;
+    for (int it = 0;; it++) {
+        *iters = it;
+        if (!chain_system(sc, k, tau, xD, xL, x, C, J, terms)) return ST_DEGENERATE;
+        double nrm = 0.0;
+        for (int i = 0; i < m; i++) if (fabs(C[i]) > nrm) nrm = fabs(C[i]);
+        if (res_hist) res_hist[it] = nrm;
+        if (nrm < o->tol) return ST_CONVERGED;
+        if (it == o->max_iters) return ST_MAXITER;
+        for (int i = 0; i < m; i++) D[i] = -C[i];
+        if (!lu_solve(J, m, D, 1)) return ST_DEGENERATE;
+        /* proposed points q_i on the geometric tangent planes */
+        cvtx y[KMAX];
+        int ok = 1;
+        v3 prev = xD;
+        for (int i = 0; i < k && ok; i++) {
+            v3 q = add(x[i].p, mul(add(mul(terms[i].sg, D[2 * i]), mul(terms[i].tg, D[2 * i + 1])), beta));
+            v3 dir = sub(q, prev);
+            double dl = len(dir);
+            if (!(dl > 0.0)) { ok = 0; break; }
+            dir = mul(dir, 1.0 / dl);
+            hit_t h = closest(sc, prev, dir, eps, 1e300, 1, 1);
+            if (h.surf < 0 || h.surf != x[i].surf) { ok = 0; break; }
+            y[i].p = h.p; y[i].prim = h.prim; y[i].surf = h.surf;
+            prev = h.p;
+        }
+        if (ok) { for (int i = 0; i < k; i++) x[i] = y[i]; beta = beta * 2.0 < 1.0 ? beta * 2.0 : 1.0; }
+        else beta *= 0.5;
+    }
+}
+
+/* sidedness per tau_i with the geometric normal [R8][R9] */
+static int sides_ok(const orc_scene *sc, int k, uint32_t tau, v3 xD, v3 xL, const cvtx *x) {
+    for (int i = 0; i < k; i++) {
+        v3 a = i == 0 ? xD : x[i - 1].p, b = i == k - 1 ? xL : x[i + 1].p;
+        v3 ng = geo_normal(sc, &x[i]);
+        double di = dot(sub(a, x[i].p), ng), dd = dot(sub(b, x[i].p), ng);
+        if ((tau >> i) & 1u) { if (!(di * dd < 0.0)) return 0; }
+        else { if (!(di * dd > 0.0)) return 0; }
+    }
+    return 1;
+}
+
+/* V: any hit against all surfaces on every segment, t in (eps, len-eps) */
+static int visible_chain(const orc_scene *sc, int k, v3 xD, v3 xL, const cvtx *x, double eps) {
+    for (int j = 0; j <= k; j++) {
+        v3 a = j == 0 ? xD : x[j - 1].p, b = j == k ? xL : x[j].p;
+        v3 d = sub(b, a);
+        double l = len(d);
+        d = mul(d, 1.0 / l);
+        hit_t h = closest(sc, a, d, eps, l - eps, 0, 1);
+        if (h.surf >= 0) return 0;
+    }
+    return 1;
+}
+
+/* unpolarized dielectric Fresnel reflectance; eta1 = medium of incidence */
+double orc_fresnel(double cos_i, double eta1, double eta2) {
+    cos_i = fabs(cos_i);
+    double st2 = (eta1 / eta2) * (eta1 / eta2) * (1.0 - cos_i * cos_i);
+    if (st2 >= 1.0) return 1.0;
+    double ct = sqrt(1.0 - st2);
+    double rs = (eta1 * cos_i - eta2 * ct) / (eta1 * cos_i + eta2 * ct);
+    double rp = (eta2 * cos_i - eta1 * ct) / (eta2 * cos_i + eta1 * ct);
+    return 0.5 * (rs * rs + rp * rp);
+}
+
+/* kappa: product of Fresnel R / (1-F) T / conductor rho, times (eta_D/eta_L)^2 [R12] */
+static double kappa_of(const orc_scene *sc, int k, uint32_t tau, v3 xD, v3 xL, const cvtx *x) {
+    double kap = 1.0, etaD = 1.0, etaL = 1.0;
+    for (int i = 0; i < k; i++) {
+        const orc_surface *f = &sc->surf[x[i].surf];
+        v3 a = i == 0 ? xD : x[i - 1].p, b = i == k - 1 ? xL : x[i + 1].p;
+        v3 wi = nrmz(sub(a, x[i].p)), wo = nrmz(sub(b, x[i].p));
+        v3 ng = geo_normal(sc, &x[i]);
+        v3 dummy[1];
+        v3 ns = shading_normal(sc, &x[i], 0, NULL, dummy);
+        int out_i = dot(wi, ng) > 0.0, out_o = dot(wo, ng) > 0.0;
+        double eta_wi = out_i ? f->eta_out : f->eta_in;
+        double eta_wo = out_o ? f->eta_out : f->eta_in;
+        if (i == 0) etaD = eta_wi;
+        if (i == k - 1) etaL = eta_wo;
+        if (f->mat == 0) kap *= f->reflectance;
+        else {
+            double eta_other = out_i ? f->eta_in : f->eta_out;
+            double F = orc_fresnel(dot(wi, ns), eta_wi, eta_other);
+            kap *= ((tau >> i) & 1u) ? (1.0 - F) : F;
+        }
+    }
+    return kap * (etaD / etaL) * (etaD / etaL);
+}
+
+/* light-side axes: area light: orthonormal axes of its plane; point light: of the
+ * plane orthogonal to x_L - x_k [R11] */
+static void light_axes(const orc_light *L, v3 xL, v3 xk, v3 *l1, v3 *l2) {
+    if (L->kind == 1) {
+        v3 nl = nrmz(cross(vf(L->edge_u), vf(L->edge_v)));
+        *l1 = nrmz(vf(L->edge_u));
+        *l2 = nrmz(cross(nl, *l1));
+    } else {
+        onb(nrmz(sub(xL, xk)), l1, l2);
+    }
+}
+
+/* analytic generalized geometric term (without V): G = |n_D.w| |det dw_D/dA_L| [R11] */
+static double ggt_analytic(const orc_scene *sc, int k, uint32_t tau, v3 xD, v3 nD, v3 xL, const orc_light *L,
+                           const cvtx *x) {
+    double C[2 * KMAX], J[4 * KMAX * KMAX], B[2 * KMAX * 2];
+    cterm terms[KMAX];
+    int m = 2 * k;
+    if (!chain_system(sc, k, tau, xD, xL, x, C, J, terms)) return 0.0;
+    v3 l1, l2;
+    light_axes(L, xL, x[k - 1].p, &l1, &l2);
+    memset(B, 0, sizeof(B));
+    double d0[2], d1[2];
+    dC_db(&terms[k - 1], l1, d0);
+    dC_db(&terms[k - 1], l2, d1);
+    B[(m - 2) * 2 + 0] = -d0[0]; B[(m - 1) * 2 + 0] = -d0[1];
+    B[(m - 2) * 2 + 1] = -d1[0]; B[(m - 1) * 2 + 1] = -d1[1];
+    if (!lu_solve(J, m, B, 2)) return 0.0;
+    v3 r = sub(x[0].p, xD);
+    double rl = len(r);
+    v3 w = mul(r, 1.0 / rl);
+    v3 e1, e2;
+    onb(w, &e1, &e2);
+    double M[2][2];
+    for (int c = 0; c < 2; c++) {
+        v3 dx = add(mul(terms[0].sg, B[0 * 2 + c]), mul(terms[0].tg, B[1 * 2 + c]));
+        v3 dw = mul(sub(dx, mul(w, dot(w, dx))), 1.0 / rl);
+        M[0][c] = dot(e1, dw);
+        M[1][c] = dot(e2, dw);
+    }
+    return fabs(dot(nD, w)) * fabs(M[0][0] * M[1][1] - M[0][1] * M[1][0]);
+}
+
+/* ------------------------------------------------------------------------ */
+/* guide tables (histogram stand-in for Eqs. 10-13) [R20]                     */
+/* W_b = E_b>0 ? max(1, floor(fp32(E_b/E_max) * 2^20)) : 0;                    */
+/* W'_b = sum W + nbins*W_b  (= 1/2 uniform + 1/2 learned, Eq. 13, alpha=1/2)  */
+/* empty cell -> uniform ("learned component is absent")          */
+/* ------------------------------------------------------------------------ */
+void orc_guide_tables(const float *E, int n_cells, int n_bins, uint64_t *prefix) {
+    for (int c = 0; c < n_cells; c++) {
+        const float *e = E + (size_t)c * n_bins;
+        float emax = 0.0f;
+        for (int b = 0; b < n_bins; b++) if (e[b] > emax) emax = e[b];
+        uint64_t sumW = 0;
+        uint32_t *W = (uint32_t *)malloc(sizeof(uint32_t) * (size_t)n_bins);
+        for (int b = 0; b < n_bins; b++) {
+            uint32_t wb = 0;
+            if (e[b] > 0.0f && emax > 0.0f) {
+                float r = e[b] / emax;
+                float q = floorf(r * 1048576.0f);
+                wb = (uint32_t)q;
+                if (wb < 1u) wb = 1u;
+            }
+            W[b] = wb;
+            sumW += wb;
+        }
+        uint64_t acc = 0;
+        for (int b = 0; b < n_bins; b++) {
+            uint64_t wp = sumW == 0 ? 1u : sumW + (uint64_t)n_bins * W[b];
+            acc += wp;
+            prefix[(size_t)c * n_bins + b] = acc;
+        }
+        free(W);
+    }
+}
+
+/* ------------------------------------------------------------------------ */
+/* seeds: fp32, no contraction [R23]                                          */
+/* ------------------------------------------------------------------------ */
+static void onb_f(const float n[3], float b1[3], float b2[3]) {
+    float sign = copysignf(1.0f, n[2]);
+    float a = -1.0f / (sign + n[2]);
+    float b = n[0] * n[1] * a;
+    b1[0] = 1.0f + sign * n[0] * n[0] * a; b1[1] = sign * b; b1[2] = -sign * n[0];
+    b2[0] = b; b2[1] = sign + n[1] * n[1] * a; b2[2] = -n[1];
+}
+
+/* light sample (purpose 0, trial 0) [R15] */
+static void sample_light(const orc_scene *sc, const orc_opts *o, uint64_t walk, float xL[3], double *pdf, int *lid) {
+    uint32_t r[4];
+    draw(o, walk, 0u, 0u, r);
+    int li = sc->n_light > 1 ? (int)uidx(r[2], (uint32_t)sc->n_light) : 0;
+    const orc_light *L = &sc->light[li];
+    *lid = li;
+    if (L->kind == 1) {
+        float a = u01(r[0]) - 0.5f, b = u01(r[1]) - 0.5f;
+        for (int j = 0; j < 3; j++) xL[j] = L->position[j] + (a * L->edge_u[j] + b * L->edge_v[j]);
+        double area = len(cross(vf(L->edge_u), vf(L->edge_v)));
+        *pdf = 1.0 / (area * sc->n_light);
+    } else {
+        for (int j = 0; j < 3; j++) xL[j] = L->position[j];
+        *pdf = 1.0 / sc->n_light;
+    }
+}
+
+/* seed target for (walk, trial): returns 0 on failure.  The deduction ray is
+ * x_D -> target (Eq. 6, x_1 = r(x_D, w_D)). */
+static int seed_target(const orc_scene *sc, const orc_seed_cfg *cfg, const orc_opts *o, uint64_t walk, uint32_t trial,
+                       const float xD[3], float tgt[3], int32_t *bin) {
+    uint32_t r[4];
+    *bin = -1;
+    if (cfg->mode == 0) { /* uniform on the sphere cap visible from x_D [R21-cfg0] */
+        const orc_surface *f = &sc->surf[cfg->surf_id];
+        float d[3] = {xD[0] - f->center[0], xD[1] - f->center[1], xD[2] - f->center[2]};
+        float L = sqrtf(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
+        float a[3] = {d[0] / L, d[1] / L, d[2] / L};
+        float cmin = f->radius / L;
+        draw(o, walk, 2u, trial, r);
+        float u1 = u01(r[0]), u2 = u01(r[1]);
+        float ct = 1.0f - u1 * (1.0f - cmin);
+        float st2 = 1.0f - ct * ct;
+        float st = sqrtf(st2 > 0.0f ? st2 : 0.0f);
+        float phi = 6.28318530717958647692f * u2;
+        float cp = cosf(phi), sp = sinf(phi);
+        float b1[3], b2[3];
+        onb_f(a, b1, b2);
+        for (int j = 0; j < 3; j++) {
+            float dir = ct * a[j] + st * (cp * b1[j] + sp * b2[j]);
+            tgt[j] = f->center[j] + f->radius * dir;
+        }
+        return 1;
+    }
+    if (cfg->mode == 1) { /* triangle uniform by count among front-facing, rejection <= 32 [R21-cfg1] */
+        const orc_surface *f = &sc->surf[cfg->surf_id];
+        int tri = -1;
+        for (uint32_t rr = 0; rr < 32u; rr++) {
+            draw(o, walk, 16u + rr, trial, r);
+            int t = f->tri_begin + (int)uidx(r[0], (uint32_t)f->tri_count);
+            const double *P = sc->P;
+            float v0[3], v1[3], v2[3];
+            for (int j = 0; j < 3; j++) {
+                v0[j] = (float)P[3 * sc->I[3 * t] + j];
+                v1[j] = (float)P[3 * sc->I[3 * t + 1] + j];
+                v2[j] = (float)P[3 * sc->I[3 * t + 2] + j];
+            }
+            float e1[3] = {v1[0] - v0[0], v1[1] - v0[1], v1[2] - v0[2]};
+            float e2[3] = {v2[0] - v0[0], v2[1] - v0[1], v2[2] - v0[2]};
+            float ng[3] = {e1[1] * e2[2] - e1[2] * e2[1], e1[2] * e2[0] - e1[0] * e2[2], e1[0] * e2[1] - e1[1] * e2[0]};
+            float dd[3] = {xD[0] - v0[0], xD[1] - v0[1], xD[2] - v0[2]};
+            float fdot = dd[0] * ng[0] + dd[1] * ng[1] + dd[2] * ng[2];
+            if (fdot > 0.0f) { tri = t; break; }
+        }
+        if (tri < 0) return 0;
+        *bin = tri;
+        draw(o, walk, 2u, trial, r);
+        float u1 = u01(r[0]), u2 = u01(r[1]);
+        float sq = sqrtf(u1);
+        float b1 = sq * (1.0f - u2), b2 = sq * u2;
+        for (int j = 0; j < 3; j++) {
+            float v0 = (float)sc->P[3 * sc->I[3 * tri] + j];
+            float e1 = (float)sc->P[3 * sc->I[3 * tri + 1] + j] - v0;
+            float e2 = (float)sc->P[3 * sc->I[3 * tri + 2] + j] - v0;
+            tgt[j] = v0 + (b1 * e1 + b2 * e2);
+        }
+        return 1;
+    }
+    if (cfg->mode == 2) { /* guided bin over surface (u,v) via integer CDF [R20] */
+        int cx = (int)floorf(((xD[0] - cfg->grid_origin[0]) * (float)cfg->cells_x) / cfg->grid_extent[0]);
+        int cz = (int)floorf(((xD[2] - cfg->grid_origin[1]) * (float)cfg->cells_y) / cfg->grid_extent[1]);
+        if (cx < 0) cx = 0;
+        if (cx > cfg->cells_x - 1) cx = cfg->cells_x - 1;
+        if (cz < 0) cz = 0;
+        if (cz > cfg->cells_y - 1) cz = cfg->cells_y - 1;
+        int nb = cfg->bins_x * cfg->bins_y;
+        const uint64_t *pf = cfg->prefix + (size_t)(cz * cfg->cells_x + cx) * nb;
+        uint64_t S = pf[nb - 1];
+        draw(o, walk, 1u, trial, r);
+        uint64_t x = r[0];
+        uint64_t t = x * (S >> 32) + ((x * (S & 0xffffffffu)) >> 32); /* floor(x*S/2^32) */
+        int b = 0;
+        while (pf[b] <= t) b++; /* upper_bound: first prefix > t */
+        *bin = b;
+        int bx = b % cfg->bins_x, by = b / cfg->bins_x;
+        draw(o, walk, 2u, trial, r);
+        float u = ((float)bx + u01(r[0])) / (float)cfg->bins_x;
+        float v = ((float)by + u01(r[1])) / (float)cfg->bins_y;
+        tgt[0] = cfg->uv_origin[0] + u * cfg->uv_scale[0];
+        tgt[1] = cfg->uv_plane_y;
+        tgt[2] = cfg->uv_origin[1] + v * cfg->uv_scale[1];
+        return 1;
+    }
+    return 0;
+}
+
+/* deduction recursion Eq. 6 with s_R / s_T by tau [R14] */
+static int deduce(const orc_scene *sc, int k, uint32_t tau, v3 xD, v3 target, double eps, cvtx *x) {
+    v3 d = sub(target, xD);
+    double dl = len(d);
+    if (!(dl > 0.0)) return 0;
+    d = mul(d, 1.0 / dl);
+    v3 o = xD;
+    for (int i = 0; i < k; i++) {
+        hit_t h = closest(sc, o, d, eps, 1e300, 1, 1);
+        if (h.surf < 0) return 0;
+        x[i].p = h.p; x[i].prim = h.prim; x[i].surf = h.surf;
+        if (i < k - 1) {
+            const orc_surface *f = &sc->surf[h.surf];
+            v3 ng = geo_normal(sc, &x[i]);
+            v3 dummy[1];
+            v3 n = shading_normal(sc, &x[i], 0, NULL, dummy);
+            int outside = dot(d, ng) < 0.0;
+            if (dot(d, n) > 0.0) n = mul(n, -1.0);
+            double ci = -dot(d, n);
+            if (!(ci > 0.0)) return 0;
+            if (!((tau >> i) & 1u)) {
+                d = add(d, mul(n, 2.0 * ci));
+            } else {
+                if (f->mat != 1) return 0;
+                double e1 = outside ? f->eta_out : f->eta_in, e2 = outside ? f->eta_in : f->eta_out;
+                double eta = e1 / e2;
+                double k2 = 1.0 - eta * eta * (1.0 - ci * ci);
+                if (k2 < 0.0) return 0; /* TIR */
+                d = nrmz(add(mul(d, eta), mul(n, eta * ci - sqrt(k2))));
+            }
+        }
+        o = h.p;
+    }
+    return 1;
+}
+
+static int same_chain(int k, const cvtx *a, const cvtx *b, double eps) {
+    for (int i = 0; i < k; i++) {
+        if (a[i].surf != b[i].surf) return 0;
+        if (len(sub(a[i].p, b[i].p)) >= eps) return 0;
+    }
+    return 1;
+}
+
+static double eps_ray(const orc_scene *sc, const orc_opts *o) { return o->ray_eps > 0.0 ? o->ray_eps : 1e-4 * sc->extent; }
+static double eps_same(const orc_scene *sc, const orc_opts *o) { return o->same_chain_eps > 0.0 ? o->same_chain_eps : 1e-4 * sc->extent; }
+
+/* one attempt: seed -> deduce -> Newton -> sides (O4-O7) */
+static int attempt(const orc_scene *sc, const orc_seed_cfg *cfg, const orc_opts *o, uint64_t walk, uint32_t trial,
+                   const float xD[3], v3 xL, cvtx *x, int *iters, float tgt[3], int32_t *bin) {
+    *iters = 0;
+    if (!seed_target(sc, cfg, o, walk, trial, xD, tgt, bin)) return ST_SEED_FAIL;
+    v3 xd = vf(xD);
+    double eps = eps_ray(sc, o);
+    if (!deduce(sc, cfg->k, cfg->tau, xd, vf(tgt), eps, x)) return ST_SEED_FAIL;
+    int st = newton(sc, o, cfg->k, cfg->tau, xd, xL, x, iters, eps, NULL);
+    if (st == ST_CONVERGED && !sides_ok(sc, cfg->k, cfg->tau, xd, xL, x)) st = ST_BAD_SIDE;
+    return st;
+}
+
+/* finish a converged chain: V, kappa, G, T (Eq. 2) */
+static int finish(const orc_scene *sc, const orc_opts *o, int k, uint32_t tau, v3 xD, v3 nD, v3 xL, const orc_light *L,
+                  const cvtx *x, double *G, double *T, double *kap) {
+    *G = *T = *kap = 0.0;
+    if (!visible_chain(sc, k, xD, xL, x, eps_ray(sc, o))) return ST_OCCLUDED;
+    *kap = kappa_of(sc, k, tau, xD, xL, x);
+    *G = ggt_analytic(sc, k, tau, xD, nD, xL, L, x);
+    double Le = L->emit;
+    if (L->kind == 1) { /* one-sided emitter */
+        v3 nl = nrmz(cross(vf(L->edge_u), vf(L->edge_v)));
+        if (!(dot(sub(x[k - 1].p, xL), nl) > 0.0)) Le = 0.0;
+    }
+    *T = *kap * *G * Le;
+    return ST_CONVERGED;
+}
+
+/* The batched walk over explicit walk indices (walk = recv*spp + s).
+ * Primary attempt (trial 0), then reciprocal-probability trials (Eq. 15):
+ * first trial t whose converged, side-valid chain is same_chain(., x*) gives
+ * k=t; w = T*k/(P(n)*pdf_L) with P(n)=1 for fixed-length configs [R13]. */
+int orc_walks(const void *h, const orc_seed_cfg *cfg, const orc_opts *o, const float *xD, const float *nD, int32_t spp,
+              const int64_t *walks, int64_t n, orc_walk_out *out) {
+    const orc_scene *sc = (const orc_scene *)h;
+    for (int64_t q = 0; q < n; q++) {
+        orc_walk_out *r = &out[q];
+        memset(r, 0, sizeof(*r));
+        int64_t wi = walks[q];
+        int64_t recv = wi / spp;
+        uint64_t wid = o->walk_id_base + (uint64_t)wi;
+        const float *xd = xD + 3 * recv, *nd = nD + 3 * recv;
+        float xLf[3];
+        int lid;
+        sample_light(sc, o, wid, xLf, &r->pdfL, &lid);
+        v3 xL = vf(xLf);
+        r->xL[0] = xL.x; r->xL[1] = xL.y; r->xL[2] = xL.z;
+        cvtx x[KMAX];
+        int iters;
+        int st = attempt(sc, cfg, o, wid, 0u, xd, xL, x, &iters, r->target, &r->bin);
+        r->attempts = 1;
+        r->iters = iters;
+        r->total_iters = iters;
+        if (st == ST_CONVERGED) st = finish(sc, o, cfg->k, cfg->tau, vf(xd), vf(nd), xL, &sc->light[lid], x, &r->G, &r->T, &r->kappa);
+        r->status = st;
+        if (st == ST_CONVERGED || st == ST_OCCLUDED || st == ST_BAD_SIDE || st == ST_MAXITER || st == ST_DEGENERATE) {
+            for (int i = 0; i < cfg->k; i++) {
+                r->pos[i][0] = x[i].p.x; r->pos[i][1] = x[i].p.y; r->pos[i][2] = x[i].p.z;
+                r->prim[i] = x[i].prim; r->surf[i] = x[i].surf;
+            }
+        }
+        if (st == ST_CONVERGED && r->T > 0.0 && o->trials) {
+            uint32_t kk = 0;
+            double es = eps_same(sc, o);
+            for (uint32_t t = 1; t <= o->k_max; t++) {
+                cvtx y[KMAX];
+                int it2;
+                float tg[3];
+                int32_t b2;
+                int s2 = attempt(sc, cfg, o, wid, t, xd, xL, y, &it2, tg, &b2);
+                r->attempts++;
+                r->total_iters += it2;
+                if (s2 == ST_CONVERGED && same_chain(cfg->k, y, x, es)) { kk = t; break; }
+            }
+            if (kk == 0) { kk = o->k_max; r->truncated = 1; }
+            r->trials = kk;
+            r->w = r->T * (double)kk / (1.0 * r->pdfL);
+        }
+    }
+    return 0;
+}
+
+/* ------------------------------------------------------------------------ */
+/* exports for pins                                                           */
+/* ------------------------------------------------------------------------ */
+/* closest hit: returns surf (-1 miss); t, prim, p */
+int orc_closest(const void *h, const double o[3], const double d[3], double tmin, double tmax, int spec_only,
+                int use_bvh, double *t, int32_t *prim, double p[3]) {
+    hit_t r = closest((const orc_scene *)h, V(o[0], o[1], o[2]), V(d[0], d[1], d[2]), tmin, tmax, spec_only, use_bvh);
+    *t = r.t; *prim = r.prim; p[0] = r.p.x; p[1] = r.p.y; p[2] = r.p.z;
+    return r.surf;
+}
+
+/* constraint vector and dense Jacobian at an explicit chain */
+int orc_constraint(const void *h, int k, uint32_t tau, const double xD[3], const double xL[3], const double *pos,
+                   const int32_t *prim, const int32_t *surf, double *C, double *J) {
+    cvtx x[KMAX];
+    cterm terms[KMAX];
+    for (int i = 0; i < k; i++) { x[i].p = V(pos[3 * i], pos[3 * i + 1], pos[3 * i + 2]); x[i].prim = prim[i]; x[i].surf = surf[i]; }
+    return chain_system((const orc_scene *)h, k, tau, V(xD[0], xD[1], xD[2]), V(xL[0], xL[1], xL[2]), x, C, J, terms);
+}
+
+/* Newton from an explicit chain (idempotence, quadratic convergence);
+ * chain updated in place; res_hist[max_iters+1] gets ||C||_inf per iteration */
+int orc_newton_chain(const void *h, const orc_opts *o, int k, uint32_t tau, const double xD[3], const double xL[3],
+                     double *pos, int32_t *prim, int32_t *surf, int32_t *iters, double *res_hist) {
+    const orc_scene *sc = (const orc_scene *)h;
+    cvtx x[KMAX];
+    for (int i = 0; i < k; i++) { x[i].p = V(pos[3 * i], pos[3 * i + 1], pos[3 * i + 2]); x[i].prim = prim[i]; x[i].surf = surf[i]; }
+    int it;
+    int st = newton(sc, o, k, tau, V(xD[0], xD[1], xD[2]), V(xL[0], xL[1], xL[2]), x, &it, eps_ray(sc, o), res_hist);
+    for (int i = 0; i < k; i++) { pos[3 * i] = x[i].p.x; pos[3 * i + 1] = x[i].p.y; pos[3 * i + 2] = x[i].p.z; prim[i] = x[i].prim; surf[i] = x[i].surf; }
+    *iters = it;
+    return st;
+}
+
+/* full single walk from an explicit seed target and x_L (no trials):
+ * deduce -> Newton -> sides -> V -> kappa, G, T.  Used for basin maps. */
+int orc_walk_from_target(const void *h, const orc_opts *o, int k, uint32_t tau, int light_id, const double xD[3],
+                         const double nD[3], const double xL[3], const double target[3], double *pos, int32_t *prim,
+                         int32_t *surf, int32_t *iters, double *G, double *T) {
+    const orc_scene *sc = (const orc_scene *)h;
+    cvtx x[KMAX];
+    v3 xd = V(xD[0], xD[1], xD[2]), xl = V(xL[0], xL[1], xL[2]);
+    double eps = eps_ray(sc, o), kap;
+    *iters = 0; *G = *T = 0.0;
+    if (!deduce(sc, k, tau, xd, V(target[0], target[1], target[2]), eps, x)) return ST_SEED_FAIL;
+    int st = newton(sc, o, k, tau, xd, xl, x, iters, eps, NULL);
+    if (st == ST_CONVERGED && !sides_ok(sc, k, tau, xd, xl, x)) st = ST_BAD_SIDE;
+    if (st == ST_CONVERGED) st = finish(sc, o, k, tau, xd, V(nD[0], nD[1], nD[2]), xl, &sc->light[light_id], x, G, T, &kap);
+    for (int i = 0; i < k; i++) { pos[3 * i] = x[i].p.x; pos[3 * i + 1] = x[i].p.y; pos[3 * i + 2] = x[i].p.z; prim[i] = x[i].prim; surf[i] = x[i].surf; }
+    return st;
+}
+
+/* G at an explicit admissible chain: analytic (method=0) or finite-difference
+ * re-convergence with step delta (method=1; test-only) */
+double orc_ggt(const void *h, const orc_opts *o, int method, double delta, int k, uint32_t tau, int light_id,
+               const double xD[3], const double nD[3], const double xL[3], const double *pos, const int32_t *prim,
+               const int32_t *surf) {
+    const orc_scene *sc = (const orc_scene *)h;
+    cvtx x[KMAX];
+    for (int i = 0; i < k; i++) { x[i].p = V(pos[3 * i], pos[3 * i + 1], pos[3 * i + 2]); x[i].prim = prim[i]; x[i].surf = surf[i]; }
+    v3 xd = V(xD[0], xD[1], xD[2]), nd = V(nD[0], nD[1], nD[2]), xl = V(xL[0], xL[1], xL[2]);
+    const orc_light *L = &sc->light[light_id];
+    if (method == 0) return ggt_analytic(sc, k, tau, xd, nd, xl, L, x);
+    v3 l1, l2;
+    light_axes(L, xl, x[k - 1].p, &l1, &l2);
+    v3 ax[2] = {l1, l2};
+    v3 dw[2];
+    orc_opts oo = *o;
+    oo.tol = 1e-13;
+    oo.max_iters = 60;
+    for (int a = 0; a < 2; a++) {
+        v3 wpm[2];
+        for (int sgn = 0; sgn < 2; sgn++) {
+            cvtx y[KMAX];
+            memcpy(y, x, sizeof(cvtx) * (size_t)k);
+            v3 xl2 = add(xl, mul(ax[a], sgn ? -delta : delta));
+            int it;
+            int st = newton(sc, &oo, k, tau, xd, xl2, y, &it, eps_ray(sc, o), NULL);
+            if (st != ST_CONVERGED) return -1.0;
+            wpm[sgn] = nrmz(sub(y[0].p, xd));
+        }
+        dw[a] = mul(sub(wpm[0], wpm[1]), 0.5 / delta);
+    }
+    v3 w = nrmz(sub(x[0].p, xd)), e1, e2;
+    onb(w, &e1, &e2);
+    double M00 = dot(e1, dw[0]), M01 = dot(e1, dw[1]), M10 = dot(e2, dw[0]), M11 = dot(e2, dw[1]);
+    return fabs(dot(nd, w)) * fabs(M00 * M11 - M01 * M10);
+}
+
+double orc_kappa(const void *h, int k, uint32_t tau, const double xD[3], const double xL[3], const double *pos,
+                 const int32_t *prim, const int32_t *surf) {
+    cvtx x[KMAX];
+    for (int i = 0; i < k; i++) { x[i].p = V(pos[3 * i], pos[3 * i + 1], pos[3 * i + 2]); x[i].prim = prim[i]; x[i].surf = surf[i]; }
+    return kappa_of((const orc_scene *)h, k, tau, V(xD[0], xD[1], xD[2]), V(xL[0], xL[1], xL[2]), x);
+}
+
+/* seed draw only (light + target + bin) for walk/trial; returns 0 on failure */
+int orc_seed(const void *h, const orc_seed_cfg *cfg, const orc_opts *o, const float *xD, int32_t spp, int64_t walk,
+             uint32_t trial, float xL[3], double *pdfL, float tgt[3], int32_t *bin) {
+    const orc_scene *sc = (const orc_scene *)h;
+    int lid;
+    uint64_t wid = o->walk_id_base + (uint64_t)walk;
+    sample_light(sc, o, wid, xL, pdfL, &lid);
+    return seed_target(sc, cfg, o, wid, trial, xD + 3 * (walk / spp), tgt, bin);
+}
+
+/* reflect / refract with the deduction's conventions (d along propagation) */
+int orc_scatter(int isT, double eta1, double eta2, const double d[3], const double n[3], double out[3]) {
+    v3 dd = V(d[0], d[1], d[2]), nn = V(n[0], n[1], n[2]);
+    if (dot(dd, nn) > 0.0) nn = mul(nn, -1.0);
+    double ci = -dot(dd, nn);
+    v3 r;
+    if (!isT) r = add(dd, mul(nn, 2.0 * ci));
+    else {
+        double eta = eta1 / eta2, k2 = 1.0 - eta * eta * (1.0 - ci * ci);
+        if (k2 < 0.0) return 0;
+        r = nrmz(add(mul(dd, eta), mul(nn, eta * ci - sqrt(k2))));
+    }
+    out[0] = r.x; out[1] = r.y; out[2] = r.z;
+    return 1;
+}
+
+/* geometric tangent basis (s^g, t^g) of the step parameterization [R4] */
+void orc_tangent_basis(const void *h, int32_t prim, int32_t surf, const double p[3], double sg[3], double tg[3]) {
+    cvtx x;
+    x.p = V(p[0], p[1], p[2]); x.prim = prim; x.surf = surf;
+    v3 a, b;
+    onb(geo_normal((const orc_scene *)h, &x), &a, &b);
+    sg[0] = a.x; sg[1] = a.y; sg[2] = a.z;
+    tg[0] = b.x; tg[1] = b.y; tg[2] = b.z;
+}

@@ -1,0 +1,318 @@
+"""ctypes front end of the C oracle (oracle/mpg_oracle.c) -- TEST INFRASTRUCTURE ONLY.
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline leg may import
+this module.  It shares nothing with the CUDA library: it builds its own
+shared object from oracle/mpg_oracle.c with gcc and marshals the seeded input
+arrays of paper_2311_12818_b200/workloads.py (inputs only, no method
+arithmetic) into the oracle's own records.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+SRC = os.path.join(HERE, "mpg_oracle.c")
+LIB = os.path.join(HERE, "libmpg_oracle.so")
+KMAX = 8
+
+STATUS = {0: "CONVERGED", 1: "MAXITER", 2: "SEED_FAIL", 3: "BAD_SIDE", 4: "DEGENERATE", 5: "OCCLUDED"}
+
+
+def build(force: bool = False) -> str:
+    """Compile the oracle (plain C, -O2, no FP contraction, no fast-math)."""
+    if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < os.path.getmtime(SRC):
+        subprocess.check_call(["gcc", "-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared",
+                               "-o", LIB, SRC, "-lm"])
+    return LIB
+
+
+class Surface(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("mat", C.c_int32), ("tri_begin", C.c_int32), ("tri_count", C.c_int32),
+                ("eta_in", C.c_float), ("eta_out", C.c_float), ("reflectance", C.c_float), ("radius", C.c_float),
+                ("center", C.c_float * 3), ("origin", C.c_float * 3), ("edge_u", C.c_float * 3),
+                ("edge_v", C.c_float * 3)]
+
+
+class Light(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("emit", C.c_float), ("position", C.c_float * 3), ("edge_u", C.c_float * 3),
+                ("edge_v", C.c_float * 3)]
+
+
+class SeedCfg(C.Structure):
+    _fields_ = [("mode", C.c_int32), ("surf_id", C.c_int32), ("k", C.c_int32), ("tau", C.c_uint32),
+                ("grid_origin", C.c_float * 2), ("grid_extent", C.c_float * 2), ("cells_x", C.c_int32),
+                ("cells_y", C.c_int32), ("bins_x", C.c_int32), ("bins_y", C.c_int32), ("uv_origin", C.c_float * 2),
+                ("uv_scale", C.c_float * 2), ("uv_plane_y", C.c_float), ("prefix", C.POINTER(C.c_uint64))]
+
+
+class Opts(C.Structure):
+    _fields_ = [("max_iters", C.c_int32), ("trials", C.c_int32), ("k_max", C.c_uint32), ("pad", C.c_int32),
+                ("tol", C.c_double), ("beta0", C.c_double), ("same_chain_eps", C.c_double), ("ray_eps", C.c_double),
+                ("seed", C.c_uint64), ("walk_id_base", C.c_uint64)]
+
+
+class WalkOut(C.Structure):
+    _fields_ = [("status", C.c_int32), ("iters", C.c_int32), ("trials", C.c_uint32), ("truncated", C.c_int32),
+                ("G", C.c_double), ("T", C.c_double), ("kappa", C.c_double), ("w", C.c_double),
+                ("pos", (C.c_double * 3) * KMAX), ("prim", C.c_int32 * KMAX), ("surf", C.c_int32 * KMAX),
+                ("xL", C.c_double * 3), ("pdfL", C.c_double), ("target", C.c_float * 3), ("bin", C.c_int32),
+                ("total_iters", C.c_int64), ("attempts", C.c_int64)]
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        _lib = C.CDLL(build())
+        P = C.c_void_p
+        dp = C.POINTER(C.c_double)
+        _lib.orc_scene_create.restype = P
+        _lib.orc_scene_create.argtypes = [C.POINTER(Surface), C.c_int, P, P, C.c_int, P, P, C.c_int,
+                                          C.POINTER(Light), C.c_int]
+        _lib.orc_scene_destroy.argtypes = [P]
+        _lib.orc_scene_extent.restype = C.c_double
+        _lib.orc_scene_extent.argtypes = [P]
+        _lib.orc_walks.argtypes = [P, C.POINTER(SeedCfg), C.POINTER(Opts), P, P, C.c_int32, P, C.c_int64,
+                                   C.POINTER(WalkOut)]
+        _lib.orc_closest.restype = C.c_int
+        _lib.orc_closest.argtypes = [P, dp, dp, C.c_double, C.c_double, C.c_int, C.c_int, dp,
+                                     C.POINTER(C.c_int32), dp]
+        _lib.orc_constraint.restype = C.c_int
+        _lib.orc_constraint.argtypes = [P, C.c_int, C.c_uint32, dp, dp, dp, P, P, dp, dp]
+        _lib.orc_newton_chain.restype = C.c_int
+        _lib.orc_newton_chain.argtypes = [P, C.POINTER(Opts), C.c_int, C.c_uint32, dp, dp, dp, P, P,
+                                          C.POINTER(C.c_int32), dp]
+        _lib.orc_walk_from_target.restype = C.c_int
+        _lib.orc_walk_from_target.argtypes = [P, C.POINTER(Opts), C.c_int, C.c_uint32, C.c_int, dp, dp, dp, dp, dp,
+                                              P, P, C.POINTER(C.c_int32), dp, dp]
+        _lib.orc_ggt.restype = C.c_double
+        _lib.orc_ggt.argtypes = [P, C.POINTER(Opts), C.c_int, C.c_double, C.c_int, C.c_uint32, C.c_int, dp, dp, dp,
+                                 dp, P, P]
+        _lib.orc_kappa.restype = C.c_double
+        _lib.orc_kappa.argtypes = [P, C.c_int, C.c_uint32, dp, dp, dp, P, P]
+        _lib.orc_seed.restype = C.c_int
+        _lib.orc_seed.argtypes = [P, C.POINTER(SeedCfg), C.POINTER(Opts), P, C.c_int32, C.c_int64, C.c_uint32,
+                                  C.POINTER(C.c_float), dp, C.POINTER(C.c_float), C.POINTER(C.c_int32)]
+        _lib.orc_fresnel.restype = C.c_double
+        _lib.orc_fresnel.argtypes = [C.c_double, C.c_double, C.c_double]
+        _lib.orc_philox.argtypes = [P, P, P]
+        _lib.orc_philox_batch.argtypes = [P, C.c_int64, P, P]
+        _lib.orc_guide_tables.argtypes = [P, C.c_int, C.c_int, P]
+        _lib.orc_tangent_basis.argtypes = [P, C.c_int32, C.c_int32, dp, dp, dp]
+        _lib.orc_scatter.restype = C.c_int
+        _lib.orc_scatter.argtypes = [C.c_int, C.c_double, C.c_double, dp, dp, dp]
+    return _lib
+
+
+def _d3(v):
+    return (C.c_double * 3)(*[float(x) for x in v])
+
+
+def _ptr(a: np.ndarray):
+    return a.ctypes.data_as(C.c_void_p)
+
+
+def philox(ctr: np.ndarray, key) -> np.ndarray:
+    """Philox4x32-10 on counters ctr [n,4] u32 with key (k0,k1)."""
+    L = lib()
+    ctr = np.ascontiguousarray(ctr, np.uint32)
+    out = np.zeros_like(ctr)
+    k = np.asarray(key, np.uint32)
+    L.orc_philox_batch(_ptr(ctr), C.c_int64(ctr.shape[0]), _ptr(k), _ptr(out))
+    return out
+
+
+def fresnel(cos_i, eta1, eta2) -> float:
+    return lib().orc_fresnel(float(cos_i), float(eta1), float(eta2))
+
+
+def scatter(isT, eta1, eta2, d, n):
+    out = (C.c_double * 3)()
+    ok = lib().orc_scatter(int(isT), float(eta1), float(eta2), _d3(d), _d3(n), out)
+    return (np.array(out[:]) if ok else None)
+
+
+def guide_tables(E: np.ndarray) -> np.ndarray:
+    """Inclusive prefix sums of the defensive integer weights W' per cell."""
+    E = np.ascontiguousarray(E, np.float32)
+    prefix = np.zeros(E.shape, np.uint64)
+    lib().orc_guide_tables(_ptr(E), int(E.shape[0]), int(E.shape[1]), _ptr(prefix))
+    return prefix
+
+
+def make_opts(w, **over) -> Opts:
+    o = w.opts
+    d = dict(max_iters=o.max_iters, trials=o.trials, k_max=o.k_max, tol=o.tol, beta0=o.beta0, seed=o.seed,
+             walk_id_base=o.walk_id_base, same_chain_eps=0.0, ray_eps=0.0)
+    d.update(over)
+    r = Opts()
+    for k, v in d.items():
+        setattr(r, k, v)
+    return r
+
+
+class OracleScene:
+    """The oracle's own copy of a workload's scene (fp64 + its median-split BVH)."""
+
+    def __init__(self, w):
+        L = lib()
+        self.w = w
+        pos, nrm, idx, ts, ranges = w.mesh_arrays()
+        self._keep = [pos, nrm, idx, ts]
+        S = (Surface * max(1, len(w.surfaces)))()
+        for i, s in enumerate(w.surfaces):
+            S[i].kind, S[i].mat = s.kind, s.mat
+            S[i].tri_begin, S[i].tri_count = ranges[i]
+            S[i].eta_in, S[i].eta_out, S[i].reflectance, S[i].radius = s.eta_in, s.eta_out, s.reflectance, s.radius
+            S[i].center[:] = list(s.center)
+            S[i].origin[:] = list(s.origin)
+            S[i].edge_u[:] = list(s.edge_u)
+            S[i].edge_v[:] = list(s.edge_v)
+        Ls = (Light * max(1, len(w.lights)))()
+        for i, l in enumerate(w.lights):
+            Ls[i].kind, Ls[i].emit = l.kind, l.emit
+            Ls[i].position[:] = list(l.position)
+            Ls[i].edge_u[:] = list(l.edge_u)
+            Ls[i].edge_v[:] = list(l.edge_v)
+        self._S, self._L = S, Ls
+        self.h = L.orc_scene_create(S, len(w.surfaces), _ptr(pos), _ptr(nrm), pos.shape[0], _ptr(idx), _ptr(ts),
+                                    idx.shape[0], Ls, len(w.lights))
+        self.extent = L.orc_scene_extent(self.h)
+        self.prefix = None
+        self.cfg = self._seed_cfg()
+
+    def __del__(self):
+        try:
+            lib().orc_scene_destroy(self.h)
+        except Exception:
+            pass
+
+    def _seed_cfg(self) -> SeedCfg:
+        s = self.w.seed
+        c = SeedCfg()
+        c.mode, c.surf_id, c.k, c.tau = s.mode, s.surf_id, s.k, s.tau
+        c.grid_origin[:] = list(s.grid_origin)
+        c.grid_extent[:] = list(s.grid_extent)
+        c.cells_x, c.cells_y, c.bins_x, c.bins_y = s.cells_x, s.cells_y, s.bins_x, s.bins_y
+        c.uv_origin[:] = list(s.uv_origin)
+        c.uv_scale[:] = list(s.uv_scale)
+        c.uv_plane_y = s.uv_plane_y
+        if self.w.energies is not None:
+            self.set_energies(self.w.energies, c)
+        return c
+
+    def set_energies(self, E, c=None):
+        c = c or self.cfg
+        self.prefix = guide_tables(E)
+        c.prefix = self.prefix.ctypes.data_as(C.POINTER(C.c_uint64))
+
+    def opts(self, **over) -> Opts:
+        return make_opts(self.w, **over)
+
+    def walks(self, walk_ids, opts: Opts = None):
+        """Run the walk (primary + trials) for explicit walk indices."""
+        opts = opts or self.opts()
+        ids = np.ascontiguousarray(walk_ids, np.int64)
+        out = (WalkOut * max(1, ids.shape[0]))()
+        w = self.w
+        lib().orc_walks(self.h, C.byref(self.cfg), C.byref(opts), _ptr(w.xD), _ptr(w.nD), w.spp, _ptr(ids),
+                        ids.shape[0], out)
+        n = ids.shape[0]
+        k = w.seed.k
+        raw = np.frombuffer(out, dtype=np.dtype(_np_walkout()), count=n)
+        res = {f: raw[f].copy() for f in raw.dtype.names}
+        res["pos"] = res["pos"][:, :k]
+        res["prim"] = res["prim"][:, :k]
+        res["surf"] = res["surf"][:, :k]
+        res["walk"] = ids
+        return res
+
+    def closest(self, o, d, tmin=1e-9, tmax=1e300, spec_only=True, use_bvh=True):
+        t = C.c_double()
+        prim = C.c_int32()
+        p = (C.c_double * 3)()
+        s = lib().orc_closest(self.h, _d3(o), _d3(d), tmin, tmax, int(spec_only), int(use_bvh), C.byref(t),
+                              C.byref(prim), p)
+        return s, t.value, prim.value, np.array(p[:])
+
+    def constraint(self, k, tau, xD, xL, pos, prim, surf):
+        pos = np.ascontiguousarray(pos, np.float64).reshape(-1)
+        prim = np.ascontiguousarray(prim, np.int32)
+        surf = np.ascontiguousarray(surf, np.int32)
+        Cv = (C.c_double * (2 * k))()
+        J = (C.c_double * (4 * k * k))()
+        ok = lib().orc_constraint(self.h, k, tau, _d3(xD), _d3(xL), pos.ctypes.data_as(C.POINTER(C.c_double)),
+                                  _ptr(prim), _ptr(surf), Cv, J)
+        return ok, np.array(Cv[:]), np.array(J[:]).reshape(2 * k, 2 * k)
+
+    def newton_chain(self, k, tau, xD, xL, pos, prim, surf, opts=None):
+        opts = opts or self.opts()
+        pos = np.ascontiguousarray(pos, np.float64).reshape(-1).copy()
+        prim = np.ascontiguousarray(prim, np.int32).copy()
+        surf = np.ascontiguousarray(surf, np.int32).copy()
+        it = C.c_int32()
+        hist = np.zeros(opts.max_iters + 2, np.float64)
+        st = lib().orc_newton_chain(self.h, C.byref(opts), k, tau, _d3(xD), _d3(xL),
+                                    pos.ctypes.data_as(C.POINTER(C.c_double)), _ptr(prim), _ptr(surf), C.byref(it),
+                                    hist.ctypes.data_as(C.POINTER(C.c_double)))
+        return st, it.value, pos.reshape(k, 3), prim, surf, hist[:it.value + 1]
+
+    def walk_from_target(self, xD, nD, xL, target, light_id=0, opts=None, k=None, tau=None):
+        opts = opts or self.opts()
+        k = self.w.seed.k if k is None else k
+        tau = self.w.seed.tau if tau is None else tau
+        pos = np.zeros(3 * k, np.float64)
+        prim = np.zeros(k, np.int32)
+        surf = np.zeros(k, np.int32)
+        it = C.c_int32()
+        G = C.c_double()
+        T = C.c_double()
+        st = lib().orc_walk_from_target(self.h, C.byref(opts), k, tau, light_id, _d3(xD), _d3(nD), _d3(xL),
+                                        _d3(target), pos.ctypes.data_as(C.POINTER(C.c_double)), _ptr(prim),
+                                        _ptr(surf), C.byref(it), C.byref(G), C.byref(T))
+        return dict(status=st, iters=it.value, pos=pos.reshape(k, 3), prim=prim, surf=surf, G=G.value, T=T.value)
+
+    def ggt(self, k, tau, xD, nD, xL, pos, prim, surf, method=0, delta=1e-5, light_id=0, opts=None):
+        opts = opts or self.opts()
+        pos = np.ascontiguousarray(pos, np.float64).reshape(-1)
+        prim = np.ascontiguousarray(prim, np.int32)
+        surf = np.ascontiguousarray(surf, np.int32)
+        return lib().orc_ggt(self.h, C.byref(opts), method, delta, k, tau, light_id, _d3(xD), _d3(nD), _d3(xL),
+                             pos.ctypes.data_as(C.POINTER(C.c_double)), _ptr(prim), _ptr(surf))
+
+    def tangent_basis(self, prim, surf, p):
+        a = (C.c_double * 3)()
+        b = (C.c_double * 3)()
+        lib().orc_tangent_basis(self.h, int(prim), int(surf), _d3(p), a, b)
+        return np.array(a[:]), np.array(b[:])
+
+    def kappa(self, k, tau, xD, xL, pos, prim, surf):
+        pos = np.ascontiguousarray(pos, np.float64).reshape(-1)
+        prim = np.ascontiguousarray(prim, np.int32)
+        surf = np.ascontiguousarray(surf, np.int32)
+        return lib().orc_kappa(self.h, k, tau, _d3(xD), _d3(xL), pos.ctypes.data_as(C.POINTER(C.c_double)),
+                               _ptr(prim), _ptr(surf))
+
+    def seed(self, walk, trial=0, opts=None):
+        opts = opts or self.opts()
+        xL = (C.c_float * 3)()
+        tgt = (C.c_float * 3)()
+        pdf = C.c_double()
+        b = C.c_int32()
+        ok = lib().orc_seed(self.h, C.byref(self.cfg), C.byref(opts), _ptr(self.w.xD), self.w.spp, int(walk),
+                            int(trial), xL, C.byref(pdf), tgt, C.byref(b))
+        return ok, np.array(xL[:], np.float32), pdf.value, np.array(tgt[:], np.float32), b.value
+
+
+def _np_walkout():
+    return np.dtype([("status", np.int32), ("iters", np.int32), ("trials", np.uint32), ("truncated", np.int32),
+                     ("G", np.float64), ("T", np.float64), ("kappa", np.float64), ("w", np.float64),
+                     ("pos", np.float64, (KMAX, 3)), ("prim", np.int32, (KMAX,)), ("surf", np.int32, (KMAX,)),
+                     ("xL", np.float64, (3,)), ("pdfL", np.float64), ("target", np.float32, (3,)), ("bin", np.int32),
+                     ("total_iters", np.int64), ("attempts", np.int64)])

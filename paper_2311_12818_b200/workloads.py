@@ -1,0 +1,421 @@
+"""Seeded synthetic inputs for the batched manifold walk (BASELINE.json configs 0-4).
+
+This module is the ONE place both the CUDA path and the oracle get their inputs
+from.  It builds plain fp32/int32 arrays (geometry, receivers, lights, guide
+energies) and small option records; it holds none of the method's arithmetic
+(no seeds, no constraints, no Newton, no tables).  Every recipe is stated in
+DESIGN.md §"Input recipe" and follows SURVEY.md §8(d) (the frozen proposals).
+
+Scene conventions (readings R9/R15/R16):
+  * dielectric outward normals point from the dense medium (eta_in) to eta_out;
+    mesh winding is chosen so that (v1-v0)x(v2-v0) is that outward normal;
+  * area lights are one-sided parallelograms centred at `position`, emitting
+    along normalize(edge_u x edge_v) (all configs: -y);
+  * receivers are cell centres lo + (i+1/2)(hi-lo)/N on a plane y = const,
+    n_D = (0,1,0).
+"""
+from __future__ import annotations
+
+import dataclasses
+import math
+from typing import List, Optional
+
+import numpy as np
+
+# ----------------------------------------------------------------------------
+# plain records
+# ----------------------------------------------------------------------------
+SURF_SPHERE, SURF_QUAD, SURF_MESH = 0, 1, 2
+MAT_CONDUCTOR, MAT_DIELECTRIC, MAT_DIFFUSE = 0, 1, 2
+LIGHT_POINT, LIGHT_QUAD = 0, 1
+SEED_CAP, SEED_TRIANGLE, SEED_GUIDE_UV, SEED_GUIDE_DIR = 0, 1, 2, 3
+
+
+@dataclasses.dataclass
+class Surface:
+    kind: int
+    mat: int
+    eta_in: float = 1.0
+    eta_out: float = 1.0
+    reflectance: float = 1.0
+    center: tuple = (0.0, 0.0, 0.0)
+    radius: float = 0.0
+    origin: tuple = (0.0, 0.0, 0.0)
+    edge_u: tuple = (0.0, 0.0, 0.0)
+    edge_v: tuple = (0.0, 0.0, 0.0)
+    positions: Optional[np.ndarray] = None   # float32 [nv,3]
+    normals: Optional[np.ndarray] = None     # float32 [nv,3] shading normals (outward)
+    indices: Optional[np.ndarray] = None     # int32 [nt,3]
+
+
+@dataclasses.dataclass
+class Light:
+    kind: int
+    emit: float                      # radiance (quad) or intensity (point)
+    position: tuple = (0.0, 0.0, 0.0)
+    edge_u: tuple = (0.0, 0.0, 0.0)
+    edge_v: tuple = (0.0, 0.0, 0.0)
+
+
+@dataclasses.dataclass
+class SeedSpec:
+    mode: int
+    surf_id: int = 0
+    k: int = 1
+    tau: int = 0                     # bit i set <=> vertex i+1 is a refraction (T)
+    # guide (SEED_GUIDE_UV): spatial grid over receivers (x,z), bins over a surface (u,v)
+    grid_origin: tuple = (0.0, 0.0)
+    grid_extent: tuple = (1.0, 1.0)
+    cells_x: int = 1
+    cells_y: int = 1
+    bins_x: int = 1
+    bins_y: int = 1
+    uv_origin: tuple = (0.0, 0.0)    # x = uv_origin[0] + u*uv_scale[0], z = uv_origin[1] + v*uv_scale[1]
+    uv_scale: tuple = (1.0, 1.0)
+    uv_plane_y: float = 0.0
+
+
+@dataclasses.dataclass
+class WalkOpts:
+    max_iters: int = 20
+    tol: float = 1e-5
+    beta0: float = 1.0
+    trials: int = 1
+    k_max: int = 1024
+    same_chain_rel: float = 1e-4     # x scene extent
+    ray_eps_rel: float = 1e-4        # x scene extent
+    seed: int = 0
+    walk_id_base: int = 0
+
+
+@dataclasses.dataclass
+class Workload:
+    name: str
+    surfaces: List[Surface]
+    lights: List[Light]
+    xD: np.ndarray                   # float32 [n_recv,3]
+    nD: np.ndarray                   # float32 [n_recv,3]
+    spp: int
+    seed: SeedSpec
+    opts: WalkOpts
+    energies: Optional[np.ndarray] = None   # float32 [cells, bins] guide energies (or None)
+    recv_shape: tuple = (1, 1)
+
+    @property
+    def n_recv(self) -> int:
+        return int(self.xD.shape[0])
+
+    @property
+    def n_walks(self) -> int:
+        return self.n_recv * self.spp
+
+    def mesh_arrays(self):
+        """Concatenate all mesh surfaces into global vertex/index arrays.
+
+        Returns (positions [nv,3] f32, normals [nv,3] f32, indices [nt,3] i32,
+        tri_surf [nt] i32, ranges [(tri_begin, tri_count) per surface]).
+        """
+        P, N, I, S, ranges = [], [], [], [], []
+        nv = nt = 0
+        for sid, s in enumerate(self.surfaces):
+            if s.kind == SURF_MESH:
+                P.append(s.positions)
+                N.append(s.normals)
+                I.append(s.indices + nv)
+                S.append(np.full(s.indices.shape[0], sid, np.int32))
+                ranges.append((nt, s.indices.shape[0]))
+                nv += s.positions.shape[0]
+                nt += s.indices.shape[0]
+            else:
+                ranges.append((0, 0))
+        if P:
+            pos = np.ascontiguousarray(np.concatenate(P).astype(np.float32))
+            nrm = np.ascontiguousarray(np.concatenate(N).astype(np.float32))
+            idx = np.ascontiguousarray(np.concatenate(I).astype(np.int32))
+            ts = np.ascontiguousarray(np.concatenate(S).astype(np.int32))
+        else:
+            pos = np.zeros((0, 3), np.float32)
+            nrm = np.zeros((0, 3), np.float32)
+            idx = np.zeros((0, 3), np.int32)
+            ts = np.zeros((0,), np.int32)
+        return pos, nrm, idx, ts, ranges
+
+
+# ----------------------------------------------------------------------------
+# geometry generators
+# ----------------------------------------------------------------------------
+def icosphere(level: int = 4, radius: float = 1.0, center=(0.0, 0.0, 0.0)):
+    """Icosahedron subdivided `level` times (L4: 2,562 vertices, 5,120 triangles).
+
+    Vertices are projected to the sphere; shading normals are the normalised
+    vertex positions (BASELINE.json configs[1]: "interpolated vertex normals").
+    Winding is outward ((v1-v0)x(v2-v0) points away from the centre).
+    """
+    t = (1.0 + math.sqrt(5.0)) / 2.0
+    verts = [(-1, t, 0), (1, t, 0), (-1, -t, 0), (1, -t, 0),
+             (0, -1, t), (0, 1, t), (0, -1, -t), (0, 1, -t),
+             (t, 0, -1), (t, 0, 1), (-t, 0, -1), (-t, 0, 1)]
+    faces = [(0, 11, 5), (0, 5, 1), (0, 1, 7), (0, 7, 10), (0, 10, 11),
+             (1, 5, 9), (5, 11, 4), (11, 10, 2), (10, 7, 6), (7, 1, 8),
+             (3, 9, 4), (3, 4, 2), (3, 2, 6), (3, 6, 8), (3, 8, 9),
+             (4, 9, 5), (2, 4, 11), (6, 2, 10), (8, 6, 7), (9, 8, 1)]
+    V = [np.array(v, np.float64) / np.linalg.norm(v) for v in verts]
+    for _ in range(level):
+        cache = {}
+        nf = []
+
+        def mid(a, b):
+            key = (min(a, b), max(a, b))
+            if key not in cache:
+                m = V[a] + V[b]
+                V.append(m / np.linalg.norm(m))
+                cache[key] = len(V) - 1
+            return cache[key]
+
+        for (a, b, c) in faces:
+            ab, bc, ca = mid(a, b), mid(b, c), mid(c, a)
+            nf += [(a, ab, ca), (b, bc, ab), (c, ca, bc), (ab, bc, ca)]
+        faces = nf
+    Vn = np.array(V, np.float64)
+    F = np.array(faces, np.int64)
+    # enforce outward winding
+    e1 = Vn[F[:, 1]] - Vn[F[:, 0]]
+    e2 = Vn[F[:, 2]] - Vn[F[:, 0]]
+    cr = np.cross(e1, e2)
+    flip = np.einsum("ij,ij->i", cr, Vn[F[:, 0]]) < 0
+    F[flip] = F[flip][:, [0, 2, 1]]
+    pos = (Vn * radius + np.asarray(center, np.float64)).astype(np.float32)
+    nrm = Vn.astype(np.float32)
+    return pos, nrm, F.astype(np.int32)
+
+
+def grid_mesh(xs: np.ndarray, zs: np.ndarray, y: np.ndarray, ny: np.ndarray, up: bool):
+    """Triangulate a height field y[i,j] over (xs[i], zs[j]).
+
+    `ny` are the (unnormalised-ok) upward normals [n,n,3]; the mesh winding and
+    the stored normals point up (+y) if `up`, else down.
+    Returns positions [n*n,3], normals [n*n,3], indices [2(n-1)^2,3].
+    """
+    n, m = len(xs), len(zs)
+    X, Z = np.meshgrid(xs, zs, indexing="ij")
+    pos = np.stack([X, y, Z], -1).reshape(-1, 3)
+    nn = ny / np.linalg.norm(ny, axis=-1, keepdims=True)
+    nrm = nn.reshape(-1, 3)
+    i, j = np.meshgrid(np.arange(n - 1), np.arange(m - 1), indexing="ij")
+    v00 = (i * m + j).ravel()
+    v01 = (i * m + j + 1).ravel()
+    v10 = ((i + 1) * m + j).ravel()
+    v11 = ((i + 1) * m + j + 1).ravel()
+    # (v00,v01,v10) and (v10,v01,v11) wind to +y for x along i and z along j
+    t1 = np.stack([v00, v01, v10], -1)
+    t2 = np.stack([v10, v01, v11], -1)
+    idx = np.stack([t1, t2], 1).reshape(-1, 3)
+    if not up:
+        idx = idx[:, [0, 2, 1]]
+        nrm = -nrm
+    return pos.astype(np.float32), nrm.astype(np.float32), idx.astype(np.int32)
+
+
+def water_waves(n_waves: int = 16, amp_total: float = 0.05, seed: int = 0):
+    """Sum-of-sinusoids parameters (BASELINE.json configs[2]; SURVEY §8(d) note:
+    equal amplitudes amp_total/n_waves, wavelengths log-uniform in [0.5, 5],
+    uniform directions and phases, numpy seed 0)."""
+    rng = np.random.default_rng(seed)
+    lam = np.exp(rng.uniform(np.log(0.5), np.log(5.0), n_waves))
+    ang = rng.uniform(0.0, 2 * np.pi, n_waves)
+    phase = rng.uniform(0.0, 2 * np.pi, n_waves)
+    amp = np.full(n_waves, amp_total / n_waves)
+    return lam, ang, phase, amp
+
+
+def heightfield_water(n: int = 512, size: float = 10.0, amp_total: float = 0.05, seed: int = 0):
+    xs = np.linspace(0.0, size, n)
+    zs = np.linspace(0.0, size, n)
+    X, Z = np.meshgrid(xs, zs, indexing="ij")
+    lam, ang, phase, amp = water_waves(16, amp_total, seed)
+    h = np.zeros_like(X)
+    hx = np.zeros_like(X)
+    hz = np.zeros_like(X)
+    for j in range(len(lam)):
+        k = 2 * np.pi / lam[j]
+        dx, dz = np.cos(ang[j]), np.sin(ang[j])
+        arg = k * (dx * X + dz * Z) + phase[j]
+        h += amp[j] * np.sin(arg)
+        hx += amp[j] * k * dx * np.cos(arg)
+        hz += amp[j] * k * dz * np.cos(arg)
+    ny = np.stack([-hx, np.ones_like(h), -hz], -1)
+    return grid_mesh(xs, zs, h, ny, up=True)
+
+
+class _Perlin2:
+    """Classic 2D gradient noise with quintic fade and analytic derivative."""
+
+    def __init__(self, seed: int):
+        rng = np.random.default_rng(seed)
+        self.perm = np.concatenate([rng.permutation(256)] * 2)
+        a = rng.uniform(0, 2 * np.pi, 256)
+        self.g = np.stack([np.cos(a), np.sin(a)], -1)
+
+    def __call__(self, x, z):
+        xi = np.floor(x).astype(np.int64)
+        zi = np.floor(z).astype(np.int64)
+        fx, fz = x - xi, z - zi
+        xi &= 255
+        zi &= 255
+        p = self.perm
+
+        def grad(ix, iz):
+            return self.g[p[p[ix] + iz] & 255]
+
+        g00, g10 = grad(xi, zi), grad(xi + 1, zi)
+        g01, g11 = grad(xi, zi + 1), grad(xi + 1, zi + 1)
+        n00 = g00[..., 0] * fx + g00[..., 1] * fz
+        n10 = g10[..., 0] * (fx - 1) + g10[..., 1] * fz
+        n01 = g01[..., 0] * fx + g01[..., 1] * (fz - 1)
+        n11 = g11[..., 0] * (fx - 1) + g11[..., 1] * (fz - 1)
+        u = fx ** 3 * (fx * (fx * 6 - 15) + 10)
+        v = fz ** 3 * (fz * (fz * 6 - 15) + 10)
+        du = 30 * fx ** 2 * (fx - 1) ** 2
+        dv = 30 * fz ** 2 * (fz - 1) ** 2
+        c = n00 - n10 - n01 + n11
+        val = n00 + u * (n10 - n00) + v * (n01 - n00) + u * v * c
+        cx = g00[..., 0] - g10[..., 0] - g01[..., 0] + g11[..., 0]
+        cz = g00[..., 1] - g10[..., 1] - g01[..., 1] + g11[..., 1]
+        dx = (g00[..., 0] + u * (g10[..., 0] - g00[..., 0]) + v * (g01[..., 0] - g00[..., 0])
+              + u * v * cx + du * (n10 - n00 + v * c))
+        dz = (g00[..., 1] + u * (g10[..., 1] - g00[..., 1]) + v * (g01[..., 1] - g00[..., 1])
+              + u * v * cz + dv * (n01 - n00 + u * c))
+        return val, dx, dz
+
+
+def glass_slabs(n: int = 256, seed: int = 0):
+    """Config 3 geometry: three curved bumpy glass slabs (frozen here).
+
+    slab j in {0,1,2}, y_j = 0, 0.35, 0.7, over (x,z) in [-1,1]^2:
+      bottom_j = y_j + 0.1(x^2+z^2) + 0.02 N_j(4x,4z)          (outward normal down)
+      top_j    = y_j + 0.1(x^2+z^2) + 0.1 + 0.02 N'_j(4x,4z)    (outward normal up)
+    N_j, N'_j independent Perlin gradient noises seeded seed+2j, seed+2j+1.
+    Returns a list of 6 (positions, normals, indices), bottom-to-top order.
+    """
+    xs = np.linspace(-1.0, 1.0, n)
+    zs = np.linspace(-1.0, 1.0, n)
+    X, Z = np.meshgrid(xs, zs, indexing="ij")
+    out = []
+    for j, yj in enumerate((0.0, 0.35, 0.7)):
+        for side in (0, 1):
+            noise = _Perlin2(seed + 2 * j + side)
+            nv, ndx, ndz = noise(4 * X, 4 * Z)
+            y = yj + 0.1 * (X * X + Z * Z) + 0.1 * side + 0.02 * nv
+            fx = 0.2 * X + 0.02 * 4 * ndx
+            fz = 0.2 * Z + 0.02 * 4 * ndz
+            ny = np.stack([-fx, np.ones_like(y), -fz], -1)
+            out.append(grid_mesh(xs, zs, y, ny, up=(side == 1)))
+    return out
+
+
+def receiver_grid(lo: float, hi: float, n: int, y: float, lo_z: Optional[float] = None,
+                  hi_z: Optional[float] = None, nz: Optional[int] = None):
+    """Cell centres x_i = lo + (i+1/2)(hi-lo)/n (reading R16), row-major (z outer)."""
+    lo_z = lo if lo_z is None else lo_z
+    hi_z = hi if hi_z is None else hi_z
+    nz = n if nz is None else nz
+    xs = lo + (np.arange(n) + 0.5) * (hi - lo) / n
+    zs = lo_z + (np.arange(nz) + 0.5) * (hi_z - lo_z) / nz
+    Z, X = np.meshgrid(zs, xs, indexing="ij")
+    xD = np.stack([X.ravel(), np.full(X.size, y), Z.ravel()], -1).astype(np.float32)
+    nD = np.tile(np.array([0.0, 1.0, 0.0], np.float32), (xD.shape[0], 1))
+    return np.ascontiguousarray(xD), np.ascontiguousarray(nD)
+
+
+# ----------------------------------------------------------------------------
+# the BASELINE.json configurations (and their closed-form test twins)
+# ----------------------------------------------------------------------------
+def config0(n_side: int = 64, spp: int = 16) -> Workload:
+    """configs[0]: k=1 R off an analytic mirror sphere r=1 at the origin, point
+    light (0,4,0), 64x64 receivers on y=-1.5 over [-3,3]^2, 16 cap seeds each."""
+    sph = Surface(SURF_SPHERE, MAT_CONDUCTOR, reflectance=1.0, center=(0.0, 0.0, 0.0), radius=1.0)
+    light = Light(LIGHT_POINT, 1.0, position=(0.0, 4.0, 0.0))
+    xD, nD = receiver_grid(-3.0, 3.0, n_side, -1.5)
+    return Workload("cfg0_sphere_mirror_k1", [sph], [light], xD, nD, spp,
+                    SeedSpec(SEED_CAP, surf_id=0, k=1, tau=0b0),
+                    WalkOpts(max_iters=20), recv_shape=(n_side, n_side))
+
+
+def config1(n_side: int = 1024, spp: int = 1, analytic: bool = False) -> Workload:
+    """configs[1]: k=2 TT through a glass icosphere (L4, Phong normals, eta 1.5),
+    unit square area light at y=5, 1024^2 receivers on y=-1.2 over [-2,2]^2,
+    1 seed per receiver, uniform over front-facing triangles.
+    `analytic=True` is twin 1a (analytic glass sphere, cap seeds) for closed-form pins."""
+    if analytic:
+        s = Surface(SURF_SPHERE, MAT_DIELECTRIC, eta_in=1.5, eta_out=1.0, center=(0.0, 0.0, 0.0), radius=1.0)
+        seed = SeedSpec(SEED_CAP, surf_id=0, k=2, tau=0b11)
+    else:
+        P, N, F = icosphere(4)
+        s = Surface(SURF_MESH, MAT_DIELECTRIC, eta_in=1.5, eta_out=1.0, positions=P, normals=N, indices=F)
+        seed = SeedSpec(SEED_TRIANGLE, surf_id=0, k=2, tau=0b11)
+    light = Light(LIGHT_QUAD, 1.0, position=(0.0, 5.0, 0.0), edge_u=(1.0, 0.0, 0.0), edge_v=(0.0, 0.0, 1.0))
+    xD, nD = receiver_grid(-2.0, 2.0, n_side, -1.2)
+    return Workload("cfg1_glass_icosphere_k2" + ("_analytic" if analytic else ""), [s], [light], xD, nD,
+                    spp, seed, WalkOpts(max_iters=20), recv_shape=(n_side, n_side))
+
+
+def config2(n_side: int = 2048, spp: int = 4, flat: bool = False, grid_n: int = 512) -> Workload:
+    """configs[2]: water-pool caustics, k=1 T (eta 1.33), 512^2-vertex heightfield
+    over [0,10]^2, 1x1 area light at y=8, floor y=-2, guided seeds from a
+    16x16-cell x 32x32-bin (u,v) histogram of LogNormal(0,1) energies, 4 seeds
+    per receiver on a 2048^2 floor grid.  `flat=True` is twin 2a (all amplitudes 0)."""
+    P, N, F = heightfield_water(grid_n, 10.0, 0.0 if flat else 0.05, 0)
+    water = Surface(SURF_MESH, MAT_DIELECTRIC, eta_in=1.33, eta_out=1.0, positions=P, normals=N, indices=F)
+    light = Light(LIGHT_QUAD, 1.0, position=(5.0, 8.0, 5.0), edge_u=(1.0, 0.0, 0.0), edge_v=(0.0, 0.0, 1.0))
+    xD, nD = receiver_grid(0.0, 10.0, n_side, -2.0)
+    seed = SeedSpec(SEED_GUIDE_UV, surf_id=0, k=1, tau=0b1, grid_origin=(0.0, 0.0), grid_extent=(10.0, 10.0),
+                    cells_x=16, cells_y=16, bins_x=32, bins_y=32, uv_origin=(0.0, 0.0), uv_scale=(10.0, 10.0),
+                    uv_plane_y=0.0)
+    rng = np.random.default_rng(0)
+    E = rng.lognormal(0.0, 1.0, size=(16 * 16, 32 * 32)).astype(np.float32)
+    return Workload("cfg2_water_pool_k1" + ("_flat" if flat else ""), [water], [light], xD, nD, spp, seed,
+                    WalkOpts(max_iters=20), energies=np.ascontiguousarray(E), recv_shape=(n_side, n_side))
+
+
+def config3(n_side: int = 1024, spp: int = 1, grid_n: int = 256) -> Workload:
+    """configs[3]: k=6 TTTTTT through three stacked bumpy glass slabs, point light
+    (0,2.5,0), receivers on y=-1 over [-1.5,1.5]^2, guide 8x8 cells x 64x64 bins on
+    the first interface, Dirichlet(0.3) energies, max 40 Newton iterations."""
+    surfs = []
+    for (P, N, F) in glass_slabs(grid_n, 0):
+        surfs.append(Surface(SURF_MESH, MAT_DIELECTRIC, eta_in=1.5, eta_out=1.0, positions=P, normals=N, indices=F))
+    light = Light(LIGHT_POINT, 1.0, position=(0.0, 2.5, 0.0))
+    xD, nD = receiver_grid(-1.5, 1.5, n_side, -1.0)
+    seed = SeedSpec(SEED_GUIDE_UV, surf_id=0, k=6, tau=0b111111, grid_origin=(-1.5, -1.5), grid_extent=(3.0, 3.0),
+                    cells_x=8, cells_y=8, bins_x=64, bins_y=64, uv_origin=(-1.0, -1.0), uv_scale=(2.0, 2.0),
+                    uv_plane_y=0.0)
+    rng = np.random.default_rng(0)
+    E = rng.dirichlet(np.full(64 * 64, 0.3), size=64).astype(np.float32)
+    return Workload("cfg3_glass_slabs_k6", surfs, [light], xD, nD, spp, seed,
+                    WalkOpts(max_iters=40), energies=np.ascontiguousarray(E), recv_shape=(n_side, n_side))
+
+
+CONFIGS = {0: config0, 1: config1, 2: config2, 3: config3}
+
+
+def scene_extent(w: Workload) -> float:
+    """Diagonal of the bounding box of all surfaces and lights (reading R10)."""
+    pts = []
+    for s in w.surfaces:
+        if s.kind == SURF_SPHERE:
+            c = np.asarray(s.center, np.float64)
+            pts += [c - s.radius, c + s.radius]
+        elif s.kind == SURF_QUAD:
+            o, u, v = (np.asarray(a, np.float64) for a in (s.origin, s.edge_u, s.edge_v))
+            pts += [o, o + u, o + v, o + u + v]
+        else:
+            pts += [s.positions.min(0).astype(np.float64), s.positions.max(0).astype(np.float64)]
+    for l in w.lights:
+        c = np.asarray(l.position, np.float64)
+        if l.kind == LIGHT_QUAD:
+            u, v = np.asarray(l.edge_u, np.float64), np.asarray(l.edge_v, np.float64)
+            pts += [c - 0.5 * u - 0.5 * v, c + 0.5 * u + 0.5 * v, c + 0.5 * u - 0.5 * v, c - 0.5 * u + 0.5 * v]
+        else:
+            pts.append(c)
+    P = np.stack(pts)
+    return float(np.linalg.norm(P.max(0) - P.min(0)))
