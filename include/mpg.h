@@ -1,0 +1,223 @@
+/*
+ * mpg.h -- C ABI of the B200-native batched manifold walk (libmpg.so).
+ *
+ * Method: Fan, Hong, Guo, Zou, Guo, Yan, "Manifold Path Guiding for Importance
+ * Sampling Specular Chains", ACM TOG 42(6) 2023 (arXiv 2311.12818).
+ * Citations "P:n" are lines of that paper's text; "Rn" are the
+ * numbered readings of DESIGN.md §3 where the paper is silent.
+ *
+ * Conventions for every entry point
+ *  - All functions return an mpg_status; on failure mpg_last_error() returns a
+ *    thread-local message.  Argument errors are detected synchronously before
+ *    anything is enqueued.  CUDA launch errors surface as MPG_ERR_CUDA.
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *    The hot calls (mpg_sample_seeds, mpg_manifold_walk, mpg_estimate,
+ *    mpg_guide_*) are asynchronous on that stream and never allocate.
+ *  - "device" pointers must be CUDA device (or managed) memory of the current
+ *    device; "host" pointers are ordinary host memory.  The caller owns every
+ *    query/output buffer; scene and guide objects own deep copies of what is
+ *    passed at creation/upload.
+ *  - float4 arrays are 16-byte aligned [n][4] float arrays.
+ *  - A walk index w in [0, n_recv*spp) belongs to receiver w / spp; its Philox
+ *    counter is (walk_id_base + w) (reading R2), so results do not depend on
+ *    launch shape, batching or device.
+ */
+#ifndef MPG_H
+#define MPG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct mpg_scene mpg_scene; /* opaque: surfaces + lights + BVH on the device */
+typedef struct mpg_guide mpg_guide; /* opaque: guide histogram + sampling tables     */
+
+typedef enum {
+    MPG_OK = 0,
+    MPG_ERR_INVALID_ARG = 1,
+    MPG_ERR_CUDA = 2,
+    MPG_ERR_OOM = 3,
+    MPG_ERR_UNSUPPORTED = 4,
+    MPG_ERR_STATE = 5
+} mpg_status;
+
+enum { MPG_SURF_SPHERE = 0, MPG_SURF_QUAD = 1, MPG_SURF_MESH = 2 };
+enum { MPG_MAT_CONDUCTOR = 0, MPG_MAT_DIELECTRIC = 1, MPG_MAT_DIFFUSE = 2 };
+enum { MPG_LIGHT_POINT = 0, MPG_LIGHT_QUAD = 1 };
+/* seed distributions p(x_S | x_D, x_L) */
+enum {
+    MPG_SEED_CAP = 0,      /* x_1 uniform by area on the cap of sphere surf_id visible from x_D (init) */
+    MPG_SEED_TRIANGLE = 1, /* x_1 uniform in a triangle drawn uniformly among front-facing ones of mesh surf_id */
+    MPG_SEED_GUIDE_UV = 2  /* x_1 target from the guide histogram over surface (u,v), defensive alpha=1/2 (Eq. 13) */
+};
+/* per-walk status; "converged" = CONVERGED or OCCLUDED */
+enum {
+    MPG_WALK_CONVERGED = 0,  /* admissible, sides valid, visible                  */
+    MPG_WALK_MAXITER = 1,    /* Newton iteration cap reached                      */
+    MPG_WALK_SEED_FAIL = 2,  /* no seed, deduction missed, TIR or type mismatch   */
+    MPG_WALK_BAD_SIDE = 3,   /* spurious constraint zero (R8)                     */
+    MPG_WALK_DEGENERATE = 4, /* singular block, zero-length segment or NaN        */
+    MPG_WALK_OCCLUDED = 5    /* admissible but V = 0                      */
+};
+
+/* One specular (or diffuse occluder) surface.  Outward normal (R9):
+ * sphere: (p-c)/r; quad: normalize(edge_u x edge_v); mesh: (v1-v0)x(v2-v0).
+ * eta_in is the medium behind the outward normal, eta_out in front of it.
+ * Mesh arrays are HOST pointers, copied at mpg_scene_create. */
+typedef struct {
+    int32_t kind, mat;
+    float eta_in, eta_out, reflectance;
+    float center[3], radius;                  /* sphere */
+    float origin[3], edge_u[3], edge_v[3];    /* quad: origin + a*edge_u + b*edge_v, a,b in [0,1] */
+    const float *positions;                   /* mesh: host [n_vertices*3] */
+    const float *normals;                     /* mesh: host [n_vertices*3] shading normals (outward) */
+    const int32_t *indices;                   /* mesh: host [n_triangles*3] */
+    int32_t n_vertices, n_triangles;
+} mpg_surface_desc;
+
+/* Emitter (R15): point (intensity emit) or one-sided parallelogram
+ * centred at position, emitting along normalize(edge_u x edge_v) (radiance emit). */
+typedef struct {
+    int32_t kind;
+    float emit;
+    float position[3], edge_u[3], edge_v[3];
+} mpg_light_desc;
+
+/* Chain type and seed distribution.  tau bit i = 1 <=> vertex i+1 refracts (T),
+ * else reflects (R) (Eq. 6).  1 <= k <= MPG_KMAX. */
+#define MPG_KMAX 8
+typedef struct {
+    int32_t mode;    /* MPG_SEED_* */
+    int32_t surf_id; /* sphere (CAP) or mesh (TRIANGLE) the first vertex is drawn on */
+    int32_t k;
+    uint32_t tau;
+} mpg_sampler_desc;
+
+/* Guide layout (R20): a grid of cells_x*cells_y spatial cells over the receiver
+ * plane (x,z) in [grid_origin, grid_origin+grid_extent), each holding bins_x*bins_y
+ * bins over the surface parameter (u,v) in [0,1)^2, where the seed target of bin
+ * (u,v) is (uv_origin[0]+u*uv_scale[0], uv_plane_y, uv_origin[1]+v*uv_scale[1]). */
+typedef struct {
+    float grid_origin[2], grid_extent[2];
+    int32_t cells_x, cells_y, bins_x, bins_y;
+    float uv_origin[2], uv_scale[2], uv_plane_y;
+} mpg_guide_desc;
+
+typedef struct {
+    int32_t max_iters;     /* Newton cap (BASELINE configs: 20, or 40 for k=6)       */
+    float tol;             /* ||C||_inf threshold (1e-5)                              */
+    float beta0;           /* initial step scale (1)                                  */
+    int32_t trials;        /* 1: reciprocal-probability trials (Eq. 15); 0: walk only */
+    uint32_t k_max;        /* trial cap (1024); truncation counted                    */
+    float same_chain_eps;  /* 0 => 1e-4 * scene extent (R17/SPEC.md:280)              */
+    float ray_eps;         /* 0 => 1e-4 * scene extent (R10)                          */
+    uint32_t flags;        /* reserved, 0                                             */
+    uint64_t seed;         /* Philox key                                              */
+    uint64_t walk_id_base; /* added to the walk index in the Philox counter          */
+} mpg_walk_opts;
+
+/* Configurations (x_D, x_L): receivers; walk w uses receiver w / spp. */
+typedef struct {
+    const float *xD; /* device float4 [n_recv] (xyz used) */
+    const float *nD; /* device float4 [n_recv] receiver normals */
+    int64_t n_recv;
+    int32_t spp;     /* walks per receiver, >= 1 */
+} mpg_query;
+
+/* Seeds (mpg_sample_seeds output, mpg_manifold_walk input); device, length n. */
+typedef struct {
+    float *xL;       /* float4 [n]: light sample x_L, w = its pdf (area x choice)     */
+    float *target;   /* float4 [n]: deduction target (ray x_D -> target gives x_1)   */
+    int32_t *bin;    /* [n]: drawn bin (GUIDE_UV) or triangle (TRIANGLE); -1 none, -2 seed failure */
+} mpg_seed_buf;
+
+/* Walk outputs; device, length n (chain: kmax planes of n float4). */
+typedef struct {
+    float *chain;      /* float4 [k][n]: vertex i of walk w at chain[(i*n + w)*4]; w = prim id bits (int; -1 analytic) */
+    uint8_t *status;   /* [n] MPG_WALK_* of the primary walk                     */
+    uint16_t *iters;   /* [n] Newton iterations of the primary walk              */
+    float *G;          /* [n] generalized geometric term incl. V         */
+    float *T;          /* [n] throughput kappa*G*L_o (Eq. 2)                     */
+    float *w;          /* [n] weight T*<1/P>/pdf_L (Eqs. 9, 15); 0 if no chain   */
+    uint32_t *trials;  /* [n] geometric trial count k (0 if not run)             */
+} mpg_walk_buf;
+
+typedef struct {
+    unsigned long long walks;         /* primary walks processed                     */
+    unsigned long long converged;     /* CONVERGED or OCCLUDED primaries             */
+    unsigned long long newton_iters;  /* all Newton iterations incl. trials          */
+    unsigned long long primary_iters; /* Newton iterations of primaries              */
+    unsigned long long attempts;      /* seed draws incl. trials                     */
+    unsigned long long rays;          /* closest-hit + any-hit rays                  */
+    unsigned long long trials;        /* sum of k over walks that ran trials         */
+    unsigned long long truncated;     /* trial loops that hit k_max                  */
+    unsigned long long node_visits;   /* BVH inner nodes visited                     */
+    unsigned long long tri_tests;     /* ray-triangle tests                          */
+    unsigned long long vertex_iters;  /* sum over Newton iterations of k (solves)    */
+    unsigned long long by_status[8];
+} mpg_walk_stats;
+
+typedef struct {
+    float extent;      /* bbox diagonal of surfaces + lights (R10) */
+    int32_t n_surf, n_light, n_tri, n_nodes;
+    size_t device_bytes;
+} mpg_scene_info;
+
+/* Build the device scene: copies all descriptors and mesh arrays (host), builds
+ * a binned-SAH BVH over all mesh triangles (host, C++), uploads it.  Synchronous. */
+mpg_status mpg_scene_create(const mpg_surface_desc *surfaces, int32_t n_surf, const mpg_light_desc *lights,
+                            int32_t n_light, void *stream, mpg_scene **out);
+mpg_status mpg_scene_destroy(mpg_scene *scene);
+mpg_status mpg_scene_get_info(const mpg_scene *scene, mpg_scene_info *info);
+
+/* Debug/test entry: closest specular (spec_only=1) or any-surface hit of n rays.
+ * orig/dir: device float4 [n]; outputs device: t [n], prim [n] (original triangle id or -1),
+ * surf [n] (-1 = miss). */
+mpg_status mpg_trace_rays(const mpg_scene *scene, const float *orig, const float *dir, int64_t n, float tmin,
+                          int32_t spec_only, float *t, int32_t *prim, int32_t *surf, void *stream);
+
+/* Guide (BASELINE.json histogram stand-in for P:424-482, R20). */
+mpg_status mpg_guide_create(const mpg_guide_desc *desc, mpg_guide **out);
+mpg_status mpg_guide_destroy(mpg_guide *guide);
+/* energies: device [cells][bins] float >= 0; builds the defensive integer tables (Eq. 13). */
+mpg_status mpg_guide_upload(mpg_guide *guide, const float *energy, void *stream);
+/* learned branch absent: uniform tables, histogram zeroed. */
+mpg_status mpg_guide_reset(mpg_guide *guide, void *stream);
+/* histogram[cell(x_D)][bin(x_1*)] += w for walks with status CONVERGED and w > 0 (Eq. 9). */
+mpg_status mpg_guide_accumulate(mpg_guide *guide, const mpg_query *query, const mpg_walk_buf *walks, int64_t n,
+                                void *stream);
+/* tables <- histogram ("last iteration only", P:426 footnote); histogram zeroed. */
+mpg_status mpg_guide_rebuild(mpg_guide *guide, void *stream);
+/* copies: histogram -> energy (device [cells][bins] float); tables -> prefix (device [cells][bins] u64). */
+mpg_status mpg_guide_download(const mpg_guide *guide, float *energy, uint64_t *prefix, void *stream);
+
+/* Light samples + seed targets for the n = n_recv*spp primary walks (trial 0). */
+mpg_status mpg_sample_seeds(const mpg_scene *scene, const mpg_guide *guide, const mpg_sampler_desc *sampler,
+                            const mpg_query *query, const mpg_walk_opts *opts, mpg_seed_buf *seeds, void *stream);
+
+/* Workspace bytes mpg_manifold_walk needs for n walks (work-queue counters). */
+size_t mpg_walk_workspace_size(int64_t n, const mpg_walk_opts *opts);
+
+/* The batched manifold walk: per walk, deduce the seed chain
+ * (Eq. 6), Newton-iterate the half-vector constraints with ray-traced
+ * reprojection, validate sides and visibility, evaluate kappa, G, T (Eq. 2),
+ * then (opts->trials) count reciprocal-probability trials k (Eq. 15) and write
+ * w = T*k/pdf_L.  stats (device, may be NULL) is overwritten. */
+mpg_status mpg_manifold_walk(const mpg_scene *scene, const mpg_guide *guide, const mpg_sampler_desc *sampler,
+                             const mpg_query *query, const mpg_seed_buf *seeds, const mpg_walk_opts *opts,
+                             mpg_walk_buf *out, mpg_walk_stats *stats, void *workspace, size_t workspace_bytes,
+                             void *stream);
+
+/* Estimator (Eq. 3): mean[r] = (1/spp) sum_s w[r*spp+s]; var (nullable) = sample variance. */
+mpg_status mpg_estimate(const float *w, int64_t n_recv, int32_t spp, float *mean, float *var, void *stream);
+
+const char *mpg_last_error(void);
+int32_t mpg_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MPG_H */

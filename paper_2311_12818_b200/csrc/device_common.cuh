@@ -1,0 +1,356 @@
+// device_common.cuh -- fp32 vector math, Philox4x32-10, scene records, ray
+// intersection and BVH traversal for the sm_100a manifold-walk kernels.
+//
+// Everything here is the product path (no oracle code is shared).  Readings
+// "Rn" refer to DESIGN.md §3; "P:n" to PAPER.md lines.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#define MPG_FULL 0xffffffffu
+
+// ----------------------------------------------------------------------------
+// float3 helpers (contraction allowed: this is the Newton / traversal math)
+// ----------------------------------------------------------------------------
+__device__ __forceinline__ float3 f3(float x, float y, float z) { return make_float3(x, y, z); }
+__device__ __forceinline__ float3 xyz(float4 a) { return make_float3(a.x, a.y, a.z); }
+__device__ __forceinline__ float3 operator+(float3 a, float3 b) { return f3(a.x + b.x, a.y + b.y, a.z + b.z); }
+__device__ __forceinline__ float3 operator-(float3 a, float3 b) { return f3(a.x - b.x, a.y - b.y, a.z - b.z); }
+__device__ __forceinline__ float3 operator-(float3 a) { return f3(-a.x, -a.y, -a.z); }
+__device__ __forceinline__ float3 operator*(float3 a, float s) { return f3(a.x * s, a.y * s, a.z * s); }
+__device__ __forceinline__ float3 operator*(float s, float3 a) { return f3(a.x * s, a.y * s, a.z * s); }
+__device__ __forceinline__ float dot(float3 a, float3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
+__device__ __forceinline__ float3 cross(float3 a, float3 b) {
+    return f3(a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x);
+}
+__device__ __forceinline__ float len(float3 a) { return sqrtf(dot(a, a)); }
+__device__ __forceinline__ float3 nrmz(float3 a) { return a * rsqrtf(dot(a, a)); }
+__device__ __forceinline__ float comp(float3 v, int i) { return i == 0 ? v.x : (i == 1 ? v.y : v.z); }
+
+// Orthonormal basis of a unit vector (Duff et al. 2017); any basis is valid for
+// the constraint frame and the step parameterization (R3, R4).
+__device__ __forceinline__ void onb(float3 n, float3 &b1, float3 &b2) {
+    float sign = copysignf(1.0f, n.z);
+    float a = -1.0f / (sign + n.z);
+    float b = n.x * n.y * a;
+    b1 = f3(1.0f + sign * n.x * n.x * a, sign * b, -sign * n.x);
+    b2 = f3(b, sign + n.y * n.y * a, -n.y);
+}
+
+// ----------------------------------------------------------------------------
+// exact fp32 helpers for the seed path (R23): these intrinsics are never
+// contracted into FMAs, so seeds match the oracle's plain C float arithmetic.
+// ----------------------------------------------------------------------------
+#define FM(a, b) __fmul_rn((a), (b))
+#define FA(a, b) __fadd_rn((a), (b))
+#define FS(a, b) __fsub_rn((a), (b))
+#define FD(a, b) __fdiv_rn((a), (b))
+
+// ----------------------------------------------------------------------------
+// Philox4x32-10 (Salmon et al. 2011): key (seed_lo, seed_hi), counter
+// (walk_lo, walk_hi, purpose, trial) (R2)
+// ----------------------------------------------------------------------------
+__device__ __forceinline__ uint4 philox10(uint4 c, uint2 k) {
+#pragma unroll
+    for (int r = 0; r < 10; r++) {
+        unsigned hi0 = __umulhi(0xD2511F53u, c.x), lo0 = 0xD2511F53u * c.x;
+        unsigned hi1 = __umulhi(0xCD9E8D57u, c.z), lo1 = 0xCD9E8D57u * c.z;
+        c = make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
+        k.x += 0x9E3779B9u;
+        k.y += 0xBB67AE85u;
+    }
+    return c;
+}
+__device__ __forceinline__ uint4 rng_draw(uint64_t seed, uint64_t walk, uint32_t purpose, uint32_t trial) {
+    return philox10(make_uint4((uint32_t)walk, (uint32_t)(walk >> 32), purpose, trial),
+                    make_uint2((uint32_t)seed, (uint32_t)(seed >> 32)));
+}
+// (x>>8)*2^-24 and floor(x*m/2^32): both exact (R2)
+__device__ __forceinline__ float u01(uint32_t x) { return (float)(x >> 8) * (1.0f / 16777216.0f); }
+__device__ __forceinline__ uint32_t uidx(uint32_t x, uint32_t m) { return __umulhi(x, m); }
+
+// ----------------------------------------------------------------------------
+// scene records (passed by value as a kernel parameter)
+// ----------------------------------------------------------------------------
+#define DS_MAX_SURF 16
+#define DS_MAX_LIGHT 8
+
+struct DSurf {
+    int kind, mat, tri_begin, tri_count;
+    float eta_in, eta_out, refl, radius;
+    float3 center, origin, eu, ev, nq; // nq: unit quad normal
+};
+
+struct DLight {
+    int kind;
+    float emit, pdf;            // pdf of x_L: 1/(area*n_light) (quad) or 1/n_light (point)
+    float3 pos, eu, ev, n, l1, l2; // n: emission normal; l1,l2: orthonormal axes of the light plane
+};
+
+struct DScene {
+    int n_surf, n_light, n_tri, n_nodes;
+    float extent;
+    DSurf surf[DS_MAX_SURF];
+    DLight light[DS_MAX_LIGHT];
+    const float4 *nodes; // 4 float4 per BVH2 node: child boxes + child refs
+    const float4 *tpos;  // BVH order, 3 float4 per tri; v0.w = original tri id, v1.w = surf id, v2.w = specular flag
+    const float4 *tnrm;  // BVH order, 3 float4 per tri: vertex shading normals
+    const int4 *oidx;    // original order: vertex indices (w: BVH slot)
+    const float4 *vpos;  // original vertex positions
+};
+
+// A hit / chain vertex: prim = BVH-order triangle slot (>= 0) or -1 (analytic)
+struct Hit {
+    float t;
+    int prim, surf;
+    float3 p;
+};
+
+// per-lane work counters (reduced once per kernel)
+struct LaneStats {
+    uint32_t rays, nodes, tris;
+};
+
+// ----------------------------------------------------------------------------
+// intersection
+// ----------------------------------------------------------------------------
+struct RayW {
+    float3 o, d, idir;
+    int kx, ky, kz;
+    float Sx, Sy, Sz;
+};
+
+__device__ __forceinline__ void ray_setup(RayW &r, float3 o, float3 d) {
+    r.o = o;
+    r.d = d;
+    r.idir = f3(d.x != 0.0f ? 1.0f / d.x : copysignf(1e30f, d.x), d.y != 0.0f ? 1.0f / d.y : copysignf(1e30f, d.y),
+                d.z != 0.0f ? 1.0f / d.z : copysignf(1e30f, d.z));
+    float ax = fabsf(d.x), ay = fabsf(d.y), az = fabsf(d.z);
+    int kz = (ax > ay) ? (ax > az ? 0 : 2) : (ay > az ? 1 : 2);
+    int kx = kz == 2 ? 0 : kz + 1;
+    int ky = kx == 2 ? 0 : kx + 1;
+    if (comp(d, kz) < 0.0f) { int t = kx; kx = ky; ky = t; }
+    r.kx = kx; r.ky = ky; r.kz = kz;
+    float dz = comp(d, kz);
+    r.Sx = comp(d, kx) / dz;
+    r.Sy = comp(d, ky) / dz;
+    r.Sz = 1.0f / dz;
+}
+
+// Watertight ray/triangle test (Woop, Benthin, Wald 2013), double-sided.  The
+// edge functions use non-contracted products so a shared edge evaluates to
+// exactly opposite values in both triangles (no cracks for reprojection rays).
+__device__ __forceinline__ bool tri_hit(const RayW &r, float3 v0, float3 v1, float3 v2, float tmin, float tmax,
+                                        float &t, float &b0, float &b1, float &b2) {
+    float3 A = v0 - r.o, B = v1 - r.o, C = v2 - r.o;
+    float Akz = comp(A, r.kz), Bkz = comp(B, r.kz), Ckz = comp(C, r.kz);
+    float Ax = comp(A, r.kx) - r.Sx * Akz, Ay = comp(A, r.ky) - r.Sy * Akz;
+    float Bx = comp(B, r.kx) - r.Sx * Bkz, By = comp(B, r.ky) - r.Sy * Bkz;
+    float Cx = comp(C, r.kx) - r.Sx * Ckz, Cy = comp(C, r.ky) - r.Sy * Ckz;
+    float U = __fsub_rn(__fmul_rn(Cx, By), __fmul_rn(Cy, Bx));
+    float V = __fsub_rn(__fmul_rn(Ax, Cy), __fmul_rn(Ay, Cx));
+    float W = __fsub_rn(__fmul_rn(Bx, Ay), __fmul_rn(By, Ax));
+    if ((U < 0.0f || V < 0.0f || W < 0.0f) && (U > 0.0f || V > 0.0f || W > 0.0f)) return false;
+    float det = U + V + W;
+    if (det == 0.0f) return false;
+    float T = U * (r.Sz * Akz) + V * (r.Sz * Bkz) + W * (r.Sz * Ckz);
+    float inv = 1.0f / det;
+    t = T * inv;
+    if (!(t > tmin && t < tmax)) return false;
+    b0 = U * inv; b1 = V * inv; b2 = W * inv;
+    return true;
+}
+
+__device__ __forceinline__ bool sphere_hit(float3 o, float3 d, float3 c, float R, float tmin, float tmax, float &t) {
+    float3 oc = o - c;
+    float b = dot(oc, d);
+    float3 q = oc - b * d;
+    float disc = R * R - dot(q, q);
+    if (disc < 0.0f) return false;
+    float sq = sqrtf(disc);
+    float t0 = -b - sq, t1 = -b + sq;
+    if (t0 > tmin && t0 < tmax) { t = t0; return true; }
+    if (t1 > tmin && t1 < tmax) { t = t1; return true; }
+    return false;
+}
+
+__device__ __forceinline__ bool quad_hit(float3 o, float3 d, float3 q0, float3 e1, float3 e2, float tmin, float tmax,
+                                         float &t) {
+    float3 pv = cross(d, e2);
+    float det = dot(e1, pv);
+    if (det == 0.0f) return false;
+    float inv = 1.0f / det;
+    float3 tv = o - q0;
+    float u = dot(tv, pv) * inv;
+    if (u < 0.0f || u > 1.0f) return false;
+    float3 qv = cross(tv, e1);
+    float v = dot(d, qv) * inv;
+    if (v < 0.0f || v > 1.0f) return false;
+    float tt = dot(e2, qv) * inv;
+    if (!(tt > tmin && tt < tmax)) return false;
+    t = tt;
+    return true;
+}
+
+// Closest hit (ANY=false) or any hit (ANY=true) with t in (tmin, tmax) over all
+// surfaces, or only specular ones (spec_only): the operator r(x, w) of Eq. 6
+// and the visibility V of Eq. 2.
+template <bool ANY>
+__device__ bool trace(const DScene &S, float3 o, float3 d, float tmin, float tmax, bool spec_only, Hit &h,
+                      LaneStats &st) {
+    st.rays++;
+    float best = tmax;
+    int bprim = -2, bsurf = -1;
+    float bb0 = 0.f, bb1 = 0.f, bb2 = 0.f;
+    for (int i = 0; i < S.n_surf; i++) {
+        const DSurf &f = S.surf[i];
+        if (f.kind == 2 || (spec_only && f.mat == 2)) continue;
+        float t;
+        bool hit = f.kind == 0 ? sphere_hit(o, d, f.center, f.radius, tmin, best, t)
+                               : quad_hit(o, d, f.origin, f.eu, f.ev, tmin, best, t);
+        if (hit) {
+            best = t; bprim = -1; bsurf = i;
+            if (ANY) { h.t = t; h.prim = -1; h.surf = i; return true; }
+        }
+    }
+    if (S.n_tri > 0) {
+        RayW r;
+        ray_setup(r, o, d);
+        int stack[48];
+        int sp = 0;
+        int node = 0;
+        while (true) {
+            if (node >= 0) {
+                st.nodes++;
+                const float4 *nd = S.nodes + 4 * node;
+                float4 a = __ldg(nd), b = __ldg(nd + 1), c = __ldg(nd + 2);
+                int4 ch = __ldg(reinterpret_cast<const int4 *>(nd + 3));
+                float3 lo0 = f3(a.x, a.y, a.z), hi0 = f3(a.w, b.x, b.y);
+                float3 lo1 = f3(b.z, b.w, c.x), hi1 = f3(c.y, c.z, c.w);
+                float3 t0a = (lo0 - o), t0b = (hi0 - o);
+                float tx0 = t0a.x * r.idir.x, tx1 = t0b.x * r.idir.x;
+                float ty0 = t0a.y * r.idir.y, ty1 = t0b.y * r.idir.y;
+                float tz0 = t0a.z * r.idir.z, tz1 = t0b.z * r.idir.z;
+                float n0 = fmaxf(fmaxf(fminf(tx0, tx1), fminf(ty0, ty1)), fmaxf(fminf(tz0, tz1), tmin));
+                float f0 = fminf(fminf(fmaxf(tx0, tx1), fmaxf(ty0, ty1)), fminf(fmaxf(tz0, tz1), best));
+                float3 t1a = (lo1 - o), t1b = (hi1 - o);
+                float sx0 = t1a.x * r.idir.x, sx1 = t1b.x * r.idir.x;
+                float sy0 = t1a.y * r.idir.y, sy1 = t1b.y * r.idir.y;
+                float sz0 = t1a.z * r.idir.z, sz1 = t1b.z * r.idir.z;
+                float n1 = fmaxf(fmaxf(fminf(sx0, sx1), fminf(sy0, sy1)), fmaxf(fminf(sz0, sz1), tmin));
+                float f1 = fminf(fminf(fmaxf(sx0, sx1), fmaxf(sy0, sy1)), fminf(fmaxf(sz0, sz1), best));
+                bool h0 = n0 <= f0, h1 = n1 <= f1;
+                if (h0 && h1) {
+                    int nearc = n0 <= n1 ? ch.x : ch.y, farc = n0 <= n1 ? ch.y : ch.x;
+                    stack[sp++] = farc;
+                    node = nearc;
+                    continue;
+                } else if (h0) {
+                    node = ch.x;
+                    continue;
+                } else if (h1) {
+                    node = ch.y;
+                    continue;
+                }
+            } else {
+                int v = ~node;
+                int start = v >> 3, cnt = (v & 7) + 1;
+                for (int j = start; j < start + cnt; j++) {
+                    st.tris++;
+                    float4 p0 = __ldg(S.tpos + 3 * j), p1 = __ldg(S.tpos + 3 * j + 1), p2 = __ldg(S.tpos + 3 * j + 2);
+                    if (spec_only && __float_as_int(p2.w) == 0) continue;
+                    float t, c0, c1, c2;
+                    if (tri_hit(r, xyz(p0), xyz(p1), xyz(p2), tmin, best, t, c0, c1, c2)) {
+                        best = t; bprim = j; bsurf = __float_as_int(p1.w);
+                        bb0 = c0; bb1 = c1; bb2 = c2;
+                        if (ANY) { h.t = t; h.prim = j; h.surf = bsurf; return true; }
+                    }
+                }
+            }
+            if (sp == 0) break;
+            node = stack[--sp];
+        }
+    }
+    if (ANY) return false;
+    h.t = best; h.prim = bprim; h.surf = bsurf;
+    if (bsurf < 0) return false;
+    if (bprim >= 0) {
+        // hit point from barycentrics: lies on the triangle plane up to rounding
+        float3 v0 = xyz(__ldg(S.tpos + 3 * bprim)), v1 = xyz(__ldg(S.tpos + 3 * bprim + 1)),
+               v2 = xyz(__ldg(S.tpos + 3 * bprim + 2));
+        h.p = v0 * bb0 + v1 * bb1 + v2 * bb2;
+    } else {
+        h.p = o + d * best;
+    }
+    return true;
+}
+
+// ----------------------------------------------------------------------------
+// local geometry at a chain vertex (R3, R4, R9)
+// ----------------------------------------------------------------------------
+__device__ __forceinline__ float3 geo_normal(const DScene &S, int prim, int surf, float3 p) {
+    const DSurf &f = S.surf[surf];
+    if (prim >= 0) {
+        float3 v0 = xyz(__ldg(S.tpos + 3 * prim)), v1 = xyz(__ldg(S.tpos + 3 * prim + 1)),
+               v2 = xyz(__ldg(S.tpos + 3 * prim + 2));
+        return nrmz(cross(v1 - v0, v2 - v0));
+    }
+    if (f.kind == 0) return nrmz(p - f.center);
+    return f.nq;
+}
+
+// shading normal n_s and its derivatives along two tangent vectors a, b.
+// mesh: Phong n = n~/|n~|, n~ = sum b_j n_j (BASELINE configs[1]); sphere: (p-c)/|p-c|.
+__device__ __forceinline__ float3 shading(const DScene &S, int prim, int surf, float3 p, float3 a, float3 b,
+                                          float3 &dna, float3 &dnb) {
+    if (prim >= 0) {
+        float3 v0 = xyz(__ldg(S.tpos + 3 * prim)), v1 = xyz(__ldg(S.tpos + 3 * prim + 1)),
+               v2 = xyz(__ldg(S.tpos + 3 * prim + 2));
+        float3 n0 = xyz(__ldg(S.tnrm + 3 * prim)), n1 = xyz(__ldg(S.tnrm + 3 * prim + 1)),
+               n2 = xyz(__ldg(S.tnrm + 3 * prim + 2));
+        float3 e1 = v1 - v0, e2 = v2 - v0;
+        float3 Ng = cross(e1, e2);
+        float inv = 1.0f / dot(Ng, Ng);
+        float3 g1 = cross(e2, Ng) * inv, g2 = cross(Ng, e1) * inv; // barycentric gradients
+        float3 r = p - v0;
+        float c1 = dot(r, g1), c2 = dot(r, g2), c0 = 1.0f - c1 - c2;
+        float3 nt = n0 * c0 + n1 * c1 + n2 * c2;
+        float il = rsqrtf(dot(nt, nt));
+        float3 n = nt * il;
+        float3 d1 = n1 - n0, d2 = n2 - n0;
+        float3 ta = d1 * dot(a, g1) + d2 * dot(a, g2);
+        float3 tb = d1 * dot(b, g1) + d2 * dot(b, g2);
+        dna = (ta - n * dot(n, ta)) * il;
+        dnb = (tb - n * dot(n, tb)) * il;
+        return n;
+    }
+    const DSurf &f = S.surf[surf];
+    if (f.kind == 0) {
+        float3 r = p - f.center;
+        float il = rsqrtf(dot(r, r));
+        float3 n = r * il;
+        dna = (a - n * dot(n, a)) * il;
+        dnb = (b - n * dot(n, b)) * il;
+        return n;
+    }
+    dna = f3(0.f, 0.f, 0.f);
+    dnb = dna;
+    return f.nq;
+}
+
+__device__ __forceinline__ float3 shading_normal(const DScene &S, int prim, int surf, float3 p) {
+    float3 da, db;
+    return shading(S, prim, surf, p, f3(0.f, 0.f, 0.f), f3(0.f, 0.f, 0.f), da, db);
+}
+
+// unpolarized dielectric Fresnel reflectance (eta1 = medium of incidence)
+__device__ __forceinline__ float fresnel(float ci, float eta1, float eta2) {
+    ci = fabsf(ci);
+    float e = eta1 / eta2;
+    float st2 = e * e * (1.0f - ci * ci);
+    if (st2 >= 1.0f) return 1.0f;
+    float ct = sqrtf(1.0f - st2);
+    float rs = (eta1 * ci - eta2 * ct) / (eta1 * ci + eta2 * ct);
+    float rp = (eta2 * ci - eta1 * ct) / (eta2 * ci + eta1 * ct);
+    return 0.5f * (rs * rs + rp * rp);
+}

@@ -1,0 +1,762 @@
+// mpg.cu -- libmpg.so: the C ABI of include/mpg.h, host-side scene/BVH build,
+// guide tables, and the launch of the sm_100a kernels (seed, walk, estimate,
+// guide build/accumulate, debug trace).
+//
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -shared
+//        -Xcompiler -fPIC -I include (see paper_2311_12818_b200/build.py)
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "mpg.h"
+#include "device_common.cuh"
+#include "seed.cuh"
+#include "walk.cuh"
+
+// ----------------------------------------------------------------------------
+// error plumbing
+// ----------------------------------------------------------------------------
+static thread_local std::string g_err;
+static mpg_status fail(mpg_status s, const std::string &msg) {
+    g_err = msg;
+    return s;
+}
+#define CUDA_TRY(expr)                                                                                  \
+    do {                                                                                                \
+        cudaError_t e_ = (expr);                                                                        \
+        if (e_ != cudaSuccess)                                                                          \
+            return fail(e_ == cudaErrorMemoryAllocation ? MPG_ERR_OOM : MPG_ERR_CUDA,                   \
+                        std::string(#expr) + ": " + cudaGetErrorString(e_));                           \
+    } while (0)
+#define ARG_CHECK(cond, msg)                                                                            \
+    do {                                                                                                \
+        if (!(cond)) return fail(MPG_ERR_INVALID_ARG, msg);                                             \
+    } while (0)
+
+static cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// ----------------------------------------------------------------------------
+// opaque objects
+// ----------------------------------------------------------------------------
+struct mpg_scene {
+    DScene d;
+    std::vector<void *> allocs;
+    size_t bytes = 0;
+    int n_vert = 0;
+};
+
+struct mpg_guide {
+    mpg_guide_desc desc;
+    int n_cells = 0, n_bins = 0;
+    uint64_t *prefix = nullptr;
+    float *hist = nullptr;
+    bool ready = false;
+};
+
+// ----------------------------------------------------------------------------
+// host math
+// ----------------------------------------------------------------------------
+struct hv3 {
+    double x, y, z;
+};
+static hv3 H(const float *f) { return {f[0], f[1], f[2]}; }
+static hv3 hsub(hv3 a, hv3 b) { return {a.x - b.x, a.y - b.y, a.z - b.z}; }
+static hv3 hcross(hv3 a, hv3 b) { return {a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x}; }
+static double hlen(hv3 a) { return std::sqrt(a.x * a.x + a.y * a.y + a.z * a.z); }
+static float3 F3(hv3 a) { return make_float3((float)a.x, (float)a.y, (float)a.z); }
+static hv3 hnrm(hv3 a) {
+    double l = hlen(a);
+    return {a.x / l, a.y / l, a.z / l};
+}
+
+// ----------------------------------------------------------------------------
+// binned-SAH BVH2 over all mesh triangles (host C++).  Node = two child boxes +
+// two child refs (>= 0 inner node, < 0 leaf ~(start<<3 | count-1)), 64 bytes.
+// ----------------------------------------------------------------------------
+namespace {
+struct BTri {
+    float lo[3], hi[3], c[3];
+};
+struct BNode {
+    float b[12];
+    int c0, c1;
+};
+struct Builder {
+    const std::vector<BTri> &T;
+    std::vector<int> idx;
+    std::vector<BNode> nodes;
+    int max_depth = 0;
+    explicit Builder(const std::vector<BTri> &t) : T(t), idx(t.size()) {
+        for (size_t i = 0; i < t.size(); i++) idx[i] = (int)i;
+    }
+    static float area(const float lo[3], const float hi[3]) {
+        float dx = hi[0] - lo[0], dy = hi[1] - lo[1], dz = hi[2] - lo[2];
+        if (dx < 0 || dy < 0 || dz < 0) return 0.f;
+        return 2.f * (dx * dy + dy * dz + dz * dx);
+    }
+    void bounds(int b, int e, float lo[3], float hi[3], float clo[3], float chi[3]) const {
+        for (int a = 0; a < 3; a++) { lo[a] = clo[a] = 3e38f; hi[a] = chi[a] = -3e38f; }
+        for (int i = b; i < e; i++) {
+            const BTri &t = T[idx[i]];
+            for (int a = 0; a < 3; a++) {
+                lo[a] = std::min(lo[a], t.lo[a]); hi[a] = std::max(hi[a], t.hi[a]);
+                clo[a] = std::min(clo[a], t.c[a]); chi[a] = std::max(chi[a], t.c[a]);
+            }
+        }
+    }
+    int leaf(int b, int e) { return ~((b << 3) | (e - b - 1)); }
+    // returns child ref; box of the range in lo/hi
+    int build(int b, int e, int depth, float lo[3], float hi[3]) {
+        max_depth = std::max(max_depth, depth);
+        float clo[3], chi[3];
+        bounds(b, e, lo, hi, clo, chi);
+        int n = e - b;
+        if (n <= 2) return leaf(b, e);
+        const int NB = 16;
+        int best_axis = -1, best_split = -1;
+        float best_cost = 3e38f;
+        if (depth < 56) {
+            for (int a = 0; a < 3; a++) {
+                float ext = chi[a] - clo[a];
+                if (!(ext > 0.f)) continue;
+                int cnt[NB] = {0};
+                float blo[NB][3], bhi[NB][3];
+                for (int j = 0; j < NB; j++)
+                    for (int c = 0; c < 3; c++) { blo[j][c] = 3e38f; bhi[j][c] = -3e38f; }
+                float sc = NB / ext;
+                for (int i = b; i < e; i++) {
+                    const BTri &t = T[idx[i]];
+                    int j = std::min(NB - 1, (int)((t.c[a] - clo[a]) * sc));
+                    cnt[j]++;
+                    for (int c = 0; c < 3; c++) { blo[j][c] = std::min(blo[j][c], t.lo[c]); bhi[j][c] = std::max(bhi[j][c], t.hi[c]); }
+                }
+                float rA[NB];
+                int rN[NB];
+                float alo[3] = {3e38f, 3e38f, 3e38f}, ahi[3] = {-3e38f, -3e38f, -3e38f};
+                int acc = 0;
+                for (int j = NB - 1; j > 0; j--) {
+                    for (int c = 0; c < 3; c++) { alo[c] = std::min(alo[c], blo[j][c]); ahi[c] = std::max(ahi[c], bhi[j][c]); }
+                    acc += cnt[j];
+                    rA[j] = area(alo, ahi);
+                    rN[j] = acc;
+                }
+                for (int c = 0; c < 3; c++) { alo[c] = 3e38f; ahi[c] = -3e38f; }
+                acc = 0;
+                for (int j = 0; j < NB - 1; j++) {
+                    for (int c = 0; c < 3; c++) { alo[c] = std::min(alo[c], blo[j][c]); ahi[c] = std::max(ahi[c], bhi[j][c]); }
+                    acc += cnt[j];
+                    if (acc == 0 || rN[j + 1] == 0) continue;
+                    float cost = area(alo, ahi) * acc + rA[j + 1] * rN[j + 1];
+                    if (cost < best_cost) { best_cost = cost; best_axis = a; best_split = j; }
+                }
+            }
+        }
+        float pa = area(lo, hi);
+        float leaf_cost = (float)n;
+        float split_cost = 0.5f + (pa > 0.f ? best_cost / pa : 3e38f);
+        if (n <= 4 && (best_axis < 0 || split_cost >= leaf_cost)) return leaf(b, e);
+        int mid;
+        if (best_axis >= 0) {
+            float ext = chi[best_axis] - clo[best_axis], sc = NB / ext, c0 = clo[best_axis];
+            int a = best_axis, s = best_split;
+            mid = (int)(std::partition(idx.begin() + b, idx.begin() + e, [&](int t) {
+                        return std::min(NB - 1, (int)((T[t].c[a] - c0) * sc)) <= s;
+                    }) - idx.begin());
+            if (mid == b || mid == e) mid = (b + e) / 2;
+        } else {
+            int a = 0;
+            for (int c = 1; c < 3; c++) if (chi[c] - clo[c] > chi[a] - clo[a]) a = c;
+            mid = (b + e) / 2;
+            std::nth_element(idx.begin() + b, idx.begin() + mid, idx.begin() + e,
+                             [&](int x, int y) { return T[x].c[a] < T[y].c[a]; });
+        }
+        int id = (int)nodes.size();
+        nodes.push_back(BNode());
+        float l0[3], h0[3], l1[3], h1[3];
+        int c0 = build(b, mid, depth + 1, l0, h0);
+        int c1 = build(mid, e, depth + 1, l1, h1);
+        BNode &nd = nodes[id];
+        nd.b[0] = l0[0]; nd.b[1] = l0[1]; nd.b[2] = l0[2]; nd.b[3] = h0[0];
+        nd.b[4] = h0[1]; nd.b[5] = h0[2]; nd.b[6] = l1[0]; nd.b[7] = l1[1];
+        nd.b[8] = l1[2]; nd.b[9] = h1[0]; nd.b[10] = h1[1]; nd.b[11] = h1[2];
+        nd.c0 = c0; nd.c1 = c1;
+        return id;
+    }
+};
+} // namespace
+
+template <class T>
+static mpg_status upload(mpg_scene *s, const std::vector<T> &v, const T **dst) {
+    void *p = nullptr;
+    size_t bytes = std::max<size_t>(sizeof(T), v.size() * sizeof(T));
+    CUDA_TRY(cudaMalloc(&p, bytes));
+    s->allocs.push_back(p);
+    s->bytes += bytes;
+    if (!v.empty()) CUDA_TRY(cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+    *dst = reinterpret_cast<const T *>(p);
+    return MPG_OK;
+}
+
+extern "C" mpg_status mpg_scene_destroy(mpg_scene *scene) {
+    if (!scene) return MPG_OK;
+    for (void *p : scene->allocs) cudaFree(p);
+    delete scene;
+    return MPG_OK;
+}
+
+extern "C" mpg_status mpg_scene_create(const mpg_surface_desc *surfaces, int32_t n_surf, const mpg_light_desc *lights,
+                                       int32_t n_light, void *stream, mpg_scene **out) {
+    (void)stream;
+    ARG_CHECK(out, "out is NULL");
+    *out = nullptr;
+    ARG_CHECK(surfaces && n_surf >= 1 && n_surf <= DS_MAX_SURF, "need 1..16 surfaces");
+    ARG_CHECK(lights && n_light >= 1 && n_light <= DS_MAX_LIGHT, "need 1..8 lights");
+    mpg_scene *s = new mpg_scene();
+    memset(&s->d, 0, sizeof(DScene));
+    DScene &d = s->d;
+    d.n_surf = n_surf;
+    d.n_light = n_light;
+    // global triangle numbering: meshes concatenated in surface order
+    std::vector<float4> vpos, vnrm;
+    std::vector<int4> oidx;
+    std::vector<int> tsurf;
+    double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+    auto grow = [&](hv3 p) {
+        double q[3] = {p.x, p.y, p.z};
+        for (int a = 0; a < 3; a++) { lo[a] = std::min(lo[a], q[a]); hi[a] = std::max(hi[a], q[a]); }
+    };
+    for (int i = 0; i < n_surf; i++) {
+        const mpg_surface_desc &sd = surfaces[i];
+        DSurf &f = d.surf[i];
+        if (sd.kind < 0 || sd.kind > 2 || sd.mat < 0 || sd.mat > 2) { mpg_scene_destroy(s); return fail(MPG_ERR_INVALID_ARG, "bad surface kind/mat"); }
+        if (sd.mat == 1 && !(sd.eta_in > 0.f && sd.eta_out > 0.f && sd.eta_in != sd.eta_out)) {
+            mpg_scene_destroy(s);
+            return fail(MPG_ERR_INVALID_ARG, "dielectric needs eta_in != eta_out > 0 (R2: index-matched T excluded)");
+        }
+        f.kind = sd.kind; f.mat = sd.mat;
+        f.eta_in = sd.eta_in > 0.f ? sd.eta_in : 1.f;
+        f.eta_out = sd.eta_out > 0.f ? sd.eta_out : 1.f;
+        f.refl = sd.reflectance;
+        f.radius = sd.radius;
+        f.center = F3(H(sd.center));
+        f.origin = F3(H(sd.origin));
+        f.eu = F3(H(sd.edge_u));
+        f.ev = F3(H(sd.edge_v));
+        f.nq = make_float3(0, 0, 1);
+        if (sd.kind == 0) {
+            if (!(sd.radius > 0.f)) { mpg_scene_destroy(s); return fail(MPG_ERR_INVALID_ARG, "sphere radius <= 0"); }
+            hv3 c = H(sd.center);
+            grow({c.x - sd.radius, c.y - sd.radius, c.z - sd.radius});
+            grow({c.x + sd.radius, c.y + sd.radius, c.z + sd.radius});
+        } else if (sd.kind == 1) {
+            hv3 o = H(sd.origin), u = H(sd.edge_u), v = H(sd.edge_v);
+            hv3 n = hcross(u, v);
+            if (!(hlen(n) > 0)) { mpg_scene_destroy(s); return fail(MPG_ERR_INVALID_ARG, "degenerate quad"); }
+            f.nq = F3(hnrm(n));
+            grow(o); grow({o.x + u.x, o.y + u.y, o.z + u.z}); grow({o.x + v.x, o.y + v.y, o.z + v.z});
+            grow({o.x + u.x + v.x, o.y + u.y + v.y, o.z + u.z + v.z});
+        } else {
+            if (!sd.positions || !sd.normals || !sd.indices || sd.n_vertices <= 0 || sd.n_triangles <= 0) {
+                mpg_scene_destroy(s);
+                return fail(MPG_ERR_INVALID_ARG, "mesh arrays missing");
+            }
+            int vb = (int)vpos.size();
+            f.tri_begin = (int)oidx.size();
+            f.tri_count = sd.n_triangles;
+            for (int v = 0; v < sd.n_vertices; v++) {
+                vpos.push_back(make_float4(sd.positions[3 * v], sd.positions[3 * v + 1], sd.positions[3 * v + 2], 0.f));
+                vnrm.push_back(make_float4(sd.normals[3 * v], sd.normals[3 * v + 1], sd.normals[3 * v + 2], 0.f));
+            }
+            for (int t = 0; t < sd.n_triangles; t++) {
+                int a = sd.indices[3 * t], b = sd.indices[3 * t + 1], c = sd.indices[3 * t + 2];
+                if (a < 0 || b < 0 || c < 0 || a >= sd.n_vertices || b >= sd.n_vertices || c >= sd.n_vertices) {
+                    mpg_scene_destroy(s);
+                    return fail(MPG_ERR_INVALID_ARG, "mesh index out of range");
+                }
+                oidx.push_back(make_int4(vb + a, vb + b, vb + c, 0));
+                tsurf.push_back(i);
+                for (int q : {a, b, c}) grow(H(sd.positions + 3 * q));
+            }
+        }
+    }
+    d.n_tri = (int)oidx.size();
+    for (int i = 0; i < n_light; i++) {
+        const mpg_light_desc &ld = lights[i];
+        DLight &L = d.light[i];
+        ARG_CHECK(ld.kind == 0 || ld.kind == 1, "bad light kind");
+        L.kind = ld.kind;
+        L.emit = ld.emit;
+        L.pos = F3(H(ld.position));
+        L.eu = F3(H(ld.edge_u));
+        L.ev = F3(H(ld.edge_v));
+        hv3 c = H(ld.position);
+        if (ld.kind == 1) {
+            hv3 u = H(ld.edge_u), v = H(ld.edge_v), n = hcross(u, v);
+            double area = hlen(n);
+            if (!(area > 0)) { mpg_scene_destroy(s); return fail(MPG_ERR_INVALID_ARG, "degenerate area light"); }
+            hv3 nn = hnrm(n), l1 = hnrm(u), l2 = hnrm(hcross(nn, l1));
+            L.n = F3(nn); L.l1 = F3(l1); L.l2 = F3(l2);
+            L.pdf = (float)(1.0 / (area * n_light));
+            for (int sx = -1; sx <= 1; sx += 2)
+                for (int sy = -1; sy <= 1; sy += 2)
+                    grow({c.x + 0.5 * sx * u.x + 0.5 * sy * v.x, c.y + 0.5 * sx * u.y + 0.5 * sy * v.y,
+                          c.z + 0.5 * sx * u.z + 0.5 * sy * v.z});
+        } else {
+            L.pdf = (float)(1.0 / n_light);
+            L.n = make_float3(0, 0, 0);
+            grow(c);
+        }
+    }
+    d.extent = (float)std::sqrt((hi[0] - lo[0]) * (hi[0] - lo[0]) + (hi[1] - lo[1]) * (hi[1] - lo[1]) +
+                                (hi[2] - lo[2]) * (hi[2] - lo[2]));
+    // BVH
+    std::vector<float4> nodes4, tpos, tnrm;
+    if (d.n_tri > 0) {
+        std::vector<BTri> bt(d.n_tri);
+        for (int t = 0; t < d.n_tri; t++) {
+            const int4 &ix = oidx[t];
+            const float4 *p[3] = {&vpos[ix.x], &vpos[ix.y], &vpos[ix.z]};
+            for (int a = 0; a < 3; a++) {
+                float v0 = (&p[0]->x)[a], v1 = (&p[1]->x)[a], v2 = (&p[2]->x)[a];
+                bt[t].lo[a] = std::min(v0, std::min(v1, v2));
+                bt[t].hi[a] = std::max(v0, std::max(v1, v2));
+                bt[t].c[a] = (v0 + v1 + v2) * (1.0f / 3.0f);
+            }
+        }
+        Builder B(bt);
+        B.nodes.reserve(d.n_tri);
+        float rlo[3], rhi[3];
+        int root = B.build(0, d.n_tri, 0, rlo, rhi);
+        if (root < 0) { // single leaf: wrap in a root with an empty sibling
+            BNode nd;
+            for (int a = 0; a < 3; a++) { nd.b[a] = rlo[a]; }
+            nd.b[3] = rhi[0]; nd.b[4] = rhi[1]; nd.b[5] = rhi[2];
+            for (int a = 6; a < 9; a++) nd.b[a] = 3e38f;
+            for (int a = 9; a < 12; a++) nd.b[a] = -3e38f;
+            nd.c0 = root; nd.c1 = root;
+            B.nodes.insert(B.nodes.begin(), nd);
+        }
+        if (B.max_depth > 60) { mpg_scene_destroy(s); return fail(MPG_ERR_UNSUPPORTED, "BVH too deep"); }
+        d.n_nodes = (int)B.nodes.size();
+        nodes4.resize(4 * d.n_nodes);
+        for (int i = 0; i < d.n_nodes; i++) {
+            const BNode &nd = B.nodes[i];
+            nodes4[4 * i + 0] = make_float4(nd.b[0], nd.b[1], nd.b[2], nd.b[3]);
+            nodes4[4 * i + 1] = make_float4(nd.b[4], nd.b[5], nd.b[6], nd.b[7]);
+            nodes4[4 * i + 2] = make_float4(nd.b[8], nd.b[9], nd.b[10], nd.b[11]);
+            int4 ch = make_int4(nd.c0, nd.c1, 0, 0);
+            memcpy(&nodes4[4 * i + 3], &ch, sizeof(int4));
+        }
+        tpos.resize(3 * d.n_tri);
+        tnrm.resize(3 * d.n_tri);
+        for (int j = 0; j < d.n_tri; j++) {
+            int t = B.idx[j];
+            int4 &ix = oidx[t];
+            ix.w = j;
+            int sid = tsurf[t];
+            int spec = d.surf[sid].mat != 2 ? 1 : 0;
+            float4 a = vpos[ix.x], b = vpos[ix.y], c = vpos[ix.z];
+            int tw = t;
+            memcpy(&a.w, &tw, 4);
+            memcpy(&b.w, &sid, 4);
+            memcpy(&c.w, &spec, 4);
+            tpos[3 * j] = a; tpos[3 * j + 1] = b; tpos[3 * j + 2] = c;
+            tnrm[3 * j] = vnrm[ix.x]; tnrm[3 * j + 1] = vnrm[ix.y]; tnrm[3 * j + 2] = vnrm[ix.z];
+        }
+    }
+    mpg_status st;
+    if ((st = upload(s, nodes4, &d.nodes)) != MPG_OK || (st = upload(s, tpos, &d.tpos)) != MPG_OK ||
+        (st = upload(s, tnrm, &d.tnrm)) != MPG_OK || (st = upload(s, oidx, &d.oidx)) != MPG_OK ||
+        (st = upload(s, vpos, &d.vpos)) != MPG_OK) {
+        mpg_scene_destroy(s);
+        return st;
+    }
+    s->n_vert = (int)vpos.size();
+    *out = s;
+    return MPG_OK;
+}
+
+extern "C" mpg_status mpg_scene_get_info(const mpg_scene *scene, mpg_scene_info *info) {
+    ARG_CHECK(scene && info, "NULL argument");
+    info->extent = scene->d.extent;
+    info->n_surf = scene->d.n_surf;
+    info->n_light = scene->d.n_light;
+    info->n_tri = scene->d.n_tri;
+    info->n_nodes = scene->d.n_nodes;
+    info->device_bytes = scene->bytes;
+    return MPG_OK;
+}
+
+// ----------------------------------------------------------------------------
+// debug trace kernel
+// ----------------------------------------------------------------------------
+__global__ void k_trace(const DScene S, const float4 *orig, const float4 *dir, int64_t n, float tmin, int spec_only,
+                        float *t, int *prim, int *surf) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        LaneStats ls = {0, 0, 0};
+        Hit h;
+        bool ok = trace<false>(S, xyz(orig[i]), nrmz(xyz(dir[i])), tmin, 3.0e38f, spec_only != 0, h, ls);
+        t[i] = ok ? h.t : -1.0f;
+        prim[i] = ok && h.prim >= 0 ? __float_as_int(S.tpos[3 * h.prim].w) : -1;
+        surf[i] = ok ? h.surf : -1;
+    }
+}
+
+extern "C" mpg_status mpg_trace_rays(const mpg_scene *scene, const float *orig, const float *dir, int64_t n,
+                                     float tmin, int32_t spec_only, float *t, int32_t *prim, int32_t *surf,
+                                     void *stream) {
+    ARG_CHECK(scene && orig && dir && t && prim && surf && n >= 0, "bad argument");
+    if (n == 0) return MPG_OK;
+    int blocks = (int)std::min<int64_t>((n + 127) / 128, 148 * 16);
+    k_trace<<<blocks, 128, 0, as_stream(stream)>>>(scene->d, (const float4 *)orig, (const float4 *)dir, n, tmin,
+                                                   spec_only, t, prim, surf);
+    CUDA_TRY(cudaPeekAtLastError());
+    return MPG_OK;
+}
+
+// ----------------------------------------------------------------------------
+// guide: integer defensive tables (R20), accumulate (Eq. 9), rebuild
+// ----------------------------------------------------------------------------
+#define GT_THREADS 256
+__global__ void __launch_bounds__(GT_THREADS) k_guide_tables(const float *E, int nb, uint64_t *prefix) {
+    __shared__ float s_max[GT_THREADS];
+    __shared__ unsigned long long s_sum[GT_THREADS];
+    const int c = blockIdx.x, tid = threadIdx.x;
+    const float *e = E + (size_t)c * nb;
+    uint64_t *pf = prefix + (size_t)c * nb;
+    int per = (nb + GT_THREADS - 1) / GT_THREADS;
+    int b0 = tid * per, b1 = min(nb, b0 + per);
+    float m = 0.f;
+    for (int b = b0; b < b1; b++) m = fmaxf(m, e[b]);
+    s_max[tid] = m;
+    __syncthreads();
+    for (int o = GT_THREADS / 2; o > 0; o >>= 1) {
+        if (tid < o) s_max[tid] = fmaxf(s_max[tid], s_max[tid + o]);
+        __syncthreads();
+    }
+    float emax = s_max[0];
+    auto Wb = [&](float eb) -> uint32_t {
+        if (!(eb > 0.f) || !(emax > 0.f)) return 0u;
+        uint32_t q = (uint32_t)floorf(__fmul_rn(__fdiv_rn(eb, emax), 1048576.0f));
+        return q < 1u ? 1u : q;
+    };
+    unsigned long long loc = 0;
+    for (int b = b0; b < b1; b++) loc += Wb(e[b]);
+    s_sum[tid] = loc;
+    __syncthreads();
+    for (int o = GT_THREADS / 2; o > 0; o >>= 1) {
+        if (tid < o) s_sum[tid] += s_sum[tid + o];
+        __syncthreads();
+    }
+    unsigned long long sumW = s_sum[0];
+    __syncthreads();
+    auto Wp = [&](float eb) -> unsigned long long { return sumW == 0 ? 1ull : sumW + (unsigned long long)nb * Wb(eb); };
+    loc = 0;
+    for (int b = b0; b < b1; b++) loc += Wp(e[b]);
+    s_sum[tid] = loc;
+    __syncthreads();
+    // inclusive Hillis-Steele scan over the per-thread totals
+    for (int o = 1; o < GT_THREADS; o <<= 1) {
+        unsigned long long v = tid >= o ? s_sum[tid - o] : 0ull;
+        __syncthreads();
+        s_sum[tid] += v;
+        __syncthreads();
+    }
+    unsigned long long acc = tid > 0 ? s_sum[tid - 1] : 0ull;
+    for (int b = b0; b < b1; b++) {
+        acc += Wp(e[b]);
+        pf[b] = acc;
+    }
+}
+
+__global__ void k_fill_f32(float *p, int64_t n, float v) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) p[i] = v;
+}
+
+__device__ __forceinline__ int guide_cell(const mpg_guide_desc &g, float3 xD) {
+    int cx = (int)floorf(FD(FM(FS(xD.x, g.grid_origin[0]), (float)g.cells_x), g.grid_extent[0]));
+    int cz = (int)floorf(FD(FM(FS(xD.z, g.grid_origin[1]), (float)g.cells_y), g.grid_extent[1]));
+    cx = min(max(cx, 0), g.cells_x - 1);
+    cz = min(max(cz, 0), g.cells_y - 1);
+    return cz * g.cells_x + cx;
+}
+
+// histogram[cell(x_D)][bin(x_1*)] += w (Eq. 9; lobes sit at the found chains),
+// warp-aggregated: lanes with equal (cell,bin) keys combine before one atomic.
+__global__ void k_accumulate(const mpg_guide_desc g, const float4 *xD, int spp, int64_t n, const float4 *chain0,
+                             const uint8_t *status, const float *w, float *hist) {
+    const int nb = g.bins_x * g.bins_y;
+    const int lane = threadIdx.x & 31;
+    for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < n; base += (int64_t)gridDim.x * blockDim.x) {
+        int64_t i = base + threadIdx.x;
+        int key = -1;
+        float val = 0.f;
+        if (i < n && status[i] == 0 && w[i] > 0.f) {
+            float3 x1 = xyz(chain0[i]);
+            int cell = guide_cell(g, xyz(xD[i / spp]));
+            float u = (x1.x - g.uv_origin[0]) / g.uv_scale[0], v = (x1.z - g.uv_origin[1]) / g.uv_scale[1];
+            int bx = min(max((int)floorf(u * g.bins_x), 0), g.bins_x - 1);
+            int by = min(max((int)floorf(v * g.bins_y), 0), g.bins_y - 1);
+            key = cell * nb + by * g.bins_x + bx;
+            val = w[i];
+        }
+        unsigned grp = __match_any_sync(MPG_FULL, key);
+        float sum = 0.f;
+        for (int j = 0; j < 32; j++) {
+            float vj = __shfl_sync(MPG_FULL, val, j);
+            if (grp & (1u << j)) sum += vj;
+        }
+        if (key >= 0 && lane == __ffs(grp) - 1) atomicAdd(hist + key, sum);
+    }
+}
+
+extern "C" mpg_status mpg_guide_create(const mpg_guide_desc *desc, mpg_guide **out) {
+    ARG_CHECK(desc && out, "NULL argument");
+    ARG_CHECK(desc->cells_x >= 1 && desc->cells_y >= 1 && desc->bins_x >= 1 && desc->bins_y >= 1, "empty guide");
+    ARG_CHECK(desc->grid_extent[0] > 0.f && desc->grid_extent[1] > 0.f && desc->uv_scale[0] != 0.f &&
+                  desc->uv_scale[1] != 0.f, "bad guide extents");
+    ARG_CHECK((int64_t)desc->bins_x * desc->bins_y <= 65536, "at most 65536 bins per cell");
+    mpg_guide *g = new mpg_guide();
+    g->desc = *desc;
+    g->n_cells = desc->cells_x * desc->cells_y;
+    g->n_bins = desc->bins_x * desc->bins_y;
+    size_t ne = (size_t)g->n_cells * g->n_bins;
+    cudaError_t e1 = cudaMalloc(&g->prefix, ne * sizeof(uint64_t));
+    cudaError_t e2 = cudaMalloc(&g->hist, ne * sizeof(float));
+    if (e1 != cudaSuccess || e2 != cudaSuccess) {
+        cudaFree(g->prefix); cudaFree(g->hist); delete g;
+        return fail(MPG_ERR_OOM, "guide allocation failed");
+    }
+    *out = g;
+    return MPG_OK;
+}
+
+extern "C" mpg_status mpg_guide_destroy(mpg_guide *g) {
+    if (!g) return MPG_OK;
+    cudaFree(g->prefix);
+    cudaFree(g->hist);
+    delete g;
+    return MPG_OK;
+}
+
+extern "C" mpg_status mpg_guide_upload(mpg_guide *g, const float *energy, void *stream) {
+    ARG_CHECK(g && energy, "NULL argument");
+    k_guide_tables<<<g->n_cells, GT_THREADS, 0, as_stream(stream)>>>(energy, g->n_bins, g->prefix);
+    CUDA_TRY(cudaPeekAtLastError());
+    CUDA_TRY(cudaMemsetAsync(g->hist, 0, sizeof(float) * (size_t)g->n_cells * g->n_bins, as_stream(stream)));
+    g->ready = true;
+    return MPG_OK;
+}
+
+extern "C" mpg_status mpg_guide_reset(mpg_guide *g, void *stream) {
+    ARG_CHECK(g, "NULL guide");
+    CUDA_TRY(cudaMemsetAsync(g->hist, 0, sizeof(float) * (size_t)g->n_cells * g->n_bins, as_stream(stream)));
+    k_guide_tables<<<g->n_cells, GT_THREADS, 0, as_stream(stream)>>>(g->hist, g->n_bins, g->prefix);
+    CUDA_TRY(cudaPeekAtLastError());
+    g->ready = true;
+    return MPG_OK;
+}
+
+extern "C" mpg_status mpg_guide_accumulate(mpg_guide *g, const mpg_query *q, const mpg_walk_buf *wb, int64_t n,
+                                           void *stream) {
+    ARG_CHECK(g && q && wb && q->xD && wb->chain && wb->status && wb->w, "NULL argument");
+    ARG_CHECK(q->spp >= 1 && n == q->n_recv * q->spp, "n must equal n_recv*spp");
+    if (n == 0) return MPG_OK;
+    int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 8);
+    k_accumulate<<<blocks, 256, 0, as_stream(stream)>>>(g->desc, (const float4 *)q->xD, q->spp, n,
+                                                        (const float4 *)wb->chain, wb->status, wb->w, g->hist);
+    CUDA_TRY(cudaPeekAtLastError());
+    return MPG_OK;
+}
+
+extern "C" mpg_status mpg_guide_rebuild(mpg_guide *g, void *stream) {
+    ARG_CHECK(g, "NULL guide");
+    k_guide_tables<<<g->n_cells, GT_THREADS, 0, as_stream(stream)>>>(g->hist, g->n_bins, g->prefix);
+    CUDA_TRY(cudaPeekAtLastError());
+    CUDA_TRY(cudaMemsetAsync(g->hist, 0, sizeof(float) * (size_t)g->n_cells * g->n_bins, as_stream(stream)));
+    return MPG_OK;
+}
+
+extern "C" mpg_status mpg_guide_download(const mpg_guide *g, float *energy, uint64_t *prefix, void *stream) {
+    ARG_CHECK(g, "NULL guide");
+    size_t ne = (size_t)g->n_cells * g->n_bins;
+    if (energy) CUDA_TRY(cudaMemcpyAsync(energy, g->hist, ne * sizeof(float), cudaMemcpyDeviceToDevice, as_stream(stream)));
+    if (prefix) CUDA_TRY(cudaMemcpyAsync(prefix, g->prefix, ne * sizeof(uint64_t), cudaMemcpyDeviceToDevice, as_stream(stream)));
+    return MPG_OK;
+}
+
+// ----------------------------------------------------------------------------
+// seeds
+// ----------------------------------------------------------------------------
+static mpg_status make_seed_ctx(const mpg_scene *scene, const mpg_guide *guide, const mpg_sampler_desc *sd,
+                                const mpg_walk_opts *o, SeedCtx &g) {
+    memset(&g, 0, sizeof(g));
+    ARG_CHECK(sd->k >= 1 && sd->k <= MPG_KMAX, "k must be in [1, 8]");
+    ARG_CHECK(sd->mode >= 0 && sd->mode <= 2, "bad sampler mode");
+    ARG_CHECK(sd->surf_id >= 0 && sd->surf_id < scene->d.n_surf, "sampler surf_id out of range");
+    const DSurf &f = scene->d.surf[sd->surf_id];
+    if (sd->mode == 0) ARG_CHECK(f.kind == 0, "CAP sampler needs a sphere");
+    if (sd->mode == 1) ARG_CHECK(f.kind == 2, "TRIANGLE sampler needs a mesh");
+    g.mode = sd->mode;
+    g.surf_id = sd->surf_id;
+    g.k = sd->k;
+    g.tau = sd->tau & ((1u << sd->k) - 1u);
+    g.seed = o->seed;
+    if (sd->mode == 2) {
+        ARG_CHECK(guide && guide->ready, "GUIDE_UV sampler needs an uploaded/reset guide");
+        const mpg_guide_desc &d = guide->desc;
+        g.gox = d.grid_origin[0]; g.goz = d.grid_origin[1]; g.gex = d.grid_extent[0]; g.gez = d.grid_extent[1];
+        g.cells_x = d.cells_x; g.cells_y = d.cells_y; g.bins_x = d.bins_x; g.bins_y = d.bins_y;
+        g.uvox = d.uv_origin[0]; g.uvoz = d.uv_origin[1]; g.uvsx = d.uv_scale[0]; g.uvsz = d.uv_scale[1];
+        g.uv_y = d.uv_plane_y;
+        g.prefix = guide->prefix;
+    }
+    return MPG_OK;
+}
+
+__global__ void k_seeds(const DScene S, const SeedCtx g, const float4 *xD, int64_t n, int spp, uint64_t base,
+                        float4 *xL, float4 *tgt, int *bin) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        uint64_t wid = base + (uint64_t)i;
+        float3 l;
+        int lid;
+        float pdf = sample_light(S, g.seed, wid, l, lid);
+        xL[i] = make_float4(l.x, l.y, l.z, pdf);
+        float3 t = f3(0.f, 0.f, 0.f);
+        int b;
+        bool ok = seed_target(S, g, wid, 0u, xyz(xD[i / spp]), t, b);
+        tgt[i] = make_float4(t.x, t.y, t.z, 0.f);
+        bin[i] = ok ? b : -2;
+    }
+}
+
+static int g_num_sms = 0;
+static int num_sms() {
+    if (!g_num_sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+        if (g_num_sms <= 0) g_num_sms = 148;
+    }
+    return g_num_sms;
+}
+
+extern "C" mpg_status mpg_sample_seeds(const mpg_scene *scene, const mpg_guide *guide, const mpg_sampler_desc *sd,
+                                       const mpg_query *q, const mpg_walk_opts *o, mpg_seed_buf *sb, void *stream) {
+    ARG_CHECK(scene && sd && q && o && sb && q->xD && sb->xL && sb->target && sb->bin, "NULL argument");
+    ARG_CHECK(q->n_recv >= 0 && q->spp >= 1, "bad query sizes");
+    SeedCtx g;
+    mpg_status st = make_seed_ctx(scene, guide, sd, o, g);
+    if (st != MPG_OK) return st;
+    int64_t n = q->n_recv * q->spp;
+    if (n == 0) return MPG_OK;
+    int blocks = (int)std::min<int64_t>((n + 255) / 256, (int64_t)num_sms() * 8);
+    k_seeds<<<blocks, 256, 0, as_stream(stream)>>>(scene->d, g, (const float4 *)q->xD, n, q->spp, o->walk_id_base,
+                                                   (float4 *)sb->xL, (float4 *)sb->target, sb->bin);
+    CUDA_TRY(cudaPeekAtLastError());
+    return MPG_OK;
+}
+
+// ----------------------------------------------------------------------------
+// walk
+// ----------------------------------------------------------------------------
+extern "C" size_t mpg_walk_workspace_size(int64_t n, const mpg_walk_opts *opts) {
+    (void)n; (void)opts;
+    return 256;
+}
+
+template <int KMAX>
+static mpg_status launch_walk(const DScene &S, const SeedCtx &g, const WalkParams &P, cudaStream_t st) {
+    static int occ = 0;
+    if (!occ) {
+        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_walk<KMAX>, 128, 0));
+        if (occ <= 0) occ = 1;
+    }
+    int64_t want = (P.n + 127) / 128;
+    int blocks = (int)std::min<int64_t>(want, (int64_t)num_sms() * occ);
+    k_walk<KMAX><<<blocks, 128, 0, st>>>(S, g, P);
+    CUDA_TRY(cudaPeekAtLastError());
+    return MPG_OK;
+}
+
+extern "C" mpg_status mpg_manifold_walk(const mpg_scene *scene, const mpg_guide *guide, const mpg_sampler_desc *sd,
+                                        const mpg_query *q, const mpg_seed_buf *sb, const mpg_walk_opts *o,
+                                        mpg_walk_buf *out, mpg_walk_stats *stats, void *workspace,
+                                        size_t workspace_bytes, void *stream) {
+    ARG_CHECK(scene && sd && q && sb && o && out, "NULL argument");
+    ARG_CHECK(q->xD && q->nD && sb->xL && sb->target && sb->bin, "NULL query/seed array");
+    ARG_CHECK(out->chain && out->status && out->iters && out->G && out->T && out->w && out->trials, "NULL output array");
+    ARG_CHECK(q->n_recv >= 0 && q->spp >= 1, "bad query sizes");
+    ARG_CHECK(workspace && workspace_bytes >= mpg_walk_workspace_size(q->n_recv * q->spp, o), "workspace too small");
+    ARG_CHECK(o->max_iters >= 0 && o->max_iters < 65536 && o->tol > 0.f && o->beta0 > 0.f, "bad walk options");
+    ARG_CHECK(!o->trials || o->k_max >= 1, "k_max must be >= 1");
+    SeedCtx g;
+    mpg_status st = make_seed_ctx(scene, guide, sd, o, g);
+    if (st != MPG_OK) return st;
+    WalkParams P;
+    memset(&P, 0, sizeof(P));
+    P.n_recv = q->n_recv;
+    P.spp = q->spp;
+    P.n = q->n_recv * q->spp;
+    cudaStream_t s = as_stream(stream);
+    if (stats) CUDA_TRY(cudaMemsetAsync(stats, 0, sizeof(mpg_walk_stats), s));
+    if (P.n == 0) return MPG_OK;
+    P.xD = (const float4 *)q->xD;
+    P.nD = (const float4 *)q->nD;
+    P.seed_xL = (const float4 *)sb->xL;
+    P.seed_tgt = (const float4 *)sb->target;
+    P.seed_bin = sb->bin;
+    P.chain = (float4 *)out->chain;
+    P.status = out->status;
+    P.iters = out->iters;
+    P.G = out->G; P.T = out->T; P.w = out->w;
+    P.trials = out->trials;
+    P.queue = (unsigned long long *)workspace;
+    P.stats = (unsigned long long *)stats;
+    P.max_iters = o->max_iters;
+    P.trials_on = o->trials;
+    P.k_max = o->k_max;
+    P.tol = o->tol;
+    P.beta0 = o->beta0;
+    P.same_eps = o->same_chain_eps > 0.f ? o->same_chain_eps : 1e-4f * scene->d.extent;
+    P.ray_eps = o->ray_eps > 0.f ? o->ray_eps : 1e-4f * scene->d.extent;
+    P.walk_id_base = o->walk_id_base;
+    CUDA_TRY(cudaMemsetAsync(workspace, 0, 64, s));
+    int k = g.k;
+    if (k <= 1) return launch_walk<1>(scene->d, g, P, s);
+    if (k <= 2) return launch_walk<2>(scene->d, g, P, s);
+    if (k <= 4) return launch_walk<4>(scene->d, g, P, s);
+    if (k <= 6) return launch_walk<6>(scene->d, g, P, s);
+    return launch_walk<8>(scene->d, g, P, s);
+}
+
+// ----------------------------------------------------------------------------
+// estimator (Eq. 3)
+// ----------------------------------------------------------------------------
+__global__ void k_estimate(const float *w, int64_t n_recv, int spp, float *mean, float *var) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n_recv; r += (int64_t)gridDim.x * blockDim.x) {
+        double s = 0.0, s2 = 0.0;
+        for (int j = 0; j < spp; j++) {
+            double v = w[r * spp + j];
+            s += v;
+            s2 += v * v;
+        }
+        mean[r] = (float)(s / spp);
+        if (var) var[r] = spp > 1 ? (float)((s2 - s * s / spp) / (spp - 1)) : 0.0f;
+    }
+}
+
+extern "C" mpg_status mpg_estimate(const float *w, int64_t n_recv, int32_t spp, float *mean, float *var, void *stream) {
+    ARG_CHECK(w && mean && n_recv >= 0 && spp >= 1, "bad argument");
+    if (n_recv == 0) return MPG_OK;
+    int blocks = (int)std::min<int64_t>((n_recv + 255) / 256, (int64_t)num_sms() * 8);
+    k_estimate<<<blocks, 256, 0, as_stream(stream)>>>(w, n_recv, spp, mean, var);
+    CUDA_TRY(cudaPeekAtLastError());
+    return MPG_OK;
+}
+
+extern "C" const char *mpg_last_error(void) { return g_err.c_str(); }
+extern "C" int32_t mpg_version(void) { return 1; }

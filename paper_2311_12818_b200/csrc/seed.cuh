@@ -1,0 +1,127 @@
+// seed.cuh -- light samples and seed-chain targets (device), shared by the
+// seed kernel (primary walks, trial 0) and the walk kernel (trials t >= 1).
+//
+// P:395-406 (initialization: x_1 uniform on specular surfaces)
+// (Eq. 8), P:501-512 (Eq. 13 defensive mixture, alpha = 1/2), P:337 (x_L by
+// uniform emitter sampling).  All arithmetic that decides a seed is fp32
+// without contraction (R23), so the oracle's plain C float code draws the
+// same seeds; discrete choices are integer-exact (R2, R20).
+#pragma once
+#include "device_common.cuh"
+
+struct SeedCtx {
+    int mode, surf_id, k;
+    uint32_t tau;
+    uint64_t seed;
+    // guide (MPG_SEED_GUIDE_UV)
+    float gox, goz, gex, gez;
+    int cells_x, cells_y, bins_x, bins_y;
+    float uvox, uvoz, uvsx, uvsz, uv_y;
+    const uint64_t *prefix; // [cells][bins] inclusive prefix of W'
+};
+
+// x_L (purpose 0, trial 0) (R15); returns its pdf
+__device__ __forceinline__ float sample_light(const DScene &S, uint64_t seed, uint64_t wid, float3 &xL, int &lid) {
+    uint4 r = rng_draw(seed, wid, 0u, 0u);
+    int li = S.n_light > 1 ? (int)uidx(r.z, (uint32_t)S.n_light) : 0;
+    const DLight &L = S.light[li];
+    lid = li;
+    if (L.kind == 1) {
+        float a = u01(r.x) - 0.5f, b = u01(r.y) - 0.5f;
+        xL = f3(FA(L.pos.x, FA(FM(a, L.eu.x), FM(b, L.ev.x))), FA(L.pos.y, FA(FM(a, L.eu.y), FM(b, L.ev.y))),
+                FA(L.pos.z, FA(FM(a, L.eu.z), FM(b, L.ev.z))));
+    } else {
+        xL = L.pos;
+    }
+    return L.pdf;
+}
+
+__device__ __forceinline__ void onb_exact(float3 n, float3 &b1, float3 &b2) {
+    float sign = copysignf(1.0f, n.z);
+    float a = FD(-1.0f, FA(sign, n.z));
+    float b = FM(FM(n.x, n.y), a);
+    b1 = f3(FA(1.0f, FM(FM(FM(sign, n.x), n.x), a)), FM(sign, b), FM(-sign, n.x));
+    b2 = f3(b, FA(sign, FM(FM(n.y, n.y), a)), -n.y);
+}
+
+// Seed target for (walk, trial): the deduction ray x_D -> target gives x_1
+// (Eq. 6).  Returns false if no seed could be drawn (SEED_FAIL).
+__device__ __forceinline__ bool seed_target(const DScene &S, const SeedCtx &g, uint64_t wid, uint32_t trial,
+                                            float3 xD, float3 &tgt, int &bin) {
+    bin = -1;
+    if (g.mode == 0) { // uniform on the cap of a sphere visible from x_D
+        const DSurf &f = S.surf[g.surf_id];
+        float dx = FS(xD.x, f.center.x), dy = FS(xD.y, f.center.y), dz = FS(xD.z, f.center.z);
+        float L = __fsqrt_rn(FA(FA(FM(dx, dx), FM(dy, dy)), FM(dz, dz)));
+        float3 a = f3(FD(dx, L), FD(dy, L), FD(dz, L));
+        float cmin = FD(f.radius, L);
+        uint4 r = rng_draw(g.seed, wid, 2u, trial);
+        float u1 = u01(r.x), u2 = u01(r.y);
+        float ct = FS(1.0f, FM(u1, FS(1.0f, cmin)));
+        float st2 = FS(1.0f, FM(ct, ct));
+        float st = __fsqrt_rn(st2 > 0.0f ? st2 : 0.0f);
+        float phi = FM(6.28318530717958647692f, u2);
+        float cp = cosf(phi), sp = sinf(phi);
+        float3 b1, b2;
+        onb_exact(a, b1, b2);
+        float ddx = FA(FM(ct, a.x), FM(st, FA(FM(cp, b1.x), FM(sp, b2.x))));
+        float ddy = FA(FM(ct, a.y), FM(st, FA(FM(cp, b1.y), FM(sp, b2.y))));
+        float ddz = FA(FM(ct, a.z), FM(st, FA(FM(cp, b1.z), FM(sp, b2.z))));
+        tgt = f3(FA(f.center.x, FM(f.radius, ddx)), FA(f.center.y, FM(f.radius, ddy)),
+                 FA(f.center.z, FM(f.radius, ddz)));
+        return true;
+    }
+    if (g.mode == 1) { // triangle uniform by count among front-facing, <= 32 rejection draws
+        const DSurf &f = S.surf[g.surf_id];
+        int tri = -1;
+        float3 v0, e1, e2;
+        for (uint32_t rr = 0; rr < 32u; rr++) {
+            uint4 r = rng_draw(g.seed, wid, 16u + rr, trial);
+            int t = f.tri_begin + (int)uidx(r.x, (uint32_t)f.tri_count);
+            int4 ix = __ldg(S.oidx + t);
+            float3 p0 = xyz(__ldg(S.vpos + ix.x)), p1 = xyz(__ldg(S.vpos + ix.y)), p2 = xyz(__ldg(S.vpos + ix.z));
+            float3 a = f3(FS(p1.x, p0.x), FS(p1.y, p0.y), FS(p1.z, p0.z));
+            float3 b = f3(FS(p2.x, p0.x), FS(p2.y, p0.y), FS(p2.z, p0.z));
+            float ngx = FS(FM(a.y, b.z), FM(a.z, b.y));
+            float ngy = FS(FM(a.z, b.x), FM(a.x, b.z));
+            float ngz = FS(FM(a.x, b.y), FM(a.y, b.x));
+            float dd = FA(FA(FM(FS(xD.x, p0.x), ngx), FM(FS(xD.y, p0.y), ngy)), FM(FS(xD.z, p0.z), ngz));
+            if (dd > 0.0f) { tri = t; v0 = p0; e1 = a; e2 = b; break; }
+        }
+        if (tri < 0) return false;
+        bin = tri;
+        uint4 r = rng_draw(g.seed, wid, 2u, trial);
+        float u1 = u01(r.x), u2 = u01(r.y);
+        float sq = __fsqrt_rn(u1);
+        float c1 = FM(sq, FS(1.0f, u2)), c2 = FM(sq, u2);
+        tgt = f3(FA(v0.x, FA(FM(c1, e1.x), FM(c2, e2.x))), FA(v0.y, FA(FM(c1, e1.y), FM(c2, e2.y))),
+                 FA(v0.z, FA(FM(c1, e1.z), FM(c2, e2.z))));
+        return true;
+    }
+    if (g.mode == 2) { // guided bin over the surface (u,v): integer CDF of W' (R20)
+        int cx = (int)floorf(FD(FM(FS(xD.x, g.gox), (float)g.cells_x), g.gex));
+        int cz = (int)floorf(FD(FM(FS(xD.z, g.goz), (float)g.cells_y), g.gez));
+        cx = min(max(cx, 0), g.cells_x - 1);
+        cz = min(max(cz, 0), g.cells_y - 1);
+        int nb = g.bins_x * g.bins_y;
+        const uint64_t *pf = g.prefix + (size_t)(cz * g.cells_x + cx) * nb;
+        uint64_t S_ = __ldg((const unsigned long long *)pf + nb - 1);
+        uint4 r = rng_draw(g.seed, wid, 1u, trial);
+        uint64_t x = r.x;
+        uint64_t t = x * (S_ >> 32) + ((x * (S_ & 0xffffffffull)) >> 32); // floor(x*S/2^32)
+        int lo = 0, hi = nb - 1; // upper_bound: first b with prefix[b] > t
+        while (lo < hi) {
+            int mid = (lo + hi) >> 1;
+            if ((uint64_t)__ldg((const unsigned long long *)pf + mid) > t) hi = mid;
+            else lo = mid + 1;
+        }
+        bin = lo;
+        int bx = lo % g.bins_x, by = lo / g.bins_x;
+        uint4 r2 = rng_draw(g.seed, wid, 2u, trial);
+        float u = FD(FA((float)bx, u01(r2.x)), (float)g.bins_x);
+        float v = FD(FA((float)by, u01(r2.y)), (float)g.bins_y);
+        tgt = f3(FA(g.uvox, FM(u, g.uvsx)), g.uv_y, FA(g.uvoz, FM(v, g.uvsz)));
+        return true;
+    }
+    return false;
+}

@@ -1,0 +1,551 @@
+// walk.cuh -- the persistent manifold-walk kernel (sm_100a).
+//
+// One chain per lane.  Lanes run a small state machine
+//   FETCH -> SEED -> DEDUCE(trace k rays) -> SOLVE -> REPROJ(trace k rays) -> SOLVE ... -> END
+// at Newton-iteration granularity, so a lane whose walk (or trial) ends takes
+// the next work item from a global queue (warp-aggregated atomicAdd) while the
+// other lanes of its warp keep iterating: warp execution stays full despite
+// iteration counts of 0..max_iters and geometric trial counts (SURVEY §7
+// "Divergence").  Deduction and reprojection share one trace loop.
+//
+// Method: Newton on the stacked generalized-half-vector
+// constraints C_i = (s.h, t.h) (R1-R3) with the block-tridiagonal Jacobian
+// solved by block Thomas elimination fused with the block evaluation (only
+// D'^-1_i, U_i, r'_i survive per vertex), step on the geometric tangent planes
+// (R4), sequential ray-traced reprojection with step halving (R5, R6),
+// convergence on ||C||_inf < tol (R7), sides (R8), visibility, kappa (R12),
+// analytic GGT by one more back-substitution with the 2-column light RHS (R11),
+// and reciprocal-probability trials (Eq. 15, R13).
+#pragma once
+#include "device_common.cuh"
+#include "seed.cuh"
+
+enum { PH_FETCH = 0, PH_SEED = 1, PH_DEDUCE = 2, PH_SOLVE = 3, PH_REPROJ = 4, PH_END = 5, PH_IDLE = 6 };
+enum { ST_CONVERGED = 0, ST_MAXITER = 1, ST_SEED_FAIL = 2, ST_BAD_SIDE = 3, ST_DEGENERATE = 4, ST_OCCLUDED = 5 };
+
+struct WalkParams {
+    const float4 *xD, *nD;
+    int64_t n_recv, n;
+    int spp;
+    const float4 *seed_xL, *seed_tgt;
+    const int *seed_bin;
+    float4 *chain;
+    uint8_t *status;
+    uint16_t *iters;
+    float *G, *T, *w;
+    uint32_t *trials;
+    unsigned long long *queue;
+    unsigned long long *stats; // mpg_walk_stats as u64[21]
+    int max_iters, trials_on;
+    uint32_t k_max;
+    float tol, beta0, same_eps, ray_eps;
+    uint64_t walk_id_base;
+};
+
+// stats slots (mirror mpg_walk_stats field order)
+enum { SS_WALKS = 0, SS_CONV, SS_NEWTON, SS_PRIM_IT, SS_ATTEMPTS, SS_RAYS, SS_TRIALS, SS_TRUNC, SS_NODES, SS_TRIS,
+       SS_VTX, SS_STATUS0, SS_N = SS_STATUS0 + 8 };
+
+// reflect / refract the propagation direction d at a vertex (deduction, Eq. 6);
+// media from the side of d w.r.t. the geometric normal (R9, R14)
+__device__ __forceinline__ bool scatter_dir(const DScene &S, float3 &d, int prim, int surf, float3 p, bool isT) {
+    const DSurf &f = S.surf[surf];
+    float3 ng = geo_normal(S, prim, surf, p);
+    float3 n = shading_normal(S, prim, surf, p);
+    bool outside = dot(d, ng) < 0.0f;
+    if (dot(d, n) > 0.0f) n = -n;
+    float ci = -dot(d, n);
+    if (!(ci > 0.0f)) return false;
+    if (!isT) {
+        d = d + n * (2.0f * ci);
+        return true;
+    }
+    if (f.mat != 1) return false;
+    float e1 = outside ? f.eta_out : f.eta_in, e2 = outside ? f.eta_in : f.eta_out;
+    float eta = e1 / e2;
+    float k2 = 1.0f - eta * eta * (1.0f - ci * ci);
+    if (k2 < 0.0f) return false; // TIR
+    d = nrmz(d * eta + n * (eta * ci - sqrtf(k2)));
+    return true;
+}
+
+// Trace the k chain vertices from x_D: deduction (scatter by tau) or
+// reprojection toward q_i (must stay on surf_i).  Rolled loop: one traversal
+// site.  y/yp/ys/q live in local memory (dynamic index).
+template <int KMAX>
+__device__ __forceinline__ bool trace_chain(const DScene &S, bool deduce, int k, uint32_t tau, float3 xD, float3 tgt,
+                                            const float3 *q, uint32_t surf_req, float eps, float3 *y, int *yp,
+                                            int *ys, LaneStats &st) {
+    float3 o = xD;
+    float3 d = f3(0.f, 0.f, 0.f);
+    if (deduce) {
+        float3 v = tgt - xD;
+        float l2 = dot(v, v);
+        if (!(l2 > 0.0f)) return false;
+        d = v * rsqrtf(l2);
+    }
+#pragma unroll 1
+    for (int i = 0; i < k; i++) {
+        if (!deduce) {
+            float3 v = q[i] - o;
+            float l2 = dot(v, v);
+            if (!(l2 > 0.0f)) return false;
+            d = v * rsqrtf(l2);
+        } else if (i > 0) {
+            if (!scatter_dir(S, d, yp[i - 1], ys[i - 1], y[i - 1], (tau >> (i - 1)) & 1u)) return false;
+        }
+        Hit h;
+        if (!trace<false>(S, o, d, eps, 3.0e38f, true, h, st)) return false;
+        if (!deduce && h.surf != (int)((surf_req >> (4 * i)) & 15u)) return false;
+        y[i] = h.p;
+        yp[i] = h.prim;
+        ys[i] = h.surf;
+        o = h.p;
+    }
+    return true;
+}
+
+// per-vertex constraint pieces
+struct VTerm {
+    float3 wi, wo, h, s, t;
+    float li, lo, ei, eo, hl, hn;
+};
+
+__device__ __forceinline__ bool vterm(float3 a, float3 p, float3 b, float3 ng, float3 n, const DSurf &f, bool isT,
+                                      VTerm &v) {
+    float3 da = a - p, db = b - p;
+    v.li = len(da);
+    v.lo = len(db);
+    if (!(v.li > 0.0f) || !(v.lo > 0.0f)) return false;
+    v.wi = da * (1.0f / v.li);
+    v.wo = db * (1.0f / v.lo);
+    if (isT) {
+        bool out = dot(v.wi, ng) > 0.0f;
+        v.ei = out ? f.eta_out : f.eta_in;
+        v.eo = out ? f.eta_in : f.eta_out;
+    } else {
+        v.ei = v.eo = 1.0f;
+    }
+    float3 ht = v.wi * v.ei + v.wo * v.eo;
+    v.hl = len(ht);
+    if (!(v.hl > 0.0f) || !isfinite(v.hl)) return false;
+    v.h = ht * (1.0f / v.hl);
+    onb(n, v.s, v.t);
+    v.hn = dot(v.h, n);
+    return true;
+}
+
+// dC along a neighbour displacement: c*P v with P the projector of w over l (L, U, D_L blocks)
+__device__ __forceinline__ float2 dC_nb(const VTerm &v, float3 w, float l, float eta, float3 dir) {
+    float3 u = (dir - w * dot(w, dir)) * (eta / l);
+    float3 dh = (u - v.h * dot(v.h, u)) * (1.0f / v.hl);
+    return make_float2(dot(v.s, dh), dot(v.t, dh));
+}
+// dC along the vertex's own displacement (D block; minimal-rotation frame, R3)
+__device__ __forceinline__ float2 dC_self(const VTerm &v, float3 dir, float3 dn) {
+    float3 u = (dir - v.wi * dot(v.wi, dir)) * (-v.ei / v.li) - (dir - v.wo * dot(v.wo, dir)) * (v.eo / v.lo);
+    float3 dh = (u - v.h * dot(v.h, u)) * (1.0f / v.hl);
+    return make_float2(dot(v.s, dh) - v.hn * dot(v.s, dn), dot(v.t, dh) - v.hn * dot(v.t, dn));
+}
+
+// Forward sweep: constraint + blocks + block-Thomas elimination; then (if not
+// converged) back substitution into world-space step directions dq.
+// returns 0: step ready, 1: converged, 2: degenerate.  `singular` reports a
+// singular pivot (used only if converged: G is then 0).
+template <int KMAX>
+__device__ __forceinline__ int newton_system(const DScene &S, int k, uint32_t tau, float3 xD, float3 xL,
+                                             const float3 (&x)[KMAX], const int (&prim)[KMAX],
+                                             const int (&surf)[KMAX], float tol, float (&Di)[KMAX][4],
+                                             float (&Ub)[KMAX][4], float3 (&sg)[KMAX], float3 (&tg)[KMAX],
+                                             float3 (&dq)[KMAX], bool &singular) {
+    float rp[KMAX][2];
+    bool degen = false;
+    singular = false;
+    float cmax = 0.0f;
+#pragma unroll
+    for (int i = 0; i < KMAX; i++) {
+        if (i >= k) break;
+        float3 ng = geo_normal(S, prim[i], surf[i], x[i]);
+        onb(ng, sg[i], tg[i]);
+    }
+#pragma unroll
+    for (int i = 0; i < KMAX; i++) {
+        if (i >= k) break;
+        float3 a = i == 0 ? xD : x[i > 0 ? i - 1 : 0];
+        float3 b = i == k - 1 ? xL : x[i + 1 < KMAX ? i + 1 : i];
+        const DSurf &f = S.surf[surf[i]];
+        float3 dna, dnb;
+        float3 n = shading(S, prim[i], surf[i], x[i], sg[i], tg[i], dna, dnb);
+        VTerm v;
+        if (!vterm(a, x[i], b, cross(sg[i], tg[i]), n, f, (tau >> i) & 1u, v)) { degen = true; break; }
+        float c0 = dot(v.s, v.h), c1 = dot(v.t, v.h);
+        cmax = fmaxf(cmax, fmaxf(fabsf(c0), fabsf(c1)));
+        float2 d0 = dC_self(v, sg[i], dna), d1 = dC_self(v, tg[i], dnb);
+        float D00 = d0.x, D10 = d0.y, D01 = d1.x, D11 = d1.y;
+        float r0 = -c0, r1 = -c1;
+        if (i > 0) {
+            const int j = i > 0 ? i - 1 : 0;
+            float2 l0 = dC_nb(v, v.wi, v.li, v.ei, sg[j]), l1 = dC_nb(v, v.wi, v.li, v.ei, tg[j]);
+            // M = L * Di[j]
+            float M00 = l0.x * Di[j][0] + l1.x * Di[j][2], M01 = l0.x * Di[j][1] + l1.x * Di[j][3];
+            float M10 = l0.y * Di[j][0] + l1.y * Di[j][2], M11 = l0.y * Di[j][1] + l1.y * Di[j][3];
+            D00 -= M00 * Ub[j][0] + M01 * Ub[j][2];
+            D01 -= M00 * Ub[j][1] + M01 * Ub[j][3];
+            D10 -= M10 * Ub[j][0] + M11 * Ub[j][2];
+            D11 -= M10 * Ub[j][1] + M11 * Ub[j][3];
+            r0 -= M00 * rp[j][0] + M01 * rp[j][1];
+            r1 -= M10 * rp[j][0] + M11 * rp[j][1];
+        }
+        if (i < k - 1) {
+            const int j = i + 1 < KMAX ? i + 1 : i;
+            float2 u0 = dC_nb(v, v.wo, v.lo, v.eo, sg[j]), u1 = dC_nb(v, v.wo, v.lo, v.eo, tg[j]);
+            Ub[i][0] = u0.x; Ub[i][1] = u1.x; Ub[i][2] = u0.y; Ub[i][3] = u1.y;
+        }
+        float det = D00 * D11 - D01 * D10;
+        if (!(det != 0.0f) || !isfinite(det)) singular = true;
+        float id = 1.0f / det;
+        Di[i][0] = D11 * id; Di[i][1] = -D01 * id; Di[i][2] = -D10 * id; Di[i][3] = D00 * id;
+        rp[i][0] = r0; rp[i][1] = r1;
+    }
+    if (degen || !isfinite(cmax)) return 2;
+    if (cmax < tol) return 1;
+    if (singular) return 2;
+    float n0 = 0.f, n1 = 0.f; // Delta_{i+1}
+#pragma unroll
+    for (int i = KMAX - 1; i >= 0; i--) {
+        if (i > k - 1) continue;
+        float r0 = rp[i][0], r1 = rp[i][1];
+        if (i < k - 1) {
+            r0 -= Ub[i][0] * n0 + Ub[i][1] * n1;
+            r1 -= Ub[i][2] * n0 + Ub[i][3] * n1;
+        }
+        float a0 = Di[i][0] * r0 + Di[i][1] * r1;
+        float a1 = Di[i][2] * r0 + Di[i][3] * r1;
+        if (!isfinite(a0) || !isfinite(a1)) return 2;
+        dq[i] = sg[i] * a0 + tg[i] * a1;
+        n0 = a0; n1 = a1;
+    }
+    return 0;
+}
+
+// sides (R8), kappa (R12) and the light-side block D_L at a converged chain.
+// returns false on a side violation.
+template <int KMAX>
+__device__ __forceinline__ bool post_sweep(const DScene &S, const DLight &L, int k, uint32_t tau, float3 xD,
+                                           float3 xL, const float3 (&x)[KMAX], const int (&prim)[KMAX],
+                                           const int (&surf)[KMAX], bool want_kappa, float &kappa, float (&DL)[4]) {
+    float kap = 1.0f, etaD = 1.0f, etaL = 1.0f;
+#pragma unroll
+    for (int i = 0; i < KMAX; i++) {
+        if (i >= k) break;
+        float3 a = i == 0 ? xD : x[i > 0 ? i - 1 : 0];
+        float3 b = i == k - 1 ? xL : x[i + 1 < KMAX ? i + 1 : i];
+        const DSurf &f = S.surf[surf[i]];
+        float3 ng = geo_normal(S, prim[i], surf[i], x[i]);
+        float di = dot(a - x[i], ng), dd = dot(b - x[i], ng);
+        bool isT = (tau >> i) & 1u;
+        if (isT ? !(di * dd < 0.0f) : !(di * dd > 0.0f)) return false;
+        if (!want_kappa) continue;
+        float3 n = shading_normal(S, prim[i], surf[i], x[i]);
+        bool oi = di > 0.0f, oo = dd > 0.0f;
+        float e_wi = oi ? f.eta_out : f.eta_in, e_wo = oo ? f.eta_out : f.eta_in;
+        if (i == 0) etaD = e_wi;
+        if (i == k - 1) {
+            etaL = e_wo;
+            VTerm v;
+            if (!vterm(a, x[i], b, ng, n, f, isT, v)) { DL[0] = DL[1] = DL[2] = DL[3] = 0.f; }
+            else {
+                float3 l1, l2;
+                if (L.kind == 1) { l1 = L.l1; l2 = L.l2; }
+                else onb(nrmz(xL - x[i]), l1, l2);
+                float2 c0 = dC_nb(v, v.wo, v.lo, v.eo, l1), c1 = dC_nb(v, v.wo, v.lo, v.eo, l2);
+                DL[0] = c0.x; DL[1] = c1.x; DL[2] = c0.y; DL[3] = c1.y;
+            }
+        }
+        if (f.mat == 0) kap *= f.refl;
+        else {
+            float e_other = oi ? f.eta_in : f.eta_out;
+            float3 wi = nrmz(a - x[i]);
+            float F = fresnel(dot(wi, n), e_wi, e_other);
+            kap *= isT ? (1.0f - F) : F;
+        }
+    }
+    kappa = kap * (etaD / etaL) * (etaD / etaL);
+    return true;
+}
+
+// analytic GGT: back-substitute J Y = -[0..0; D_L] with the stored D'^-1, U (R11)
+template <int KMAX>
+__device__ __forceinline__ float ggt_from_blocks(int k, float3 xD, float3 nD, const float3 (&x)[KMAX],
+                                                 const float (&Di)[KMAX][4], const float (&Ub)[KMAX][4],
+                                                 const float3 (&sg)[KMAX], const float3 (&tg)[KMAX],
+                                                 const float (&DL)[4]) {
+    float y00 = 0.f, y01 = 0.f, y10 = 0.f, y11 = 0.f; // Y_{i+1}
+#pragma unroll
+    for (int i = KMAX - 1; i >= 0; i--) {
+        if (i > k - 1) continue;
+        float b00, b01, b10, b11;
+        if (i == k - 1) { b00 = -DL[0]; b01 = -DL[1]; b10 = -DL[2]; b11 = -DL[3]; }
+        else {
+            b00 = -(Ub[i][0] * y00 + Ub[i][1] * y10);
+            b01 = -(Ub[i][0] * y01 + Ub[i][1] * y11);
+            b10 = -(Ub[i][2] * y00 + Ub[i][3] * y10);
+            b11 = -(Ub[i][2] * y01 + Ub[i][3] * y11);
+        }
+        float n00 = Di[i][0] * b00 + Di[i][1] * b10, n01 = Di[i][0] * b01 + Di[i][1] * b11;
+        float n10 = Di[i][2] * b00 + Di[i][3] * b10, n11 = Di[i][2] * b01 + Di[i][3] * b11;
+        y00 = n00; y01 = n01; y10 = n10; y11 = n11;
+    }
+    float3 r = x[0] - xD;
+    float rl = len(r);
+    float3 w = r * (1.0f / rl);
+    float3 e1, e2;
+    onb(w, e1, e2);
+    float3 dx0 = sg[0] * y00 + tg[0] * y10, dx1 = sg[0] * y01 + tg[0] * y11;
+    float3 dw0 = (dx0 - w * dot(w, dx0)) * (1.0f / rl), dw1 = (dx1 - w * dot(w, dx1)) * (1.0f / rl);
+    float M00 = dot(e1, dw0), M01 = dot(e1, dw1), M10 = dot(e2, dw0), M11 = dot(e2, dw1);
+    float G = fabsf(dot(nD, w)) * fabsf(M00 * M11 - M01 * M10);
+    return isfinite(G) ? G : 0.0f;
+}
+
+template <int KMAX>
+__global__ void __launch_bounds__(128) k_walk(const DScene S, const SeedCtx g, const WalkParams P) {
+    __shared__ unsigned long long s_stats[SS_N];
+    for (int i = threadIdx.x; i < SS_N; i += blockDim.x) s_stats[i] = 0ull;
+    __syncthreads();
+
+    const int lane = threadIdx.x & 31;
+    const int k = g.k;
+    const uint32_t tau = g.tau;
+
+    // lane state
+    int phase = PH_FETCH;
+    int64_t w = -1;
+    uint32_t trial = 0;
+    int end_status = 0;
+    float3 xD = f3(0, 0, 0), nD = f3(0, 1, 0), xL = f3(0, 0, 0), tgt = f3(0, 0, 0);
+    float pdfL = 1.f, Tprim = 0.f;
+    int lid = 0;
+    int it = 0;
+    float beta = 1.f;
+    bool fresh = false;
+    uint32_t psurf = 0; // primary surf ids, 4 bits each
+    float3 x[KMAX], sg[KMAX], tg[KMAX], dq[KMAX];
+    int prim[KMAX], surf[KMAX];
+    float Di[KMAX][4], Ub[KMAX][4];
+    float3 q[KMAX], y[KMAX];
+    int yp[KMAX], ys[KMAX];
+    bool singular = false;
+#pragma unroll
+    for (int i = 0; i < KMAX; i++) { x[i] = sg[i] = tg[i] = dq[i] = f3(0, 0, 0); prim[i] = -1; surf[i] = 0; }
+    LaneStats ls = {0u, 0u, 0u};
+    uint32_t c_newton = 0, c_vtx = 0, c_attempts = 0;
+
+    while (true) {
+        // ---- fetch (warp-aggregated) -------------------------------------
+        unsigned need = __ballot_sync(MPG_FULL, phase == PH_FETCH);
+        if (need) {
+            int leader = __ffs(need) - 1;
+            unsigned long long base = 0;
+            if (lane == leader) base = atomicAdd(P.queue, (unsigned long long)__popc(need));
+            base = __shfl_sync(MPG_FULL, base, leader);
+            if (phase == PH_FETCH) {
+                int64_t idx = (int64_t)base + __popc(need & ((1u << lane) - 1u));
+                if (idx < P.n) {
+                    w = idx;
+                    trial = 0;
+                    int64_t rcv = idx / P.spp;
+                    xD = xyz(__ldg(P.xD + rcv));
+                    nD = xyz(__ldg(P.nD + rcv));
+                    float4 l4 = __ldg(P.seed_xL + idx);
+                    xL = xyz(l4);
+                    pdfL = l4.w;
+                    lid = 0;
+                    if (S.n_light > 1) lid = (int)uidx(rng_draw(g.seed, P.walk_id_base + idx, 0u, 0u).z, (uint32_t)S.n_light);
+                    phase = PH_SEED;
+                } else {
+                    phase = PH_IDLE;
+                }
+            }
+        }
+        if (__all_sync(MPG_FULL, phase == PH_IDLE)) break;
+
+        // ---- seed ---------------------------------------------------------
+        if (phase == PH_SEED) {
+            c_attempts++;
+            bool ok;
+            if (trial == 0) {
+                ok = __ldg(P.seed_bin + w) != -2;
+                tgt = xyz(__ldg(P.seed_tgt + w));
+            } else {
+                int bin;
+                ok = seed_target(S, g, P.walk_id_base + w, trial, xD, tgt, bin);
+            }
+            it = 0;
+            if (ok) phase = PH_DEDUCE;
+            else { end_status = ST_SEED_FAIL; phase = PH_END; }
+        }
+
+        // ---- trace: deduction (Eq. 6) or reprojection --------------------
+        if (phase == PH_DEDUCE || phase == PH_REPROJ) {
+            bool ded = phase == PH_DEDUCE;
+            uint32_t sreq = 0;
+#pragma unroll
+            for (int i = 0; i < KMAX; i++) sreq |= (uint32_t)(surf[i] & 15) << (4 * i);
+            bool ok = trace_chain<KMAX>(S, ded, k, tau, xD, tgt, q, sreq, P.ray_eps, y, yp, ys, ls);
+            if (ok) {
+#pragma unroll
+                for (int i = 0; i < KMAX; i++) {
+                    if (i >= k) break;
+                    x[i] = y[i]; prim[i] = yp[i]; surf[i] = ys[i];
+                }
+                fresh = true;
+                if (ded) { beta = P.beta0; it = 0; }
+                else { beta = fminf(1.0f, 2.0f * beta); it++; }
+                phase = PH_SOLVE;
+            } else if (ded) {
+                end_status = ST_SEED_FAIL;
+                phase = PH_END;
+            } else {
+                beta *= 0.5f;
+                it++;
+                phase = PH_SOLVE;
+            }
+        }
+
+        // ---- Newton system / step ------------------------------------------
+        if (phase == PH_SOLVE) {
+            if (fresh) {
+                fresh = false;
+                c_vtx += k;
+                int r = newton_system<KMAX>(S, k, tau, xD, xL, x, prim, surf, P.tol, Di, Ub, sg, tg, dq, singular);
+                if (r == 1) { end_status = ST_CONVERGED; phase = PH_END; }
+                else if (r == 2) { end_status = ST_DEGENERATE; phase = PH_END; }
+            }
+            if (phase == PH_SOLVE) {
+                if (it >= P.max_iters) { end_status = ST_MAXITER; phase = PH_END; }
+                else {
+#pragma unroll
+                    for (int i = 0; i < KMAX; i++) {
+                        if (i >= k) break;
+                        q[i] = x[i] + dq[i] * beta;
+                    }
+                    phase = PH_REPROJ;
+                }
+            }
+        }
+
+        // ---- end of an attempt ---------------------------------------------
+        if (phase == PH_END) {
+            c_newton += it;
+            int st = end_status;
+            if (trial == 0) {
+                float G = 0.f, T = 0.f;
+                if (st == ST_CONVERGED) {
+                    const DLight &L = S.light[lid];
+                    float kap, DL[4];
+                    if (!post_sweep<KMAX>(S, L, k, tau, xD, xL, x, prim, surf, true, kap, DL)) st = ST_BAD_SIDE;
+                    else {
+                        // visibility: k+1 any-hit segments against all surfaces
+                        bool vis = true;
+                        float3 a = xD;
+#pragma unroll 1
+                        for (int j = 0; j <= k; j++) {
+                            float3 b = j == k ? xL : y[j];
+                            float3 dd = b - a;
+                            float l = len(dd);
+                            Hit hh;
+                            if (trace<true>(S, a, dd * (1.0f / l), P.ray_eps, l - P.ray_eps, false, hh, ls)) {
+                                vis = false;
+                                break;
+                            }
+                            a = b;
+                        }
+                        if (!vis) st = ST_OCCLUDED;
+                        else {
+                            G = singular ? 0.0f : ggt_from_blocks<KMAX>(k, xD, nD, x, Di, Ub, sg, tg, DL);
+                            float Le = L.emit;
+                            if (L.kind == 1 && !(dot(x[k - 1] - xL, L.n) > 0.0f)) Le = 0.0f;
+                            T = kap * G * Le;
+                        }
+                    }
+                }
+                if (st != ST_SEED_FAIL) {
+#pragma unroll
+                    for (int i = 0; i < KMAX; i++) {
+                        if (i >= k) break;
+                        int pid = prim[i] >= 0 ? __float_as_int(__ldg(S.tpos + 3 * prim[i]).w) : -1;
+                        P.chain[(int64_t)i * P.n + w] = make_float4(x[i].x, x[i].y, x[i].z, __int_as_float(pid));
+                    }
+                }
+                P.status[w] = (uint8_t)st;
+                P.iters[w] = (uint16_t)it;
+                P.G[w] = G;
+                P.T[w] = T;
+                atomicAdd(&s_stats[SS_STATUS0 + st], 1ull);
+                atomicAdd(&s_stats[SS_PRIM_IT], (unsigned long long)it);
+                atomicAdd(&s_stats[SS_WALKS], 1ull);
+                if (st == ST_CONVERGED || st == ST_OCCLUDED) atomicAdd(&s_stats[SS_CONV], 1ull);
+                if (st == ST_CONVERGED && T > 0.0f && P.trials_on) {
+                    Tprim = T;
+                    psurf = 0;
+#pragma unroll
+                    for (int i = 0; i < KMAX; i++) {
+                        if (i >= k) break;
+                        psurf |= (uint32_t)(surf[i] & 15) << (4 * i);
+                    }
+                    trial = 1;
+                    phase = PH_SEED;
+                } else {
+                    P.trials[w] = 0;
+                    P.w[w] = 0.0f;
+                    phase = PH_FETCH;
+                }
+            } else {
+                bool same = false;
+                float kdummy, DLdummy[4];
+                if (st == ST_CONVERGED &&
+                    post_sweep<KMAX>(S, S.light[lid], k, tau, xD, xL, x, prim, surf, false, kdummy, DLdummy)) {
+                    same = true;
+#pragma unroll
+                    for (int i = 0; i < KMAX; i++) {
+                        if (i >= k) break;
+                        float4 c = P.chain[(int64_t)i * P.n + w];
+                        float3 dd = x[i] - xyz(c);
+                        if ((int)((psurf >> (4 * i)) & 15u) != (surf[i] & 15) || !(len(dd) < P.same_eps)) same = false;
+                    }
+                }
+                if (same || trial >= P.k_max) {
+                    if (!same) atomicAdd(&s_stats[SS_TRUNC], 1ull);
+                    P.trials[w] = trial;
+                    P.w[w] = Tprim * (float)trial / pdfL;
+                    atomicAdd(&s_stats[SS_TRIALS], (unsigned long long)trial);
+                    phase = PH_FETCH;
+                } else {
+                    trial++;
+                    phase = PH_SEED;
+                }
+            }
+        }
+    }
+
+    // ---- stats reduction ----------------------------------------------------
+    unsigned long long v[6] = {c_newton, c_attempts, ls.rays, ls.nodes, ls.tris, c_vtx};
+#pragma unroll
+    for (int j = 0; j < 6; j++) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v[j] += __shfl_down_sync(MPG_FULL, v[j], o);
+    }
+    if (lane == 0) {
+        atomicAdd(&s_stats[SS_NEWTON], v[0]);
+        atomicAdd(&s_stats[SS_ATTEMPTS], v[1]);
+        atomicAdd(&s_stats[SS_RAYS], v[2]);
+        atomicAdd(&s_stats[SS_NODES], v[3]);
+        atomicAdd(&s_stats[SS_TRIS], v[4]);
+        atomicAdd(&s_stats[SS_VTX], v[5]);
+    }
+    __syncthreads();
+    if (P.stats)
+        for (int i = threadIdx.x; i < SS_N; i += blockDim.x)
+            if (s_stats[i]) atomicAdd(P.stats + i, s_stats[i]);
+}

@@ -1,0 +1,377 @@
+"""Thin ctypes binding of libmpg.so (include/mpg.h).
+
+Argument marshalling only: every step of the walk runs in the CUDA kernels of
+csrc/.  PyTorch provides device memory and streams.  There is no CPU fallback:
+if the shared library is missing or no CUDA device is present, the calls raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import Optional
+
+import numpy as np
+
+from . import workloads as W
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libmpg.so")
+KMAX = 8
+STATUS_NAMES = ["CONVERGED", "MAXITER", "SEED_FAIL", "BAD_SIDE", "DEGENERATE", "OCCLUDED"]
+
+
+class MPGError(RuntimeError):
+    pass
+
+
+# ----------------------------------------------------------------------------
+# C records (same layout as include/mpg.h)
+# ----------------------------------------------------------------------------
+class mpg_surface_desc(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("mat", C.c_int32), ("eta_in", C.c_float), ("eta_out", C.c_float),
+                ("reflectance", C.c_float), ("center", C.c_float * 3), ("radius", C.c_float),
+                ("origin", C.c_float * 3), ("edge_u", C.c_float * 3), ("edge_v", C.c_float * 3),
+                ("positions", C.c_void_p), ("normals", C.c_void_p), ("indices", C.c_void_p),
+                ("n_vertices", C.c_int32), ("n_triangles", C.c_int32)]
+
+
+class mpg_light_desc(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("emit", C.c_float), ("position", C.c_float * 3), ("edge_u", C.c_float * 3),
+                ("edge_v", C.c_float * 3)]
+
+
+class mpg_sampler_desc(C.Structure):
+    _fields_ = [("mode", C.c_int32), ("surf_id", C.c_int32), ("k", C.c_int32), ("tau", C.c_uint32)]
+
+
+class mpg_guide_desc(C.Structure):
+    _fields_ = [("grid_origin", C.c_float * 2), ("grid_extent", C.c_float * 2), ("cells_x", C.c_int32),
+                ("cells_y", C.c_int32), ("bins_x", C.c_int32), ("bins_y", C.c_int32), ("uv_origin", C.c_float * 2),
+                ("uv_scale", C.c_float * 2), ("uv_plane_y", C.c_float)]
+
+
+class mpg_walk_opts(C.Structure):
+    _fields_ = [("max_iters", C.c_int32), ("tol", C.c_float), ("beta0", C.c_float), ("trials", C.c_int32),
+                ("k_max", C.c_uint32), ("same_chain_eps", C.c_float), ("ray_eps", C.c_float), ("flags", C.c_uint32),
+                ("seed", C.c_uint64), ("walk_id_base", C.c_uint64)]
+
+
+class mpg_query(C.Structure):
+    _fields_ = [("xD", C.c_void_p), ("nD", C.c_void_p), ("n_recv", C.c_int64), ("spp", C.c_int32)]
+
+
+class mpg_seed_buf(C.Structure):
+    _fields_ = [("xL", C.c_void_p), ("target", C.c_void_p), ("bin", C.c_void_p)]
+
+
+class mpg_walk_buf(C.Structure):
+    _fields_ = [("chain", C.c_void_p), ("status", C.c_void_p), ("iters", C.c_void_p), ("G", C.c_void_p),
+                ("T", C.c_void_p), ("w", C.c_void_p), ("trials", C.c_void_p)]
+
+
+STATS_FIELDS = ["walks", "converged", "newton_iters", "primary_iters", "attempts", "rays", "trials", "truncated",
+                "node_visits", "tri_tests", "vertex_iters"]
+
+
+class mpg_walk_stats(C.Structure):
+    _fields_ = [(f, C.c_ulonglong) for f in STATS_FIELDS] + [("by_status", C.c_ulonglong * 8)]
+
+
+class mpg_scene_info(C.Structure):
+    _fields_ = [("extent", C.c_float), ("n_surf", C.c_int32), ("n_light", C.c_int32), ("n_tri", C.c_int32),
+                ("n_nodes", C.c_int32), ("device_bytes", C.c_size_t)]
+
+
+EXPORTS = ["mpg_scene_create", "mpg_scene_destroy", "mpg_scene_get_info", "mpg_trace_rays", "mpg_guide_create",
+           "mpg_guide_destroy", "mpg_guide_upload", "mpg_guide_reset", "mpg_guide_accumulate", "mpg_guide_rebuild",
+           "mpg_guide_download", "mpg_sample_seeds", "mpg_walk_workspace_size", "mpg_manifold_walk", "mpg_estimate",
+           "mpg_last_error", "mpg_version"]
+
+_lib = None
+
+
+def lib():
+    """Load libmpg.so (fails loudly if it was not built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise MPGError(f"{LIB_PATH} not built: run `python -c 'import __graft_entry__ as g; g.build()'`")
+        L = C.CDLL(LIB_PATH)
+        P = C.c_void_p
+        st = C.c_int
+        sig = {
+            "mpg_scene_create": (st, [C.POINTER(mpg_surface_desc), C.c_int32, C.POINTER(mpg_light_desc), C.c_int32, P,
+                                      C.POINTER(P)]),
+            "mpg_scene_destroy": (st, [P]),
+            "mpg_scene_get_info": (st, [P, C.POINTER(mpg_scene_info)]),
+            "mpg_trace_rays": (st, [P, P, P, C.c_int64, C.c_float, C.c_int32, P, P, P, P]),
+            "mpg_guide_create": (st, [C.POINTER(mpg_guide_desc), C.POINTER(P)]),
+            "mpg_guide_destroy": (st, [P]),
+            "mpg_guide_upload": (st, [P, P, P]),
+            "mpg_guide_reset": (st, [P, P]),
+            "mpg_guide_accumulate": (st, [P, C.POINTER(mpg_query), C.POINTER(mpg_walk_buf), C.c_int64, P]),
+            "mpg_guide_rebuild": (st, [P, P]),
+            "mpg_guide_download": (st, [P, P, P, P]),
+            "mpg_sample_seeds": (st, [P, P, C.POINTER(mpg_sampler_desc), C.POINTER(mpg_query),
+                                      C.POINTER(mpg_walk_opts), C.POINTER(mpg_seed_buf), P]),
+            "mpg_walk_workspace_size": (C.c_size_t, [C.c_int64, C.POINTER(mpg_walk_opts)]),
+            "mpg_manifold_walk": (st, [P, P, C.POINTER(mpg_sampler_desc), C.POINTER(mpg_query),
+                                       C.POINTER(mpg_seed_buf), C.POINTER(mpg_walk_opts), C.POINTER(mpg_walk_buf), P,
+                                       P, C.c_size_t, P]),
+            "mpg_estimate": (st, [P, C.c_int64, C.c_int32, P, P, P]),
+            "mpg_last_error": (C.c_char_p, []),
+            "mpg_version": (C.c_int32, []),
+        }
+        for name, (res, args) in sig.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    return _lib
+
+
+def _check(status: int, what: str):
+    if status != 0:
+        msg = lib().mpg_last_error().decode()
+        raise MPGError(f"{what} failed ({status}): {msg}")
+
+
+def _stream_ptr(stream=None):
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+def _ptr(t):
+    return C.c_void_p(t.data_ptr()) if t is not None else None
+
+
+# ----------------------------------------------------------------------------
+# same-named Python entry points
+# ----------------------------------------------------------------------------
+def mpg_scene_create(surfaces, lights, stream=None):
+    n = len(surfaces)
+    S = (mpg_surface_desc * n)(*surfaces)
+    Ls = (mpg_light_desc * len(lights))(*lights)
+    h = C.c_void_p()
+    _check(lib().mpg_scene_create(S, n, Ls, len(lights), _stream_ptr(stream), C.byref(h)), "mpg_scene_create")
+    return h
+
+
+def mpg_scene_destroy(h):
+    _check(lib().mpg_scene_destroy(h), "mpg_scene_destroy")
+
+
+def mpg_scene_get_info(h) -> mpg_scene_info:
+    info = mpg_scene_info()
+    _check(lib().mpg_scene_get_info(h, C.byref(info)), "mpg_scene_get_info")
+    return info
+
+
+def mpg_trace_rays(h, orig, direc, tmin, spec_only, t, prim, surf, stream=None):
+    _check(lib().mpg_trace_rays(h, _ptr(orig), _ptr(direc), orig.shape[0], tmin, int(spec_only), _ptr(t), _ptr(prim),
+                                _ptr(surf), _stream_ptr(stream)), "mpg_trace_rays")
+
+
+def mpg_guide_create(desc: mpg_guide_desc):
+    h = C.c_void_p()
+    _check(lib().mpg_guide_create(C.byref(desc), C.byref(h)), "mpg_guide_create")
+    return h
+
+
+def mpg_guide_destroy(h):
+    _check(lib().mpg_guide_destroy(h), "mpg_guide_destroy")
+
+
+def mpg_guide_upload(h, energy, stream=None):
+    _check(lib().mpg_guide_upload(h, _ptr(energy), _stream_ptr(stream)), "mpg_guide_upload")
+
+
+def mpg_guide_reset(h, stream=None):
+    _check(lib().mpg_guide_reset(h, _stream_ptr(stream)), "mpg_guide_reset")
+
+
+def mpg_guide_accumulate(h, query: mpg_query, walks: mpg_walk_buf, n: int, stream=None):
+    _check(lib().mpg_guide_accumulate(h, C.byref(query), C.byref(walks), n, _stream_ptr(stream)),
+           "mpg_guide_accumulate")
+
+
+def mpg_guide_rebuild(h, stream=None):
+    _check(lib().mpg_guide_rebuild(h, _stream_ptr(stream)), "mpg_guide_rebuild")
+
+
+def mpg_guide_download(h, energy=None, prefix=None, stream=None):
+    _check(lib().mpg_guide_download(h, _ptr(energy), _ptr(prefix), _stream_ptr(stream)), "mpg_guide_download")
+
+
+def mpg_sample_seeds(scene, guide, sampler, query, opts, seeds, stream=None):
+    _check(lib().mpg_sample_seeds(scene, guide, C.byref(sampler), C.byref(query), C.byref(opts), C.byref(seeds),
+                                  _stream_ptr(stream)), "mpg_sample_seeds")
+
+
+def mpg_walk_workspace_size(n, opts) -> int:
+    return int(lib().mpg_walk_workspace_size(n, C.byref(opts)))
+
+
+def mpg_manifold_walk(scene, guide, sampler, query, seeds, opts, out, stats, workspace, stream=None):
+    _check(lib().mpg_manifold_walk(scene, guide, C.byref(sampler), C.byref(query), C.byref(seeds), C.byref(opts),
+                                   C.byref(out), _ptr(stats), _ptr(workspace), workspace.numel(),
+                                   _stream_ptr(stream)), "mpg_manifold_walk")
+
+
+def mpg_estimate(w, n_recv, spp, mean, var=None, stream=None):
+    _check(lib().mpg_estimate(_ptr(w), n_recv, spp, _ptr(mean), _ptr(var), _stream_ptr(stream)), "mpg_estimate")
+
+
+def mpg_version() -> int:
+    return int(lib().mpg_version())
+
+
+# ----------------------------------------------------------------------------
+# convenience: a Workload (paper_2311_12818_b200.workloads) on the device
+# ----------------------------------------------------------------------------
+def _f3(v):
+    return (C.c_float * 3)(*[float(a) for a in v])
+
+
+class DeviceScene:
+    """Scene + (optional) guide of a Workload, resident on the current CUDA device."""
+
+    def __init__(self, w: "W.Workload", stream=None):
+        import torch
+        if not torch.cuda.is_available():
+            raise MPGError("no CUDA device: the manifold walk has no CPU path")
+        self.w = w
+        descs = []
+        self._keep = []
+        for s in w.surfaces:
+            d = mpg_surface_desc()
+            d.kind, d.mat = s.kind, s.mat
+            d.eta_in, d.eta_out, d.reflectance, d.radius = s.eta_in, s.eta_out, s.reflectance, s.radius
+            d.center, d.origin, d.edge_u, d.edge_v = _f3(s.center), _f3(s.origin), _f3(s.edge_u), _f3(s.edge_v)
+            if s.kind == W.SURF_MESH:
+                P = np.ascontiguousarray(s.positions, np.float32)
+                N = np.ascontiguousarray(s.normals, np.float32)
+                I = np.ascontiguousarray(s.indices, np.int32)
+                self._keep += [P, N, I]
+                d.positions, d.normals, d.indices = P.ctypes.data, N.ctypes.data, I.ctypes.data
+                d.n_vertices, d.n_triangles = P.shape[0], I.shape[0]
+            descs.append(d)
+        lights = []
+        for l in w.lights:
+            L = mpg_light_desc()
+            L.kind, L.emit = l.kind, l.emit
+            L.position, L.edge_u, L.edge_v = _f3(l.position), _f3(l.edge_u), _f3(l.edge_v)
+            lights.append(L)
+        self.h = mpg_scene_create(descs, lights, stream)
+        self.info = mpg_scene_get_info(self.h)
+        self.extent = float(self.info.extent)
+        sp = w.seed
+        self.sampler = mpg_sampler_desc(sp.mode, sp.surf_id, sp.k, sp.tau)
+        self.guide = None
+        if sp.mode == W.SEED_GUIDE_UV:
+            g = mpg_guide_desc()
+            g.grid_origin = (C.c_float * 2)(*sp.grid_origin)
+            g.grid_extent = (C.c_float * 2)(*sp.grid_extent)
+            g.cells_x, g.cells_y, g.bins_x, g.bins_y = sp.cells_x, sp.cells_y, sp.bins_x, sp.bins_y
+            g.uv_origin = (C.c_float * 2)(*sp.uv_origin)
+            g.uv_scale = (C.c_float * 2)(*sp.uv_scale)
+            g.uv_plane_y = sp.uv_plane_y
+            self.guide_desc = g
+            self.guide = mpg_guide_create(g)
+            if w.energies is not None:
+                self.upload_energies(w.energies, stream)
+            else:
+                mpg_guide_reset(self.guide, stream)
+
+    def upload_energies(self, E, stream=None):
+        import torch
+        e = torch.as_tensor(np.ascontiguousarray(E, np.float32)).cuda()
+        mpg_guide_upload(self.guide, e, stream)
+        torch.cuda.synchronize()
+
+    def opts(self, **over) -> mpg_walk_opts:
+        o = self.w.opts
+        d = dict(max_iters=o.max_iters, tol=o.tol, beta0=o.beta0, trials=o.trials, k_max=o.k_max,
+                 same_chain_eps=0.0, ray_eps=0.0, flags=0, seed=o.seed, walk_id_base=o.walk_id_base)
+        d.update(over)
+        r = mpg_walk_opts()
+        for k, v in d.items():
+            setattr(r, k, v)
+        return r
+
+    def close(self):
+        if getattr(self, "guide", None):
+            mpg_guide_destroy(self.guide)
+            self.guide = None
+        if getattr(self, "h", None):
+            mpg_scene_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Batch:
+    """Device buffers for n_recv receivers x spp walks (query, seeds, outputs)."""
+
+    def __init__(self, xD, nD, spp: int, k: int, device="cuda"):
+        import torch
+        self.n_recv = int(xD.shape[0])
+        self.spp = int(spp)
+        self.n = self.n_recv * self.spp
+        self.k = k
+        f4 = lambda a: torch.cat([torch.as_tensor(np.asarray(a, np.float32)),
+                                  torch.zeros(a.shape[0], 1)], 1).contiguous()
+        self.xD_host = f4(xD).pin_memory() if torch.cuda.is_available() else f4(xD)
+        self.nD_host = f4(nD).pin_memory() if torch.cuda.is_available() else f4(nD)
+        self.xD = self.xD_host.to(device)
+        self.nD = self.nD_host.to(device)
+        n = max(1, self.n)
+        self.xL = torch.empty(n, 4, device=device)
+        self.target = torch.empty(n, 4, device=device)
+        self.bin = torch.empty(n, dtype=torch.int32, device=device)
+        self.chain = torch.empty(k, n, 4, device=device)
+        self.status = torch.empty(n, dtype=torch.uint8, device=device)
+        self.iters = torch.empty(n, dtype=torch.int16, device=device)
+        self.G = torch.empty(n, device=device)
+        self.T = torch.empty(n, device=device)
+        self.w = torch.empty(n, device=device)
+        self.trials = torch.empty(n, dtype=torch.int32, device=device)
+        self.mean = torch.empty(max(1, self.n_recv), device=device)
+        self.var = torch.empty(max(1, self.n_recv), device=device)
+        self.stats = torch.zeros(len(STATS_FIELDS) + 8, dtype=torch.int64, device=device)
+        self.workspace = torch.zeros(256, dtype=torch.uint8, device=device)
+        self.query = mpg_query(self.xD.data_ptr(), self.nD.data_ptr(), self.n_recv, self.spp)
+        self.seeds = mpg_seed_buf(self.xL.data_ptr(), self.target.data_ptr(), self.bin.data_ptr())
+        self.out = mpg_walk_buf(self.chain.data_ptr(), self.status.data_ptr(), self.iters.data_ptr(),
+                                self.G.data_ptr(), self.T.data_ptr(), self.w.data_ptr(), self.trials.data_ptr())
+
+    def stats_dict(self):
+        v = self.stats.cpu().numpy().astype(np.int64)
+        d = {f: int(v[i]) for i, f in enumerate(STATS_FIELDS)}
+        d["by_status"] = [int(x) for x in v[len(STATS_FIELDS):]]
+        return d
+
+    def results(self):
+        """Host copies of the per-walk outputs (numpy)."""
+        chain = self.chain.cpu().numpy()
+        return dict(pos=np.ascontiguousarray(chain[:, :, :3].transpose(1, 0, 2)),
+                    prim=np.ascontiguousarray(chain[:, :, 3].view(np.int32).T),
+                    status=self.status.cpu().numpy(), iters=self.iters.cpu().numpy().astype(np.int32),
+                    G=self.G.cpu().numpy(), T=self.T.cpu().numpy(), w=self.w.cpu().numpy(),
+                    trials=self.trials.cpu().numpy().astype(np.int64), xL=self.xL.cpu().numpy(),
+                    target=self.target.cpu().numpy(), bin=self.bin.cpu().numpy())
+
+
+def run_step(ds: DeviceScene, b: Batch, opts: mpg_walk_opts, stream=None, estimate=True, accumulate=False):
+    """One pass of the hot path: seeds -> walk (+trials) -> estimator [-> guide accumulate]."""
+    mpg_sample_seeds(ds.h, ds.guide, ds.sampler, b.query, opts, b.seeds, stream)
+    mpg_manifold_walk(ds.h, ds.guide, ds.sampler, b.query, b.seeds, opts, b.out, b.stats, b.workspace, stream)
+    if estimate:
+        mpg_estimate(b.w, b.n_recv, b.spp, b.mean, b.var, stream)
+    if accumulate and ds.guide is not None:
+        mpg_guide_accumulate(ds.guide, b.query, b.out, b.n, stream)

@@ -1,0 +1,65 @@
+"""GPU-vs-oracle comparison helpers for the -m gpu parity tests (tests only)."""
+import numpy as np
+
+from oracle import oracle as O
+
+
+def run_gpu(w, **opt_over):
+    import torch
+    from paper_2311_12818_b200 import mpg
+    ds = mpg.DeviceScene(w)
+    b = mpg.Batch(w.xD, w.nD, w.spp, w.seed.k)
+    opts = ds.opts(**opt_over)
+    mpg.run_step(ds, b, opts)
+    torch.cuda.synchronize()
+    res = b.results()
+    res["mean"] = b.mean.cpu().numpy()[:b.n_recv]
+    res["var"] = b.var.cpu().numpy()[:b.n_recv]
+    st = b.stats_dict()
+    ext = ds.extent
+    ds.close()
+    return res, st, ext
+
+
+def run_oracle(w, ids, **opt_over):
+    s = O.OracleScene(w)
+    return s.walks(np.asarray(ids, np.int64), s.opts(**opt_over)), s
+
+
+def compare(g, o, ids, extent, k):
+    """Walk-level parity report for walk indices `ids` (g: full GPU arrays, o: oracle on ids)."""
+    gs = g["status"][ids].astype(np.int64)
+    os_ = o["status"].astype(np.int64)
+    cg = np.isin(gs, (0, 5))
+    co = np.isin(os_, (0, 5))
+    both = cg & co
+    rep = {"n": len(ids), "conv_gpu": int(cg.sum()), "conv_orc": int(co.sum()),
+           "flag_agree": float((cg == co).mean()), "status_agree": float((gs == os_).mean()),
+           "both": int(both.sum())}
+    gp = g["pos"][ids][:, :k]
+    dpos = np.linalg.norm(gp - o["pos"][:, :k], axis=2).max(1)
+    rep["max_dpos_rel"] = float(dpos[both].max() / extent) if both.any() else 0.0
+    gprim = g["prim"][ids][:, :k]
+    same_prim = (gprim == o["prim"][:, :k]).all(1)
+    rep["prim_agree"] = float(same_prim[both].mean()) if both.any() else 1.0
+    vis = (gs == 0) & (os_ == 0)
+    rep["both_visible"] = int(vis.sum())
+    if vis.any():
+        rg = np.abs(g["G"][ids][vis] - o["G"][vis]) / np.maximum(np.abs(o["G"][vis]), 1e-30)
+        rep["G_rel_med"] = float(np.median(rg))
+        rep["G_rel_p99"] = float(np.quantile(rg, 0.99))
+        rep["G_rel_max"] = float(rg.max())
+        tr = (g["trials"][ids][vis] == o["trials"][vis])
+        rep["trials_agree"] = float(tr.mean())
+    rep["disagree_ids"] = np.asarray(ids)[cg != co]
+    rep["prim_mismatch_ids"] = np.asarray(ids)[both & ~same_prim]
+    return rep
+
+
+def tile_means(wv, spp, recv_shape, tile):
+    """Per-tile (tile x tile receivers) mean and SE of w (reading R19)."""
+    ny, nx = recv_shape
+    a = wv.reshape(ny, nx, spp)
+    ty, tx = ny // tile, nx // tile
+    a = a[:ty * tile, :tx * tile].reshape(ty, tile, tx, tile, spp).transpose(0, 2, 1, 3, 4).reshape(ty * tx, -1)
+    return a.mean(1), a.std(1, ddof=1), a.shape[1]

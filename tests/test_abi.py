@@ -1,0 +1,66 @@
+"""CPU checks of the C ABI boundary: the library loads, exports every symbol
+include/mpg.h declares, and rejects bad arguments synchronously (no GPU needed)."""
+import ctypes as C
+import os
+import re
+
+import pytest
+
+from paper_2311_12818_b200 import mpg, build as B
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def L():
+    B.build()
+    return mpg.lib()
+
+
+def declared_symbols():
+    src = open(os.path.join(ROOT, "include", "mpg.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(mpg_[a-z_]+)\s*\(", src)))
+
+
+def test_header_declares_the_boundary():
+    syms = declared_symbols()
+    for s in ["mpg_scene_create", "mpg_guide_upload", "mpg_sample_seeds", "mpg_manifold_walk",
+              "mpg_guide_accumulate"]:
+        assert s in syms
+
+
+def test_library_exports_every_declared_symbol(L):
+    syms = declared_symbols()
+    assert set(syms) == set(mpg.EXPORTS)
+    for s in syms:
+        assert hasattr(L, s), s
+
+
+def test_version(L):
+    assert mpg.mpg_version() == 1
+
+
+def test_invalid_arguments_rejected_synchronously(L):
+    h = C.c_void_p()
+    assert L.mpg_scene_create(None, 0, None, 0, None, C.byref(h)) == 1
+    assert b"surfaces" in L.mpg_last_error()
+    g = mpg.mpg_guide_desc()
+    assert L.mpg_guide_create(C.byref(g), C.byref(h)) == 1
+    assert L.mpg_estimate(None, 1, 1, None, None, None) == 1
+    q = mpg.mpg_query()
+    sd = mpg.mpg_sampler_desc()
+    o = mpg.mpg_walk_opts()
+    s = mpg.mpg_seed_buf()
+    wb = mpg.mpg_walk_buf()
+    assert L.mpg_manifold_walk(None, None, C.byref(sd), C.byref(q), C.byref(s), C.byref(o), C.byref(wb), None,
+                               None, 0, None) == 1
+    assert L.mpg_walk_workspace_size(10, C.byref(o)) >= 8
+
+
+def test_struct_layouts():
+    # layouts mirrored by the binding (natural alignment, see include/mpg.h)
+    assert C.sizeof(mpg.mpg_walk_opts) == 48
+    assert C.sizeof(mpg.mpg_walk_stats) == 19 * 8
+    assert C.sizeof(mpg.mpg_query) == 32
+    assert C.sizeof(mpg.mpg_sampler_desc) == 16
