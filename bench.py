@@ -1,0 +1,315 @@
+#!/usr/bin/env python3
+"""bench.py -- batched manifold walk throughput on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config 1]
+
+A step is one pass of the whole hot path over one batch of synthetic input
+(SURVEY §8(a)): light samples + guided/initial seeds (mpg_sample_seeds) ->
+deduction, Newton with ray-traced reprojection, validation, kappa/G/T and
+reciprocal-probability trials (mpg_manifold_walk) -> per-pixel estimator
+(mpg_estimate) [-> guide accumulation for guided configs].  The workload is
+BASELINE.json configs[1] (1,048,576 k=2 walks through a glass icosphere) unless
+--config says otherwise.  N>1: one process per GPU (torchrun), each rank walks
+its own independent partition (walk_id_base = rank*n); no data-path collective.
+
+Prints ONE JSON line (rank 0).  --impl reference times the oracle (the plain
+CPU implementation in oracle/, single-threaded) on a bounded sample.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "converged manifold walks/s"
+CONFIG_NAMES = {0: "configs[0]: k=1 mirror sphere, 64x64 receivers x 16 cap seeds (65,536 walks)",
+                1: "configs[1]: k=2 TT glass icosphere (5,120 tris), 1024x1024 receivers x 1 seed (1,048,576 walks)",
+                2: "configs[2]: k=1 T water heightfield (522,242 tris), 2048x2048 receivers x 4 guided seeds (16,777,216 walks)",
+                3: "configs[3]: k=6 TTTTTT three bumpy glass slabs (780,300 tris), 1024x1024 receivers, guided seeds (1,048,576 walks)"}
+
+# algorithmic FP32 work per unit: a Newton vertex evaluation
+# (constraint + 3 Jacobian blocks + block-Thomas step) and the ray-casting units
+FLOP_PER_VERTEX_SWEEP = 540.0
+FLOP_PER_NODE = 40.0
+FLOP_PER_TRI = 40.0
+# FP32 peak from unit counts and the max SM clock (B200_PROFILING.md: 148 SMs,
+# 128 FP32 lanes/SM, FMA = 2 flops, clocks.max.sm 1965 MHz)
+def fp32_peak_tflops(sm_mhz=1965.0, sms=148):
+    return sms * 128 * 2 * sm_mhz * 1e6 / 1e12
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, idx=0):
+        self.idx = idx
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.idx),
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        rows = [r for r in self.rows if len(r) >= 7]
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[j] for r in rows for j in range(4) if r[3 + j].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def make_workload(cfg):
+    from paper_2311_12818_b200 import workloads as W
+    return W.CONFIGS[cfg]()
+
+
+def oracle_rate(w, n_walks, seed_base=0):
+    """Time the oracle (oracle/, plain single-threaded C) on the first n_walks."""
+    from oracle import oracle as O
+    s = O.OracleScene(w)
+    ids = np.arange(n_walks, dtype=np.int64)
+    t0 = time.perf_counter()
+    r = s.walks(ids, s.opts(walk_id_base=seed_base))
+    dt = time.perf_counter() - t0
+    conv = int(np.isin(r["status"], (0, 5)).sum())
+    return conv / dt, dt, conv, int(r["total_iters"].sum())
+
+
+def run_reference(args):
+    rank, world, local = dist_env()
+    if rank != 0:
+        return
+    w = make_workload(args.config)
+    n = min(w.n_walks, args.ref_walks)
+    for _ in range(args.warmup):
+        oracle_rate(w, max(64, n // 20))
+    vals, dts = [], []
+    t_all = time.perf_counter()
+    for _ in range(args.steps):
+        v, dt, conv, iters = oracle_rate(w, n)
+        vals.append(v)
+        dts.append(dt)
+    wall = time.perf_counter() - t_all
+    value = float(np.mean(vals))
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "walks/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * wall / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": CONFIG_NAMES[args.config], "sample_walks_per_step": n},
+            "cpu_baseline": {"value": value, "unit": "walks/s", "cores": 1, "kind": "oracle",
+                             "sample": f"first {n} walks of the workload per step (of {w.n_walks})"},
+            "e2e": {"value": value, "unit": "walks/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    from paper_2311_12818_b200 import mpg
+    rank, world, local = dist_env()
+    if world > 1:
+        dist.init_process_group("nccl")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    w = make_workload(args.config)
+    w.opts.walk_id_base = rank * w.n_walks          # independent partitions (weak scaling)
+    ds = mpg.DeviceScene(w)
+    b = mpg.Batch(w.xD, w.nD, w.spp, w.seed.k)
+    opts = ds.opts()
+    stream = torch.cuda.current_stream()
+    guided = ds.guide is not None
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)   # > 126 MB L2
+
+    def step():
+        mpg.run_step(ds, b, opts, accumulate=guided)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+
+    # ---- device-timed region: K steps, L2 flushed before each (outside the events) ----
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+           torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    clocks = ClockSampler(local)
+    stats = []
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    time.sleep(0.3)
+    wall0 = time.perf_counter()
+    for i in range(args.steps):
+        flush.fill_(float(i))
+        e0, e1, e2, e3 = ev[i]
+        e0.record(stream)
+        mpg.mpg_sample_seeds(ds.h, ds.guide, ds.sampler, b.query, opts, b.seeds)
+        e1.record(stream)
+        mpg.mpg_manifold_walk(ds.h, ds.guide, ds.sampler, b.query, b.seeds, opts, b.out, b.stats, b.workspace)
+        e2.record(stream)
+        mpg.mpg_estimate(b.w, b.n_recv, b.spp, b.mean, b.var)
+        if guided:
+            mpg.mpg_guide_accumulate(ds.guide, b.query, b.out, b.n)
+        e3.record(stream)
+        stats.append(b.stats.clone())
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - wall0
+    clk = clocks.stop()
+    step_ms = [ev[i][0].elapsed_time(ev[i][3]) for i in range(args.steps)]
+    walk_ms = [ev[i][1].elapsed_time(ev[i][2]) for i in range(args.steps)]
+    seed_ms = [ev[i][0].elapsed_time(ev[i][1]) for i in range(args.steps)]
+    tot_ms = sum(step_ms)
+    st = torch.stack(stats).cpu().numpy().astype(np.int64)
+    fields = mpg.STATS_FIELDS
+    S = {f: int(st[:, j].sum()) for j, f in enumerate(fields)}
+    conv_total = S["converged"]
+    if world > 1:
+        t = torch.tensor([tot_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot_ms = float(t.item())
+        c = torch.tensor([conv_total, S["newton_iters"]], device=dev, dtype=torch.float64)
+        dist.all_reduce(c, op=dist.ReduceOp.SUM)
+        conv_all, newton_all = float(c[0]), float(c[1])
+    else:
+        conv_all, newton_all = float(conv_total), float(S["newton_iters"])
+    value = conv_all / (tot_ms / 1e3)
+
+    # ---- roofline of the dominant kernel (k_walk): ALU bound ----
+    walk_s = sum(walk_ms) / 1e3
+    flops = (FLOP_PER_VERTEX_SWEEP * S["vertex_iters"] + FLOP_PER_NODE * S["node_visits"] +
+             FLOP_PER_TRI * S["tri_tests"])
+    achieved = flops / walk_s / 1e12
+    peak = fp32_peak_tflops()
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", f"ncu_walk_cfg{args.config}.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    # ---- end to end through the public API: pinned host in -> device -> host result ----
+    e2e = None
+    if not args.no_e2e:
+        xh, nh = b.xD_host, b.nD_host
+        out_h = torch.empty(b.n_recv, dtype=torch.float32, pin_memory=True)
+        for _ in range(2):
+            b.xD.copy_(xh, non_blocking=True); b.nD.copy_(nh, non_blocking=True)
+            step(); out_h.copy_(b.mean[:b.n_recv], non_blocking=True)
+        torch.cuda.synchronize()
+        e_ms = []
+        conv_e = 0
+        for i in range(args.steps):
+            flush.fill_(float(i))
+            s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s0.record(stream)
+            b.xD.copy_(xh, non_blocking=True)
+            b.nD.copy_(nh, non_blocking=True)
+            step()
+            out_h.copy_(b.mean[:b.n_recv], non_blocking=True)
+            s1.record(stream)
+            s1.synchronize()
+            e_ms.append(s0.elapsed_time(s1))
+            conv_e += int(b.stats[1].item())
+        te = sum(e_ms)
+        if world > 1:
+            t = torch.tensor([te], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            te = float(t.item())
+            c = torch.tensor([float(conv_e)], device=dev, dtype=torch.float64)
+            dist.all_reduce(c, op=dist.ReduceOp.SUM)
+            conv_e = float(c.item())
+        e2e = {"value": conv_e / (te / 1e3), "unit": "walks/s",
+               "h2d_bytes_per_step": int(xh.numel() * 4 + nh.numel() * 4),
+               "d2h_bytes_per_step": int(out_h.numel() * 4), "ms_per_step": te / args.steps}
+
+    # ---- CPU baseline: the oracle on a bounded sample (rank 0, N=1 only) ----
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        n = min(w.n_walks, args.ref_walks)
+        v, dt, conv, iters = oracle_rate(w, n)
+        cpu = {"value": v, "unit": "walks/s", "cores": 1, "kind": "oracle",
+               "sample": f"first {n} walks of the workload ({dt:.1f} s, {conv} converged)"}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "walks/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                "config": {"workload": CONFIG_NAMES[args.config], "n_walks_per_gpu": b.n, "k": w.seed.k,
+                           "max_iters": w.opts.max_iters, "trials": "on (k_max 1024)",
+                           "l2": "256 MB buffer written before every timed step (inputs < 126 MB L2)",
+                           "precision": "fp32 traversal/Jacobian/storage; fp64 residual and hit refinement"},
+                "newton_iters_per_s": newton_all / (tot_ms / 1e3),
+                "walks_incl_trials_per_s": S["attempts"] * world / (tot_ms / 1e3),
+                "rays_per_s": S["rays"] * world / (tot_ms / 1e3),
+                "breakdown_ms": {"seeds": sum(seed_ms) / args.steps, "walk": sum(walk_ms) / args.steps,
+                                 "estimate+accumulate": (tot_ms - sum(seed_ms) - sum(walk_ms)) / args.steps},
+                "roofline": {"bound": "alu", "kernel": "k_walk", "achieved": achieved, "peak": peak,
+                             "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
+                             "peak_source": "148 SM x 128 FP32 lanes x 2 x 1965 MHz (B200_PROFILING.md unit counts)",
+                             "algorithmic_flops_per_launch": flops / args.steps},
+                "hbm": {"bytes_per_step": None},
+                "stats_per_step": {k: v / args.steps for k, v in S.items()},
+                "gpu_launches": 3 * args.steps + (args.steps if guided else 0),
+                "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
+                "wall_s_timed_region": wall}
+        print(json.dumps(line), flush=True)
+    ds.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=1)
+    ap.add_argument("--ref-walks", type=int, default=100000)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

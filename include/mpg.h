@@ -214,6 +214,11 @@ mpg_status mpg_manifold_walk(const mpg_scene *scene, const mpg_guide *guide, con
 /* Estimator (Eq. 3): mean[r] = (1/spp) sum_s w[r*spp+s]; var (nullable) = sample variance. */
 mpg_status mpg_estimate(const float *w, int64_t n_recv, int32_t spp, float *mean, float *var, void *stream);
 
+/* Debug: for the next mpg_manifold_walk calls, record (||C||_inf, beta) of every
+ * primary Newton iteration of walks w < n_walks into buf[w*stride + 2*it + {0,1}]
+ * (device float); buf = NULL disables.  Not thread-safe; for tests and tools. */
+mpg_status mpg_debug_trace(float *buf, int64_t n_walks, int32_t stride);
+
 const char *mpg_last_error(void);
 int32_t mpg_version(void);
 

@@ -547,6 +547,7 @@ static int lu_solve(double *A, int m, double *B, int nr) {
 /* ------------------------------------------------------------------------ */
 /* the manifold walk: Newton + sequential ray-traced reprojection [R5-R7]    */
 /* ------------------------------------------------------------------------ */
+static double *g_beta_hist = NULL; /* debug: beta per iteration (orc_walk_trace) */
 static int newton(const orc_scene *sc, const orc_opts *o, int k, uint32_t tau, v3 xD, v3 xL, cvtx *x, int *iters,
                   double eps, double *res_hist) {
     double C[2 * KMAX], J[4 * KMAX * KMAX], D[2 * KMAX];
@@ -559,6 +560,7 @@ static int newton(const orc_scene *sc, const orc_opts *o, int k, uint32_t tau, v
         double nrm = 0.0;
         for (int i = 0; i < m; i++) if (fabs(C[i]) > nrm) nrm = fabs(C[i]);
         if (res_hist) res_hist[it] = nrm;
+        if (g_beta_hist) g_beta_hist[it] = beta;
         if (nrm < o->tol) return ST_CONVERGED;
         if (it == o->max_iters) return ST_MAXITER;
         for (int i = 0; i < m; i++) D[i] = -C[i];
@@ -1099,4 +1101,19 @@ void orc_tangent_basis(const void *h, int32_t prim, int32_t surf, const double p
     onb(geo_normal((const orc_scene *)h, &x), &a, &b);
     sg[0] = a.x; sg[1] = a.y; sg[2] = a.z;
     tg[0] = b.x; tg[1] = b.y; tg[2] = b.z;
+}
+
+/* debug: primary walk from an explicit target with per-iteration ||C||_inf and beta */
+int orc_walk_trace(const void *h, const orc_opts *o, int k, uint32_t tau, const double xD[3], const double xL[3],
+                   const double target[3], double *res_hist, double *beta_hist, int32_t *iters) {
+    const orc_scene *sc = (const orc_scene *)h;
+    cvtx x[KMAX];
+    v3 xd = V(xD[0], xD[1], xD[2]), xl = V(xL[0], xL[1], xL[2]);
+    double eps = eps_ray(sc, o);
+    *iters = 0;
+    if (!deduce(sc, k, tau, xd, V(target[0], target[1], target[2]), eps, x)) return ST_SEED_FAIL;
+    g_beta_hist = beta_hist;
+    int st = newton(sc, o, k, tau, xd, xl, x, iters, eps, res_hist);
+    g_beta_hist = NULL;
+    return st;
 }

@@ -104,6 +104,9 @@ def lib():
         _lib.orc_philox.argtypes = [P, P, P]
         _lib.orc_philox_batch.argtypes = [P, C.c_int64, P, P]
         _lib.orc_guide_tables.argtypes = [P, C.c_int, C.c_int, P]
+        _lib.orc_walk_trace.restype = C.c_int
+        _lib.orc_walk_trace.argtypes = [P, C.POINTER(Opts), C.c_int, C.c_uint32, dp, dp, dp, dp, dp,
+                                        C.POINTER(C.c_int32)]
         _lib.orc_tangent_basis.argtypes = [P, C.c_int32, C.c_int32, dp, dp, dp]
         _lib.orc_scatter.restype = C.c_int
         _lib.orc_scatter.argtypes = [C.c_int, C.c_double, C.c_double, dp, dp, dp]
@@ -285,6 +288,16 @@ class OracleScene:
         surf = np.ascontiguousarray(surf, np.int32)
         return lib().orc_ggt(self.h, C.byref(opts), method, delta, k, tau, light_id, _d3(xD), _d3(nD), _d3(xL),
                              pos.ctypes.data_as(C.POINTER(C.c_double)), _ptr(prim), _ptr(surf))
+
+    def walk_trace(self, xD, xL, target, opts=None):
+        opts = opts or self.opts()
+        res = np.zeros(opts.max_iters + 2)
+        beta = np.zeros(opts.max_iters + 2)
+        it = C.c_int32()
+        st = lib().orc_walk_trace(self.h, C.byref(opts), self.w.seed.k, self.w.seed.tau, _d3(xD), _d3(xL),
+                                  _d3(target), res.ctypes.data_as(C.POINTER(C.c_double)),
+                                  beta.ctypes.data_as(C.POINTER(C.c_double)), C.byref(it))
+        return st, it.value, res[:it.value + 1], beta[:it.value + 1]
 
     def tangent_basis(self, prim, surf, p):
         a = (C.c_double * 3)()

@@ -161,17 +161,27 @@ __device__ __forceinline__ bool tri_hit(const RayW &r, float3 v0, float3 v1, flo
     return true;
 }
 
-__device__ __forceinline__ bool sphere_hit(float3 o, float3 d, float3 c, float R, float tmin, float tmax, float &t) {
-    float3 oc = o - c;
-    float b = dot(oc, d);
-    float3 q = oc - b * d;
-    float disc = R * R - dot(q, q);
-    if (disc < 0.0f) return false;
-    float sq = sqrtf(disc);
-    float t0 = -b - sq, t1 = -b + sq;
-    if (t0 > tmin && t0 < tmax) { t = t0; return true; }
-    if (t1 > tmin && t1 < tmax) { t = t1; return true; }
-    return false;
+// Ray/sphere in fp64 (a few DP flops per analytic surface): the reprojected
+// vertex must be accurate to ~1 ulp of its fp32 coordinates, because near
+// grazing reflection the residual's sensitivity to position is ~1/(2cos theta)
+// larger than nominal and o + t*d in fp32 stalls Newton at ||C|| ~ 2e-5 (measured).
+__device__ __forceinline__ bool sphere_hit(float3 o, float3 d, float3 c, float R, float tmin, float tmax, float &t,
+                                           float3 &p) {
+    double ox = (double)o.x - c.x, oy = (double)o.y - c.y, oz = (double)o.z - c.z;
+    double dx = d.x, dy = d.y, dz = d.z;
+    double dd = dx * dx + dy * dy + dz * dz;
+    double b = (ox * dx + oy * dy + oz * dz) / dd;
+    double qx = ox - b * dx, qy = oy - b * dy, qz = oz - b * dz;
+    double disc = ((double)R * R - (qx * qx + qy * qy + qz * qz)) / dd;
+    if (disc < 0.0) return false;
+    double sq = sqrt(disc);
+    double t0 = -b - sq, t1 = -b + sq, tt;
+    if (t0 > tmin && t0 < tmax) tt = t0;
+    else if (t1 > tmin && t1 < tmax) tt = t1;
+    else return false;
+    t = (float)tt;
+    p = make_float3((float)((double)o.x + tt * dx), (float)((double)o.y + tt * dy), (float)((double)o.z + tt * dz));
+    return true;
 }
 
 __device__ __forceinline__ bool quad_hit(float3 o, float3 d, float3 q0, float3 e1, float3 e2, float tmin, float tmax,
@@ -202,58 +212,71 @@ __device__ bool trace(const DScene &S, float3 o, float3 d, float tmin, float tma
     float best = tmax;
     int bprim = -2, bsurf = -1;
     float bb0 = 0.f, bb1 = 0.f, bb2 = 0.f;
+    float3 bp = f3(0.f, 0.f, 0.f);
     for (int i = 0; i < S.n_surf; i++) {
         const DSurf &f = S.surf[i];
         if (f.kind == 2 || (spec_only && f.mat == 2)) continue;
         float t;
-        bool hit = f.kind == 0 ? sphere_hit(o, d, f.center, f.radius, tmin, best, t)
-                               : quad_hit(o, d, f.origin, f.eu, f.ev, tmin, best, t);
+        float3 p;
+        bool hit;
+        if (f.kind == 0) hit = sphere_hit(o, d, f.center, f.radius, tmin, best, t, p);
+        else {
+            hit = quad_hit(o, d, f.origin, f.eu, f.ev, tmin, best, t);
+            p = o + d * t;
+        }
         if (hit) {
-            best = t; bprim = -1; bsurf = i;
+            best = t; bprim = -1; bsurf = i; bp = p;
             if (ANY) { h.t = t; h.prim = -1; h.surf = i; return true; }
         }
     }
     if (S.n_tri > 0) {
+        // while-while traversal with postponed leaves (Aila & Laine 2009): lanes
+        // keep visiting inner nodes together until every active lane has a leaf
+        // waiting, then intersect leaves together -- node visits and triangle
+        // tests execute with most lanes of the warp active.
+        const int SENT = 0x7fffffff, NONE = 0;
         RayW r;
         ray_setup(r, o, d);
-        int stack[48];
-        int sp = 0;
-        int node = 0;
-        while (true) {
-            if (node >= 0) {
+        int stack[64];
+        stack[0] = SENT;
+        int sp = 1;
+        int node = 0, leaf = NONE;
+        while (node != SENT || leaf != NONE) {
+            while (node >= 0 && node != SENT) {
                 st.nodes++;
                 const float4 *nd = S.nodes + 4 * node;
                 float4 a = __ldg(nd), b = __ldg(nd + 1), c = __ldg(nd + 2);
                 int4 ch = __ldg(reinterpret_cast<const int4 *>(nd + 3));
-                float3 lo0 = f3(a.x, a.y, a.z), hi0 = f3(a.w, b.x, b.y);
-                float3 lo1 = f3(b.z, b.w, c.x), hi1 = f3(c.y, c.z, c.w);
-                float3 t0a = (lo0 - o), t0b = (hi0 - o);
-                float tx0 = t0a.x * r.idir.x, tx1 = t0b.x * r.idir.x;
-                float ty0 = t0a.y * r.idir.y, ty1 = t0b.y * r.idir.y;
-                float tz0 = t0a.z * r.idir.z, tz1 = t0b.z * r.idir.z;
+                float tx0 = (a.x - o.x) * r.idir.x, tx1 = (a.w - o.x) * r.idir.x;
+                float ty0 = (a.y - o.y) * r.idir.y, ty1 = (b.x - o.y) * r.idir.y;
+                float tz0 = (a.z - o.z) * r.idir.z, tz1 = (b.y - o.z) * r.idir.z;
                 float n0 = fmaxf(fmaxf(fminf(tx0, tx1), fminf(ty0, ty1)), fmaxf(fminf(tz0, tz1), tmin));
                 float f0 = fminf(fminf(fmaxf(tx0, tx1), fmaxf(ty0, ty1)), fminf(fmaxf(tz0, tz1), best));
-                float3 t1a = (lo1 - o), t1b = (hi1 - o);
-                float sx0 = t1a.x * r.idir.x, sx1 = t1b.x * r.idir.x;
-                float sy0 = t1a.y * r.idir.y, sy1 = t1b.y * r.idir.y;
-                float sz0 = t1a.z * r.idir.z, sz1 = t1b.z * r.idir.z;
+                float sx0 = (b.z - o.x) * r.idir.x, sx1 = (c.y - o.x) * r.idir.x;
+                float sy0 = (b.w - o.y) * r.idir.y, sy1 = (c.z - o.y) * r.idir.y;
+                float sz0 = (c.x - o.z) * r.idir.z, sz1 = (c.w - o.z) * r.idir.z;
                 float n1 = fmaxf(fmaxf(fminf(sx0, sx1), fminf(sy0, sy1)), fmaxf(fminf(sz0, sz1), tmin));
                 float f1 = fminf(fminf(fmaxf(sx0, sx1), fmaxf(sy0, sy1)), fminf(fmaxf(sz0, sz1), best));
                 bool h0 = n0 <= f0, h1 = n1 <= f1;
                 if (h0 && h1) {
-                    int nearc = n0 <= n1 ? ch.x : ch.y, farc = n0 <= n1 ? ch.y : ch.x;
-                    stack[sp++] = farc;
-                    node = nearc;
-                    continue;
+                    bool swp = n1 < n0;
+                    node = swp ? ch.y : ch.x;
+                    stack[sp++] = swp ? ch.x : ch.y;
                 } else if (h0) {
                     node = ch.x;
-                    continue;
                 } else if (h1) {
                     node = ch.y;
-                    continue;
+                } else {
+                    node = stack[--sp];
                 }
-            } else {
-                int v = ~node;
+                if (node < 0 && leaf == NONE) { // postpone the leaf, keep traversing
+                    leaf = node;
+                    node = stack[--sp];
+                }
+                if (!__any_sync(__activemask(), leaf == NONE)) break;
+            }
+            while (leaf != NONE) {
+                int v = ~leaf;
                 int start = v >> 3, cnt = (v & 7) + 1;
                 for (int j = start; j < start + cnt; j++) {
                     st.tris++;
@@ -266,9 +289,12 @@ __device__ bool trace(const DScene &S, float3 o, float3 d, float tmin, float tma
                         if (ANY) { h.t = t; h.prim = j; h.surf = bsurf; return true; }
                     }
                 }
+                leaf = NONE;
+                if (node < 0) { // the traversal stopped on another leaf
+                    leaf = node;
+                    node = stack[--sp];
+                }
             }
-            if (sp == 0) break;
-            node = stack[--sp];
         }
     }
     if (ANY) return false;
@@ -280,7 +306,7 @@ __device__ bool trace(const DScene &S, float3 o, float3 d, float tmin, float tma
                v2 = xyz(__ldg(S.tpos + 3 * bprim + 2));
         h.p = v0 * bb0 + v1 * bb1 + v2 * bb2;
     } else {
-        h.p = o + d * best;
+        h.p = bp;
     }
     return true;
 }

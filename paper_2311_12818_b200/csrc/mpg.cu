@@ -646,13 +646,14 @@ static int num_sms() {
 
 extern "C" mpg_status mpg_sample_seeds(const mpg_scene *scene, const mpg_guide *guide, const mpg_sampler_desc *sd,
                                        const mpg_query *q, const mpg_walk_opts *o, mpg_seed_buf *sb, void *stream) {
-    ARG_CHECK(scene && sd && q && o && sb && q->xD && sb->xL && sb->target && sb->bin, "NULL argument");
+    ARG_CHECK(scene && sd && q && o && sb, "NULL argument");
     ARG_CHECK(q->n_recv >= 0 && q->spp >= 1, "bad query sizes");
     SeedCtx g;
     mpg_status st = make_seed_ctx(scene, guide, sd, o, g);
     if (st != MPG_OK) return st;
     int64_t n = q->n_recv * q->spp;
     if (n == 0) return MPG_OK;
+    ARG_CHECK(q->xD && sb->xL && sb->target && sb->bin, "NULL query/seed array");
     int blocks = (int)std::min<int64_t>((n + 255) / 256, (int64_t)num_sms() * 8);
     k_seeds<<<blocks, 256, 0, as_stream(stream)>>>(scene->d, g, (const float4 *)q->xD, n, q->spp, o->walk_id_base,
                                                    (float4 *)sb->xL, (float4 *)sb->target, sb->bin);
@@ -663,13 +664,28 @@ extern "C" mpg_status mpg_sample_seeds(const mpg_scene *scene, const mpg_guide *
 // ----------------------------------------------------------------------------
 // walk
 // ----------------------------------------------------------------------------
+static float *g_dbg = nullptr;
+static int64_t g_dbg_n = 0;
+static int g_dbg_stride = 0;
+extern "C" mpg_status mpg_debug_trace(float *buf, int64_t n_walks, int32_t stride) {
+    g_dbg = buf;
+    g_dbg_n = buf ? n_walks : 0;
+    g_dbg_stride = stride;
+    return MPG_OK;
+}
+
+// trial rounds: walks unresolved after LOCAL_TRIALS sequential trials are run
+// in rounds of B = 4, 8, 16, ... parallel trials
+#define LOCAL_TRIALS 4u
+static uint32_t hard_cap(int64_t n) { return (uint32_t)std::min<int64_t>(std::max<int64_t>(n, 1), 1 << 21); }
 extern "C" size_t mpg_walk_workspace_size(int64_t n, const mpg_walk_opts *opts) {
-    (void)n; (void)opts;
-    return 256;
+    (void)opts;
+    size_t cap = hard_cap(n);
+    return 256 + 2 * cap * (sizeof(int64_t) + 2 * sizeof(uint32_t));
 }
 
 template <int KMAX>
-static mpg_status launch_walk(const DScene &S, const SeedCtx &g, const WalkParams &P, cudaStream_t st) {
+static mpg_status launch_walk(const DScene &S, const SeedCtx &g, WalkParams P, cudaStream_t st, void *ws) {
     static int occ = 0;
     if (!occ) {
         CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_walk<KMAX>, 128, 0));
@@ -679,6 +695,36 @@ static mpg_status launch_walk(const DScene &S, const SeedCtx &g, const WalkParam
     int blocks = (int)std::min<int64_t>(want, (int64_t)num_sms() * occ);
     k_walk<KMAX><<<blocks, 128, 0, st>>>(S, g, P);
     CUDA_TRY(cudaPeekAtLastError());
+    if (!P.trials_on || P.k_max <= P.local_trials) return MPG_OK;
+    // parallel trial rounds over the hard list (ping-pong buffers A/B)
+    char *base = (char *)ws;
+    unsigned int *cnt = (unsigned int *)(base + 16); // cnt[0] list A, cnt[1] list B
+    uint32_t cap = P.hard_cap;
+    int64_t *wl[2] = {(int64_t *)(base + 256), (int64_t *)(base + 256 + (size_t)cap * 8)};
+    uint32_t *pl[2] = {(uint32_t *)(base + 256 + (size_t)cap * 16), (uint32_t *)(base + 256 + (size_t)cap * 20)};
+    uint32_t *bl[2] = {(uint32_t *)(base + 256 + (size_t)cap * 24), (uint32_t *)(base + 256 + (size_t)cap * 28)};
+    uint32_t t0 = P.local_trials + 1, B = 4;
+    int cur = 0, rblocks = num_sms() * occ;
+    while (t0 <= P.k_max) {
+        uint32_t Bc = std::min(B, P.k_max - t0 + 1);
+        WalkParams R = P;
+        R.round_mode = 1;
+        R.round_t0 = t0;
+        R.round_B = Bc;
+        R.hard_walk = wl[cur]; R.hard_psurf = pl[cur]; R.hard_best = bl[cur]; R.hard_count = cnt + cur;
+        R.queue = (unsigned long long *)(base + 8);
+        CUDA_TRY(cudaMemsetAsync(base + 8, 0, 8, st));
+        k_walk<KMAX><<<rblocks, 128, 0, st>>>(S, g, R);
+        CUDA_TRY(cudaPeekAtLastError());
+        CUDA_TRY(cudaMemsetAsync(cnt + (cur ^ 1), 0, 4, st));
+        k_hard_compact<<<num_sms() * 2, 256, 0, st>>>(wl[cur], pl[cur], bl[cur], cnt + cur, cap, wl[cur ^ 1],
+                                                      pl[cur ^ 1], bl[cur ^ 1], cnt + (cur ^ 1), t0 + Bc - 1,
+                                                      P.k_max, P.T, P.seed_xL, P.trials, P.w, P.stats);
+        CUDA_TRY(cudaPeekAtLastError());
+        cur ^= 1;
+        t0 += Bc;
+        B *= 2;
+    }
     return MPG_OK;
 }
 
@@ -687,9 +733,12 @@ extern "C" mpg_status mpg_manifold_walk(const mpg_scene *scene, const mpg_guide 
                                         mpg_walk_buf *out, mpg_walk_stats *stats, void *workspace,
                                         size_t workspace_bytes, void *stream) {
     ARG_CHECK(scene && sd && q && sb && o && out, "NULL argument");
-    ARG_CHECK(q->xD && q->nD && sb->xL && sb->target && sb->bin, "NULL query/seed array");
-    ARG_CHECK(out->chain && out->status && out->iters && out->G && out->T && out->w && out->trials, "NULL output array");
     ARG_CHECK(q->n_recv >= 0 && q->spp >= 1, "bad query sizes");
+    if (q->n_recv > 0) {
+        ARG_CHECK(q->xD && q->nD && sb->xL && sb->target && sb->bin, "NULL query/seed array");
+        ARG_CHECK(out->chain && out->status && out->iters && out->G && out->T && out->w && out->trials,
+                  "NULL output array");
+    }
     ARG_CHECK(workspace && workspace_bytes >= mpg_walk_workspace_size(q->n_recv * q->spp, o), "workspace too small");
     ARG_CHECK(o->max_iters >= 0 && o->max_iters < 65536 && o->tol > 0.f && o->beta0 > 0.f, "bad walk options");
     ARG_CHECK(!o->trials || o->k_max >= 1, "k_max must be >= 1");
@@ -724,13 +773,25 @@ extern "C" mpg_status mpg_manifold_walk(const mpg_scene *scene, const mpg_guide 
     P.same_eps = o->same_chain_eps > 0.f ? o->same_chain_eps : 1e-4f * scene->d.extent;
     P.ray_eps = o->ray_eps > 0.f ? o->ray_eps : 1e-4f * scene->d.extent;
     P.walk_id_base = o->walk_id_base;
+    P.dbg = g_dbg;
+    P.n_dbg = g_dbg_n;
+    P.dbg_stride = g_dbg_stride;
+    P.local_trials = LOCAL_TRIALS;
+    P.hard_cap = hard_cap(P.n);
+    {
+        char *base = (char *)workspace;
+        P.hard_walk = (int64_t *)(base + 256);
+        P.hard_psurf = (uint32_t *)(base + 256 + (size_t)P.hard_cap * 16);
+        P.hard_best = (uint32_t *)(base + 256 + (size_t)P.hard_cap * 24);
+        P.hard_count = (unsigned int *)(base + 16);
+    }
     CUDA_TRY(cudaMemsetAsync(workspace, 0, 64, s));
     int k = g.k;
-    if (k <= 1) return launch_walk<1>(scene->d, g, P, s);
-    if (k <= 2) return launch_walk<2>(scene->d, g, P, s);
-    if (k <= 4) return launch_walk<4>(scene->d, g, P, s);
-    if (k <= 6) return launch_walk<6>(scene->d, g, P, s);
-    return launch_walk<8>(scene->d, g, P, s);
+    if (k <= 1) return launch_walk<1>(scene->d, g, P, s, workspace);
+    if (k <= 2) return launch_walk<2>(scene->d, g, P, s, workspace);
+    if (k <= 4) return launch_walk<4>(scene->d, g, P, s, workspace);
+    if (k <= 6) return launch_walk<6>(scene->d, g, P, s, workspace);
+    return launch_walk<8>(scene->d, g, P, s, workspace);
 }
 
 // ----------------------------------------------------------------------------

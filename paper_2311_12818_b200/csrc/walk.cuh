@@ -21,6 +21,7 @@
 #include "seed.cuh"
 
 enum { PH_FETCH = 0, PH_SEED = 1, PH_DEDUCE = 2, PH_SOLVE = 3, PH_REPROJ = 4, PH_END = 5, PH_IDLE = 6 };
+#define HARD_NONE 0xffffffffu
 enum { ST_CONVERGED = 0, ST_MAXITER = 1, ST_SEED_FAIL = 2, ST_BAD_SIDE = 3, ST_DEGENERATE = 4, ST_OCCLUDED = 5 };
 
 struct WalkParams {
@@ -40,6 +41,19 @@ struct WalkParams {
     uint32_t k_max;
     float tol, beta0, same_eps, ray_eps;
     uint64_t walk_id_base;
+    float *dbg;      // debug: [n_dbg][stride] (||C||_inf, beta) per primary iteration, or NULL
+    int64_t n_dbg;
+    int dbg_stride;
+    // reciprocal-probability trials beyond the first `local_trials` run in
+    // parallel rounds over a list of unresolved ("hard") walks (see k_walk).
+    uint32_t local_trials;
+    uint32_t hard_cap;
+    int64_t *hard_walk; // list written by the main pass / read by a round
+    uint32_t *hard_psurf;
+    uint32_t *hard_best; // min successful trial index (0xffffffff: none yet)
+    unsigned int *hard_count;
+    int round_mode;     // 0: main pass; 1: trial round over the hard list
+    uint32_t round_t0, round_B; // round covers trials [t0, t0+B)
 };
 
 // stats slots (mirror mpg_walk_stats field order)
@@ -69,11 +83,54 @@ __device__ __forceinline__ bool scatter_dir(const DScene &S, float3 &d, int prim
     return true;
 }
 
+// Hit point of the line o + t*(q - o) with the primitive the fp32 traversal
+// found, recomputed in fp64 from the fp32 inputs (exact differences) and
+// rounded once: the reprojected vertex is within 1/2 ulp of the exact point,
+// so the Newton residual is not floored by reprojection noise (which near
+// grazing chains reached ~1e-5 in fp32, measured).
+__device__ __forceinline__ float3 refine_hit(const DScene &S, int prim, int surf, float3 o, float3 q, float3 pf) {
+    double ox = o.x, oy = o.y, oz = o.z;
+    double dx = (double)q.x - ox, dy = (double)q.y - oy, dz = (double)q.z - oz;
+    double t;
+    if (prim >= 0) {
+        float3 a = xyz(__ldg(S.tpos + 3 * prim)), b = xyz(__ldg(S.tpos + 3 * prim + 1)), c = xyz(__ldg(S.tpos + 3 * prim + 2));
+        double e1x = (double)b.x - a.x, e1y = (double)b.y - a.y, e1z = (double)b.z - a.z;
+        double e2x = (double)c.x - a.x, e2y = (double)c.y - a.y, e2z = (double)c.z - a.z;
+        double nx = e1y * e2z - e1z * e2y, ny = e1z * e2x - e1x * e2z, nz = e1x * e2y - e1y * e2x;
+        double den = dx * nx + dy * ny + dz * nz;
+        if (den == 0.0) return pf;
+        t = (((double)a.x - ox) * nx + ((double)a.y - oy) * ny + ((double)a.z - oz) * nz) / den;
+    } else {
+        const DSurf &f = S.surf[surf];
+        if (f.kind == 0) {
+            double cx = ox - f.center.x, cy = oy - f.center.y, cz = oz - f.center.z;
+            double dd = dx * dx + dy * dy + dz * dz;
+            double bb = (cx * dx + cy * dy + cz * dz) / dd;
+            double rx = cx - bb * dx, ry = cy - bb * dy, rz = cz - bb * dz;
+            double disc = ((double)f.radius * f.radius - (rx * rx + ry * ry + rz * rz)) / dd;
+            if (disc < 0.0) return pf;
+            double sq = sqrt(disc);
+            // the root nearest to the fp32 hit the traversal selected
+            double tf = ((double)pf.x - ox) * dx + ((double)pf.y - oy) * dy + ((double)pf.z - oz) * dz;
+            tf /= dd;
+            double t0 = -bb - sq, t1 = -bb + sq;
+            t = fabs(t0 - tf) <= fabs(t1 - tf) ? t0 : t1;
+        } else {
+            double nx = f.nq.x, ny = f.nq.y, nz = f.nq.z;
+            double den = dx * nx + dy * ny + dz * nz;
+            if (den == 0.0) return pf;
+            t = (((double)f.origin.x - ox) * nx + ((double)f.origin.y - oy) * ny + ((double)f.origin.z - oz) * nz) / den;
+        }
+    }
+    return make_float3((float)(ox + t * dx), (float)(oy + t * dy), (float)(oz + t * dz));
+}
+
 // Trace the k chain vertices from x_D: deduction (scatter by tau) or
 // reprojection toward q_i (must stay on surf_i).  Rolled loop: one traversal
 // site.  y/yp/ys/q live in local memory (dynamic index).
+// returns 0 on success, else 1 + (i << 4) | reason (1 miss, 2 wrong surface, 3 zero length, 4 scatter)
 template <int KMAX>
-__device__ __forceinline__ bool trace_chain(const DScene &S, bool deduce, int k, uint32_t tau, float3 xD, float3 tgt,
+__device__ __forceinline__ int trace_chain(const DScene &S, bool deduce, int k, uint32_t tau, float3 xD, float3 tgt,
                                             const float3 *q, uint32_t surf_req, float eps, float3 *y, int *yp,
                                             int *ys, LaneStats &st) {
     float3 o = xD;
@@ -81,7 +138,7 @@ __device__ __forceinline__ bool trace_chain(const DScene &S, bool deduce, int k,
     if (deduce) {
         float3 v = tgt - xD;
         float l2 = dot(v, v);
-        if (!(l2 > 0.0f)) return false;
+        if (!(l2 > 0.0f)) return 3;
         d = v * rsqrtf(l2);
     }
 #pragma unroll 1
@@ -89,36 +146,47 @@ __device__ __forceinline__ bool trace_chain(const DScene &S, bool deduce, int k,
         if (!deduce) {
             float3 v = q[i] - o;
             float l2 = dot(v, v);
-            if (!(l2 > 0.0f)) return false;
+            if (!(l2 > 0.0f)) return 3 | (i << 4);
             d = v * rsqrtf(l2);
         } else if (i > 0) {
-            if (!scatter_dir(S, d, yp[i - 1], ys[i - 1], y[i - 1], (tau >> (i - 1)) & 1u)) return false;
+            if (!scatter_dir(S, d, yp[i - 1], ys[i - 1], y[i - 1], (tau >> (i - 1)) & 1u)) return 4 | (i << 4);
         }
         Hit h;
-        if (!trace<false>(S, o, d, eps, 3.0e38f, true, h, st)) return false;
-        if (!deduce && h.surf != (int)((surf_req >> (4 * i)) & 15u)) return false;
-        y[i] = h.p;
+        if (!trace<false>(S, o, d, eps, 3.0e38f, true, h, st)) return 1 | (i << 4);
+        if (!deduce && h.surf != (int)((surf_req >> (4 * i)) & 15u)) return 2 | (i << 4);
+        y[i] = refine_hit(S, h.prim, h.surf, o, deduce ? o + d : q[i], h.p);
         yp[i] = h.prim;
         ys[i] = h.surf;
         o = h.p;
     }
-    return true;
+    return 0;
 }
 
-// per-vertex constraint pieces
+// per-vertex constraint pieces.  The residual C = (s.h, t.h) is evaluated in
+// fp64 from the fp32 vertex positions (their differences are exact in fp64):
+// near grazing reflection |h~| = 2cos(theta) -> 0 amplifies fp32 rounding of
+// w_i + w_o by 1/|h~| up to the 1e-5 tolerance (measured: GPU MAXITER where
+// the fp64 oracle converged).  The Jacobian blocks stay fp32: their error only
+// slows the (quasi-)Newton contraction, it does not move the converged point.
 struct VTerm {
     float3 wi, wo, h, s, t;
     float li, lo, ei, eo, hl, hn;
+    double c0, c1;
 };
 
 __device__ __forceinline__ bool vterm(float3 a, float3 p, float3 b, float3 ng, float3 n, const DSurf &f, bool isT,
                                       VTerm &v) {
-    float3 da = a - p, db = b - p;
-    v.li = len(da);
-    v.lo = len(db);
-    if (!(v.li > 0.0f) || !(v.lo > 0.0f)) return false;
-    v.wi = da * (1.0f / v.li);
-    v.wo = db * (1.0f / v.lo);
+    double ax = (double)a.x - (double)p.x, ay = (double)a.y - (double)p.y, az = (double)a.z - (double)p.z;
+    double bx = (double)b.x - (double)p.x, by = (double)b.y - (double)p.y, bz = (double)b.z - (double)p.z;
+    double la2 = ax * ax + ay * ay + az * az, lb2 = bx * bx + by * by + bz * bz;
+    if (!(la2 > 0.0) || !(lb2 > 0.0)) return false;
+    double ia = rsqrt(la2), ib = rsqrt(lb2);
+    ax *= ia; ay *= ia; az *= ia;
+    bx *= ib; by *= ib; bz *= ib;
+    v.li = (float)(la2 * ia);
+    v.lo = (float)(lb2 * ib);
+    v.wi = f3((float)ax, (float)ay, (float)az);
+    v.wo = f3((float)bx, (float)by, (float)bz);
     if (isT) {
         bool out = dot(v.wi, ng) > 0.0f;
         v.ei = out ? f.eta_out : f.eta_in;
@@ -126,11 +194,17 @@ __device__ __forceinline__ bool vterm(float3 a, float3 p, float3 b, float3 ng, f
     } else {
         v.ei = v.eo = 1.0f;
     }
-    float3 ht = v.wi * v.ei + v.wo * v.eo;
-    v.hl = len(ht);
-    if (!(v.hl > 0.0f) || !isfinite(v.hl)) return false;
-    v.h = ht * (1.0f / v.hl);
+    double hx = (double)v.ei * ax + (double)v.eo * bx, hy = (double)v.ei * ay + (double)v.eo * by,
+           hz = (double)v.ei * az + (double)v.eo * bz;
+    double hl2 = hx * hx + hy * hy + hz * hz;
+    if (!(hl2 > 0.0) || !isfinite(hl2)) return false;
+    double ih = rsqrt(hl2);
+    hx *= ih; hy *= ih; hz *= ih;
+    v.hl = (float)(hl2 * ih);
+    v.h = f3((float)hx, (float)hy, (float)hz);
     onb(n, v.s, v.t);
+    v.c0 = (double)v.s.x * hx + (double)v.s.y * hy + (double)v.s.z * hz;
+    v.c1 = (double)v.t.x * hx + (double)v.t.y * hy + (double)v.t.z * hz;
     v.hn = dot(v.h, n);
     return true;
 }
@@ -157,11 +231,11 @@ __device__ __forceinline__ int newton_system(const DScene &S, int k, uint32_t ta
                                              const float3 (&x)[KMAX], const int (&prim)[KMAX],
                                              const int (&surf)[KMAX], float tol, float (&Di)[KMAX][4],
                                              float (&Ub)[KMAX][4], float3 (&sg)[KMAX], float3 (&tg)[KMAX],
-                                             float3 (&dq)[KMAX], bool &singular) {
+                                             float3 (&dq)[KMAX], bool &singular, float &cmax_out) {
     float rp[KMAX][2];
     bool degen = false;
     singular = false;
-    float cmax = 0.0f;
+    double cmax = 0.0;
 #pragma unroll
     for (int i = 0; i < KMAX; i++) {
         if (i >= k) break;
@@ -178,8 +252,8 @@ __device__ __forceinline__ int newton_system(const DScene &S, int k, uint32_t ta
         float3 n = shading(S, prim[i], surf[i], x[i], sg[i], tg[i], dna, dnb);
         VTerm v;
         if (!vterm(a, x[i], b, cross(sg[i], tg[i]), n, f, (tau >> i) & 1u, v)) { degen = true; break; }
-        float c0 = dot(v.s, v.h), c1 = dot(v.t, v.h);
-        cmax = fmaxf(cmax, fmaxf(fabsf(c0), fabsf(c1)));
+        float c0 = (float)v.c0, c1 = (float)v.c1;
+        cmax = fmax(cmax, fmax(fabs(v.c0), fabs(v.c1)));
         float2 d0 = dC_self(v, sg[i], dna), d1 = dC_self(v, tg[i], dnb);
         float D00 = d0.x, D10 = d0.y, D01 = d1.x, D11 = d1.y;
         float r0 = -c0, r1 = -c1;
@@ -207,8 +281,9 @@ __device__ __forceinline__ int newton_system(const DScene &S, int k, uint32_t ta
         Di[i][0] = D11 * id; Di[i][1] = -D01 * id; Di[i][2] = -D10 * id; Di[i][3] = D00 * id;
         rp[i][0] = r0; rp[i][1] = r1;
     }
+    cmax_out = (float)cmax;
     if (degen || !isfinite(cmax)) return 2;
-    if (cmax < tol) return 1;
+    if (cmax < (double)tol) return 1;
     if (singular) return 2;
     float n0 = 0.f, n1 = 0.f; // Delta_{i+1}
 #pragma unroll
@@ -341,6 +416,10 @@ __global__ void __launch_bounds__(128) k_walk(const DScene S, const SeedCtx g, c
     LaneStats ls = {0u, 0u, 0u};
     uint32_t c_newton = 0, c_vtx = 0, c_attempts = 0;
 
+    // round mode: work items are (hard entry e, trial t0 + j), j < B
+    const int64_t n_items = P.round_mode ? (int64_t)min(*(volatile unsigned int *)P.hard_count, P.hard_cap) * P.round_B
+                                         : P.n;
+    uint32_t cur_e = 0;
     while (true) {
         // ---- fetch (warp-aggregated) -------------------------------------
         unsigned need = __ballot_sync(MPG_FULL, phase == PH_FETCH);
@@ -349,7 +428,29 @@ __global__ void __launch_bounds__(128) k_walk(const DScene S, const SeedCtx g, c
             unsigned long long base = 0;
             if (lane == leader) base = atomicAdd(P.queue, (unsigned long long)__popc(need));
             base = __shfl_sync(MPG_FULL, base, leader);
-            if (phase == PH_FETCH) {
+            if (phase == PH_FETCH && P.round_mode) {
+                int64_t idx = (int64_t)base + __popc(need & ((1u << lane) - 1u));
+                if (idx < n_items) {
+                    cur_e = (uint32_t)(idx / P.round_B);
+                    trial = P.round_t0 + (uint32_t)(idx % P.round_B);
+                    // skip trials beyond an already-found success of this walk
+                    if (*(volatile uint32_t *)(P.hard_best + cur_e) > trial) {
+                        w = P.hard_walk[cur_e];
+                        psurf = P.hard_psurf[cur_e];
+                        int64_t rcv = w / P.spp;
+                        xD = xyz(__ldg(P.xD + rcv));
+                        nD = xyz(__ldg(P.nD + rcv));
+                        float4 l4 = __ldg(P.seed_xL + w);
+                        xL = xyz(l4);
+                        pdfL = l4.w;
+                        lid = 0;
+                        if (S.n_light > 1) lid = (int)uidx(rng_draw(g.seed, P.walk_id_base + w, 0u, 0u).z, (uint32_t)S.n_light);
+                        phase = PH_SEED;
+                    }
+                } else {
+                    phase = PH_IDLE;
+                }
+            } else if (phase == PH_FETCH) {
                 int64_t idx = (int64_t)base + __popc(need & ((1u << lane) - 1u));
                 if (idx < P.n) {
                     w = idx;
@@ -392,7 +493,10 @@ __global__ void __launch_bounds__(128) k_walk(const DScene S, const SeedCtx g, c
             uint32_t sreq = 0;
 #pragma unroll
             for (int i = 0; i < KMAX; i++) sreq |= (uint32_t)(surf[i] & 15) << (4 * i);
-            bool ok = trace_chain<KMAX>(S, ded, k, tau, xD, tgt, q, sreq, P.ray_eps, y, yp, ys, ls);
+            int why = trace_chain<KMAX>(S, ded, k, tau, xD, tgt, q, sreq, P.ray_eps, y, yp, ys, ls);
+            bool ok = why == 0;
+            if (!ok && !ded && P.dbg && trial == 0 && w < P.n_dbg && 2 * it + 3 < P.dbg_stride)
+                P.dbg[w * P.dbg_stride + 2 * (it + 1)] = -(float)(why + 1);
             if (ok) {
 #pragma unroll
                 for (int i = 0; i < KMAX; i++) {
@@ -418,7 +522,12 @@ __global__ void __launch_bounds__(128) k_walk(const DScene S, const SeedCtx g, c
             if (fresh) {
                 fresh = false;
                 c_vtx += k;
-                int r = newton_system<KMAX>(S, k, tau, xD, xL, x, prim, surf, P.tol, Di, Ub, sg, tg, dq, singular);
+                float cm = 0.f;
+                int r = newton_system<KMAX>(S, k, tau, xD, xL, x, prim, surf, P.tol, Di, Ub, sg, tg, dq, singular, cm);
+                if (P.dbg && trial == 0 && w < P.n_dbg && 2 * it + 1 < P.dbg_stride) {
+                    P.dbg[w * P.dbg_stride + 2 * it] = cm;
+                    P.dbg[w * P.dbg_stride + 2 * it + 1] = beta;
+                }
                 if (r == 1) { end_status = ST_CONVERGED; phase = PH_END; }
                 else if (r == 2) { end_status = ST_DEGENERATE; phase = PH_END; }
             }
@@ -515,15 +624,32 @@ __global__ void __launch_bounds__(128) k_walk(const DScene S, const SeedCtx g, c
                         if ((int)((psurf >> (4 * i)) & 15u) != (surf[i] & 15) || !(len(dd) < P.same_eps)) same = false;
                     }
                 }
-                if (same || trial >= P.k_max) {
+                if (P.round_mode) {
+                    if (same) atomicMin(P.hard_best + cur_e, trial);
+                    phase = PH_FETCH;
+                } else if (same || trial >= P.k_max) {
                     if (!same) atomicAdd(&s_stats[SS_TRUNC], 1ull);
                     P.trials[w] = trial;
                     P.w[w] = Tprim * (float)trial / pdfL;
                     atomicAdd(&s_stats[SS_TRIALS], (unsigned long long)trial);
                     phase = PH_FETCH;
                 } else {
-                    trial++;
-                    phase = PH_SEED;
+                    bool published = false;
+                    if (trial >= P.local_trials && P.hard_walk) {
+                        // hand the remaining trials to the parallel rounds
+                        unsigned int e = atomicAdd(P.hard_count, 1u);
+                        if (e < P.hard_cap) {
+                            P.hard_walk[e] = w;
+                            P.hard_psurf[e] = psurf;
+                            P.hard_best[e] = HARD_NONE;
+                            published = true;
+                        }
+                    }
+                    if (published) phase = PH_FETCH;
+                    else {
+                        trial++;
+                        phase = PH_SEED;
+                    }
                 }
             }
         }
@@ -548,4 +674,38 @@ __global__ void __launch_bounds__(128) k_walk(const DScene S, const SeedCtx g, c
     if (P.stats)
         for (int i = threadIdx.x; i < SS_N; i += blockDim.x)
             if (s_stats[i]) atomicAdd(P.stats + i, s_stats[i]);
+}
+
+// After a trial round: resolved walks get k = min successful trial index (the
+// sequential definition of Eq. 15's geometric count, since every trial below
+// it was run); walks past k_max are truncated at k_max; the rest move to the
+// next round's list.
+__global__ void k_hard_compact(const int64_t *walk_in, const uint32_t *psurf_in, const uint32_t *best_in,
+                               const unsigned int *count_in, uint32_t cap, int64_t *walk_out, uint32_t *psurf_out,
+                               uint32_t *best_out, unsigned int *count_out, uint32_t t_end, uint32_t k_max,
+                               const float *T, const float4 *seed_xL, uint32_t *trials, float *w,
+                               unsigned long long *stats) {
+    uint32_t cnt = min(*count_in, cap);
+    unsigned long long s_tr = 0, s_tc = 0;
+    for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < cnt; e += gridDim.x * blockDim.x) {
+        int64_t wk = walk_in[e];
+        uint32_t b = best_in[e];
+        uint32_t kk = 0;
+        if (b != HARD_NONE) kk = b;
+        else if (t_end >= k_max) { kk = k_max; s_tc++; }
+        if (kk) {
+            trials[wk] = kk;
+            w[wk] = T[wk] * (float)kk / seed_xL[wk].w;
+            s_tr += kk;
+        } else {
+            unsigned int o = atomicAdd(count_out, 1u);
+            walk_out[o] = wk;
+            psurf_out[o] = psurf_in[e];
+            best_out[o] = HARD_NONE;
+        }
+    }
+    if (stats) {
+        if (s_tr) atomicAdd(stats + SS_TRIALS, s_tr);
+        if (s_tc) atomicAdd(stats + SS_TRUNC, s_tc);
+    }
 }

@@ -85,7 +85,7 @@ class mpg_scene_info(C.Structure):
 EXPORTS = ["mpg_scene_create", "mpg_scene_destroy", "mpg_scene_get_info", "mpg_trace_rays", "mpg_guide_create",
            "mpg_guide_destroy", "mpg_guide_upload", "mpg_guide_reset", "mpg_guide_accumulate", "mpg_guide_rebuild",
            "mpg_guide_download", "mpg_sample_seeds", "mpg_walk_workspace_size", "mpg_manifold_walk", "mpg_estimate",
-           "mpg_last_error", "mpg_version"]
+           "mpg_debug_trace", "mpg_last_error", "mpg_version"]
 
 _lib = None
 
@@ -119,6 +119,7 @@ def lib():
                                        C.POINTER(mpg_seed_buf), C.POINTER(mpg_walk_opts), C.POINTER(mpg_walk_buf), P,
                                        P, C.c_size_t, P]),
             "mpg_estimate": (st, [P, C.c_int64, C.c_int32, P, P, P]),
+            "mpg_debug_trace": (st, [P, C.c_int64, C.c_int32]),
             "mpg_last_error": (C.c_char_p, []),
             "mpg_version": (C.c_int32, []),
         }
@@ -221,6 +222,10 @@ def mpg_manifold_walk(scene, guide, sampler, query, seeds, opts, out, stats, wor
 
 def mpg_estimate(w, n_recv, spp, mean, var=None, stream=None):
     _check(lib().mpg_estimate(_ptr(w), n_recv, spp, _ptr(mean), _ptr(var), _stream_ptr(stream)), "mpg_estimate")
+
+
+def mpg_debug_trace(buf=None, n_walks=0, stride=0):
+    _check(lib().mpg_debug_trace(_ptr(buf), n_walks, stride), "mpg_debug_trace")
 
 
 def mpg_version() -> int:
@@ -344,7 +349,8 @@ class Batch:
         self.mean = torch.empty(max(1, self.n_recv), device=device)
         self.var = torch.empty(max(1, self.n_recv), device=device)
         self.stats = torch.zeros(len(STATS_FIELDS) + 8, dtype=torch.int64, device=device)
-        self.workspace = torch.zeros(256, dtype=torch.uint8, device=device)
+        self.workspace = torch.zeros(mpg_walk_workspace_size(self.n, mpg_walk_opts()), dtype=torch.uint8,
+                                     device=device)
         self.query = mpg_query(self.xD.data_ptr(), self.nD.data_ptr(), self.n_recv, self.spp)
         self.seeds = mpg_seed_buf(self.xL.data_ptr(), self.target.data_ptr(), self.bin.data_ptr())
         self.out = mpg_walk_buf(self.chain.data_ptr(), self.status.data_ptr(), self.iters.data_ptr(),

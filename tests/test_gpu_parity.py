@@ -60,7 +60,13 @@ def test_seeds_match_oracle(which):
             assert g["bin"][i] == -2
             continue
         assert g["bin"][i] == b                                        # discrete choice bit-exact
-        assert _ulp_diff(g["target"][i, :3], tgt).max() <= 4           # R23
+        if w.seed.mode == W.SEED_CAP:
+            # sin/cos differ by <= 2 ulp between CUDA and glibc (R23): the target moves by a few
+            # ulp of the sphere's scale, not of each (possibly tiny) coordinate
+            scale = np.abs(np.asarray(w.surfaces[w.seed.surf_id].center)).max() + w.surfaces[w.seed.surf_id].radius
+            assert np.abs(g["target"][i, :3] - tgt).max() <= 8 * 2.0 ** -24 * scale
+        else:
+            assert np.array_equal(g["target"][i, :3], tgt)             # only +,-,*,/,sqrt: bit-exact
 
 
 def _check_walk_parity(rep, min_agree=0.999):
