@@ -151,7 +151,7 @@ def run_ours(args):
     w.opts.walk_id_base = rank * w.n_walks          # independent partitions (weak scaling)
     ds = mpg.DeviceScene(w)
     b = mpg.Batch(w.xD, w.nD, w.spp, w.seed.k)
-    opts = ds.opts()
+    opts = ds.opts(flags=(1 if args.wavefront else 0) | (2 if args.hostloop else 0))
     stream = torch.cuda.current_stream()
     guided = ds.guide is not None
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)   # > 126 MB L2
@@ -304,6 +304,8 @@ def main():
     ap.add_argument("--ref-walks", type=int, default=100000)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--wavefront", action="store_true", help="wavefront path (MPG_FLAG_WAVEFRONT)")
+    ap.add_argument("--hostloop", action="store_true", help="wavefront with host-driven waves (profiling)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

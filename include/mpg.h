@@ -106,6 +106,10 @@ typedef struct {
     float uv_origin[2], uv_scale[2], uv_plane_y;
 } mpg_guide_desc;
 
+#define MPG_FLAG_WAVEFRONT 1u /* wavefront path (slots + CUDA-graph wave loop) instead of the default
+                                  persistent one-chain-per-lane kernel */
+#define MPG_FLAG_HOSTLOOP 2u  /* wavefront waves launched from the host (blocking; for profilers) */
+
 typedef struct {
     int32_t max_iters;     /* Newton cap (BASELINE configs: 20, or 40 for k=6)       */
     float tol;             /* ||C||_inf threshold (1e-5)                              */
@@ -114,7 +118,7 @@ typedef struct {
     uint32_t k_max;        /* trial cap (1024); truncation counted                    */
     float same_chain_eps;  /* 0 => 1e-4 * scene extent (R17/SPEC.md:280)              */
     float ray_eps;         /* 0 => 1e-4 * scene extent (R10)                          */
-    uint32_t flags;        /* reserved, 0                                             */
+    uint32_t flags;        /* MPG_FLAG_* (0 = default persistent kernel)              */
     uint64_t seed;         /* Philox key                                              */
     uint64_t walk_id_base; /* added to the walk index in the Philox counter          */
 } mpg_walk_opts;
@@ -198,8 +202,9 @@ mpg_status mpg_guide_download(const mpg_guide *guide, float *energy, uint64_t *p
 mpg_status mpg_sample_seeds(const mpg_scene *scene, const mpg_guide *guide, const mpg_sampler_desc *sampler,
                             const mpg_query *query, const mpg_walk_opts *opts, mpg_seed_buf *seeds, void *stream);
 
-/* Workspace bytes mpg_manifold_walk needs for n walks (work-queue counters). */
-size_t mpg_walk_workspace_size(int64_t n, const mpg_walk_opts *opts);
+/* Workspace bytes mpg_manifold_walk needs for n walks of chain length sampler->k
+ * (wavefront slots, ray lists, trial entries/items). */
+size_t mpg_walk_workspace_size(int64_t n, const mpg_sampler_desc *sampler, const mpg_walk_opts *opts);
 
 /* The batched manifold walk: per walk, deduce the seed chain
  * (Eq. 6), Newton-iterate the half-vector constraints with ray-traced

@@ -27,6 +27,14 @@ __device__ __forceinline__ float len(float3 a) { return sqrtf(dot(a, a)); }
 __device__ __forceinline__ float3 nrmz(float3 a) { return a * rsqrtf(dot(a, a)); }
 __device__ __forceinline__ float comp(float3 v, int i) { return i == 0 ? v.x : (i == 1 ? v.y : v.z); }
 
+// fp64 points: chain vertex positions are kept in fp64 (see walk.cuh, R24)
+__device__ __forceinline__ double3 d3f(float3 a) { return make_double3(a.x, a.y, a.z); }
+__device__ __forceinline__ float3 f3d(double3 a) { return make_float3((float)a.x, (float)a.y, (float)a.z); }
+__device__ __forceinline__ double3 operator+(double3 a, double3 b) { return make_double3(a.x + b.x, a.y + b.y, a.z + b.z); }
+__device__ __forceinline__ double3 operator-(double3 a, double3 b) { return make_double3(a.x - b.x, a.y - b.y, a.z - b.z); }
+__device__ __forceinline__ double3 operator*(double3 a, double s) { return make_double3(a.x * s, a.y * s, a.z * s); }
+__device__ __forceinline__ double ddot(double3 a, double3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
+
 // Orthonormal basis of a unit vector (Duff et al. 2017); any basis is valid for
 // the constraint frame and the step parameterization (R3, R4).
 __device__ __forceinline__ void onb(float3 n, float3 &b1, float3 &b2) {

@@ -15,6 +15,7 @@
 #include "device_common.cuh"
 #include "seed.cuh"
 #include "walk.cuh"
+#include "wavefront.cuh"
 
 // ----------------------------------------------------------------------------
 // error plumbing
@@ -678,10 +679,43 @@ extern "C" mpg_status mpg_debug_trace(float *buf, int64_t n_walks, int32_t strid
 // in rounds of B = 4, 8, 16, ... parallel trials
 #define LOCAL_TRIALS 4u
 static uint32_t hard_cap(int64_t n) { return (uint32_t)std::min<int64_t>(std::max<int64_t>(n, 1), 1 << 21); }
-extern "C" size_t mpg_walk_workspace_size(int64_t n, const mpg_walk_opts *opts) {
-    (void)opts;
+static size_t mk_ws_bytes(int64_t n) {
     size_t cap = hard_cap(n);
     return 256 + 2 * cap * (sizeof(int64_t) + 2 * sizeof(uint32_t));
+}
+
+// wavefront workspace layout: header, ray lists, free stack,
+// per-slot SoA state, hard entries, trial items
+struct WFLayout {
+    uint32_t S, H, C;
+    size_t hdr, list0, list1, fstack, s_walk, s_trial, s_flags, s_surf, s_ysurf, s_psurf, s_entry, s_beta, s_tgt,
+        s_x, s_dq, s_y, e_walk, e_psurf, e_best, e_issued, e_pending, e_batch, it_entry, it_trial, total;
+};
+static WFLayout wf_layout(int64_t n, int k) {
+    WFLayout L;
+    int64_t nn = std::max<int64_t>(n, 1);
+    L.S = (uint32_t)std::min<int64_t>(nn, 1 << 20);
+    L.H = (uint32_t)std::min<int64_t>(nn, 1 << 22);
+    L.C = 4u * L.H + 65536u;
+    size_t o = 0;
+    auto take = [&](size_t bytes) { size_t r = o; o += (bytes + 255) & ~(size_t)255; return r; };
+    L.hdr = take(sizeof(WFHeader));
+    L.list0 = take(4ull * L.S); L.list1 = take(4ull * L.S); L.fstack = take(4ull * L.S);
+    L.s_walk = take(4ull * L.S); L.s_trial = take(4ull * L.S); L.s_flags = take(4ull * L.S);
+    L.s_surf = take(4ull * L.S); L.s_ysurf = take(4ull * L.S); L.s_psurf = take(4ull * L.S);
+    L.s_entry = take(4ull * L.S); L.s_beta = take(4ull * L.S); L.s_tgt = take(16ull * L.S);
+    L.s_x = take(32ull * L.S * k); L.s_dq = take(16ull * L.S * k); L.s_y = take(32ull * L.S * k);
+    L.e_walk = take(4ull * L.H); L.e_psurf = take(4ull * L.H); L.e_best = take(4ull * L.H);
+    L.e_issued = take(4ull * L.H); L.e_pending = take(4ull * L.H); L.e_batch = take(4ull * L.H);
+    L.it_entry = take(4ull * L.C); L.it_trial = take(4ull * L.C);
+    L.total = o;
+    return L;
+}
+
+extern "C" size_t mpg_walk_workspace_size(int64_t n, const mpg_sampler_desc *sampler, const mpg_walk_opts *opts) {
+    int k = sampler ? std::max(1, std::min(MPG_KMAX, (int)sampler->k)) : MPG_KMAX;
+    (void)opts; // one size serves both paths
+    return std::max(wf_layout(n, k).total, mk_ws_bytes(n));
 }
 
 template <int KMAX>
@@ -728,6 +762,126 @@ static mpg_status launch_walk(const DScene &S, const SeedCtx &g, WalkParams P, c
     return MPG_OK;
 }
 
+// ---- wavefront launch: init + CUDA graph { while (more) { trace; update; plan; refill } } ----
+struct WFGraphCache {
+    std::vector<char> key;
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+};
+static WFGraphCache g_wfcache;
+
+template <int KMAX>
+static mpg_status launch_wavefront(const DScene &S, const SeedCtx &g, const WalkParams &MP, void *ws, size_t wsb,
+                                   cudaStream_t st) {
+    WFLayout L = wf_layout(MP.n, g.k);
+    if (wsb < L.total) return fail(MPG_ERR_INVALID_ARG, "workspace too small for the wavefront walk");
+    char *b = (char *)ws;
+    WFParams P;
+    memset(&P, 0, sizeof(P));
+    P.xD = MP.xD; P.nD = MP.nD; P.n = MP.n; P.spp = MP.spp;
+    P.seed_xL = MP.seed_xL; P.seed_tgt = MP.seed_tgt; P.seed_bin = MP.seed_bin;
+    P.chain = MP.chain; P.status = MP.status; P.iters = MP.iters; P.G = MP.G; P.T = MP.T; P.w = MP.w;
+    P.trials = MP.trials; P.stats = MP.stats;
+    P.max_iters = MP.max_iters; P.trials_on = MP.trials_on; P.k_max = MP.k_max;
+    P.tol = MP.tol; P.beta0 = MP.beta0; P.same_eps = MP.same_eps; P.ray_eps = MP.ray_eps;
+    P.walk_id_base = MP.walk_id_base;
+    P.hdr = (WFHeader *)(b + L.hdr);
+    P.S = L.S; P.H = L.H; P.C = L.C;
+    P.list[0] = (uint32_t *)(b + L.list0); P.list[1] = (uint32_t *)(b + L.list1);
+    P.free_stack = (uint32_t *)(b + L.fstack);
+    P.s_walk = (int32_t *)(b + L.s_walk); P.s_trial = (uint32_t *)(b + L.s_trial);
+    P.s_flags = (uint32_t *)(b + L.s_flags); P.s_surf = (uint32_t *)(b + L.s_surf);
+    P.s_ysurf = (uint32_t *)(b + L.s_ysurf); P.s_psurf = (uint32_t *)(b + L.s_psurf);
+    P.s_entry = (int32_t *)(b + L.s_entry); P.s_beta = (float *)(b + L.s_beta);
+    P.s_tgt = (float4 *)(b + L.s_tgt); P.s_x = (double4 *)(b + L.s_x); P.s_dq = (float4 *)(b + L.s_dq);
+    P.s_y = (double4 *)(b + L.s_y);
+    P.e_walk = (int32_t *)(b + L.e_walk); P.e_psurf = (uint32_t *)(b + L.e_psurf);
+    P.e_best = (uint32_t *)(b + L.e_best); P.e_issued = (uint32_t *)(b + L.e_issued);
+    P.e_pending = (uint32_t *)(b + L.e_pending); P.e_batch = (uint32_t *)(b + L.e_batch);
+    P.it_entry = (int32_t *)(b + L.it_entry); P.it_trial = (uint32_t *)(b + L.it_trial);
+
+    static int occ_t = 0, occ_u = 0;
+    if (!occ_t) {
+        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_t, k_wf_trace<KMAX>, 128, 0));
+        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_u, k_wf_update<KMAX>, 128, 0));
+        occ_t = std::max(occ_t, 1); occ_u = std::max(occ_u, 1);
+    }
+    int gt = num_sms() * occ_t;
+    int gu = (int)std::min<int64_t>((L.S + 127) / 128, (int64_t)num_sms() * occ_u * 4);
+    int gr = (int)std::min<int64_t>((L.S + 255) / 256, (int64_t)num_sms() * 8);
+    int gi = (int)std::min<int64_t>((L.S + 255) / 256, (int64_t)num_sms() * 8);
+
+    if (MP.host_loop) { // host-driven waves (profilers cannot see kernels inside conditional graphs)
+        P.use_cond = 0;
+        k_wf_init<KMAX><<<gi, 256, 0, st>>>(S, g, P);
+        CUDA_TRY(cudaPeekAtLastError());
+        unsigned int more = 1;
+        for (int wave = 0; more; wave++) {
+            k_wf_trace<KMAX><<<gt, 128, 0, st>>>(S, g, P);
+            k_wf_update<KMAX><<<gu, 128, 0, st>>>(S, g, P);
+            k_wf_plan<<<1, 1, 0, st>>>(P);
+            k_wf_refill<KMAX><<<gr, 256, 0, st>>>(S, g, P);
+            CUDA_TRY(cudaPeekAtLastError());
+            if ((wave & 7) == 7) {
+                CUDA_TRY(cudaMemcpyAsync(&more, &P.hdr->more, 4, cudaMemcpyDeviceToHost, st));
+                CUDA_TRY(cudaStreamSynchronize(st));
+            }
+        }
+        return MPG_OK;
+    }
+    P.use_cond = 1;
+    // graph cache key: every byte the graph depends on
+    std::vector<char> key(sizeof(DScene) + sizeof(SeedCtx) + sizeof(WFParams) + 4 * sizeof(int));
+    {
+        char *kp = key.data();
+        memcpy(kp, &S, sizeof(DScene)); kp += sizeof(DScene);
+        memcpy(kp, &g, sizeof(SeedCtx)); kp += sizeof(SeedCtx);
+        WFParams Pk = P; Pk.cond = 0;
+        memcpy(kp, &Pk, sizeof(WFParams)); kp += sizeof(WFParams);
+        int dims[4] = {gt, gu, gr, KMAX};
+        memcpy(kp, dims, sizeof(dims));
+    }
+    if (!g_wfcache.exec || g_wfcache.key != key) {
+        if (g_wfcache.exec) { cudaGraphExecDestroy(g_wfcache.exec); g_wfcache.exec = nullptr; }
+        if (g_wfcache.graph) { cudaGraphDestroy(g_wfcache.graph); g_wfcache.graph = nullptr; }
+        cudaGraph_t graph;
+        CUDA_TRY(cudaGraphCreate(&graph, 0));
+        cudaGraphConditionalHandle h;
+        CUDA_TRY(cudaGraphConditionalHandleCreate(&h, graph, 1, cudaGraphCondAssignDefault));
+        P.cond = h;
+        cudaGraphNodeParams cp = {};
+        cp.type = cudaGraphNodeTypeConditional;
+        cp.conditional.handle = h;
+        cp.conditional.type = cudaGraphCondTypeWhile;
+        cp.conditional.size = 1;
+        cudaGraphNode_t cnode;
+        CUDA_TRY(cudaGraphAddNode(&cnode, graph, nullptr, 0, &cp));
+        cudaGraph_t body = cp.conditional.phGraph_out[0];
+        DScene Sv = S; SeedCtx gv = g; WFParams Pv = P;
+        void *args3[] = {&Sv, &gv, &Pv};
+        void *args1[] = {&Pv};
+        cudaKernelNodeParams kt = {}, ku = {}, kpn = {}, kr = {};
+        kt.func = (void *)k_wf_trace<KMAX>; kt.gridDim = dim3(gt); kt.blockDim = dim3(128); kt.kernelParams = args3;
+        ku.func = (void *)k_wf_update<KMAX>; ku.gridDim = dim3(gu); ku.blockDim = dim3(128); ku.kernelParams = args3;
+        kpn.func = (void *)k_wf_plan; kpn.gridDim = dim3(1); kpn.blockDim = dim3(1); kpn.kernelParams = args1;
+        kr.func = (void *)k_wf_refill<KMAX>; kr.gridDim = dim3(gr); kr.blockDim = dim3(256); kr.kernelParams = args3;
+        cudaGraphNode_t n1, n2, n3, n4;
+        CUDA_TRY(cudaGraphAddKernelNode(&n1, body, nullptr, 0, &kt));
+        CUDA_TRY(cudaGraphAddKernelNode(&n2, body, &n1, 1, &ku));
+        CUDA_TRY(cudaGraphAddKernelNode(&n3, body, &n2, 1, &kpn));
+        CUDA_TRY(cudaGraphAddKernelNode(&n4, body, &n3, 1, &kr));
+        cudaGraphExec_t ex;
+        CUDA_TRY(cudaGraphInstantiate(&ex, graph, 0));
+        g_wfcache.graph = graph;
+        g_wfcache.exec = ex;
+        g_wfcache.key = key;
+    }
+    k_wf_init<KMAX><<<gi, 256, 0, st>>>(S, g, P);
+    CUDA_TRY(cudaPeekAtLastError());
+    CUDA_TRY(cudaGraphLaunch(g_wfcache.exec, st));
+    return MPG_OK;
+}
+
 extern "C" mpg_status mpg_manifold_walk(const mpg_scene *scene, const mpg_guide *guide, const mpg_sampler_desc *sd,
                                         const mpg_query *q, const mpg_seed_buf *sb, const mpg_walk_opts *o,
                                         mpg_walk_buf *out, mpg_walk_stats *stats, void *workspace,
@@ -739,7 +893,8 @@ extern "C" mpg_status mpg_manifold_walk(const mpg_scene *scene, const mpg_guide 
         ARG_CHECK(out->chain && out->status && out->iters && out->G && out->T && out->w && out->trials,
                   "NULL output array");
     }
-    ARG_CHECK(workspace && workspace_bytes >= mpg_walk_workspace_size(q->n_recv * q->spp, o), "workspace too small");
+    ARG_CHECK(workspace && workspace_bytes >= mpg_walk_workspace_size(q->n_recv * q->spp, sd, o), "workspace too small");
+    ARG_CHECK(q->n_recv * (int64_t)q->spp < (int64_t)1 << 31, "at most 2^31-1 walks per call");
     ARG_CHECK(o->max_iters >= 0 && o->max_iters < 65536 && o->tol > 0.f && o->beta0 > 0.f, "bad walk options");
     ARG_CHECK(!o->trials || o->k_max >= 1, "k_max must be >= 1");
     SeedCtx g;
@@ -773,6 +928,7 @@ extern "C" mpg_status mpg_manifold_walk(const mpg_scene *scene, const mpg_guide 
     P.same_eps = o->same_chain_eps > 0.f ? o->same_chain_eps : 1e-4f * scene->d.extent;
     P.ray_eps = o->ray_eps > 0.f ? o->ray_eps : 1e-4f * scene->d.extent;
     P.walk_id_base = o->walk_id_base;
+    P.host_loop = (o->flags & MPG_FLAG_HOSTLOOP) != 0;
     P.dbg = g_dbg;
     P.n_dbg = g_dbg_n;
     P.dbg_stride = g_dbg_stride;
@@ -785,8 +941,15 @@ extern "C" mpg_status mpg_manifold_walk(const mpg_scene *scene, const mpg_guide 
         P.hard_best = (uint32_t *)(base + 256 + (size_t)P.hard_cap * 24);
         P.hard_count = (unsigned int *)(base + 16);
     }
-    CUDA_TRY(cudaMemsetAsync(workspace, 0, 64, s));
     int k = g.k;
+    if (o->flags & MPG_FLAG_WAVEFRONT) {
+        if (k <= 1) return launch_wavefront<1>(scene->d, g, P, workspace, workspace_bytes, s);
+        if (k <= 2) return launch_wavefront<2>(scene->d, g, P, workspace, workspace_bytes, s);
+        if (k <= 4) return launch_wavefront<4>(scene->d, g, P, workspace, workspace_bytes, s);
+        if (k <= 6) return launch_wavefront<6>(scene->d, g, P, workspace, workspace_bytes, s);
+        return launch_wavefront<8>(scene->d, g, P, workspace, workspace_bytes, s);
+    }
+    CUDA_TRY(cudaMemsetAsync(workspace, 0, 64, s));
     if (k <= 1) return launch_walk<1>(scene->d, g, P, s, workspace);
     if (k <= 2) return launch_walk<2>(scene->d, g, P, s, workspace);
     if (k <= 4) return launch_walk<4>(scene->d, g, P, s, workspace);

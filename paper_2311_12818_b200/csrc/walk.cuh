@@ -53,6 +53,7 @@ struct WalkParams {
     uint32_t *hard_best; // min successful trial index (0xffffffff: none yet)
     unsigned int *hard_count;
     int round_mode;     // 0: main pass; 1: trial round over the hard list
+    int host_loop;      // wavefront: host-driven waves (MPG_FLAG_HOSTLOOP)
     uint32_t round_t0, round_B; // round covers trials [t0, t0+B)
 };
 
@@ -61,25 +62,34 @@ enum { SS_WALKS = 0, SS_CONV, SS_NEWTON, SS_PRIM_IT, SS_ATTEMPTS, SS_RAYS, SS_TR
        SS_VTX, SS_STATUS0, SS_N = SS_STATUS0 + 8 };
 
 // reflect / refract the propagation direction d at a vertex (deduction, Eq. 6);
-// media from the side of d w.r.t. the geometric normal (R9, R14)
-__device__ __forceinline__ bool scatter_dir(const DScene &S, float3 &d, int prim, int surf, float3 p, bool isT) {
+// media from the side of d w.r.t. the geometric normal (R9, R14).  fp64: the
+// deduced seed chain then matches the oracle's to fp32 rounding of positions.
+__device__ __forceinline__ bool scatter_dir(const DScene &S, double3 &dd, int prim, int surf, float3 p, bool isT) {
     const DSurf &f = S.surf[surf];
     float3 ng = geo_normal(S, prim, surf, p);
-    float3 n = shading_normal(S, prim, surf, p);
-    bool outside = dot(d, ng) < 0.0f;
-    if (dot(d, n) > 0.0f) n = -n;
-    float ci = -dot(d, n);
-    if (!(ci > 0.0f)) return false;
+    float3 nf = shading_normal(S, prim, surf, p);
+    double dx = dd.x, dy = dd.y, dz = dd.z, nx = nf.x, ny = nf.y, nz = nf.z;
+    double il = rsqrt(nx * nx + ny * ny + nz * nz);
+    nx *= il; ny *= il; nz *= il;
+    bool outside = (dx * ng.x + dy * ng.y + dz * ng.z) < 0.0;
+    double dn = dx * nx + dy * ny + dz * nz;
+    if (dn > 0.0) { nx = -nx; ny = -ny; nz = -nz; dn = -dn; }
+    double ci = -dn;
+    if (!(ci > 0.0)) return false;
+    double rx, ry, rz;
     if (!isT) {
-        d = d + n * (2.0f * ci);
-        return true;
+        rx = dx + 2.0 * ci * nx; ry = dy + 2.0 * ci * ny; rz = dz + 2.0 * ci * nz;
+    } else {
+        if (f.mat != 1) return false;
+        double e1 = outside ? f.eta_out : f.eta_in, e2 = outside ? f.eta_in : f.eta_out;
+        double eta = e1 / e2;
+        double k2 = 1.0 - eta * eta * (1.0 - ci * ci);
+        if (k2 < 0.0) return false; // TIR
+        double c = eta * ci - sqrt(k2);
+        rx = eta * dx + c * nx; ry = eta * dy + c * ny; rz = eta * dz + c * nz;
     }
-    if (f.mat != 1) return false;
-    float e1 = outside ? f.eta_out : f.eta_in, e2 = outside ? f.eta_in : f.eta_out;
-    float eta = e1 / e2;
-    float k2 = 1.0f - eta * eta * (1.0f - ci * ci);
-    if (k2 < 0.0f) return false; // TIR
-    d = nrmz(d * eta + n * (eta * ci - sqrtf(k2)));
+    double ir = rsqrt(rx * rx + ry * ry + rz * rz);
+    dd = make_double3(rx * ir, ry * ir, rz * ir);
     return true;
 }
 
@@ -88,9 +98,9 @@ __device__ __forceinline__ bool scatter_dir(const DScene &S, float3 &d, int prim
 // rounded once: the reprojected vertex is within 1/2 ulp of the exact point,
 // so the Newton residual is not floored by reprojection noise (which near
 // grazing chains reached ~1e-5 in fp32, measured).
-__device__ __forceinline__ float3 refine_hit(const DScene &S, int prim, int surf, float3 o, float3 q, float3 pf) {
+__device__ __forceinline__ double3 refine_hit(const DScene &S, int prim, int surf, double3 o, double3 q, float3 pf) {
     double ox = o.x, oy = o.y, oz = o.z;
-    double dx = (double)q.x - ox, dy = (double)q.y - oy, dz = (double)q.z - oz;
+    double dx = q.x - ox, dy = q.y - oy, dz = q.z - oz;
     double t;
     if (prim >= 0) {
         float3 a = xyz(__ldg(S.tpos + 3 * prim)), b = xyz(__ldg(S.tpos + 3 * prim + 1)), c = xyz(__ldg(S.tpos + 3 * prim + 2));
@@ -98,7 +108,7 @@ __device__ __forceinline__ float3 refine_hit(const DScene &S, int prim, int surf
         double e2x = (double)c.x - a.x, e2y = (double)c.y - a.y, e2z = (double)c.z - a.z;
         double nx = e1y * e2z - e1z * e2y, ny = e1z * e2x - e1x * e2z, nz = e1x * e2y - e1y * e2x;
         double den = dx * nx + dy * ny + dz * nz;
-        if (den == 0.0) return pf;
+        if (den == 0.0) return d3f(pf);
         t = (((double)a.x - ox) * nx + ((double)a.y - oy) * ny + ((double)a.z - oz) * nz) / den;
     } else {
         const DSurf &f = S.surf[surf];
@@ -108,7 +118,7 @@ __device__ __forceinline__ float3 refine_hit(const DScene &S, int prim, int surf
             double bb = (cx * dx + cy * dy + cz * dz) / dd;
             double rx = cx - bb * dx, ry = cy - bb * dy, rz = cz - bb * dz;
             double disc = ((double)f.radius * f.radius - (rx * rx + ry * ry + rz * rz)) / dd;
-            if (disc < 0.0) return pf;
+            if (disc < 0.0) return d3f(pf);
             double sq = sqrt(disc);
             // the root nearest to the fp32 hit the traversal selected
             double tf = ((double)pf.x - ox) * dx + ((double)pf.y - oy) * dy + ((double)pf.z - oz) * dz;
@@ -118,46 +128,49 @@ __device__ __forceinline__ float3 refine_hit(const DScene &S, int prim, int surf
         } else {
             double nx = f.nq.x, ny = f.nq.y, nz = f.nq.z;
             double den = dx * nx + dy * ny + dz * nz;
-            if (den == 0.0) return pf;
+            if (den == 0.0) return d3f(pf);
             t = (((double)f.origin.x - ox) * nx + ((double)f.origin.y - oy) * ny + ((double)f.origin.z - oz) * nz) / den;
         }
     }
-    return make_float3((float)(ox + t * dx), (float)(oy + t * dy), (float)(oz + t * dz));
+    return make_double3(ox + t * dx, oy + t * dy, oz + t * dz);
 }
 
 // Trace the k chain vertices from x_D: deduction (scatter by tau) or
 // reprojection toward q_i (must stay on surf_i).  Rolled loop: one traversal
 // site.  y/yp/ys/q live in local memory (dynamic index).
 // returns 0 on success, else 1 + (i << 4) | reason (1 miss, 2 wrong surface, 3 zero length, 4 scatter)
+// Traversal runs in fp32 (the hit/miss and which-primitive decisions); the hit
+// point is recomputed in fp64 on the exact line (refine_hit) and kept in fp64.
 template <int KMAX>
 __device__ __forceinline__ int trace_chain(const DScene &S, bool deduce, int k, uint32_t tau, float3 xD, float3 tgt,
-                                            const float3 *q, uint32_t surf_req, float eps, float3 *y, int *yp,
-                                            int *ys, LaneStats &st) {
-    float3 o = xD;
-    float3 d = f3(0.f, 0.f, 0.f);
+                                           const double3 *q, uint32_t surf_req, float eps, double3 *y, int *yp,
+                                           int *ys, LaneStats &st) {
+    double3 o = d3f(xD);
+    double3 dd = make_double3(0.0, 0.0, 0.0);
     if (deduce) {
-        float3 v = tgt - xD;
-        float l2 = dot(v, v);
-        if (!(l2 > 0.0f)) return 3;
-        d = v * rsqrtf(l2);
+        double3 v = d3f(tgt) - o;
+        double l2 = ddot(v, v);
+        if (!(l2 > 0.0)) return 3;
+        dd = v * rsqrt(l2);
     }
 #pragma unroll 1
     for (int i = 0; i < k; i++) {
         if (!deduce) {
-            float3 v = q[i] - o;
-            float l2 = dot(v, v);
-            if (!(l2 > 0.0f)) return 3 | (i << 4);
-            d = v * rsqrtf(l2);
+            double3 v = q[i] - o;
+            double l2 = ddot(v, v);
+            if (!(l2 > 0.0)) return 3 | (i << 4);
+            dd = v * rsqrt(l2);
         } else if (i > 0) {
-            if (!scatter_dir(S, d, yp[i - 1], ys[i - 1], y[i - 1], (tau >> (i - 1)) & 1u)) return 4 | (i << 4);
+            if (!scatter_dir(S, dd, yp[i - 1], ys[i - 1], f3d(y[i - 1]), (tau >> (i - 1)) & 1u)) return 4 | (i << 4);
         }
         Hit h;
-        if (!trace<false>(S, o, d, eps, 3.0e38f, true, h, st)) return 1 | (i << 4);
+        float3 of = f3d(o), d = nrmz(f3d(dd));
+        if (!trace<false>(S, of, d, eps, 3.0e38f, true, h, st)) return 1 | (i << 4);
         if (!deduce && h.surf != (int)((surf_req >> (4 * i)) & 15u)) return 2 | (i << 4);
-        y[i] = refine_hit(S, h.prim, h.surf, o, deduce ? o + d : q[i], h.p);
+        y[i] = refine_hit(S, h.prim, h.surf, o, deduce ? o + dd : q[i], h.p);
         yp[i] = h.prim;
         ys[i] = h.surf;
-        o = h.p;
+        o = y[i];
     }
     return 0;
 }
@@ -174,10 +187,10 @@ struct VTerm {
     double c0, c1;
 };
 
-__device__ __forceinline__ bool vterm(float3 a, float3 p, float3 b, float3 ng, float3 n, const DSurf &f, bool isT,
+__device__ __forceinline__ bool vterm(double3 a, double3 p, double3 b, float3 ng, float3 n, const DSurf &f, bool isT,
                                       VTerm &v) {
-    double ax = (double)a.x - (double)p.x, ay = (double)a.y - (double)p.y, az = (double)a.z - (double)p.z;
-    double bx = (double)b.x - (double)p.x, by = (double)b.y - (double)p.y, bz = (double)b.z - (double)p.z;
+    double ax = a.x - p.x, ay = a.y - p.y, az = a.z - p.z;
+    double bx = b.x - p.x, by = b.y - p.y, bz = b.z - p.z;
     double la2 = ax * ax + ay * ay + az * az, lb2 = bx * bx + by * by + bz * bz;
     if (!(la2 > 0.0) || !(lb2 > 0.0)) return false;
     double ia = rsqrt(la2), ib = rsqrt(lb2);
@@ -228,7 +241,7 @@ __device__ __forceinline__ float2 dC_self(const VTerm &v, float3 dir, float3 dn)
 // singular pivot (used only if converged: G is then 0).
 template <int KMAX>
 __device__ __forceinline__ int newton_system(const DScene &S, int k, uint32_t tau, float3 xD, float3 xL,
-                                             const float3 (&x)[KMAX], const int (&prim)[KMAX],
+                                             const double3 (&x)[KMAX], const int (&prim)[KMAX],
                                              const int (&surf)[KMAX], float tol, float (&Di)[KMAX][4],
                                              float (&Ub)[KMAX][4], float3 (&sg)[KMAX], float3 (&tg)[KMAX],
                                              float3 (&dq)[KMAX], bool &singular, float &cmax_out) {
@@ -239,17 +252,17 @@ __device__ __forceinline__ int newton_system(const DScene &S, int k, uint32_t ta
 #pragma unroll
     for (int i = 0; i < KMAX; i++) {
         if (i >= k) break;
-        float3 ng = geo_normal(S, prim[i], surf[i], x[i]);
+        float3 ng = geo_normal(S, prim[i], surf[i], f3d(x[i]));
         onb(ng, sg[i], tg[i]);
     }
 #pragma unroll
     for (int i = 0; i < KMAX; i++) {
         if (i >= k) break;
-        float3 a = i == 0 ? xD : x[i > 0 ? i - 1 : 0];
-        float3 b = i == k - 1 ? xL : x[i + 1 < KMAX ? i + 1 : i];
+        double3 a = i == 0 ? d3f(xD) : x[i > 0 ? i - 1 : 0];
+        double3 b = i == k - 1 ? d3f(xL) : x[i + 1 < KMAX ? i + 1 : i];
         const DSurf &f = S.surf[surf[i]];
         float3 dna, dnb;
-        float3 n = shading(S, prim[i], surf[i], x[i], sg[i], tg[i], dna, dnb);
+        float3 n = shading(S, prim[i], surf[i], f3d(x[i]), sg[i], tg[i], dna, dnb);
         VTerm v;
         if (!vterm(a, x[i], b, cross(sg[i], tg[i]), n, f, (tau >> i) & 1u, v)) { degen = true; break; }
         float c0 = (float)v.c0, c1 = (float)v.c1;
@@ -307,21 +320,22 @@ __device__ __forceinline__ int newton_system(const DScene &S, int k, uint32_t ta
 // returns false on a side violation.
 template <int KMAX>
 __device__ __forceinline__ bool post_sweep(const DScene &S, const DLight &L, int k, uint32_t tau, float3 xD,
-                                           float3 xL, const float3 (&x)[KMAX], const int (&prim)[KMAX],
+                                           float3 xL, const double3 (&x)[KMAX], const int (&prim)[KMAX],
                                            const int (&surf)[KMAX], bool want_kappa, float &kappa, float (&DL)[4]) {
     float kap = 1.0f, etaD = 1.0f, etaL = 1.0f;
 #pragma unroll
     for (int i = 0; i < KMAX; i++) {
         if (i >= k) break;
-        float3 a = i == 0 ? xD : x[i > 0 ? i - 1 : 0];
-        float3 b = i == k - 1 ? xL : x[i + 1 < KMAX ? i + 1 : i];
+        double3 a = i == 0 ? d3f(xD) : x[i > 0 ? i - 1 : 0];
+        double3 b = i == k - 1 ? d3f(xL) : x[i + 1 < KMAX ? i + 1 : i];
         const DSurf &f = S.surf[surf[i]];
-        float3 ng = geo_normal(S, prim[i], surf[i], x[i]);
-        float di = dot(a - x[i], ng), dd = dot(b - x[i], ng);
+        const float3 xi = f3d(x[i]);
+        float3 ng = geo_normal(S, prim[i], surf[i], xi);
+        float di = dot(f3d(a - x[i]), ng), dd = dot(f3d(b - x[i]), ng);
         bool isT = (tau >> i) & 1u;
         if (isT ? !(di * dd < 0.0f) : !(di * dd > 0.0f)) return false;
         if (!want_kappa) continue;
-        float3 n = shading_normal(S, prim[i], surf[i], x[i]);
+        float3 n = shading_normal(S, prim[i], surf[i], xi);
         bool oi = di > 0.0f, oo = dd > 0.0f;
         float e_wi = oi ? f.eta_out : f.eta_in, e_wo = oo ? f.eta_out : f.eta_in;
         if (i == 0) etaD = e_wi;
@@ -332,7 +346,7 @@ __device__ __forceinline__ bool post_sweep(const DScene &S, const DLight &L, int
             else {
                 float3 l1, l2;
                 if (L.kind == 1) { l1 = L.l1; l2 = L.l2; }
-                else onb(nrmz(xL - x[i]), l1, l2);
+                else onb(nrmz(f3d(d3f(xL) - x[i])), l1, l2);
                 float2 c0 = dC_nb(v, v.wo, v.lo, v.eo, l1), c1 = dC_nb(v, v.wo, v.lo, v.eo, l2);
                 DL[0] = c0.x; DL[1] = c1.x; DL[2] = c0.y; DL[3] = c1.y;
             }
@@ -340,7 +354,7 @@ __device__ __forceinline__ bool post_sweep(const DScene &S, const DLight &L, int
         if (f.mat == 0) kap *= f.refl;
         else {
             float e_other = oi ? f.eta_in : f.eta_out;
-            float3 wi = nrmz(a - x[i]);
+            float3 wi = nrmz(f3d(a - x[i]));
             float F = fresnel(dot(wi, n), e_wi, e_other);
             kap *= isT ? (1.0f - F) : F;
         }
@@ -351,7 +365,7 @@ __device__ __forceinline__ bool post_sweep(const DScene &S, const DLight &L, int
 
 // analytic GGT: back-substitute J Y = -[0..0; D_L] with the stored D'^-1, U (R11)
 template <int KMAX>
-__device__ __forceinline__ float ggt_from_blocks(int k, float3 xD, float3 nD, const float3 (&x)[KMAX],
+__device__ __forceinline__ float ggt_from_blocks(int k, float3 xD, float3 nD, const double3 (&x)[KMAX],
                                                  const float (&Di)[KMAX][4], const float (&Ub)[KMAX][4],
                                                  const float3 (&sg)[KMAX], const float3 (&tg)[KMAX],
                                                  const float (&DL)[4]) {
@@ -371,7 +385,7 @@ __device__ __forceinline__ float ggt_from_blocks(int k, float3 xD, float3 nD, co
         float n10 = Di[i][2] * b00 + Di[i][3] * b10, n11 = Di[i][2] * b01 + Di[i][3] * b11;
         y00 = n00; y01 = n01; y10 = n10; y11 = n11;
     }
-    float3 r = x[0] - xD;
+    float3 r = f3d(x[0] - d3f(xD));
     float rl = len(r);
     float3 w = r * (1.0f / rl);
     float3 e1, e2;
@@ -405,14 +419,19 @@ __global__ void __launch_bounds__(128) k_walk(const DScene S, const SeedCtx g, c
     float beta = 1.f;
     bool fresh = false;
     uint32_t psurf = 0; // primary surf ids, 4 bits each
-    float3 x[KMAX], sg[KMAX], tg[KMAX], dq[KMAX];
+    double3 x[KMAX];
+    float3 sg[KMAX], tg[KMAX], dq[KMAX];
     int prim[KMAX], surf[KMAX];
     float Di[KMAX][4], Ub[KMAX][4];
-    float3 q[KMAX], y[KMAX];
+    double3 q[KMAX], y[KMAX];
     int yp[KMAX], ys[KMAX];
     bool singular = false;
 #pragma unroll
-    for (int i = 0; i < KMAX; i++) { x[i] = sg[i] = tg[i] = dq[i] = f3(0, 0, 0); prim[i] = -1; surf[i] = 0; }
+    for (int i = 0; i < KMAX; i++) {
+        x[i] = make_double3(0.0, 0.0, 0.0);
+        sg[i] = tg[i] = dq[i] = f3(0, 0, 0);
+        prim[i] = -1; surf[i] = 0;
+    }
     LaneStats ls = {0u, 0u, 0u};
     uint32_t c_newton = 0, c_vtx = 0, c_attempts = 0;
 
@@ -537,7 +556,7 @@ __global__ void __launch_bounds__(128) k_walk(const DScene S, const SeedCtx g, c
 #pragma unroll
                     for (int i = 0; i < KMAX; i++) {
                         if (i >= k) break;
-                        q[i] = x[i] + dq[i] * beta;
+                        q[i] = x[i] + d3f(dq[i]) * (double)beta;
                     }
                     phase = PH_REPROJ;
                 }
@@ -560,7 +579,7 @@ __global__ void __launch_bounds__(128) k_walk(const DScene S, const SeedCtx g, c
                         float3 a = xD;
 #pragma unroll 1
                         for (int j = 0; j <= k; j++) {
-                            float3 b = j == k ? xL : y[j];
+                            float3 b = j == k ? xL : f3d(y[j]);
                             float3 dd = b - a;
                             float l = len(dd);
                             Hit hh;
@@ -574,7 +593,7 @@ __global__ void __launch_bounds__(128) k_walk(const DScene S, const SeedCtx g, c
                         else {
                             G = singular ? 0.0f : ggt_from_blocks<KMAX>(k, xD, nD, x, Di, Ub, sg, tg, DL);
                             float Le = L.emit;
-                            if (L.kind == 1 && !(dot(x[k - 1] - xL, L.n) > 0.0f)) Le = 0.0f;
+                            if (L.kind == 1 && !(dot(f3d(x[k - 1]) - xL, L.n) > 0.0f)) Le = 0.0f;
                             T = kap * G * Le;
                         }
                     }
@@ -584,7 +603,7 @@ __global__ void __launch_bounds__(128) k_walk(const DScene S, const SeedCtx g, c
                     for (int i = 0; i < KMAX; i++) {
                         if (i >= k) break;
                         int pid = prim[i] >= 0 ? __float_as_int(__ldg(S.tpos + 3 * prim[i]).w) : -1;
-                        P.chain[(int64_t)i * P.n + w] = make_float4(x[i].x, x[i].y, x[i].z, __int_as_float(pid));
+                        P.chain[(int64_t)i * P.n + w] = make_float4((float)x[i].x, (float)x[i].y, (float)x[i].z, __int_as_float(pid));
                     }
                 }
                 P.status[w] = (uint8_t)st;
@@ -620,7 +639,7 @@ __global__ void __launch_bounds__(128) k_walk(const DScene S, const SeedCtx g, c
                     for (int i = 0; i < KMAX; i++) {
                         if (i >= k) break;
                         float4 c = P.chain[(int64_t)i * P.n + w];
-                        float3 dd = x[i] - xyz(c);
+                        float3 dd = f3d(x[i]) - xyz(c);
                         if ((int)((psurf >> (4 * i)) & 15u) != (surf[i] & 15) || !(len(dd) < P.same_eps)) same = false;
                     }
                 }

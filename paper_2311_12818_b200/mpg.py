@@ -114,7 +114,7 @@ def lib():
             "mpg_guide_download": (st, [P, P, P, P]),
             "mpg_sample_seeds": (st, [P, P, C.POINTER(mpg_sampler_desc), C.POINTER(mpg_query),
                                       C.POINTER(mpg_walk_opts), C.POINTER(mpg_seed_buf), P]),
-            "mpg_walk_workspace_size": (C.c_size_t, [C.c_int64, C.POINTER(mpg_walk_opts)]),
+            "mpg_walk_workspace_size": (C.c_size_t, [C.c_int64, C.POINTER(mpg_sampler_desc), C.POINTER(mpg_walk_opts)]),
             "mpg_manifold_walk": (st, [P, P, C.POINTER(mpg_sampler_desc), C.POINTER(mpg_query),
                                        C.POINTER(mpg_seed_buf), C.POINTER(mpg_walk_opts), C.POINTER(mpg_walk_buf), P,
                                        P, C.c_size_t, P]),
@@ -210,8 +210,8 @@ def mpg_sample_seeds(scene, guide, sampler, query, opts, seeds, stream=None):
                                   _stream_ptr(stream)), "mpg_sample_seeds")
 
 
-def mpg_walk_workspace_size(n, opts) -> int:
-    return int(lib().mpg_walk_workspace_size(n, C.byref(opts)))
+def mpg_walk_workspace_size(n, sampler, opts) -> int:
+    return int(lib().mpg_walk_workspace_size(n, C.byref(sampler), C.byref(opts)))
 
 
 def mpg_manifold_walk(scene, guide, sampler, query, seeds, opts, out, stats, workspace, stream=None):
@@ -349,7 +349,8 @@ class Batch:
         self.mean = torch.empty(max(1, self.n_recv), device=device)
         self.var = torch.empty(max(1, self.n_recv), device=device)
         self.stats = torch.zeros(len(STATS_FIELDS) + 8, dtype=torch.int64, device=device)
-        self.workspace = torch.zeros(mpg_walk_workspace_size(self.n, mpg_walk_opts()), dtype=torch.uint8,
+        smp = mpg_sampler_desc(0, 0, k, 0)
+        self.workspace = torch.zeros(mpg_walk_workspace_size(self.n, smp, mpg_walk_opts()), dtype=torch.uint8,
                                      device=device)
         self.query = mpg_query(self.xD.data_ptr(), self.nD.data_ptr(), self.n_recv, self.spp)
         self.seeds = mpg_seed_buf(self.xL.data_ptr(), self.target.data_ptr(), self.bin.data_ptr())

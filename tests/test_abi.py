@@ -55,7 +55,7 @@ def test_invalid_arguments_rejected_synchronously(L):
     wb = mpg.mpg_walk_buf()
     assert L.mpg_manifold_walk(None, None, C.byref(sd), C.byref(q), C.byref(s), C.byref(o), C.byref(wb), None,
                                None, 0, None) == 1
-    assert L.mpg_walk_workspace_size(10, C.byref(o)) >= 8
+    assert L.mpg_walk_workspace_size(10, C.byref(sd), C.byref(o)) >= 8
 
 
 def test_struct_layouts():
