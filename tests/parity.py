@@ -38,7 +38,9 @@ def compare(g, o, ids, extent, k):
            "both": int(both.sum())}
     gp = g["pos"][ids][:, :k]
     dpos = np.linalg.norm(gp - o["pos"][:, :k], axis=2).max(1)
-    rep["max_dpos_rel"] = float(dpos[both].max() / extent) if both.any() else 0.0
+    same = both & (dpos < 1e-4 * extent)
+    rep["max_dpos_rel"] = float(dpos[same].max() / extent) if same.any() else 0.0
+    rep["n_other_chain"] = int((both & ~same).sum())
     gprim = g["prim"][ids][:, :k]
     same_prim = (gprim == o["prim"][:, :k]).all(1)
     rep["prim_agree"] = float(same_prim[both].mean()) if both.any() else 1.0
@@ -63,3 +65,35 @@ def tile_means(wv, spp, recv_shape, tile):
     ty, tx = ny // tile, nx // tile
     a = a[:ty * tile, :tx * tile].reshape(ty, tile, tx, tile, spp).transpose(0, 2, 1, 3, 4).reshape(ty * tx, -1)
     return a.mean(1), a.std(1, ddof=1), a.shape[1]
+
+
+def classify_boundary(s, w, o, ids, extent, max_n=300, seed=0):
+    """Reading R18: a flag disagreement is a basin/budget boundary case if the
+    oracle's own outcome changes under one of 8 seed-target perturbations of
+    1e-4 x extent, or under max_iters +- 3.  Returns (n_boundary, n_checked, non_boundary_ids)."""
+    rng = np.random.default_rng(seed)
+    pos = {int(x): j for j, x in enumerate(o["walk"])}
+    nb, bad = 0, []
+    for i in list(ids)[:max_n]:
+        j = pos[int(i)]
+        xD = w.xD[int(i) // w.spp].astype(np.float64)
+        base = o["status"][j] in (0, 5)
+        tgt = o["target"][j].astype(np.float64)
+        changed = False
+        for _ in range(8):
+            v = rng.normal(size=3)
+            v /= np.linalg.norm(v)
+            r = s.walk_from_target(xD, w.nD[0], o["xL"][j], tgt + 1e-4 * extent * v)
+            if (r["status"] in (0, 5)) != base:
+                changed = True
+                break
+        if not changed:
+            for mi in (w.opts.max_iters - 3, w.opts.max_iters + 3):
+                r = s.walk_from_target(xD, w.nD[0], o["xL"][j], tgt, opts=s.opts(max_iters=mi))
+                if (r["status"] in (0, 5)) != base:
+                    changed = True
+                    break
+        nb += changed
+        if not changed:
+            bad.append(int(i))
+    return nb, min(len(ids), max_n), bad
