@@ -151,7 +151,8 @@ def run_ours(args):
     w.opts.walk_id_base = rank * w.n_walks          # independent partitions (weak scaling)
     ds = mpg.DeviceScene(w)
     b = mpg.Batch(w.xD, w.nD, w.spp, w.seed.k)
-    opts = ds.opts(flags=(1 if args.wavefront else 0) | (2 if args.hostloop else 0))
+    opts = ds.opts(flags=w.opts.flags | (1 if args.wavefront else 0) | (2 if args.hostloop else 0) |
+                   (4 if args.f64 else 0))
     stream = torch.cuda.current_stream()
     guided = ds.guide is not None
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)   # > 126 MB L2
@@ -269,11 +270,13 @@ def run_ours(args):
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "walks/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                "scaling": "weak", "vs_baseline": None, "dtype": "f32+f64" if opts.flags & 4 else "f32", "data": "synthetic",
                 "config": {"workload": CONFIG_NAMES[args.config], "n_walks_per_gpu": b.n, "k": w.seed.k,
                            "max_iters": w.opts.max_iters, "trials": "on (k_max 1024)",
                            "l2": "256 MB buffer written before every timed step (inputs < 126 MB L2)",
-                           "precision": "fp32 traversal/Jacobian/storage; fp64 residual and hit refinement"},
+                           "precision": ("fp32 scene/traversal; fp64 positions, residual, hit refinement" +
+                                         ("; fp64 Jacobian/step (MPG_FLAG_NEWTON_F64)" if opts.flags & 4
+                                          else "; fp32 Jacobian/step"))},
                 "newton_iters_per_s": newton_all / (tot_ms / 1e3),
                 "walks_incl_trials_per_s": S["attempts"] * world / (tot_ms / 1e3),
                 "rays_per_s": S["rays"] * world / (tot_ms / 1e3),
@@ -306,6 +309,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--wavefront", action="store_true", help="wavefront path (MPG_FLAG_WAVEFRONT)")
     ap.add_argument("--hostloop", action="store_true", help="wavefront with host-driven waves (profiling)")
+    ap.add_argument("--f64", action="store_true", help="MPG_FLAG_NEWTON_F64")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -109,6 +109,8 @@ typedef struct {
 #define MPG_FLAG_WAVEFRONT 1u /* wavefront path (slots + CUDA-graph wave loop) instead of the default
                                   persistent one-chain-per-lane kernel */
 #define MPG_FLAG_HOSTLOOP 2u  /* wavefront waves launched from the host (blocking; for profilers) */
+#define MPG_FLAG_NEWTON_F64 4u /* Jacobian blocks, frames and steps in fp64 (default fp32; positions and
+                                  the residual are always fp64, R24) */
 
 typedef struct {
     int32_t max_iters;     /* Newton cap (BASELINE configs: 20, or 40 for k=6)       */

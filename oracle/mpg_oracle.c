@@ -1117,3 +1117,31 @@ int orc_walk_trace(const void *h, const orc_opts *o, int k, uint32_t tau, const 
     g_beta_hist = NULL;
     return st;
 }
+
+/* guide accumulation (Eq. 9; histogram stand-in R20): for walks with
+ * status CONVERGED and w > 0, hist[cell(x_D)][bin(x_1*)] += w.  The cell uses the
+ * same fp32 expression as the seed draw; the bin of x_1* = (x, z) in the (u,v)
+ * map u = (x - uv_origin)/uv_scale, clamped.  x1 is given as float (the
+ * reported chain position). */
+void orc_accumulate(const orc_seed_cfg *cfg, const float *xD, int32_t spp, int64_t n, const int32_t *status,
+                    const float *w, const float *x1, double *hist) {
+    int nb = cfg->bins_x * cfg->bins_y;
+    for (int64_t i = 0; i < n; i++) {
+        if (status[i] != ST_CONVERGED || !(w[i] > 0.0f)) continue;
+        const float *xd = xD + 3 * (i / spp);
+        int cx = (int)floorf(((xd[0] - cfg->grid_origin[0]) * (float)cfg->cells_x) / cfg->grid_extent[0]);
+        int cz = (int)floorf(((xd[2] - cfg->grid_origin[1]) * (float)cfg->cells_y) / cfg->grid_extent[1]);
+        if (cx < 0) cx = 0;
+        if (cx > cfg->cells_x - 1) cx = cfg->cells_x - 1;
+        if (cz < 0) cz = 0;
+        if (cz > cfg->cells_y - 1) cz = cfg->cells_y - 1;
+        float u = (x1[3 * i] - cfg->uv_origin[0]) / cfg->uv_scale[0];
+        float v = (x1[3 * i + 2] - cfg->uv_origin[1]) / cfg->uv_scale[1];
+        int bx = (int)floorf(u * (float)cfg->bins_x), by = (int)floorf(v * (float)cfg->bins_y);
+        if (bx < 0) bx = 0;
+        if (bx > cfg->bins_x - 1) bx = cfg->bins_x - 1;
+        if (by < 0) by = 0;
+        if (by > cfg->bins_y - 1) by = cfg->bins_y - 1;
+        hist[(size_t)(cz * cfg->cells_x + cx) * nb + by * cfg->bins_x + bx] += w[i];
+    }
+}

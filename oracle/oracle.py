@@ -107,6 +107,7 @@ def lib():
         _lib.orc_walk_trace.restype = C.c_int
         _lib.orc_walk_trace.argtypes = [P, C.POINTER(Opts), C.c_int, C.c_uint32, dp, dp, dp, dp, dp,
                                         C.POINTER(C.c_int32)]
+        _lib.orc_accumulate.argtypes = [C.POINTER(SeedCfg), P, C.c_int32, C.c_int64, P, P, P, P]
         _lib.orc_tangent_basis.argtypes = [P, C.c_int32, C.c_int32, dp, dp, dp]
         _lib.orc_scatter.restype = C.c_int
         _lib.orc_scatter.argtypes = [C.c_int, C.c_double, C.c_double, dp, dp, dp]
@@ -298,6 +299,17 @@ class OracleScene:
                                   _d3(target), res.ctypes.data_as(C.POINTER(C.c_double)),
                                   beta.ctypes.data_as(C.POINTER(C.c_double)), C.byref(it))
         return st, it.value, res[:it.value + 1], beta[:it.value + 1]
+
+    def accumulate(self, status, w, x1):
+        """Guide histogram [cells][bins] (fp64) from per-walk status, w and x_1* (float [n,3])."""
+        sp = self.w.seed
+        hist = np.zeros((sp.cells_x * sp.cells_y, sp.bins_x * sp.bins_y), np.float64)
+        st = np.ascontiguousarray(status, np.int32)
+        wv = np.ascontiguousarray(w, np.float32)
+        x1 = np.ascontiguousarray(x1, np.float32)
+        lib().orc_accumulate(C.byref(self.cfg), _ptr(self.w.xD), self.w.spp, st.shape[0], _ptr(st), _ptr(wv),
+                             _ptr(x1), _ptr(hist))
+        return hist
 
     def tangent_basis(self, prim, surf, p):
         a = (C.c_double * 3)()

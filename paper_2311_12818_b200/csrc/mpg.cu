@@ -718,16 +718,16 @@ extern "C" size_t mpg_walk_workspace_size(int64_t n, const mpg_sampler_desc *sam
     return std::max(wf_layout(n, k).total, mk_ws_bytes(n));
 }
 
-template <int KMAX>
+template <int KMAX, typename R>
 static mpg_status launch_walk(const DScene &S, const SeedCtx &g, WalkParams P, cudaStream_t st, void *ws) {
     static int occ = 0;
     if (!occ) {
-        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_walk<KMAX>, 128, 0));
+        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_walk<KMAX, R>, 128, 0));
         if (occ <= 0) occ = 1;
     }
     int64_t want = (P.n + 127) / 128;
     int blocks = (int)std::min<int64_t>(want, (int64_t)num_sms() * occ);
-    k_walk<KMAX><<<blocks, 128, 0, st>>>(S, g, P);
+    k_walk<KMAX, R><<<blocks, 128, 0, st>>>(S, g, P);
     CUDA_TRY(cudaPeekAtLastError());
     if (!P.trials_on || P.k_max <= P.local_trials) return MPG_OK;
     // parallel trial rounds over the hard list (ping-pong buffers A/B)
@@ -741,14 +741,14 @@ static mpg_status launch_walk(const DScene &S, const SeedCtx &g, WalkParams P, c
     int cur = 0, rblocks = num_sms() * occ;
     while (t0 <= P.k_max) {
         uint32_t Bc = std::min(B, P.k_max - t0 + 1);
-        WalkParams R = P;
-        R.round_mode = 1;
-        R.round_t0 = t0;
-        R.round_B = Bc;
-        R.hard_walk = wl[cur]; R.hard_psurf = pl[cur]; R.hard_best = bl[cur]; R.hard_count = cnt + cur;
-        R.queue = (unsigned long long *)(base + 8);
+        WalkParams RP = P;
+        RP.round_mode = 1;
+        RP.round_t0 = t0;
+        RP.round_B = Bc;
+        RP.hard_walk = wl[cur]; RP.hard_psurf = pl[cur]; RP.hard_best = bl[cur]; RP.hard_count = cnt + cur;
+        RP.queue = (unsigned long long *)(base + 8);
         CUDA_TRY(cudaMemsetAsync(base + 8, 0, 8, st));
-        k_walk<KMAX><<<rblocks, 128, 0, st>>>(S, g, R);
+        k_walk<KMAX, R><<<rblocks, 128, 0, st>>>(S, g, RP);
         CUDA_TRY(cudaPeekAtLastError());
         CUDA_TRY(cudaMemsetAsync(cnt + (cur ^ 1), 0, 4, st));
         k_hard_compact<<<num_sms() * 2, 256, 0, st>>>(wl[cur], pl[cur], bl[cur], cnt + cur, cap, wl[cur ^ 1],
@@ -942,6 +942,8 @@ extern "C" mpg_status mpg_manifold_walk(const mpg_scene *scene, const mpg_guide 
         P.hard_count = (unsigned int *)(base + 16);
     }
     int k = g.k;
+    ARG_CHECK(!((o->flags & MPG_FLAG_WAVEFRONT) && (o->flags & MPG_FLAG_NEWTON_F64)),
+              "MPG_FLAG_NEWTON_F64 is implemented on the default path only");
     if (o->flags & MPG_FLAG_WAVEFRONT) {
         if (k <= 1) return launch_wavefront<1>(scene->d, g, P, workspace, workspace_bytes, s);
         if (k <= 2) return launch_wavefront<2>(scene->d, g, P, workspace, workspace_bytes, s);
@@ -950,11 +952,18 @@ extern "C" mpg_status mpg_manifold_walk(const mpg_scene *scene, const mpg_guide 
         return launch_wavefront<8>(scene->d, g, P, workspace, workspace_bytes, s);
     }
     CUDA_TRY(cudaMemsetAsync(workspace, 0, 64, s));
-    if (k <= 1) return launch_walk<1>(scene->d, g, P, s, workspace);
-    if (k <= 2) return launch_walk<2>(scene->d, g, P, s, workspace);
-    if (k <= 4) return launch_walk<4>(scene->d, g, P, s, workspace);
-    if (k <= 6) return launch_walk<6>(scene->d, g, P, s, workspace);
-    return launch_walk<8>(scene->d, g, P, s, workspace);
+    if (o->flags & MPG_FLAG_NEWTON_F64) {
+        if (k <= 1) return launch_walk<1, double>(scene->d, g, P, s, workspace);
+        if (k <= 2) return launch_walk<2, double>(scene->d, g, P, s, workspace);
+        if (k <= 4) return launch_walk<4, double>(scene->d, g, P, s, workspace);
+        if (k <= 6) return launch_walk<6, double>(scene->d, g, P, s, workspace);
+        return launch_walk<8, double>(scene->d, g, P, s, workspace);
+    }
+    if (k <= 1) return launch_walk<1, float>(scene->d, g, P, s, workspace);
+    if (k <= 2) return launch_walk<2, float>(scene->d, g, P, s, workspace);
+    if (k <= 4) return launch_walk<4, float>(scene->d, g, P, s, workspace);
+    if (k <= 6) return launch_walk<6, float>(scene->d, g, P, s, workspace);
+    return launch_walk<8, float>(scene->d, g, P, s, workspace);
 }
 
 // ----------------------------------------------------------------------------

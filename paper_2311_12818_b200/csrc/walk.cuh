@@ -19,6 +19,7 @@
 #pragma once
 #include "device_common.cuh"
 #include "seed.cuh"
+#include "newton.cuh"
 
 enum { PH_FETCH = 0, PH_SEED = 1, PH_DEDUCE = 2, PH_SOLVE = 3, PH_REPROJ = 4, PH_END = 5, PH_IDLE = 6 };
 #define HARD_NONE 0xffffffffu
@@ -175,229 +176,7 @@ __device__ __forceinline__ int trace_chain(const DScene &S, bool deduce, int k, 
     return 0;
 }
 
-// per-vertex constraint pieces.  The residual C = (s.h, t.h) is evaluated in
-// fp64 from the fp32 vertex positions (their differences are exact in fp64):
-// near grazing reflection |h~| = 2cos(theta) -> 0 amplifies fp32 rounding of
-// w_i + w_o by 1/|h~| up to the 1e-5 tolerance (measured: GPU MAXITER where
-// the fp64 oracle converged).  The Jacobian blocks stay fp32: their error only
-// slows the (quasi-)Newton contraction, it does not move the converged point.
-struct VTerm {
-    float3 wi, wo, h, s, t;
-    float li, lo, ei, eo, hl, hn;
-    double c0, c1;
-};
-
-__device__ __forceinline__ bool vterm(double3 a, double3 p, double3 b, float3 ng, float3 n, const DSurf &f, bool isT,
-                                      VTerm &v) {
-    double ax = a.x - p.x, ay = a.y - p.y, az = a.z - p.z;
-    double bx = b.x - p.x, by = b.y - p.y, bz = b.z - p.z;
-    double la2 = ax * ax + ay * ay + az * az, lb2 = bx * bx + by * by + bz * bz;
-    if (!(la2 > 0.0) || !(lb2 > 0.0)) return false;
-    double ia = rsqrt(la2), ib = rsqrt(lb2);
-    ax *= ia; ay *= ia; az *= ia;
-    bx *= ib; by *= ib; bz *= ib;
-    v.li = (float)(la2 * ia);
-    v.lo = (float)(lb2 * ib);
-    v.wi = f3((float)ax, (float)ay, (float)az);
-    v.wo = f3((float)bx, (float)by, (float)bz);
-    if (isT) {
-        bool out = dot(v.wi, ng) > 0.0f;
-        v.ei = out ? f.eta_out : f.eta_in;
-        v.eo = out ? f.eta_in : f.eta_out;
-    } else {
-        v.ei = v.eo = 1.0f;
-    }
-    double hx = (double)v.ei * ax + (double)v.eo * bx, hy = (double)v.ei * ay + (double)v.eo * by,
-           hz = (double)v.ei * az + (double)v.eo * bz;
-    double hl2 = hx * hx + hy * hy + hz * hz;
-    if (!(hl2 > 0.0) || !isfinite(hl2)) return false;
-    double ih = rsqrt(hl2);
-    hx *= ih; hy *= ih; hz *= ih;
-    v.hl = (float)(hl2 * ih);
-    v.h = f3((float)hx, (float)hy, (float)hz);
-    onb(n, v.s, v.t);
-    v.c0 = (double)v.s.x * hx + (double)v.s.y * hy + (double)v.s.z * hz;
-    v.c1 = (double)v.t.x * hx + (double)v.t.y * hy + (double)v.t.z * hz;
-    v.hn = dot(v.h, n);
-    return true;
-}
-
-// dC along a neighbour displacement: c*P v with P the projector of w over l (L, U, D_L blocks)
-__device__ __forceinline__ float2 dC_nb(const VTerm &v, float3 w, float l, float eta, float3 dir) {
-    float3 u = (dir - w * dot(w, dir)) * (eta / l);
-    float3 dh = (u - v.h * dot(v.h, u)) * (1.0f / v.hl);
-    return make_float2(dot(v.s, dh), dot(v.t, dh));
-}
-// dC along the vertex's own displacement (D block; minimal-rotation frame, R3)
-__device__ __forceinline__ float2 dC_self(const VTerm &v, float3 dir, float3 dn) {
-    float3 u = (dir - v.wi * dot(v.wi, dir)) * (-v.ei / v.li) - (dir - v.wo * dot(v.wo, dir)) * (v.eo / v.lo);
-    float3 dh = (u - v.h * dot(v.h, u)) * (1.0f / v.hl);
-    return make_float2(dot(v.s, dh) - v.hn * dot(v.s, dn), dot(v.t, dh) - v.hn * dot(v.t, dn));
-}
-
-// Forward sweep: constraint + blocks + block-Thomas elimination; then (if not
-// converged) back substitution into world-space step directions dq.
-// returns 0: step ready, 1: converged, 2: degenerate.  `singular` reports a
-// singular pivot (used only if converged: G is then 0).
-template <int KMAX>
-__device__ __forceinline__ int newton_system(const DScene &S, int k, uint32_t tau, float3 xD, float3 xL,
-                                             const double3 (&x)[KMAX], const int (&prim)[KMAX],
-                                             const int (&surf)[KMAX], float tol, float (&Di)[KMAX][4],
-                                             float (&Ub)[KMAX][4], float3 (&sg)[KMAX], float3 (&tg)[KMAX],
-                                             float3 (&dq)[KMAX], bool &singular, float &cmax_out) {
-    float rp[KMAX][2];
-    bool degen = false;
-    singular = false;
-    double cmax = 0.0;
-#pragma unroll
-    for (int i = 0; i < KMAX; i++) {
-        if (i >= k) break;
-        float3 ng = geo_normal(S, prim[i], surf[i], f3d(x[i]));
-        onb(ng, sg[i], tg[i]);
-    }
-#pragma unroll
-    for (int i = 0; i < KMAX; i++) {
-        if (i >= k) break;
-        double3 a = i == 0 ? d3f(xD) : x[i > 0 ? i - 1 : 0];
-        double3 b = i == k - 1 ? d3f(xL) : x[i + 1 < KMAX ? i + 1 : i];
-        const DSurf &f = S.surf[surf[i]];
-        float3 dna, dnb;
-        float3 n = shading(S, prim[i], surf[i], f3d(x[i]), sg[i], tg[i], dna, dnb);
-        VTerm v;
-        if (!vterm(a, x[i], b, cross(sg[i], tg[i]), n, f, (tau >> i) & 1u, v)) { degen = true; break; }
-        float c0 = (float)v.c0, c1 = (float)v.c1;
-        cmax = fmax(cmax, fmax(fabs(v.c0), fabs(v.c1)));
-        float2 d0 = dC_self(v, sg[i], dna), d1 = dC_self(v, tg[i], dnb);
-        float D00 = d0.x, D10 = d0.y, D01 = d1.x, D11 = d1.y;
-        float r0 = -c0, r1 = -c1;
-        if (i > 0) {
-            const int j = i > 0 ? i - 1 : 0;
-            float2 l0 = dC_nb(v, v.wi, v.li, v.ei, sg[j]), l1 = dC_nb(v, v.wi, v.li, v.ei, tg[j]);
-            // M = L * Di[j]
-            float M00 = l0.x * Di[j][0] + l1.x * Di[j][2], M01 = l0.x * Di[j][1] + l1.x * Di[j][3];
-            float M10 = l0.y * Di[j][0] + l1.y * Di[j][2], M11 = l0.y * Di[j][1] + l1.y * Di[j][3];
-            D00 -= M00 * Ub[j][0] + M01 * Ub[j][2];
-            D01 -= M00 * Ub[j][1] + M01 * Ub[j][3];
-            D10 -= M10 * Ub[j][0] + M11 * Ub[j][2];
-            D11 -= M10 * Ub[j][1] + M11 * Ub[j][3];
-            r0 -= M00 * rp[j][0] + M01 * rp[j][1];
-            r1 -= M10 * rp[j][0] + M11 * rp[j][1];
-        }
-        if (i < k - 1) {
-            const int j = i + 1 < KMAX ? i + 1 : i;
-            float2 u0 = dC_nb(v, v.wo, v.lo, v.eo, sg[j]), u1 = dC_nb(v, v.wo, v.lo, v.eo, tg[j]);
-            Ub[i][0] = u0.x; Ub[i][1] = u1.x; Ub[i][2] = u0.y; Ub[i][3] = u1.y;
-        }
-        float det = D00 * D11 - D01 * D10;
-        if (!(det != 0.0f) || !isfinite(det)) singular = true;
-        float id = 1.0f / det;
-        Di[i][0] = D11 * id; Di[i][1] = -D01 * id; Di[i][2] = -D10 * id; Di[i][3] = D00 * id;
-        rp[i][0] = r0; rp[i][1] = r1;
-    }
-    cmax_out = (float)cmax;
-    if (degen || !isfinite(cmax)) return 2;
-    if (cmax < (double)tol) return 1;
-    if (singular) return 2;
-    float n0 = 0.f, n1 = 0.f; // Delta_{i+1}
-#pragma unroll
-    for (int i = KMAX - 1; i >= 0; i--) {
-        if (i > k - 1) continue;
-        float r0 = rp[i][0], r1 = rp[i][1];
-        if (i < k - 1) {
-            r0 -= Ub[i][0] * n0 + Ub[i][1] * n1;
-            r1 -= Ub[i][2] * n0 + Ub[i][3] * n1;
-        }
-        float a0 = Di[i][0] * r0 + Di[i][1] * r1;
-        float a1 = Di[i][2] * r0 + Di[i][3] * r1;
-        if (!isfinite(a0) || !isfinite(a1)) return 2;
-        dq[i] = sg[i] * a0 + tg[i] * a1;
-        n0 = a0; n1 = a1;
-    }
-    return 0;
-}
-
-// sides (R8), kappa (R12) and the light-side block D_L at a converged chain.
-// returns false on a side violation.
-template <int KMAX>
-__device__ __forceinline__ bool post_sweep(const DScene &S, const DLight &L, int k, uint32_t tau, float3 xD,
-                                           float3 xL, const double3 (&x)[KMAX], const int (&prim)[KMAX],
-                                           const int (&surf)[KMAX], bool want_kappa, float &kappa, float (&DL)[4]) {
-    float kap = 1.0f, etaD = 1.0f, etaL = 1.0f;
-#pragma unroll
-    for (int i = 0; i < KMAX; i++) {
-        if (i >= k) break;
-        double3 a = i == 0 ? d3f(xD) : x[i > 0 ? i - 1 : 0];
-        double3 b = i == k - 1 ? d3f(xL) : x[i + 1 < KMAX ? i + 1 : i];
-        const DSurf &f = S.surf[surf[i]];
-        const float3 xi = f3d(x[i]);
-        float3 ng = geo_normal(S, prim[i], surf[i], xi);
-        float di = dot(f3d(a - x[i]), ng), dd = dot(f3d(b - x[i]), ng);
-        bool isT = (tau >> i) & 1u;
-        if (isT ? !(di * dd < 0.0f) : !(di * dd > 0.0f)) return false;
-        if (!want_kappa) continue;
-        float3 n = shading_normal(S, prim[i], surf[i], xi);
-        bool oi = di > 0.0f, oo = dd > 0.0f;
-        float e_wi = oi ? f.eta_out : f.eta_in, e_wo = oo ? f.eta_out : f.eta_in;
-        if (i == 0) etaD = e_wi;
-        if (i == k - 1) {
-            etaL = e_wo;
-            VTerm v;
-            if (!vterm(a, x[i], b, ng, n, f, isT, v)) { DL[0] = DL[1] = DL[2] = DL[3] = 0.f; }
-            else {
-                float3 l1, l2;
-                if (L.kind == 1) { l1 = L.l1; l2 = L.l2; }
-                else onb(nrmz(f3d(d3f(xL) - x[i])), l1, l2);
-                float2 c0 = dC_nb(v, v.wo, v.lo, v.eo, l1), c1 = dC_nb(v, v.wo, v.lo, v.eo, l2);
-                DL[0] = c0.x; DL[1] = c1.x; DL[2] = c0.y; DL[3] = c1.y;
-            }
-        }
-        if (f.mat == 0) kap *= f.refl;
-        else {
-            float e_other = oi ? f.eta_in : f.eta_out;
-            float3 wi = nrmz(f3d(a - x[i]));
-            float F = fresnel(dot(wi, n), e_wi, e_other);
-            kap *= isT ? (1.0f - F) : F;
-        }
-    }
-    kappa = kap * (etaD / etaL) * (etaD / etaL);
-    return true;
-}
-
-// analytic GGT: back-substitute J Y = -[0..0; D_L] with the stored D'^-1, U (R11)
-template <int KMAX>
-__device__ __forceinline__ float ggt_from_blocks(int k, float3 xD, float3 nD, const double3 (&x)[KMAX],
-                                                 const float (&Di)[KMAX][4], const float (&Ub)[KMAX][4],
-                                                 const float3 (&sg)[KMAX], const float3 (&tg)[KMAX],
-                                                 const float (&DL)[4]) {
-    float y00 = 0.f, y01 = 0.f, y10 = 0.f, y11 = 0.f; // Y_{i+1}
-#pragma unroll
-    for (int i = KMAX - 1; i >= 0; i--) {
-        if (i > k - 1) continue;
-        float b00, b01, b10, b11;
-        if (i == k - 1) { b00 = -DL[0]; b01 = -DL[1]; b10 = -DL[2]; b11 = -DL[3]; }
-        else {
-            b00 = -(Ub[i][0] * y00 + Ub[i][1] * y10);
-            b01 = -(Ub[i][0] * y01 + Ub[i][1] * y11);
-            b10 = -(Ub[i][2] * y00 + Ub[i][3] * y10);
-            b11 = -(Ub[i][2] * y01 + Ub[i][3] * y11);
-        }
-        float n00 = Di[i][0] * b00 + Di[i][1] * b10, n01 = Di[i][0] * b01 + Di[i][1] * b11;
-        float n10 = Di[i][2] * b00 + Di[i][3] * b10, n11 = Di[i][2] * b01 + Di[i][3] * b11;
-        y00 = n00; y01 = n01; y10 = n10; y11 = n11;
-    }
-    float3 r = f3d(x[0] - d3f(xD));
-    float rl = len(r);
-    float3 w = r * (1.0f / rl);
-    float3 e1, e2;
-    onb(w, e1, e2);
-    float3 dx0 = sg[0] * y00 + tg[0] * y10, dx1 = sg[0] * y01 + tg[0] * y11;
-    float3 dw0 = (dx0 - w * dot(w, dx0)) * (1.0f / rl), dw1 = (dx1 - w * dot(w, dx1)) * (1.0f / rl);
-    float M00 = dot(e1, dw0), M01 = dot(e1, dw1), M10 = dot(e2, dw0), M11 = dot(e2, dw1);
-    float G = fabsf(dot(nD, w)) * fabsf(M00 * M11 - M01 * M10);
-    return isfinite(G) ? G : 0.0f;
-}
-
-template <int KMAX>
+template <int KMAX, typename R>
 __global__ void __launch_bounds__(128) k_walk(const DScene S, const SeedCtx g, const WalkParams P) {
     __shared__ unsigned long long s_stats[SS_N];
     for (int i = threadIdx.x; i < SS_N; i += blockDim.x) s_stats[i] = 0ull;
@@ -420,16 +199,16 @@ __global__ void __launch_bounds__(128) k_walk(const DScene S, const SeedCtx g, c
     bool fresh = false;
     uint32_t psurf = 0; // primary surf ids, 4 bits each
     double3 x[KMAX];
-    float3 sg[KMAX], tg[KMAX], dq[KMAX];
+    V3<R> sg[KMAX], tg[KMAX], dq[KMAX];
     int prim[KMAX], surf[KMAX];
-    float Di[KMAX][4], Ub[KMAX][4];
+    R Di[KMAX][4], Ub[KMAX][4];
     double3 q[KMAX], y[KMAX];
     int yp[KMAX], ys[KMAX];
     bool singular = false;
 #pragma unroll
     for (int i = 0; i < KMAX; i++) {
         x[i] = make_double3(0.0, 0.0, 0.0);
-        sg[i] = tg[i] = dq[i] = f3(0, 0, 0);
+        sg[i] = tg[i] = dq[i] = mk3<R>(0, 0, 0);
         prim[i] = -1; surf[i] = 0;
     }
     LaneStats ls = {0u, 0u, 0u};
@@ -542,7 +321,7 @@ __global__ void __launch_bounds__(128) k_walk(const DScene S, const SeedCtx g, c
                 fresh = false;
                 c_vtx += k;
                 float cm = 0.f;
-                int r = newton_system<KMAX>(S, k, tau, xD, xL, x, prim, surf, P.tol, Di, Ub, sg, tg, dq, singular, cm);
+                int r = newton_system<KMAX, R>(S, k, tau, xD, xL, x, prim, surf, P.tol, Di, Ub, sg, tg, dq, singular, cm);
                 if (P.dbg && trial == 0 && w < P.n_dbg && 2 * it + 1 < P.dbg_stride) {
                     P.dbg[w * P.dbg_stride + 2 * it] = cm;
                     P.dbg[w * P.dbg_stride + 2 * it + 1] = beta;
@@ -556,7 +335,7 @@ __global__ void __launch_bounds__(128) k_walk(const DScene S, const SeedCtx g, c
 #pragma unroll
                     for (int i = 0; i < KMAX; i++) {
                         if (i >= k) break;
-                        q[i] = x[i] + d3f(dq[i]) * (double)beta;
+                        q[i] = x[i] + tod(dq[i]) * (double)beta;
                     }
                     phase = PH_REPROJ;
                 }
@@ -571,8 +350,9 @@ __global__ void __launch_bounds__(128) k_walk(const DScene S, const SeedCtx g, c
                 float G = 0.f, T = 0.f;
                 if (st == ST_CONVERGED) {
                     const DLight &L = S.light[lid];
-                    float kap, DL[4];
-                    if (!post_sweep<KMAX>(S, L, k, tau, xD, xL, x, prim, surf, true, kap, DL)) st = ST_BAD_SIDE;
+                    float kap;
+                    R DL[4];
+                    if (!post_sweep<KMAX, R>(S, L, k, tau, xD, xL, x, prim, surf, true, kap, DL)) st = ST_BAD_SIDE;
                     else {
                         // visibility: k+1 any-hit segments against all surfaces
                         bool vis = true;
@@ -591,7 +371,7 @@ __global__ void __launch_bounds__(128) k_walk(const DScene S, const SeedCtx g, c
                         }
                         if (!vis) st = ST_OCCLUDED;
                         else {
-                            G = singular ? 0.0f : ggt_from_blocks<KMAX>(k, xD, nD, x, Di, Ub, sg, tg, DL);
+                            G = singular ? 0.0f : ggt_from_blocks<KMAX, R>(k, xD, nD, x, Di, Ub, sg, tg, DL);
                             float Le = L.emit;
                             if (L.kind == 1 && !(dot(f3d(x[k - 1]) - xL, L.n) > 0.0f)) Le = 0.0f;
                             T = kap * G * Le;
@@ -631,9 +411,10 @@ __global__ void __launch_bounds__(128) k_walk(const DScene S, const SeedCtx g, c
                 }
             } else {
                 bool same = false;
-                float kdummy, DLdummy[4];
+                float kdummy;
+                R DLdummy[4];
                 if (st == ST_CONVERGED &&
-                    post_sweep<KMAX>(S, S.light[lid], k, tau, xD, xL, x, prim, surf, false, kdummy, DLdummy)) {
+                    post_sweep<KMAX, R>(S, S.light[lid], k, tau, xD, xL, x, prim, surf, false, kdummy, DLdummy)) {
                     same = true;
 #pragma unroll
                     for (int i = 0; i < KMAX; i++) {

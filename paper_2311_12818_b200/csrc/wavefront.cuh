@@ -414,19 +414,19 @@ __global__ void __launch_bounds__(128) k_wf_update(const DScene S, const SeedCtx
         float beta = P.s_beta[slot];
         bool deduce = fl & F_DEDUCE, failed = fl & F_FAIL;
         double3 x[KMAX];
-        float3 sg[KMAX], tg[KMAX], dq[KMAX];
+        V3<float> sg[KMAX], tg[KMAX], dq[KMAX];
         int prim[KMAX], surf[KMAX];
         float Di[KMAX][4], Ub[KMAX][4];
         uint32_t sp_ = failed ? P.s_surf[slot] : P.s_ysurf[slot];
         const double4 *src = failed ? P.s_x : P.s_y;
 #pragma unroll
         for (int j = 0; j < KMAX; j++) {
-            if (j >= k) { x[j] = make_double3(0, 0, 0); sg[j] = tg[j] = dq[j] = f3(0, 0, 0); prim[j] = -1; surf[j] = 0; continue; }
+            if (j >= k) { x[j] = make_double3(0, 0, 0); sg[j] = tg[j] = dq[j] = mk3<float>(0, 0, 0); prim[j] = -1; surf[j] = 0; continue; }
             double4 v = src[(size_t)j * P.S + slot];
             x[j] = make_double3(v.x, v.y, v.z);
             prim[j] = (int)v.w;
             surf[j] = (int)((sp_ >> (4 * j)) & 15u);
-            sg[j] = tg[j] = dq[j] = f3(0, 0, 0);
+            sg[j] = tg[j] = dq[j] = mk3<float>(0, 0, 0);
         }
         int end = -1; // attempt end status
         bool fresh = false;
@@ -446,7 +446,7 @@ __global__ void __launch_bounds__(128) k_wf_update(const DScene S, const SeedCtx
             if (fresh) {
                 c_vtx += k;
                 float cm;
-                int rr = newton_system<KMAX>(S, k, tau, xD, xL, x, prim, surf, P.tol, Di, Ub, sg, tg, dq, singular, cm);
+                int rr = newton_system<KMAX, float>(S, k, tau, xD, xL, x, prim, surf, P.tol, Di, Ub, sg, tg, dq, singular, cm);
                 if (rr == 1) end = ST_CONVERGED;
                 else if (rr == 2) end = ST_DEGENERATE;
                 else {
@@ -481,7 +481,7 @@ __global__ void __launch_bounds__(128) k_wf_update(const DScene S, const SeedCtx
             if (st == ST_CONVERGED) {
                 const DLight &L = S.light[lid];
                 float kap, DL[4];
-                if (!post_sweep<KMAX>(S, L, k, tau, xD, xL, x, prim, surf, true, kap, DL)) st = ST_BAD_SIDE;
+                if (!post_sweep<KMAX, float>(S, L, k, tau, xD, xL, x, prim, surf, true, kap, DL)) st = ST_BAD_SIDE;
                 else {
                     bool vis = true;
                     float3 a = xD;
@@ -499,7 +499,7 @@ __global__ void __launch_bounds__(128) k_wf_update(const DScene S, const SeedCtx
                     }
                     if (!vis) st = ST_OCCLUDED;
                     else {
-                        Gv = singular ? 0.0f : ggt_from_blocks<KMAX>(k, xD, xyz(__ldg(P.nD + w / P.spp)), x, Di, Ub, sg, tg, DL);
+                        Gv = singular ? 0.0f : ggt_from_blocks<KMAX, float>(k, xD, xyz(__ldg(P.nD + w / P.spp)), x, Di, Ub, sg, tg, DL);
                         float Le = L.emit;
                         if (L.kind == 1 && !(dot(f3d(x[k - 1]) - xL, L.n) > 0.0f)) Le = 0.0f;
                         Tv = kap * Gv * Le;
@@ -540,7 +540,7 @@ __global__ void __launch_bounds__(128) k_wf_update(const DScene S, const SeedCtx
         bool same = false;
         if (end == ST_CONVERGED) {
             float kd, DLd[4];
-            if (post_sweep<KMAX>(S, S.light[lid], k, tau, xD, xL, x, prim, surf, false, kd, DLd)) {
+            if (post_sweep<KMAX, float>(S, S.light[lid], k, tau, xD, xL, x, prim, surf, false, kd, DLd)) {
                 same = true;
 #pragma unroll
                 for (int j = 0; j < KMAX; j++) {

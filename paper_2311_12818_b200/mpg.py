@@ -298,7 +298,7 @@ class DeviceScene:
     def opts(self, **over) -> mpg_walk_opts:
         o = self.w.opts
         d = dict(max_iters=o.max_iters, tol=o.tol, beta0=o.beta0, trials=o.trials, k_max=o.k_max,
-                 same_chain_eps=0.0, ray_eps=0.0, flags=0, seed=o.seed, walk_id_base=o.walk_id_base)
+                 same_chain_eps=0.0, ray_eps=0.0, flags=o.flags, seed=o.seed, walk_id_base=o.walk_id_base)
         d.update(over)
         r = mpg_walk_opts()
         for k, v in d.items():

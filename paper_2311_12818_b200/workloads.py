@@ -86,6 +86,10 @@ class WalkOpts:
     ray_eps_rel: float = 1e-4        # x scene extent
     seed: int = 0
     walk_id_base: int = 0
+    flags: int = 0                   # MPG_FLAG_* (4 = MPG_FLAG_NEWTON_F64)
+
+
+FLAG_NEWTON_F64 = 4
 
 
 @dataclasses.dataclass
@@ -373,8 +377,11 @@ def config2(n_side: int = 2048, spp: int = 4, flat: bool = False, grid_n: int = 
                     uv_plane_y=0.0)
     rng = np.random.default_rng(0)
     E = rng.lognormal(0.0, 1.0, size=(16 * 16, 32 * 32)).astype(np.float32)
+    # configs[2] does not fix fp32; its walks start far from the solution (chaotic halving
+    # sequences), so the Newton arithmetic runs in fp64 to meet the 99.9% flag parity (R24)
     return Workload("cfg2_water_pool_k1" + ("_flat" if flat else ""), [water], [light], xD, nD, spp, seed,
-                    WalkOpts(max_iters=20), energies=np.ascontiguousarray(E), recv_shape=(n_side, n_side))
+                    WalkOpts(max_iters=20, flags=FLAG_NEWTON_F64), energies=np.ascontiguousarray(E),
+                    recv_shape=(n_side, n_side))
 
 
 def config3(n_side: int = 1024, spp: int = 1, grid_n: int = 256) -> Workload:
@@ -392,7 +399,8 @@ def config3(n_side: int = 1024, spp: int = 1, grid_n: int = 256) -> Workload:
     rng = np.random.default_rng(0)
     E = rng.dirichlet(np.full(64 * 64, 0.3), size=64).astype(np.float32)
     return Workload("cfg3_glass_slabs_k6", surfs, [light], xD, nD, spp, seed,
-                    WalkOpts(max_iters=40), energies=np.ascontiguousarray(E), recv_shape=(n_side, n_side))
+                    WalkOpts(max_iters=40, flags=FLAG_NEWTON_F64), energies=np.ascontiguousarray(E),
+                    recv_shape=(n_side, n_side))
 
 
 CONFIGS = {0: config0, 1: config1, 2: config2, 3: config3}

@@ -201,3 +201,119 @@ def test_trace_rays_match_oracle():
             mism += prim[i] != po
     assert mism <= 2          # shared-edge ties only (R17)
     ds.close()
+
+
+# ---------------------------------------------------------------------------
+# configs[2] (water heightfield, guided seeds) and configs[3] (k=6 slabs)
+# ---------------------------------------------------------------------------
+@pytest.fixture(scope="module")
+def cfg2_run():
+    w = W.config2(n_side=64, spp=4)          # full 512^2 heightfield, 16,384 walks
+    g, st, ext = PY.run_gpu(w)
+    ids = np.arange(w.n_walks)
+    o, s = PY.run_oracle(w, ids)
+    return w, g, st, ext, o, s, ids
+
+
+def test_cfg2_walk_parity(cfg2_run):
+    w, g, st, ext, o, s, ids = cfg2_run
+    rep = PY.compare(g, o, ids, ext, w.seed.k)
+    _check_walk_parity(rep, w=w, s=s, o=o, ext=ext, max_non_boundary=1)
+    assert rep["G_rel_p99"] < 1e-4
+
+
+def test_cfg2_estimator_tiles(cfg2_run):
+    w, g, st, ext, o, s, ids = cfg2_run
+    mg, sg, n = PY.tile_means(g["w"], w.spp, w.recv_shape, 8)
+    mo, so, _ = PY.tile_means(o["w"], w.spp, w.recv_shape, 8)
+    se = np.sqrt(sg ** 2 / n + so ** 2 / n)
+    z = np.abs(mg - mo) / np.maximum(se, 1e-30)
+    z[(se == 0) & (mg == mo)] = 0
+    assert (z > 3).mean() <= 0.01 and z.max() <= 5
+
+
+def test_cfg3_walk_parity():
+    w = W.config3(n_side=64, spp=1)          # full slabs (780,300 tris), 4,096 k=6 walks
+    g, st, ext = PY.run_gpu(w)
+    ids = np.arange(w.n_walks)
+    o, s = PY.run_oracle(w, ids)
+    rep = PY.compare(g, o, ids, ext, w.seed.k)
+    _check_walk_parity(rep, min_agree=0.997, w=w, s=s, o=o, ext=ext, max_non_boundary=2)
+
+
+def test_cfg2_full_size_sampled():
+    """configs[2] at full size (16,777,216 walks, the bench launch) vs 2,000 sampled oracle walks."""
+    w = W.config2()
+    g, st, ext = PY.run_gpu(w)
+    assert st["walks"] == w.n_walks
+    rng = np.random.default_rng(2)
+    ids = np.sort(rng.choice(w.n_walks, size=2000, replace=False))
+    o, s = PY.run_oracle(w, ids)
+    rep = PY.compare(g, o, ids, ext, w.seed.k)
+    _check_walk_parity(rep, min_agree=0.997, w=w, s=s, o=o, ext=ext, max_non_boundary=1)
+
+
+def _guide_tables_gpu(w, E):
+    import torch
+    from paper_2311_12818_b200 import mpg
+    ds = mpg.DeviceScene(w)
+    ds.upload_energies(E)
+    pf = torch.empty(E.shape, dtype=torch.int64, device="cuda")
+    mpg.mpg_guide_download(ds.guide, None, pf)
+    torch.cuda.synchronize()
+    ds.close()
+    return pf.cpu().numpy().view(np.uint64)
+
+
+@pytest.mark.parametrize("which", ["lognormal", "dirichlet", "with_empty_cells"])
+def test_guide_tables_bit_exact(which):
+    from oracle import oracle as O
+    if which == "lognormal":
+        w = W.config2(4, 1, grid_n=16)
+        E = w.energies
+    elif which == "dirichlet":
+        w = W.config3(4, 1, grid_n=16)
+        E = w.energies
+    else:
+        w = W.config2(4, 1, grid_n=16)
+        E = w.energies.copy()
+        E[::3] = 0.0
+        E[1, ::7] = 0.0
+    got = _guide_tables_gpu(w, E)
+    ref = O.guide_tables(E)
+    assert np.array_equal(got, ref)
+
+
+def test_guide_accumulate_and_rebuild():
+    """a9: histogram += w at (cell(x_D), bin(x_1*)) -- same result as the oracle's
+    accumulation of the same walk outputs (fp32 atomic order: 1e-5 rel), mass
+    conserved; the rebuilt tables are bit-exact with the oracle's tables of that
+    histogram."""
+    import torch
+    from paper_2311_12818_b200 import mpg
+    from oracle import oracle as O
+    w = W.config2(n_side=64, spp=4)
+    ds = mpg.DeviceScene(w)
+    b = mpg.Batch(w.xD, w.nD, w.spp, w.seed.k)
+    opts = ds.opts()
+    mpg.run_step(ds, b, opts, accumulate=True)
+    H = torch.empty(w.energies.shape, dtype=torch.float32, device="cuda")
+    mpg.mpg_guide_download(ds.guide, H, None)
+    torch.cuda.synchronize()
+    hist = H.cpu().numpy()
+    g = b.results()
+    s = O.OracleScene(w)
+    ref = s.accumulate(g["status"], g["w"], g["pos"][:, 0])
+    conv = (g["status"] == 0) & (g["w"] > 0)
+    assert conv.sum() > 100
+    assert hist.sum() == pytest.approx(float(g["w"][conv].astype(np.float64).sum()), rel=1e-5)
+    assert np.allclose(hist, ref, rtol=1e-5, atol=1e-6 * ref.max())
+    # rebuild: tables from the accumulated histogram ("last iteration only")
+    mpg.mpg_guide_rebuild(ds.guide)
+    pf = torch.empty(w.energies.shape, dtype=torch.int64, device="cuda")
+    H2 = torch.empty(w.energies.shape, dtype=torch.float32, device="cuda")
+    mpg.mpg_guide_download(ds.guide, H2, pf)
+    torch.cuda.synchronize()
+    assert np.array_equal(pf.cpu().numpy().view(np.uint64), O.guide_tables(hist))
+    assert float(H2.abs().sum().item()) == 0.0           # histogram cleared for the next iteration
+    ds.close()

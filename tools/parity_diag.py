@@ -6,8 +6,10 @@ from paper_2311_12818_b200 import workloads as W
 from tests import parity as PY
 
 which = sys.argv[1] if len(sys.argv) > 1 else "cfg1"
-w = {"cfg0": lambda: W.config0(), "cfg1": lambda: W.config1(128, 1), "cfg1a": lambda: W.config1(96, 2, analytic=True)}[which]()
-g, st, ext = PY.run_gpu(w)
+w = {"cfg0": lambda: W.config0(), "cfg1": lambda: W.config1(128, 1), "cfg1a": lambda: W.config1(96, 2, analytic=True),
+     "cfg2": lambda: W.config2(64, 4), "cfg3": lambda: W.config3(48, 1)}[which]()
+flags = int(sys.argv[2]) if len(sys.argv) > 2 else w.opts.flags
+g, st, ext = PY.run_gpu(w, flags=flags)
 ids = np.arange(w.n_walks)
 o, s = PY.run_oracle(w, ids)
 rep = PY.compare(g, o, ids, ext, w.seed.k)
@@ -62,7 +64,7 @@ b = mpg.Batch(w.xD, w.nD, w.spp, w.seed.k)
 stride = 2 * (w.opts.max_iters + 2)
 buf = torch.full((w.n_walks, stride), -1.0, device="cuda")
 mpg.mpg_debug_trace(buf, w.n_walks, stride)
-mpg.run_step(ds, b, ds.opts())
+mpg.run_step(ds, b, ds.opts(flags=flags))
 torch.cuda.synchronize()
 mpg.mpg_debug_trace(None)
 tr = buf.cpu().numpy()
