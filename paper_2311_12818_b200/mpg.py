@@ -15,7 +15,7 @@ import numpy as np
 from . import workloads as W
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libmpg.so")
+LIB_PATH = os.environ.get("MPG_LIB", os.path.join(HERE, "libmpg.so"))   # MPG_LIB: experiment variants
 KMAX = 8
 STATUS_NAMES = ["CONVERGED", "MAXITER", "SEED_FAIL", "BAD_SIDE", "DEGENERATE", "OCCLUDED"]
 
