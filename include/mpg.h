@@ -51,7 +51,10 @@ enum { MPG_LIGHT_POINT = 0, MPG_LIGHT_QUAD = 1 };
 enum {
     MPG_SEED_CAP = 0,      /* x_1 uniform by area on the cap of sphere surf_id visible from x_D (init) */
     MPG_SEED_TRIANGLE = 1, /* x_1 uniform in a triangle drawn uniformly among front-facing ones of mesh surf_id */
-    MPG_SEED_GUIDE_UV = 2  /* x_1 target from the guide histogram over surface (u,v), defensive alpha=1/2 (Eq. 13) */
+    MPG_SEED_GUIDE_UV = 2, /* x_1 target from the guide histogram over surface (u,v), defensive alpha=1/2 (Eq. 13) */
+    MPG_SEED_GUIDE_DIR = 3 /* configs[4]: n ~ 1/2 P_0 + 1/2 P_e (Eqs. 10, 13); (w_D, tau) by one-sample MIS of the
+                              initializer (w_D uniform on the hemisphere, tau traced) and the learned
+                              P_e(tau|n) x direction histogram (Eqs. 8, 11); sampler.k = max chain length (<= 6) */
 };
 /* per-walk status; "converged" = CONVERGED or OCCLUDED */
 enum {
@@ -104,6 +107,10 @@ typedef struct {
     float grid_origin[2], grid_extent[2];
     int32_t cells_x, cells_y, bins_x, bins_y;
     float uv_origin[2], uv_scale[2], uv_plane_y;
+    int32_t domain;  /* 0: bins over surface (u,v) (MPG_SEED_GUIDE_UV); 1: typed direction bins
+                        (MPG_SEED_GUIDE_DIR): 126 chain types (n <= 6) x equal-area hemisphere bins
+                        u = cos(theta) about +y (bins_x), v = (phi + pi)/(2 pi) (bins_y) */
+    int32_t n_types; /* 1 (domain 0) or 126 (domain 1) */
 } mpg_guide_desc;
 
 #define MPG_FLAG_WAVEFRONT 1u /* wavefront path (slots + CUDA-graph wave loop) instead of the default
@@ -123,6 +130,8 @@ typedef struct {
     uint32_t flags;        /* MPG_FLAG_* (0 = default persistent kernel)              */
     uint64_t seed;         /* Philox key                                              */
     uint64_t walk_id_base; /* added to the walk index in the Philox counter          */
+    int32_t max_iters_long;/* Newton cap for chains with k >= 3 (0: max_iters)        */
+    int32_t reserved;
 } mpg_walk_opts;
 
 /* Configurations (x_D, x_L): receivers; walk w uses receiver w / spp. */
@@ -137,7 +146,9 @@ typedef struct {
 typedef struct {
     float *xL;       /* float4 [n]: light sample x_L, w = its pdf (area x choice)     */
     float *target;   /* float4 [n]: deduction target (ray x_D -> target gives x_1)   */
-    int32_t *bin;    /* [n]: drawn bin (GUIDE_UV) or triangle (TRIANGLE); -1 none, -2 seed failure */
+    int32_t *bin;    /* [n]: drawn bin (GUIDE_UV/DIR) or triangle (TRIANGLE); -1 none, -2 seed failure */
+    uint32_t *ctype; /* [n]: chain length n (bits 0-3) | tau or initializer bits (4-11) | learned (12) */
+    float *pn;       /* [n]: P(n) of the length mixture (1 for fixed-length samplers) */
 } mpg_seed_buf;
 
 /* Walk outputs; device, length n (chain: kmax planes of n float4). */
@@ -149,6 +160,7 @@ typedef struct {
     float *T;          /* [n] throughput kappa*G*L_o (Eq. 2)                     */
     float *w;          /* [n] weight T*<1/P>/pdf_L (Eqs. 9, 15); 0 if no chain   */
     uint32_t *trials;  /* [n] geometric trial count k (0 if not run)             */
+    uint16_t *ctype;   /* [n] primary chain type: n (bits 0-3) | tau << 4 (bit i: vertex i+1 is T) */
 } mpg_walk_buf;
 
 typedef struct {
@@ -188,7 +200,7 @@ mpg_status mpg_trace_rays(const mpg_scene *scene, const float *orig, const float
 /* Guide (BASELINE.json histogram stand-in for P:424-482, R20). */
 mpg_status mpg_guide_create(const mpg_guide_desc *desc, mpg_guide **out);
 mpg_status mpg_guide_destroy(mpg_guide *guide);
-/* energies: device [cells][bins] float >= 0; builds the defensive integer tables (Eq. 13). */
+/* energies: device [cells][n_types][bins] float >= 0; builds the integer sampling tables (R20/R22). */
 mpg_status mpg_guide_upload(mpg_guide *guide, const float *energy, void *stream);
 /* learned branch absent: uniform tables, histogram zeroed. */
 mpg_status mpg_guide_reset(mpg_guide *guide, void *stream);
@@ -197,8 +209,12 @@ mpg_status mpg_guide_accumulate(mpg_guide *guide, const mpg_query *query, const 
                                 void *stream);
 /* tables <- histogram ("last iteration only", P:426 footnote); histogram zeroed. */
 mpg_status mpg_guide_rebuild(mpg_guide *guide, void *stream);
-/* copies: histogram -> energy (device [cells][bins] float); tables -> prefix (device [cells][bins] u64). */
+/* copies: histogram -> energy (device [cells][n_types][bins] float); tables -> prefix (domain 0:
+ * device [cells][bins] u64).  Either may be NULL. */
 mpg_status mpg_guide_download(const mpg_guide *guide, float *energy, uint64_t *prefix, void *stream);
+/* domain 1 tables: n_prefix [cells][6] u64, type_prefix [cells][126] u64, dir_prefix [cells][126][bins] u32. */
+mpg_status mpg_guide_download_dir_tables(const mpg_guide *guide, uint64_t *n_prefix, uint64_t *type_prefix,
+                                         uint32_t *dir_prefix, void *stream);
 
 /* Light samples + seed targets for the n = n_recv*spp primary walks (trial 0). */
 mpg_status mpg_sample_seeds(const mpg_scene *scene, const mpg_guide *guide, const mpg_sampler_desc *sampler,

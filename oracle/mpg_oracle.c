@@ -62,13 +62,17 @@ typedef struct {
     int32_t cells_x, cells_y, bins_x, bins_y;
     float uv_origin[2], uv_scale[2], uv_plane_y;
     const uint64_t *prefix; /* [cells][bins] inclusive prefix sums of W' (orc_guide_tables) */
+    /* mode 3 (typed direction guide, configs[4]; orc_guide_dir_tables) */
+    const uint64_t *n_prefix;    /* [cells][6] defensive length mixture (Eqs. 10, 13)  */
+    const uint64_t *type_prefix; /* [cells][126] per-length type weights (Eq. 11)      */
+    const uint32_t *dir_prefix;  /* [cells][126][bins] learned direction weights        */
 } orc_seed_cfg;
 
 typedef struct {
     int32_t max_iters;
     int32_t trials;
     uint32_t k_max;
-    int32_t pad;
+    int32_t max_iters_long; /* cap for chains with k >= 3 (0: max_iters) */
     double tol, beta0, same_chain_eps, ray_eps;
     uint64_t seed, walk_id_base;
 } orc_opts;
@@ -86,6 +90,9 @@ typedef struct {
     int32_t bin;
     int64_t total_iters; /* Newton iterations over the primary and all trials */
     int64_t attempts;    /* seed draws (primary + trials) */
+    int32_t k;           /* chain length n of the primary */
+    uint32_t tau;        /* resolved type string of the primary (bit i: vertex i+1 is T) */
+    double Pn;           /* P(n) of the defensive length mixture (1 for fixed-length configs) */
 } orc_walk_out;
 
 /* ------------------------------------------------------------------------ */
@@ -562,7 +569,8 @@ static int newton(const orc_scene *sc, const orc_opts *o, int k, uint32_t tau, v
         if (res_hist) res_hist[it] = nrm;
         if (g_beta_hist) g_beta_hist[it] = beta;
         if (nrm < o->tol) return ST_CONVERGED;
-        if (it == o->max_iters) return ST_MAXITER;
+        int mx = (k >= 3 && o->max_iters_long > 0) ? o->max_iters_long : o->max_iters;
+        if (it == mx) return ST_MAXITER;
         for (int i = 0; i < m; i++) D[i] = -C[i];
         if (!lu_solve(J, m, D, 1)) return ST_DEGENERATE;
         /* proposed points q_i on the geometric tangent planes */
@@ -752,12 +760,39 @@ static void sample_light(const orc_scene *sc, const orc_opts *o, uint64_t walk, 
     }
 }
 
-/* seed target for (walk, trial): returns 0 on failure.  The deduction ray is
- * x_D -> target (Eq. 6, x_1 = r(x_D, w_D)). */
+/* seed draw result: the deduction ray x_D -> tgt gives x_1 (Eq. 6); n = chain
+ * length, tau = type string (learned/fixed) or init_bits (initializer: R/T per
+ * dielectric vertex chosen while tracing), Pn = P(n) of the length mixture. */
+typedef struct { float tgt[3]; int32_t bin; int n; uint32_t tau; int learned; uint32_t init_bits; double Pn; } seed_res;
+
+static const uint32_t P0_INT[6] = {20, 20, 20, 20, 20, 19}; /* P_0(n) = (1,1,1,1,1,0.95)/5.95 [R22] */
+
+static uint64_t mulhi_u64(uint32_t x, uint64_t S) { /* floor(x*S/2^32), exact */
+    uint64_t X = x;
+    return X * (S >> 32) + ((X * (S & 0xffffffffu)) >> 32);
+}
+
+static int guide_cell(const orc_seed_cfg *cfg, const float xD[3]) {
+    int cx = (int)floorf(((xD[0] - cfg->grid_origin[0]) * (float)cfg->cells_x) / cfg->grid_extent[0]);
+    int cz = (int)floorf(((xD[2] - cfg->grid_origin[1]) * (float)cfg->cells_y) / cfg->grid_extent[1]);
+    if (cx < 0) cx = 0;
+    if (cx > cfg->cells_x - 1) cx = cfg->cells_x - 1;
+    if (cz < 0) cz = 0;
+    if (cz > cfg->cells_y - 1) cz = cfg->cells_y - 1;
+    return cz * cfg->cells_x + cx;
+}
+
 static int seed_target(const orc_scene *sc, const orc_seed_cfg *cfg, const orc_opts *o, uint64_t walk, uint32_t trial,
-                       const float xD[3], float tgt[3], int32_t *bin) {
+                       const float xD[3], seed_res *sr) {
     uint32_t r[4];
+    float *tgt = sr->tgt;
+    int32_t *bin = &sr->bin;
     *bin = -1;
+    sr->n = cfg->k;
+    sr->tau = cfg->tau;
+    sr->learned = 1;
+    sr->init_bits = 0;
+    sr->Pn = 1.0;
     if (cfg->mode == 0) { /* uniform on the sphere cap visible from x_D [R21-cfg0] */
         const orc_surface *f = &sc->surf[cfg->surf_id];
         float d[3] = {xD[0] - f->center[0], xD[1] - f->center[1], xD[2] - f->center[2]};
@@ -814,18 +849,11 @@ static int seed_target(const orc_scene *sc, const orc_seed_cfg *cfg, const orc_o
         return 1;
     }
     if (cfg->mode == 2) { /* guided bin over surface (u,v) via integer CDF [R20] */
-        int cx = (int)floorf(((xD[0] - cfg->grid_origin[0]) * (float)cfg->cells_x) / cfg->grid_extent[0]);
-        int cz = (int)floorf(((xD[2] - cfg->grid_origin[1]) * (float)cfg->cells_y) / cfg->grid_extent[1]);
-        if (cx < 0) cx = 0;
-        if (cx > cfg->cells_x - 1) cx = cfg->cells_x - 1;
-        if (cz < 0) cz = 0;
-        if (cz > cfg->cells_y - 1) cz = cfg->cells_y - 1;
         int nb = cfg->bins_x * cfg->bins_y;
-        const uint64_t *pf = cfg->prefix + (size_t)(cz * cfg->cells_x + cx) * nb;
+        const uint64_t *pf = cfg->prefix + (size_t)guide_cell(cfg, xD) * nb;
         uint64_t S = pf[nb - 1];
         draw(o, walk, 1u, trial, r);
-        uint64_t x = r[0];
-        uint64_t t = x * (S >> 32) + ((x * (S & 0xffffffffu)) >> 32); /* floor(x*S/2^32) */
+        uint64_t t = mulhi_u64(r[0], S); /* floor(x*S/2^32) */
         int b = 0;
         while (pf[b] <= t) b++; /* upper_bound: first prefix > t */
         *bin = b;
@@ -838,11 +866,69 @@ static int seed_target(const orc_scene *sc, const orc_seed_cfg *cfg, const orc_o
         tgt[2] = cfg->uv_origin[1] + v * cfg->uv_scale[1];
         return 1;
     }
+    if (cfg->mode == 3) { /* configs[4]: n ~ 1/2 P_0 + 1/2 P_e (Eqs. 10, 13), then one-sample MIS
+                             of the initializer and the learned (tau, w_D) (Eqs. 8, 11, 13) [R22] */
+        int c = guide_cell(cfg, xD);
+        const uint64_t *npf = cfg->n_prefix + (size_t)c * 6;
+        draw(o, walk, 1u, 0u, r); /* n reused by every trial */
+        uint64_t S = npf[5];
+        uint64_t t = mulhi_u64(r[0], S);
+        int n = 0;
+        while (npf[n] <= t) n++;
+        sr->n = n + 1;
+        sr->Pn = (double)(npf[n] - (n > 0 ? npf[n - 1] : 0)) / (double)S;
+        draw(o, walk, 1u, trial, r);
+        int g0 = (1 << sr->n) - 2, gn = 1 << sr->n;
+        const uint64_t *tpf = cfg->type_prefix + (size_t)c * 126 + g0;
+        uint64_t Wg = tpf[gn - 1];
+        float u, v;
+        if (Wg > 0 && (r[1] >> 31)) {
+            uint64_t tt = mulhi_u64(r[2], Wg);
+            int m = 0;
+            while (tpf[m] <= tt) m++;
+            sr->tau = (uint32_t)m;
+            sr->learned = 1;
+            int nb = cfg->bins_x * cfg->bins_y;
+            const uint32_t *dpf = cfg->dir_prefix + ((size_t)c * 126 + g0 + m) * nb;
+            uint64_t Sd = dpf[nb - 1];
+            uint64_t td = mulhi_u64(r[3], Sd);
+            int b = 0;
+            while (dpf[b] <= td) b++;
+            *bin = b;
+            uint32_t r2[4];
+            draw(o, walk, 2u, trial, r2);
+            u = ((float)(b % cfg->bins_x) + u01(r2[0])) / (float)cfg->bins_x;
+            v = ((float)(b / cfg->bins_x) + u01(r2[1])) / (float)cfg->bins_y;
+        } else {
+            uint32_t r3[4];
+            draw(o, walk, 3u, trial, r3);
+            u = u01(r3[0]);
+            v = u01(r3[1]);
+            sr->learned = 0;
+            sr->tau = 0;
+            sr->init_bits = r3[2];
+        }
+        /* equal-area hemisphere about +y: u = cos(theta), v = (phi + pi)/(2 pi) */
+        float st2 = 1.0f - u * u;
+        float st = sqrtf(st2 > 0.0f ? st2 : 0.0f);
+        float phi = 6.28318530717958647692f * v - 3.14159265358979323846f;
+        float cp = cosf(phi), sp = sinf(phi);
+        tgt[0] = xD[0] + st * cp;
+        tgt[1] = xD[1] + u;
+        tgt[2] = xD[2] + st * sp;
+        return 1;
+    }
     return 0;
 }
 
-/* deduction recursion Eq. 6 with s_R / s_T by tau [R14] */
-static int deduce(const orc_scene *sc, int k, uint32_t tau, v3 xD, v3 target, double eps, cvtx *x) {
+
+/* deduction recursion Eq. 6 with s_R / s_T by tau [R14].
+ * learned = 0 (initializer, "generated by ray tracing, deciding the
+ * scattering type"): vertex i on a dielectric takes bit i of tau as T/R, a
+ * conductor always R; the resolved string is returned in *tau_out [R22]. */
+static int deduce_ex(const orc_scene *sc, int k, uint32_t tau, int learned, v3 xD, v3 target, double eps, cvtx *x,
+                     uint32_t *tau_out) {
+    uint32_t res = 0;
     v3 d = sub(target, xD);
     double dl = len(d);
     if (!(dl > 0.0)) return 0;
@@ -852,6 +938,10 @@ static int deduce(const orc_scene *sc, int k, uint32_t tau, v3 xD, v3 target, do
         hit_t h = closest(sc, o, d, eps, 1e300, 1, 1);
         if (h.surf < 0) return 0;
         x[i].p = h.p; x[i].prim = h.prim; x[i].surf = h.surf;
+        uint32_t bit = (tau >> i) & 1u;
+        if (!learned && sc->surf[h.surf].mat == 0) bit = 0u;
+        if (bit && sc->surf[h.surf].mat != 1) return 0; /* T on a conductor */
+        res |= bit << i;
         if (i < k - 1) {
             const orc_surface *f = &sc->surf[h.surf];
             v3 ng = geo_normal(sc, &x[i]);
@@ -861,10 +951,9 @@ static int deduce(const orc_scene *sc, int k, uint32_t tau, v3 xD, v3 target, do
             if (dot(d, n) > 0.0) n = mul(n, -1.0);
             double ci = -dot(d, n);
             if (!(ci > 0.0)) return 0;
-            if (!((tau >> i) & 1u)) {
+            if (!bit) {
                 d = add(d, mul(n, 2.0 * ci));
             } else {
-                if (f->mat != 1) return 0;
                 double e1 = outside ? f->eta_out : f->eta_in, e2 = outside ? f->eta_in : f->eta_out;
                 double eta = e1 / e2;
                 double k2 = 1.0 - eta * eta * (1.0 - ci * ci);
@@ -874,7 +963,13 @@ static int deduce(const orc_scene *sc, int k, uint32_t tau, v3 xD, v3 target, do
         }
         o = h.p;
     }
+    *tau_out = res;
     return 1;
+}
+
+static int deduce(const orc_scene *sc, int k, uint32_t tau, v3 xD, v3 target, double eps, cvtx *x) {
+    uint32_t t2;
+    return deduce_ex(sc, k, tau, 1, xD, target, eps, x, &t2);
 }
 
 static int same_chain(int k, const cvtx *a, const cvtx *b, double eps) {
@@ -888,16 +983,20 @@ static int same_chain(int k, const cvtx *a, const cvtx *b, double eps) {
 static double eps_ray(const orc_scene *sc, const orc_opts *o) { return o->ray_eps > 0.0 ? o->ray_eps : 1e-4 * sc->extent; }
 static double eps_same(const orc_scene *sc, const orc_opts *o) { return o->same_chain_eps > 0.0 ? o->same_chain_eps : 1e-4 * sc->extent; }
 
-/* one attempt: seed -> deduce -> Newton -> sides (O4-O7) */
+/* one attempt: seed -> deduce -> Newton -> sides (O4-O7); *k, *tau: the chain type */
 static int attempt(const orc_scene *sc, const orc_seed_cfg *cfg, const orc_opts *o, uint64_t walk, uint32_t trial,
-                   const float xD[3], v3 xL, cvtx *x, int *iters, float tgt[3], int32_t *bin) {
+                   const float xD[3], v3 xL, cvtx *x, int *iters, seed_res *sr, int *k, uint32_t *tau) {
     *iters = 0;
-    if (!seed_target(sc, cfg, o, walk, trial, xD, tgt, bin)) return ST_SEED_FAIL;
+    *k = cfg->k;
+    *tau = cfg->tau;
+    if (!seed_target(sc, cfg, o, walk, trial, xD, sr)) return ST_SEED_FAIL;
+    *k = sr->n;
     v3 xd = vf(xD);
     double eps = eps_ray(sc, o);
-    if (!deduce(sc, cfg->k, cfg->tau, xd, vf(tgt), eps, x)) return ST_SEED_FAIL;
-    int st = newton(sc, o, cfg->k, cfg->tau, xd, xL, x, iters, eps, NULL);
-    if (st == ST_CONVERGED && !sides_ok(sc, cfg->k, cfg->tau, xd, xL, x)) st = ST_BAD_SIDE;
+    if (!deduce_ex(sc, sr->n, sr->learned ? sr->tau : sr->init_bits, sr->learned, xd, vf(sr->tgt), eps, x, tau))
+        return ST_SEED_FAIL;
+    int st = newton(sc, o, *k, *tau, xd, xL, x, iters, eps, NULL);
+    if (st == ST_CONVERGED && !sides_ok(sc, *k, *tau, xd, xL, x)) st = ST_BAD_SIDE;
     return st;
 }
 
@@ -937,15 +1036,22 @@ int orc_walks(const void *h, const orc_seed_cfg *cfg, const orc_opts *o, const f
         v3 xL = vf(xLf);
         r->xL[0] = xL.x; r->xL[1] = xL.y; r->xL[2] = xL.z;
         cvtx x[KMAX];
-        int iters;
-        int st = attempt(sc, cfg, o, wid, 0u, xd, xL, x, &iters, r->target, &r->bin);
+        int iters, k;
+        uint32_t tau;
+        seed_res sr;
+        int st = attempt(sc, cfg, o, wid, 0u, xd, xL, x, &iters, &sr, &k, &tau);
+        memcpy(r->target, sr.tgt, sizeof(sr.tgt));
+        r->bin = sr.bin;
+        r->k = k;
+        r->tau = tau;
+        r->Pn = sr.Pn;
         r->attempts = 1;
         r->iters = iters;
         r->total_iters = iters;
-        if (st == ST_CONVERGED) st = finish(sc, o, cfg->k, cfg->tau, vf(xd), vf(nd), xL, &sc->light[lid], x, &r->G, &r->T, &r->kappa);
+        if (st == ST_CONVERGED) st = finish(sc, o, k, tau, vf(xd), vf(nd), xL, &sc->light[lid], x, &r->G, &r->T, &r->kappa);
         r->status = st;
         if (st == ST_CONVERGED || st == ST_OCCLUDED || st == ST_BAD_SIDE || st == ST_MAXITER || st == ST_DEGENERATE) {
-            for (int i = 0; i < cfg->k; i++) {
+            for (int i = 0; i < k; i++) {
                 r->pos[i][0] = x[i].p.x; r->pos[i][1] = x[i].p.y; r->pos[i][2] = x[i].p.z;
                 r->prim[i] = x[i].prim; r->surf[i] = x[i].surf;
             }
@@ -955,17 +1061,17 @@ int orc_walks(const void *h, const orc_seed_cfg *cfg, const orc_opts *o, const f
             double es = eps_same(sc, o);
             for (uint32_t t = 1; t <= o->k_max; t++) {
                 cvtx y[KMAX];
-                int it2;
-                float tg[3];
-                int32_t b2;
-                int s2 = attempt(sc, cfg, o, wid, t, xd, xL, y, &it2, tg, &b2);
+                int it2, k2;
+                uint32_t tau2;
+                seed_res s2r;
+                int s2 = attempt(sc, cfg, o, wid, t, xd, xL, y, &it2, &s2r, &k2, &tau2);
                 r->attempts++;
                 r->total_iters += it2;
-                if (s2 == ST_CONVERGED && same_chain(cfg->k, y, x, es)) { kk = t; break; }
+                if (s2 == ST_CONVERGED && k2 == k && tau2 == tau && same_chain(k, y, x, es)) { kk = t; break; }
             }
             if (kk == 0) { kk = o->k_max; r->truncated = 1; }
             r->trials = kk;
-            r->w = r->T * (double)kk / (1.0 * r->pdfL);
+            r->w = r->T * (double)kk / (r->Pn * r->pdfL); /* Eq. 15: w = T k / (P(n) pdf_L) */
         }
     }
     return 0;
@@ -1074,7 +1180,23 @@ int orc_seed(const void *h, const orc_seed_cfg *cfg, const orc_opts *o, const fl
     int lid;
     uint64_t wid = o->walk_id_base + (uint64_t)walk;
     sample_light(sc, o, wid, xL, pdfL, &lid);
-    return seed_target(sc, cfg, o, wid, trial, xD + 3 * (walk / spp), tgt, bin);
+    seed_res sr;
+    int ok = seed_target(sc, cfg, o, wid, trial, xD + 3 * (walk / spp), &sr);
+    memcpy(tgt, sr.tgt, sizeof(sr.tgt));
+    *bin = sr.bin;
+    return ok;
+}
+
+/* full seed draw (configs[4] tests): n, tau/init bits, learned flag, P(n) */
+int orc_seed_ex(const void *h, const orc_seed_cfg *cfg, const orc_opts *o, const float *xD, int32_t spp, int64_t walk,
+                uint32_t trial, float tgt[3], int32_t *bin, int32_t *n, uint32_t *tau, int32_t *learned,
+                uint32_t *init_bits, double *Pn) {
+    const orc_scene *sc = (const orc_scene *)h;
+    seed_res sr;
+    int ok = seed_target(sc, cfg, o, o->walk_id_base + (uint64_t)walk, trial, xD + 3 * (walk / spp), &sr);
+    memcpy(tgt, sr.tgt, sizeof(sr.tgt));
+    *bin = sr.bin; *n = sr.n; *tau = sr.tau; *learned = sr.learned; *init_bits = sr.init_bits; *Pn = sr.Pn;
+    return ok;
 }
 
 /* reflect / refract with the deduction's conventions (d along propagation) */
@@ -1143,5 +1265,98 @@ void orc_accumulate(const orc_seed_cfg *cfg, const float *xD, int32_t spp, int64
         if (by < 0) by = 0;
         if (by > cfg->bins_y - 1) by = cfg->bins_y - 1;
         hist[(size_t)(cz * cfg->cells_x + cx) * nb + by * cfg->bins_x + bx] += w[i];
+    }
+}
+
+/* configs[4] guide tables from a typed direction histogram hist[cells][126][nb]
+ * (R22): per (cell, type) energy E = sum of bins (fp64, bin order); per length
+ * E_n = sum of its types (type order); W_n = E_n>0 ? max(1, floor(E_n/E_max 2^20)) : 0,
+ * n_prefix = cumsum(c_n sum W + 119 W_n) (= 1/2 P_0 + 1/2 P_e, Eqs. 10, 13; empty
+ * cell -> c_n); type weights per length group likewise from E_tau (Eq. 11);
+ * direction weights per (cell, type) as R20 (fp32) but learned only. */
+void orc_guide_dir_tables(const float *hist, int n_cells, int nb, uint64_t *n_prefix, uint64_t *type_prefix,
+                          uint32_t *dir_prefix) {
+    double *E = (double *)malloc(sizeof(double) * 126);
+    for (int c = 0; c < n_cells; c++) {
+        for (int t = 0; t < 126; t++) {
+            const float *h = hist + ((size_t)c * 126 + t) * nb;
+            double e = 0.0;
+            float hmax = 0.0f;
+            for (int b = 0; b < nb; b++) { e += (double)h[b]; if (h[b] > hmax) hmax = h[b]; }
+            E[t] = e;
+            uint32_t acc = 0;
+            uint32_t *dp = dir_prefix + ((size_t)c * 126 + t) * nb;
+            for (int b = 0; b < nb; b++) {
+                uint32_t wb = 0;
+                if (h[b] > 0.0f && hmax > 0.0f) {
+                    float q = floorf((h[b] / hmax) * 1048576.0f);
+                    wb = (uint32_t)q;
+                    if (wb < 1u) wb = 1u;
+                }
+                acc += wb;
+                dp[b] = acc;
+            }
+        }
+        double En[6], emax = 0.0;
+        for (int n = 1; n <= 6; n++) {
+            double e = 0.0;
+            for (int m = 0; m < (1 << n); m++) e += E[(1 << n) - 2 + m];
+            En[n - 1] = e;
+            if (e > emax) emax = e;
+        }
+        uint64_t Wn[6], sumW = 0;
+        for (int n = 0; n < 6; n++) {
+            uint64_t w = 0;
+            if (En[n] > 0.0 && emax > 0.0) {
+                w = (uint64_t)floor((En[n] / emax) * 1048576.0);
+                if (w < 1u) w = 1u;
+            }
+            Wn[n] = w;
+            sumW += w;
+        }
+        uint64_t acc = 0;
+        for (int n = 0; n < 6; n++) {
+            acc += sumW == 0 ? P0_INT[n] : P0_INT[n] * sumW + 119u * Wn[n];
+            n_prefix[(size_t)c * 6 + n] = acc;
+        }
+        for (int n = 1; n <= 6; n++) {
+            int g0 = (1 << n) - 2, gn = 1 << n;
+            double gmax = 0.0;
+            for (int m = 0; m < gn; m++) if (E[g0 + m] > gmax) gmax = E[g0 + m];
+            uint64_t a2 = 0;
+            for (int m = 0; m < gn; m++) {
+                uint64_t w = 0;
+                if (E[g0 + m] > 0.0 && gmax > 0.0) {
+                    w = (uint64_t)floor((E[g0 + m] / gmax) * 1048576.0);
+                    if (w < 1u) w = 1u;
+                }
+                a2 += w;
+                type_prefix[(size_t)c * 126 + g0 + m] = a2;
+            }
+        }
+    }
+    free(E);
+}
+
+/* configs[4] accumulation: hist[cell(x_D)][type(n, tau)][bin(w_D*)] += w, bins of the
+ * equal-area map u = cos(theta) (about +y), v = (atan2(w_z, w_x) + pi)/(2 pi) */
+void orc_accumulate_dir(const orc_seed_cfg *cfg, const float *xD, int32_t spp, int64_t n, const int32_t *status,
+                        const float *w, const float *x1, const int32_t *k, const uint32_t *tau, double *hist) {
+    int nb = cfg->bins_x * cfg->bins_y;
+    for (int64_t i = 0; i < n; i++) {
+        if (status[i] != ST_CONVERGED || !(w[i] > 0.0f) || k[i] < 1 || k[i] > 6) continue;
+        const float *xd = xD + 3 * (i / spp);
+        int c = guide_cell(cfg, xd);
+        float dx = x1[3 * i] - xd[0], dy = x1[3 * i + 1] - xd[1], dz = x1[3 * i + 2] - xd[2];
+        float l = sqrtf(dx * dx + dy * dy + dz * dz);
+        float u = dy / l;
+        float v = (atan2f(dz, dx) + 3.14159265358979323846f) / 6.28318530717958647692f;
+        int bu = (int)floorf(u * (float)cfg->bins_x), bv = (int)floorf(v * (float)cfg->bins_y);
+        if (bu < 0) bu = 0;
+        if (bu > cfg->bins_x - 1) bu = cfg->bins_x - 1;
+        if (bv < 0) bv = 0;
+        if (bv > cfg->bins_y - 1) bv = cfg->bins_y - 1;
+        int type = (1 << k[i]) - 2 + (int)tau[i];
+        hist[((size_t)c * 126 + type) * nb + bv * cfg->bins_x + bu] += w[i];
     }
 }

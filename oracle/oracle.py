@@ -46,11 +46,12 @@ class SeedCfg(C.Structure):
     _fields_ = [("mode", C.c_int32), ("surf_id", C.c_int32), ("k", C.c_int32), ("tau", C.c_uint32),
                 ("grid_origin", C.c_float * 2), ("grid_extent", C.c_float * 2), ("cells_x", C.c_int32),
                 ("cells_y", C.c_int32), ("bins_x", C.c_int32), ("bins_y", C.c_int32), ("uv_origin", C.c_float * 2),
-                ("uv_scale", C.c_float * 2), ("uv_plane_y", C.c_float), ("prefix", C.POINTER(C.c_uint64))]
+                ("uv_scale", C.c_float * 2), ("uv_plane_y", C.c_float), ("prefix", C.POINTER(C.c_uint64)),
+                ("n_prefix", C.c_void_p), ("type_prefix", C.c_void_p), ("dir_prefix", C.c_void_p)]
 
 
 class Opts(C.Structure):
-    _fields_ = [("max_iters", C.c_int32), ("trials", C.c_int32), ("k_max", C.c_uint32), ("pad", C.c_int32),
+    _fields_ = [("max_iters", C.c_int32), ("trials", C.c_int32), ("k_max", C.c_uint32), ("max_iters_long", C.c_int32),
                 ("tol", C.c_double), ("beta0", C.c_double), ("same_chain_eps", C.c_double), ("ray_eps", C.c_double),
                 ("seed", C.c_uint64), ("walk_id_base", C.c_uint64)]
 
@@ -60,7 +61,8 @@ class WalkOut(C.Structure):
                 ("G", C.c_double), ("T", C.c_double), ("kappa", C.c_double), ("w", C.c_double),
                 ("pos", (C.c_double * 3) * KMAX), ("prim", C.c_int32 * KMAX), ("surf", C.c_int32 * KMAX),
                 ("xL", C.c_double * 3), ("pdfL", C.c_double), ("target", C.c_float * 3), ("bin", C.c_int32),
-                ("total_iters", C.c_int64), ("attempts", C.c_int64)]
+                ("total_iters", C.c_int64), ("attempts", C.c_int64), ("k", C.c_int32), ("tau", C.c_uint32),
+                ("Pn", C.c_double)]
 
 
 _lib = None
@@ -108,6 +110,11 @@ def lib():
         _lib.orc_walk_trace.argtypes = [P, C.POINTER(Opts), C.c_int, C.c_uint32, dp, dp, dp, dp, dp,
                                         C.POINTER(C.c_int32)]
         _lib.orc_accumulate.argtypes = [C.POINTER(SeedCfg), P, C.c_int32, C.c_int64, P, P, P, P]
+        _lib.orc_seed_ex.restype = C.c_int
+        _lib.orc_seed_ex.argtypes = [P, C.POINTER(SeedCfg), C.POINTER(Opts), P, C.c_int32, C.c_int64, C.c_uint32,
+                                     P, P, P, P, P, P, P]
+        _lib.orc_guide_dir_tables.argtypes = [P, C.c_int, C.c_int, P, P, P]
+        _lib.orc_accumulate_dir.argtypes = [C.POINTER(SeedCfg), P, C.c_int32, C.c_int64, P, P, P, P, P, P]
         _lib.orc_tangent_basis.argtypes = [P, C.c_int32, C.c_int32, dp, dp, dp]
         _lib.orc_scatter.restype = C.c_int
         _lib.orc_scatter.argtypes = [C.c_int, C.c_double, C.c_double, dp, dp, dp]
@@ -150,10 +157,23 @@ def guide_tables(E: np.ndarray) -> np.ndarray:
     return prefix
 
 
+def guide_dir_tables(H: np.ndarray):
+    """configs[4] tables from a typed direction histogram H [cells, 126, bins]."""
+    H = np.ascontiguousarray(H, np.float32)
+    nc, nt, nb = H.shape
+    assert nt == 126
+    npf = np.zeros((nc, 6), np.uint64)
+    tpf = np.zeros((nc, 126), np.uint64)
+    dpf = np.zeros((nc, 126, nb), np.uint32)
+    lib().orc_guide_dir_tables(_ptr(H), nc, nb, _ptr(npf), _ptr(tpf), _ptr(dpf))
+    return npf, tpf, dpf
+
+
 def make_opts(w, **over) -> Opts:
     o = w.opts
     d = dict(max_iters=o.max_iters, trials=o.trials, k_max=o.k_max, tol=o.tol, beta0=o.beta0, seed=o.seed,
-             walk_id_base=o.walk_id_base, same_chain_eps=0.0, ray_eps=0.0)
+             walk_id_base=o.walk_id_base, same_chain_eps=0.0, ray_eps=0.0,
+             max_iters_long=getattr(o, "max_iters_long", 0))
     d.update(over)
     r = Opts()
     for k, v in d.items():
@@ -207,9 +227,19 @@ class OracleScene:
         c.uv_origin[:] = list(s.uv_origin)
         c.uv_scale[:] = list(s.uv_scale)
         c.uv_plane_y = s.uv_plane_y
-        if self.w.energies is not None:
+        if s.mode == 3:
+            nb = s.bins_x * s.bins_y
+            self.set_dir_hist(np.zeros((s.cells_x * s.cells_y, 126, nb), np.float32), c)
+        elif self.w.energies is not None:
             self.set_energies(self.w.energies, c)
         return c
+
+    def set_dir_hist(self, H, c=None):
+        """configs[4]: build the typed tables from histogram H [cells,126,bins] (zeros = reset)."""
+        c = c or self.cfg
+        self.dir_tables = guide_dir_tables(H)
+        npf, tpf, dpf = self.dir_tables
+        c.n_prefix, c.type_prefix, c.dir_prefix = _ptr(npf), _ptr(tpf), _ptr(dpf)
 
     def set_energies(self, E, c=None):
         c = c or self.cfg
@@ -311,6 +341,29 @@ class OracleScene:
                              _ptr(x1), _ptr(hist))
         return hist
 
+    def seed_ex(self, walk, trial=0, opts=None):
+        opts = opts or self.opts()
+        tgt = np.zeros(3, np.float32)
+        b, n, learned = (np.zeros(1, np.int32) for _ in range(3))
+        tau, ib = np.zeros(1, np.uint32), np.zeros(1, np.uint32)
+        pn = np.zeros(1, np.float64)
+        ok = lib().orc_seed_ex(self.h, C.byref(self.cfg), C.byref(opts), _ptr(self.w.xD), self.w.spp, int(walk),
+                               int(trial), _ptr(tgt), _ptr(b), _ptr(n), _ptr(tau), _ptr(learned), _ptr(ib), _ptr(pn))
+        return dict(ok=ok, target=tgt, bin=int(b[0]), n=int(n[0]), tau=int(tau[0]), learned=int(learned[0]),
+                    init_bits=int(ib[0]), Pn=float(pn[0]))
+
+    def accumulate_dir(self, status, w, x1, k, tau):
+        sp = self.w.seed
+        hist = np.zeros((sp.cells_x * sp.cells_y, 126, sp.bins_x * sp.bins_y), np.float64)
+        st = np.ascontiguousarray(status, np.int32)
+        wv = np.ascontiguousarray(w, np.float32)
+        x1 = np.ascontiguousarray(x1, np.float32)
+        kk = np.ascontiguousarray(k, np.int32)
+        tt = np.ascontiguousarray(tau, np.uint32)
+        lib().orc_accumulate_dir(C.byref(self.cfg), _ptr(self.w.xD), self.w.spp, st.shape[0], _ptr(st), _ptr(wv),
+                                 _ptr(x1), _ptr(kk), _ptr(tt), _ptr(hist))
+        return hist
+
     def tangent_basis(self, prim, surf, p):
         a = (C.c_double * 3)()
         b = (C.c_double * 3)()
@@ -340,4 +393,5 @@ def _np_walkout():
                      ("G", np.float64), ("T", np.float64), ("kappa", np.float64), ("w", np.float64),
                      ("pos", np.float64, (KMAX, 3)), ("prim", np.int32, (KMAX,)), ("surf", np.int32, (KMAX,)),
                      ("xL", np.float64, (3,)), ("pdfL", np.float64), ("target", np.float32, (3,)), ("bin", np.int32),
-                     ("total_iters", np.int64), ("attempts", np.int64)])
+                     ("total_iters", np.int64), ("attempts", np.int64), ("k", np.int32), ("tau", np.uint32),
+                     ("Pn", np.float64)])

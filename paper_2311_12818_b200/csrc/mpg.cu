@@ -51,9 +51,14 @@ struct mpg_scene {
 
 struct mpg_guide {
     mpg_guide_desc desc;
-    int n_cells = 0, n_bins = 0;
-    uint64_t *prefix = nullptr;
-    float *hist = nullptr;
+    int n_cells = 0, n_bins = 0, n_types = 1;
+    uint64_t *prefix = nullptr;   // domain 0: [cells][bins]
+    float *hist = nullptr;        // [cells][types][bins]
+    // domain 1 (typed directions, R22)
+    uint64_t *n_prefix = nullptr; // [cells][6]
+    uint64_t *type_prefix = nullptr; // [cells][126]
+    uint32_t *dir_prefix = nullptr;  // [cells][126][bins]
+    double *type_energy = nullptr;   // scratch [cells][126]
     bool ready = false;
 };
 
@@ -520,15 +525,26 @@ extern "C" mpg_status mpg_guide_create(const mpg_guide_desc *desc, mpg_guide **o
     ARG_CHECK(desc->grid_extent[0] > 0.f && desc->grid_extent[1] > 0.f && desc->uv_scale[0] != 0.f &&
                   desc->uv_scale[1] != 0.f, "bad guide extents");
     ARG_CHECK((int64_t)desc->bins_x * desc->bins_y <= 65536, "at most 65536 bins per cell");
+    ARG_CHECK(desc->domain == 0 || desc->domain == 1, "guide domain must be 0 (uv) or 1 (typed directions)");
+    ARG_CHECK(desc->domain == 0 || desc->n_types == 126, "typed direction guide needs n_types = 126 (n <= 6)");
     mpg_guide *g = new mpg_guide();
     g->desc = *desc;
     g->n_cells = desc->cells_x * desc->cells_y;
     g->n_bins = desc->bins_x * desc->bins_y;
-    size_t ne = (size_t)g->n_cells * g->n_bins;
-    cudaError_t e1 = cudaMalloc(&g->prefix, ne * sizeof(uint64_t));
-    cudaError_t e2 = cudaMalloc(&g->hist, ne * sizeof(float));
-    if (e1 != cudaSuccess || e2 != cudaSuccess) {
-        cudaFree(g->prefix); cudaFree(g->hist); delete g;
+    g->n_types = desc->domain == 1 ? 126 : 1;
+    size_t ne = (size_t)g->n_cells * g->n_types * g->n_bins;
+    cudaError_t e = cudaMalloc(&g->hist, ne * sizeof(float));
+    if (e == cudaSuccess) {
+        if (desc->domain == 0) e = cudaMalloc(&g->prefix, ne * sizeof(uint64_t));
+        else {
+            e = cudaMalloc(&g->n_prefix, (size_t)g->n_cells * 6 * sizeof(uint64_t));
+            if (e == cudaSuccess) e = cudaMalloc(&g->type_prefix, (size_t)g->n_cells * 126 * sizeof(uint64_t));
+            if (e == cudaSuccess) e = cudaMalloc(&g->dir_prefix, ne * sizeof(uint32_t));
+            if (e == cudaSuccess) e = cudaMalloc(&g->type_energy, (size_t)g->n_cells * 126 * sizeof(double));
+        }
+    }
+    if (e != cudaSuccess) {
+        mpg_guide_destroy(g);
         return fail(MPG_ERR_OOM, "guide allocation failed");
     }
     *out = g;
@@ -539,23 +555,163 @@ extern "C" mpg_status mpg_guide_destroy(mpg_guide *g) {
     if (!g) return MPG_OK;
     cudaFree(g->prefix);
     cudaFree(g->hist);
+    cudaFree(g->n_prefix);
+    cudaFree(g->type_prefix);
+    cudaFree(g->dir_prefix);
+    cudaFree(g->type_energy);
     delete g;
     return MPG_OK;
 }
 
+// ---- typed direction guide (configs[4], R22): tables from hist[cells][126][bins] ----
+// (1) one thread per (cell, type): E = sum of bins in fp64 (bin order), learned
+//     direction weights (R20 quantization, learned only) and their u32 prefix.
+__global__ void k_dir_type_tables(const float *hist, int n_cells, int nb, double *E, uint32_t *dir_prefix) {
+    int id = blockIdx.x * blockDim.x + threadIdx.x;
+    if (id >= n_cells * 126) return;
+    const float *h = hist + (size_t)id * nb;
+    double e = 0.0;
+    float hmax = 0.0f;
+    for (int b = 0; b < nb; b++) {
+        float v = h[b];
+        e += (double)v;
+        hmax = fmaxf(hmax, v);
+    }
+    E[id] = e;
+    uint32_t acc = 0;
+    uint32_t *dp = dir_prefix + (size_t)id * nb;
+    for (int b = 0; b < nb; b++) {
+        uint32_t wb = 0;
+        float v = h[b];
+        if (v > 0.0f && hmax > 0.0f) {
+            wb = (uint32_t)floorf(__fmul_rn(__fdiv_rn(v, hmax), 1048576.0f));
+            if (wb < 1u) wb = 1u;
+        }
+        acc += wb;
+        dp[b] = acc;
+    }
+}
+// (2) one thread per cell: length mixture (Eqs. 10, 13) and per-length type tables (Eq. 11)
+__global__ void k_dir_cell_tables(const double *E, int n_cells, uint64_t *n_prefix, uint64_t *type_prefix) {
+    int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= n_cells) return;
+    const double *e = E + (size_t)c * 126;
+    const uint32_t P0[6] = {20, 20, 20, 20, 20, 19};
+    double En[6], emax = 0.0;
+    for (int n = 1; n <= 6; n++) {
+        double s = 0.0;
+        for (int m = 0; m < (1 << n); m++) s += e[(1 << n) - 2 + m];
+        En[n - 1] = s;
+        emax = fmax(emax, s);
+    }
+    uint64_t Wn[6], sumW = 0;
+    for (int n = 0; n < 6; n++) {
+        uint64_t w = 0;
+        if (En[n] > 0.0 && emax > 0.0) {
+            w = (uint64_t)floor(__dmul_rn(__ddiv_rn(En[n], emax), 1048576.0));
+            if (w < 1u) w = 1u;
+        }
+        Wn[n] = w;
+        sumW += w;
+    }
+    uint64_t acc = 0;
+    for (int n = 0; n < 6; n++) {
+        acc += sumW == 0 ? (uint64_t)P0[n] : (uint64_t)P0[n] * sumW + 119ull * Wn[n];
+        n_prefix[(size_t)c * 6 + n] = acc;
+    }
+    for (int n = 1; n <= 6; n++) {
+        int g0 = (1 << n) - 2, gn = 1 << n;
+        double gmax = 0.0;
+        for (int m = 0; m < gn; m++) gmax = fmax(gmax, e[g0 + m]);
+        uint64_t a2 = 0;
+        for (int m = 0; m < gn; m++) {
+            uint64_t w = 0;
+            if (e[g0 + m] > 0.0 && gmax > 0.0) {
+                w = (uint64_t)floor(__dmul_rn(__ddiv_rn(e[g0 + m], gmax), 1048576.0));
+                if (w < 1u) w = 1u;
+            }
+            a2 += w;
+            type_prefix[(size_t)c * 126 + g0 + m] = a2;
+        }
+    }
+}
+
+static mpg_status build_dir_tables(mpg_guide *g, const float *hist, cudaStream_t st) {
+    int nt = g->n_cells * 126;
+    k_dir_type_tables<<<(nt + 127) / 128, 128, 0, st>>>(hist, g->n_cells, g->n_bins, g->type_energy, g->dir_prefix);
+    CUDA_TRY(cudaPeekAtLastError());
+    k_dir_cell_tables<<<(g->n_cells + 127) / 128, 128, 0, st>>>(g->type_energy, g->n_cells, g->n_prefix,
+                                                                 g->type_prefix);
+    CUDA_TRY(cudaPeekAtLastError());
+    return MPG_OK;
+}
+
+// accumulate for the typed direction guide: hist[cell(x_D)][type(n,tau)][bin(w_D*)] += w (Eq. 9)
+__global__ void k_accumulate_dir(const mpg_guide_desc g, const float4 *xD, int spp, int64_t n, const float4 *chain0,
+                                 const uint8_t *status, const float *w, const uint16_t *ctype, float *hist) {
+    const int nb = g.bins_x * g.bins_y;
+    const int lane = threadIdx.x & 31;
+    for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < n; base += (int64_t)gridDim.x * blockDim.x) {
+        int64_t i = base + threadIdx.x;
+        long long key = -1;
+        float val = 0.f;
+        if (i < n && status[i] == 0 && w[i] > 0.f) {
+            uint32_t ct = ctype[i];
+            int kk = (int)(ct & 15u);
+            uint32_t tau = ct >> 4;
+            float3 xd = xyz(xD[i / spp]);
+            float3 x1 = xyz(chain0[i]);
+            int cx = (int)floorf(FD(FM(FS(xd.x, g.grid_origin[0]), (float)g.cells_x), g.grid_extent[0]));
+            int cz = (int)floorf(FD(FM(FS(xd.z, g.grid_origin[1]), (float)g.cells_y), g.grid_extent[1]));
+            cx = min(max(cx, 0), g.cells_x - 1);
+            cz = min(max(cz, 0), g.cells_y - 1);
+            float dx = FS(x1.x, xd.x), dy = FS(x1.y, xd.y), dz = FS(x1.z, xd.z);
+            float l = __fsqrt_rn(FA(FA(FM(dx, dx), FM(dy, dy)), FM(dz, dz)));
+            float u = FD(dy, l);
+            float v = FD(FA(atan2f(dz, dx), 3.14159265358979323846f), 6.28318530717958647692f);
+            int bu = min(max((int)floorf(FM(u, (float)g.bins_x)), 0), g.bins_x - 1);
+            int bv = min(max((int)floorf(FM(v, (float)g.bins_y)), 0), g.bins_y - 1);
+            if (kk >= 1 && kk <= 6) {
+                int type = (1 << kk) - 2 + (int)tau;
+                key = ((long long)(cz * g.cells_x + cx) * 126 + type) * nb + bv * g.bins_x + bu;
+                val = w[i];
+            }
+        }
+        unsigned grp = __match_any_sync(MPG_FULL, key);
+        float sum = 0.f;
+        for (int j = 0; j < 32; j++) {
+            float vj = __shfl_sync(MPG_FULL, val, j);
+            if (grp & (1u << j)) sum += vj;
+        }
+        if (key >= 0 && lane == __ffs(grp) - 1) atomicAdd(hist + key, sum);
+    }
+}
+
 extern "C" mpg_status mpg_guide_upload(mpg_guide *g, const float *energy, void *stream) {
     ARG_CHECK(g && energy, "NULL argument");
-    k_guide_tables<<<g->n_cells, GT_THREADS, 0, as_stream(stream)>>>(energy, g->n_bins, g->prefix);
+    if (g->desc.domain == 1) {
+        mpg_status st = build_dir_tables(g, energy, as_stream(stream));
+        if (st != MPG_OK) return st;
+    } else {
+        k_guide_tables<<<g->n_cells, GT_THREADS, 0, as_stream(stream)>>>(energy, g->n_bins, g->prefix);
+    }
     CUDA_TRY(cudaPeekAtLastError());
-    CUDA_TRY(cudaMemsetAsync(g->hist, 0, sizeof(float) * (size_t)g->n_cells * g->n_bins, as_stream(stream)));
+    CUDA_TRY(cudaMemsetAsync(g->hist, 0, sizeof(float) * (size_t)g->n_cells * g->n_types * g->n_bins,
+                             as_stream(stream)));
     g->ready = true;
     return MPG_OK;
 }
 
 extern "C" mpg_status mpg_guide_reset(mpg_guide *g, void *stream) {
     ARG_CHECK(g, "NULL guide");
-    CUDA_TRY(cudaMemsetAsync(g->hist, 0, sizeof(float) * (size_t)g->n_cells * g->n_bins, as_stream(stream)));
-    k_guide_tables<<<g->n_cells, GT_THREADS, 0, as_stream(stream)>>>(g->hist, g->n_bins, g->prefix);
+    CUDA_TRY(cudaMemsetAsync(g->hist, 0, sizeof(float) * (size_t)g->n_cells * g->n_types * g->n_bins,
+                             as_stream(stream)));
+    if (g->desc.domain == 1) {
+        mpg_status st = build_dir_tables(g, g->hist, as_stream(stream));
+        if (st != MPG_OK) return st;
+    } else {
+        k_guide_tables<<<g->n_cells, GT_THREADS, 0, as_stream(stream)>>>(g->hist, g->n_bins, g->prefix);
+    }
     CUDA_TRY(cudaPeekAtLastError());
     g->ready = true;
     return MPG_OK;
@@ -567,25 +723,54 @@ extern "C" mpg_status mpg_guide_accumulate(mpg_guide *g, const mpg_query *q, con
     ARG_CHECK(q->spp >= 1 && n == q->n_recv * q->spp, "n must equal n_recv*spp");
     if (n == 0) return MPG_OK;
     int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 8);
-    k_accumulate<<<blocks, 256, 0, as_stream(stream)>>>(g->desc, (const float4 *)q->xD, q->spp, n,
-                                                        (const float4 *)wb->chain, wb->status, wb->w, g->hist);
+    if (g->desc.domain == 1) {
+        ARG_CHECK(wb->ctype, "typed direction guide needs walk ctype");
+        k_accumulate_dir<<<blocks, 256, 0, as_stream(stream)>>>(g->desc, (const float4 *)q->xD, q->spp, n,
+                                                                (const float4 *)wb->chain, wb->status, wb->w,
+                                                                wb->ctype, g->hist);
+    } else {
+        k_accumulate<<<blocks, 256, 0, as_stream(stream)>>>(g->desc, (const float4 *)q->xD, q->spp, n,
+                                                            (const float4 *)wb->chain, wb->status, wb->w, g->hist);
+    }
     CUDA_TRY(cudaPeekAtLastError());
     return MPG_OK;
 }
 
 extern "C" mpg_status mpg_guide_rebuild(mpg_guide *g, void *stream) {
     ARG_CHECK(g, "NULL guide");
-    k_guide_tables<<<g->n_cells, GT_THREADS, 0, as_stream(stream)>>>(g->hist, g->n_bins, g->prefix);
+    if (g->desc.domain == 1) {
+        mpg_status st = build_dir_tables(g, g->hist, as_stream(stream));
+        if (st != MPG_OK) return st;
+    } else {
+        k_guide_tables<<<g->n_cells, GT_THREADS, 0, as_stream(stream)>>>(g->hist, g->n_bins, g->prefix);
+    }
     CUDA_TRY(cudaPeekAtLastError());
-    CUDA_TRY(cudaMemsetAsync(g->hist, 0, sizeof(float) * (size_t)g->n_cells * g->n_bins, as_stream(stream)));
+    CUDA_TRY(cudaMemsetAsync(g->hist, 0, sizeof(float) * (size_t)g->n_cells * g->n_types * g->n_bins,
+                             as_stream(stream)));
     return MPG_OK;
 }
 
 extern "C" mpg_status mpg_guide_download(const mpg_guide *g, float *energy, uint64_t *prefix, void *stream) {
     ARG_CHECK(g, "NULL guide");
-    size_t ne = (size_t)g->n_cells * g->n_bins;
+    size_t ne = (size_t)g->n_cells * g->n_types * g->n_bins;
     if (energy) CUDA_TRY(cudaMemcpyAsync(energy, g->hist, ne * sizeof(float), cudaMemcpyDeviceToDevice, as_stream(stream)));
-    if (prefix) CUDA_TRY(cudaMemcpyAsync(prefix, g->prefix, ne * sizeof(uint64_t), cudaMemcpyDeviceToDevice, as_stream(stream)));
+    if (prefix) {
+        ARG_CHECK(g->desc.domain == 0, "domain-1 tables: use mpg_guide_download_dir_tables");
+        CUDA_TRY(cudaMemcpyAsync(prefix, g->prefix, ne * sizeof(uint64_t), cudaMemcpyDeviceToDevice, as_stream(stream)));
+    }
+    return MPG_OK;
+}
+
+extern "C" mpg_status mpg_guide_download_dir_tables(const mpg_guide *g, uint64_t *n_prefix, uint64_t *type_prefix,
+                                                    uint32_t *dir_prefix, void *stream) {
+    ARG_CHECK(g && g->desc.domain == 1, "needs a typed direction guide");
+    cudaStream_t s = as_stream(stream);
+    if (n_prefix) CUDA_TRY(cudaMemcpyAsync(n_prefix, g->n_prefix, (size_t)g->n_cells * 6 * 8, cudaMemcpyDeviceToDevice, s));
+    if (type_prefix)
+        CUDA_TRY(cudaMemcpyAsync(type_prefix, g->type_prefix, (size_t)g->n_cells * 126 * 8, cudaMemcpyDeviceToDevice, s));
+    if (dir_prefix)
+        CUDA_TRY(cudaMemcpyAsync(dir_prefix, g->dir_prefix, (size_t)g->n_cells * 126 * g->n_bins * 4,
+                                 cudaMemcpyDeviceToDevice, s));
     return MPG_OK;
 }
 
@@ -596,7 +781,8 @@ static mpg_status make_seed_ctx(const mpg_scene *scene, const mpg_guide *guide, 
                                 const mpg_walk_opts *o, SeedCtx &g) {
     memset(&g, 0, sizeof(g));
     ARG_CHECK(sd->k >= 1 && sd->k <= MPG_KMAX, "k must be in [1, 8]");
-    ARG_CHECK(sd->mode >= 0 && sd->mode <= 2, "bad sampler mode");
+    ARG_CHECK(sd->mode >= 0 && sd->mode <= 3, "bad sampler mode");
+    if (sd->mode == 3) ARG_CHECK(sd->k == 6, "GUIDE_DIR samples n <= 6: set k = 6");
     ARG_CHECK(sd->surf_id >= 0 && sd->surf_id < scene->d.n_surf, "sampler surf_id out of range");
     const DSurf &f = scene->d.surf[sd->surf_id];
     if (sd->mode == 0) ARG_CHECK(f.kind == 0, "CAP sampler needs a sphere");
@@ -606,31 +792,36 @@ static mpg_status make_seed_ctx(const mpg_scene *scene, const mpg_guide *guide, 
     g.k = sd->k;
     g.tau = sd->tau & ((1u << sd->k) - 1u);
     g.seed = o->seed;
-    if (sd->mode == 2) {
-        ARG_CHECK(guide && guide->ready, "GUIDE_UV sampler needs an uploaded/reset guide");
+    if (sd->mode >= 2) {
+        ARG_CHECK(guide && guide->ready, "guided sampler needs an uploaded/reset guide");
+        ARG_CHECK(guide->desc.domain == (sd->mode == 3 ? 1 : 0), "sampler mode / guide domain mismatch");
         const mpg_guide_desc &d = guide->desc;
         g.gox = d.grid_origin[0]; g.goz = d.grid_origin[1]; g.gex = d.grid_extent[0]; g.gez = d.grid_extent[1];
         g.cells_x = d.cells_x; g.cells_y = d.cells_y; g.bins_x = d.bins_x; g.bins_y = d.bins_y;
         g.uvox = d.uv_origin[0]; g.uvoz = d.uv_origin[1]; g.uvsx = d.uv_scale[0]; g.uvsz = d.uv_scale[1];
         g.uv_y = d.uv_plane_y;
         g.prefix = guide->prefix;
+        g.n_prefix = guide->n_prefix;
+        g.type_prefix = guide->type_prefix;
+        g.dir_prefix = guide->dir_prefix;
     }
     return MPG_OK;
 }
 
 __global__ void k_seeds(const DScene S, const SeedCtx g, const float4 *xD, int64_t n, int spp, uint64_t base,
-                        float4 *xL, float4 *tgt, int *bin) {
+                        float4 *xL, float4 *tgt, int *bin, uint32_t *ctype, float *pn) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         uint64_t wid = base + (uint64_t)i;
         float3 l;
         int lid;
         float pdf = sample_light(S, g.seed, wid, l, lid);
         xL[i] = make_float4(l.x, l.y, l.z, pdf);
-        float3 t = f3(0.f, 0.f, 0.f);
-        int b;
-        bool ok = seed_target(S, g, wid, 0u, xyz(xD[i / spp]), t, b);
-        tgt[i] = make_float4(t.x, t.y, t.z, 0.f);
-        bin[i] = ok ? b : -2;
+        SeedRes sr;
+        bool ok = seed_target(S, g, wid, 0u, xyz(xD[i / spp]), sr);
+        tgt[i] = make_float4(sr.tgt.x, sr.tgt.y, sr.tgt.z, 0.f);
+        bin[i] = ok ? sr.bin : -2;
+        if (ctype) ctype[i] = (uint32_t)sr.n | ((sr.bits & 255u) << 4) | ((sr.learned ? 1u : 0u) << 12);
+        if (pn) pn[i] = sr.Pn;
     }
 }
 
@@ -657,7 +848,8 @@ extern "C" mpg_status mpg_sample_seeds(const mpg_scene *scene, const mpg_guide *
     ARG_CHECK(q->xD && sb->xL && sb->target && sb->bin, "NULL query/seed array");
     int blocks = (int)std::min<int64_t>((n + 255) / 256, (int64_t)num_sms() * 8);
     k_seeds<<<blocks, 256, 0, as_stream(stream)>>>(scene->d, g, (const float4 *)q->xD, n, q->spp, o->walk_id_base,
-                                                   (float4 *)sb->xL, (float4 *)sb->target, sb->bin);
+                                                   (float4 *)sb->xL, (float4 *)sb->target, sb->bin, sb->ctype,
+                                                   sb->pn);
     CUDA_TRY(cudaPeekAtLastError());
     return MPG_OK;
 }
@@ -679,9 +871,9 @@ extern "C" mpg_status mpg_debug_trace(float *buf, int64_t n_walks, int32_t strid
 // in rounds of B = 4, 8, 16, ... parallel trials
 #define LOCAL_TRIALS 4u
 static uint32_t hard_cap(int64_t n) { return (uint32_t)std::min<int64_t>(std::max<int64_t>(n, 1), 1 << 21); }
-static size_t mk_ws_bytes(int64_t n) {
+static size_t mk_ws_bytes(int64_t n) { // hard lists A/B: walk (8 B), psurf, pct, best (4 B each)
     size_t cap = hard_cap(n);
-    return 256 + 2 * cap * (sizeof(int64_t) + 2 * sizeof(uint32_t));
+    return 256 + 2 * cap * (sizeof(int64_t) + 3 * sizeof(uint32_t));
 }
 
 // wavefront workspace layout: header, ray lists, free stack,
@@ -737,6 +929,7 @@ static mpg_status launch_walk(const DScene &S, const SeedCtx &g, WalkParams P, c
     int64_t *wl[2] = {(int64_t *)(base + 256), (int64_t *)(base + 256 + (size_t)cap * 8)};
     uint32_t *pl[2] = {(uint32_t *)(base + 256 + (size_t)cap * 16), (uint32_t *)(base + 256 + (size_t)cap * 20)};
     uint32_t *bl[2] = {(uint32_t *)(base + 256 + (size_t)cap * 24), (uint32_t *)(base + 256 + (size_t)cap * 28)};
+    uint32_t *cl[2] = {(uint32_t *)(base + 256 + (size_t)cap * 32), (uint32_t *)(base + 256 + (size_t)cap * 36)};
     uint32_t t0 = P.local_trials + 1, B = 4;
     int cur = 0, rblocks = num_sms() * occ;
     while (t0 <= P.k_max) {
@@ -746,14 +939,16 @@ static mpg_status launch_walk(const DScene &S, const SeedCtx &g, WalkParams P, c
         RP.round_t0 = t0;
         RP.round_B = Bc;
         RP.hard_walk = wl[cur]; RP.hard_psurf = pl[cur]; RP.hard_best = bl[cur]; RP.hard_count = cnt + cur;
+        RP.hard_pct = cl[cur];
         RP.queue = (unsigned long long *)(base + 8);
         CUDA_TRY(cudaMemsetAsync(base + 8, 0, 8, st));
         k_walk<KMAX, R><<<rblocks, 128, 0, st>>>(S, g, RP);
         CUDA_TRY(cudaPeekAtLastError());
         CUDA_TRY(cudaMemsetAsync(cnt + (cur ^ 1), 0, 4, st));
-        k_hard_compact<<<num_sms() * 2, 256, 0, st>>>(wl[cur], pl[cur], bl[cur], cnt + cur, cap, wl[cur ^ 1],
-                                                      pl[cur ^ 1], bl[cur ^ 1], cnt + (cur ^ 1), t0 + Bc - 1,
-                                                      P.k_max, P.T, P.seed_xL, P.trials, P.w, P.stats);
+        k_hard_compact<<<num_sms() * 2, 256, 0, st>>>(wl[cur], pl[cur], cl[cur], bl[cur], cnt + cur, cap, wl[cur ^ 1],
+                                                      pl[cur ^ 1], cl[cur ^ 1], bl[cur ^ 1], cnt + (cur ^ 1),
+                                                      t0 + Bc - 1, P.k_max, P.T, P.seed_xL, P.seed_pn, P.trials,
+                                                      P.w, P.stats);
         CUDA_TRY(cudaPeekAtLastError());
         cur ^= 1;
         t0 += Bc;
@@ -913,6 +1108,10 @@ extern "C" mpg_status mpg_manifold_walk(const mpg_scene *scene, const mpg_guide 
     P.seed_xL = (const float4 *)sb->xL;
     P.seed_tgt = (const float4 *)sb->target;
     P.seed_bin = sb->bin;
+    P.seed_ctype = sb->ctype;
+    P.seed_pn = sb->pn;
+    P.out_ctype = out->ctype;
+    P.max_iters_long = o->max_iters_long;
     P.chain = (float4 *)out->chain;
     P.status = out->status;
     P.iters = out->iters;
@@ -938,12 +1137,17 @@ extern "C" mpg_status mpg_manifold_walk(const mpg_scene *scene, const mpg_guide 
         char *base = (char *)workspace;
         P.hard_walk = (int64_t *)(base + 256);
         P.hard_psurf = (uint32_t *)(base + 256 + (size_t)P.hard_cap * 16);
+        P.hard_pct = (uint32_t *)(base + 256 + (size_t)P.hard_cap * 32);
         P.hard_best = (uint32_t *)(base + 256 + (size_t)P.hard_cap * 24);
         P.hard_count = (unsigned int *)(base + 16);
     }
     int k = g.k;
     ARG_CHECK(!((o->flags & MPG_FLAG_WAVEFRONT) && (o->flags & MPG_FLAG_NEWTON_F64)),
               "MPG_FLAG_NEWTON_F64 is implemented on the default path only");
+    ARG_CHECK(!((o->flags & MPG_FLAG_WAVEFRONT) && sd->mode == MPG_SEED_GUIDE_DIR),
+              "MPG_SEED_GUIDE_DIR is implemented on the default path only");
+    if (sd->mode == MPG_SEED_GUIDE_DIR)
+        ARG_CHECK(sb->ctype && sb->pn && out->ctype, "GUIDE_DIR needs seed ctype/pn and walk ctype arrays");
     if (o->flags & MPG_FLAG_WAVEFRONT) {
         if (k <= 1) return launch_wavefront<1>(scene->d, g, P, workspace, workspace_bytes, s);
         if (k <= 2) return launch_wavefront<2>(scene->d, g, P, workspace, workspace_bytes, s);

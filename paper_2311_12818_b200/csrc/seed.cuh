@@ -18,7 +18,35 @@ struct SeedCtx {
     int cells_x, cells_y, bins_x, bins_y;
     float uvox, uvoz, uvsx, uvsz, uv_y;
     const uint64_t *prefix; // [cells][bins] inclusive prefix of W'
+    // typed direction guide (MPG_SEED_GUIDE_DIR, configs[4], R22)
+    const uint64_t *n_prefix;    // [cells][6]
+    const uint64_t *type_prefix; // [cells][126]
+    const uint32_t *dir_prefix;  // [cells][126][bins]
 };
+
+// one seed draw: the deduction ray x_D -> tgt gives x_1 (Eq. 6); n = chain
+// length; bits = tau (learned / fixed type) or per-vertex R/T choices of the
+// initializer (learned = false); Pn = P(n)
+struct SeedRes {
+    float3 tgt;
+    int bin, n;
+    uint32_t bits;
+    bool learned;
+    float Pn;
+};
+
+__device__ __forceinline__ uint64_t mulhi_u64(uint32_t x, uint64_t S) { // floor(x*S/2^32), exact
+    uint64_t X = x;
+    return X * (S >> 32) + ((X * (S & 0xffffffffull)) >> 32);
+}
+
+__device__ __forceinline__ int seed_cell(const SeedCtx &g, float3 xD) {
+    int cx = (int)floorf(FD(FM(FS(xD.x, g.gox), (float)g.cells_x), g.gex));
+    int cz = (int)floorf(FD(FM(FS(xD.z, g.goz), (float)g.cells_y), g.gez));
+    cx = min(max(cx, 0), g.cells_x - 1);
+    cz = min(max(cz, 0), g.cells_y - 1);
+    return cz * g.cells_x + cx;
+}
 
 // x_L (purpose 0, trial 0) (R15); returns its pdf
 __device__ __forceinline__ float sample_light(const DScene &S, uint64_t seed, uint64_t wid, float3 &xL, int &lid) {
@@ -47,8 +75,14 @@ __device__ __forceinline__ void onb_exact(float3 n, float3 &b1, float3 &b2) {
 // Seed target for (walk, trial): the deduction ray x_D -> target gives x_1
 // (Eq. 6).  Returns false if no seed could be drawn (SEED_FAIL).
 __device__ __forceinline__ bool seed_target(const DScene &S, const SeedCtx &g, uint64_t wid, uint32_t trial,
-                                            float3 xD, float3 &tgt, int &bin) {
+                                            float3 xD, SeedRes &sr) {
+    float3 &tgt = sr.tgt;
+    int &bin = sr.bin;
     bin = -1;
+    sr.n = g.k;
+    sr.bits = g.tau;
+    sr.learned = true;
+    sr.Pn = 1.0f;
     if (g.mode == 0) { // uniform on the cap of a sphere visible from x_D
         const DSurf &f = S.surf[g.surf_id];
         float dx = FS(xD.x, f.center.x), dy = FS(xD.y, f.center.y), dz = FS(xD.z, f.center.z);
@@ -99,12 +133,8 @@ __device__ __forceinline__ bool seed_target(const DScene &S, const SeedCtx &g, u
         return true;
     }
     if (g.mode == 2) { // guided bin over the surface (u,v): integer CDF of W' (R20)
-        int cx = (int)floorf(FD(FM(FS(xD.x, g.gox), (float)g.cells_x), g.gex));
-        int cz = (int)floorf(FD(FM(FS(xD.z, g.goz), (float)g.cells_y), g.gez));
-        cx = min(max(cx, 0), g.cells_x - 1);
-        cz = min(max(cz, 0), g.cells_y - 1);
         int nb = g.bins_x * g.bins_y;
-        const uint64_t *pf = g.prefix + (size_t)(cz * g.cells_x + cx) * nb;
+        const uint64_t *pf = g.prefix + (size_t)seed_cell(g, xD) * nb;
         uint64_t S_ = __ldg((const unsigned long long *)pf + nb - 1);
         uint4 r = rng_draw(g.seed, wid, 1u, trial);
         uint64_t x = r.x;
@@ -121,6 +151,58 @@ __device__ __forceinline__ bool seed_target(const DScene &S, const SeedCtx &g, u
         float u = FD(FA((float)bx, u01(r2.x)), (float)g.bins_x);
         float v = FD(FA((float)by, u01(r2.y)), (float)g.bins_y);
         tgt = f3(FA(g.uvox, FM(u, g.uvsx)), g.uv_y, FA(g.uvoz, FM(v, g.uvsz)));
+        return true;
+    }
+    if (g.mode == 3) { // configs[4]: n ~ 1/2 P_0 + 1/2 P_e, then one-sample MIS for (w_D, tau) (R22)
+        int c = seed_cell(g, xD);
+        const unsigned long long *npf = (const unsigned long long *)g.n_prefix + (size_t)c * 6;
+        uint4 r0 = rng_draw(g.seed, wid, 1u, 0u); // n is reused by every trial
+        uint64_t S6 = __ldg(npf + 5);
+        uint64_t t = mulhi_u64(r0.x, S6);
+        int n = 0;
+        while ((uint64_t)__ldg(npf + n) <= t) n++;
+        uint64_t lo = n > 0 ? (uint64_t)__ldg(npf + n - 1) : 0ull;
+        sr.Pn = (float)((double)((uint64_t)__ldg(npf + n) - lo) / (double)S6);
+        n += 1;
+        sr.n = n;
+        uint4 r = rng_draw(g.seed, wid, 1u, trial);
+        int g0 = (1 << n) - 2, gn = 1 << n;
+        const unsigned long long *tpf = (const unsigned long long *)g.type_prefix + (size_t)c * 126 + g0;
+        uint64_t Wg = __ldg(tpf + gn - 1);
+        float u, v;
+        if (Wg > 0 && (r.y >> 31)) {
+            uint64_t tt = mulhi_u64(r.z, Wg);
+            int m = 0;
+            while ((uint64_t)__ldg(tpf + m) <= tt) m++;
+            sr.bits = (uint32_t)m;
+            sr.learned = true;
+            int nb = g.bins_x * g.bins_y;
+            const uint32_t *dpf = g.dir_prefix + ((size_t)c * 126 + g0 + m) * nb;
+            uint64_t Sd = __ldg(dpf + nb - 1);
+            uint64_t td = mulhi_u64(r.w, Sd);
+            int lo2 = 0, hi2 = nb - 1;
+            while (lo2 < hi2) {
+                int mid = (lo2 + hi2) >> 1;
+                if ((uint64_t)__ldg(dpf + mid) > td) hi2 = mid;
+                else lo2 = mid + 1;
+            }
+            bin = lo2;
+            uint4 r2 = rng_draw(g.seed, wid, 2u, trial);
+            u = FD(FA((float)(lo2 % g.bins_x), u01(r2.x)), (float)g.bins_x);
+            v = FD(FA((float)(lo2 / g.bins_x), u01(r2.y)), (float)g.bins_y);
+        } else {
+            uint4 r3 = rng_draw(g.seed, wid, 3u, trial);
+            u = u01(r3.x);
+            v = u01(r3.y);
+            sr.learned = false;
+            sr.bits = r3.z;
+        }
+        // equal-area hemisphere about +y: u = cos(theta), v = (phi + pi)/(2 pi)
+        float st2 = FS(1.0f, FM(u, u));
+        float st = __fsqrt_rn(st2 > 0.0f ? st2 : 0.0f);
+        float phi = FS(FM(6.28318530717958647692f, v), 3.14159265358979323846f);
+        float cp = cosf(phi), sp = sinf(phi);
+        tgt = f3(FA(xD.x, FM(st, cp)), FA(xD.y, u), FA(xD.z, FM(st, sp)));
         return true;
     }
     return false;

@@ -33,6 +33,10 @@ struct WalkParams {
     int spp;
     const float4 *seed_xL, *seed_tgt;
     const int *seed_bin;
+    const uint32_t *seed_ctype; // n | bits << 4 | learned << 12 (may be NULL: fixed type)
+    const float *seed_pn;       // P(n) (may be NULL: 1)
+    uint16_t *out_ctype;        // primary chain type n | tau << 4 (may be NULL)
+    int max_iters_long;
     float4 *chain;
     uint8_t *status;
     uint16_t *iters;
@@ -53,6 +57,7 @@ struct WalkParams {
     uint32_t hard_cap;
     int64_t *hard_walk; // list written by the main pass / read by a round
     uint32_t *hard_psurf;
+    uint32_t *hard_pct;  // primary chain type (n | tau << 4)
     uint32_t *hard_best; // min successful trial index (0xffffffff: none yet)
     unsigned int *hard_count;
     int round_mode;     // 0: main pass; 1: trial round over the hard list
@@ -144,10 +149,14 @@ __device__ __forceinline__ double3 refine_hit(const DScene &S, int prim, int sur
 // returns 0 on success, else 1 + (i << 4) | reason (1 miss, 2 wrong surface, 3 zero length, 4 scatter)
 // Traversal runs in fp32 (the hit/miss and which-primitive decisions); the hit
 // point is recomputed in fp64 on the exact line (refine_hit) and kept in fp64.
+// Deduction resolves the type string: vertex i takes bit i of `bits`, except
+// that the initializer (learned = false) always reflects on a conductor; T on
+// a conductor fails (R22, R14).  The resolved string is returned in tau_res.
 template <int KMAX>
-__device__ __forceinline__ int trace_chain(const DScene &S, bool deduce, int k, uint32_t tau, float3 xD, float3 tgt,
-                                           const double3 *q, uint32_t surf_req, float eps, double3 *y, int *yp,
-                                           int *ys, LaneStats &st) {
+__device__ __forceinline__ int trace_chain(const DScene &S, bool deduce, int k, uint32_t bits, bool learned,
+                                           float3 xD, float3 tgt, const double3 *q, uint32_t surf_req, float eps,
+                                           double3 *y, int *yp, int *ys, LaneStats &st, uint32_t &tau_res) {
+    uint32_t res = 0;
     double3 o = d3f(xD);
     double3 dd = make_double3(0.0, 0.0, 0.0);
     if (deduce) {
@@ -164,17 +173,25 @@ __device__ __forceinline__ int trace_chain(const DScene &S, bool deduce, int k, 
             if (!(l2 > 0.0)) return 3 | (i << 4);
             dd = v * rsqrt(l2);
         } else if (i > 0) {
-            if (!scatter_dir(S, dd, yp[i - 1], ys[i - 1], f3d(y[i - 1]), (tau >> (i - 1)) & 1u)) return 4 | (i << 4);
+            if (!scatter_dir(S, dd, yp[i - 1], ys[i - 1], f3d(y[i - 1]), (res >> (i - 1)) & 1u)) return 4 | (i << 4);
         }
         Hit h;
         float3 of = f3d(o), d = nrmz(f3d(dd));
         if (!trace<false>(S, of, d, eps, 3.0e38f, true, h, st)) return 1 | (i << 4);
         if (!deduce && h.surf != (int)((surf_req >> (4 * i)) & 15u)) return 2 | (i << 4);
+        if (deduce) {
+            uint32_t bit = (bits >> i) & 1u;
+            const int mat = S.surf[h.surf].mat;
+            if (!learned && mat == 0) bit = 0u;
+            if (bit && mat != 1) return 4 | (i << 4);
+            res |= bit << i;
+        }
         y[i] = refine_hit(S, h.prim, h.surf, o, deduce ? o + dd : q[i], h.p);
         yp[i] = h.prim;
         ys[i] = h.surf;
         o = y[i];
     }
+    tau_res = res;
     return 0;
 }
 
@@ -185,8 +202,11 @@ __global__ void __launch_bounds__(128, (KMAX <= 2 ? 6 : 2)) k_walk(const DScene 
     __syncthreads();
 
     const int lane = threadIdx.x & 31;
-    const int k = g.k;
-    const uint32_t tau = g.tau;
+    // chain type of the current attempt (per lane: configs[4] draws n and tau per sample)
+    int k = g.k, pk = g.k;
+    uint32_t tau = g.tau, ptau = g.tau, bits = g.tau;
+    bool learned = true;
+    float Pn = 1.0f;
 
     // lane state
     int phase = PH_FETCH;
@@ -237,6 +257,9 @@ __global__ void __launch_bounds__(128, (KMAX <= 2 ? 6 : 2)) k_walk(const DScene 
                     if (*(volatile uint32_t *)(P.hard_best + cur_e) > trial) {
                         w = P.hard_walk[cur_e];
                         psurf = P.hard_psurf[cur_e];
+                        uint32_t pct = P.hard_pct[cur_e];
+                        pk = (int)(pct & 15u);
+                        ptau = pct >> 4;
                         int64_t rcv = w / P.spp;
                         xD = xyz(__ldg(P.xD + rcv));
                         nD = xyz(__ldg(P.nD + rcv));
@@ -278,10 +301,23 @@ __global__ void __launch_bounds__(128, (KMAX <= 2 ? 6 : 2)) k_walk(const DScene 
             if (trial == 0) {
                 ok = __ldg(P.seed_bin + w) != -2;
                 tgt = xyz(__ldg(P.seed_tgt + w));
+                if (P.seed_ctype) {
+                    uint32_t ct = __ldg(P.seed_ctype + w);
+                    k = (int)(ct & 15u);
+                    bits = (ct >> 4) & 255u;
+                    learned = (ct >> 12) & 1u;
+                }
+                Pn = P.seed_pn ? __ldg(P.seed_pn + w) : 1.0f;
             } else {
-                int bin;
-                ok = seed_target(S, g, P.walk_id_base + w, trial, xD, tgt, bin);
+                SeedRes sr;
+                ok = seed_target(S, g, P.walk_id_base + w, trial, xD, sr);
+                tgt = sr.tgt;
+                k = sr.n;
+                bits = sr.bits;
+                learned = sr.learned;
+                Pn = sr.Pn;
             }
+            k = max(1, min(k, KMAX));
             it = 0;
             if (ok) phase = PH_DEDUCE;
             else { end_status = ST_SEED_FAIL; phase = PH_END; }
@@ -293,8 +329,10 @@ __global__ void __launch_bounds__(128, (KMAX <= 2 ? 6 : 2)) k_walk(const DScene 
             uint32_t sreq = 0;
 #pragma unroll
             for (int i = 0; i < KMAX; i++) sreq |= (uint32_t)(surf[i] & 15) << (4 * i);
-            int why = trace_chain<KMAX>(S, ded, k, tau, xD, tgt, q, sreq, P.ray_eps, y, yp, ys, ls);
+            uint32_t tres = tau;
+            int why = trace_chain<KMAX>(S, ded, k, bits, learned, xD, tgt, q, sreq, P.ray_eps, y, yp, ys, ls, tres);
             bool ok = why == 0;
+            if (ok && ded) tau = tres;
             if (!ok && !ded && P.dbg && trial == 0 && w < P.n_dbg && 2 * it + 3 < P.dbg_stride)
                 P.dbg[w * P.dbg_stride + 2 * (it + 1)] = -(float)(why + 1);
             if (ok) {
@@ -332,7 +370,10 @@ __global__ void __launch_bounds__(128, (KMAX <= 2 ? 6 : 2)) k_walk(const DScene 
                 else if (r == 2) { end_status = ST_DEGENERATE; phase = PH_END; }
             }
             if (phase == PH_SOLVE) {
-                if (it >= P.max_iters) { end_status = ST_MAXITER; phase = PH_END; }
+                if (it >= ((k >= 3 && P.max_iters_long > 0) ? P.max_iters_long : P.max_iters)) {
+                    end_status = ST_MAXITER;
+                    phase = PH_END;
+                }
                 else {
 #pragma unroll
                     for (int i = 0; i < KMAX; i++) {
@@ -392,12 +433,15 @@ __global__ void __launch_bounds__(128, (KMAX <= 2 ? 6 : 2)) k_walk(const DScene 
                 P.iters[w] = (uint16_t)it;
                 P.G[w] = G;
                 P.T[w] = T;
+                if (P.out_ctype) P.out_ctype[w] = (uint16_t)((uint32_t)k | (tau << 4));
                 atomicAdd(&s_stats[SS_STATUS0 + st], 1ull);
                 atomicAdd(&s_stats[SS_PRIM_IT], (unsigned long long)it);
                 atomicAdd(&s_stats[SS_WALKS], 1ull);
                 if (st == ST_CONVERGED || st == ST_OCCLUDED) atomicAdd(&s_stats[SS_CONV], 1ull);
                 if (st == ST_CONVERGED && T > 0.0f && P.trials_on) {
                     Tprim = T;
+                    pk = k;
+                    ptau = tau;
                     psurf = 0;
 #pragma unroll
                     for (int i = 0; i < KMAX; i++) {
@@ -415,7 +459,7 @@ __global__ void __launch_bounds__(128, (KMAX <= 2 ? 6 : 2)) k_walk(const DScene 
                 bool same = false;
                 float kdummy;
                 R DLdummy[4];
-                if (st == ST_CONVERGED &&
+                if (st == ST_CONVERGED && k == pk && tau == ptau &&
                     post_sweep<KMAX, R>(S, S.light[lid], k, tau, xD, xL, x, prim, surf, false, kdummy, DLdummy)) {
                     same = true;
 #pragma unroll
@@ -432,7 +476,7 @@ __global__ void __launch_bounds__(128, (KMAX <= 2 ? 6 : 2)) k_walk(const DScene 
                 } else if (same || trial >= P.k_max) {
                     if (!same) atomicAdd(&s_stats[SS_TRUNC], 1ull);
                     P.trials[w] = trial;
-                    P.w[w] = Tprim * (float)trial / pdfL;
+                    P.w[w] = Tprim * (float)trial / (Pn * pdfL);
                     atomicAdd(&s_stats[SS_TRIALS], (unsigned long long)trial);
                     phase = PH_FETCH;
                 } else {
@@ -443,6 +487,7 @@ __global__ void __launch_bounds__(128, (KMAX <= 2 ? 6 : 2)) k_walk(const DScene 
                         if (e < P.hard_cap) {
                             P.hard_walk[e] = w;
                             P.hard_psurf[e] = psurf;
+                            P.hard_pct[e] = (uint32_t)pk | (ptau << 4);
                             P.hard_best[e] = HARD_NONE;
                             published = true;
                         }
@@ -482,11 +527,11 @@ __global__ void __launch_bounds__(128, (KMAX <= 2 ? 6 : 2)) k_walk(const DScene 
 // sequential definition of Eq. 15's geometric count, since every trial below
 // it was run); walks past k_max are truncated at k_max; the rest move to the
 // next round's list.
-__global__ void k_hard_compact(const int64_t *walk_in, const uint32_t *psurf_in, const uint32_t *best_in,
-                               const unsigned int *count_in, uint32_t cap, int64_t *walk_out, uint32_t *psurf_out,
-                               uint32_t *best_out, unsigned int *count_out, uint32_t t_end, uint32_t k_max,
-                               const float *T, const float4 *seed_xL, uint32_t *trials, float *w,
-                               unsigned long long *stats) {
+__global__ void k_hard_compact(const int64_t *walk_in, const uint32_t *psurf_in, const uint32_t *pct_in,
+                               const uint32_t *best_in, const unsigned int *count_in, uint32_t cap, int64_t *walk_out,
+                               uint32_t *psurf_out, uint32_t *pct_out, uint32_t *best_out, unsigned int *count_out,
+                               uint32_t t_end, uint32_t k_max, const float *T, const float4 *seed_xL,
+                               const float *seed_pn, uint32_t *trials, float *w, unsigned long long *stats) {
     uint32_t cnt = min(*count_in, cap);
     unsigned long long s_tr = 0, s_tc = 0;
     for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < cnt; e += gridDim.x * blockDim.x) {
@@ -497,12 +542,13 @@ __global__ void k_hard_compact(const int64_t *walk_in, const uint32_t *psurf_in,
         else if (t_end >= k_max) { kk = k_max; s_tc++; }
         if (kk) {
             trials[wk] = kk;
-            w[wk] = T[wk] * (float)kk / seed_xL[wk].w;
+            w[wk] = T[wk] * (float)kk / ((seed_pn ? seed_pn[wk] : 1.0f) * seed_xL[wk].w);
             s_tr += kk;
         } else {
             unsigned int o = atomicAdd(count_out, 1u);
             walk_out[o] = wk;
             psurf_out[o] = psurf_in[e];
+            pct_out[o] = pct_in[e];
             best_out[o] = HARD_NONE;
         }
     }

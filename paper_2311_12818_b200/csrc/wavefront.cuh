@@ -124,8 +124,9 @@ __device__ __forceinline__ void wf_seed(const DScene &S, const SeedCtx &g, const
         ok = __ldg(P.seed_bin + w) != -2;
         tgt = xyz(__ldg(P.seed_tgt + w));
     } else {
-        int bin;
-        ok = seed_target(S, g, P.walk_id_base + w, trial, xyz(__ldg(P.xD + w / P.spp)), tgt, bin);
+        SeedRes sr;
+        ok = seed_target(S, g, P.walk_id_base + w, trial, xyz(__ldg(P.xD + w / P.spp)), sr);
+        tgt = sr.tgt;
     }
     P.s_walk[slot] = (int32_t)w;
     P.s_trial[slot] = trial;

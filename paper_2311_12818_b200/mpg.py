@@ -47,13 +47,14 @@ class mpg_sampler_desc(C.Structure):
 class mpg_guide_desc(C.Structure):
     _fields_ = [("grid_origin", C.c_float * 2), ("grid_extent", C.c_float * 2), ("cells_x", C.c_int32),
                 ("cells_y", C.c_int32), ("bins_x", C.c_int32), ("bins_y", C.c_int32), ("uv_origin", C.c_float * 2),
-                ("uv_scale", C.c_float * 2), ("uv_plane_y", C.c_float)]
+                ("uv_scale", C.c_float * 2), ("uv_plane_y", C.c_float), ("domain", C.c_int32), ("n_types", C.c_int32)]
 
 
 class mpg_walk_opts(C.Structure):
     _fields_ = [("max_iters", C.c_int32), ("tol", C.c_float), ("beta0", C.c_float), ("trials", C.c_int32),
                 ("k_max", C.c_uint32), ("same_chain_eps", C.c_float), ("ray_eps", C.c_float), ("flags", C.c_uint32),
-                ("seed", C.c_uint64), ("walk_id_base", C.c_uint64)]
+                ("seed", C.c_uint64), ("walk_id_base", C.c_uint64), ("max_iters_long", C.c_int32),
+                ("reserved", C.c_int32)]
 
 
 class mpg_query(C.Structure):
@@ -61,12 +62,13 @@ class mpg_query(C.Structure):
 
 
 class mpg_seed_buf(C.Structure):
-    _fields_ = [("xL", C.c_void_p), ("target", C.c_void_p), ("bin", C.c_void_p)]
+    _fields_ = [("xL", C.c_void_p), ("target", C.c_void_p), ("bin", C.c_void_p), ("ctype", C.c_void_p),
+                ("pn", C.c_void_p)]
 
 
 class mpg_walk_buf(C.Structure):
     _fields_ = [("chain", C.c_void_p), ("status", C.c_void_p), ("iters", C.c_void_p), ("G", C.c_void_p),
-                ("T", C.c_void_p), ("w", C.c_void_p), ("trials", C.c_void_p)]
+                ("T", C.c_void_p), ("w", C.c_void_p), ("trials", C.c_void_p), ("ctype", C.c_void_p)]
 
 
 STATS_FIELDS = ["walks", "converged", "newton_iters", "primary_iters", "attempts", "rays", "trials", "truncated",
@@ -84,7 +86,7 @@ class mpg_scene_info(C.Structure):
 
 EXPORTS = ["mpg_scene_create", "mpg_scene_destroy", "mpg_scene_get_info", "mpg_trace_rays", "mpg_guide_create",
            "mpg_guide_destroy", "mpg_guide_upload", "mpg_guide_reset", "mpg_guide_accumulate", "mpg_guide_rebuild",
-           "mpg_guide_download", "mpg_sample_seeds", "mpg_walk_workspace_size", "mpg_manifold_walk", "mpg_estimate",
+           "mpg_guide_download", "mpg_guide_download_dir_tables", "mpg_sample_seeds", "mpg_walk_workspace_size", "mpg_manifold_walk", "mpg_estimate",
            "mpg_debug_trace", "mpg_last_error", "mpg_version"]
 
 _lib = None
@@ -112,6 +114,7 @@ def lib():
             "mpg_guide_accumulate": (st, [P, C.POINTER(mpg_query), C.POINTER(mpg_walk_buf), C.c_int64, P]),
             "mpg_guide_rebuild": (st, [P, P]),
             "mpg_guide_download": (st, [P, P, P, P]),
+            "mpg_guide_download_dir_tables": (st, [P, P, P, P, P]),
             "mpg_sample_seeds": (st, [P, P, C.POINTER(mpg_sampler_desc), C.POINTER(mpg_query),
                                       C.POINTER(mpg_walk_opts), C.POINTER(mpg_seed_buf), P]),
             "mpg_walk_workspace_size": (C.c_size_t, [C.c_int64, C.POINTER(mpg_sampler_desc), C.POINTER(mpg_walk_opts)]),
@@ -205,6 +208,11 @@ def mpg_guide_download(h, energy=None, prefix=None, stream=None):
     _check(lib().mpg_guide_download(h, _ptr(energy), _ptr(prefix), _stream_ptr(stream)), "mpg_guide_download")
 
 
+def mpg_guide_download_dir_tables(h, n_prefix=None, type_prefix=None, dir_prefix=None, stream=None):
+    _check(lib().mpg_guide_download_dir_tables(h, _ptr(n_prefix), _ptr(type_prefix), _ptr(dir_prefix),
+                                               _stream_ptr(stream)), "mpg_guide_download_dir_tables")
+
+
 def mpg_sample_seeds(scene, guide, sampler, query, opts, seeds, stream=None):
     _check(lib().mpg_sample_seeds(scene, guide, C.byref(sampler), C.byref(query), C.byref(opts), C.byref(seeds),
                                   _stream_ptr(stream)), "mpg_sample_seeds")
@@ -274,7 +282,7 @@ class DeviceScene:
         sp = w.seed
         self.sampler = mpg_sampler_desc(sp.mode, sp.surf_id, sp.k, sp.tau)
         self.guide = None
-        if sp.mode == W.SEED_GUIDE_UV:
+        if sp.mode in (W.SEED_GUIDE_UV, W.SEED_GUIDE_DIR):
             g = mpg_guide_desc()
             g.grid_origin = (C.c_float * 2)(*sp.grid_origin)
             g.grid_extent = (C.c_float * 2)(*sp.grid_extent)
@@ -282,9 +290,11 @@ class DeviceScene:
             g.uv_origin = (C.c_float * 2)(*sp.uv_origin)
             g.uv_scale = (C.c_float * 2)(*sp.uv_scale)
             g.uv_plane_y = sp.uv_plane_y
+            g.domain = 1 if sp.mode == W.SEED_GUIDE_DIR else 0
+            g.n_types = sp.n_types
             self.guide_desc = g
             self.guide = mpg_guide_create(g)
-            if w.energies is not None:
+            if w.energies is not None and sp.mode == W.SEED_GUIDE_UV:
                 self.upload_energies(w.energies, stream)
             else:
                 mpg_guide_reset(self.guide, stream)
@@ -298,7 +308,8 @@ class DeviceScene:
     def opts(self, **over) -> mpg_walk_opts:
         o = self.w.opts
         d = dict(max_iters=o.max_iters, tol=o.tol, beta0=o.beta0, trials=o.trials, k_max=o.k_max,
-                 same_chain_eps=0.0, ray_eps=0.0, flags=o.flags, seed=o.seed, walk_id_base=o.walk_id_base)
+                 same_chain_eps=0.0, ray_eps=0.0, flags=o.flags, seed=o.seed, walk_id_base=o.walk_id_base,
+                 max_iters_long=o.max_iters_long)
         d.update(over)
         r = mpg_walk_opts()
         for k, v in d.items():
@@ -346,6 +357,9 @@ class Batch:
         self.T = torch.empty(n, device=device)
         self.w = torch.empty(n, device=device)
         self.trials = torch.empty(n, dtype=torch.int32, device=device)
+        self.ctype_seed = torch.empty(n, dtype=torch.int32, device=device)
+        self.pn = torch.empty(n, dtype=torch.float32, device=device)
+        self.ctype = torch.empty(n, dtype=torch.int16, device=device)
         self.mean = torch.empty(max(1, self.n_recv), device=device)
         self.var = torch.empty(max(1, self.n_recv), device=device)
         self.stats = torch.zeros(len(STATS_FIELDS) + 8, dtype=torch.int64, device=device)
@@ -353,9 +367,11 @@ class Batch:
         self.workspace = torch.zeros(mpg_walk_workspace_size(self.n, smp, mpg_walk_opts()), dtype=torch.uint8,
                                      device=device)
         self.query = mpg_query(self.xD.data_ptr(), self.nD.data_ptr(), self.n_recv, self.spp)
-        self.seeds = mpg_seed_buf(self.xL.data_ptr(), self.target.data_ptr(), self.bin.data_ptr())
+        self.seeds = mpg_seed_buf(self.xL.data_ptr(), self.target.data_ptr(), self.bin.data_ptr(),
+                                  self.ctype_seed.data_ptr(), self.pn.data_ptr())
         self.out = mpg_walk_buf(self.chain.data_ptr(), self.status.data_ptr(), self.iters.data_ptr(),
-                                self.G.data_ptr(), self.T.data_ptr(), self.w.data_ptr(), self.trials.data_ptr())
+                                self.G.data_ptr(), self.T.data_ptr(), self.w.data_ptr(), self.trials.data_ptr(),
+                                self.ctype.data_ptr())
 
     def stats_dict(self):
         v = self.stats.cpu().numpy().astype(np.int64)
@@ -371,7 +387,26 @@ class Batch:
                     status=self.status.cpu().numpy(), iters=self.iters.cpu().numpy().astype(np.int32),
                     G=self.G.cpu().numpy(), T=self.T.cpu().numpy(), w=self.w.cpu().numpy(),
                     trials=self.trials.cpu().numpy().astype(np.int64), xL=self.xL.cpu().numpy(),
-                    target=self.target.cpu().numpy(), bin=self.bin.cpu().numpy())
+                    target=self.target.cpu().numpy(), bin=self.bin.cpu().numpy(),
+                    ctype=self.ctype.cpu().numpy().astype(np.int64) & 0xffff,
+                    seed_ctype=self.ctype_seed.cpu().numpy().astype(np.int64), pn=self.pn.cpu().numpy())
+
+
+def run_progressive(ds: DeviceScene, b: Batch, opts: mpg_walk_opts, iterations: int = 8, stream=None,
+                    on_iteration=None):
+    """configs[4] (R22): guide reset (learned branch absent) at iteration 0, then per
+    iteration: seeds -> walk (+trials) -> estimator -> accumulate -> rebuild tables
+    from this iteration only (P:426 footnote).  Iteration it uses
+    walk_id_base = base + it*n so every iteration draws fresh random numbers."""
+    mpg_guide_reset(ds.guide, stream)
+    base = opts.walk_id_base
+    for it in range(iterations):
+        opts.walk_id_base = base + it * b.n
+        run_step(ds, b, opts, stream, estimate=True, accumulate=True)
+        if on_iteration is not None:
+            on_iteration(it)
+        mpg_guide_rebuild(ds.guide, stream)
+    opts.walk_id_base = base
 
 
 def run_step(ds: DeviceScene, b: Batch, opts: mpg_walk_opts, stream=None, estimate=True, accumulate=False):

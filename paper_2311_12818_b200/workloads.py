@@ -73,6 +73,7 @@ class SeedSpec:
     uv_origin: tuple = (0.0, 0.0)    # x = uv_origin[0] + u*uv_scale[0], z = uv_origin[1] + v*uv_scale[1]
     uv_scale: tuple = (1.0, 1.0)
     uv_plane_y: float = 0.0
+    n_types: int = 1                 # SEED_GUIDE_DIR: 126 chain types (n <= 6)
 
 
 @dataclasses.dataclass
@@ -87,6 +88,7 @@ class WalkOpts:
     seed: int = 0
     walk_id_base: int = 0
     flags: int = 0                   # MPG_FLAG_* (4 = MPG_FLAG_NEWTON_F64)
+    max_iters_long: int = 0          # Newton cap for chains with k >= 3 (0: max_iters)
 
 
 FLAG_NEWTON_F64 = 4
@@ -403,7 +405,30 @@ def config3(n_side: int = 1024, spp: int = 1, grid_n: int = 256) -> Workload:
                     recv_shape=(n_side, n_side))
 
 
-CONFIGS = {0: config0, 1: config1, 2: config2, 3: config3}
+def config4(n_side: int = 1024, grid_n: int = 512) -> Workload:
+    """configs[4]: mirror sphere (cfg0) at (-5,0,2.5), glass icosphere (cfg1) at
+    (-5,0,7.5), water pool (cfg2) over [0,10]^2 (SURVEY 8(d) layout); their three
+    lights with the same offsets; 1024^2 receivers on the floor y=-2 over
+    x in [-7.5,10], z in [0,10]; chain length n in 1..6 and type per sample;
+    guide: 16x16 cells x 126 types x 32x32 equal-area direction bins; Newton
+    cap 20 (k<=2) / 40 (k>=3); 8 progressive iterations (bench / run_progressive).
+    The guide starts empty (learned branch absent, reset at iteration 0)."""
+    sph = Surface(SURF_SPHERE, MAT_CONDUCTOR, reflectance=1.0, center=(-5.0, 0.0, 2.5), radius=1.0)
+    P, N, F = icosphere(4, 1.0, center=(-5.0, 0.0, 7.5))
+    ico = Surface(SURF_MESH, MAT_DIELECTRIC, eta_in=1.5, eta_out=1.0, positions=P, normals=N, indices=F)
+    P2, N2, F2 = heightfield_water(grid_n, 10.0, 0.05, 0)
+    water = Surface(SURF_MESH, MAT_DIELECTRIC, eta_in=1.33, eta_out=1.0, positions=P2, normals=N2, indices=F2)
+    lights = [Light(LIGHT_POINT, 1.0, position=(-5.0, 4.0, 2.5)),
+              Light(LIGHT_QUAD, 1.0, position=(-5.0, 5.0, 7.5), edge_u=(1.0, 0.0, 0.0), edge_v=(0.0, 0.0, 1.0)),
+              Light(LIGHT_QUAD, 1.0, position=(5.0, 8.0, 5.0), edge_u=(1.0, 0.0, 0.0), edge_v=(0.0, 0.0, 1.0))]
+    xD, nD = receiver_grid(-7.5, 10.0, n_side, -2.0, 0.0, 10.0, n_side)
+    seed = SeedSpec(SEED_GUIDE_DIR, surf_id=0, k=6, tau=0, grid_origin=(-7.5, 0.0), grid_extent=(17.5, 10.0),
+                    cells_x=16, cells_y=16, bins_x=32, bins_y=32, n_types=126)
+    return Workload("cfg4_mixed_progressive", [sph, ico, water], lights, xD, nD, 1, seed,
+                    WalkOpts(max_iters=20, max_iters_long=40, flags=FLAG_NEWTON_F64), recv_shape=(n_side, n_side))
+
+
+CONFIGS = {0: config0, 1: config1, 2: config2, 3: config3, 4: config4}
 
 
 def scene_extent(w: Workload) -> float:

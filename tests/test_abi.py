@@ -60,7 +60,7 @@ def test_invalid_arguments_rejected_synchronously(L):
 
 def test_struct_layouts():
     # layouts mirrored by the binding (natural alignment, see include/mpg.h)
-    assert C.sizeof(mpg.mpg_walk_opts) == 48
+    assert C.sizeof(mpg.mpg_walk_opts) == 56
     assert C.sizeof(mpg.mpg_walk_stats) == 19 * 8
     assert C.sizeof(mpg.mpg_query) == 32
     assert C.sizeof(mpg.mpg_sampler_desc) == 16

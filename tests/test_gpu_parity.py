@@ -317,3 +317,140 @@ def test_guide_accumulate_and_rebuild():
     assert np.array_equal(pf.cpu().numpy().view(np.uint64), O.guide_tables(hist))
     assert float(H2.abs().sum().item()) == 0.0           # histogram cleared for the next iteration
     ds.close()
+
+
+# ---------------------------------------------------------------------------
+# configs[4]: typed direction guide, per-sample chain type, progressive loop
+# ---------------------------------------------------------------------------
+def _typed_hist(seed=21, cells=256):
+    rng = np.random.default_rng(seed)
+    H = np.zeros((cells, 126, 1024), np.float32)
+    for c in range(cells):
+        if c % 5 == 0:
+            continue                                   # some cells empty
+        for t in (0, 1, 2, 3, 5, 9, 20):               # types R, T, RR, RT, TT... present in the scene
+            m = rng.random(1024) < 0.05
+            H[c, t, m] = rng.lognormal(0, 1, m.sum()).astype(np.float32)
+    return H
+
+
+def _upload_hist(ds, H):
+    import torch
+    from paper_2311_12818_b200 import mpg
+    mpg.mpg_guide_upload(ds.guide, torch.as_tensor(H).cuda())
+    torch.cuda.synchronize()
+
+
+def test_cfg4_dir_tables_bit_exact():
+    import torch
+    from paper_2311_12818_b200 import mpg
+    from oracle import oracle as O
+    w = W.config4(n_side=8, grid_n=16)
+    ds = mpg.DeviceScene(w)
+    H = _typed_hist()
+    _upload_hist(ds, H)
+    npf = torch.empty(256, 6, dtype=torch.int64, device="cuda")
+    tpf = torch.empty(256, 126, dtype=torch.int64, device="cuda")
+    dpf = torch.empty(256, 126, 1024, dtype=torch.int32, device="cuda")
+    mpg.mpg_guide_download_dir_tables(ds.guide, npf, tpf, dpf)
+    torch.cuda.synchronize()
+    rn, rt, rd = O.guide_dir_tables(H)
+    assert np.array_equal(npf.cpu().numpy().view(np.uint64), rn)
+    assert np.array_equal(tpf.cpu().numpy().view(np.uint64), rt)
+    assert np.array_equal(dpf.cpu().numpy().view(np.uint32), rd)
+    ds.close()
+
+
+@pytest.fixture(scope="module")
+def cfg4_guided_run():
+    """One guided iteration with identical tables on both sides (a typed histogram
+    uploaded to the GPU guide and given to the oracle)."""
+    import torch
+    from paper_2311_12818_b200 import mpg
+    from oracle import oracle as O
+    w = W.config4(n_side=96)
+    H = _typed_hist()
+    ds = mpg.DeviceScene(w)
+    _upload_hist(ds, H)
+    b = mpg.Batch(w.xD, w.nD, w.spp, w.seed.k)
+    mpg.run_step(ds, b, ds.opts())
+    torch.cuda.synchronize()
+    g = b.results()
+    g["extent"] = ds.extent
+    ds.close()
+    s = O.OracleScene(w)
+    s.set_dir_hist(H)
+    o = s.walks(np.arange(w.n_walks))
+    return w, g, o, s
+
+
+def test_cfg4_seeds_match_oracle(cfg4_guided_run):
+    w, g, o, s = cfg4_guided_run
+    rng = np.random.default_rng(3)
+    nlearned = 0
+    for i in rng.choice(w.n_walks, 2000, replace=False):
+        d = s.seed_ex(int(i))
+        ct = int(g["seed_ctype"][i])
+        assert (ct & 15) == d["n"]                                    # length: bit-exact
+        assert ((ct >> 12) & 1) == d["learned"]                       # MIS branch: bit-exact
+        assert ((ct >> 4) & 255) == ((d["tau"] if d["learned"] else d["init_bits"]) & 255)
+        assert g["pn"][i] == pytest.approx(d["Pn"], rel=1e-6)
+        assert g["bin"][i] == d["bin"]
+        assert np.abs(g["target"][i, :3] - d["target"]).max() <= 16 * 2.0 ** -24 * 12.0   # sin/cos (R23)
+        nlearned += d["learned"]
+    assert nlearned > 100
+
+
+def test_cfg4_walk_parity(cfg4_guided_run):
+    w, g, o, s = cfg4_guided_run
+    ids = np.arange(w.n_walks)
+    rep = PY.compare(g, o, ids, g["extent"], 6)
+    cg = np.isin(g["status"], (0, 5)); co = np.isin(o["status"], (0, 5))
+    both = cg & co
+    ct = g["ctype"][both]
+    assert np.array_equal(ct & 15, o["k"][both]) and np.array_equal(ct >> 4, o["tau"][both])  # chain types
+    print({k: v for k, v in rep.items() if not isinstance(v, np.ndarray)})
+    assert rep["flag_agree"] >= 0.999
+    assert rep["n_other_chain"] <= max(1, 0.001 * rep["both"])
+    wg, wo = g["w"][both & (g["status"] == 0)], o["w"][both & (g["status"] == 0)]
+    assert np.median(np.abs(wg - wo) / np.maximum(wo, 1e-30)) < 1e-3        # same trials, same P(n)
+
+
+def test_cfg4_progressive_loop_per_iteration():
+    """configs[4] loop on the GPU (reset, then 4 iterations of seeds -> walk ->
+    accumulate -> rebuild).  Each iteration is compared with the oracle run on
+    the same guide (the oracle builds its tables from the GPU's histogram of the
+    previous iteration), and each accumulated histogram with the oracle's
+    accumulation of the same walk outputs."""
+    import torch
+    from paper_2311_12818_b200 import mpg
+    from oracle import oracle as O
+    w = W.config4(n_side=64)
+    ds = mpg.DeviceScene(w)
+    b = mpg.Batch(w.xD, w.nD, w.spp, w.seed.k)
+    opts = ds.opts()
+    s = O.OracleScene(w)
+    H = torch.empty(256, 126, 1024, dtype=torch.float32, device="cuda")
+    log = []
+
+    def hook(it):
+        mpg.mpg_guide_download(ds.guide, H, None)
+        torch.cuda.synchronize()
+        g = b.results()
+        o = s.walks(np.arange(w.n_walks), s.opts(walk_id_base=it * w.n_walks))
+        rep = PY.compare(g, o, np.arange(w.n_walks), ds.extent, 6)
+        hist = H.cpu().numpy()
+        ref = s.accumulate_dir(g["status"], g["w"], g["pos"][:, 0], g["ctype"] & 15, g["ctype"] >> 4)
+        log.append((rep["flag_agree"], int(np.isin(g["status"], (0, 5)).sum()), hist.sum(),
+                    float(g["w"][(g["status"] == 0) & (g["w"] > 0)].astype(np.float64).sum()),
+                    np.abs(hist - ref).max() / max(ref.max(), 1e-30)))
+        s.set_dir_hist(hist)                              # the oracle's next guide = the GPU's histogram
+
+    mpg.run_progressive(ds, b, opts, iterations=4, on_iteration=hook)
+    ds.close()
+    print(log)
+    for agree, nconv, hs, ws, rel in log:
+        assert agree >= 0.998
+        assert hs == pytest.approx(ws, rel=1e-5)          # mass conservation
+        assert rel < 1e-5                                 # same bins, fp32 atomic order
+    assert log[-1][1] > log[0][1]                          # the guide learns

@@ -575,3 +575,118 @@ def test_light_samples_uniform_on_quad():
     assert abs(xs[:, 0].mean()) < 0.01 and abs(xs[:, 2].mean()) < 0.01
     assert xs[:, 0].var() == pytest.approx(1 / 12, rel=0.05)
     assert s.seed(0)[2] == pytest.approx(1.0)
+
+
+# ---------------------------------------------------------------------------
+# configs[4]: typed direction guide and the Eq. 8 / Eq. 13 sampler (R22)
+# ---------------------------------------------------------------------------
+def _random_typed_hist(rng, cells=4, nb=1024):
+    H = np.zeros((cells, 126, nb), np.float32)
+    for c in range(1, cells):                       # cell 0 empty: learned branch absent
+        for t in rng.choice(126, size=12, replace=False):
+            if c == 2 and t >= 62:                  # cell 2: no mass for n = 6
+                continue
+            m = rng.random(nb) < 0.1
+            H[c, t, m] = rng.lognormal(0, 1, m.sum()).astype(np.float32)
+    return H
+
+
+def test_dir_tables_are_defensive_mixtures():
+    rng = np.random.default_rng(11)
+    H = _random_typed_hist(rng)
+    npf, tpf, dpf = O.guide_dir_tables(H)
+    P0 = np.array([1, 1, 1, 1, 1, 0.95]) / 5.95               # RR from bounce 5, gamma 0.95
+    for c in range(H.shape[0]):
+        Pn = np.diff(np.concatenate([[0.0], npf[c].astype(np.float64)])) / float(npf[c, -1])
+        E = H[c].astype(np.float64).sum(1)
+        En = np.array([E[(1 << n) - 2:(1 << (n + 1)) - 2].sum() for n in range(1, 7)])
+        if En.sum() == 0:
+            assert np.allclose(Pn, P0, atol=1e-15)               # learned branch absent
+            continue
+        Pe = 2 * Pn - P0                                        # Eq. 13, alpha = 1/2
+        assert np.all(Pn >= 0.5 * P0 * (1 - 1e-12))               # defensive bound
+        assert np.allclose(Pe, En / En.sum(), atol=1e-5)         # Eq. 10 within 2^-20 quantisation
+        for n in range(1, 7):
+            g0, gn = (1 << n) - 2, 1 << n
+            Eg = E[g0:g0 + gn]
+            w = np.diff(np.concatenate([[0], tpf[c, g0:g0 + gn].astype(np.float64)]))
+            if Eg.sum() == 0:
+                assert w.sum() == 0
+            else:
+                assert np.allclose(w / w.sum(), Eg / Eg.sum(), atol=1e-5)   # Eq. 11
+        for t in range(126):
+            d = np.diff(np.concatenate([[0], dpf[c, t].astype(np.float64)]))
+            if H[c, t].sum() > 0:
+                assert np.allclose(d / d.sum(), H[c, t] / H[c, t].astype(np.float64).sum(), atol=1e-5)
+                assert np.all((d > 0) == (H[c, t] > 0))
+            else:
+                assert d.sum() == 0
+
+
+def test_dir_sampler_follows_eq8_and_eq13():
+    """n ~ P(n) table; the learned branch is taken with probability 1/2 when available
+    (one-sample MIS, Eq. 13); learned types ~ P_e(tau|n) (Eq. 11); initializer
+    directions uniform on the hemisphere (cos(theta), phi uniform; "direction")."""
+    w = W.config4(n_side=4, grid_n=16)
+    rng = np.random.default_rng(12)
+    H = np.zeros((256, 126, 1024), np.float32)
+    Hs = _random_typed_hist(rng, cells=4)
+    rcv = 5
+    cx = int(np.floor(((w.xD[rcv, 0] + 7.5) * 16) / 17.5)); cz = int(np.floor((w.xD[rcv, 2] * 16) / 10.0))
+    H[cz * 16 + cx] = Hs[1]
+    one = dataclasses.replace(w, xD=w.xD[rcv:rcv + 1].copy(), nD=w.nD[:1].copy(), spp=20000)
+    s = O.OracleScene(one)
+    s.set_dir_hist(H)
+    npf, tpf, dpf = s.dir_tables
+    c = cz * 16 + cx
+    Pn = np.diff(np.concatenate([[0.0], npf[c].astype(np.float64)])) / float(npf[c, -1])
+    draws = [s.seed_ex(i) for i in range(20000)]
+    ns = np.array([d["n"] for d in draws])
+    cnt = np.bincount(ns, minlength=7)[1:]
+    chi2 = ((cnt - 20000 * Pn) ** 2 / (20000 * Pn)).sum()
+    assert chi2 < 5 + 6 * np.sqrt(10)
+    assert all(abs(d["Pn"] - Pn[d["n"] - 1]) < 1e-12 for d in draws[:200])
+    E = Hs[1].astype(np.float64).sum(1)
+    avail = [d for d in draws if E[(1 << d["n"]) - 2:(1 << (d["n"] + 1)) - 2].sum() > 0]
+    frac = np.mean([d["learned"] for d in avail])
+    assert abs(frac - 0.5) < 4 * np.sqrt(0.25 / len(avail))
+    init = [d for d in draws if not d["learned"]]
+    dirs = np.array([d["target"] for d in init], np.float64) - one.xD[0]
+    u = np.sort(dirs[:, 1])
+    ks = np.max(np.abs(u - (np.arange(len(u)) + 0.5) / len(u)))
+    assert ks < 1.63 / np.sqrt(len(u)) + 1e-3
+    phi = np.sort((np.arctan2(dirs[:, 2], dirs[:, 0]) + np.pi) / (2 * np.pi))
+    assert np.max(np.abs(phi - (np.arange(len(phi)) + 0.5) / len(phi))) < 1.63 / np.sqrt(len(phi)) + 1e-3
+    # learned types within the most frequent learned length follow P_e(tau|n)
+    lrn = [d for d in draws if d["learned"]]
+    nbest = np.bincount([d["n"] for d in lrn]).argmax()
+    g0, gn = (1 << nbest) - 2, 1 << nbest
+    ts = np.bincount([d["tau"] for d in lrn if d["n"] == nbest], minlength=gn)
+    pt = E[g0:g0 + gn] / E[g0:g0 + gn].sum()
+    m = pt > 0
+    assert np.all(ts[~m] == 0)
+    chi2 = ((ts[m] - ts.sum() * pt[m]) ** 2 / (ts.sum() * pt[m])).sum()
+    assert chi2 < m.sum() + 6 * np.sqrt(2 * m.sum())
+
+
+def run_oracle_progressive(w, iterations):
+    s = O.OracleScene(w)
+    out = []
+    for it in range(iterations):
+        r = s.walks(np.arange(w.n_walks), s.opts(walk_id_base=it * w.n_walks))
+        out.append(r)
+        H = s.accumulate_dir(r["status"], r["w"], r["pos"][:, 0].astype(np.float32), r["k"], r["tau"])
+        s.set_dir_hist(H.astype(np.float32))            # last iteration only (P:426 footnote)
+    return out
+
+
+def test_progressive_loop_learns():
+    """The guided distribution approaches the energy distribution (Eq. 5): after
+    the initializer-only iteration 0, guided iterations convert far more seeds into
+    admissible chains and need fewer reciprocal trials."""
+    w = W.config4(n_side=48, grid_n=64)
+    res = run_oracle_progressive(w, 3)
+    conv = [np.mean(r["status"] == 0) for r in res]
+    tri = [r["trials"][r["trials"] > 0].mean() for r in res]
+    assert conv[2] > 2 * conv[0], conv
+    assert tri[2] < tri[0], tri
