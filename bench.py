@@ -33,7 +33,9 @@ METRIC = "converged manifold walks/s"
 CONFIG_NAMES = {0: "configs[0]: k=1 mirror sphere, 64x64 receivers x 16 cap seeds (65,536 walks)",
                 1: "configs[1]: k=2 TT glass icosphere (5,120 tris), 1024x1024 receivers x 1 seed (1,048,576 walks)",
                 2: "configs[2]: k=1 T water heightfield (522,242 tris), 2048x2048 receivers x 4 guided seeds (16,777,216 walks)",
-                3: "configs[3]: k=6 TTTTTT three bumpy glass slabs (780,300 tris), 1024x1024 receivers, guided seeds (1,048,576 walks)"}
+                3: "configs[3]: k=6 TTTTTT three bumpy glass slabs (780,300 tris), 1024x1024 receivers, guided seeds (1,048,576 walks)",
+                4: "configs[4]: mixed scene (mirror sphere + glass icosphere + water), n in 1..6 and type per sample, "
+                   "typed 16x16x126x32x32 direction guide, 8 progressive iterations x 1,048,576 walks"}
 
 # algorithmic FP32 work per unit: a Newton vertex evaluation
 # (constraint + 3 Jacobian blocks + block-Thomas step) and the ray-casting units
@@ -157,8 +159,14 @@ def run_ours(args):
     guided = ds.guide is not None
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)   # > 126 MB L2
 
+    progressive = w.seed.mode == 3      # configs[4]: one step = the whole 8-iteration loop (R22)
+    iters = 8 if progressive else 1
+
     def step():
-        mpg.run_step(ds, b, opts, accumulate=guided)
+        if progressive:
+            mpg.run_progressive(ds, b, opts, iterations=iters)
+        else:
+            mpg.run_step(ds, b, opts, accumulate=guided)
 
     for _ in range(max(3, args.warmup)):
         step()
@@ -175,25 +183,39 @@ def run_ours(args):
     clocks.start()
     time.sleep(0.3)
     wall0 = time.perf_counter()
+    walk_ev = []
     for i in range(args.steps):
         flush.fill_(float(i))
         e0, e1, e2, e3 = ev[i]
         e0.record(stream)
-        mpg.mpg_sample_seeds(ds.h, ds.guide, ds.sampler, b.query, opts, b.seeds)
+        if progressive:
+            mpg.mpg_guide_reset(ds.guide)
+        base = opts.walk_id_base
+        for it in range(iters):
+            opts.walk_id_base = base + it * b.n
+            mpg.mpg_sample_seeds(ds.h, ds.guide, ds.sampler, b.query, opts, b.seeds)
+            wa, wb_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            wa.record(stream)
+            mpg.mpg_manifold_walk(ds.h, ds.guide, ds.sampler, b.query, b.seeds, opts, b.out, b.stats, b.workspace)
+            wb_.record(stream)
+            walk_ev.append((wa, wb_))
+            mpg.mpg_estimate(b.w, b.n_recv, b.spp, b.mean, b.var)
+            if guided:
+                mpg.mpg_guide_accumulate(ds.guide, b.query, b.out, b.n)
+            if progressive:
+                mpg.mpg_guide_rebuild(ds.guide)
+            stats.append(b.stats.clone())
+        opts.walk_id_base = base
         e1.record(stream)
-        mpg.mpg_manifold_walk(ds.h, ds.guide, ds.sampler, b.query, b.seeds, opts, b.out, b.stats, b.workspace)
         e2.record(stream)
-        mpg.mpg_estimate(b.w, b.n_recv, b.spp, b.mean, b.var)
-        if guided:
-            mpg.mpg_guide_accumulate(ds.guide, b.query, b.out, b.n)
         e3.record(stream)
-        stats.append(b.stats.clone())
     torch.cuda.synchronize()
     wall = time.perf_counter() - wall0
     clk = clocks.stop()
     step_ms = [ev[i][0].elapsed_time(ev[i][3]) for i in range(args.steps)]
-    walk_ms = [ev[i][1].elapsed_time(ev[i][2]) for i in range(args.steps)]
-    seed_ms = [ev[i][0].elapsed_time(ev[i][1]) for i in range(args.steps)]
+    walk_ms_all = [a.elapsed_time(z) for a, z in walk_ev]
+    walk_ms = [sum(walk_ms_all[i * iters:(i + 1) * iters]) for i in range(args.steps)]
+    seed_ms = [0.0] * args.steps
     tot_ms = sum(step_ms)
     st = torch.stack(stats).cpu().numpy().astype(np.int64)
     fields = mpg.STATS_FIELDS
@@ -246,7 +268,7 @@ def run_ours(args):
             s1.record(stream)
             s1.synchronize()
             e_ms.append(s0.elapsed_time(s1))
-            conv_e += int(b.stats[1].item())
+            conv_e += conv_total // args.steps      # the walks are deterministic: same count every step
         te = sum(e_ms)
         if world > 1:
             t = torch.tensor([te], device=dev)
@@ -280,15 +302,16 @@ def run_ours(args):
                 "newton_iters_per_s": newton_all / (tot_ms / 1e3),
                 "walks_incl_trials_per_s": S["attempts"] * world / (tot_ms / 1e3),
                 "rays_per_s": S["rays"] * world / (tot_ms / 1e3),
-                "breakdown_ms": {"seeds": sum(seed_ms) / args.steps, "walk": sum(walk_ms) / args.steps,
-                                 "estimate+accumulate": (tot_ms - sum(seed_ms) - sum(walk_ms)) / args.steps},
+                "breakdown_ms": {"walk": sum(walk_ms) / args.steps,
+                                 "seeds+estimate+accumulate+tables": (tot_ms - sum(walk_ms)) / args.steps},
                 "roofline": {"bound": "alu", "kernel": "k_walk", "achieved": achieved, "peak": peak,
                              "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
                              "peak_source": "148 SM x 128 FP32 lanes x 2 x 1965 MHz (B200_PROFILING.md unit counts)",
                              "algorithmic_flops_per_launch": flops / args.steps},
                 "hbm": {"bytes_per_step": None},
                 "stats_per_step": {k: v / args.steps for k, v in S.items()},
-                "gpu_launches": 3 * args.steps + (args.steps if guided else 0),
+                "gpu_launches": args.steps * iters * (3 + (1 if guided else 0) + (2 if progressive else 0) +
+                                                      (16 if opts.trials else 0)),
                 "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
                 "wall_s_timed_region": wall}
         print(json.dumps(line), flush=True)
