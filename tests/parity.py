@@ -37,12 +37,18 @@ def compare(g, o, ids, extent, k):
            "flag_agree": float((cg == co).mean()), "status_agree": float((gs == os_).mean()),
            "both": int(both.sum())}
     gp = g["pos"][ids][:, :k]
-    dpos = np.linalg.norm(gp - o["pos"][:, :k], axis=2).max(1)
+    dv = np.linalg.norm(gp - o["pos"][:, :k], axis=2)
+    if "k" in o:                       # per-walk chain length (configs[4]): vertices beyond n are unused
+        dv = np.where(np.arange(k)[None, :] < o["k"][:, None], dv, 0.0)
+    dpos = dv.max(1)
     same = both & (dpos < 1e-4 * extent)
     rep["max_dpos_rel"] = float(dpos[same].max() / extent) if same.any() else 0.0
     rep["n_other_chain"] = int((both & ~same).sum())
     gprim = g["prim"][ids][:, :k]
-    same_prim = (gprim == o["prim"][:, :k]).all(1)
+    pm = gprim == o["prim"][:, :k]
+    if "k" in o:
+        pm |= np.arange(k)[None, :] >= o["k"][:, None]
+    same_prim = pm.all(1)
     rep["prim_agree"] = float(same_prim[both].mean()) if both.any() else 1.0
     vis = (gs == 0) & (os_ == 0)
     rep["both_visible"] = int(vis.sum())
