@@ -95,13 +95,17 @@ struct DLight {
     float3 pos, eu, ev, n, l1, l2; // n: emission normal; l1,l2: orthonormal axes of the light plane
 };
 
+// triangle record stride in float4: v0, v1, v2 (48 B; a 64-B record read with two
+// 256-bit loads, LDG.E.ENL2.256, measured no faster on configs[1,2])
+#define TSTRIDE 3
+
 struct DScene {
     int n_surf, n_light, n_tri, n_nodes;
     float extent;
     DSurf surf[DS_MAX_SURF];
     DLight light[DS_MAX_LIGHT];
     const float4 *nodes; // 4 float4 per BVH2 node: child boxes + child refs
-    const float4 *tpos;  // BVH order, 3 float4 per tri; v0.w = original tri id, v1.w = surf id, v2.w = specular flag
+    const float4 *tpos;  // BVH order, TSTRIDE float4 per tri; v0.w = original tri id, v1.w = surf id, v2.w = specular flag
     const float4 *tnrm;  // BVH order, 3 float4 per tri: vertex shading normals
     const int4 *oidx;    // original order: vertex indices (w: BVH slot)
     const float4 *vpos;  // original vertex positions
@@ -215,7 +219,7 @@ __device__ __forceinline__ bool quad_hit(float3 o, float3 d, float3 q0, float3 e
 // and the visibility V of Eq. 2.
 template <bool ANY>
 __device__ bool trace(const DScene &S, float3 o, float3 d, float tmin, float tmax, bool spec_only, Hit &h,
-                      LaneStats &st) {
+                      LaneStats &st, int hint = -1) {
     st.rays++;
     float best = tmax;
     int bprim = -2, bsurf = -1;
@@ -245,6 +249,21 @@ __device__ bool trace(const DScene &S, float3 o, float3 d, float tmin, float tma
         const int SENT = 0x7fffffff, NONE = 0;
         RayW r;
         ray_setup(r, o, d);
+        if (!ANY && hint >= 0) {
+            // Bound the search by the hit on a hinted triangle (the chain vertex's current
+            // triangle on a reprojection ray): the traversal below then only enters boxes
+            // closer than that hit.  The closest hit is unchanged (strict t < best), except
+            // that among hits at exactly equal t the hinted one is kept (shared edges, R17).
+            st.tris++;
+            float4 p0 = __ldg(S.tpos + TSTRIDE * hint), p1 = __ldg(S.tpos + TSTRIDE * hint + 1),
+                   p2 = __ldg(S.tpos + TSTRIDE * hint + 2);
+            float t, c0, c1, c2;
+            if (!(spec_only && __float_as_int(p2.w) == 0) &&
+                tri_hit(r, xyz(p0), xyz(p1), xyz(p2), tmin, best, t, c0, c1, c2)) {
+                best = t; bprim = hint; bsurf = __float_as_int(p1.w);
+                bb0 = c0; bb1 = c1; bb2 = c2;
+            }
+        }
         int stack[64];
         stack[0] = SENT;
         int sp = 1;
@@ -288,7 +307,8 @@ __device__ bool trace(const DScene &S, float3 o, float3 d, float tmin, float tma
                 int start = v >> 3, cnt = (v & 7) + 1;
                 for (int j = start; j < start + cnt; j++) {
                     st.tris++;
-                    float4 p0 = __ldg(S.tpos + 3 * j), p1 = __ldg(S.tpos + 3 * j + 1), p2 = __ldg(S.tpos + 3 * j + 2);
+                    float4 p0 = __ldg(S.tpos + TSTRIDE * j), p1 = __ldg(S.tpos + TSTRIDE * j + 1),
+                           p2 = __ldg(S.tpos + TSTRIDE * j + 2);
                     if (spec_only && __float_as_int(p2.w) == 0) continue;
                     float t, c0, c1, c2;
                     if (tri_hit(r, xyz(p0), xyz(p1), xyz(p2), tmin, best, t, c0, c1, c2)) {
@@ -310,8 +330,8 @@ __device__ bool trace(const DScene &S, float3 o, float3 d, float tmin, float tma
     if (bsurf < 0) return false;
     if (bprim >= 0) {
         // hit point from barycentrics: lies on the triangle plane up to rounding
-        float3 v0 = xyz(__ldg(S.tpos + 3 * bprim)), v1 = xyz(__ldg(S.tpos + 3 * bprim + 1)),
-               v2 = xyz(__ldg(S.tpos + 3 * bprim + 2));
+        float3 v0 = xyz(__ldg(S.tpos + TSTRIDE * bprim)), v1 = xyz(__ldg(S.tpos + TSTRIDE * bprim + 1)),
+               v2 = xyz(__ldg(S.tpos + TSTRIDE * bprim + 2));
         h.p = v0 * bb0 + v1 * bb1 + v2 * bb2;
     } else {
         h.p = bp;
@@ -325,8 +345,8 @@ __device__ bool trace(const DScene &S, float3 o, float3 d, float tmin, float tma
 __device__ __forceinline__ float3 geo_normal(const DScene &S, int prim, int surf, float3 p) {
     const DSurf &f = S.surf[surf];
     if (prim >= 0) {
-        float3 v0 = xyz(__ldg(S.tpos + 3 * prim)), v1 = xyz(__ldg(S.tpos + 3 * prim + 1)),
-               v2 = xyz(__ldg(S.tpos + 3 * prim + 2));
+        float3 v0 = xyz(__ldg(S.tpos + TSTRIDE * prim)), v1 = xyz(__ldg(S.tpos + TSTRIDE * prim + 1)),
+               v2 = xyz(__ldg(S.tpos + TSTRIDE * prim + 2));
         return nrmz(cross(v1 - v0, v2 - v0));
     }
     if (f.kind == 0) return nrmz(p - f.center);
@@ -338,8 +358,8 @@ __device__ __forceinline__ float3 geo_normal(const DScene &S, int prim, int surf
 __device__ __forceinline__ float3 shading(const DScene &S, int prim, int surf, float3 p, float3 a, float3 b,
                                           float3 &dna, float3 &dnb) {
     if (prim >= 0) {
-        float3 v0 = xyz(__ldg(S.tpos + 3 * prim)), v1 = xyz(__ldg(S.tpos + 3 * prim + 1)),
-               v2 = xyz(__ldg(S.tpos + 3 * prim + 2));
+        float3 v0 = xyz(__ldg(S.tpos + TSTRIDE * prim)), v1 = xyz(__ldg(S.tpos + TSTRIDE * prim + 1)),
+               v2 = xyz(__ldg(S.tpos + TSTRIDE * prim + 2));
         float3 n0 = xyz(__ldg(S.tnrm + 3 * prim)), n1 = xyz(__ldg(S.tnrm + 3 * prim + 1)),
                n2 = xyz(__ldg(S.tnrm + 3 * prim + 2));
         float3 e1 = v1 - v0, e2 = v2 - v0;

@@ -356,7 +356,7 @@ extern "C" mpg_status mpg_scene_create(const mpg_surface_desc *surfaces, int32_t
             int4 ch = make_int4(nd.c0, nd.c1, 0, 0);
             memcpy(&nodes4[4 * i + 3], &ch, sizeof(int4));
         }
-        tpos.resize(3 * d.n_tri);
+        tpos.assign((size_t)TSTRIDE * d.n_tri, make_float4(0.f, 0.f, 0.f, 0.f));
         tnrm.resize(3 * d.n_tri);
         for (int j = 0; j < d.n_tri; j++) {
             int t = B.idx[j];
@@ -369,7 +369,7 @@ extern "C" mpg_status mpg_scene_create(const mpg_surface_desc *surfaces, int32_t
             memcpy(&a.w, &tw, 4);
             memcpy(&b.w, &sid, 4);
             memcpy(&c.w, &spec, 4);
-            tpos[3 * j] = a; tpos[3 * j + 1] = b; tpos[3 * j + 2] = c;
+            tpos[TSTRIDE * j] = a; tpos[TSTRIDE * j + 1] = b; tpos[TSTRIDE * j + 2] = c;
             tnrm[3 * j] = vnrm[ix.x]; tnrm[3 * j + 1] = vnrm[ix.y]; tnrm[3 * j + 2] = vnrm[ix.z];
         }
     }
@@ -406,7 +406,7 @@ __global__ void k_trace(const DScene S, const float4 *orig, const float4 *dir, i
         Hit h;
         bool ok = trace<false>(S, xyz(orig[i]), nrmz(xyz(dir[i])), tmin, 3.0e38f, spec_only != 0, h, ls);
         t[i] = ok ? h.t : -1.0f;
-        prim[i] = ok && h.prim >= 0 ? __float_as_int(S.tpos[3 * h.prim].w) : -1;
+        prim[i] = ok && h.prim >= 0 ? __float_as_int(S.tpos[TSTRIDE * h.prim].w) : -1;
         surf[i] = ok ? h.surf : -1;
     }
 }
@@ -876,12 +876,13 @@ static size_t mk_ws_bytes(int64_t n) { // hard lists A/B: walk (8 B), psurf, pct
     return 256 + 2 * cap * (sizeof(int64_t) + 3 * sizeof(uint32_t));
 }
 
-// wavefront workspace layout: header, ray lists, free stack,
-// per-slot SoA state, hard entries, trial items
+// wavefront workspace layout: header, slot lists, free stack,
+// per-slot SoA state, ray lists, hits, hard entries, trial items
 struct WFLayout {
     uint32_t S, H, C;
     size_t hdr, list0, list1, fstack, s_walk, s_trial, s_flags, s_surf, s_ysurf, s_psurf, s_entry, s_beta, s_tgt,
-        s_x, s_dq, s_y, e_walk, e_psurf, e_best, e_issued, e_pending, e_batch, it_entry, it_trial, total;
+        s_x, s_dq, s_y, s_ctype, s_tau, s_pct, s_pn, r0o0, r0d0, r0o1, r0d1, ro[WF_KMAX], rd[WF_KMAX], h_p, h_s,
+        e_walk, e_psurf, e_pct, e_best, e_issued, e_pending, e_batch, it_entry, it_trial, total;
 };
 static WFLayout wf_layout(int64_t n, int k) {
     WFLayout L;
@@ -896,8 +897,16 @@ static WFLayout wf_layout(int64_t n, int k) {
     L.s_walk = take(4ull * L.S); L.s_trial = take(4ull * L.S); L.s_flags = take(4ull * L.S);
     L.s_surf = take(4ull * L.S); L.s_ysurf = take(4ull * L.S); L.s_psurf = take(4ull * L.S);
     L.s_entry = take(4ull * L.S); L.s_beta = take(4ull * L.S); L.s_tgt = take(16ull * L.S);
-    L.s_x = take(32ull * L.S * k); L.s_dq = take(16ull * L.S * k); L.s_y = take(32ull * L.S * k);
-    L.e_walk = take(4ull * L.H); L.e_psurf = take(4ull * L.H); L.e_best = take(4ull * L.H);
+    L.s_x = take(32ull * L.S * k); L.s_dq = take(32ull * L.S * k); L.s_y = take(32ull * L.S * k);
+    L.s_ctype = take(4ull * L.S); L.s_tau = take(4ull * L.S); L.s_pct = take(4ull * L.S); L.s_pn = take(4ull * L.S);
+    const size_t r0 = 16ull * L.S * (k + 1);
+    L.r0o0 = take(r0); L.r0d0 = take(r0); L.r0o1 = take(r0); L.r0d1 = take(r0);
+    for (int i = 0; i < WF_KMAX; i++) {
+        L.ro[i] = i >= 1 && i < k ? take(16ull * L.S) : 0;
+        L.rd[i] = i >= 1 && i < k ? take(16ull * L.S) : 0;
+    }
+    L.h_p = take(16ull * L.S); L.h_s = take(4ull * L.S);
+    L.e_walk = take(4ull * L.H); L.e_psurf = take(4ull * L.H); L.e_pct = take(4ull * L.H); L.e_best = take(4ull * L.H);
     L.e_issued = take(4ull * L.H); L.e_pending = take(4ull * L.H); L.e_batch = take(4ull * L.H);
     L.it_entry = take(4ull * L.C); L.it_trial = take(4ull * L.C);
     L.total = o;
@@ -965,7 +974,7 @@ struct WFGraphCache {
 };
 static WFGraphCache g_wfcache;
 
-template <int KMAX>
+template <int KMAX, typename R>
 static mpg_status launch_wavefront(const DScene &S, const SeedCtx &g, const WalkParams &MP, void *ws, size_t wsb,
                                    cudaStream_t st) {
     WFLayout L = wf_layout(MP.n, g.k);
@@ -980,6 +989,8 @@ static mpg_status launch_wavefront(const DScene &S, const SeedCtx &g, const Walk
     P.max_iters = MP.max_iters; P.trials_on = MP.trials_on; P.k_max = MP.k_max;
     P.tol = MP.tol; P.beta0 = MP.beta0; P.same_eps = MP.same_eps; P.ray_eps = MP.ray_eps;
     P.walk_id_base = MP.walk_id_base;
+    P.seed_ctype = MP.seed_ctype; P.seed_pn = MP.seed_pn; P.out_ctype = MP.out_ctype;
+    P.max_iters_long = MP.max_iters_long;
     P.hdr = (WFHeader *)(b + L.hdr);
     P.S = L.S; P.H = L.H; P.C = L.C;
     P.list[0] = (uint32_t *)(b + L.list0); P.list[1] = (uint32_t *)(b + L.list1);
@@ -988,32 +999,49 @@ static mpg_status launch_wavefront(const DScene &S, const SeedCtx &g, const Walk
     P.s_flags = (uint32_t *)(b + L.s_flags); P.s_surf = (uint32_t *)(b + L.s_surf);
     P.s_ysurf = (uint32_t *)(b + L.s_ysurf); P.s_psurf = (uint32_t *)(b + L.s_psurf);
     P.s_entry = (int32_t *)(b + L.s_entry); P.s_beta = (float *)(b + L.s_beta);
-    P.s_tgt = (float4 *)(b + L.s_tgt); P.s_x = (double4 *)(b + L.s_x); P.s_dq = (float4 *)(b + L.s_dq);
+    P.s_tgt = (float4 *)(b + L.s_tgt); P.s_x = (double4 *)(b + L.s_x); P.s_dq = (double4 *)(b + L.s_dq);
     P.s_y = (double4 *)(b + L.s_y);
-    P.e_walk = (int32_t *)(b + L.e_walk); P.e_psurf = (uint32_t *)(b + L.e_psurf);
+    P.s_ctype = (uint32_t *)(b + L.s_ctype); P.s_tau = (uint32_t *)(b + L.s_tau);
+    P.s_pct = (uint32_t *)(b + L.s_pct); P.s_pn = (float *)(b + L.s_pn);
+    P.r0o0 = (float4 *)(b + L.r0o0); P.r0d0 = (float4 *)(b + L.r0d0);
+    P.r0o1 = (float4 *)(b + L.r0o1); P.r0d1 = (float4 *)(b + L.r0d1);
+    P.h_p = (float4 *)(b + L.h_p); P.h_s = (int32_t *)(b + L.h_s);
+    P.e_walk = (int32_t *)(b + L.e_walk); P.e_psurf = (uint32_t *)(b + L.e_psurf); P.e_pct = (uint32_t *)(b + L.e_pct);
     P.e_best = (uint32_t *)(b + L.e_best); P.e_issued = (uint32_t *)(b + L.e_issued);
     P.e_pending = (uint32_t *)(b + L.e_pending); P.e_batch = (uint32_t *)(b + L.e_batch);
     P.it_entry = (int32_t *)(b + L.it_entry); P.it_trial = (uint32_t *)(b + L.it_trial);
+    const int nk = std::max(1, std::min(g.k, KMAX));   // sub-steps per wave
+    float4 *ro[WF_KMAX + 1], *rd[WF_KMAX + 1];
+    for (int i = 0; i <= WF_KMAX; i++) {
+        ro[i] = i >= 1 && i < nk ? (float4 *)(b + L.ro[i]) : nullptr;
+        rd[i] = i >= 1 && i < nk ? (float4 *)(b + L.rd[i]) : nullptr;
+    }
 
     static int occ_t = 0, occ_u = 0;
     if (!occ_t) {
-        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_t, k_wf_trace<KMAX>, 128, 0));
-        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_u, k_wf_update<KMAX>, 128, 0));
+        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_t, k_wf_rays, 128, 0));
+        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_u, k_wf_update<KMAX, R>, 128, 0));
         occ_t = std::max(occ_t, 1); occ_u = std::max(occ_u, 1);
     }
     int gt = num_sms() * occ_t;
+    int gp0 = (int)std::min<int64_t>(((int64_t)L.S * (nk + 1) + 127) / 128, (int64_t)num_sms() * 16);
+    int gp = (int)std::min<int64_t>((L.S + 127) / 128, (int64_t)num_sms() * 16);
     int gu = (int)std::min<int64_t>((L.S + 127) / 128, (int64_t)num_sms() * occ_u * 4);
     int gr = (int)std::min<int64_t>((L.S + 255) / 256, (int64_t)num_sms() * 8);
     int gi = (int)std::min<int64_t>((L.S + 255) / 256, (int64_t)num_sms() * 8);
 
+    CUDA_TRY(cudaMemsetAsync(P.hdr, 0, sizeof(WFHeader), st));
     if (MP.host_loop) { // host-driven waves (profilers cannot see kernels inside conditional graphs)
         P.use_cond = 0;
         k_wf_init<KMAX><<<gi, 256, 0, st>>>(S, g, P);
         CUDA_TRY(cudaPeekAtLastError());
         unsigned int more = 1;
         for (int wave = 0; more; wave++) {
-            k_wf_trace<KMAX><<<gt, 128, 0, st>>>(S, g, P);
-            k_wf_update<KMAX><<<gu, 128, 0, st>>>(S, g, P);
+            for (int i = 0; i < nk; i++) {
+                k_wf_rays<<<gt, 128, 0, st>>>(S, P, i, ro[i], rd[i]);
+                k_wf_post<<<i == 0 ? gp0 : gp, 128, 0, st>>>(S, P, i, rd[i], ro[i + 1], rd[i + 1]);
+            }
+            k_wf_update<KMAX, R><<<gu, 128, 0, st>>>(S, g, P);
             k_wf_plan<<<1, 1, 0, st>>>(P);
             k_wf_refill<KMAX><<<gr, 256, 0, st>>>(S, g, P);
             CUDA_TRY(cudaPeekAtLastError());
@@ -1026,14 +1054,14 @@ static mpg_status launch_wavefront(const DScene &S, const SeedCtx &g, const Walk
     }
     P.use_cond = 1;
     // graph cache key: every byte the graph depends on
-    std::vector<char> key(sizeof(DScene) + sizeof(SeedCtx) + sizeof(WFParams) + 4 * sizeof(int));
+    std::vector<char> key(sizeof(DScene) + sizeof(SeedCtx) + sizeof(WFParams) + 8 * sizeof(int));
     {
         char *kp = key.data();
         memcpy(kp, &S, sizeof(DScene)); kp += sizeof(DScene);
         memcpy(kp, &g, sizeof(SeedCtx)); kp += sizeof(SeedCtx);
         WFParams Pk = P; Pk.cond = 0;
         memcpy(kp, &Pk, sizeof(WFParams)); kp += sizeof(WFParams);
-        int dims[4] = {gt, gu, gr, KMAX};
+        int dims[8] = {gt, gu, gr, KMAX * 16 + (int)sizeof(R), nk, gp0, gp, 0};
         memcpy(kp, dims, sizeof(dims));
     }
     if (!g_wfcache.exec || g_wfcache.key != key) {
@@ -1053,18 +1081,30 @@ static mpg_status launch_wavefront(const DScene &S, const SeedCtx &g, const Walk
         CUDA_TRY(cudaGraphAddNode(&cnode, graph, nullptr, 0, &cp));
         cudaGraph_t body = cp.conditional.phGraph_out[0];
         DScene Sv = S; SeedCtx gv = g; WFParams Pv = P;
+        int subs[WF_KMAX];
         void *args3[] = {&Sv, &gv, &Pv};
         void *args1[] = {&Pv};
-        cudaKernelNodeParams kt = {}, ku = {}, kpn = {}, kr = {};
-        kt.func = (void *)k_wf_trace<KMAX>; kt.gridDim = dim3(gt); kt.blockDim = dim3(128); kt.kernelParams = args3;
-        ku.func = (void *)k_wf_update<KMAX>; ku.gridDim = dim3(gu); ku.blockDim = dim3(128); ku.kernelParams = args3;
-        kpn.func = (void *)k_wf_plan; kpn.gridDim = dim3(1); kpn.blockDim = dim3(1); kpn.kernelParams = args1;
-        kr.func = (void *)k_wf_refill<KMAX>; kr.gridDim = dim3(gr); kr.blockDim = dim3(256); kr.kernelParams = args3;
-        cudaGraphNode_t n1, n2, n3, n4;
-        CUDA_TRY(cudaGraphAddKernelNode(&n1, body, nullptr, 0, &kt));
-        CUDA_TRY(cudaGraphAddKernelNode(&n2, body, &n1, 1, &ku));
-        CUDA_TRY(cudaGraphAddKernelNode(&n3, body, &n2, 1, &kpn));
-        CUDA_TRY(cudaGraphAddKernelNode(&n4, body, &n3, 1, &kr));
+        void *argr[WF_KMAX][5], *argp[WF_KMAX][6];
+        cudaGraphNode_t prev = nullptr;
+        auto add = [&](void *fn, int grid, int block, void **args) -> cudaError_t {
+            cudaKernelNodeParams kn = {};
+            kn.func = fn; kn.gridDim = dim3(grid); kn.blockDim = dim3(block); kn.kernelParams = args;
+            cudaGraphNode_t nd;
+            cudaError_t e = cudaGraphAddKernelNode(&nd, body, prev ? &prev : nullptr, prev ? 1 : 0, &kn);
+            prev = nd;
+            return e;
+        };
+        for (int i = 0; i < nk; i++) {
+            subs[i] = i;
+            argr[i][0] = &Sv; argr[i][1] = &Pv; argr[i][2] = &subs[i]; argr[i][3] = &ro[i]; argr[i][4] = &rd[i];
+            argp[i][0] = &Sv; argp[i][1] = &Pv; argp[i][2] = &subs[i]; argp[i][3] = &rd[i];
+            argp[i][4] = &ro[i + 1]; argp[i][5] = &rd[i + 1];
+            CUDA_TRY(add((void *)k_wf_rays, gt, 128, argr[i]));
+            CUDA_TRY(add((void *)k_wf_post, i == 0 ? gp0 : gp, 128, argp[i]));
+        }
+        CUDA_TRY(add((void *)k_wf_update<KMAX, R>, gu, 128, args3));
+        CUDA_TRY(add((void *)k_wf_plan, 1, 1, args1));
+        CUDA_TRY(add((void *)k_wf_refill<KMAX>, gr, 256, args3));
         cudaGraphExec_t ex;
         CUDA_TRY(cudaGraphInstantiate(&ex, graph, 0));
         g_wfcache.graph = graph;
@@ -1142,18 +1182,21 @@ extern "C" mpg_status mpg_manifold_walk(const mpg_scene *scene, const mpg_guide 
         P.hard_count = (unsigned int *)(base + 16);
     }
     int k = g.k;
-    ARG_CHECK(!((o->flags & MPG_FLAG_WAVEFRONT) && (o->flags & MPG_FLAG_NEWTON_F64)),
-              "MPG_FLAG_NEWTON_F64 is implemented on the default path only");
-    ARG_CHECK(!((o->flags & MPG_FLAG_WAVEFRONT) && sd->mode == MPG_SEED_GUIDE_DIR),
-              "MPG_SEED_GUIDE_DIR is implemented on the default path only");
     if (sd->mode == MPG_SEED_GUIDE_DIR)
         ARG_CHECK(sb->ctype && sb->pn && out->ctype, "GUIDE_DIR needs seed ctype/pn and walk ctype arrays");
     if (o->flags & MPG_FLAG_WAVEFRONT) {
-        if (k <= 1) return launch_wavefront<1>(scene->d, g, P, workspace, workspace_bytes, s);
-        if (k <= 2) return launch_wavefront<2>(scene->d, g, P, workspace, workspace_bytes, s);
-        if (k <= 4) return launch_wavefront<4>(scene->d, g, P, workspace, workspace_bytes, s);
-        if (k <= 6) return launch_wavefront<6>(scene->d, g, P, workspace, workspace_bytes, s);
-        return launch_wavefront<8>(scene->d, g, P, workspace, workspace_bytes, s);
+        if (o->flags & MPG_FLAG_NEWTON_F64) {
+            if (k <= 1) return launch_wavefront<1, double>(scene->d, g, P, workspace, workspace_bytes, s);
+            if (k <= 2) return launch_wavefront<2, double>(scene->d, g, P, workspace, workspace_bytes, s);
+            if (k <= 4) return launch_wavefront<4, double>(scene->d, g, P, workspace, workspace_bytes, s);
+            if (k <= 6) return launch_wavefront<6, double>(scene->d, g, P, workspace, workspace_bytes, s);
+            return launch_wavefront<8, double>(scene->d, g, P, workspace, workspace_bytes, s);
+        }
+        if (k <= 1) return launch_wavefront<1, float>(scene->d, g, P, workspace, workspace_bytes, s);
+        if (k <= 2) return launch_wavefront<2, float>(scene->d, g, P, workspace, workspace_bytes, s);
+        if (k <= 4) return launch_wavefront<4, float>(scene->d, g, P, workspace, workspace_bytes, s);
+        if (k <= 6) return launch_wavefront<6, float>(scene->d, g, P, workspace, workspace_bytes, s);
+        return launch_wavefront<8, float>(scene->d, g, P, workspace, workspace_bytes, s);
     }
     CUDA_TRY(cudaMemsetAsync(workspace, 0, 64, s));
     if (o->flags & MPG_FLAG_NEWTON_F64) {

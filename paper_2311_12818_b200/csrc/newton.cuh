@@ -46,8 +46,8 @@ template <typename R> __device__ __forceinline__ void onbR(V3<R> n, V3<R> &b1, V
 // geometric normal (outward, R9)
 template <typename R> __device__ __forceinline__ V3<R> geo_normalR(const DScene &S, int prim, int surf, double3 p) {
     if (prim >= 0) {
-        V3<R> v0 = fromf<R>(xyz(__ldg(S.tpos + 3 * prim))), v1 = fromf<R>(xyz(__ldg(S.tpos + 3 * prim + 1))),
-              v2 = fromf<R>(xyz(__ldg(S.tpos + 3 * prim + 2)));
+        V3<R> v0 = fromf<R>(xyz(__ldg(S.tpos + TSTRIDE * prim))), v1 = fromf<R>(xyz(__ldg(S.tpos + TSTRIDE * prim + 1))),
+              v2 = fromf<R>(xyz(__ldg(S.tpos + TSTRIDE * prim + 2)));
         return nrmR(crossR(v1 - v0, v2 - v0));
     }
     const DSurf &f = S.surf[surf];
@@ -60,9 +60,9 @@ template <typename R>
 __device__ __forceinline__ V3<R> shadingR(const DScene &S, int prim, int surf, double3 p, V3<R> a, V3<R> b,
                                           V3<R> &dna, V3<R> &dnb) {
     if (prim >= 0) {
-        float3 fv0 = xyz(__ldg(S.tpos + 3 * prim));
-        V3<R> v0 = fromf<R>(fv0), v1 = fromf<R>(xyz(__ldg(S.tpos + 3 * prim + 1))),
-              v2 = fromf<R>(xyz(__ldg(S.tpos + 3 * prim + 2)));
+        float3 fv0 = xyz(__ldg(S.tpos + TSTRIDE * prim));
+        V3<R> v0 = fromf<R>(fv0), v1 = fromf<R>(xyz(__ldg(S.tpos + TSTRIDE * prim + 1))),
+              v2 = fromf<R>(xyz(__ldg(S.tpos + TSTRIDE * prim + 2)));
         V3<R> n0 = fromf<R>(xyz(__ldg(S.tnrm + 3 * prim))), n1 = fromf<R>(xyz(__ldg(S.tnrm + 3 * prim + 1))),
               n2 = fromf<R>(xyz(__ldg(S.tnrm + 3 * prim + 2)));
         V3<R> e1 = v1 - v0, e2 = v2 - v0;

@@ -111,7 +111,7 @@ __device__ __forceinline__ double3 refine_hit(const DScene &S, int prim, int sur
     double dx = q.x - ox, dy = q.y - oy, dz = q.z - oz;
     double t;
     if (prim >= 0) {
-        float3 a = xyz(__ldg(S.tpos + 3 * prim)), b = xyz(__ldg(S.tpos + 3 * prim + 1)), c = xyz(__ldg(S.tpos + 3 * prim + 2));
+        float3 a = xyz(__ldg(S.tpos + TSTRIDE * prim)), b = xyz(__ldg(S.tpos + TSTRIDE * prim + 1)), c = xyz(__ldg(S.tpos + TSTRIDE * prim + 2));
         double e1x = (double)b.x - a.x, e1y = (double)b.y - a.y, e1z = (double)b.z - a.z;
         double e2x = (double)c.x - a.x, e2y = (double)c.y - a.y, e2z = (double)c.z - a.z;
         double nx = e1y * e2z - e1z * e2y, ny = e1z * e2x - e1x * e2z, nz = e1x * e2y - e1y * e2x;
@@ -154,7 +154,8 @@ __device__ __forceinline__ double3 refine_hit(const DScene &S, int prim, int sur
 // a conductor fails (R22, R14).  The resolved string is returned in tau_res.
 template <int KMAX>
 __device__ __forceinline__ int trace_chain(const DScene &S, bool deduce, int k, uint32_t bits, bool learned,
-                                           float3 xD, float3 tgt, const double3 *q, uint32_t surf_req, float eps,
+                                           float3 xD, float3 tgt, const double3 *q, const int *hint,
+                                           uint32_t surf_req, float eps,
                                            double3 *y, int *yp, int *ys, LaneStats &st, uint32_t &tau_res) {
     uint32_t res = 0;
     double3 o = d3f(xD);
@@ -177,7 +178,7 @@ __device__ __forceinline__ int trace_chain(const DScene &S, bool deduce, int k, 
         }
         Hit h;
         float3 of = f3d(o), d = nrmz(f3d(dd));
-        if (!trace<false>(S, of, d, eps, 3.0e38f, true, h, st)) return 1 | (i << 4);
+        if (!trace<false>(S, of, d, eps, 3.0e38f, true, h, st, deduce ? -1 : hint[i])) return 1 | (i << 4);
         if (!deduce && h.surf != (int)((surf_req >> (4 * i)) & 15u)) return 2 | (i << 4);
         if (deduce) {
             uint32_t bit = (bits >> i) & 1u;
@@ -330,7 +331,7 @@ __global__ void __launch_bounds__(128, (KMAX <= 2 ? 6 : 2)) k_walk(const DScene 
 #pragma unroll
             for (int i = 0; i < KMAX; i++) sreq |= (uint32_t)(surf[i] & 15) << (4 * i);
             uint32_t tres = tau;
-            int why = trace_chain<KMAX>(S, ded, k, bits, learned, xD, tgt, q, sreq, P.ray_eps, y, yp, ys, ls, tres);
+            int why = trace_chain<KMAX>(S, ded, k, bits, learned, xD, tgt, q, prim, sreq, P.ray_eps, y, yp, ys, ls, tres);
             bool ok = why == 0;
             if (ok && ded) tau = tres;
             if (!ok && !ded && P.dbg && trial == 0 && w < P.n_dbg && 2 * it + 3 < P.dbg_stride)
@@ -425,7 +426,7 @@ __global__ void __launch_bounds__(128, (KMAX <= 2 ? 6 : 2)) k_walk(const DScene 
 #pragma unroll
                     for (int i = 0; i < KMAX; i++) {
                         if (i >= k) break;
-                        int pid = prim[i] >= 0 ? __float_as_int(__ldg(S.tpos + 3 * prim[i]).w) : -1;
+                        int pid = prim[i] >= 0 ? __float_as_int(__ldg(S.tpos + TSTRIDE * prim[i]).w) : -1;
                         P.chain[(int64_t)i * P.n + w] = make_float4((float)x[i].x, (float)x[i].y, (float)x[i].z, __int_as_float(pid));
                     }
                 }

@@ -1,44 +1,65 @@
-// wavefront.cuh -- wavefront formulation of the batched manifold walk (default path).
+// wavefront.cuh -- wavefront formulation of the batched manifold walk (MPG_FLAG_WAVEFRONT).
 //
-// The megakernel (walk.cuh) keeps one chain per lane, so a warp waits for the
-// slowest of 32 chained ray traversals each Newton iteration: ncu measured 4.6
-// active threads per warp.  Here the walk state lives in S "slots" in global
-// memory (SoA) and every Newton iteration is one *wave* of four kernels, run
-// by a CUDA-graph while loop (device-side cudaGraphSetConditional, no host sync):
+// The persistent one-chain-per-lane kernel (walk.cuh) runs BVH traversal at
+// ~6 active threads per warp (ncu, configs[1]): a lane's next ray depends on
+// its own chain, so a warp waits for its slowest traversal and cannot refill
+// finished lanes.  Here the walk state lives in S "slots" in global memory
+// (SoA) and rays are separated from the chain arithmetic.  One Newton
+// iteration of every active slot is one *wave*, run by a CUDA-graph while loop
+// (device-side cudaGraphSetConditional, no host round trip):
 //
-//   k_wf_trace   persistent, per-lane job fetch (Aila & Laine 2009): a job is
-//                the k sequential rays of one slot (deduction, Eq. 6, or
-//                ray-traced reprojection); a lane that finishes its job takes
-//                the next one, so traversal runs with full warps regardless of
-//                per-ray trip counts.  While-while traversal, postponed leaves.
-//   k_wf_update  one thread per traced slot: accept/halve (R6), Newton system
-//                fused with block-Thomas (R1-R4, R7), step; at the end of an
-//                attempt: sides (R8), visibility, kappa, G, T (Eq. 2); trials
-//                (Eq. 15): sequential up to LOCAL_TRIALS, then the walk becomes
-//                a "hard entry" whose further trials run as independent items
-//                in doubling batches; k = min successful trial (exactly the
-//                sequential geometric count).  Freed slots go to a free stack.
-//   k_wf_plan    one thread: snapshot of free slots / pending items / queue,
-//                assignment plan, loop condition.
-//   k_wf_refill  assigns hard-entry trial items, then new primary walks, to
-//                free slots (deterministic from the plan, no contention).
+//   for sub-step i = 0 .. KMAX-1:
+//     k_wf_rays(i)  pure ray engine over ray list i: persistent warps,
+//                   while-while traversal with postponed leaves and dynamic
+//                   fetch (a warp refills finished lanes from the list as soon
+//                   as fewer than WF_FETCH_MIN lanes are still traversing).
+//                   A ray is 32 B (origin, t_max or a hinted triangle, direction, slot | any-hit
+//                   bit); a closest hit is written per slot, an any-hit
+//                   (visibility) ORs F_FAIL into the slot.
+//     k_wf_post(i)  one thread per chain ray of list i: fp64 hit refinement
+//                   (R24), surface / type checks (R22, R14), scatter
+//                   (deduction, Eq. 6) or next reprojection target (R5), and
+//                   emission of ray i+1 into list i+1.
+//   k_wf_update     one thread per slot, no traversal: accept/halve (R6),
+//                   Newton system fused with block-Thomas (R1-R4, R7), step,
+//                   and emission of the next wave's ray 0; at a converged
+//                   primary: sides (R8), kappa, G, T (Eq. 2) and its k+1
+//                   visibility rays; trials (Eq. 15): sequential up to
+//                   WF_LOCAL_TRIALS, then the walk becomes a "hard entry" whose
+//                   trials run as independent items in doubling batches; k = the
+//                   smallest successful trial (exactly the sequential count).
+//   k_wf_plan       one thread: snapshot of free slots / pending items / queue,
+//                   assignment plan, counter resets, loop condition.
+//   k_wf_refill     assigns trial items, then new primary walks, to free slots
+//                   and emits their deduction rays.
+//
+// Every walk's result depends only on its own counter-based draws, not on the
+// slot, lane or wave that ran it: both paths compute the same walks.
 #pragma once
 #include "walk.cuh"
 
 #define WF_LOCAL_TRIALS 4u
 #define WF_BATCH0 4u
 #define WF_NONE 0xffffffffu
-// slot flag bits (s_flags)
-#define F_DEDUCE (1u << 16)
-#define F_FAIL (1u << 17)
-#define F_ITEM (1u << 18)
-#define F_SEEDFAIL (1u << 19)
-#define F_SEQ (1u << 20)      // hard entry continued sequentially in this slot (item list full)
+#define WF_KMAX 8
+#ifndef WF_TRACE_MINB
+#define WF_TRACE_MINB 8
+#endif
+#ifndef WF_FETCH_MIN
+#define WF_FETCH_MIN 16
+#endif
+#define WF_ANY (1u << 31)     // ray meta: any-hit over all surfaces (visibility)
+// slot flag bits (s_flags); bits 0-15: Newton iteration count
 #define F_IT_MASK 0xffffu
+#define F_DEDUCE (1u << 16)   // this wave traces the deduction rays
+#define F_FAIL (1u << 17)     // a ray of this wave failed (miss / wrong surface / TIR / zero length) or was occluded
+#define F_ITEM (1u << 18)     // slot runs a trial item of a hard entry
+#define F_SEQ (1u << 20)      // hard entry continued sequentially in this slot (item list full)
+#define F_VIS (1u << 21)      // this wave traces the visibility segments of a converged primary
 
-struct WFHeader {                 // device counters (in the workspace)
+struct WFHeader {                 // device counters (in the workspace; zeroed before k_wf_init)
     unsigned long long queue;     // next primary walk
-    unsigned int wave;            // parity of the current ray list
+    unsigned int wave;            // parity of the current slot list / ray list 0
     unsigned int list_count[2];
     unsigned int free_top;        // free-slot stack size
     unsigned int n_entries;       // hard entries published
@@ -47,24 +68,29 @@ struct WFHeader {                 // device counters (in the workspace)
     unsigned int plan_free, plan_items, plan_prims, plan_list;
     unsigned long long plan_queue0;
     unsigned int plan_item0;
-    unsigned int trace_cursor;    // job cursor of k_wf_trace (reset by k_wf_plan)
     unsigned int more;            // work remains after this wave (host-loop mode)
+    unsigned int ray0_count[2];   // ray list 0, double-buffered by wave parity
+    unsigned int ray_count[WF_KMAX];  // ray lists i >= 1
+    unsigned int cursor[WF_KMAX];     // ray-engine fetch cursor per sub-step
 };
 
 struct WFParams {
-    // inputs / outputs (as the megakernel)
+    // inputs / outputs (as the persistent kernel)
     const float4 *xD, *nD;
     int64_t n;
     int spp;
     const float4 *seed_xL, *seed_tgt;
     const int *seed_bin;
+    const uint32_t *seed_ctype;
+    const float *seed_pn;
+    uint16_t *out_ctype;
     float4 *chain;
     uint8_t *status;
     uint16_t *iters;
     float *G, *T, *w;
     uint32_t *trials;
     unsigned long long *stats;
-    int max_iters, trials_on;
+    int max_iters, max_iters_long, trials_on;
     uint32_t k_max;
     float tol, beta0, same_eps, ray_eps;
     uint64_t walk_id_base;
@@ -75,14 +101,24 @@ struct WFParams {
     uint32_t *free_stack;
     int32_t *s_walk;
     uint32_t *s_trial, *s_flags, *s_surf, *s_ysurf, *s_psurf;
+    uint32_t *s_ctype;            // n | bits << 4 | learned << 12 of the current attempt
+    uint32_t *s_tau;              // resolved type string of the current chain
+    uint32_t *s_pct;              // primary chain type n | tau << 4 (trials compare against it)
+    float *s_pn;                  // P(n)
     int32_t *s_entry;
     float *s_beta;
     float4 *s_tgt;
-    double4 *s_x, *s_y;           // [k][S] chain / traced vertices (fp64 positions, w = prim)
-    float4 *s_dq;                 // [k][S] Newton step directions
+    double4 *s_x, *s_y;           // [k][S] chain / traced vertices (fp64 positions, w = prim);
+                                  // during deduction s_x[i] holds the fp64 direction of ray i
+    double4 *s_dq;                // [k][S] Newton step directions (R: the Newton precision)
+    // rays: list 0 double-buffered (S * (KMAX + 1) entries: a chain ray or k+1 visibility rays
+    // per slot), lists 1..KMAX-1 (S entries)
+    float4 *r0o0, *r0d0, *r0o1, *r0d1;
+    float4 *h_p;                  // [S] closest hit point (fp32) | prim (w)
+    int32_t *h_s;                 // [S] closest hit surface (-1: miss)
     uint32_t H;                   // hard entry capacity
     int32_t *e_walk;
-    uint32_t *e_psurf, *e_best, *e_issued, *e_pending, *e_batch;
+    uint32_t *e_psurf, *e_pct, *e_best, *e_issued, *e_pending, *e_batch;
     uint32_t C;                   // item capacity
     int32_t *it_entry;
     uint32_t *it_trial;
@@ -93,262 +129,284 @@ struct WFParams {
 // --------------------------------------------------------------------------
 // shared helpers
 // --------------------------------------------------------------------------
-__device__ __forceinline__ void wf_append(const WFParams &P, uint32_t lst, uint32_t slot) {
-    // warp-aggregated append to ray list `lst`
+__device__ __forceinline__ unsigned wf_agg_add(unsigned int *ctr) {   // warp-aggregated atomicAdd(ctr, 1)
     unsigned m = __activemask();
     int leader = __ffs(m) - 1;
     int lane = threadIdx.x & 31;
     unsigned base = 0;
-    if (lane == leader) base = atomicAdd(&P.hdr->list_count[lst], (unsigned)__popc(m));
+    if (lane == leader) base = atomicAdd(ctr, (unsigned)__popc(m));
     base = __shfl_sync(m, base, leader);
-    P.list[lst][base + __popc(m & ((1u << lane) - 1u))] = slot;
+    return base + __popc(m & ((1u << lane) - 1u));
+}
+
+__device__ __forceinline__ void wf_append(const WFParams &P, uint32_t lst, uint32_t slot) {
+    P.list[lst][wf_agg_add(&P.hdr->list_count[lst])] = slot;
 }
 
 __device__ __forceinline__ void wf_free(const WFParams &P, uint32_t slot) {
-    unsigned m = __activemask();
-    int leader = __ffs(m) - 1;
-    int lane = threadIdx.x & 31;
-    unsigned base = 0;
-    if (lane == leader) base = atomicAdd(&P.hdr->free_top, (unsigned)__popc(m));
-    base = __shfl_sync(m, base, leader);
-    P.free_stack[base + __popc(m & ((1u << lane) - 1u))] = slot;
+    P.free_stack[wf_agg_add(&P.hdr->free_top)] = slot;
     P.s_walk[slot] = -1;
 }
 
-// start an attempt (seed) in `slot`: deduction target for (walk, trial)
-__device__ __forceinline__ void wf_seed(const DScene &S, const SeedCtx &g, const WFParams &P, uint32_t slot,
-                                        int64_t w, uint32_t trial, uint32_t extra_flags) {
+// append a ray to list 0 of wave parity `par`
+__device__ __forceinline__ void wf_emit0(const WFParams &P, unsigned par, float3 o, float3 d, float tmax,
+                                         uint32_t meta) {
+    unsigned idx = wf_agg_add(&P.hdr->ray0_count[par]);
+    float4 *ro = par ? P.r0o1 : P.r0o0;
+    float4 *rd = par ? P.r0d1 : P.r0d0;
+    ro[idx] = make_float4(o.x, o.y, o.z, tmax);
+    rd[idx] = make_float4(d.x, d.y, d.z, __uint_as_float(meta));
+}
+
+__device__ __forceinline__ double3 ld3(const double4 *a, size_t i) {
+    double4 v = a[i];
+    return make_double3(v.x, v.y, v.z);
+}
+
+// start an attempt (seed) in `slot` for (walk, trial) and emit its deduction ray 0
+// into ray list 0 of parity `par` (Eq. 6: x_1 = r(x_D, normalize(target - x_D)))
+__device__ __forceinline__ void wf_start(const DScene &S, const SeedCtx &g, const WFParams &P, uint32_t slot,
+                                         int64_t w, uint32_t trial, uint32_t extra_flags, unsigned par) {
     float3 tgt = f3(0.f, 0.f, 0.f);
     bool ok;
+    uint32_t ct;
+    float pn;
+    const float3 xD = xyz(__ldg(P.xD + w / P.spp));
     if (trial == 0) {
         ok = __ldg(P.seed_bin + w) != -2;
         tgt = xyz(__ldg(P.seed_tgt + w));
+        ct = P.seed_ctype ? __ldg(P.seed_ctype + w) : ((uint32_t)g.k | ((g.tau & 255u) << 4) | (1u << 12));
+        pn = P.seed_pn ? __ldg(P.seed_pn + w) : 1.0f;
     } else {
         SeedRes sr;
-        ok = seed_target(S, g, P.walk_id_base + w, trial, xyz(__ldg(P.xD + w / P.spp)), sr);
+        ok = seed_target(S, g, P.walk_id_base + w, trial, xD, sr);
         tgt = sr.tgt;
+        ct = (uint32_t)sr.n | ((sr.bits & 255u) << 4) | ((sr.learned ? 1u : 0u) << 12);
+        pn = sr.Pn;
     }
     P.s_walk[slot] = (int32_t)w;
     P.s_trial[slot] = trial;
-    P.s_flags[slot] = F_DEDUCE | extra_flags | (ok ? 0u : F_SEEDFAIL);
-    P.s_tgt[slot] = make_float4(tgt.x, tgt.y, tgt.z, 0.f);
+    P.s_ctype[slot] = ct;
+    P.s_pn[slot] = pn;
+    if (ok) {
+        double3 od = d3f(xD);
+        double3 v = d3f(tgt) - od;
+        double l2 = ddot(v, v);
+        ok = l2 > 0.0;
+        if (ok) {
+            double3 dd = v * rsqrt(l2);
+            P.s_x[slot] = make_double4(dd.x, dd.y, dd.z, 0.0);
+            wf_emit0(P, par, xD, nrmz(f3d(dd)), __int_as_float(-1), slot);
+        }
+    }
+    P.s_flags[slot] = F_DEDUCE | extra_flags | (ok ? 0u : F_FAIL);
 }
 
 // --------------------------------------------------------------------------
-// init: slots 0..min(S,n)-1 <- walks 0..; list[0] = those slots
+// init: slots 0..min(S,n)-1 <- walks 0..; list[0] = those slots (header zeroed by the host)
 // --------------------------------------------------------------------------
 template <int KMAX>
 __global__ void k_wf_init(const DScene S, const SeedCtx g, const WFParams P) {
     uint32_t s0 = (uint32_t)min((int64_t)P.S, P.n);
     for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < P.S; s += gridDim.x * blockDim.x) {
         if (s < s0) {
-            wf_seed(S, g, P, s, (int64_t)s, 0u, 0u);
+            wf_start(S, g, P, s, (int64_t)s, 0u, 0u, 0u);
             P.list[0][s] = s;
         } else {
             P.s_walk[s] = -1;
         }
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) {
-        WFHeader *h = P.hdr;
-        h->queue = s0;
-        h->wave = 0;
-        h->list_count[0] = s0;
-        h->list_count[1] = 0;
-        h->free_top = 0;
-        h->n_entries = 0;
-        h->item_head = h->item_tail = 0;
-        h->trace_cursor = 0;
+        P.hdr->queue = s0;
+        P.hdr->list_count[0] = s0;
     }
 }
 
 // --------------------------------------------------------------------------
-// trace: persistent, per-lane job fetch, while-while traversal
+// ray engine: closest specular hit (chain rays) or any hit over all surfaces
+// (visibility) -- the operator r(x, w) of Eq. 6 and V of Eq. 2.
+// Same arithmetic as trace<> in device_common.cuh.
 // --------------------------------------------------------------------------
-template <int KMAX>
-__global__ void __launch_bounds__(128) k_wf_trace(const DScene S, const SeedCtx g, const WFParams P) {
+__global__ void __launch_bounds__(128, WF_TRACE_MINB) k_wf_rays(const DScene S, const WFParams P, int sub,
+                                                                const float4 *ro_s, const float4 *rd_s) {
     __shared__ unsigned long long s_acc[3];
     if (threadIdx.x < 3) s_acc[threadIdx.x] = 0ull;
     __syncthreads();
     const int lane = threadIdx.x & 31;
     const unsigned par = *(volatile unsigned int *)&P.hdr->wave & 1u;
-    const uint32_t *list = P.list[par];
-    const unsigned count = *(volatile unsigned int *)&P.hdr->list_count[par];
-    const int k = g.k;
-    const uint32_t tau = g.tau;
+    const float4 *ro, *rd;
+    unsigned count;
+    if (sub == 0) {
+        ro = par ? P.r0o1 : P.r0o0;
+        rd = par ? P.r0d1 : P.r0d0;
+        count = *(volatile unsigned int *)&P.hdr->ray0_count[par];
+    } else {
+        ro = ro_s;
+        rd = rd_s;
+        count = *(volatile unsigned int *)&P.hdr->ray_count[sub];
+    }
+    unsigned int *cursor = &P.hdr->cursor[sub];
     const float eps = P.ray_eps;
     const int SENT = 0x7fffffff, NONE = 0;
-    // job / ray state
-    int slot = -1, i = 0;
-    bool deduce = false, active = false, job_done = false;
-    uint32_t surf_req = 0, ysurf = 0;
-    float3 xD = f3(0, 0, 0), o = f3(0, 0, 0), d = f3(0, 0, 0);
-    double3 od = make_double3(0, 0, 0), dd = make_double3(0, 0, 0), q = make_double3(0, 0, 0);
-    int pprim = -1, psurf_ = -1; // previous hit (for deduction scattering)
-    float beta = 1.f;
+
+    int rid = -1;
+    bool drained = false;
+    uint32_t meta = 0;
     RayW r;
-    r.o = o; r.d = d; r.idir = d; r.kx = 0; r.ky = 1; r.kz = 2; r.Sx = r.Sy = r.Sz = 0.f;
-    float best = 0.f, bb0 = 0.f, bb1 = 0.f, bb2 = 0.f;
-    int bprim = -2, bsurf = -1;
-    float3 bp = f3(0, 0, 0);
+    r.o = r.d = r.idir = f3(0, 0, 0);
+    r.kx = r.ky = r.kz = 0;
+    r.Sx = r.Sy = r.Sz = 0.f;
+    float tmax = 0.f;
     int node = SENT, leaf = NONE, sp = 0;
     int stack[64];
+    int bprim = -2, bsurf = -1;
+    float bb0 = 0.f, bb1 = 0.f, bb2 = 0.f;   // barycentrics, or the analytic hit point
     LaneStats ls = {0u, 0u, 0u};
-    unsigned int *cursor = &P.hdr->trace_cursor;  // jobs = entries of the current ray list
 
     while (true) {
-        // ---- lanes without a job fetch one (warp-aggregated) ----
-        unsigned need = __ballot_sync(MPG_FULL, slot < 0 && !job_done);
-        if (need) {
-            int leader = __ffs(need) - 1;
+        // ---- refill finished lanes (one atomic per warp) ----
+        unsigned im = __ballot_sync(MPG_FULL, rid < 0 && !drained);
+        if (im) {
+            int leader = __ffs(im) - 1;
             unsigned base = 0;
-            if (lane == leader) base = atomicAdd(cursor, (unsigned)__popc(need));
+            if (lane == leader) base = atomicAdd(cursor, (unsigned)__popc(im));
             base = __shfl_sync(MPG_FULL, base, leader);
-            if (slot < 0 && !job_done) {
-                unsigned idx = base + __popc(need & ((1u << lane) - 1u));
+            if (rid < 0 && !drained) {
+                unsigned idx = base + __popc(im & ((1u << lane) - 1u));
                 if (idx < count) {
-                    slot = (int)list[idx];
-                    uint32_t fl = P.s_flags[slot];
-                    deduce = (fl & F_DEDUCE) != 0;
-                    int64_t w = P.s_walk[slot];
-                    xD = xyz(__ldg(P.xD + w / P.spp));
-                    i = 0;
-                    ysurf = 0;
-                    if (fl & F_SEEDFAIL) {
-                        P.s_flags[slot] = fl | F_FAIL;
-                        slot = -1;
-                    } else {
-                        surf_req = P.s_surf[slot];
-                        beta = P.s_beta[slot];
-                        if (deduce) {
-                            double3 v = d3f(xyz(P.s_tgt[slot])) - d3f(xD);
-                            double l2 = ddot(v, v);
-                            dd = l2 > 0.0 ? v * rsqrt(l2) : make_double3(0, 0, 0);
+                    rid = (int)idx;
+                    float4 a = ro[idx], b = rd[idx];
+                    float3 o = xyz(a), d = xyz(b);
+                    meta = __float_as_uint(b.w);
+                    const bool any = (meta & WF_ANY) != 0;
+                    // any-hit rays carry t_max; chain rays a hinted triangle (or -1), t_max = inf
+                    tmax = any ? a.w : 3.0e38f;
+                    const int hint = any ? -1 : __float_as_int(a.w);
+                    ls.rays++;
+                    bsurf = -1;
+                    bprim = -2;
+                    for (int s = 0; s < S.n_surf; s++) {
+                        const DSurf &f = S.surf[s];
+                        if (f.kind == 2 || (!any && f.mat == 2)) continue;
+                        float t;
+                        float3 p;
+                        bool hit;
+                        if (f.kind == 0) hit = sphere_hit(o, d, f.center, f.radius, eps, tmax, t, p);
+                        else {
+                            hit = quad_hit(o, d, f.origin, f.eu, f.ev, eps, tmax, t);
+                            p = o + d * t;
                         }
-                        active = false; // ray 0 set up below
+                        if (hit) { tmax = t; bsurf = s; bprim = -1; bb0 = p.x; bb1 = p.y; bb2 = p.z; }
+                    }
+                    node = SENT;
+                    leaf = NONE;
+                    if (S.n_tri > 0 && !(any && bsurf >= 0)) {
+                        ray_setup(r, o, d);
+                        if (hint >= 0) { // bound the search by the hinted triangle (see trace<>)
+                            ls.tris++;
+                            float4 p0 = __ldg(S.tpos + TSTRIDE * hint), p1 = __ldg(S.tpos + TSTRIDE * hint + 1),
+                                   p2 = __ldg(S.tpos + TSTRIDE * hint + 2);
+                            float t, c0, c1, c2;
+                            if (__float_as_int(p2.w) != 0 &&
+                                tri_hit(r, xyz(p0), xyz(p1), xyz(p2), eps, tmax, t, c0, c1, c2)) {
+                                tmax = t; bprim = hint; bsurf = __float_as_int(p1.w);
+                                bb0 = c0; bb1 = c1; bb2 = c2;
+                            }
+                        }
+                        node = 0;
+                        stack[0] = SENT;
+                        sp = 1;
                     }
                 } else {
-                    job_done = true; // queue drained
+                    drained = true;
                 }
             }
         }
-        if (__all_sync(MPG_FULL, slot < 0 && job_done)) break;
+        if (__all_sync(MPG_FULL, rid < 0)) break;
 
-        // ---- set up ray i of the job (if not yet active) ----
-        if (slot >= 0 && !active) {
-            bool ok = true;
-            if (i == 0) od = d3f(xD);
-            if (deduce) {
-                if (i > 0) ok = scatter_dir(S, dd, pprim, psurf_, f3d(od), (tau >> (i - 1)) & 1u);
-                else ok = ddot(dd, dd) > 0.0;
-            } else {
-                double4 x4 = P.s_x[(size_t)i * P.S + slot];
-                float4 dq4 = P.s_dq[(size_t)i * P.S + slot];
-                q = make_double3(x4.x + (double)dq4.x * beta, x4.y + (double)dq4.y * beta, x4.z + (double)dq4.z * beta);
-                double3 v = q - od;
-                double l2 = ddot(v, v);
-                ok = l2 > 0.0;
-                if (ok) dd = v * rsqrt(l2);
-            }
-            o = f3d(od);
-            d = nrmz(f3d(dd));
-            if (!ok) {
-                P.s_flags[slot] |= F_FAIL;
-                slot = -1;
-            } else {
-                ls.rays++;
-                best = 3.0e38f; bprim = -2; bsurf = -1;
-                for (int s = 0; s < S.n_surf; s++) {
-                    const DSurf &f = S.surf[s];
-                    if (f.kind == 2 || f.mat == 2) continue;
-                    float t; float3 p; bool hit;
-                    if (f.kind == 0) hit = sphere_hit(o, d, f.center, f.radius, eps, best, t, p);
-                    else { hit = quad_hit(o, d, f.origin, f.eu, f.ev, eps, best, t); p = o + d * t; }
-                    if (hit) { best = t; bprim = -1; bsurf = s; bp = p; }
+        // ---- traverse until done, or until the warp is too sparse (dynamic fetch) ----
+        if (rid >= 0) {
+            const bool any = (meta & WF_ANY) != 0;
+            const float3 o = r.o;
+            while (node != SENT || leaf != NONE) {
+                while (node >= 0 && node != SENT) {
+                    ls.nodes++;
+                    const float4 *nd = S.nodes + 4 * node;
+                    float4 a = __ldg(nd), b = __ldg(nd + 1), c = __ldg(nd + 2);
+                    int4 ch = __ldg(reinterpret_cast<const int4 *>(nd + 3));
+                    float tx0 = (a.x - o.x) * r.idir.x, tx1 = (a.w - o.x) * r.idir.x;
+                    float ty0 = (a.y - o.y) * r.idir.y, ty1 = (b.x - o.y) * r.idir.y;
+                    float tz0 = (a.z - o.z) * r.idir.z, tz1 = (b.y - o.z) * r.idir.z;
+                    float n0 = fmaxf(fmaxf(fminf(tx0, tx1), fminf(ty0, ty1)), fmaxf(fminf(tz0, tz1), eps));
+                    float f0 = fminf(fminf(fmaxf(tx0, tx1), fmaxf(ty0, ty1)), fminf(fmaxf(tz0, tz1), tmax));
+                    float sx0 = (b.z - o.x) * r.idir.x, sx1 = (c.y - o.x) * r.idir.x;
+                    float sy0 = (b.w - o.y) * r.idir.y, sy1 = (c.z - o.y) * r.idir.y;
+                    float sz0 = (c.x - o.z) * r.idir.z, sz1 = (c.w - o.z) * r.idir.z;
+                    float n1 = fmaxf(fmaxf(fminf(sx0, sx1), fminf(sy0, sy1)), fmaxf(fminf(sz0, sz1), eps));
+                    float f1 = fminf(fminf(fmaxf(sx0, sx1), fmaxf(sy0, sy1)), fminf(fmaxf(sz0, sz1), tmax));
+                    bool h0 = n0 <= f0, h1 = n1 <= f1;
+                    if (h0 && h1) {
+                        bool swp = n1 < n0;
+                        node = swp ? ch.y : ch.x;
+                        stack[sp++] = swp ? ch.x : ch.y;
+                    } else if (h0) {
+                        node = ch.x;
+                    } else if (h1) {
+                        node = ch.y;
+                    } else {
+                        node = stack[--sp];
+                    }
+                    if (node < 0 && leaf == NONE) { // postpone the leaf, keep traversing
+                        leaf = node;
+                        node = stack[--sp];
+                    }
+                    if (!__any_sync(__activemask(), leaf == NONE)) break;
                 }
-                if (S.n_tri > 0) {
-                    ray_setup(r, o, d);
-                    node = 0; leaf = NONE; stack[0] = SENT; sp = 1;
-                } else {
-                    node = SENT; leaf = NONE;
-                }
-                active = true;
-            }
-        }
-
-        // ---- traversal: while-while with postponed leaves ----
-        if (slot >= 0 && active) {
-            while (node >= 0 && node != SENT) {
-                ls.nodes++;
-                const float4 *nd = S.nodes + 4 * node;
-                float4 a = __ldg(nd), b = __ldg(nd + 1), c = __ldg(nd + 2);
-                int4 ch = __ldg(reinterpret_cast<const int4 *>(nd + 3));
-                float tx0 = (a.x - o.x) * r.idir.x, tx1 = (a.w - o.x) * r.idir.x;
-                float ty0 = (a.y - o.y) * r.idir.y, ty1 = (b.x - o.y) * r.idir.y;
-                float tz0 = (a.z - o.z) * r.idir.z, tz1 = (b.y - o.z) * r.idir.z;
-                float n0 = fmaxf(fmaxf(fminf(tx0, tx1), fminf(ty0, ty1)), fmaxf(fminf(tz0, tz1), eps));
-                float f0 = fminf(fminf(fmaxf(tx0, tx1), fmaxf(ty0, ty1)), fminf(fmaxf(tz0, tz1), best));
-                float sx0 = (b.z - o.x) * r.idir.x, sx1 = (c.y - o.x) * r.idir.x;
-                float sy0 = (b.w - o.y) * r.idir.y, sy1 = (c.z - o.y) * r.idir.y;
-                float sz0 = (c.x - o.z) * r.idir.z, sz1 = (c.w - o.z) * r.idir.z;
-                float n1 = fmaxf(fmaxf(fminf(sx0, sx1), fminf(sy0, sy1)), fmaxf(fminf(sz0, sz1), eps));
-                float f1 = fminf(fminf(fmaxf(sx0, sx1), fmaxf(sy0, sy1)), fminf(fmaxf(sz0, sz1), best));
-                bool h0 = n0 <= f0, h1 = n1 <= f1;
-                if (h0 && h1) {
-                    bool swp = n1 < n0;
-                    node = swp ? ch.y : ch.x;
-                    stack[sp++] = swp ? ch.x : ch.y;
-                } else if (h0) node = ch.x;
-                else if (h1) node = ch.y;
-                else node = stack[--sp];
-                if (node < 0 && leaf == NONE) { leaf = node; node = stack[--sp]; }
-                if (!__any_sync(__activemask(), leaf == NONE)) break;
-            }
-            while (leaf != NONE) {
-                int v = ~leaf;
-                int start = v >> 3, cnt = (v & 7) + 1;
-                for (int j = start; j < start + cnt; j++) {
-                    ls.tris++;
-                    float4 p0 = __ldg(S.tpos + 3 * j), p1 = __ldg(S.tpos + 3 * j + 1), p2 = __ldg(S.tpos + 3 * j + 2);
-                    if (__float_as_int(p2.w) == 0) continue;
-                    float t, c0, c1, c2;
-                    if (tri_hit(r, xyz(p0), xyz(p1), xyz(p2), eps, best, t, c0, c1, c2)) {
-                        best = t; bprim = j; bsurf = __float_as_int(p1.w);
-                        bb0 = c0; bb1 = c1; bb2 = c2;
+                while (leaf != NONE) {
+                    int v = ~leaf;
+                    int start = v >> 3, cnt = (v & 7) + 1;
+                    bool found = false;
+                    for (int j = start; j < start + cnt; j++) {
+                        ls.tris++;
+                        float4 p0 = __ldg(S.tpos + TSTRIDE * j), p1 = __ldg(S.tpos + TSTRIDE * j + 1),
+                               p2 = __ldg(S.tpos + TSTRIDE * j + 2);
+                        if (!any && __float_as_int(p2.w) == 0) continue;
+                        float t, c0, c1, c2;
+                        if (tri_hit(r, xyz(p0), xyz(p1), xyz(p2), eps, tmax, t, c0, c1, c2)) {
+                            tmax = t; bprim = j; bsurf = __float_as_int(p1.w);
+                            bb0 = c0; bb1 = c1; bb2 = c2;
+                            if (any) { found = true; break; }
+                        }
+                    }
+                    if (found) { node = SENT; leaf = NONE; break; }
+                    leaf = NONE;
+                    if (node < 0) { // the traversal stopped on another leaf
+                        leaf = node;
+                        node = stack[--sp];
                     }
                 }
-                leaf = NONE;
-                if (node < 0) { leaf = node; node = stack[--sp]; }
+                if (__popc(__activemask()) < WF_FETCH_MIN) break;
             }
-            // ---- ray finished? ----
-            if (node == SENT && leaf == NONE) {
-                active = false;
-                bool ok = bsurf >= 0 && (deduce || bsurf == (int)((surf_req >> (4 * i)) & 15u));
-                if (!ok) {
-                    P.s_flags[slot] |= F_FAIL;
-                    slot = -1;
+            if (node == SENT && leaf == NONE) { // ray done
+                const uint32_t slot = meta & ~WF_ANY;
+                if (any) {
+                    if (bsurf >= 0) atomicOr(P.s_flags + slot, F_FAIL);
                 } else {
                     float3 pf;
                     if (bprim >= 0) {
-                        float3 v0 = xyz(__ldg(S.tpos + 3 * bprim)), v1 = xyz(__ldg(S.tpos + 3 * bprim + 1)),
-                               v2 = xyz(__ldg(S.tpos + 3 * bprim + 2));
+                        float3 v0 = xyz(__ldg(S.tpos + TSTRIDE * bprim)), v1 = xyz(__ldg(S.tpos + TSTRIDE * bprim + 1)),
+                               v2 = xyz(__ldg(S.tpos + TSTRIDE * bprim + 2));
                         pf = v0 * bb0 + v1 * bb1 + v2 * bb2;
-                    } else pf = bp;
-                    double3 y = refine_hit(S, bprim, bsurf, od, deduce ? od + dd : q, pf);
-                    P.s_y[(size_t)i * P.S + slot] = make_double4(y.x, y.y, y.z, (double)bprim);
-                    ysurf |= (uint32_t)(bsurf & 15) << (4 * i);
-                    pprim = bprim; psurf_ = bsurf;
-                    od = y;
-                    i++;
-                    if (i >= k) {
-                        P.s_ysurf[slot] = ysurf;
-                        P.s_flags[slot] &= ~F_FAIL;
-                        slot = -1;
+                    } else {
+                        pf = f3(bb0, bb1, bb2);
                     }
+                    P.h_p[slot] = make_float4(pf.x, pf.y, pf.z, __int_as_float(bprim));
+                    P.h_s[slot] = bsurf;
                 }
+                rid = -1;
             }
         }
     }
-    // stats
     unsigned long long v3[3] = {ls.rays, ls.nodes, ls.tris};
 #pragma unroll
     for (int j = 0; j < 3; j++)
@@ -368,12 +426,91 @@ __global__ void __launch_bounds__(128) k_wf_trace(const DScene S, const SeedCtx 
 }
 
 // --------------------------------------------------------------------------
+// post: vertex i of every chain ray of list i -- refine, check, emit ray i+1
+// --------------------------------------------------------------------------
+__global__ void __launch_bounds__(128) k_wf_post(const DScene S, const WFParams P, int sub, const float4 *rd_s,
+                                                 float4 *ro_n, float4 *rd_n) {
+    const unsigned par = *(volatile unsigned int *)&P.hdr->wave & 1u;
+    const float4 *rd = sub == 0 ? (par ? P.r0d1 : P.r0d0) : rd_s;
+    const unsigned count = sub == 0 ? *(volatile unsigned int *)&P.hdr->ray0_count[par]
+                                    : *(volatile unsigned int *)&P.hdr->ray_count[sub];
+    const int i = sub;
+    for (unsigned idx = blockIdx.x * blockDim.x + threadIdx.x; idx < count; idx += gridDim.x * blockDim.x) {
+        const uint32_t meta = __float_as_uint(rd[idx].w);
+        if (meta & WF_ANY) continue;
+        const uint32_t slot = meta;
+        const uint32_t fl = P.s_flags[slot];
+        const bool ded = (fl & F_DEDUCE) != 0;
+        const int hs = P.h_s[slot];
+        const float4 hp = P.h_p[slot];
+        const int prim = __float_as_int(hp.w);
+        const uint32_t ct = P.s_ctype[slot];
+        const int k = (int)(ct & 15u);
+        bool ok = hs >= 0 && (ded || hs == (int)((P.s_surf[slot] >> (4 * i)) & 15u));
+        uint32_t bit = 0;
+        if (ok && ded) { // resolve the type of vertex i (R22, R14)
+            bit = (ct >> (4 + i)) & 1u;
+            const int mat = S.surf[hs].mat;
+            if (!((ct >> 12) & 1u) && mat == 0) bit = 0u;
+            if (bit && mat != 1) ok = false;
+        }
+        if (!ok) {
+            P.s_flags[slot] = fl | F_FAIL;
+            continue;
+        }
+        const int64_t wk = P.s_walk[slot];
+        const double3 od = i == 0 ? d3f(xyz(__ldg(P.xD + wk / P.spp))) : ld3(P.s_y, (size_t)(i - 1) * P.S + slot);
+        double3 tg;
+        const double bt = (double)P.s_beta[slot];
+        if (ded) tg = od + ld3(P.s_x, (size_t)i * P.S + slot);
+        else {
+            double4 x4 = P.s_x[(size_t)i * P.S + slot];
+            double4 dq4 = P.s_dq[(size_t)i * P.S + slot];
+            tg = make_double3(x4.x + dq4.x * bt, x4.y + dq4.y * bt, x4.z + dq4.z * bt);
+        }
+        // the hit on the exact line, in fp64 (R24)
+        const double3 y = refine_hit(S, prim, hs, od, tg, xyz(hp));
+        P.s_y[(size_t)i * P.S + slot] = make_double4(y.x, y.y, y.z, (double)prim);
+        P.s_ysurf[slot] = (i == 0 ? 0u : P.s_ysurf[slot]) | ((uint32_t)(hs & 15) << (4 * i));
+        if (ded) P.s_tau[slot] = (i == 0 ? 0u : P.s_tau[slot]) | (bit << i);
+        if (i + 1 < k) { // ray i+1 from y_i
+            double3 dd;
+            if (ded) {
+                dd = ld3(P.s_x, (size_t)i * P.S + slot);
+                if (!scatter_dir(S, dd, prim, hs, f3d(y), bit)) {
+                    P.s_flags[slot] = fl | F_FAIL;
+                    continue;
+                }
+                P.s_x[(size_t)(i + 1) * P.S + slot] = make_double4(dd.x, dd.y, dd.z, 0.0);
+            } else {
+                double4 x4 = P.s_x[(size_t)(i + 1) * P.S + slot];
+                double4 dq4 = P.s_dq[(size_t)(i + 1) * P.S + slot];
+                double3 q = make_double3(x4.x + dq4.x * bt, x4.y + dq4.y * bt, x4.z + dq4.z * bt);
+                double3 v = q - y;
+                double l2 = ddot(v, v);
+                if (!(l2 > 0.0)) {
+                    P.s_flags[slot] = fl | F_FAIL;
+                    continue;
+                }
+                dd = v * rsqrt(l2);
+            }
+            const int hint = ded ? -1 : (int)P.s_x[(size_t)(i + 1) * P.S + slot].w;
+            unsigned j = wf_agg_add(&P.hdr->ray_count[i + 1]);
+            float3 o = f3d(y), d = nrmz(f3d(dd));
+            ro_n[j] = make_float4(o.x, o.y, o.z, __int_as_float(hint));
+            rd_n[j] = make_float4(d.x, d.y, d.z, __uint_as_float(slot));
+        }
+    }
+}
+
+// --------------------------------------------------------------------------
 // hard entries: finalize / next batch
 // --------------------------------------------------------------------------
 __device__ __forceinline__ void wf_finalize_walk(const WFParams &P, int64_t w, uint32_t kk, bool truncated,
                                                  unsigned long long *s_stats) {
     P.trials[w] = kk;
-    P.w[w] = P.T[w] * (float)kk / __ldg(P.seed_xL + w).w;
+    float pn = P.seed_pn ? __ldg(P.seed_pn + w) : 1.0f;
+    P.w[w] = P.T[w] * (float)kk / (pn * __ldg(P.seed_xL + w).w);
     atomicAdd(&s_stats[SS_TRIALS], (unsigned long long)kk);
     if (truncated) atomicAdd(&s_stats[SS_TRUNC], 1ull);
 }
@@ -389,11 +526,21 @@ __device__ __forceinline__ bool wf_push_items(const WFParams &P, uint32_t e, uin
     return true;
 }
 
+__device__ __forceinline__ void wf_primary_status(const WFParams &P, int64_t w, int st, int it,
+                                                  unsigned long long *s_stats) {
+    P.status[w] = (uint8_t)st;
+    P.iters[w] = (uint16_t)it;
+    atomicAdd(&s_stats[SS_STATUS0 + st], 1ull);
+    atomicAdd(&s_stats[SS_PRIM_IT], (unsigned long long)it);
+    atomicAdd(&s_stats[SS_WALKS], 1ull);
+    if (st == ST_CONVERGED || st == ST_OCCLUDED) atomicAdd(&s_stats[SS_CONV], 1ull);
+}
+
 // --------------------------------------------------------------------------
-// update: one thread per traced slot
+// update: one thread per slot of this wave (no traversal)
 // --------------------------------------------------------------------------
-template <int KMAX>
-__global__ void __launch_bounds__(128) k_wf_update(const DScene S, const SeedCtx g, const WFParams P) {
+template <int KMAX, typename R>
+__global__ void __launch_bounds__(128, 4) k_wf_update(const DScene S, const SeedCtx g, const WFParams P) {
     __shared__ unsigned long long s_stats[SS_N];
     for (int j = threadIdx.x; j < SS_N; j += blockDim.x) s_stats[j] = 0ull;
     __syncthreads();
@@ -401,35 +548,53 @@ __global__ void __launch_bounds__(128) k_wf_update(const DScene S, const SeedCtx
     const uint32_t *list = P.list[par];
     const unsigned count = *(volatile unsigned int *)&P.hdr->list_count[par];
     const unsigned nxt = par ^ 1u;
-    const int k = g.k;
-    const uint32_t tau = g.tau;
-    uint32_t c_newton = 0, c_vtx = 0, c_att = 0, c_rays = 0;
-    LaneStats ls = {0u, 0u, 0u};
+    uint32_t c_newton = 0, c_vtx = 0, c_att = 0;
 
     for (unsigned idx = blockIdx.x * blockDim.x + threadIdx.x; idx < count; idx += gridDim.x * blockDim.x) {
         const uint32_t slot = list[idx];
-        uint32_t fl = P.s_flags[slot];
+        const uint32_t fl = P.s_flags[slot];
         const int64_t w = P.s_walk[slot];
-        uint32_t trial = P.s_trial[slot];
+        const uint32_t trial = P.s_trial[slot];
         int it = (int)(fl & F_IT_MASK);
+        const uint32_t ct = P.s_ctype[slot];
+        const int k = max(1, min((int)(ct & 15u), KMAX));
+
+        // ---------------- visibility result of a converged primary ----------------
+        if (fl & F_VIS) {
+            const bool occluded = (fl & F_FAIL) != 0;
+            float Tv = P.T[w];
+            if (occluded) { P.G[w] = 0.f; P.T[w] = 0.f; Tv = 0.f; }
+            wf_primary_status(P, w, occluded ? ST_OCCLUDED : ST_CONVERGED, it, s_stats);
+            if (!occluded && Tv > 0.0f && P.trials_on) {
+                wf_start(S, g, P, slot, w, 1u, 0u, nxt);
+                wf_append(P, nxt, slot);
+            } else {
+                P.trials[w] = 0;
+                P.w[w] = 0.0f;
+                wf_free(P, slot);
+            }
+            continue;
+        }
+
         float beta = P.s_beta[slot];
-        bool deduce = fl & F_DEDUCE, failed = fl & F_FAIL;
+        const bool deduce = fl & F_DEDUCE, failed = fl & F_FAIL;
+        const uint32_t tau = P.s_tau[slot];
         double3 x[KMAX];
-        V3<float> sg[KMAX], tg[KMAX], dq[KMAX];
+        V3<R> sg[KMAX], tg[KMAX], dq[KMAX];
         int prim[KMAX], surf[KMAX];
-        float Di[KMAX][4], Ub[KMAX][4];
-        uint32_t sp_ = failed ? P.s_surf[slot] : P.s_ysurf[slot];
+        R Di[KMAX][4], Ub[KMAX][4];
+        const uint32_t sp_ = failed ? P.s_surf[slot] : P.s_ysurf[slot];
         const double4 *src = failed ? P.s_x : P.s_y;
 #pragma unroll
         for (int j = 0; j < KMAX; j++) {
-            if (j >= k) { x[j] = make_double3(0, 0, 0); sg[j] = tg[j] = dq[j] = mk3<float>(0, 0, 0); prim[j] = -1; surf[j] = 0; continue; }
+            sg[j] = tg[j] = dq[j] = mk3<R>(0, 0, 0);
+            if (j >= k) { x[j] = make_double3(0, 0, 0); prim[j] = -1; surf[j] = 0; continue; }
             double4 v = src[(size_t)j * P.S + slot];
             x[j] = make_double3(v.x, v.y, v.z);
             prim[j] = (int)v.w;
             surf[j] = (int)((sp_ >> (4 * j)) & 15u);
-            sg[j] = tg[j] = dq[j] = mk3<float>(0, 0, 0);
         }
-        int end = -1; // attempt end status
+        int end = -1;
         bool fresh = false;
         if (deduce) {
             if (failed) end = ST_SEED_FAIL;
@@ -440,34 +605,42 @@ __global__ void __launch_bounds__(128) k_wf_update(const DScene S, const SeedCtx
             beta = fminf(1.0f, 2.0f * beta); it++; fresh = true;
         }
         const float3 xD = xyz(__ldg(P.xD + w / P.spp));
-        const float4 l4 = __ldg(P.seed_xL + w);
-        const float3 xL = xyz(l4);
+        const float3 xL = xyz(__ldg(P.seed_xL + w));
         bool singular = false;
         if (end < 0) {
             if (fresh) {
                 c_vtx += k;
                 float cm;
-                int rr = newton_system<KMAX, float>(S, k, tau, xD, xL, x, prim, surf, P.tol, Di, Ub, sg, tg, dq, singular, cm);
+                int rr = newton_system<KMAX, R>(S, k, tau, xD, xL, x, prim, surf, P.tol, Di, Ub, sg, tg, dq,
+                                                    singular, cm);
                 if (rr == 1) end = ST_CONVERGED;
                 else if (rr == 2) end = ST_DEGENERATE;
                 else {
 #pragma unroll
                     for (int j = 0; j < KMAX; j++)
-                        if (j < k) P.s_dq[(size_t)j * P.S + slot] = make_float4(dq[j].x, dq[j].y, dq[j].z, 0.f);
+                        if (j < k) P.s_dq[(size_t)j * P.S + slot] = make_double4(dq[j].x, dq[j].y, dq[j].z, 0.0);
                 }
             }
-            if (end < 0 && it >= P.max_iters) end = ST_MAXITER;
+            if (end < 0 && it >= ((k >= 3 && P.max_iters_long > 0) ? P.max_iters_long : P.max_iters)) end = ST_MAXITER;
         }
-        if (end < 0) {
-            // continue: reprojection next wave
-            if (fresh) {
+        if (fresh) {
 #pragma unroll
-                for (int j = 0; j < KMAX; j++)
-                    if (j < k) P.s_x[(size_t)j * P.S + slot] = make_double4(x[j].x, x[j].y, x[j].z, (double)prim[j]);
-                P.s_surf[slot] = sp_;
-            }
+            for (int j = 0; j < KMAX; j++)
+                if (j < k) P.s_x[(size_t)j * P.S + slot] = make_double4(x[j].x, x[j].y, x[j].z, (double)prim[j]);
+            P.s_surf[slot] = sp_;
+        }
+        if (end < 0) { // continue: reprojection ray 0 toward q_0 = x_0 + beta dq_0 next wave (R5)
             P.s_beta[slot] = beta;
-            P.s_flags[slot] = (fl & (F_ITEM | F_SEQ)) | (uint32_t)it;
+            double3 d0;
+            if (fresh) d0 = make_double3((double)dq[0].x, (double)dq[0].y, (double)dq[0].z);
+            else d0 = ld3(P.s_dq, slot);
+            const double bt = (double)beta;
+            double3 q = make_double3(x[0].x + d0.x * bt, x[0].y + d0.y * bt, x[0].z + d0.z * bt);
+            double3 v = q - d3f(xD);
+            double l2 = ddot(v, v);
+            bool ok = l2 > 0.0;
+            if (ok) wf_emit0(P, nxt, xD, nrmz(f3d(v * rsqrt(l2))), __int_as_float(prim[0]), slot);
+            P.s_flags[slot] = (fl & (F_ITEM | F_SEQ)) | (uint32_t)it | (ok ? 0u : F_FAIL);
             wf_append(P, nxt, slot);
             continue;
         }
@@ -477,57 +650,49 @@ __global__ void __launch_bounds__(128) k_wf_update(const DScene S, const SeedCtx
         int lid = 0;
         if (S.n_light > 1) lid = (int)uidx(rng_draw(g.seed, P.walk_id_base + w, 0u, 0u).z, (uint32_t)S.n_light);
         if (trial == 0) {
-            float Gv = 0.f, Tv = 0.f;
             int st = end;
+            float Gv = 0.f, Tv = 0.f;
             if (st == ST_CONVERGED) {
                 const DLight &L = S.light[lid];
-                float kap, DL[4];
-                if (!post_sweep<KMAX, float>(S, L, k, tau, xD, xL, x, prim, surf, true, kap, DL)) st = ST_BAD_SIDE;
+                float kap;
+                R DL[4];
+                if (!post_sweep<KMAX, R>(S, L, k, tau, xD, xL, x, prim, surf, true, kap, DL)) st = ST_BAD_SIDE;
                 else {
-                    bool vis = true;
-                    float3 a = xD;
-#pragma unroll 1
-                    for (int j = 0; j <= k; j++) {
-                        float3 b = xL;
-#pragma unroll
-                        for (int jj = 0; jj < KMAX; jj++)
-                            if (jj == j) b = f3d(x[jj]);
-                        float3 dd = b - a;
-                        float l = len(dd);
-                        Hit hh;
-                        if (trace<true>(S, a, dd * (1.0f / l), P.ray_eps, l - P.ray_eps, false, hh, ls)) { vis = false; break; }
-                        a = b;
-                    }
-                    if (!vis) st = ST_OCCLUDED;
-                    else {
-                        Gv = singular ? 0.0f : ggt_from_blocks<KMAX, float>(k, xD, xyz(__ldg(P.nD + w / P.spp)), x, Di, Ub, sg, tg, DL);
-                        float Le = L.emit;
-                        if (L.kind == 1 && !(dot(f3d(x[k - 1]) - xL, L.n) > 0.0f)) Le = 0.0f;
-                        Tv = kap * Gv * Le;
-                    }
+                    Gv = singular ? 0.0f : ggt_from_blocks<KMAX, R>(k, xD, xyz(__ldg(P.nD + w / P.spp)), x, Di,
+                                                                        Ub, sg, tg, DL);
+                    float Le = L.emit;
+                    if (L.kind == 1 && !(dot(f3d(x[k - 1]) - xL, L.n) > 0.0f)) Le = 0.0f;
+                    Tv = kap * Gv * Le;
                 }
             }
             if (st != ST_SEED_FAIL) {
 #pragma unroll
                 for (int j = 0; j < KMAX; j++) {
                     if (j >= k) break;
-                    int pid = prim[j] >= 0 ? __float_as_int(__ldg(S.tpos + 3 * prim[j]).w) : -1;
-                    P.chain[(int64_t)j * P.n + w] = make_float4((float)x[j].x, (float)x[j].y, (float)x[j].z, __int_as_float(pid));
+                    int pid = prim[j] >= 0 ? __float_as_int(__ldg(S.tpos + TSTRIDE * prim[j]).w) : -1;
+                    P.chain[(int64_t)j * P.n + w] = make_float4((float)x[j].x, (float)x[j].y, (float)x[j].z,
+                                                                __int_as_float(pid));
                 }
             }
-            P.status[w] = (uint8_t)st;
-            P.iters[w] = (uint16_t)it;
             P.G[w] = Gv;
             P.T[w] = Tv;
-            atomicAdd(&s_stats[SS_STATUS0 + st], 1ull);
-            atomicAdd(&s_stats[SS_PRIM_IT], (unsigned long long)it);
-            atomicAdd(&s_stats[SS_WALKS], 1ull);
-            if (st == ST_CONVERGED || st == ST_OCCLUDED) atomicAdd(&s_stats[SS_CONV], 1ull);
-            if (st == ST_CONVERGED && Tv > 0.0f && P.trials_on) {
+            if (P.out_ctype) P.out_ctype[w] = (uint16_t)((uint32_t)k | (tau << 4));
+            if (st == ST_CONVERGED) { // the k+1 visibility segments are traced next wave
                 P.s_psurf[slot] = sp_;
-                wf_seed(S, g, P, slot, w, 1u, 0u);
+                P.s_pct[slot] = (uint32_t)k | (tau << 4);
+                P.s_flags[slot] = F_VIS | (uint32_t)it;
+                float3 a = xD;
+#pragma unroll 1
+                for (int j = 0; j <= k; j++) { // fp32 segments as walk.cuh
+                    float3 bq = j == k ? xL : f3d(x[j]);
+                    float3 dv = bq - a;
+                    float l = len(dv);
+                    wf_emit0(P, nxt, a, dv * (1.0f / l), l - P.ray_eps, slot | WF_ANY);
+                    a = bq;
+                }
                 wf_append(P, nxt, slot);
             } else {
+                wf_primary_status(P, w, st, it, s_stats);
                 P.trials[w] = 0;
                 P.w[w] = 0.0f;
                 wf_free(P, slot);
@@ -538,10 +703,12 @@ __global__ void __launch_bounds__(128) k_wf_update(const DScene S, const SeedCtx
         const bool item = fl & F_ITEM;
         const uint32_t e = item ? (uint32_t)P.s_entry[slot] : 0u;
         const uint32_t psurf = item ? P.e_psurf[e] : P.s_psurf[slot];
+        const uint32_t pct = item ? P.e_pct[e] : P.s_pct[slot];
         bool same = false;
-        if (end == ST_CONVERGED) {
-            float kd, DLd[4];
-            if (post_sweep<KMAX, float>(S, S.light[lid], k, tau, xD, xL, x, prim, surf, false, kd, DLd)) {
+        if (end == ST_CONVERGED && (uint32_t)k == (pct & 15u) && tau == (pct >> 4)) {
+            float kd;
+            R DLd[4];
+            if (post_sweep<KMAX, R>(S, S.light[lid], k, tau, xD, xL, x, prim, surf, false, kd, DLd)) {
                 same = true;
 #pragma unroll
                 for (int j = 0; j < KMAX; j++) {
@@ -570,7 +737,7 @@ __global__ void __launch_bounds__(128) k_wf_update(const DScene S, const SeedCtx
                     if (!wf_push_items(P, e, issued + 1, B)) {
                         // item list full: continue this entry sequentially in this slot
                         P.e_pending[e] = 0;
-                        wf_seed(S, g, P, slot, w, issued + 1, F_ITEM | F_SEQ);
+                        wf_start(S, g, P, slot, w, issued + 1, F_ITEM | F_SEQ, nxt);
                         P.s_entry[slot] = (int32_t)e;
                         wf_append(P, nxt, slot);
                         continue;
@@ -592,6 +759,7 @@ __global__ void __launch_bounds__(128) k_wf_update(const DScene S, const SeedCtx
                 uint32_t B = min(WF_BATCH0, P.k_max - trial);
                 P.e_walk[e2] = (int32_t)w;
                 P.e_psurf[e2] = psurf;
+                P.e_pct[e2] = pct;
                 P.e_best[e2] = WF_NONE;
                 P.e_batch[e2] = B;
                 P.e_pending[e2] = B;
@@ -604,17 +772,13 @@ __global__ void __launch_bounds__(128) k_wf_update(const DScene S, const SeedCtx
                 P.e_pending[e2] = 0;
             }
         }
-        wf_seed(S, g, P, slot, w, trial + 1, fl & (F_ITEM | F_SEQ));
+        wf_start(S, g, P, slot, w, trial + 1, fl & (F_ITEM | F_SEQ), nxt);
+        if (item) P.s_entry[slot] = (int32_t)e;
         wf_append(P, nxt, slot);
     }
-    // stats
-    c_rays = ls.rays;
     atomicAdd(&s_stats[SS_NEWTON], (unsigned long long)c_newton);
     atomicAdd(&s_stats[SS_VTX], (unsigned long long)c_vtx);
     atomicAdd(&s_stats[SS_ATTEMPTS], (unsigned long long)c_att);
-    atomicAdd(&s_stats[SS_RAYS], (unsigned long long)c_rays);
-    atomicAdd(&s_stats[SS_NODES], (unsigned long long)ls.nodes);
-    atomicAdd(&s_stats[SS_TRIS], (unsigned long long)ls.tris);
     __syncthreads();
     if (P.stats)
         for (int j = threadIdx.x; j < SS_N; j += blockDim.x)
@@ -639,13 +803,16 @@ __global__ void k_wf_plan(const WFParams P) {
     h->plan_list = nxt;
     h->plan_queue0 = h->queue;
     h->plan_item0 = h->item_head;
-    h->trace_cursor = 0;
     h->item_head += a;
     h->queue += p;
     h->free_top = F - a - p;
     unsigned more = h->list_count[nxt] + a + p;
-    // next wave: swap lists, clear the one just consumed
-    h->list_count[par] = 0;
+    h->list_count[par] = 0;   // next wave: swap lists, clear the ones just consumed
+    h->ray0_count[par] = 0;
+    for (int i = 0; i < WF_KMAX; i++) {
+        h->ray_count[i] = 0;
+        h->cursor[i] = 0;
+    }
     h->wave = h->wave + 1;
     h->more = more;
     if (P.use_cond) cudaGraphSetConditional(P.cond, more > 0 ? 1u : 0u);
@@ -666,9 +833,9 @@ __global__ void k_wf_refill(const DScene S, const SeedCtx g, const WFParams P) {
             uint32_t e = (uint32_t)P.it_entry[i0 + j];
             uint32_t t = P.it_trial[i0 + j];
             P.s_entry[slot] = (int32_t)e;
-            wf_seed(S, g, P, slot, (int64_t)P.e_walk[e], t, F_ITEM);
+            wf_start(S, g, P, slot, (int64_t)P.e_walk[e], t, F_ITEM, lst);
         } else {
-            wf_seed(S, g, P, slot, (int64_t)(q0 + (j - a)), 0u, 0u);
+            wf_start(S, g, P, slot, (int64_t)(q0 + (j - a)), 0u, 0u, lst);
         }
         wf_append(P, lst, slot);
     }
