@@ -184,7 +184,9 @@ __device__ __forceinline__ int newton_system(const DScene &S, int k, uint32_t ta
         if (i >= k) break;
         onbR(geo_normalR<R>(S, prim[i], surf[i], x[i]), sg[i], tg[i]);
     }
-#pragma unroll
+    // rolled: one copy of the per-vertex body keeps the hot code small (ncu: 37% of the
+    // persistent kernel's stall samples were instruction-fetch stalls with it unrolled)
+#pragma unroll 1
     for (int i = 0; i < KMAX; i++) {
         if (i >= k) break;
         double3 a = i == 0 ? d3f(xD) : x[i > 0 ? i - 1 : 0];
@@ -250,11 +252,11 @@ __device__ __forceinline__ int newton_system(const DScene &S, int k, uint32_t ta
 
 // sides (R8), kappa (R12) and the light-side block D_L at a converged chain
 template <int KMAX, typename R>
-__device__ __forceinline__ bool post_sweep(const DScene &S, const DLight &L, int k, uint32_t tau, float3 xD,
+__device__ MPG_COLD bool post_sweep(const DScene &S, const DLight &L, int k, uint32_t tau, float3 xD,
                                            float3 xL, const double3 (&x)[KMAX], const int (&prim)[KMAX],
                                            const int (&surf)[KMAX], bool want_kappa, float &kappa, R (&DL)[4]) {
     R kap = 1, etaD = 1, etaL = 1;
-#pragma unroll
+#pragma unroll 1
     for (int i = 0; i < KMAX; i++) {
         if (i >= k) break;
         double3 a = i == 0 ? d3f(xD) : x[i > 0 ? i - 1 : 0];
@@ -296,7 +298,7 @@ __device__ __forceinline__ bool post_sweep(const DScene &S, const DLight &L, int
 
 // analytic GGT: back-substitute J Y = -[0..0; D_L] with the stored D'^-1, U (R11)
 template <int KMAX, typename R>
-__device__ __forceinline__ float ggt_from_blocks(int k, float3 xD, float3 nD, const double3 (&x)[KMAX],
+__device__ MPG_COLD float ggt_from_blocks(int k, float3 xD, float3 nD, const double3 (&x)[KMAX],
                                                  const R (&Di)[KMAX][4], const R (&Ub)[KMAX][4],
                                                  const V3<R> (&sg)[KMAX], const V3<R> (&tg)[KMAX],
                                                  const R (&DL)[4]) {

@@ -74,7 +74,7 @@ __device__ __forceinline__ void onb_exact(float3 n, float3 &b1, float3 &b2) {
 
 // Seed target for (walk, trial): the deduction ray x_D -> target gives x_1
 // (Eq. 6).  Returns false if no seed could be drawn (SEED_FAIL).
-__device__ __forceinline__ bool seed_target(const DScene &S, const SeedCtx &g, uint64_t wid, uint32_t trial,
+__device__ MPG_COLD bool seed_target(const DScene &S, const SeedCtx &g, uint64_t wid, uint32_t trial,
                                             float3 xD, SeedRes &sr) {
     float3 &tgt = sr.tgt;
     int &bin = sr.bin;
