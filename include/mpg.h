@@ -244,6 +244,10 @@ mpg_status mpg_debug_trace(float *buf, int64_t n_walks, int32_t stride);
 
 const char *mpg_last_error(void);
 int32_t mpg_version(void);
+/* Number of kernel launches this library has enqueued since load (host-side
+ * counter, all threads; a CUDA-graph launch of the wavefront loop counts each
+ * node of its body once per wave only in host-loop mode, else as 1). */
+uint64_t mpg_kernel_launches(void);
 
 #ifdef __cplusplus
 }

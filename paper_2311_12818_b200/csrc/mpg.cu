@@ -9,6 +9,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <atomic>
 #include <vector>
 
 #include "mpg.h"
@@ -21,6 +22,8 @@
 // error plumbing
 // ----------------------------------------------------------------------------
 static thread_local std::string g_err;
+static std::atomic<unsigned long long> g_launches{0};   // mpg_kernel_launches()
+#define COUNT_LAUNCH(n) g_launches.fetch_add((n), std::memory_order_relaxed)
 static mpg_status fail(mpg_status s, const std::string &msg) {
     g_err = msg;
     return s;
@@ -417,6 +420,7 @@ extern "C" mpg_status mpg_trace_rays(const mpg_scene *scene, const float *orig, 
     ARG_CHECK(scene && orig && dir && t && prim && surf && n >= 0, "bad argument");
     if (n == 0) return MPG_OK;
     int blocks = (int)std::min<int64_t>((n + 127) / 128, 148 * 16);
+    COUNT_LAUNCH(1);
     k_trace<<<blocks, 128, 0, as_stream(stream)>>>(scene->d, (const float4 *)orig, (const float4 *)dir, n, tmin,
                                                    spec_only, t, prim, surf);
     CUDA_TRY(cudaPeekAtLastError());
@@ -638,8 +642,10 @@ __global__ void k_dir_cell_tables(const double *E, int n_cells, uint64_t *n_pref
 
 static mpg_status build_dir_tables(mpg_guide *g, const float *hist, cudaStream_t st) {
     int nt = g->n_cells * 126;
+    COUNT_LAUNCH(1);
     k_dir_type_tables<<<(nt + 127) / 128, 128, 0, st>>>(hist, g->n_cells, g->n_bins, g->type_energy, g->dir_prefix);
     CUDA_TRY(cudaPeekAtLastError());
+    COUNT_LAUNCH(1);
     k_dir_cell_tables<<<(g->n_cells + 127) / 128, 128, 0, st>>>(g->type_energy, g->n_cells, g->n_prefix,
                                                                  g->type_prefix);
     CUDA_TRY(cudaPeekAtLastError());
@@ -693,6 +699,7 @@ extern "C" mpg_status mpg_guide_upload(mpg_guide *g, const float *energy, void *
         mpg_status st = build_dir_tables(g, energy, as_stream(stream));
         if (st != MPG_OK) return st;
     } else {
+        COUNT_LAUNCH(1);
         k_guide_tables<<<g->n_cells, GT_THREADS, 0, as_stream(stream)>>>(energy, g->n_bins, g->prefix);
     }
     CUDA_TRY(cudaPeekAtLastError());
@@ -710,6 +717,7 @@ extern "C" mpg_status mpg_guide_reset(mpg_guide *g, void *stream) {
         mpg_status st = build_dir_tables(g, g->hist, as_stream(stream));
         if (st != MPG_OK) return st;
     } else {
+        COUNT_LAUNCH(1);
         k_guide_tables<<<g->n_cells, GT_THREADS, 0, as_stream(stream)>>>(g->hist, g->n_bins, g->prefix);
     }
     CUDA_TRY(cudaPeekAtLastError());
@@ -725,10 +733,12 @@ extern "C" mpg_status mpg_guide_accumulate(mpg_guide *g, const mpg_query *q, con
     int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 8);
     if (g->desc.domain == 1) {
         ARG_CHECK(wb->ctype, "typed direction guide needs walk ctype");
+        COUNT_LAUNCH(1);
         k_accumulate_dir<<<blocks, 256, 0, as_stream(stream)>>>(g->desc, (const float4 *)q->xD, q->spp, n,
                                                                 (const float4 *)wb->chain, wb->status, wb->w,
                                                                 wb->ctype, g->hist);
     } else {
+        COUNT_LAUNCH(1);
         k_accumulate<<<blocks, 256, 0, as_stream(stream)>>>(g->desc, (const float4 *)q->xD, q->spp, n,
                                                             (const float4 *)wb->chain, wb->status, wb->w, g->hist);
     }
@@ -742,6 +752,7 @@ extern "C" mpg_status mpg_guide_rebuild(mpg_guide *g, void *stream) {
         mpg_status st = build_dir_tables(g, g->hist, as_stream(stream));
         if (st != MPG_OK) return st;
     } else {
+        COUNT_LAUNCH(1);
         k_guide_tables<<<g->n_cells, GT_THREADS, 0, as_stream(stream)>>>(g->hist, g->n_bins, g->prefix);
     }
     CUDA_TRY(cudaPeekAtLastError());
@@ -847,6 +858,7 @@ extern "C" mpg_status mpg_sample_seeds(const mpg_scene *scene, const mpg_guide *
     if (n == 0) return MPG_OK;
     ARG_CHECK(q->xD && sb->xL && sb->target && sb->bin, "NULL query/seed array");
     int blocks = (int)std::min<int64_t>((n + 255) / 256, (int64_t)num_sms() * 8);
+    COUNT_LAUNCH(1);
     k_seeds<<<blocks, 256, 0, as_stream(stream)>>>(scene->d, g, (const float4 *)q->xD, n, q->spp, o->walk_id_base,
                                                    (float4 *)sb->xL, (float4 *)sb->target, sb->bin, sb->ctype,
                                                    sb->pn);
@@ -928,6 +940,7 @@ static mpg_status launch_walk(const DScene &S, const SeedCtx &g, WalkParams P, c
     }
     int64_t want = (P.n + 127) / 128;
     int blocks = (int)std::min<int64_t>(want, (int64_t)num_sms() * occ);
+    COUNT_LAUNCH(1);
     k_walk<KMAX, R><<<blocks, 128, 0, st>>>(S, g, P);
     CUDA_TRY(cudaPeekAtLastError());
     if (!P.trials_on || P.k_max <= P.local_trials) return MPG_OK;
@@ -951,9 +964,11 @@ static mpg_status launch_walk(const DScene &S, const SeedCtx &g, WalkParams P, c
         RP.hard_pct = cl[cur];
         RP.queue = (unsigned long long *)(base + 8);
         CUDA_TRY(cudaMemsetAsync(base + 8, 0, 8, st));
+        COUNT_LAUNCH(1);
         k_walk<KMAX, R><<<rblocks, 128, 0, st>>>(S, g, RP);
         CUDA_TRY(cudaPeekAtLastError());
         CUDA_TRY(cudaMemsetAsync(cnt + (cur ^ 1), 0, 4, st));
+        COUNT_LAUNCH(1);
         k_hard_compact<<<num_sms() * 2, 256, 0, st>>>(wl[cur], pl[cur], cl[cur], bl[cur], cnt + cur, cap, wl[cur ^ 1],
                                                       pl[cur ^ 1], cl[cur ^ 1], bl[cur ^ 1], cnt + (cur ^ 1),
                                                       t0 + Bc - 1, P.k_max, P.T, P.seed_xL, P.seed_pn, P.trials,
@@ -1033,16 +1048,22 @@ static mpg_status launch_wavefront(const DScene &S, const SeedCtx &g, const Walk
     CUDA_TRY(cudaMemsetAsync(P.hdr, 0, sizeof(WFHeader), st));
     if (MP.host_loop) { // host-driven waves (profilers cannot see kernels inside conditional graphs)
         P.use_cond = 0;
+        COUNT_LAUNCH(1);
         k_wf_init<KMAX><<<gi, 256, 0, st>>>(S, g, P);
         CUDA_TRY(cudaPeekAtLastError());
         unsigned int more = 1;
         for (int wave = 0; more; wave++) {
             for (int i = 0; i < nk; i++) {
+                COUNT_LAUNCH(1);
                 k_wf_rays<<<gt, 128, 0, st>>>(S, P, i, ro[i], rd[i]);
+                COUNT_LAUNCH(1);
                 k_wf_post<<<i == 0 ? gp0 : gp, 128, 0, st>>>(S, P, i, rd[i], ro[i + 1], rd[i + 1]);
             }
+            COUNT_LAUNCH(1);
             k_wf_update<KMAX, R><<<gu, 128, 0, st>>>(S, g, P);
+            COUNT_LAUNCH(1);
             k_wf_plan<<<1, 1, 0, st>>>(P);
+            COUNT_LAUNCH(1);
             k_wf_refill<KMAX><<<gr, 256, 0, st>>>(S, g, P);
             CUDA_TRY(cudaPeekAtLastError());
             if ((wave & 7) == 7) {
@@ -1111,8 +1132,10 @@ static mpg_status launch_wavefront(const DScene &S, const SeedCtx &g, const Walk
         g_wfcache.exec = ex;
         g_wfcache.key = key;
     }
+    COUNT_LAUNCH(1);
     k_wf_init<KMAX><<<gi, 256, 0, st>>>(S, g, P);
     CUDA_TRY(cudaPeekAtLastError());
+    COUNT_LAUNCH(1);
     CUDA_TRY(cudaGraphLaunch(g_wfcache.exec, st));
     return MPG_OK;
 }
@@ -1233,6 +1256,7 @@ extern "C" mpg_status mpg_estimate(const float *w, int64_t n_recv, int32_t spp, 
     ARG_CHECK(w && mean && n_recv >= 0 && spp >= 1, "bad argument");
     if (n_recv == 0) return MPG_OK;
     int blocks = (int)std::min<int64_t>((n_recv + 255) / 256, (int64_t)num_sms() * 8);
+    COUNT_LAUNCH(1);
     k_estimate<<<blocks, 256, 0, as_stream(stream)>>>(w, n_recv, spp, mean, var);
     CUDA_TRY(cudaPeekAtLastError());
     return MPG_OK;
@@ -1240,3 +1264,4 @@ extern "C" mpg_status mpg_estimate(const float *w, int64_t n_recv, int32_t spp, 
 
 extern "C" const char *mpg_last_error(void) { return g_err.c_str(); }
 extern "C" int32_t mpg_version(void) { return 1; }
+extern "C" uint64_t mpg_kernel_launches(void) { return g_launches.load(std::memory_order_relaxed); }

@@ -87,7 +87,7 @@ class mpg_scene_info(C.Structure):
 EXPORTS = ["mpg_scene_create", "mpg_scene_destroy", "mpg_scene_get_info", "mpg_trace_rays", "mpg_guide_create",
            "mpg_guide_destroy", "mpg_guide_upload", "mpg_guide_reset", "mpg_guide_accumulate", "mpg_guide_rebuild",
            "mpg_guide_download", "mpg_guide_download_dir_tables", "mpg_sample_seeds", "mpg_walk_workspace_size", "mpg_manifold_walk", "mpg_estimate",
-           "mpg_debug_trace", "mpg_last_error", "mpg_version"]
+           "mpg_debug_trace", "mpg_last_error", "mpg_version", "mpg_kernel_launches"]
 
 _lib = None
 
@@ -125,6 +125,7 @@ def lib():
             "mpg_debug_trace": (st, [P, C.c_int64, C.c_int32]),
             "mpg_last_error": (C.c_char_p, []),
             "mpg_version": (C.c_int32, []),
+            "mpg_kernel_launches": (C.c_uint64, []),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -238,6 +239,10 @@ def mpg_debug_trace(buf=None, n_walks=0, stride=0):
 
 def mpg_version() -> int:
     return int(lib().mpg_version())
+
+
+def mpg_kernel_launches() -> int:
+    return int(lib().mpg_kernel_launches())
 
 
 # ----------------------------------------------------------------------------
