@@ -100,16 +100,147 @@ struct DLight {
     float3 pos, eu, ev, n, l1, l2; // n: emission normal; l1,l2: orthonormal axes of the light plane
 };
 
+// Per-vertex arrays indexed by a rolled loop's counter.  With N <= MPG_SEL_MAX
+// the access is a select chain over register-resident elements instead of a
+// local-memory index; measured slower for k = 2 (configs[1] 67.6 -> 71.6 ms:
+// more spills at the 80-register cap), so direct indexing is the default.
+#ifndef MPG_SEL_MAX
+#define MPG_SEL_MAX 0
+#endif
+template <typename T, int N> __device__ __forceinline__ T rget(const T (&a)[N], int i) {
+    if constexpr (N <= MPG_SEL_MAX) {
+        T r = a[0];
+#pragma unroll
+        for (int j = 1; j < N; j++)
+            if (i == j) r = a[j];
+        return r;
+    } else {
+        return a[i];
+    }
+}
+template <typename T, int N> __device__ __forceinline__ void rset(T (&a)[N], int i, const T &v) {
+    if constexpr (N <= MPG_SEL_MAX) {
+#pragma unroll
+        for (int j = 0; j < N; j++)
+            if (i == j) a[j] = v;
+    } else {
+        a[i] = v;
+    }
+}
+template <typename T, int N, int M> __device__ __forceinline__ T rget2(const T (&a)[N][M], int i, int c) {
+    if constexpr (N <= MPG_SEL_MAX) {
+        T r = a[0][c];
+#pragma unroll
+        for (int j = 1; j < N; j++)
+            if (i == j) r = a[j][c];
+        return r;
+    } else {
+        return a[i][c];
+    }
+}
+template <typename T, int N, int M> __device__ __forceinline__ void rset2(T (&a)[N][M], int i, int c, T v) {
+    if constexpr (N <= MPG_SEL_MAX) {
+#pragma unroll
+        for (int j = 0; j < N; j++)
+            if (i == j) a[j][c] = v;
+    } else {
+        a[i][c] = v;
+    }
+}
+
 // triangle record stride in float4: v0, v1, v2 (48 B; a 64-B record read with two
 // 256-bit loads, LDG.E.ENL2.256, measured no faster on configs[1,2])
 #define TSTRIDE 3
+
+// BVH node layout.  MPG_BVH4 = 0 (default): binary SAH nodes, 4 float4 (64 B):
+// two child boxes + two child refs.  MPG_BVH4 = 1: 4-wide nodes collapsed from
+// the binary tree, 8 float4 (128 B) SoA: lo_x[4], hi_x[4], lo_y[4], hi_y[4],
+// lo_z[4], hi_z[4], child refs[4], pad; children sorted by entry distance.
+// Measured (ms/step, persistent kernel): configs[1] 67.4 -> 71.8, [2] 450 -> 472,
+// [3] 356 -> 299, [4] 460 -> 440 (half the node visits, but a costlier visit
+// and more spills at the 80-register cap) -- binary stays the default because
+// configs[1] is the headline workload.
+// Child ref: >= 0 node index, < 0 leaf ~(first_tri << 3 | count - 1),
+// 0x7fffffff empty slot (point box at 3e38: never entered).
+#ifndef MPG_BVH4
+#define MPG_BVH4 0
+#endif
+#define NODE_F4 (MPG_BVH4 ? 8 : 4)
+#define TRAV_STACK (MPG_BVH4 ? 96 : 64)
+
+// One node visit of the ordered traversal: returns the nearest child whose box
+// overlaps [tmin, tmax] (or pops the stack if none) and pushes the others
+// far-to-near.  Same slab arithmetic for both layouts.
+__device__ __forceinline__ int bvh_visit(const float4 *nodes, int node, float3 o, float3 idir, float tmin,
+                                         float tmax, int *stack, int &sp) {
+#if MPG_BVH4
+    const float4 *nd = nodes + NODE_F4 * node;
+    const float4 lx = __ldg(nd), hx = __ldg(nd + 1), ly = __ldg(nd + 2), hy = __ldg(nd + 3), lz = __ldg(nd + 4),
+                 hz = __ldg(nd + 5);
+    const int4 ch = __ldg(reinterpret_cast<const int4 *>(nd + 6));
+    const float INF = __int_as_float(0x7f800000);
+    float t[4];
+    int c[4] = {ch.x, ch.y, ch.z, ch.w};
+#define MPG_SLAB(J, LX, HX, LY, HY, LZ, HZ)                                                         \
+    {                                                                                                \
+        float x0 = (LX - o.x) * idir.x, x1 = (HX - o.x) * idir.x;                                    \
+        float y0 = (LY - o.y) * idir.y, y1 = (HY - o.y) * idir.y;                                    \
+        float z0 = (LZ - o.z) * idir.z, z1 = (HZ - o.z) * idir.z;                                    \
+        float tn = fmaxf(fmaxf(fminf(x0, x1), fminf(y0, y1)), fmaxf(fminf(z0, z1), tmin));           \
+        float tf = fminf(fminf(fmaxf(x0, x1), fmaxf(y0, y1)), fminf(fmaxf(z0, z1), tmax));           \
+        t[J] = tn <= tf ? tn : INF;                                                                  \
+    }
+    MPG_SLAB(0, lx.x, hx.x, ly.x, hy.x, lz.x, hz.x)
+    MPG_SLAB(1, lx.y, hx.y, ly.y, hy.y, lz.y, hz.y)
+    MPG_SLAB(2, lx.z, hx.z, ly.z, hy.z, lz.z, hz.z)
+    MPG_SLAB(3, lx.w, hx.w, ly.w, hy.w, lz.w, hz.w)
+#undef MPG_SLAB
+#define MPG_CAS(A, B)                                                                                \
+    {                                                                                                \
+        bool sw = t[B] < t[A];                                                                       \
+        float ta = sw ? t[B] : t[A], tb = sw ? t[A] : t[B];                                          \
+        int ca = sw ? c[B] : c[A], cb = sw ? c[A] : c[B];                                            \
+        t[A] = ta; t[B] = tb; c[A] = ca; c[B] = cb;                                                  \
+    }
+    MPG_CAS(0, 1) MPG_CAS(2, 3) MPG_CAS(0, 2) MPG_CAS(1, 3) MPG_CAS(1, 2)
+#undef MPG_CAS
+    if (t[0] == INF) return stack[--sp];
+    if (t[3] != INF) stack[sp++] = c[3];
+    if (t[2] != INF) stack[sp++] = c[2];
+    if (t[1] != INF) stack[sp++] = c[1];
+    return c[0];
+#else
+    const float4 *nd = nodes + NODE_F4 * node;
+    float4 a = __ldg(nd), b = __ldg(nd + 1), c = __ldg(nd + 2);
+    int4 ch = __ldg(reinterpret_cast<const int4 *>(nd + 3));
+    float tx0 = (a.x - o.x) * idir.x, tx1 = (a.w - o.x) * idir.x;
+    float ty0 = (a.y - o.y) * idir.y, ty1 = (b.x - o.y) * idir.y;
+    float tz0 = (a.z - o.z) * idir.z, tz1 = (b.y - o.z) * idir.z;
+    float n0 = fmaxf(fmaxf(fminf(tx0, tx1), fminf(ty0, ty1)), fmaxf(fminf(tz0, tz1), tmin));
+    float f0 = fminf(fminf(fmaxf(tx0, tx1), fmaxf(ty0, ty1)), fminf(fmaxf(tz0, tz1), tmax));
+    float sx0 = (b.z - o.x) * idir.x, sx1 = (c.y - o.x) * idir.x;
+    float sy0 = (b.w - o.y) * idir.y, sy1 = (c.z - o.y) * idir.y;
+    float sz0 = (c.x - o.z) * idir.z, sz1 = (c.w - o.z) * idir.z;
+    float n1 = fmaxf(fmaxf(fminf(sx0, sx1), fminf(sy0, sy1)), fmaxf(fminf(sz0, sz1), tmin));
+    float f1 = fminf(fminf(fmaxf(sx0, sx1), fmaxf(sy0, sy1)), fminf(fmaxf(sz0, sz1), tmax));
+    bool h0 = n0 <= f0, h1 = n1 <= f1;
+    if (h0 && h1) {
+        bool swp = n1 < n0;
+        stack[sp++] = swp ? ch.x : ch.y;
+        return swp ? ch.y : ch.x;
+    }
+    if (h0) return ch.x;
+    if (h1) return ch.y;
+    return stack[--sp];
+#endif
+}
 
 struct DScene {
     int n_surf, n_light, n_tri, n_nodes;
     float extent;
     DSurf surf[DS_MAX_SURF];
     DLight light[DS_MAX_LIGHT];
-    const float4 *nodes; // 4 float4 per BVH2 node: child boxes + child refs
+    const float4 *nodes; // NODE_F4 float4 per node (see bvh_visit)
     const float4 *tpos;  // BVH order, TSTRIDE float4 per tri; v0.w = original tri id, v1.w = surf id, v2.w = specular flag
     const float4 *tnrm;  // BVH order, 3 float4 per tri: vertex shading normals
     const int4 *oidx;    // original order: vertex indices (w: BVH slot)
@@ -269,38 +400,14 @@ __device__ bool trace(const DScene &S, float3 o, float3 d, float tmin, float tma
                 bb0 = c0; bb1 = c1; bb2 = c2;
             }
         }
-        int stack[64];
+        int stack[TRAV_STACK];
         stack[0] = SENT;
         int sp = 1;
         int node = 0, leaf = NONE;
         while (node != SENT || leaf != NONE) {
             while (node >= 0 && node != SENT) {
                 st.nodes++;
-                const float4 *nd = S.nodes + 4 * node;
-                float4 a = __ldg(nd), b = __ldg(nd + 1), c = __ldg(nd + 2);
-                int4 ch = __ldg(reinterpret_cast<const int4 *>(nd + 3));
-                float tx0 = (a.x - o.x) * r.idir.x, tx1 = (a.w - o.x) * r.idir.x;
-                float ty0 = (a.y - o.y) * r.idir.y, ty1 = (b.x - o.y) * r.idir.y;
-                float tz0 = (a.z - o.z) * r.idir.z, tz1 = (b.y - o.z) * r.idir.z;
-                float n0 = fmaxf(fmaxf(fminf(tx0, tx1), fminf(ty0, ty1)), fmaxf(fminf(tz0, tz1), tmin));
-                float f0 = fminf(fminf(fmaxf(tx0, tx1), fmaxf(ty0, ty1)), fminf(fmaxf(tz0, tz1), best));
-                float sx0 = (b.z - o.x) * r.idir.x, sx1 = (c.y - o.x) * r.idir.x;
-                float sy0 = (b.w - o.y) * r.idir.y, sy1 = (c.z - o.y) * r.idir.y;
-                float sz0 = (c.x - o.z) * r.idir.z, sz1 = (c.w - o.z) * r.idir.z;
-                float n1 = fmaxf(fmaxf(fminf(sx0, sx1), fminf(sy0, sy1)), fmaxf(fminf(sz0, sz1), tmin));
-                float f1 = fminf(fminf(fmaxf(sx0, sx1), fmaxf(sy0, sy1)), fminf(fmaxf(sz0, sz1), best));
-                bool h0 = n0 <= f0, h1 = n1 <= f1;
-                if (h0 && h1) {
-                    bool swp = n1 < n0;
-                    node = swp ? ch.y : ch.x;
-                    stack[sp++] = swp ? ch.x : ch.y;
-                } else if (h0) {
-                    node = ch.x;
-                } else if (h1) {
-                    node = ch.y;
-                } else {
-                    node = stack[--sp];
-                }
+                node = bvh_visit(S.nodes, node, o, r.idir, tmin, best, stack, sp);
                 if (node < 0 && leaf == NONE) { // postpone the leaf, keep traversing
                     leaf = node;
                     node = stack[--sp];

@@ -10,6 +10,7 @@
 #include <cstring>
 #include <string>
 #include <atomic>
+#include <functional>
 #include <vector>
 
 #include "mpg.h"
@@ -344,11 +345,58 @@ extern "C" mpg_status mpg_scene_create(const mpg_surface_desc *surfaces, int32_t
             for (int a = 0; a < 3; a++) { nd.b[a] = rlo[a]; }
             nd.b[3] = rhi[0]; nd.b[4] = rhi[1]; nd.b[5] = rhi[2];
             for (int a = 6; a < 9; a++) nd.b[a] = 3e38f;
-            for (int a = 9; a < 12; a++) nd.b[a] = -3e38f;
+            for (int a = 9; a < 12; a++) nd.b[a] = 3e38f;   // empty sibling: point box at 3e38 (never entered)
             nd.c0 = root; nd.c1 = root;
             B.nodes.insert(B.nodes.begin(), nd);
         }
         if (B.max_depth > 60) { mpg_scene_destroy(s); return fail(MPG_ERR_UNSUPPORTED, "BVH too deep"); }
+#if MPG_BVH4
+        // collapse the binary SAH tree into a 4-wide one (children = grandchildren):
+        // half the dependent node fetches per ray; 128-B SoA nodes (NODE_F4 float4)
+        std::vector<float> w4;
+        std::function<int(int)> collapse = [&](int n2) -> int {
+            const BNode &nd = B.nodes[n2];
+            int ref[4], cnt = 0;
+            float box[4][6];
+            for (int c = 0; c < 2; c++) {
+                int ch = c == 0 ? nd.c0 : nd.c1;
+                const float *bb = nd.b + 6 * c; // lo x,y,z, hi x,y,z
+                if (ch >= 0) {
+                    const BNode &g = B.nodes[ch];
+                    for (int e = 0; e < 2; e++) {
+                        ref[cnt] = e == 0 ? g.c0 : g.c1;
+                        for (int a = 0; a < 6; a++) box[cnt][a] = g.b[6 * e + a];
+                        cnt++;
+                    }
+                } else {
+                    ref[cnt] = ch;
+                    for (int a = 0; a < 6; a++) box[cnt][a] = bb[a];
+                    cnt++;
+                }
+            }
+            const int id = (int)(w4.size() / (4 * NODE_F4));
+            w4.resize(w4.size() + 4 * NODE_F4, 0.f);
+            for (int j = 0; j < cnt; j++)
+                if (ref[j] >= 0) ref[j] = collapse(ref[j]);
+            float *o = w4.data() + (size_t)id * 4 * NODE_F4;
+            for (int j = 0; j < 4; j++) {
+                const bool on = j < cnt;
+                for (int a = 0; a < 3; a++) {
+                    // empty slot: a point box at (3e38, 3e38, 3e38) -- never entered for any
+                    // direction sign (an inverted lo > hi box is NOT rejected by min/max slabs)
+                    o[8 * a + j] = on ? box[j][a] : 3e38f;          // lo_a[j]
+                    o[8 * a + 4 + j] = on ? box[j][3 + a] : 3e38f;  // hi_a[j]
+                }
+                int r = on ? ref[j] : 0x7fffffff;
+                memcpy(&o[24 + j], &r, 4);
+            }
+            return id;
+        };
+        collapse(0);
+        d.n_nodes = (int)(w4.size() / (4 * NODE_F4));
+        nodes4.resize((size_t)NODE_F4 * d.n_nodes);
+        memcpy(nodes4.data(), w4.data(), w4.size() * sizeof(float));
+#else
         d.n_nodes = (int)B.nodes.size();
         nodes4.resize(4 * d.n_nodes);
         for (int i = 0; i < d.n_nodes; i++) {
@@ -359,6 +407,7 @@ extern "C" mpg_status mpg_scene_create(const mpg_surface_desc *surfaces, int32_t
             int4 ch = make_int4(nd.c0, nd.c1, 0, 0);
             memcpy(&nodes4[4 * i + 3], &ch, sizeof(int4));
         }
+#endif
         tpos.assign((size_t)TSTRIDE * d.n_tri, make_float4(0.f, 0.f, 0.f, 0.f));
         tnrm.resize(3 * d.n_tri);
         for (int j = 0; j < d.n_tri; j++) {
@@ -935,6 +984,10 @@ template <int KMAX, typename R>
 static mpg_status launch_walk(const DScene &S, const SeedCtx &g, WalkParams P, cudaStream_t st, void *ws) {
     static int occ = 0;
     if (!occ) {
+#ifdef MPG_CARVEOUT
+        // unified L1/shared split: this kernel uses 152 B of shared memory; prefer L1
+        CUDA_TRY(cudaFuncSetAttribute(k_walk<KMAX, R>, cudaFuncAttributePreferredSharedMemoryCarveout, MPG_CARVEOUT));
+#endif
         CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_walk<KMAX, R>, 128, 0));
         if (occ <= 0) occ = 1;
     }

@@ -189,44 +189,50 @@ __device__ __forceinline__ int newton_system(const DScene &S, int k, uint32_t ta
 #pragma unroll 1
     for (int i = 0; i < KMAX; i++) {
         if (i >= k) break;
-        double3 a = i == 0 ? d3f(xD) : x[i > 0 ? i - 1 : 0];
-        double3 b = i == k - 1 ? d3f(xL) : x[i + 1 < KMAX ? i + 1 : i];
-        const DSurf &f = S.surf[surf[i]];
+        const double3 xi = rget(x, i);
+        const int pi = rget(prim, i), si = rget(surf, i);
+        const V3<R> sgi = rget(sg, i), tgi = rget(tg, i);
+        double3 a = i == 0 ? d3f(xD) : rget(x, i > 0 ? i - 1 : 0);
+        double3 b = i == k - 1 ? d3f(xL) : rget(x, i + 1 < KMAX ? i + 1 : i);
+        const DSurf &f = S.surf[si];
         V3<R> dna, dnb;
-        V3<R> n = shadingR<R>(S, prim[i], surf[i], x[i], sg[i], tg[i], dna, dnb);
+        V3<R> n = shadingR<R>(S, pi, si, xi, sgi, tgi, dna, dnb);
         VTermR<R> v;
-        if (!vtermR<R>(a, x[i], b, crossR(sg[i], tg[i]), n, f, (tau >> i) & 1u, v)) { degen = true; break; }
+        if (!vtermR<R>(a, xi, b, crossR(sgi, tgi), n, f, (tau >> i) & 1u, v)) { degen = true; break; }
         cmax = fmax(cmax, fmax(fabs(v.c0), fabs(v.c1)));
         R D00, D10, D01, D11;
-        dC_selfR(v, sg[i], dna, D00, D10);
-        dC_selfR(v, tg[i], dnb, D01, D11);
+        dC_selfR(v, sgi, dna, D00, D10);
+        dC_selfR(v, tgi, dnb, D01, D11);
         R r0 = (R)(-v.c0), r1 = (R)(-v.c1);
         if (i > 0) {
             const int j = i > 0 ? i - 1 : 0;
             R l00, l10, l01, l11;
-            dC_nbR(v, v.wi, v.li, v.ei, sg[j], l00, l10);
-            dC_nbR(v, v.wi, v.li, v.ei, tg[j], l01, l11);
-            R M00 = l00 * Di[j][0] + l01 * Di[j][2], M01 = l00 * Di[j][1] + l01 * Di[j][3];
-            R M10 = l10 * Di[j][0] + l11 * Di[j][2], M11 = l10 * Di[j][1] + l11 * Di[j][3];
-            D00 -= M00 * Ub[j][0] + M01 * Ub[j][2];
-            D01 -= M00 * Ub[j][1] + M01 * Ub[j][3];
-            D10 -= M10 * Ub[j][0] + M11 * Ub[j][2];
-            D11 -= M10 * Ub[j][1] + M11 * Ub[j][3];
-            r0 -= M00 * rp[j][0] + M01 * rp[j][1];
-            r1 -= M10 * rp[j][0] + M11 * rp[j][1];
+            dC_nbR(v, v.wi, v.li, v.ei, rget(sg, j), l00, l10);
+            dC_nbR(v, v.wi, v.li, v.ei, rget(tg, j), l01, l11);
+            const R d0 = rget2(Di, j, 0), d1 = rget2(Di, j, 1), d2 = rget2(Di, j, 2), d3 = rget2(Di, j, 3);
+            const R u0 = rget2(Ub, j, 0), u1 = rget2(Ub, j, 1), u2 = rget2(Ub, j, 2), u3 = rget2(Ub, j, 3);
+            R M00 = l00 * d0 + l01 * d2, M01 = l00 * d1 + l01 * d3;
+            R M10 = l10 * d0 + l11 * d2, M11 = l10 * d1 + l11 * d3;
+            D00 -= M00 * u0 + M01 * u2;
+            D01 -= M00 * u1 + M01 * u3;
+            D10 -= M10 * u0 + M11 * u2;
+            D11 -= M10 * u1 + M11 * u3;
+            const R p0 = rget2(rp, j, 0), p1 = rget2(rp, j, 1);
+            r0 -= M00 * p0 + M01 * p1;
+            r1 -= M10 * p0 + M11 * p1;
         }
         if (i < k - 1) {
             const int j = i + 1 < KMAX ? i + 1 : i;
             R u00, u10, u01, u11;
-            dC_nbR(v, v.wo, v.lo, v.eo, sg[j], u00, u10);
-            dC_nbR(v, v.wo, v.lo, v.eo, tg[j], u01, u11);
-            Ub[i][0] = u00; Ub[i][1] = u01; Ub[i][2] = u10; Ub[i][3] = u11;
+            dC_nbR(v, v.wo, v.lo, v.eo, rget(sg, j), u00, u10);
+            dC_nbR(v, v.wo, v.lo, v.eo, rget(tg, j), u01, u11);
+            rset2(Ub, i, 0, u00); rset2(Ub, i, 1, u01); rset2(Ub, i, 2, u10); rset2(Ub, i, 3, u11);
         }
         R det = D00 * D11 - D01 * D10;
         if (!(det != (R)0) || !isfinite(det)) singular = true;
         R id = (R)1 / det;
-        Di[i][0] = D11 * id; Di[i][1] = -D01 * id; Di[i][2] = -D10 * id; Di[i][3] = D00 * id;
-        rp[i][0] = r0; rp[i][1] = r1;
+        rset2(Di, i, 0, D11 * id); rset2(Di, i, 1, -D01 * id); rset2(Di, i, 2, -D10 * id); rset2(Di, i, 3, D00 * id);
+        rset2(rp, i, 0, r0); rset2(rp, i, 1, r1);
     }
     cmax_out = (float)cmax;
     if (degen || !isfinite(cmax)) return 2;
@@ -259,27 +265,29 @@ __device__ MPG_COLD bool post_sweep(const DScene &S, const DLight &L, int k, uin
 #pragma unroll 1
     for (int i = 0; i < KMAX; i++) {
         if (i >= k) break;
-        double3 a = i == 0 ? d3f(xD) : x[i > 0 ? i - 1 : 0];
-        double3 b = i == k - 1 ? d3f(xL) : x[i + 1 < KMAX ? i + 1 : i];
-        const DSurf &f = S.surf[surf[i]];
-        V3<R> ng = geo_normalR<R>(S, prim[i], surf[i], x[i]);
-        R di = dotR(fromd<R>(a - x[i]), ng), dd = dotR(fromd<R>(b - x[i]), ng);
+        const double3 xi = rget(x, i);
+        const int pi = rget(prim, i), si = rget(surf, i);
+        double3 a = i == 0 ? d3f(xD) : rget(x, i > 0 ? i - 1 : 0);
+        double3 b = i == k - 1 ? d3f(xL) : rget(x, i + 1 < KMAX ? i + 1 : i);
+        const DSurf &f = S.surf[si];
+        V3<R> ng = geo_normalR<R>(S, pi, si, xi);
+        R di = dotR(fromd<R>(a - xi), ng), dd = dotR(fromd<R>(b - xi), ng);
         bool isT = (tau >> i) & 1u;
         if (isT ? !(di * dd < (R)0) : !(di * dd > (R)0)) return false;
         if (!want_kappa) continue;
         V3<R> z = mk3<R>(0, 0, 0), dna, dnb;
-        V3<R> n = shadingR<R>(S, prim[i], surf[i], x[i], z, z, dna, dnb);
+        V3<R> n = shadingR<R>(S, pi, si, xi, z, z, dna, dnb);
         bool oi = di > (R)0, oo = dd > (R)0;
         R e_wi = oi ? (R)f.eta_out : (R)f.eta_in, e_wo = oo ? (R)f.eta_out : (R)f.eta_in;
         if (i == 0) etaD = e_wi;
         if (i == k - 1) {
             etaL = e_wo;
             VTermR<R> v;
-            if (!vtermR<R>(a, x[i], b, ng, n, f, isT, v)) { DL[0] = DL[1] = DL[2] = DL[3] = 0; }
+            if (!vtermR<R>(a, xi, b, ng, n, f, isT, v)) { DL[0] = DL[1] = DL[2] = DL[3] = 0; }
             else {
                 V3<R> l1, l2;
                 if (L.kind == 1) { l1 = fromf<R>(L.l1); l2 = fromf<R>(L.l2); }
-                else onbR(nrmR(fromd<R>(d3f(xL) - x[i])), l1, l2);
+                else onbR(nrmR(fromd<R>(d3f(xL) - xi)), l1, l2);
                 dC_nbR(v, v.wo, v.lo, v.eo, l1, DL[0], DL[2]);
                 dC_nbR(v, v.wo, v.lo, v.eo, l2, DL[1], DL[3]);
             }
@@ -287,7 +295,7 @@ __device__ MPG_COLD bool post_sweep(const DScene &S, const DLight &L, int k, uin
         if (f.mat == 0) kap *= (R)f.refl;
         else {
             R e_other = oi ? (R)f.eta_in : (R)f.eta_out;
-            V3<R> wi = nrmR(fromd<R>(a - x[i]));
+            V3<R> wi = nrmR(fromd<R>(a - xi));
             R F = fresnelR<R>(dotR(wi, n), e_wi, e_other);
             kap *= isT ? ((R)1 - F) : F;
         }

@@ -17,6 +17,9 @@
 // analytic GGT by one more back-substitution with the 2-column light RHS (R11),
 // and reciprocal-probability trials (Eq. 15, R13).
 #pragma once
+#ifndef MPG_WALK_MINB2
+#define MPG_WALK_MINB2 6   // k <= 2: 80 registers (measured best of 64/80/96/148)
+#endif
 #include "device_common.cuh"
 #include "seed.cuh"
 #include "newton.cuh"
@@ -154,9 +157,9 @@ __device__ __forceinline__ double3 refine_hit(const DScene &S, int prim, int sur
 // a conductor fails (R22, R14).  The resolved string is returned in tau_res.
 template <int KMAX>
 __device__ __forceinline__ int trace_chain(const DScene &S, bool deduce, int k, uint32_t bits, bool learned,
-                                           float3 xD, float3 tgt, const double3 *q, const int *hint,
-                                           uint32_t surf_req, float eps,
-                                           double3 *y, int *yp, int *ys, LaneStats &st, uint32_t &tau_res) {
+                                           float3 xD, float3 tgt, const double3 (&q)[KMAX], const int (&hint)[KMAX],
+                                           uint32_t surf_req, float eps, double3 (&y)[KMAX], int (&yp)[KMAX],
+                                           int (&ys)[KMAX], LaneStats &st, uint32_t &tau_res) {
     uint32_t res = 0;
     double3 o = d3f(xD);
     double3 dd = make_double3(0.0, 0.0, 0.0);
@@ -166,19 +169,21 @@ __device__ __forceinline__ int trace_chain(const DScene &S, bool deduce, int k, 
         if (!(l2 > 0.0)) return 3;
         dd = v * rsqrt(l2);
     }
+    int pprim = -1, psurf = 0;
 #pragma unroll 1
     for (int i = 0; i < k; i++) {
+        const double3 qi = rget(q, i);
         if (!deduce) {
-            double3 v = q[i] - o;
+            double3 v = qi - o;
             double l2 = ddot(v, v);
             if (!(l2 > 0.0)) return 3 | (i << 4);
             dd = v * rsqrt(l2);
         } else if (i > 0) {
-            if (!scatter_dir(S, dd, yp[i - 1], ys[i - 1], f3d(y[i - 1]), (res >> (i - 1)) & 1u)) return 4 | (i << 4);
+            if (!scatter_dir(S, dd, pprim, psurf, f3d(o), (res >> (i - 1)) & 1u)) return 4 | (i << 4);
         }
         Hit h;
         float3 of = f3d(o), d = nrmz(f3d(dd));
-        if (!trace<false>(S, of, d, eps, 3.0e38f, true, h, st, deduce ? -1 : hint[i])) return 1 | (i << 4);
+        if (!trace<false>(S, of, d, eps, 3.0e38f, true, h, st, deduce ? -1 : rget(hint, i))) return 1 | (i << 4);
         if (!deduce && h.surf != (int)((surf_req >> (4 * i)) & 15u)) return 2 | (i << 4);
         if (deduce) {
             uint32_t bit = (bits >> i) & 1u;
@@ -187,17 +192,20 @@ __device__ __forceinline__ int trace_chain(const DScene &S, bool deduce, int k, 
             if (bit && mat != 1) return 4 | (i << 4);
             res |= bit << i;
         }
-        y[i] = refine_hit(S, h.prim, h.surf, o, deduce ? o + dd : q[i], h.p);
-        yp[i] = h.prim;
-        ys[i] = h.surf;
-        o = y[i];
+        const double3 yi = refine_hit(S, h.prim, h.surf, o, deduce ? o + dd : qi, h.p);
+        rset(y, i, yi);
+        rset(yp, i, h.prim);
+        rset(ys, i, h.surf);
+        pprim = h.prim;
+        psurf = h.surf;
+        o = yi;
     }
     tau_res = res;
     return 0;
 }
 
 template <int KMAX, typename R>
-__global__ void __launch_bounds__(128, (KMAX <= 2 ? 6 : 2)) k_walk(const DScene S, const SeedCtx g, const WalkParams P) {
+__global__ void __launch_bounds__(128, (KMAX <= 2 ? MPG_WALK_MINB2 : 2)) k_walk(const DScene S, const SeedCtx g, const WalkParams P) {
     __shared__ unsigned long long s_stats[SS_N];
     for (int i = threadIdx.x; i < SS_N; i += blockDim.x) s_stats[i] = 0ull;
     __syncthreads();

@@ -258,7 +258,7 @@ __global__ void __launch_bounds__(128, WF_TRACE_MINB) k_wf_rays(const DScene S, 
     r.Sx = r.Sy = r.Sz = 0.f;
     float tmax = 0.f;
     int node = SENT, leaf = NONE, sp = 0;
-    int stack[64];
+    int stack[TRAV_STACK];
     int bprim = -2, bsurf = -1;
     float bb0 = 0.f, bb1 = 0.f, bb2 = 0.f;   // barycentrics, or the analytic hit point
     LaneStats ls = {0u, 0u, 0u};
@@ -331,31 +331,7 @@ __global__ void __launch_bounds__(128, WF_TRACE_MINB) k_wf_rays(const DScene S, 
             while (node != SENT || leaf != NONE) {
                 while (node >= 0 && node != SENT) {
                     ls.nodes++;
-                    const float4 *nd = S.nodes + 4 * node;
-                    float4 a = __ldg(nd), b = __ldg(nd + 1), c = __ldg(nd + 2);
-                    int4 ch = __ldg(reinterpret_cast<const int4 *>(nd + 3));
-                    float tx0 = (a.x - o.x) * r.idir.x, tx1 = (a.w - o.x) * r.idir.x;
-                    float ty0 = (a.y - o.y) * r.idir.y, ty1 = (b.x - o.y) * r.idir.y;
-                    float tz0 = (a.z - o.z) * r.idir.z, tz1 = (b.y - o.z) * r.idir.z;
-                    float n0 = fmaxf(fmaxf(fminf(tx0, tx1), fminf(ty0, ty1)), fmaxf(fminf(tz0, tz1), eps));
-                    float f0 = fminf(fminf(fmaxf(tx0, tx1), fmaxf(ty0, ty1)), fminf(fmaxf(tz0, tz1), tmax));
-                    float sx0 = (b.z - o.x) * r.idir.x, sx1 = (c.y - o.x) * r.idir.x;
-                    float sy0 = (b.w - o.y) * r.idir.y, sy1 = (c.z - o.y) * r.idir.y;
-                    float sz0 = (c.x - o.z) * r.idir.z, sz1 = (c.w - o.z) * r.idir.z;
-                    float n1 = fmaxf(fmaxf(fminf(sx0, sx1), fminf(sy0, sy1)), fmaxf(fminf(sz0, sz1), eps));
-                    float f1 = fminf(fminf(fmaxf(sx0, sx1), fmaxf(sy0, sy1)), fminf(fmaxf(sz0, sz1), tmax));
-                    bool h0 = n0 <= f0, h1 = n1 <= f1;
-                    if (h0 && h1) {
-                        bool swp = n1 < n0;
-                        node = swp ? ch.y : ch.x;
-                        stack[sp++] = swp ? ch.x : ch.y;
-                    } else if (h0) {
-                        node = ch.x;
-                    } else if (h1) {
-                        node = ch.y;
-                    } else {
-                        node = stack[--sp];
-                    }
+                    node = bvh_visit(S.nodes, node, o, r.idir, eps, tmax, stack, sp);
                     if (node < 0 && leaf == NONE) { // postpone the leaf, keep traversing
                         leaf = node;
                         node = stack[--sp];
