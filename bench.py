@@ -144,13 +144,17 @@ def run_ours(args):
     import torch
     import torch.distributed as dist
     from paper_2311_12818_b200 import mpg
+    from paper_2311_12818_b200 import dist as D
     rank, world, local = dist_env()
     if world > 1:
         dist.init_process_group("nccl")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     w = make_workload(args.config)
-    w.opts.walk_id_base = rank * w.n_walks          # independent partitions (weak scaling)
+    progressive = w.seed.mode == 3      # configs[4]: one step = the whole 8-iteration loop (R22)
+    iters = 8 if progressive else 1
+    # independent partitions (weak scaling): rank r owns walk ids [r*n*iters, (r+1)*n*iters)
+    w.opts.walk_id_base = D.walk_id_base(rank, w.n_walks * iters)
     ds = mpg.DeviceScene(w)
     b = mpg.Batch(w.xD, w.nD, w.spp, w.seed.k)
     opts = ds.opts(flags=w.opts.flags | (1 if args.wavefront else 0) | (2 if args.hostloop else 0) |
@@ -159,8 +163,6 @@ def run_ours(args):
     guided = ds.guide is not None
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)   # > 126 MB L2
 
-    progressive = w.seed.mode == 3      # configs[4]: one step = the whole 8-iteration loop (R22)
-    iters = 8 if progressive else 1
 
     def step():
         if progressive:
@@ -223,15 +225,7 @@ def run_ours(args):
     fields = mpg.STATS_FIELDS
     S = {f: int(st[:, j].sum()) for j, f in enumerate(fields)}
     conv_total = S["converged"]
-    if world > 1:
-        t = torch.tensor([tot_ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        tot_ms = float(t.item())
-        c = torch.tensor([conv_total, S["newton_iters"]], device=dev, dtype=torch.float64)
-        dist.all_reduce(c, op=dist.ReduceOp.SUM)
-        conv_all, newton_all = float(c[0]), float(c[1])
-    else:
-        conv_all, newton_all = float(conv_total), float(S["newton_iters"])
+    tot_ms, (conv_all, newton_all) = D.reduce_timing(tot_ms, [conv_total, S["newton_iters"]], device=dev)
     value = conv_all / (tot_ms / 1e3)
 
     # ---- roofline of the dominant kernel (k_walk): ALU bound ----
@@ -272,13 +266,7 @@ def run_ours(args):
             e_ms.append(s0.elapsed_time(s1))
             conv_e += conv_total // args.steps      # the walks are deterministic: same count every step
         te = sum(e_ms)
-        if world > 1:
-            t = torch.tensor([te], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            te = float(t.item())
-            c = torch.tensor([float(conv_e)], device=dev, dtype=torch.float64)
-            dist.all_reduce(c, op=dist.ReduceOp.SUM)
-            conv_e = float(c.item())
+        te, (conv_e,) = D.reduce_timing(te, [conv_e], device=dev)
         e2e = {"value": conv_e / (te / 1e3), "unit": "walks/s",
                "h2d_bytes_per_step": int(xh.numel() * 4 + nh.numel() * 4),
                "d2h_bytes_per_step": int(out_h.numel() * 4), "ms_per_step": te / args.steps}

@@ -1,0 +1,45 @@
+"""Multi-GPU plumbing for the batched manifold walk (host logic only).
+
+The walk partitions into independent walks: rank r of N walks
+its own batch with walk ids [base + r*n, base + (r+1)*n) -- every random number
+of a walk is drawn from its walk id (Philox counter, R13), so ranks never share
+a draw and no data-path collective is needed ("scaling": "weak").  The only
+cross-rank operations are measurement (max-over-ranks device time, summed
+counts) and, for a render that spreads one receiver set over ranks, the
+combination of per-rank estimates (Eq. 3 is a mean over walks, so the global
+estimate is the walk-count-weighted mean of the rank means).
+
+torch.distributed carries these (NCCL on the GPU box, gloo in the CPU tests).
+"""
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+
+def walk_id_base(rank: int, n_per_rank: int, base: int = 0) -> int:
+    """First walk id of rank `rank` (disjoint, contiguous partitions)."""
+    return base + rank * n_per_rank
+
+
+def reduce_timing(ms: float, counts, device=None):
+    """(max over ranks of `ms`, sum over ranks of each count) -- bench's aggregation."""
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return float(ms), [float(c) for c in counts]
+    t = torch.tensor([float(ms)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    c = torch.tensor([float(x) for x in counts], dtype=torch.float64, device=device)
+    dist.all_reduce(c, op=dist.ReduceOp.SUM)
+    return float(t.item()), [float(x) for x in c.tolist()]
+
+
+def combine_estimates(mean: torch.Tensor, spp: int) -> torch.Tensor:
+    """Global per-receiver estimate from per-rank means over `spp` walks each:
+    sum_r spp_r * mean_r / sum_r spp_r (all ranks hold the same receivers)."""
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return mean.clone()
+    num = (mean.to(torch.float64) * spp).contiguous()
+    den = torch.tensor([float(spp)], dtype=torch.float64, device=mean.device)
+    dist.all_reduce(num, op=dist.ReduceOp.SUM)
+    dist.all_reduce(den, op=dist.ReduceOp.SUM)
+    return (num / den).to(mean.dtype)
