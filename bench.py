@@ -114,28 +114,82 @@ def oracle_rate(w, n_walks, seed_base=0):
     return conv / dt, dt, conv, int(r["total_iters"].sum())
 
 
+def _oracle_shard(args):
+    cfg, lo, hi, seed_base, barrier = args
+    from oracle import oracle as O
+    w = make_workload(cfg)
+    s = O.OracleScene(w)
+    ids = np.arange(lo, hi, dtype=np.int64)
+    if barrier is not None:
+        barrier.wait()
+    t0 = time.perf_counter()
+    r = s.walks(ids, s.opts(walk_id_base=seed_base))
+    t1 = time.perf_counter()
+    return int(np.isin(r["status"], (0, 5)).sum()), int(r["total_iters"].sum()), t0, t1
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def oracle_rate_parallel(cfg, n_walks, procs, seed_base=0):
+    """The oracle (single-threaded C) on the first n_walks, split into `procs`
+    contiguous shards run by that many worker processes on the host cores.
+    Scene/BVH builds are excluded (workers start timing together after a barrier).
+    Returns (converged/s, wall s, converged, Newton iterations)."""
+    import multiprocessing as mpr
+    procs = max(1, min(procs, n_walks))
+    if procs == 1:
+        c, it, t0, t1 = _oracle_shard((cfg, 0, n_walks, seed_base, None))
+        return c / (t1 - t0), t1 - t0, c, it
+    ctx = mpr.get_context("spawn")   # the ours-arm parent holds a CUDA context: never fork it
+    bar = ctx.Manager().Barrier(procs)
+    cuts = np.linspace(0, n_walks, procs + 1).astype(np.int64)
+    with ctx.Pool(procs) as pool:
+        res = pool.map(_oracle_shard, [(cfg, int(cuts[i]), int(cuts[i + 1]), seed_base, bar) for i in range(procs)])
+    c = sum(r[0] for r in res)
+    it = sum(r[1] for r in res)
+    dt = max(r[3] for r in res) - min(r[2] for r in res)
+    return c / dt, dt, c, it
+
+
+def host_procs():
+    return max(1, min(os.cpu_count() or 1, 64))
+
+
 def run_reference(args):
     rank, world, local = dist_env()
     if rank != 0:
         return
     w = make_workload(args.config)
-    n = min(w.n_walks, args.ref_walks)
+    P = host_procs()
+    n = min(w.n_walks, args.ref_walks * P)
     for _ in range(args.warmup):
-        oracle_rate(w, max(64, n // 20))
-    vals, dts = [], []
+        oracle_rate(w, 64)
+    vals, dts, its = [], [], []
     t_all = time.perf_counter()
     for _ in range(args.steps):
-        v, dt, conv, iters = oracle_rate(w, n)
+        v, dt, conv, iters = oracle_rate_parallel(args.config, n, P)
         vals.append(v)
         dts.append(dt)
+        its.append(iters / dt)
     wall = time.perf_counter() - t_all
     value = float(np.mean(vals))
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "walks/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * wall / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": CONFIG_NAMES[args.config], "sample_walks_per_step": n},
-            "cpu_baseline": {"value": value, "unit": "walks/s", "cores": 1, "kind": "oracle",
-                             "sample": f"first {n} walks of the workload per step (of {w.n_walks})"},
+            "newton_iters_per_s": float(np.mean(its)),
+            "cpu_baseline": {"value": value, "unit": "walks/s", "cores": P, "kind": "oracle",
+                             "cpu_model": cpu_model(),
+                             "sample": f"first {n} walks of the workload per step (of {w.n_walks}), "
+                                       f"{P} single-threaded oracle processes on contiguous shards"},
             "e2e": {"value": value, "unit": "walks/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -242,6 +296,22 @@ def run_ours(args):
         except Exception:
             traffic = None
 
+    # ---- compulsory HBM traffic of a step: seeds, walk I/O, estimator ----
+    per_walk = ((16 + 16) / w.spp          # x_D, n_D read by the walk (per receiver)
+                + 16 / w.spp               # x_D read by the seed kernel
+                + 2 * (16 + 16 + 4 + (8 if progressive else 0))   # seeds written, then read (x_L, target, bin[, ctype, P(n)])
+                + 16 * w.seed.k + 1 + 2 + 12 + 4 + (2 if progressive else 0)   # chain, status, iters, G/T/w, trials[, ctype]
+                + 4 + 8 / w.spp)           # estimator: w in, mean/var out
+    hbm_bytes = per_walk * b.n * iters
+    hbm_peak = None
+    try:
+        hbm_peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
+    except Exception:
+        hbm_peak = 6533.8          # MEASURED_PEAKS.json figure for this pool (copy-bandwidth, GB/s)
+    hbm_gbs = hbm_bytes / (tot_ms / args.steps / 1e3) / 1e9
+    hbm = {"bytes_per_step": int(hbm_bytes), "achieved_gbs": hbm_gbs, "peak_gbs": hbm_peak,
+           "frac": hbm_gbs / hbm_peak, "what": "compulsory I/O per step (inputs, seeds, outputs, estimate)"}
+
     # ---- end to end through the public API: pinned host in -> device -> host result ----
     e2e = None
     if not args.no_e2e:
@@ -274,10 +344,13 @@ def run_ours(args):
     # ---- CPU baseline: the oracle on a bounded sample (rank 0, N=1 only) ----
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        n = min(w.n_walks, args.ref_walks)
-        v, dt, conv, _ = oracle_rate(w, n)
-        cpu = {"value": v, "unit": "walks/s", "cores": 1, "kind": "oracle",
-               "sample": f"first {n} walks of the workload ({dt:.1f} s, {conv} converged)"}
+        P = host_procs()
+        n = min(w.n_walks, args.ref_walks * P)
+        v, dt, conv, it = oracle_rate_parallel(args.config, n, P)
+        cpu = {"value": v, "unit": "walks/s", "cores": P, "kind": "oracle", "cpu_model": cpu_model(),
+               "newton_iters_per_s": it / dt,
+               "sample": f"first {n} walks of the workload, {P} single-threaded oracle processes on "
+                         f"contiguous shards ({dt:.1f} s wall, {conv} converged)"}
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "walks/s", "n_gpus": world, "steps": args.steps,
@@ -298,7 +371,7 @@ def run_ours(args):
                              "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
                              "peak_source": "148 SM x 128 FP32 lanes x 2 x 1965 MHz (B200_PROFILING.md unit counts)",
                              "algorithmic_flops_per_launch": flops / args.steps},
-                "hbm": {"bytes_per_step": None},
+                "hbm": hbm,
                 "stats_per_step": {k: v / args.steps for k, v in S.items()},
                 "gpu_launches": launches,
                 "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,

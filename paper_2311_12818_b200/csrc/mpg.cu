@@ -928,14 +928,29 @@ extern "C" mpg_status mpg_debug_trace(float *buf, int64_t n_walks, int32_t strid
     return MPG_OK;
 }
 
-// trial rounds: walks unresolved after LOCAL_TRIALS sequential trials are run
-// in rounds of B = 4, 8, 16, ... parallel trials
+// persistent-kernel workspace: trial header, hard entries
+// (walks unresolved after LOCAL_TRIALS sequential trials), item ring
 #define LOCAL_TRIALS 4u
-static uint32_t hard_cap(int64_t n) { return (uint32_t)std::min<int64_t>(std::max<int64_t>(n, 1), 1 << 21); }
-static size_t mk_ws_bytes(int64_t n) { // hard lists A/B: walk (8 B), psurf, pct, best (4 B each)
-    size_t cap = hard_cap(n);
-    return 256 + 2 * cap * (sizeof(int64_t) + 3 * sizeof(uint32_t));
+struct MKLayout {
+    uint32_t H, C;
+    size_t th, e_walk, e_psurf, e_pct, e_best, e_pending, e_issued, e_batch, items, total;
+};
+static MKLayout mk_layout(int64_t n) {
+    MKLayout L;
+    int64_t nn = std::max<int64_t>(n, 1);
+    L.H = (uint32_t)std::min<int64_t>(nn, 1 << 22);
+    L.C = 8u * L.H + 65536u;
+    size_t o = 0;
+    auto take = [&](size_t bytes) { size_t r = o; o += (bytes + 255) & ~(size_t)255; return r; };
+    L.th = take(sizeof(TrialHdr));
+    L.e_walk = take(8ull * L.H);
+    L.e_psurf = take(4ull * L.H); L.e_pct = take(4ull * L.H); L.e_best = take(4ull * L.H);
+    L.e_pending = take(4ull * L.H); L.e_issued = take(4ull * L.H); L.e_batch = take(4ull * L.H);
+    L.items = take(8ull * L.C);
+    L.total = o;
+    return L;
 }
+static size_t mk_ws_bytes(int64_t n) { return mk_layout(n).total; }
 
 // wavefront workspace layout: header, slot lists, free stack,
 // per-slot SoA state, ray lists, hits, hard entries, trial items
@@ -991,46 +1006,26 @@ static mpg_status launch_walk(const DScene &S, const SeedCtx &g, WalkParams P, c
         CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_walk<KMAX, R>, 128, 0));
         if (occ <= 0) occ = 1;
     }
+    MKLayout L = mk_layout(P.n);
+    char *b = (char *)ws;
+    P.local_trials = LOCAL_TRIALS;
+    P.hard_cap = L.H;
+    // tickets index the ring only below item_cap: it bounds both the reads and the clear;
+    // a full ring (or entry table) makes the walk continue its trials sequentially
+    P.item_cap = P.trials_on ? L.C : 0u;
+    P.th = (TrialHdr *)(b + L.th);
+    P.e_walk = (int64_t *)(b + L.e_walk);
+    P.e_psurf = (uint32_t *)(b + L.e_psurf); P.e_pct = (uint32_t *)(b + L.e_pct); P.e_best = (uint32_t *)(b + L.e_best);
+    P.e_pending = (uint32_t *)(b + L.e_pending); P.e_issued = (uint32_t *)(b + L.e_issued);
+    P.e_batch = (uint32_t *)(b + L.e_batch);
+    P.items = (unsigned long long *)(b + L.items);
+    CUDA_TRY(cudaMemsetAsync(P.th, 0, sizeof(TrialHdr), st));
+    if (P.trials_on) CUDA_TRY(cudaMemsetAsync(P.items, 0xff, 8ull * P.item_cap, st));
     int64_t want = (P.n + 127) / 128;
     int blocks = (int)std::min<int64_t>(want, (int64_t)num_sms() * occ);
     COUNT_LAUNCH(1);
     k_walk<KMAX, R><<<blocks, 128, 0, st>>>(S, g, P);
     CUDA_TRY(cudaPeekAtLastError());
-    if (!P.trials_on || P.k_max <= P.local_trials) return MPG_OK;
-    // parallel trial rounds over the hard list (ping-pong buffers A/B)
-    char *base = (char *)ws;
-    unsigned int *cnt = (unsigned int *)(base + 16); // cnt[0] list A, cnt[1] list B
-    uint32_t cap = P.hard_cap;
-    int64_t *wl[2] = {(int64_t *)(base + 256), (int64_t *)(base + 256 + (size_t)cap * 8)};
-    uint32_t *pl[2] = {(uint32_t *)(base + 256 + (size_t)cap * 16), (uint32_t *)(base + 256 + (size_t)cap * 20)};
-    uint32_t *bl[2] = {(uint32_t *)(base + 256 + (size_t)cap * 24), (uint32_t *)(base + 256 + (size_t)cap * 28)};
-    uint32_t *cl[2] = {(uint32_t *)(base + 256 + (size_t)cap * 32), (uint32_t *)(base + 256 + (size_t)cap * 36)};
-    uint32_t t0 = P.local_trials + 1, B = 4;
-    int cur = 0, rblocks = num_sms() * occ;
-    while (t0 <= P.k_max) {
-        uint32_t Bc = std::min(B, P.k_max - t0 + 1);
-        WalkParams RP = P;
-        RP.round_mode = 1;
-        RP.round_t0 = t0;
-        RP.round_B = Bc;
-        RP.hard_walk = wl[cur]; RP.hard_psurf = pl[cur]; RP.hard_best = bl[cur]; RP.hard_count = cnt + cur;
-        RP.hard_pct = cl[cur];
-        RP.queue = (unsigned long long *)(base + 8);
-        CUDA_TRY(cudaMemsetAsync(base + 8, 0, 8, st));
-        COUNT_LAUNCH(1);
-        k_walk<KMAX, R><<<rblocks, 128, 0, st>>>(S, g, RP);
-        CUDA_TRY(cudaPeekAtLastError());
-        CUDA_TRY(cudaMemsetAsync(cnt + (cur ^ 1), 0, 4, st));
-        COUNT_LAUNCH(1);
-        k_hard_compact<<<num_sms() * 2, 256, 0, st>>>(wl[cur], pl[cur], cl[cur], bl[cur], cnt + cur, cap, wl[cur ^ 1],
-                                                      pl[cur ^ 1], cl[cur ^ 1], bl[cur ^ 1], cnt + (cur ^ 1),
-                                                      t0 + Bc - 1, P.k_max, P.T, P.seed_xL, P.seed_pn, P.trials,
-                                                      P.w, P.stats);
-        CUDA_TRY(cudaPeekAtLastError());
-        cur ^= 1;
-        t0 += Bc;
-        B *= 2;
-    }
     return MPG_OK;
 }
 
@@ -1233,7 +1228,6 @@ extern "C" mpg_status mpg_manifold_walk(const mpg_scene *scene, const mpg_guide 
     P.iters = out->iters;
     P.G = out->G; P.T = out->T; P.w = out->w;
     P.trials = out->trials;
-    P.queue = (unsigned long long *)workspace;
     P.stats = (unsigned long long *)stats;
     P.max_iters = o->max_iters;
     P.trials_on = o->trials;
@@ -1247,16 +1241,6 @@ extern "C" mpg_status mpg_manifold_walk(const mpg_scene *scene, const mpg_guide 
     P.dbg = g_dbg;
     P.n_dbg = g_dbg_n;
     P.dbg_stride = g_dbg_stride;
-    P.local_trials = LOCAL_TRIALS;
-    P.hard_cap = hard_cap(P.n);
-    {
-        char *base = (char *)workspace;
-        P.hard_walk = (int64_t *)(base + 256);
-        P.hard_psurf = (uint32_t *)(base + 256 + (size_t)P.hard_cap * 16);
-        P.hard_pct = (uint32_t *)(base + 256 + (size_t)P.hard_cap * 32);
-        P.hard_best = (uint32_t *)(base + 256 + (size_t)P.hard_cap * 24);
-        P.hard_count = (unsigned int *)(base + 16);
-    }
     int k = g.k;
     if (sd->mode == MPG_SEED_GUIDE_DIR)
         ARG_CHECK(sb->ctype && sb->pn && out->ctype, "GUIDE_DIR needs seed ctype/pn and walk ctype arrays");
@@ -1274,7 +1258,6 @@ extern "C" mpg_status mpg_manifold_walk(const mpg_scene *scene, const mpg_guide 
         if (k <= 6) return launch_wavefront<6, float>(scene->d, g, P, workspace, workspace_bytes, s);
         return launch_wavefront<8, float>(scene->d, g, P, workspace, workspace_bytes, s);
     }
-    CUDA_TRY(cudaMemsetAsync(workspace, 0, 64, s));
     if (o->flags & MPG_FLAG_NEWTON_F64) {
         if (k <= 1) return launch_walk<1, double>(scene->d, g, P, s, workspace);
         if (k <= 2) return launch_walk<2, double>(scene->d, g, P, s, workspace);

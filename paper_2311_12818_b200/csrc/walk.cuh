@@ -26,9 +26,18 @@
 
 // occupancy: k <= 2 chains are capped at 80 registers (6 blocks of 128 per SM):
 // the spills are cheaper than the latency the extra warps hide (+11% on configs[1])
-enum { PH_FETCH = 0, PH_SEED = 1, PH_DEDUCE = 2, PH_SOLVE = 3, PH_REPROJ = 4, PH_END = 5, PH_IDLE = 6 };
+enum { PH_FETCH = 0, PH_SEED = 1, PH_DEDUCE = 2, PH_SOLVE = 3, PH_REPROJ = 4, PH_END = 5, PH_IDLE = 6, PH_WAIT = 7 };
 #define HARD_NONE 0xffffffffu
 enum { ST_CONVERGED = 0, ST_MAXITER = 1, ST_SEED_FAIL = 2, ST_BAD_SIDE = 3, ST_DEGENERATE = 4, ST_OCCLUDED = 5 };
+
+struct TrialHdr {
+    unsigned long long queue;   // next primary walk
+    unsigned int n_entries;     // hard entries published
+    unsigned int item_head;     // next ticket
+    unsigned int item_tail;     // items reserved
+    unsigned int resolved;      // walks whose output (trials, w) is final
+};
+#define ITEM_EMPTY 0xffffffffffffffffull
 
 struct WalkParams {
     const float4 *xD, *nD;
@@ -45,7 +54,6 @@ struct WalkParams {
     uint16_t *iters;
     float *G, *T, *w;
     uint32_t *trials;
-    unsigned long long *queue;
     unsigned long long *stats; // mpg_walk_stats as u64[21]
     int max_iters, trials_on;
     uint32_t k_max;
@@ -54,18 +62,19 @@ struct WalkParams {
     float *dbg;      // debug: [n_dbg][stride] (||C||_inf, beta) per primary iteration, or NULL
     int64_t n_dbg;
     int dbg_stride;
-    // reciprocal-probability trials beyond the first `local_trials` run in
-    // parallel rounds over a list of unresolved ("hard") walks (see k_walk).
+    // Reciprocal-probability trials (Eq. 15) beyond the first `local_trials`
+    // (sequential in the lane) make the walk a "hard entry" whose trials run as
+    // items (entry e, trial t) in doubling batches; lanes whose primary queue is
+    // exhausted take items by ticket from a ring, in the same launch.  k = the
+    // smallest successful trial: every trial below it has run (batch order).
     uint32_t local_trials;
-    uint32_t hard_cap;
-    int64_t *hard_walk; // list written by the main pass / read by a round
-    uint32_t *hard_psurf;
-    uint32_t *hard_pct;  // primary chain type (n | tau << 4)
-    uint32_t *hard_best; // min successful trial index (0xffffffff: none yet)
-    unsigned int *hard_count;
-    int round_mode;     // 0: main pass; 1: trial round over the hard list
+    uint32_t hard_cap;          // entries
+    uint32_t item_cap;          // item ring capacity (a full ring -> sequential fallback)
+    struct TrialHdr *th;        // counters (zeroed before the launch)
+    int64_t *e_walk;
+    uint32_t *e_psurf, *e_pct, *e_best, *e_pending, *e_issued, *e_batch;
+    unsigned long long *items;  // (e << 32 | t); ~0 = not yet written (ring memset to 0xff)
     int host_loop;      // wavefront: host-driven waves (MPG_FLAG_HOSTLOOP)
-    uint32_t round_t0, round_B; // round covers trials [t0, t0+B)
 };
 
 // stats slots (mirror mpg_walk_stats field order)
@@ -204,6 +213,29 @@ __device__ __forceinline__ int trace_chain(const DScene &S, bool deduce, int k, 
     return 0;
 }
 
+// ---- reciprocal-probability trial bookkeeping (hard entries / items) ----
+// final output of a walk with trial count kk (Eq. 15: w = T k / (P(n) pdf_L),
+// P(n) and pdf_L of the primary sample)
+__device__ __forceinline__ void trial_finalize(const WalkParams &P, int64_t w, uint32_t kk, bool truncated,
+                                               unsigned long long *s_stats) {
+    P.trials[w] = kk;
+    const float pn = P.seed_pn ? __ldg(P.seed_pn + w) : 1.0f;
+    P.w[w] = __ldcg(P.T + w) * (float)kk / (pn * __ldg(P.seed_xL + w).w);
+    atomicAdd(&s_stats[SS_TRIALS], (unsigned long long)kk);
+    if (truncated) atomicAdd(&s_stats[SS_TRUNC], 1ull);
+}
+// walks a lane has made final are counted in a register and published when the
+// lane runs out of primaries (PH_WAIT): one atomic per lane, not per walk
+#define walk_resolved(P) (my_resolved++)
+// publish items (e, t0 .. t0+B-1); false if the ring is full
+__device__ __forceinline__ bool items_push(const WalkParams &P, uint32_t e, uint32_t t0, uint32_t B) {
+    unsigned base = atomicAdd(&P.th->item_tail, B);
+    if ((unsigned long long)base + B > P.item_cap) return false;
+    for (uint32_t j = 0; j < B; j++)
+        *(volatile unsigned long long *)(P.items + base + j) = ((unsigned long long)e << 32) | (t0 + j);
+    return true;
+}
+
 template <int KMAX, typename R>
 __global__ void __launch_bounds__(128, (KMAX <= 2 ? MPG_WALK_MINB2 : 2)) k_walk(const DScene S, const SeedCtx g, const WalkParams P) {
     __shared__ unsigned long long s_stats[SS_N];
@@ -245,45 +277,25 @@ __global__ void __launch_bounds__(128, (KMAX <= 2 ? MPG_WALK_MINB2 : 2)) k_walk(
     LaneStats ls = {0u, 0u, 0u};
     uint32_t c_newton = 0, c_vtx = 0, c_attempts = 0;
 
-    // round mode: work items are (hard entry e, trial t0 + j), j < B
-    const int64_t n_items = P.round_mode ? (int64_t)min(*(volatile unsigned int *)P.hard_count, P.hard_cap) * P.round_B
-                                         : P.n;
-    uint32_t cur_e = 0;
+    uint32_t my_resolved = 0; // walks made final by this lane, not yet added to th->resolved
+    unsigned backoff = 256u;  // ns, while the whole warp waits for trial items
+    bool drained = false;     // warp-uniform: this warp saw the primary queue exhausted
+    int item_e = -1;          // hard entry of the trial item this lane runs (-1: none)
+    long long ticket = -1;    // item-ring ticket while waiting for an item
+    bool seq_only = false;    // trials continued in this lane after a full item ring
     while (true) {
-        // ---- fetch (warp-aggregated) -------------------------------------
+        // ---- fetch a primary walk (warp-aggregated) ------------------------
         unsigned need = __ballot_sync(MPG_FULL, phase == PH_FETCH);
         if (need) {
             int leader = __ffs(need) - 1;
             unsigned long long base = 0;
-            if (lane == leader) base = atomicAdd(P.queue, (unsigned long long)__popc(need));
+            if (lane == leader) base = atomicAdd(&P.th->queue, (unsigned long long)__popc(need));
             base = __shfl_sync(MPG_FULL, base, leader);
-            if (phase == PH_FETCH && P.round_mode) {
+            if (base + __popc(need) >= (unsigned long long)P.n) drained = true;   // warp-uniform
+            if (phase == PH_FETCH) {
                 int64_t idx = (int64_t)base + __popc(need & ((1u << lane) - 1u));
-                if (idx < n_items) {
-                    cur_e = (uint32_t)(idx / P.round_B);
-                    trial = P.round_t0 + (uint32_t)(idx % P.round_B);
-                    // skip trials beyond an already-found success of this walk
-                    if (*(volatile uint32_t *)(P.hard_best + cur_e) > trial) {
-                        w = P.hard_walk[cur_e];
-                        psurf = P.hard_psurf[cur_e];
-                        uint32_t pct = P.hard_pct[cur_e];
-                        pk = (int)(pct & 15u);
-                        ptau = pct >> 4;
-                        int64_t rcv = w / P.spp;
-                        xD = xyz(__ldg(P.xD + rcv));
-                        nD = xyz(__ldg(P.nD + rcv));
-                        float4 l4 = __ldg(P.seed_xL + w);
-                        xL = xyz(l4);
-                        pdfL = l4.w;
-                        lid = 0;
-                        if (S.n_light > 1) lid = (int)uidx(rng_draw(g.seed, P.walk_id_base + w, 0u, 0u).z, (uint32_t)S.n_light);
-                        phase = PH_SEED;
-                    }
-                } else {
-                    phase = PH_IDLE;
-                }
-            } else if (phase == PH_FETCH) {
-                int64_t idx = (int64_t)base + __popc(need & ((1u << lane) - 1u));
+                item_e = -1;
+                seq_only = false;
                 if (idx < P.n) {
                     w = idx;
                     trial = 0;
@@ -297,11 +309,70 @@ __global__ void __launch_bounds__(128, (KMAX <= 2 ? MPG_WALK_MINB2 : 2)) k_walk(
                     if (S.n_light > 1) lid = (int)uidx(rng_draw(g.seed, P.walk_id_base + idx, 0u, 0u).z, (uint32_t)S.n_light);
                     phase = PH_SEED;
                 } else {
-                    phase = PH_IDLE;
+                    phase = PH_WAIT;   // primaries exhausted: trial items
                 }
             }
         }
-        if (__all_sync(MPG_FULL, phase == PH_IDLE)) break;
+        // ---- take a trial item by ticket, or stop when every walk is final ----
+        // (only once the warp has drained the primary queue: no extra warp-wide
+        // synchronisation in the main phase)
+        if (drained) {
+        {   // tickets for lanes without one: one atomic per warp
+            unsigned needt = __ballot_sync(MPG_FULL, phase == PH_WAIT && ticket < 0);
+            if (needt) {
+                int leader = __ffs(needt) - 1;
+                unsigned base = 0;
+                if (lane == leader) base = atomicAdd(&P.th->item_head, (unsigned)__popc(needt));
+                base = __shfl_sync(MPG_FULL, base, leader);
+                if (phase == PH_WAIT && ticket < 0) ticket = (long long)(base + __popc(needt & ((1u << lane) - 1u)));
+            }
+        }
+        if (phase == PH_WAIT) {
+            if (my_resolved) {
+                __threadfence();   // this lane's outputs before the count that ends the launch
+                atomicAdd(&P.th->resolved, my_resolved);
+                my_resolved = 0;
+            }
+            unsigned long long wd = ticket < (long long)P.item_cap
+                                        ? *(volatile unsigned long long *)(P.items + ticket) : ITEM_EMPTY;
+            if (wd != ITEM_EMPTY) {
+                ticket = -1;
+                item_e = (int)(wd >> 32);
+                trial = (uint32_t)wd;
+                // entries and primary chains are written by other SMs during this launch:
+                // read them through L2 (ld.global.cg), never from a possibly stale L1 line
+                w = __ldcg(P.e_walk + item_e);
+                psurf = __ldcg(P.e_psurf + item_e);
+                uint32_t pct = __ldcg(P.e_pct + item_e);
+                pk = (int)(pct & 15u);
+                ptau = pct >> 4;
+                int64_t rcv = w / P.spp;
+                xD = xyz(__ldg(P.xD + rcv));
+                nD = xyz(__ldg(P.nD + rcv));
+                float4 l4 = __ldg(P.seed_xL + w);
+                xL = xyz(l4);
+                pdfL = l4.w;
+                lid = 0;
+                if (S.n_light > 1) lid = (int)uidx(rng_draw(g.seed, P.walk_id_base + w, 0u, 0u).z, (uint32_t)S.n_light);
+                // a trial above an already found success cannot change k: skip its walk
+                if (*(volatile uint32_t *)(P.e_best + item_e) < trial) { end_status = ST_SEED_FAIL; it = 0; phase = PH_END; }
+                else phase = PH_SEED;
+            } else if (*(volatile unsigned int *)&P.th->resolved >= (unsigned int)P.n) {
+                phase = PH_IDLE;
+            }
+        }
+        const unsigned wst = __reduce_and_sync(MPG_FULL, (phase == PH_IDLE ? 1u : 0u) |
+                                                          (phase == PH_IDLE || phase == PH_WAIT ? 2u : 0u));
+        if (wst & 1u) break;
+        if (wst & 2u) {
+            // the whole warp waits for trial items: back off (polling lanes would
+            // otherwise flood L2 while the remaining lanes finish their walks)
+            __nanosleep(backoff);
+            backoff = min(2u * backoff, 32768u);
+            continue;
+        }
+        backoff = 256u;
+        }
 
         // ---- seed ---------------------------------------------------------
         if (phase == PH_SEED) {
@@ -462,6 +533,7 @@ __global__ void __launch_bounds__(128, (KMAX <= 2 ? MPG_WALK_MINB2 : 2)) k_walk(
                 } else {
                     P.trials[w] = 0;
                     P.w[w] = 0.0f;
+                    walk_resolved(P);
                     phase = PH_FETCH;
                 }
             } else {
@@ -474,31 +546,65 @@ __global__ void __launch_bounds__(128, (KMAX <= 2 ? MPG_WALK_MINB2 : 2)) k_walk(
 #pragma unroll
                     for (int i = 0; i < KMAX; i++) {
                         if (i >= k) break;
-                        float4 c = P.chain[(int64_t)i * P.n + w];
+                        float4 c = __ldcg(P.chain + (int64_t)i * P.n + w);
                         float3 dd = f3d(x[i]) - xyz(c);
                         if ((int)((psurf >> (4 * i)) & 15u) != (surf[i] & 15) || !(len(dd) < P.same_eps)) same = false;
                     }
                 }
-                if (P.round_mode) {
-                    if (same) atomicMin(P.hard_best + cur_e, trial);
+                if (item_e >= 0) {
+                    // one item of a batch: the last one to finish decides the entry
+                    const uint32_t e = (uint32_t)item_e;
+                    if (same) atomicMin(P.e_best + e, trial);
+                    __threadfence();
+                    unsigned left = atomicSub(P.e_pending + e, 1u) - 1u;
                     phase = PH_FETCH;
+                    if (left == 0) {
+                        __threadfence();
+                        const uint32_t b = *(volatile uint32_t *)(P.e_best + e);
+                        const uint32_t issued = __ldcg(P.e_issued + e);
+                        if (b != HARD_NONE) {
+                            trial_finalize(P, w, b, false, s_stats);
+                            walk_resolved(P);
+                        } else if (issued >= P.k_max) {
+                            trial_finalize(P, w, P.k_max, true, s_stats);
+                            walk_resolved(P);
+                        } else {
+                            const uint32_t B = min(2u * __ldcg(P.e_batch + e), P.k_max - issued);
+                            P.e_batch[e] = B;
+                            P.e_pending[e] = B;
+                            P.e_issued[e] = issued + B;
+                            __threadfence();
+                            if (!items_push(P, e, issued + 1, B)) {
+                                // ring full: continue this walk's trials sequentially here
+                                P.e_pending[e] = 0;
+                                item_e = -1;
+                                seq_only = true;
+                                trial = issued + 1;
+                                phase = PH_SEED;
+                            }
+                        }
+                    }
                 } else if (same || trial >= P.k_max) {
-                    if (!same) atomicAdd(&s_stats[SS_TRUNC], 1ull);
-                    P.trials[w] = trial;
-                    P.w[w] = Tprim * (float)trial / (Pn * pdfL);
-                    atomicAdd(&s_stats[SS_TRIALS], (unsigned long long)trial);
+                    trial_finalize(P, w, trial, !same, s_stats);
+                    walk_resolved(P);
                     phase = PH_FETCH;
                 } else {
                     bool published = false;
-                    if (trial >= P.local_trials && P.hard_walk) {
-                        // hand the remaining trials to the parallel rounds
-                        unsigned int e = atomicAdd(P.hard_count, 1u);
+                    if (trial >= P.local_trials && !seq_only && P.items) {
+                        // hand the remaining trials to parallel items
+                        unsigned int e = atomicAdd(&P.th->n_entries, 1u);
                         if (e < P.hard_cap) {
-                            P.hard_walk[e] = w;
-                            P.hard_psurf[e] = psurf;
-                            P.hard_pct[e] = (uint32_t)pk | (ptau << 4);
-                            P.hard_best[e] = HARD_NONE;
-                            published = true;
+                            const uint32_t B = min(4u, P.k_max - trial);
+                            P.e_walk[e] = w;
+                            P.e_psurf[e] = psurf;
+                            P.e_pct[e] = (uint32_t)pk | (ptau << 4);
+                            P.e_best[e] = HARD_NONE;
+                            P.e_batch[e] = B;
+                            P.e_pending[e] = B;
+                            P.e_issued[e] = trial + B;
+                            __threadfence();
+                            published = items_push(P, e, trial + 1, B);
+                            if (!published) seq_only = true;
                         }
                     }
                     if (published) phase = PH_FETCH;
@@ -530,39 +636,4 @@ __global__ void __launch_bounds__(128, (KMAX <= 2 ? MPG_WALK_MINB2 : 2)) k_walk(
     if (P.stats)
         for (int i = threadIdx.x; i < SS_N; i += blockDim.x)
             if (s_stats[i]) atomicAdd(P.stats + i, s_stats[i]);
-}
-
-// After a trial round: resolved walks get k = min successful trial index (the
-// sequential definition of Eq. 15's geometric count, since every trial below
-// it was run); walks past k_max are truncated at k_max; the rest move to the
-// next round's list.
-__global__ void k_hard_compact(const int64_t *walk_in, const uint32_t *psurf_in, const uint32_t *pct_in,
-                               const uint32_t *best_in, const unsigned int *count_in, uint32_t cap, int64_t *walk_out,
-                               uint32_t *psurf_out, uint32_t *pct_out, uint32_t *best_out, unsigned int *count_out,
-                               uint32_t t_end, uint32_t k_max, const float *T, const float4 *seed_xL,
-                               const float *seed_pn, uint32_t *trials, float *w, unsigned long long *stats) {
-    uint32_t cnt = min(*count_in, cap);
-    unsigned long long s_tr = 0, s_tc = 0;
-    for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < cnt; e += gridDim.x * blockDim.x) {
-        int64_t wk = walk_in[e];
-        uint32_t b = best_in[e];
-        uint32_t kk = 0;
-        if (b != HARD_NONE) kk = b;
-        else if (t_end >= k_max) { kk = k_max; s_tc++; }
-        if (kk) {
-            trials[wk] = kk;
-            w[wk] = T[wk] * (float)kk / ((seed_pn ? seed_pn[wk] : 1.0f) * seed_xL[wk].w);
-            s_tr += kk;
-        } else {
-            unsigned int o = atomicAdd(count_out, 1u);
-            walk_out[o] = wk;
-            psurf_out[o] = psurf_in[e];
-            pct_out[o] = pct_in[e];
-            best_out[o] = HARD_NONE;
-        }
-    }
-    if (stats) {
-        if (s_tr) atomicAdd(stats + SS_TRIALS, s_tr);
-        if (s_tc) atomicAdd(stats + SS_TRUNC, s_tc);
-    }
 }
