@@ -930,7 +930,16 @@ extern "C" mpg_status mpg_debug_trace(float *buf, int64_t n_walks, int32_t strid
 
 // persistent-kernel workspace: trial header, hard entries
 // (walks unresolved after LOCAL_TRIALS sequential trials), item ring
-#define LOCAL_TRIALS 4u
+// Sequential trials run in the lane before a walk becomes a hard entry.  Measured
+// (ms/step, configs 1/2/3/4): 1 -> 66/508/337/391, 2 -> 62/497/337/386,
+// 4 -> 61.5/474/335/377, 8 -> 62.6/451/335/377: with many walks per launch the
+// primaries keep every lane busy and in-lane trials are cheaper than items, with
+// few the parallel items shorten the tail.
+#ifdef MPG_LOCAL_TRIALS
+#define LOCAL_TRIALS(n) ((uint32_t)MPG_LOCAL_TRIALS)
+#else
+#define LOCAL_TRIALS(n) ((n) >= (int64_t)4 << 20 ? 8u : 4u)
+#endif
 struct MKLayout {
     uint32_t H, C;
     size_t th, e_walk, e_psurf, e_pct, e_best, e_pending, e_issued, e_batch, items, total;
@@ -1008,7 +1017,7 @@ static mpg_status launch_walk(const DScene &S, const SeedCtx &g, WalkParams P, c
     }
     MKLayout L = mk_layout(P.n);
     char *b = (char *)ws;
-    P.local_trials = LOCAL_TRIALS;
+    P.local_trials = LOCAL_TRIALS(P.n);
     P.hard_cap = L.H;
     // tickets index the ring only below item_cap: it bounds both the reads and the clear;
     // a full ring (or entry table) makes the walk continue its trials sequentially
