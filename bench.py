@@ -212,7 +212,7 @@ def run_ours(args):
     ds = mpg.DeviceScene(w)
     b = mpg.Batch(w.xD, w.nD, w.spp, w.seed.k)
     opts = ds.opts(flags=w.opts.flags | (1 if args.wavefront else 0) | (2 if args.hostloop else 0) |
-                   (4 if args.f64 else 0))
+                   (4 if args.f64 else 0) | (0 if args.no_sort else 8))
     stream = torch.cuda.current_stream()
     guided = ds.guide is not None
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)   # > 126 MB L2
@@ -359,6 +359,9 @@ def run_ours(args):
                 "config": {"workload": CONFIG_NAMES[args.config], "n_walks_per_gpu": b.n, "k": w.seed.k,
                            "max_iters": w.opts.max_iters, "trials": "on (k_max 1024)",
                            "l2": "256 MB buffer written before every timed step (inputs < 126 MB L2)",
+                           "order": ("primaries in walk order" if not opts.flags & 8 else
+                                     "primaries in (receiver cell, seed direction) order, MPG_FLAG_SORT"),
+                           "path": "wavefront" if opts.flags & 1 else "persistent kernel",
                            "precision": ("fp32 scene/traversal; fp64 positions, residual, hit refinement" +
                                          ("; fp64 Jacobian/step (MPG_FLAG_NEWTON_F64)" if opts.flags & 4
                                           else "; fp32 Jacobian/step"))},
@@ -394,6 +397,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--wavefront", action="store_true", help="wavefront path (MPG_FLAG_WAVEFRONT)")
     ap.add_argument("--hostloop", action="store_true", help="wavefront with host-driven waves (profiling)")
+    ap.add_argument("--no-sort", action="store_true",
+                    help="walk-order primaries (default: coherence-sorted order, MPG_FLAG_SORT; same results)")
     ap.add_argument("--f64", action="store_true", help="MPG_FLAG_NEWTON_F64")
     args = ap.parse_args()
     if args.impl == "reference":

@@ -118,6 +118,9 @@ typedef struct {
 #define MPG_FLAG_HOSTLOOP 2u  /* wavefront waves launched from the host (blocking; for profilers) */
 #define MPG_FLAG_NEWTON_F64 4u /* Jacobian blocks, frames and steps in fp64 (default fp32; positions and
                                   the residual are always fp64, R24) */
+#define MPG_FLAG_SORT 8u      /* persistent kernel: process the primaries in the order of a key built from
+                                  (receiver cell, seed direction) for ray coherence; every walk's result is
+                                  unchanged (it depends only on its own walk id) */
 
 typedef struct {
     int32_t max_iters;     /* Newton cap (BASELINE configs: 20, or 40 for k=6)       */

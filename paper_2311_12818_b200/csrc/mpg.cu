@@ -7,11 +7,14 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <atomic>
 #include <functional>
 #include <vector>
+
+#include <cub/device/device_radix_sort.cuh>
 
 #include "mpg.h"
 #include "device_common.cuh"
@@ -99,7 +102,15 @@ struct Builder {
     std::vector<int> idx;
     std::vector<BNode> nodes;
     int max_depth = 0;
+    // SAH: traversal cost relative to one triangle test; leaves of leaf_min..leaf_max
+    // triangles (<= 8: the leaf ref holds count-1 in 3 bits).  MPG_SAH_CT /
+    // MPG_LEAF_MIN / MPG_LEAF_MAX override for experiments.
+    float sah_ct = 0.5f;
+    int leaf_min = 2, leaf_max = 4;
     explicit Builder(const std::vector<BTri> &t) : T(t), idx(t.size()) {
+        if (const char *v = getenv("MPG_SAH_CT")) sah_ct = (float)atof(v);
+        if (const char *v = getenv("MPG_LEAF_MIN")) leaf_min = std::max(1, std::min(8, atoi(v)));
+        if (const char *v = getenv("MPG_LEAF_MAX")) leaf_max = std::max(leaf_min, std::min(8, atoi(v)));
         for (size_t i = 0; i < t.size(); i++) idx[i] = (int)i;
     }
     static float area(const float lo[3], const float hi[3]) {
@@ -124,8 +135,8 @@ struct Builder {
         float clo[3], chi[3];
         bounds(b, e, lo, hi, clo, chi);
         int n = e - b;
-        if (n <= 2) return leaf(b, e);
-        const int NB = 16;
+        if (n <= leaf_min) return leaf(b, e);
+        const int NB = 32;
         int best_axis = -1, best_split = -1;
         float best_cost = 3e38f;
         if (depth < 56) {
@@ -166,8 +177,8 @@ struct Builder {
         }
         float pa = area(lo, hi);
         float leaf_cost = (float)n;
-        float split_cost = 0.5f + (pa > 0.f ? best_cost / pa : 3e38f);
-        if (n <= 4 && (best_axis < 0 || split_cost >= leaf_cost)) return leaf(b, e);
+        float split_cost = sah_ct + (pa > 0.f ? best_cost / pa : 3e38f);
+        if (n <= leaf_max && (best_axis < 0 || split_cost >= leaf_cost)) return leaf(b, e);
         int mid;
         if (best_axis >= 0) {
             float ext = chi[best_axis] - clo[best_axis], sc = NB / ext, c0 = clo[best_axis];
@@ -942,7 +953,8 @@ extern "C" mpg_status mpg_debug_trace(float *buf, int64_t n_walks, int32_t strid
 #endif
 struct MKLayout {
     uint32_t H, C;
-    size_t th, e_walk, e_psurf, e_pct, e_best, e_pending, e_issued, e_batch, items, total;
+    size_t th, e_walk, e_psurf, e_pct, e_best, e_pending, e_issued, e_batch, items, skey, skey2, sval, sval2, stemp,
+        stemp_bytes, total;
 };
 static MKLayout mk_layout(int64_t n) {
     MKLayout L;
@@ -956,8 +968,48 @@ static MKLayout mk_layout(int64_t n) {
     L.e_psurf = take(4ull * L.H); L.e_pct = take(4ull * L.H); L.e_best = take(4ull * L.H);
     L.e_pending = take(4ull * L.H); L.e_issued = take(4ull * L.H); L.e_batch = take(4ull * L.H);
     L.items = take(8ull * L.C);
+    // MPG_FLAG_SORT: keys / permutation (double-buffered) and radix-sort scratch
+    L.skey = take(4ull * nn); L.skey2 = take(4ull * nn); L.sval = take(4ull * nn); L.sval2 = take(4ull * nn);
+    L.stemp_bytes = 16ull * nn + (8u << 20);
+    L.stemp = take(L.stemp_bytes);
     L.total = o;
     return L;
+}
+
+// MPG_FLAG_SORT keys: receiver cell (4 bits per axis, cells of extent/16, Morton)
+// above the seed direction (octahedral map, 9 bits per axis, Morton); walks
+// without a seed last.  Values: walk indices.
+__device__ __forceinline__ uint32_t mpg_spread2(uint32_t v) { // 9 bits -> every 2nd bit
+    v &= 0x1ffu;
+    v = (v | (v << 8)) & 0x00ff00ffu;
+    v = (v | (v << 4)) & 0x0f0f0f0fu;
+    v = (v | (v << 2)) & 0x33333333u;
+    v = (v | (v << 1)) & 0x55555555u;
+    return v;
+}
+__global__ void k_sort_keys(const float4 *xD, const float4 *tgt, const int *bin, int64_t n, int spp, float cell,
+                            uint32_t *key, uint32_t *val) {
+    for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < n; w += (int64_t)gridDim.x * blockDim.x) {
+        val[w] = (uint32_t)w;
+        if (bin[w] == -2) { key[w] = 0xffffffffu; continue; }
+        float3 p = xyz(xD[w / spp]);
+        float3 d = xyz(tgt[w]) - p;
+        float l1 = fabsf(d.x) + fabsf(d.y) + fabsf(d.z);
+        float u = l1 > 0.f ? d.x / l1 : 0.f, v = l1 > 0.f ? d.z / l1 : 0.f;
+        if (d.y < 0.f) { // fold the lower hemisphere
+            float uu = (1.f - fabsf(v)) * copysignf(1.f, u), vv = (1.f - fabsf(u)) * copysignf(1.f, v);
+            u = uu; v = vv;
+        }
+        uint32_t qu = (uint32_t)min(511.f, fmaxf(0.f, (u * 0.5f + 0.5f) * 512.f));
+        uint32_t qv = (uint32_t)min(511.f, fmaxf(0.f, (v * 0.5f + 0.5f) * 512.f));
+        uint32_t dir = mpg_spread2(qu) | (mpg_spread2(qv) << 1);             // 18 bits
+        uint32_t cx = (uint32_t)floorf(p.x / cell) & 15u, cy = (uint32_t)floorf(p.y / cell) & 15u,
+                 cz = (uint32_t)floorf(p.z / cell) & 15u;
+        uint32_t pos = 0;
+        for (int b = 0; b < 4; b++)
+            pos |= (((cx >> b) & 1u) << (3 * b)) | (((cy >> b) & 1u) << (3 * b + 1)) | (((cz >> b) & 1u) << (3 * b + 2));
+        key[w] = (pos << 18) | dir;                                            // 30 bits
+    }
 }
 static size_t mk_ws_bytes(int64_t n) { return mk_layout(n).total; }
 
@@ -1005,7 +1057,8 @@ extern "C" size_t mpg_walk_workspace_size(int64_t n, const mpg_sampler_desc *sam
 }
 
 template <int KMAX, typename R>
-static mpg_status launch_walk(const DScene &S, const SeedCtx &g, WalkParams P, cudaStream_t st, void *ws) {
+static mpg_status launch_walk(const DScene &S, const SeedCtx &g, WalkParams P, cudaStream_t st, void *ws,
+                              bool sort) {
     static int occ = 0;
     if (!occ) {
 #ifdef MPG_CARVEOUT
@@ -1030,6 +1083,21 @@ static mpg_status launch_walk(const DScene &S, const SeedCtx &g, WalkParams P, c
     P.items = (unsigned long long *)(b + L.items);
     CUDA_TRY(cudaMemsetAsync(P.th, 0, sizeof(TrialHdr), st));
     if (P.trials_on) CUDA_TRY(cudaMemsetAsync(P.items, 0xff, 8ull * P.item_cap, st));
+    P.perm = nullptr;
+    if (sort && P.n > 1) {
+        uint32_t *k0 = (uint32_t *)(b + L.skey), *k1 = (uint32_t *)(b + L.skey2);
+        uint32_t *v0 = (uint32_t *)(b + L.sval), *v1 = (uint32_t *)(b + L.sval2);
+        int gk = (int)std::min<int64_t>((P.n + 255) / 256, (int64_t)num_sms() * 8);
+        COUNT_LAUNCH(1);
+        k_sort_keys<<<gk, 256, 0, st>>>(P.xD, P.seed_tgt, P.seed_bin, P.n, P.spp, S.extent / 16.0f, k0, v0);
+        CUDA_TRY(cudaPeekAtLastError());
+        size_t tb = 0;
+        CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, tb, k0, k1, v0, v1, (int)P.n, 0, 30, st));
+        if (tb > L.stemp_bytes) return fail(MPG_ERR_INVALID_ARG, "sort scratch larger than reserved");
+        COUNT_LAUNCH(4);   // cub onesweep: histogram + 3 passes of 10 bits (library launches, counted)
+        CUDA_TRY(cub::DeviceRadixSort::SortPairs(b + L.stemp, tb, k0, k1, v0, v1, (int)P.n, 0, 30, st));
+        P.perm = v1;
+    }
     int64_t want = (P.n + 127) / 128;
     int blocks = (int)std::min<int64_t>(want, (int64_t)num_sms() * occ);
     COUNT_LAUNCH(1);
@@ -1268,17 +1336,17 @@ extern "C" mpg_status mpg_manifold_walk(const mpg_scene *scene, const mpg_guide 
         return launch_wavefront<8, float>(scene->d, g, P, workspace, workspace_bytes, s);
     }
     if (o->flags & MPG_FLAG_NEWTON_F64) {
-        if (k <= 1) return launch_walk<1, double>(scene->d, g, P, s, workspace);
-        if (k <= 2) return launch_walk<2, double>(scene->d, g, P, s, workspace);
-        if (k <= 4) return launch_walk<4, double>(scene->d, g, P, s, workspace);
-        if (k <= 6) return launch_walk<6, double>(scene->d, g, P, s, workspace);
-        return launch_walk<8, double>(scene->d, g, P, s, workspace);
+        if (k <= 1) return launch_walk<1, double>(scene->d, g, P, s, workspace, (o->flags & MPG_FLAG_SORT) != 0);
+        if (k <= 2) return launch_walk<2, double>(scene->d, g, P, s, workspace, (o->flags & MPG_FLAG_SORT) != 0);
+        if (k <= 4) return launch_walk<4, double>(scene->d, g, P, s, workspace, (o->flags & MPG_FLAG_SORT) != 0);
+        if (k <= 6) return launch_walk<6, double>(scene->d, g, P, s, workspace, (o->flags & MPG_FLAG_SORT) != 0);
+        return launch_walk<8, double>(scene->d, g, P, s, workspace, (o->flags & MPG_FLAG_SORT) != 0);
     }
-    if (k <= 1) return launch_walk<1, float>(scene->d, g, P, s, workspace);
-    if (k <= 2) return launch_walk<2, float>(scene->d, g, P, s, workspace);
-    if (k <= 4) return launch_walk<4, float>(scene->d, g, P, s, workspace);
-    if (k <= 6) return launch_walk<6, float>(scene->d, g, P, s, workspace);
-    return launch_walk<8, float>(scene->d, g, P, s, workspace);
+    if (k <= 1) return launch_walk<1, float>(scene->d, g, P, s, workspace, (o->flags & MPG_FLAG_SORT) != 0);
+    if (k <= 2) return launch_walk<2, float>(scene->d, g, P, s, workspace, (o->flags & MPG_FLAG_SORT) != 0);
+    if (k <= 4) return launch_walk<4, float>(scene->d, g, P, s, workspace, (o->flags & MPG_FLAG_SORT) != 0);
+    if (k <= 6) return launch_walk<6, float>(scene->d, g, P, s, workspace, (o->flags & MPG_FLAG_SORT) != 0);
+    return launch_walk<8, float>(scene->d, g, P, s, workspace, (o->flags & MPG_FLAG_SORT) != 0);
 }
 
 // ----------------------------------------------------------------------------

@@ -45,6 +45,7 @@ struct WalkParams {
     int spp;
     const float4 *seed_xL, *seed_tgt;
     const int *seed_bin;
+    const uint32_t *perm;       // processing order of the primaries (MPG_FLAG_SORT), NULL = walk order
     const uint32_t *seed_ctype; // n | bits << 4 | learned << 12 (may be NULL: fixed type)
     const float *seed_pn;       // P(n) (may be NULL: 1)
     uint16_t *out_ctype;        // primary chain type n | tau << 4 (may be NULL)
@@ -297,16 +298,16 @@ __global__ void __launch_bounds__(128, (KMAX <= 2 ? MPG_WALK_MINB2 : 2)) k_walk(
                 item_e = -1;
                 seq_only = false;
                 if (idx < P.n) {
-                    w = idx;
+                    w = P.perm ? (int64_t)__ldg(P.perm + idx) : idx;
                     trial = 0;
-                    int64_t rcv = idx / P.spp;
+                    int64_t rcv = w / P.spp;
                     xD = xyz(__ldg(P.xD + rcv));
                     nD = xyz(__ldg(P.nD + rcv));
-                    float4 l4 = __ldg(P.seed_xL + idx);
+                    float4 l4 = __ldg(P.seed_xL + w);
                     xL = xyz(l4);
                     pdfL = l4.w;
                     lid = 0;
-                    if (S.n_light > 1) lid = (int)uidx(rng_draw(g.seed, P.walk_id_base + idx, 0u, 0u).z, (uint32_t)S.n_light);
+                    if (S.n_light > 1) lid = (int)uidx(rng_draw(g.seed, P.walk_id_base + w, 0u, 0u).z, (uint32_t)S.n_light);
                     phase = PH_SEED;
                 } else {
                     phase = PH_WAIT;   // primaries exhausted: trial items

@@ -454,3 +454,25 @@ def test_cfg4_progressive_loop_per_iteration():
         assert hs == pytest.approx(ws, rel=1e-5)          # mass conservation
         assert rel < 1e-5                                 # same bins, fp32 atomic order
     assert log[-1][1] > log[0][1]                          # the guide learns
+
+
+@pytest.mark.parametrize("which", ["cfg1", "cfg3", "cfg4"])
+def test_sorted_order_gives_identical_walks(which):
+    """MPG_FLAG_SORT changes only the order the persistent kernel takes the
+    primaries in: every walk depends on its own walk id alone (R13), so all
+    outputs are bit-identical to walk order."""
+    w = {"cfg1": lambda: W.config1(n_side=256, spp=2),
+         "cfg3": lambda: W.config3(n_side=64, spp=1),
+         "cfg4": lambda: W.config4(n_side=64)}[which]()
+    a, sa, _ = PY.run_gpu(w)
+    b, sb, _ = PY.run_gpu(w, flags=w.opts.flags | 8)
+    for k in ("status", "iters", "trials", "G", "T", "w"):
+        assert np.array_equal(a[k], b[k]), k
+    conv = np.isin(a["status"], (0, 5))
+    n = a["ctype"][conv] & 15 if which == "cfg4" else np.full(int(conv.sum()), w.seed.k)
+    used = np.arange(a["pos"].shape[1])[None, :] < n[:, None]          # vertices each chain has
+    assert np.array_equal(a["pos"][conv][used], b["pos"][conv][used])
+    assert np.array_equal(a["prim"][conv][used], b["prim"][conv][used])
+    # traversal counters depend on warp composition (postponed leaves wait for warp-mates)
+    drop = ("node_visits", "tri_tests")
+    assert {k: v for k, v in sa.items() if k not in drop} == {k: v for k, v in sb.items() if k not in drop}
