@@ -16,6 +16,7 @@ from paper_2311_12818_b200 import workloads as W
 from tests import parity as PY
 
 pytestmark = pytest.mark.gpu
+BENCH_FLAGS = 8          # bench.py's launch configuration: MPG_FLAG_SORT
 
 
 @pytest.fixture(scope="module")
@@ -128,10 +129,10 @@ def test_cfg1_walk_parity(cfg1_small_run):
 
 
 def test_cfg1_full_size_sampled():
-    """configs[1] at its full size (1,048,576 walks, the bench launch) vs the
-    oracle on 3,000 sampled walks."""
+    """configs[1] at its full size (1,048,576 walks) in the bench launch
+    configuration (MPG_FLAG_SORT) vs the oracle on 3,000 sampled walks."""
     w = W.config1()
-    g, st, ext = PY.run_gpu(w)
+    g, st, ext = PY.run_gpu(w, flags=w.opts.flags | BENCH_FLAGS)
     rng = np.random.default_rng(1)
     ids = np.sort(rng.choice(w.n_walks, size=3000, replace=False))
     o, s = PY.run_oracle(w, ids)
@@ -242,9 +243,9 @@ def test_cfg3_walk_parity():
 
 
 def test_cfg2_full_size_sampled():
-    """configs[2] at full size (16,777,216 walks, the bench launch) vs 2,000 sampled oracle walks."""
+    """configs[2] at full size (16,777,216 walks, bench launch configuration) vs 2,000 sampled oracle walks."""
     w = W.config2()
-    g, st, ext = PY.run_gpu(w)
+    g, st, ext = PY.run_gpu(w, flags=w.opts.flags | BENCH_FLAGS)
     assert st["walks"] == w.n_walks
     rng = np.random.default_rng(2)
     ids = np.sort(rng.choice(w.n_walks, size=2000, replace=False))
@@ -476,3 +477,48 @@ def test_sorted_order_gives_identical_walks(which):
     # traversal counters depend on warp composition (postponed leaves wait for warp-mates)
     drop = ("node_visits", "tri_tests")
     assert {k: v for k, v in sa.items() if k not in drop} == {k: v for k, v in sb.items() if k not in drop}
+
+
+def test_cfg3_full_size_sampled():
+    """configs[3] at full size (1,048,576 k=6 walks, bench launch configuration) vs 600 sampled oracle walks."""
+    w = W.config3()
+    g, st, ext = PY.run_gpu(w, flags=w.opts.flags | BENCH_FLAGS)
+    assert st["walks"] == w.n_walks
+    rng = np.random.default_rng(3)
+    ids = np.sort(rng.choice(w.n_walks, size=600, replace=False))
+    o, s = PY.run_oracle(w, ids)
+    rep = PY.compare(g, o, ids, ext, w.seed.k)
+    _check_walk_parity(rep, min_agree=0.99, w=w, s=s, o=o, ext=ext, max_non_boundary=2)
+
+
+def test_cfg4_full_size_first_iterations():
+    """configs[4] at full size (1,048,576 walks per iteration, the bench's
+    progressive loop and flags): iterations 0 and 1 vs 800 sampled oracle walks
+    each, the oracle guided by the GPU's own accumulated histogram."""
+    import torch
+    from paper_2311_12818_b200 import mpg
+    from oracle import oracle as O
+    w = W.config4()
+    ds = mpg.DeviceScene(w)
+    b = mpg.Batch(w.xD, w.nD, w.spp, w.seed.k)
+    opts = ds.opts(flags=w.opts.flags | BENCH_FLAGS)
+    s = O.OracleScene(w)
+    H = torch.empty(256, 126, 1024, dtype=torch.float32, device="cuda")
+    rng = np.random.default_rng(4)
+    agree = []
+
+    def hook(it):
+        g = b.results()
+        ids = np.sort(rng.choice(w.n_walks, size=800, replace=False))
+        o = s.walks(ids, s.opts(walk_id_base=it * w.n_walks))
+        rep = PY.compare(g, o, ids, ds.extent, 6)
+        agree.append(rep["flag_agree"])
+        assert rep["n_other_chain"] <= 1
+        mpg.mpg_guide_download(ds.guide, H, None)
+        torch.cuda.synchronize()
+        s.set_dir_hist(H.cpu().numpy())
+
+    mpg.run_progressive(ds, b, opts, iterations=2, on_iteration=hook)
+    ds.close()
+    print(agree)
+    assert min(agree) >= 0.995
