@@ -241,6 +241,7 @@ def run_ours(args):
     wall0 = time.perf_counter()
     launches0 = mpg.mpg_kernel_launches()
     walk_ev = []
+    part_ev = []
     for i in range(args.steps):
         flush.fill_(float(i))
         e0, e1, e2, e3 = ev[i]
@@ -250,17 +251,21 @@ def run_ours(args):
         base = opts.walk_id_base
         for it in range(iters):
             opts.walk_id_base = base + it * b.n
+            ev5 = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+            ev5[0].record(stream)
             mpg.mpg_sample_seeds(ds.h, ds.guide, ds.sampler, b.query, opts, b.seeds)
-            wa, wb_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            wa.record(stream)
+            ev5[1].record(stream)
             mpg.mpg_manifold_walk(ds.h, ds.guide, ds.sampler, b.query, b.seeds, opts, b.out, b.stats, b.workspace)
-            wb_.record(stream)
-            walk_ev.append((wa, wb_))
+            ev5[2].record(stream)
+            walk_ev.append((ev5[1], ev5[2]))
             mpg.mpg_estimate(b.w, b.n_recv, b.spp, b.mean, b.var)
+            ev5[3].record(stream)
             if guided:
                 mpg.mpg_guide_accumulate(ds.guide, b.query, b.out, b.n)
             if progressive:
                 mpg.mpg_guide_rebuild(ds.guide)
+            ev5[4].record(stream)
+            part_ev.append(ev5)
             stats.append(b.stats.clone())
         opts.walk_id_base = base
         e1.record(stream)
@@ -272,6 +277,7 @@ def run_ours(args):
     clk = clocks.stop()
     step_ms = [ev[i][0].elapsed_time(ev[i][3]) for i in range(args.steps)]
     walk_ms_all = [a.elapsed_time(z) for a, z in walk_ev]
+    parts = np.array([[e[j].elapsed_time(e[j + 1]) for j in range(4)] for e in part_ev]).sum(0) / args.steps
     walk_ms = [sum(walk_ms_all[i * iters:(i + 1) * iters]) for i in range(args.steps)]
     seed_ms = [0.0] * args.steps
     tot_ms = sum(step_ms)
@@ -368,8 +374,12 @@ def run_ours(args):
                 "newton_iters_per_s": newton_all / (tot_ms / 1e3),
                 "walks_incl_trials_per_s": S["attempts"] * world / (tot_ms / 1e3),
                 "rays_per_s": S["rays"] * world / (tot_ms / 1e3),
-                "breakdown_ms": {"walk": sum(walk_ms) / args.steps,
-                                 "seeds+estimate+accumulate+tables": (tot_ms - sum(walk_ms)) / args.steps},
+                "breakdown_ms": {"seeds": float(parts[0]), "walk": float(parts[1]), "estimate": float(parts[2]),
+                                 "accumulate+tables": float(parts[3])},
+                "per_walk_time": {   # rates per second of mpg_manifold_walk time
+                    "primary_converged_walks_per_s": conv_all / (sum(walk_ms) / 1e3),
+                    "walks_incl_trials_per_s": S["attempts"] * world / (sum(walk_ms) / 1e3),
+                    "newton_iters_per_s": newton_all / (sum(walk_ms) / 1e3)},
                 "roofline": {"bound": "alu", "kernel": "k_walk", "achieved": achieved, "peak": peak,
                              "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
                              "peak_source": "148 SM x 128 FP32 lanes x 2 x 1965 MHz (B200_PROFILING.md unit counts)",
