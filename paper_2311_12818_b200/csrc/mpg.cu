@@ -1075,6 +1075,9 @@ static mpg_status launch_walk(const DScene &S, const SeedCtx &g, WalkParams P, c
     // tickets index the ring only below item_cap: it bounds both the reads and the clear;
     // a full ring (or entry table) makes the walk continue its trials sequentially
     P.item_cap = P.trials_on ? L.C : 0u;
+    // test knobs: shrink the entry table / item ring to exercise the sequential fallbacks
+    if (const char *v = getenv("MPG_TEST_HARD_CAP")) P.hard_cap = std::min<uint32_t>(P.hard_cap, (uint32_t)atoi(v));
+    if (const char *v = getenv("MPG_TEST_ITEM_CAP")) P.item_cap = std::min<uint32_t>(P.item_cap, (uint32_t)atoi(v));
     P.th = (TrialHdr *)(b + L.th);
     P.e_walk = (int64_t *)(b + L.e_walk);
     P.e_psurf = (uint32_t *)(b + L.e_psurf); P.e_pct = (uint32_t *)(b + L.e_pct); P.e_best = (uint32_t *)(b + L.e_best);

@@ -522,3 +522,24 @@ def test_cfg4_full_size_first_iterations():
     ds.close()
     print(agree)
     assert min(agree) >= 0.995
+
+
+@pytest.mark.parametrize("caps", [("16", None), (None, "40"), ("3", "7")])
+def test_trial_fallbacks_give_identical_walks(caps, monkeypatch):
+    """A full entry table or item ring makes a walk continue its trials
+    sequentially in its lane: k is still the smallest successful trial, so the
+    outputs equal those of an unconstrained run (configs[1] small, configs[0])."""
+    hard, item = caps
+    for mk in (lambda: W.config1(n_side=96, spp=2), lambda: W.config0(n_side=32, spp=8)):
+        w = mk()
+        a, sa, _ = PY.run_gpu(w)
+        if hard:
+            monkeypatch.setenv("MPG_TEST_HARD_CAP", hard)
+        if item:
+            monkeypatch.setenv("MPG_TEST_ITEM_CAP", item)
+        b, sb, _ = PY.run_gpu(w)
+        monkeypatch.delenv("MPG_TEST_HARD_CAP", raising=False)
+        monkeypatch.delenv("MPG_TEST_ITEM_CAP", raising=False)
+        for k in ("status", "trials", "w"):
+            assert np.array_equal(a[k], b[k]), (w.name, k)
+        assert sa["trials"] == sb["trials"] and sa["truncated"] == sb["truncated"]
