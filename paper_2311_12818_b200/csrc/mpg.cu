@@ -1017,8 +1017,7 @@ static size_t mk_ws_bytes(int64_t n) { return mk_layout(n).total; }
 // per-slot SoA state, ray lists, hits, hard entries, trial items
 struct WFLayout {
     uint32_t S, H, C;
-    size_t hdr, list0, list1, fstack, s_walk, s_trial, s_flags, s_surf, s_ysurf, s_psurf, s_entry, s_beta, s_tgt,
-        s_x, s_dq, s_y, s_ctype, s_tau, s_pct, s_pn, r0o0, r0d0, r0o1, r0d1, ro[WF_KMAX], rd[WF_KMAX], h_p, h_s,
+    size_t hdr, list0, list1, fstack, rec, s_psurf, s_entry, s_tgt, s_x, s_dq, s_y, s_pct, s_pn, r0o0, r0d0, r0o1, r0d1, ro[WF_KMAX], rd[WF_KMAX], h_p, h_s,
         e_walk, e_psurf, e_pct, e_best, e_issued, e_pending, e_batch, it_entry, it_trial, total;
 };
 static WFLayout wf_layout(int64_t n, int k) {
@@ -1031,11 +1030,10 @@ static WFLayout wf_layout(int64_t n, int k) {
     auto take = [&](size_t bytes) { size_t r = o; o += (bytes + 255) & ~(size_t)255; return r; };
     L.hdr = take(sizeof(WFHeader));
     L.list0 = take(4ull * L.S); L.list1 = take(4ull * L.S); L.fstack = take(4ull * L.S);
-    L.s_walk = take(4ull * L.S); L.s_trial = take(4ull * L.S); L.s_flags = take(4ull * L.S);
-    L.s_surf = take(4ull * L.S); L.s_ysurf = take(4ull * L.S); L.s_psurf = take(4ull * L.S);
-    L.s_entry = take(4ull * L.S); L.s_beta = take(4ull * L.S); L.s_tgt = take(16ull * L.S);
+    L.rec = take(32ull * L.S); L.s_psurf = take(4ull * L.S);
+    L.s_entry = take(4ull * L.S); L.s_tgt = take(16ull * L.S);
     L.s_x = take(32ull * L.S * k); L.s_dq = take(32ull * L.S * k); L.s_y = take(32ull * L.S * k);
-    L.s_ctype = take(4ull * L.S); L.s_tau = take(4ull * L.S); L.s_pct = take(4ull * L.S); L.s_pn = take(4ull * L.S);
+    L.s_pct = take(4ull * L.S); L.s_pn = take(4ull * L.S);
     const size_t r0 = 16ull * L.S * (k + 1);
     L.r0o0 = take(r0); L.r0d0 = take(r0); L.r0o1 = take(r0); L.r0d1 = take(r0);
     for (int i = 0; i < WF_KMAX; i++) {
@@ -1138,13 +1136,11 @@ static mpg_status launch_wavefront(const DScene &S, const SeedCtx &g, const Walk
     P.S = L.S; P.H = L.H; P.C = L.C;
     P.list[0] = (uint32_t *)(b + L.list0); P.list[1] = (uint32_t *)(b + L.list1);
     P.free_stack = (uint32_t *)(b + L.fstack);
-    P.s_walk = (int32_t *)(b + L.s_walk); P.s_trial = (uint32_t *)(b + L.s_trial);
-    P.s_flags = (uint32_t *)(b + L.s_flags); P.s_surf = (uint32_t *)(b + L.s_surf);
-    P.s_ysurf = (uint32_t *)(b + L.s_ysurf); P.s_psurf = (uint32_t *)(b + L.s_psurf);
-    P.s_entry = (int32_t *)(b + L.s_entry); P.s_beta = (float *)(b + L.s_beta);
+    P.rec = (uint32_t *)(b + L.rec); P.s_psurf = (uint32_t *)(b + L.s_psurf);
+    P.s_entry = (int32_t *)(b + L.s_entry);
     P.s_tgt = (float4 *)(b + L.s_tgt); P.s_x = (double4 *)(b + L.s_x); P.s_dq = (double4 *)(b + L.s_dq);
     P.s_y = (double4 *)(b + L.s_y);
-    P.s_ctype = (uint32_t *)(b + L.s_ctype); P.s_tau = (uint32_t *)(b + L.s_tau);
+    
     P.s_pct = (uint32_t *)(b + L.s_pct); P.s_pn = (float *)(b + L.s_pn);
     P.r0o0 = (float4 *)(b + L.r0o0); P.r0d0 = (float4 *)(b + L.r0d0);
     P.r0o1 = (float4 *)(b + L.r0o1); P.r0d1 = (float4 *)(b + L.r0d1);
@@ -1167,10 +1163,12 @@ static mpg_status launch_wavefront(const DScene &S, const SeedCtx &g, const Walk
         occ_t = std::max(occ_t, 1); occ_u = std::max(occ_u, 1);
     }
     int gt = num_sms() * occ_t;
-    int gp0 = (int)std::min<int64_t>(((int64_t)L.S * (nk + 1) + 127) / 128, (int64_t)num_sms() * 16);
-    int gp = (int)std::min<int64_t>((L.S + 127) / 128, (int64_t)num_sms() * 16);
-    int gu = (int)std::min<int64_t>((L.S + 127) / 128, (int64_t)num_sms() * occ_u * 4);
-    int gr = (int)std::min<int64_t>((L.S + 255) / 256, (int64_t)num_sms() * 8);
+    // grid-stride kernels sized to one resident wave of blocks: most waves are far
+    // smaller than S, and every block pays its stats flush and launch share
+    int gp0 = (int)std::min<int64_t>(((int64_t)L.S * (nk + 1) + 127) / 128, (int64_t)num_sms() * 8);
+    int gp = (int)std::min<int64_t>((L.S + 127) / 128, (int64_t)num_sms() * 8);
+    int gu = (int)std::min<int64_t>((L.S + 127) / 128, (int64_t)num_sms() * occ_u);
+    int gr = (int)std::min<int64_t>((L.S + 255) / 256, (int64_t)num_sms() * 2);
     int gi = (int)std::min<int64_t>((L.S + 255) / 256, (int64_t)num_sms() * 8);
 
     CUDA_TRY(cudaMemsetAsync(P.hdr, 0, sizeof(WFHeader), st));

@@ -99,14 +99,14 @@ struct WFParams {
     uint32_t S;                   // slots
     uint32_t *list[2];
     uint32_t *free_stack;
-    int32_t *s_walk;
-    uint32_t *s_trial, *s_flags, *s_surf, *s_ysurf, *s_psurf;
-    uint32_t *s_ctype;            // n | bits << 4 | learned << 12 of the current attempt
-    uint32_t *s_tau;              // resolved type string of the current chain
+    // hot per-slot scalars, one 32-B record per slot (one sector per slot access):
+    // walk, trial, flags, surf ids of x, surf ids of y, chain type n | bits << 4 |
+    // learned << 12 of the current attempt, resolved type string, beta (see rf())
+    uint32_t *rec;
+    uint32_t *s_psurf;
     uint32_t *s_pct;              // primary chain type n | tau << 4 (trials compare against it)
     float *s_pn;                  // P(n)
     int32_t *s_entry;
-    float *s_beta;
     float4 *s_tgt;
     double4 *s_x, *s_y;           // [k][S] chain / traced vertices (fp64 positions, w = prim);
                                   // during deduction s_x[i] holds the fp64 direction of ray i
@@ -125,6 +125,22 @@ struct WFParams {
     cudaGraphConditionalHandle cond;
     int use_cond;                 // 1: inside the CUDA-graph while loop; 0: host-driven waves (profiling)
 };
+
+enum { RF_WALK = 0, RF_TRIAL, RF_FLAGS, RF_SURF, RF_YSURF, RF_CTYPE, RF_TAU, RF_BETA };
+__device__ __forceinline__ uint32_t &rf(const WFParams &P, uint32_t slot, int f) {
+    return P.rec[(size_t)slot * 8 + f];
+}
+struct SlotRec {   // a whole record, read with two 16-B loads
+    uint32_t v[8];
+};
+__device__ __forceinline__ SlotRec rec_load(const WFParams &P, uint32_t slot) {
+    const uint4 *q = reinterpret_cast<const uint4 *>(P.rec + (size_t)slot * 8);
+    uint4 a = q[0], b = q[1];
+    SlotRec r;
+    r.v[0] = a.x; r.v[1] = a.y; r.v[2] = a.z; r.v[3] = a.w;
+    r.v[4] = b.x; r.v[5] = b.y; r.v[6] = b.z; r.v[7] = b.w;
+    return r;
+}
 
 // --------------------------------------------------------------------------
 // shared helpers
@@ -145,7 +161,7 @@ __device__ __forceinline__ void wf_append(const WFParams &P, uint32_t lst, uint3
 
 __device__ __forceinline__ void wf_free(const WFParams &P, uint32_t slot) {
     P.free_stack[wf_agg_add(&P.hdr->free_top)] = slot;
-    P.s_walk[slot] = -1;
+    rf(P, slot, RF_WALK) = (uint32_t)(-1);
 }
 
 // append a ray to list 0 of wave parity `par`
@@ -184,9 +200,9 @@ __device__ __forceinline__ void wf_start(const DScene &S, const SeedCtx &g, cons
         ct = (uint32_t)sr.n | ((sr.bits & 255u) << 4) | ((sr.learned ? 1u : 0u) << 12);
         pn = sr.Pn;
     }
-    P.s_walk[slot] = (int32_t)w;
-    P.s_trial[slot] = trial;
-    P.s_ctype[slot] = ct;
+    rf(P, slot, RF_WALK) = (uint32_t)((int32_t)w);
+    rf(P, slot, RF_TRIAL) = trial;
+    rf(P, slot, RF_CTYPE) = ct;
     P.s_pn[slot] = pn;
     if (ok) {
         double3 od = d3f(xD);
@@ -199,7 +215,7 @@ __device__ __forceinline__ void wf_start(const DScene &S, const SeedCtx &g, cons
             wf_emit0(P, par, xD, nrmz(f3d(dd)), __int_as_float(-1), slot);
         }
     }
-    P.s_flags[slot] = F_DEDUCE | extra_flags | (ok ? 0u : F_FAIL);
+    rf(P, slot, RF_FLAGS) = F_DEDUCE | extra_flags | (ok ? 0u : F_FAIL);
 }
 
 // --------------------------------------------------------------------------
@@ -213,7 +229,7 @@ __global__ void k_wf_init(const DScene S, const SeedCtx g, const WFParams P) {
             wf_start(S, g, P, s, (int64_t)s, 0u, 0u, 0u);
             P.list[0][s] = s;
         } else {
-            P.s_walk[s] = -1;
+            rf(P, s, RF_WALK) = (uint32_t)(-1);
         }
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -366,7 +382,7 @@ __global__ void __launch_bounds__(128, WF_TRACE_MINB) k_wf_rays(const DScene S, 
             if (node == SENT && leaf == NONE) { // ray done
                 const uint32_t slot = meta & ~WF_ANY;
                 if (any) {
-                    if (bsurf >= 0) atomicOr(P.s_flags + slot, F_FAIL);
+                    if (bsurf >= 0) atomicOr(&rf(P, slot, RF_FLAGS), F_FAIL);
                 } else {
                     float3 pf;
                     if (bprim >= 0) {
@@ -415,14 +431,15 @@ __global__ void __launch_bounds__(128) k_wf_post(const DScene S, const WFParams 
         const uint32_t meta = __float_as_uint(rd[idx].w);
         if (meta & WF_ANY) continue;
         const uint32_t slot = meta;
-        const uint32_t fl = P.s_flags[slot];
+        const SlotRec SR = rec_load(P, slot);
+        const uint32_t fl = SR.v[RF_FLAGS];
         const bool ded = (fl & F_DEDUCE) != 0;
         const int hs = P.h_s[slot];
         const float4 hp = P.h_p[slot];
         const int prim = __float_as_int(hp.w);
-        const uint32_t ct = P.s_ctype[slot];
+        const uint32_t ct = SR.v[RF_CTYPE];
         const int k = (int)(ct & 15u);
-        bool ok = hs >= 0 && (ded || hs == (int)((P.s_surf[slot] >> (4 * i)) & 15u));
+        bool ok = hs >= 0 && (ded || hs == (int)((SR.v[RF_SURF] >> (4 * i)) & 15u));
         uint32_t bit = 0;
         if (ok && ded) { // resolve the type of vertex i (R22, R14)
             bit = (ct >> (4 + i)) & 1u;
@@ -431,13 +448,13 @@ __global__ void __launch_bounds__(128) k_wf_post(const DScene S, const WFParams 
             if (bit && mat != 1) ok = false;
         }
         if (!ok) {
-            P.s_flags[slot] = fl | F_FAIL;
+            rf(P, slot, RF_FLAGS) = fl | F_FAIL;
             continue;
         }
-        const int64_t wk = P.s_walk[slot];
+        const int64_t wk = (int32_t)SR.v[RF_WALK];
         const double3 od = i == 0 ? d3f(xyz(__ldg(P.xD + wk / P.spp))) : ld3(P.s_y, (size_t)(i - 1) * P.S + slot);
         double3 tg;
-        const double bt = (double)P.s_beta[slot];
+        const double bt = (double)__uint_as_float(SR.v[RF_BETA]);
         if (ded) tg = od + ld3(P.s_x, (size_t)i * P.S + slot);
         else {
             double4 x4 = P.s_x[(size_t)i * P.S + slot];
@@ -447,14 +464,14 @@ __global__ void __launch_bounds__(128) k_wf_post(const DScene S, const WFParams 
         // the hit on the exact line, in fp64 (R24)
         const double3 y = refine_hit(S, prim, hs, od, tg, xyz(hp));
         P.s_y[(size_t)i * P.S + slot] = make_double4(y.x, y.y, y.z, (double)prim);
-        P.s_ysurf[slot] = (i == 0 ? 0u : P.s_ysurf[slot]) | ((uint32_t)(hs & 15) << (4 * i));
-        if (ded) P.s_tau[slot] = (i == 0 ? 0u : P.s_tau[slot]) | (bit << i);
+        rf(P, slot, RF_YSURF) = (i == 0 ? 0u : SR.v[RF_YSURF]) | ((uint32_t)(hs & 15) << (4 * i));
+        if (ded) rf(P, slot, RF_TAU) = (i == 0 ? 0u : SR.v[RF_TAU]) | (bit << i);
         if (i + 1 < k) { // ray i+1 from y_i
             double3 dd;
             if (ded) {
                 dd = ld3(P.s_x, (size_t)i * P.S + slot);
                 if (!scatter_dir(S, dd, prim, hs, f3d(y), bit)) {
-                    P.s_flags[slot] = fl | F_FAIL;
+                    rf(P, slot, RF_FLAGS) = fl | F_FAIL;
                     continue;
                 }
                 P.s_x[(size_t)(i + 1) * P.S + slot] = make_double4(dd.x, dd.y, dd.z, 0.0);
@@ -465,7 +482,7 @@ __global__ void __launch_bounds__(128) k_wf_post(const DScene S, const WFParams 
                 double3 v = q - y;
                 double l2 = ddot(v, v);
                 if (!(l2 > 0.0)) {
-                    P.s_flags[slot] = fl | F_FAIL;
+                    rf(P, slot, RF_FLAGS) = fl | F_FAIL;
                     continue;
                 }
                 dd = v * rsqrt(l2);
@@ -528,11 +545,12 @@ __global__ void __launch_bounds__(128, 4) k_wf_update(const DScene S, const Seed
 
     for (unsigned idx = blockIdx.x * blockDim.x + threadIdx.x; idx < count; idx += gridDim.x * blockDim.x) {
         const uint32_t slot = list[idx];
-        const uint32_t fl = P.s_flags[slot];
-        const int64_t w = P.s_walk[slot];
-        const uint32_t trial = P.s_trial[slot];
+        const SlotRec SR = rec_load(P, slot);
+        const uint32_t fl = SR.v[RF_FLAGS];
+        const int64_t w = (int32_t)SR.v[RF_WALK];
+        const uint32_t trial = SR.v[RF_TRIAL];
         int it = (int)(fl & F_IT_MASK);
-        const uint32_t ct = P.s_ctype[slot];
+        const uint32_t ct = SR.v[RF_CTYPE];
         const int k = max(1, min((int)(ct & 15u), KMAX));
 
         // ---------------- visibility result of a converged primary ----------------
@@ -552,14 +570,14 @@ __global__ void __launch_bounds__(128, 4) k_wf_update(const DScene S, const Seed
             continue;
         }
 
-        float beta = P.s_beta[slot];
+        float beta = __uint_as_float(SR.v[RF_BETA]);
         const bool deduce = fl & F_DEDUCE, failed = fl & F_FAIL;
-        const uint32_t tau = P.s_tau[slot];
+        const uint32_t tau = SR.v[RF_TAU];
         double3 x[KMAX];
         V3<R> sg[KMAX], tg[KMAX], dq[KMAX];
         int prim[KMAX], surf[KMAX];
         R Di[KMAX][4], Ub[KMAX][4];
-        const uint32_t sp_ = failed ? P.s_surf[slot] : P.s_ysurf[slot];
+        const uint32_t sp_ = failed ? SR.v[RF_SURF] : SR.v[RF_YSURF];
         const double4 *src = failed ? P.s_x : P.s_y;
 #pragma unroll
         for (int j = 0; j < KMAX; j++) {
@@ -603,10 +621,10 @@ __global__ void __launch_bounds__(128, 4) k_wf_update(const DScene S, const Seed
 #pragma unroll
             for (int j = 0; j < KMAX; j++)
                 if (j < k) P.s_x[(size_t)j * P.S + slot] = make_double4(x[j].x, x[j].y, x[j].z, (double)prim[j]);
-            P.s_surf[slot] = sp_;
+            rf(P, slot, RF_SURF) = sp_;
         }
         if (end < 0) { // continue: reprojection ray 0 toward q_0 = x_0 + beta dq_0 next wave (R5)
-            P.s_beta[slot] = beta;
+            rf(P, slot, RF_BETA) = __float_as_uint(beta);
             double3 d0;
             if (fresh) d0 = make_double3((double)dq[0].x, (double)dq[0].y, (double)dq[0].z);
             else d0 = ld3(P.s_dq, slot);
@@ -616,7 +634,7 @@ __global__ void __launch_bounds__(128, 4) k_wf_update(const DScene S, const Seed
             double l2 = ddot(v, v);
             bool ok = l2 > 0.0;
             if (ok) wf_emit0(P, nxt, xD, nrmz(f3d(v * rsqrt(l2))), __int_as_float(prim[0]), slot);
-            P.s_flags[slot] = (fl & (F_ITEM | F_SEQ)) | (uint32_t)it | (ok ? 0u : F_FAIL);
+            rf(P, slot, RF_FLAGS) = (fl & (F_ITEM | F_SEQ)) | (uint32_t)it | (ok ? 0u : F_FAIL);
             wf_append(P, nxt, slot);
             continue;
         }
@@ -656,7 +674,7 @@ __global__ void __launch_bounds__(128, 4) k_wf_update(const DScene S, const Seed
             if (st == ST_CONVERGED) { // the k+1 visibility segments are traced next wave
                 P.s_psurf[slot] = sp_;
                 P.s_pct[slot] = (uint32_t)k | (tau << 4);
-                P.s_flags[slot] = F_VIS | (uint32_t)it;
+                rf(P, slot, RF_FLAGS) = F_VIS | (uint32_t)it;
                 float3 a = xD;
 #pragma unroll 1
                 for (int j = 0; j <= k; j++) { // fp32 segments as walk.cuh
@@ -752,9 +770,18 @@ __global__ void __launch_bounds__(128, 4) k_wf_update(const DScene S, const Seed
         if (item) P.s_entry[slot] = (int32_t)e;
         wf_append(P, nxt, slot);
     }
-    atomicAdd(&s_stats[SS_NEWTON], (unsigned long long)c_newton);
-    atomicAdd(&s_stats[SS_VTX], (unsigned long long)c_vtx);
-    atomicAdd(&s_stats[SS_ATTEMPTS], (unsigned long long)c_att);
+    // warp-reduce the per-thread counters: one shared atomic per warp and counter
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        c_newton += __shfl_down_sync(MPG_FULL, c_newton, off);
+        c_vtx += __shfl_down_sync(MPG_FULL, c_vtx, off);
+        c_att += __shfl_down_sync(MPG_FULL, c_att, off);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (c_newton) atomicAdd(&s_stats[SS_NEWTON], (unsigned long long)c_newton);
+        if (c_vtx) atomicAdd(&s_stats[SS_VTX], (unsigned long long)c_vtx);
+        if (c_att) atomicAdd(&s_stats[SS_ATTEMPTS], (unsigned long long)c_att);
+    }
     __syncthreads();
     if (P.stats)
         for (int j = threadIdx.x; j < SS_N; j += blockDim.x)
