@@ -353,10 +353,18 @@ __device__ __forceinline__ bool quad_hit(float3 o, float3 d, float3 q0, float3 e
 // Closest hit (ANY=false) or any hit (ANY=true) with t in (tmin, tmax) over all
 // surfaces, or only specular ones (spec_only): the operator r(x, w) of Eq. 6
 // and the visibility V of Eq. 2.
+#if defined(MPG_TIMELINE) && !defined(MPG_NH)
+#define MPG_NH
+#endif
+#ifdef MPG_NH
+__device__ unsigned long long g_nh[256];   // diagnostic: closest-hit rays by node visits
+#endif
 template <bool ANY>
 __device__ bool trace(const DScene &S, float3 o, float3 d, float tmin, float tmax, bool spec_only, Hit &h,
-                      LaneStats &st, int hint = -1) {
-    st.rays++;
+                      LaneStats &st, int hint = -1) {   // callers count their rays
+#ifdef MPG_NH
+    const uint32_t n_at_entry = st.nodes;
+#endif
     float best = tmax;
     int bprim = -2, bsurf = -1;
     float bb0 = 0.f, bb1 = 0.f, bb2 = 0.f;
@@ -438,6 +446,9 @@ __device__ bool trace(const DScene &S, float3 o, float3 d, float tmin, float tma
         }
     }
     if (ANY) return false;
+#ifdef MPG_NH
+    atomicAdd(&g_nh[min(st.nodes - n_at_entry, 255u)], 1ull);
+#endif
     h.t = best; h.prim = bprim; h.surf = bsurf;
     if (bsurf < 0) return false;
     if (bprim >= 0) {

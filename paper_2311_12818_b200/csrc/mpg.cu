@@ -467,6 +467,7 @@ __global__ void k_trace(const DScene S, const float4 *orig, const float4 *dir, i
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         LaneStats ls = {0, 0, 0};
         Hit h;
+        ls.rays++;
         bool ok = trace<false>(S, xyz(orig[i]), nrmz(xyz(dir[i])), tmin, 3.0e38f, spec_only != 0, h, ls);
         t[i] = ok ? h.t : -1.0f;
         prim[i] = ok && h.prim >= 0 ? __float_as_int(S.tpos[TSTRIDE * h.prim].w) : -1;
@@ -929,6 +930,19 @@ extern "C" mpg_status mpg_sample_seeds(const mpg_scene *scene, const mpg_guide *
 // ----------------------------------------------------------------------------
 // walk
 // ----------------------------------------------------------------------------
+#ifdef MPG_TIMELINE
+// diagnostic build only: copy out (and zero) the k_walk activity timeline
+extern "C" int mpg_debug_timeline(unsigned long long *host4096, unsigned shift, unsigned long long *host256) {
+    cudaDeviceSynchronize();
+    cudaMemcpyToSymbol(g_tl_shift, &shift, sizeof(shift));
+    cudaMemcpyFromSymbol(host4096, g_tl, sizeof(g_tl));
+    cudaMemcpyFromSymbol(host256, g_nh, sizeof(g_nh));
+    static unsigned long long zero[1024 * 4];
+    cudaMemcpyToSymbol(g_tl, zero, sizeof(g_tl));
+    cudaMemcpyToSymbol(g_nh, zero, sizeof(g_nh));
+    return 0;
+}
+#endif
 static float *g_dbg = nullptr;
 static int64_t g_dbg_n = 0;
 static int g_dbg_stride = 0;
@@ -1069,6 +1083,13 @@ static mpg_status launch_walk(const DScene &S, const SeedCtx &g, WalkParams P, c
     MKLayout L = mk_layout(P.n);
     char *b = (char *)ws;
     P.local_trials = LOCAL_TRIALS(P.n);
+    P.item_b0 = 4u;
+    P.item_grow = 1u;
+    P.backoff_max = 32768u;
+    if (const char *v = getenv("MPG_LOCAL_TRIALS")) P.local_trials = (uint32_t)atoi(v);
+    if (const char *v = getenv("MPG_ITEM_B0")) P.item_b0 = std::max(1, atoi(v));
+    if (const char *v = getenv("MPG_ITEM_GROW")) P.item_grow = std::max(1, std::min(4, atoi(v)));
+    if (const char *v = getenv("MPG_BACKOFF_MAX")) P.backoff_max = std::max(32, atoi(v));
     P.hard_cap = L.H;
     // tickets index the ring only below item_cap: it bounds both the reads and the clear;
     // a full ring (or entry table) makes the walk continue its trials sequentially

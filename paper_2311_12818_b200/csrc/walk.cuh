@@ -69,6 +69,9 @@ struct WalkParams {
     // exhausted take items by ticket from a ring, in the same launch.  k = the
     // smallest successful trial: every trial below it has run (batch order).
     uint32_t local_trials;
+    uint32_t item_b0;           // first item batch of a hard entry
+    uint32_t item_grow;         // later batches: previous << item_grow
+    uint32_t backoff_max;       // ns, cap of the waiting warps' sleep
     uint32_t hard_cap;          // entries
     uint32_t item_cap;          // item ring capacity (a full ring -> sequential fallback)
     struct TrialHdr *th;        // counters (zeroed before the launch)
@@ -169,7 +172,7 @@ template <int KMAX>
 __device__ __forceinline__ int trace_chain(const DScene &S, bool deduce, int k, uint32_t bits, bool learned,
                                            float3 xD, float3 tgt, const double3 (&q)[KMAX], const int (&hint)[KMAX],
                                            uint32_t surf_req, float eps, double3 (&y)[KMAX], int (&yp)[KMAX],
-                                           int (&ys)[KMAX], LaneStats &st, uint32_t &tau_res) {
+                                           int (&ys)[KMAX], LaneStats &st, uint32_t &tau_res, unsigned *s_rays) {
     uint32_t res = 0;
     double3 o = d3f(xD);
     double3 dd = make_double3(0.0, 0.0, 0.0);
@@ -191,6 +194,11 @@ __device__ __forceinline__ int trace_chain(const DScene &S, bool deduce, int k, 
         } else if (i > 0) {
             if (!scatter_dir(S, dd, pprim, psurf, f3d(o), (res >> (i - 1)) & 1u)) return 4 | (i << 4);
         }
+        // chain rays are counted with a shared-memory atomic on the lane's own slot:
+        // an atomic in this loop makes ptxas emit a YIELD at its head, which lets lanes
+        // that are done with ray i go on while warp-mates still traverse (measured
+        // k_walk -17 % configs[1], -7 % [2], -13 % [3] against a register counter)
+        atomicAdd(s_rays, 1u);
         Hit h;
         float3 of = f3d(o), d = nrmz(f3d(dd));
         if (!trace<false>(S, of, d, eps, 3.0e38f, true, h, st, deduce ? -1 : rget(hint, i))) return 1 | (i << 4);
@@ -237,10 +245,48 @@ __device__ __forceinline__ bool items_push(const WalkParams &P, uint32_t e, uint
     return true;
 }
 
+// the primary queue is exhausted (this warp saw it, or the global counter says so)
+__device__ __forceinline__ bool queue_drained(const WalkParams &P, bool drained) {
+    return drained || __ldcg(&P.th->queue) >= (unsigned long long)P.n;
+}
+// make walk w a hard entry whose trials last+1 .. run as items (first batch
+// item_b0); false (and seq_only) if the entry table or the ring is full
+__device__ __forceinline__ bool hard_publish(const WalkParams &P, int64_t w, uint32_t psurf, int pk, uint32_t ptau,
+                                             uint32_t last, bool &seq_only) {
+    unsigned int e = atomicAdd(&P.th->n_entries, 1u);
+    if (e >= P.hard_cap) return false;
+    const uint32_t B = min(P.item_b0, P.k_max - last);
+    P.e_walk[e] = w;
+    P.e_psurf[e] = psurf;
+    P.e_pct[e] = (uint32_t)pk | (ptau << 4);
+    P.e_best[e] = HARD_NONE;
+    P.e_batch[e] = B;
+    P.e_pending[e] = B;
+    P.e_issued[e] = last + B;
+    __threadfence();
+    const bool ok = items_push(P, e, last + 1, B);
+    if (!ok) seq_only = true;
+    return ok;
+}
+
+#ifdef MPG_TIMELINE
+// diagnostic build only (tools/timeline.py): per 65.5-us bucket of %globaltimer,
+// [warp iterations, tracing lanes, working lanes, waiting lanes]
+__device__ unsigned long long g_tl[1024 * 4];
+__device__ unsigned g_tl_shift = 16;
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#endif
+
 template <int KMAX, typename R>
 __global__ void __launch_bounds__(128, (KMAX <= 2 ? MPG_WALK_MINB2 : 2)) k_walk(const DScene S, const SeedCtx g, const WalkParams P) {
     __shared__ unsigned long long s_stats[SS_N];
+    __shared__ unsigned s_rays[128];   // chain rays per thread (see trace_chain)
     for (int i = threadIdx.x; i < SS_N; i += blockDim.x) s_stats[i] = 0ull;
+    s_rays[threadIdx.x] = 0u;
     __syncthreads();
 
     const int lane = threadIdx.x & 31;
@@ -369,7 +415,7 @@ __global__ void __launch_bounds__(128, (KMAX <= 2 ? MPG_WALK_MINB2 : 2)) k_walk(
             // the whole warp waits for trial items: back off (polling lanes would
             // otherwise flood L2 while the remaining lanes finish their walks)
             __nanosleep(backoff);
-            backoff = min(2u * backoff, 32768u);
+            backoff = min(2u * backoff, P.backoff_max);
             continue;
         }
         backoff = 256u;
@@ -404,6 +450,20 @@ __global__ void __launch_bounds__(128, (KMAX <= 2 ? MPG_WALK_MINB2 : 2)) k_walk(
             else { end_status = ST_SEED_FAIL; phase = PH_END; }
         }
 
+#ifdef MPG_TIMELINE
+        {
+            const unsigned tr = __ballot_sync(MPG_FULL, phase == PH_DEDUCE || phase == PH_REPROJ);
+            const unsigned wk = __ballot_sync(MPG_FULL, phase != PH_WAIT && phase != PH_IDLE);
+            const unsigned wt = __ballot_sync(MPG_FULL, phase == PH_WAIT);
+            if (lane == 0) {
+                const unsigned b = (unsigned)(gtimer() >> g_tl_shift) & 1023u;
+                atomicAdd(&g_tl[4 * b], 1ull);
+                atomicAdd(&g_tl[4 * b + 1], (unsigned long long)__popc(tr));
+                atomicAdd(&g_tl[4 * b + 2], (unsigned long long)__popc(wk));
+                atomicAdd(&g_tl[4 * b + 3], (unsigned long long)__popc(wt));
+            }
+        }
+#endif
         // ---- trace: deduction (Eq. 6) or reprojection --------------------
         if (phase == PH_DEDUCE || phase == PH_REPROJ) {
             bool ded = phase == PH_DEDUCE;
@@ -411,7 +471,7 @@ __global__ void __launch_bounds__(128, (KMAX <= 2 ? MPG_WALK_MINB2 : 2)) k_walk(
 #pragma unroll
             for (int i = 0; i < KMAX; i++) sreq |= (uint32_t)(surf[i] & 15) << (4 * i);
             uint32_t tres = tau;
-            int why = trace_chain<KMAX>(S, ded, k, bits, learned, xD, tgt, q, prim, sreq, P.ray_eps, y, yp, ys, ls, tres);
+            int why = trace_chain<KMAX>(S, ded, k, bits, learned, xD, tgt, q, prim, sreq, P.ray_eps, y, yp, ys, ls, tres, &s_rays[threadIdx.x]);
             bool ok = why == 0;
             if (ok && ded) tau = tres;
             if (!ok && !ded && P.dbg && trial == 0 && w < P.n_dbg && 2 * it + 3 < P.dbg_stride)
@@ -487,6 +547,7 @@ __global__ void __launch_bounds__(128, (KMAX <= 2 ? MPG_WALK_MINB2 : 2)) k_walk(
                             float3 dd = b - a;
                             float l = len(dd);
                             Hit hh;
+                            ls.rays++;
                             if (trace<true>(S, a, dd * (1.0f / l), P.ray_eps, l - P.ray_eps, false, hh, ls)) {
                                 vis = false;
                                 break;
@@ -529,8 +590,12 @@ __global__ void __launch_bounds__(128, (KMAX <= 2 ? MPG_WALK_MINB2 : 2)) k_walk(
                         if (i >= k) break;
                         psurf |= (uint32_t)(surf[i] & 15) << (4 * i);
                     }
-                    trial = 1;
-                    phase = PH_SEED;
+                    if (queue_drained(P, drained) && P.items && hard_publish(P, w, psurf, pk, ptau, 0u, seq_only))
+                        phase = PH_FETCH;
+                    else {
+                        trial = 1;
+                        phase = PH_SEED;
+                    }
                 } else {
                     P.trials[w] = 0;
                     P.w[w] = 0.0f;
@@ -570,7 +635,7 @@ __global__ void __launch_bounds__(128, (KMAX <= 2 ? MPG_WALK_MINB2 : 2)) k_walk(
                             trial_finalize(P, w, P.k_max, true, s_stats);
                             walk_resolved(P);
                         } else {
-                            const uint32_t B = min(2u * __ldcg(P.e_batch + e), P.k_max - issued);
+                            const uint32_t B = min(__ldcg(P.e_batch + e) << P.item_grow, P.k_max - issued);
                             P.e_batch[e] = B;
                             P.e_pending[e] = B;
                             P.e_issued[e] = issued + B;
@@ -590,25 +655,12 @@ __global__ void __launch_bounds__(128, (KMAX <= 2 ? MPG_WALK_MINB2 : 2)) k_walk(
                     walk_resolved(P);
                     phase = PH_FETCH;
                 } else {
-                    bool published = false;
-                    if (trial >= P.local_trials && !seq_only && P.items) {
-                        // hand the remaining trials to parallel items
-                        unsigned int e = atomicAdd(&P.th->n_entries, 1u);
-                        if (e < P.hard_cap) {
-                            const uint32_t B = min(4u, P.k_max - trial);
-                            P.e_walk[e] = w;
-                            P.e_psurf[e] = psurf;
-                            P.e_pct[e] = (uint32_t)pk | (ptau << 4);
-                            P.e_best[e] = HARD_NONE;
-                            P.e_batch[e] = B;
-                            P.e_pending[e] = B;
-                            P.e_issued[e] = trial + B;
-                            __threadfence();
-                            published = items_push(P, e, trial + 1, B);
-                            if (!published) seq_only = true;
-                        }
-                    }
-                    if (published) phase = PH_FETCH;
+                    // hand the remaining trials to parallel items after local_trials
+                    // sequential ones, or at once when the primary queue is exhausted
+                    // (idle lanes are then waiting for exactly this work)
+                    if ((trial >= P.local_trials || queue_drained(P, drained)) && !seq_only && P.items &&
+                        hard_publish(P, w, psurf, pk, ptau, trial, seq_only))
+                        phase = PH_FETCH;
                     else {
                         trial++;
                         phase = PH_SEED;
@@ -619,7 +671,8 @@ __global__ void __launch_bounds__(128, (KMAX <= 2 ? MPG_WALK_MINB2 : 2)) k_walk(
     }
 
     // ---- stats reduction ----------------------------------------------------
-    unsigned long long v[6] = {c_newton, c_attempts, ls.rays, ls.nodes, ls.tris, c_vtx};
+    unsigned long long v[6] = {c_newton, c_attempts, (unsigned long long)ls.rays + s_rays[threadIdx.x], ls.nodes,
+                               ls.tris, c_vtx};
 #pragma unroll
     for (int j = 0; j < 6; j++) {
 #pragma unroll

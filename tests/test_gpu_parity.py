@@ -474,8 +474,10 @@ def test_sorted_order_gives_identical_walks(which):
     used = np.arange(a["pos"].shape[1])[None, :] < n[:, None]          # vertices each chain has
     assert np.array_equal(a["pos"][conv][used], b["pos"][conv][used])
     assert np.array_equal(a["prim"][conv][used], b["prim"][conv][used])
-    # traversal counters depend on warp composition (postponed leaves wait for warp-mates)
-    drop = ("node_visits", "tri_tests")
+    # traversal counters depend on warp composition (postponed leaves wait for warp-mates);
+    # work counters include the trial items run above a walk's final k, whose number
+    # depends on when idle lanes pick items up (the outputs above do not)
+    drop = ("node_visits", "tri_tests", "rays", "vertex_iters", "newton_iters", "attempts")
     assert {k: v for k, v in sa.items() if k not in drop} == {k: v for k, v in sb.items() if k not in drop}
 
 
