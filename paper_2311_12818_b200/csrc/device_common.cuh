@@ -350,7 +350,7 @@ __device__ __forceinline__ bool quad_hit(float3 o, float3 d, float3 q0, float3 e
     return true;
 }
 
-// Closest hit (ANY=false) or any hit (ANY=true) with t in (tmin, tmax) over all
+// Closest hit (ANY false) or any hit (ANY true) with t in (tmin, tmax) over all
 // surfaces, or only specular ones (spec_only): the operator r(x, w) of Eq. 6
 // and the visibility V of Eq. 2.
 #if defined(MPG_TIMELINE) && !defined(MPG_NH)
@@ -359,9 +359,8 @@ __device__ __forceinline__ bool quad_hit(float3 o, float3 d, float3 q0, float3 e
 #ifdef MPG_NH
 __device__ unsigned long long g_nh[256];   // diagnostic: closest-hit rays by node visits
 #endif
-template <bool ANY>
-__device__ bool trace(const DScene &S, float3 o, float3 d, float tmin, float tmax, bool spec_only, Hit &h,
-                      LaneStats &st, int hint = -1) {   // callers count their rays
+__device__ __forceinline__ bool trace(const DScene &S, float3 o, float3 d, float tmin, float tmax, bool spec_only,
+                                      const bool ANY, Hit &h, LaneStats &st, int hint = -1) {   // callers count rays
 #ifdef MPG_NH
     const uint32_t n_at_entry = st.nodes;
 #endif

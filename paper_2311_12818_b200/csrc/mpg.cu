@@ -468,7 +468,7 @@ __global__ void k_trace(const DScene S, const float4 *orig, const float4 *dir, i
         LaneStats ls = {0, 0, 0};
         Hit h;
         ls.rays++;
-        bool ok = trace<false>(S, xyz(orig[i]), nrmz(xyz(dir[i])), tmin, 3.0e38f, spec_only != 0, h, ls);
+        bool ok = trace(S, xyz(orig[i]), nrmz(xyz(dir[i])), tmin, 3.0e38f, spec_only != 0, false, h, ls);
         t[i] = ok ? h.t : -1.0f;
         prim[i] = ok && h.prim >= 0 ? __float_as_int(S.tpos[TSTRIDE * h.prim].w) : -1;
         surf[i] = ok ? h.surf : -1;
@@ -1089,6 +1089,11 @@ static mpg_status launch_walk(const DScene &S, const SeedCtx &g, WalkParams P, c
     if (const char *v = getenv("MPG_LOCAL_TRIALS")) P.local_trials = (uint32_t)atoi(v);
     if (const char *v = getenv("MPG_ITEM_B0")) P.item_b0 = std::max(1, atoi(v));
     if (const char *v = getenv("MPG_ITEM_GROW")) P.item_grow = std::max(1, std::min(4, atoi(v)));
+    P.item_grow_idle = 3u;   // x8 (measured x2/x4/x8: configs[1] 49.1/47.2/46.6 ms, [4] 13.2/12.5/11.8, [2,3] flat)
+    P.idle_backlog = 0u;   // set from the grid below
+    P.item_b0_idle = 4u;
+    if (const char *v = getenv("MPG_ITEM_B0_IDLE")) P.item_b0_idle = std::max(1, atoi(v));
+    if (const char *v = getenv("MPG_ITEM_GROW_IDLE")) P.item_grow_idle = std::max(1, std::min(4, atoi(v)));
     if (const char *v = getenv("MPG_BACKOFF_MAX")) P.backoff_max = std::max(32, atoi(v));
     P.hard_cap = L.H;
     // tickets index the ring only below item_cap: it bounds both the reads and the clear;
@@ -1122,6 +1127,11 @@ static mpg_status launch_walk(const DScene &S, const SeedCtx &g, WalkParams P, c
     }
     int64_t want = (P.n + 127) / 128;
     int blocks = (int)std::min<int64_t>(want, (int64_t)num_sms() * occ);
+    {
+        int div = 8;   // idle: fewer unclaimed items than 1/div of the lanes
+        if (const char *v = getenv("MPG_IDLE_DIV")) div = std::max(1, atoi(v));
+        P.idle_backlog = (uint32_t)(blocks * 128 / div);
+    }
     COUNT_LAUNCH(1);
     k_walk<KMAX, R><<<blocks, 128, 0, st>>>(S, g, P);
     CUDA_TRY(cudaPeekAtLastError());

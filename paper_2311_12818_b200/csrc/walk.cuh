@@ -26,7 +26,8 @@
 
 // occupancy: k <= 2 chains are capped at 80 registers (6 blocks of 128 per SM):
 // the spills are cheaper than the latency the extra warps hide (+11% on configs[1])
-enum { PH_FETCH = 0, PH_SEED = 1, PH_DEDUCE = 2, PH_SOLVE = 3, PH_REPROJ = 4, PH_END = 5, PH_IDLE = 6, PH_WAIT = 7 };
+enum { PH_FETCH = 0, PH_SEED = 1, PH_DEDUCE = 2, PH_SOLVE = 3, PH_REPROJ = 4, PH_END = 5, PH_IDLE = 6, PH_WAIT = 7,
+       PH_VIS = 8 };
 #define HARD_NONE 0xffffffffu
 enum { ST_CONVERGED = 0, ST_MAXITER = 1, ST_SEED_FAIL = 2, ST_BAD_SIDE = 3, ST_DEGENERATE = 4, ST_OCCLUDED = 5 };
 
@@ -71,6 +72,10 @@ struct WalkParams {
     uint32_t local_trials;
     uint32_t item_b0;           // first item batch of a hard entry
     uint32_t item_grow;         // later batches: previous << item_grow
+    // ... or previous << item_grow_idle while the unclaimed item backlog is below
+    // idle_backlog (most lanes idle in the tail: a larger batch then costs no
+    // throughput and saves rounds of trial-walk latency on the critical path)
+    uint32_t item_grow_idle, idle_backlog, item_b0_idle;
     uint32_t backoff_max;       // ns, cap of the waiting warps' sleep
     uint32_t hard_cap;          // entries
     uint32_t item_cap;          // item ring capacity (a full ring -> sequential fallback)
@@ -168,11 +173,19 @@ __device__ __forceinline__ double3 refine_hit(const DScene &S, int prim, int sur
 // Deduction resolves the type string: vertex i takes bit i of `bits`, except
 // that the initializer (learned = false) always reflects on a conductor; T on
 // a conductor fails (R22, R14).  The resolved string is returned in tau_res.
+enum { TR_REPROJ = 0, TR_DEDUCE = 1, TR_VIS = 2 };
+// TR_VIS: the k+1 visibility segments x_D -> x_1 -> ... -> x_k -> x_L of the
+// converged chain x (any hit against all surfaces); returns 5 if occluded.
+// One traversal call site serves all three modes, so lanes tracing visibility
+// traverse together with warp-mates that reproject (no separate low-occupancy
+// visibility traversal).
 template <int KMAX>
-__device__ __forceinline__ int trace_chain(const DScene &S, bool deduce, int k, uint32_t bits, bool learned,
-                                           float3 xD, float3 tgt, const double3 (&q)[KMAX], const int (&hint)[KMAX],
+__device__ __forceinline__ int trace_chain(const DScene &S, int mode, int k, uint32_t bits, bool learned,
+                                           float3 xD, float3 xL, float3 tgt, const double3 (&q)[KMAX],
+                                           const double3 (&x)[KMAX], const int (&hint)[KMAX],
                                            uint32_t surf_req, float eps, double3 (&y)[KMAX], int (&yp)[KMAX],
                                            int (&ys)[KMAX], LaneStats &st, uint32_t &tau_res, unsigned *s_rays) {
+    const bool deduce = mode == TR_DEDUCE, vis = mode == TR_VIS;
     uint32_t res = 0;
     double3 o = d3f(xD);
     double3 dd = make_double3(0.0, 0.0, 0.0);
@@ -183,25 +196,43 @@ __device__ __forceinline__ int trace_chain(const DScene &S, bool deduce, int k, 
         dd = v * rsqrt(l2);
     }
     int pprim = -1, psurf = 0;
+    const int nr = vis ? k + 1 : k;
 #pragma unroll 1
-    for (int i = 0; i < k; i++) {
-        const double3 qi = rget(q, i);
-        if (!deduce) {
-            double3 v = qi - o;
-            double l2 = ddot(v, v);
-            if (!(l2 > 0.0)) return 3 | (i << 4);
-            dd = v * rsqrt(l2);
-        } else if (i > 0) {
-            if (!scatter_dir(S, dd, pprim, psurf, f3d(o), (res >> (i - 1)) & 1u)) return 4 | (i << 4);
+    for (int i = 0; i < nr; i++) {
+        float3 of, d;
+        float tmax = 3.0e38f;
+        if (vis) {
+            const float3 a = i == 0 ? xD : f3d(rget(x, i - 1));
+            const float3 b = i == k ? xL : f3d(rget(x, i));
+            const float3 ab = b - a;
+            const float l = len(ab);
+            of = a;
+            d = ab * (1.0f / l);
+            tmax = l - eps;
+        } else {
+            if (!deduce) {
+                double3 v = rget(q, i) - o;
+                double l2 = ddot(v, v);
+                if (!(l2 > 0.0)) return 3 | (i << 4);
+                dd = v * rsqrt(l2);
+            } else if (i > 0) {
+                if (!scatter_dir(S, dd, pprim, psurf, f3d(o), (res >> (i - 1)) & 1u)) return 4 | (i << 4);
+            }
+            of = f3d(o);
+            d = nrmz(f3d(dd));
         }
-        // chain rays are counted with a shared-memory atomic on the lane's own slot:
-        // an atomic in this loop makes ptxas emit a YIELD at its head, which lets lanes
+        // rays are counted with a shared-memory atomic on the lane's own slot: an
+        // atomic in this loop makes ptxas emit a YIELD at its head, which lets lanes
         // that are done with ray i go on while warp-mates still traverse (measured
         // k_walk -17 % configs[1], -7 % [2], -13 % [3] against a register counter)
         atomicAdd(s_rays, 1u);
         Hit h;
-        float3 of = f3d(o), d = nrmz(f3d(dd));
-        if (!trace<false>(S, of, d, eps, 3.0e38f, true, h, st, deduce ? -1 : rget(hint, i))) return 1 | (i << 4);
+        const bool hit = trace(S, of, d, eps, tmax, !vis, vis, h, st, mode == TR_REPROJ ? rget(hint, i) : -1);
+        if (vis) {
+            if (hit) return 5;
+            continue;
+        }
+        if (!hit) return 1 | (i << 4);
         if (!deduce && h.surf != (int)((surf_req >> (4 * i)) & 15u)) return 2 | (i << 4);
         if (deduce) {
             uint32_t bit = (bits >> i) & 1u;
@@ -210,7 +241,7 @@ __device__ __forceinline__ int trace_chain(const DScene &S, bool deduce, int k, 
             if (bit && mat != 1) return 4 | (i << 4);
             res |= bit << i;
         }
-        const double3 yi = refine_hit(S, h.prim, h.surf, o, deduce ? o + dd : qi, h.p);
+        const double3 yi = refine_hit(S, h.prim, h.surf, o, deduce ? o + dd : rget(q, i), h.p);
         rset(y, i, yi);
         rset(yp, i, h.prim);
         rset(ys, i, h.surf);
@@ -255,7 +286,8 @@ __device__ __forceinline__ bool hard_publish(const WalkParams &P, int64_t w, uin
                                              uint32_t last, bool &seq_only) {
     unsigned int e = atomicAdd(&P.th->n_entries, 1u);
     if (e >= P.hard_cap) return false;
-    const uint32_t B = min(P.item_b0, P.k_max - last);
+    const unsigned backlog = *(volatile unsigned *)&P.th->item_tail - *(volatile unsigned *)&P.th->item_head;
+    const uint32_t B = min((int)backlog < (int)P.idle_backlog ? P.item_b0_idle : P.item_b0, P.k_max - last);
     P.e_walk[e] = w;
     P.e_psurf[e] = psurf;
     P.e_pct[e] = (uint32_t)pk | (ptau << 4);
@@ -315,6 +347,7 @@ __global__ void __launch_bounds__(128, (KMAX <= 2 ? MPG_WALK_MINB2 : 2)) k_walk(
     double3 q[KMAX], y[KMAX];
     int yp[KMAX], ys[KMAX];
     bool singular = false;
+    bool vis_done = false, occluded = false;   // visibility of a converged primary (PH_VIS)
 #pragma unroll
     for (int i = 0; i < KMAX; i++) {
         x[i] = make_double3(0.0, 0.0, 0.0);
@@ -465,14 +498,21 @@ __global__ void __launch_bounds__(128, (KMAX <= 2 ? MPG_WALK_MINB2 : 2)) k_walk(
         }
 #endif
         // ---- trace: deduction (Eq. 6) or reprojection --------------------
-        if (phase == PH_DEDUCE || phase == PH_REPROJ) {
+        if (phase == PH_DEDUCE || phase == PH_REPROJ || phase == PH_VIS) {
             bool ded = phase == PH_DEDUCE;
             uint32_t sreq = 0;
 #pragma unroll
             for (int i = 0; i < KMAX; i++) sreq |= (uint32_t)(surf[i] & 15) << (4 * i);
             uint32_t tres = tau;
-            int why = trace_chain<KMAX>(S, ded, k, bits, learned, xD, tgt, q, prim, sreq, P.ray_eps, y, yp, ys, ls, tres, &s_rays[threadIdx.x]);
+            const int mode = ded ? TR_DEDUCE : (phase == PH_VIS ? TR_VIS : TR_REPROJ);
+            int why = trace_chain<KMAX>(S, mode, k, bits, learned, xD, xL, tgt, q, x, prim, sreq, P.ray_eps, y, yp, ys, ls,
+                                        tres, &s_rays[threadIdx.x]);
             bool ok = why == 0;
+            if (mode == TR_VIS) {
+                occluded = !ok;
+                vis_done = true;
+                phase = PH_END;
+            } else {
             if (ok && ded) tau = tres;
             if (!ok && !ded && P.dbg && trial == 0 && w < P.n_dbg && 2 * it + 3 < P.dbg_stride)
                 P.dbg[w * P.dbg_stride + 2 * (it + 1)] = -(float)(why + 1);
@@ -493,6 +533,7 @@ __global__ void __launch_bounds__(128, (KMAX <= 2 ? MPG_WALK_MINB2 : 2)) k_walk(
                 beta *= 0.5f;
                 it++;
                 phase = PH_SOLVE;
+            }
             }
         }
 
@@ -527,6 +568,9 @@ __global__ void __launch_bounds__(128, (KMAX <= 2 ? MPG_WALK_MINB2 : 2)) k_walk(
         }
 
         // ---- end of an attempt ---------------------------------------------
+        // a converged primary first traces its visibility segments (next iteration,
+        // in the shared trace phase), then comes back here
+        if (phase == PH_END && trial == 0 && end_status == ST_CONVERGED && !vis_done) phase = PH_VIS;
         if (phase == PH_END) {
             c_newton += it;
             int st = end_status;
@@ -536,25 +580,12 @@ __global__ void __launch_bounds__(128, (KMAX <= 2 ? MPG_WALK_MINB2 : 2)) k_walk(
                     const DLight &L = S.light[lid];
                     float kap;
                     R DL[4];
+                    vis_done = false;
+                    // sides first: BAD_SIDE takes precedence over OCCLUDED
                     if (!post_sweep<KMAX, R>(S, L, k, tau, xD, xL, x, prim, surf, true, kap, DL)) st = ST_BAD_SIDE;
                     else {
                         // visibility: k+1 any-hit segments against all surfaces
-                        bool vis = true;
-                        float3 a = xD;
-#pragma unroll 1
-                        for (int j = 0; j <= k; j++) {
-                            float3 b = j == k ? xL : f3d(y[j]);
-                            float3 dd = b - a;
-                            float l = len(dd);
-                            Hit hh;
-                            ls.rays++;
-                            if (trace<true>(S, a, dd * (1.0f / l), P.ray_eps, l - P.ray_eps, false, hh, ls)) {
-                                vis = false;
-                                break;
-                            }
-                            a = b;
-                        }
-                        if (!vis) st = ST_OCCLUDED;
+                        if (occluded) st = ST_OCCLUDED;
                         else {
                             G = singular ? 0.0f : ggt_from_blocks<KMAX, R>(k, xD, nD, x, Di, Ub, sg, tg, DL);
                             float Le = L.emit;
@@ -635,7 +666,10 @@ __global__ void __launch_bounds__(128, (KMAX <= 2 ? MPG_WALK_MINB2 : 2)) k_walk(
                             trial_finalize(P, w, P.k_max, true, s_stats);
                             walk_resolved(P);
                         } else {
-                            const uint32_t B = min(__ldcg(P.e_batch + e) << P.item_grow, P.k_max - issued);
+                            const unsigned backlog = *(volatile unsigned *)&P.th->item_tail -
+                                                     *(volatile unsigned *)&P.th->item_head;
+                            const uint32_t g = (int)backlog < (int)P.idle_backlog ? P.item_grow_idle : P.item_grow;
+                            const uint32_t B = min(__ldcg(P.e_batch + e) << g, P.k_max - issued);
                             P.e_batch[e] = B;
                             P.e_pending[e] = B;
                             P.e_issued[e] = issued + B;

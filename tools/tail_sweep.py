@@ -1,6 +1,6 @@
 """Time mpg_manifold_walk under trial-schedule knobs (env, read at every launch).
 
-    python tools/tail_sweep.py <config> "B0,GROW,LOCAL,BACKOFF" ...
+    python tools/tail_sweep.py <config> "B0,GROW,LOCAL,BACKOFF,GROW_IDLE,IDLE_DIV,B0_IDLE" ...
 
 Each setting: MPG_ITEM_B0 (first item batch), MPG_ITEM_GROW (batch shift),
 MPG_LOCAL_TRIALS (sequential trials before a walk becomes a hard entry),
@@ -21,7 +21,7 @@ ds = mpg.DeviceScene(w)
 b = mpg.Batch(w.xD, w.nD, w.spp, w.seed.k)
 opts = ds.opts(flags=w.opts.flags | 8)
 mpg.mpg_sample_seeds(ds.h, ds.guide, ds.sampler, b.query, opts, b.seeds)
-names = ["MPG_ITEM_B0", "MPG_ITEM_GROW", "MPG_LOCAL_TRIALS", "MPG_BACKOFF_MAX"]
+names = ["MPG_ITEM_B0", "MPG_ITEM_GROW", "MPG_LOCAL_TRIALS", "MPG_BACKOFF_MAX", "MPG_ITEM_GROW_IDLE", "MPG_IDLE_DIV", "MPG_ITEM_B0_IDLE"]
 ref = None
 for s in settings:
     for n, v in zip(names, s.split(",")):
