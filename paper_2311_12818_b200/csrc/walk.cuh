@@ -287,7 +287,8 @@ __device__ __forceinline__ bool hard_publish(const WalkParams &P, int64_t w, uin
     unsigned int e = atomicAdd(&P.th->n_entries, 1u);
     if (e >= P.hard_cap) return false;
     const unsigned backlog = *(volatile unsigned *)&P.th->item_tail - *(volatile unsigned *)&P.th->item_head;
-    const uint32_t B = min((int)backlog < (int)P.idle_backlog ? P.item_b0_idle : P.item_b0, P.k_max - last);
+    const bool idle = (int)backlog < (int)P.idle_backlog && __ldcg(&P.th->queue) >= (unsigned long long)P.n;
+    const uint32_t B = min(idle ? P.item_b0_idle : P.item_b0, P.k_max - last);
     P.e_walk[e] = w;
     P.e_psurf[e] = psurf;
     P.e_pct[e] = (uint32_t)pk | (ptau << 4);
@@ -303,8 +304,9 @@ __device__ __forceinline__ bool hard_publish(const WalkParams &P, int64_t w, uin
 
 #ifdef MPG_TIMELINE
 // diagnostic build only (tools/timeline.py): per 65.5-us bucket of %globaltimer,
-// [warp iterations, tracing lanes, working lanes, waiting lanes]
-__device__ unsigned long long g_tl[1024 * 4];
+// [warp iterations, tracing, working, waiting, primary (trial 0), item lanes]
+#define TL_W 6
+__device__ unsigned long long g_tl[1024 * TL_W];
 __device__ unsigned g_tl_shift = 16;
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;
@@ -413,7 +415,7 @@ __global__ void __launch_bounds__(128, (KMAX <= 2 ? MPG_WALK_MINB2 : 2)) k_walk(
                 atomicAdd(&P.th->resolved, my_resolved);
                 my_resolved = 0;
             }
-            unsigned long long wd = ticket < (long long)P.item_cap
+            unsigned long long wd = ticket >= 0 && ticket < (long long)P.item_cap
                                         ? *(volatile unsigned long long *)(P.items + ticket) : ITEM_EMPTY;
             if (wd != ITEM_EMPTY) {
                 ticket = -1;
@@ -485,15 +487,14 @@ __global__ void __launch_bounds__(128, (KMAX <= 2 ? MPG_WALK_MINB2 : 2)) k_walk(
 
 #ifdef MPG_TIMELINE
         {
-            const unsigned tr = __ballot_sync(MPG_FULL, phase == PH_DEDUCE || phase == PH_REPROJ);
-            const unsigned wk = __ballot_sync(MPG_FULL, phase != PH_WAIT && phase != PH_IDLE);
-            const unsigned wt = __ballot_sync(MPG_FULL, phase == PH_WAIT);
+            const bool wk = phase != PH_WAIT && phase != PH_IDLE;
+            const unsigned c[5] = {__ballot_sync(MPG_FULL, phase == PH_DEDUCE || phase == PH_REPROJ || phase == PH_VIS),
+                                   __ballot_sync(MPG_FULL, wk), __ballot_sync(MPG_FULL, phase == PH_WAIT),
+                                   __ballot_sync(MPG_FULL, wk && trial == 0), __ballot_sync(MPG_FULL, wk && item_e >= 0)};
             if (lane == 0) {
                 const unsigned b = (unsigned)(gtimer() >> g_tl_shift) & 1023u;
-                atomicAdd(&g_tl[4 * b], 1ull);
-                atomicAdd(&g_tl[4 * b + 1], (unsigned long long)__popc(tr));
-                atomicAdd(&g_tl[4 * b + 2], (unsigned long long)__popc(wk));
-                atomicAdd(&g_tl[4 * b + 3], (unsigned long long)__popc(wt));
+                atomicAdd(&g_tl[TL_W * b], 1ull);
+                for (int j = 0; j < 5; j++) atomicAdd(&g_tl[TL_W * b + 1 + j], (unsigned long long)__popc(c[j]));
             }
         }
 #endif
@@ -668,7 +669,8 @@ __global__ void __launch_bounds__(128, (KMAX <= 2 ? MPG_WALK_MINB2 : 2)) k_walk(
                         } else {
                             const unsigned backlog = *(volatile unsigned *)&P.th->item_tail -
                                                      *(volatile unsigned *)&P.th->item_head;
-                            const uint32_t g = (int)backlog < (int)P.idle_backlog ? P.item_grow_idle : P.item_grow;
+                            const uint32_t g = (int)backlog < (int)P.idle_backlog && queue_drained(P, drained) ? P.item_grow_idle
+                                                                                             : P.item_grow;
                             const uint32_t B = min(__ldcg(P.e_batch + e) << g, P.k_max - issued);
                             P.e_batch[e] = B;
                             P.e_pending[e] = B;

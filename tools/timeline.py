@@ -32,7 +32,7 @@ b = mpg.Batch(w.xD, w.nD, w.spp, w.seed.k)
 opts = ds.opts(flags=w.opts.flags | 8)   # bench default: MPG_FLAG_SORT
 L = mpg.lib()
 fn = C.CDLL(TL).mpg_debug_timeline
-buf = (C.c_ulonglong * 4096)()
+buf = (C.c_ulonglong * 6144)()
 nh = (C.c_ulonglong * 256)()
 for rep in range(3):
     mpg.mpg_sample_seeds(ds.h, ds.guide, ds.sampler, b.query, opts, b.seeds)
@@ -45,7 +45,7 @@ for rep in range(3):
     torch.cuda.synchronize()
     fn(buf, shift, nh)
     ms = e0.elapsed_time(e1)
-a = np.frombuffer(buf, dtype=np.uint64).reshape(1024, 4).astype(np.float64)
+a = np.frombuffer(buf, dtype=np.uint64).reshape(1024, 6).astype(np.float64)
 nz = np.nonzero(a[:, 0])[0]
 # buckets wrap every 1024 x 2^shift ns: start after the largest empty gap
 gaps = np.diff(np.r_[nz, nz[0] + 1024])
@@ -58,12 +58,12 @@ bw = 2.0 ** shift / 1e6   # ms per bucket
 per = max(1, int(round(bin_ms / bw)))
 print(f"config {cfg}: k_walk {ms:.2f} ms, {rows[:, 0].sum():.0f} warp iterations, "
       f"trace lanes/iter {rows[:, 1].sum() / rows[:, 0].sum():.2f}")
-print(" t_ms   iters(M)  tracing  working  waiting")
+print("   t_ms iters(M)  tracing  working  waiting  primary    items")
 for i in range(0, len(rows), per):
     r = rows[i:i + per].sum(0)
     if r[0] == 0:
         continue
-    print(f"{i * bw:7.2f} {r[0] / 1e6:8.3f} {r[1] / r[0]:8.2f} {r[2] / r[0]:8.2f} {r[3] / r[0]:8.2f}")
+    print(f"{i * bw:7.2f} {r[0] / 1e6:8.3f} " + " ".join(f"{r[j] / r[0]:8.2f}" for j in range(1, 6)))
 h = np.frombuffer(nh, dtype=np.uint64).astype(np.float64)
 if h.sum():
     c = np.cumsum(h) / h.sum()
