@@ -368,6 +368,8 @@ def run_ours(args):
                            "order": ("primaries in walk order" if not opts.flags & 8 else
                                      "primaries in (receiver cell, seed direction) order, MPG_FLAG_SORT"),
                            "path": "wavefront" if opts.flags & 1 else "persistent kernel",
+                           "bvh": (f"{ds.info.bvh_width}-wide SAH, {ds.info.n_nodes} nodes, {ds.info.n_tri} triangles"
+                                   if ds.info.n_tri else "analytic surfaces only"),
                            "precision": ("fp32 scene/traversal; fp64 positions, residual, hit refinement" +
                                          ("; fp64 Jacobian/step (MPG_FLAG_NEWTON_F64)" if opts.flags & 4
                                           else "; fp32 Jacobian/step"))},

@@ -184,11 +184,15 @@ typedef struct {
 typedef struct {
     float extent;      /* bbox diagonal of surfaces + lights (R10) */
     int32_t n_surf, n_light, n_tri, n_nodes;
+    int32_t bvh_width; /* 2 (binary nodes) or 4 (collapsed 4-wide nodes) */
     size_t device_bytes;
 } mpg_scene_info;
 
 /* Build the device scene: copies all descriptors and mesh arrays (host), builds
- * a binned-SAH BVH over all mesh triangles (host, C++), uploads it.  Synchronous. */
+ * a binned-SAH BVH over all mesh triangles (host, C++), uploads it.  Synchronous.
+ * The binary tree is collapsed to 4-wide nodes for scenes of >= 65,536
+ * triangles (environment MPG_BVH_WIDTH=2|4 overrides); traversal results are
+ * identical, only the node visits differ. */
 mpg_status mpg_scene_create(const mpg_surface_desc *surfaces, int32_t n_surf, const mpg_light_desc *lights,
                             int32_t n_light, void *stream, mpg_scene **out);
 mpg_status mpg_scene_destroy(mpg_scene *scene);

@@ -152,29 +152,28 @@ template <typename T, int N, int M> __device__ __forceinline__ void rset2(T (&a)
 // 256-bit loads, LDG.E.ENL2.256, measured no faster on configs[1,2])
 #define TSTRIDE 3
 
-// BVH node layout.  MPG_BVH4 = 0 (default): binary SAH nodes, 4 float4 (64 B):
-// two child boxes + two child refs.  MPG_BVH4 = 1: 4-wide nodes collapsed from
-// the binary tree, 8 float4 (128 B) SoA: lo_x[4], hi_x[4], lo_y[4], hi_y[4],
-// lo_z[4], hi_z[4], child refs[4], pad; children sorted by entry distance.
-// Measured (ms/step, persistent kernel): configs[1] 67.4 -> 71.8, [2] 450 -> 472,
-// [3] 356 -> 299, [4] 460 -> 440 (half the node visits, but a costlier visit
-// and more spills at the 80-register cap) -- binary stays the default because
-// configs[1] is the headline workload.
+// BVH node layouts, chosen per scene at build time (DScene::bvh_w, template W of
+// the traversal).  W = 2: binary SAH nodes, 4 float4 (64 B): two child boxes +
+// two child refs.  W = 4: 4-wide nodes collapsed from the binary tree, 8 float4
+// (128 B) SoA: lo_x[4], hi_x[4], lo_y[4], hi_y[4], lo_z[4], hi_z[4], child
+// refs[4], pad; children sorted by entry distance.  Measured (k_walk ms, binary
+// -> 4-wide): configs[1] (5 k tris) 41.8 -> 43.6, [2] (522 k) 322 -> 322,
+// [3] (780 k) 283 -> 237, [4] 11.3 -> 11.1: half the dependent node fetches pay
+// off once the tree is deep; the scene build picks 4-wide from 65,536 triangles
+// (MPG_BVH_WIDTH=2|4 overrides).
 // Child ref: >= 0 node index, < 0 leaf ~(first_tri << 3 | count - 1),
 // 0x7fffffff empty slot (point box at 3e38: never entered).
-#ifndef MPG_BVH4
-#define MPG_BVH4 0
-#endif
-#define NODE_F4 (MPG_BVH4 ? 8 : 4)
-#define TRAV_STACK (MPG_BVH4 ? 96 : 64)
+#define NODE_F4(W) ((W) == 4 ? 8 : 4)
+#define TRAV_STACK(W) ((W) == 4 ? 96 : 64)
 
 // One node visit of the ordered traversal: returns the nearest child whose box
 // overlaps [tmin, tmax] (or pops the stack if none) and pushes the others
 // far-to-near.  Same slab arithmetic for both layouts.
+template <int W>
 __device__ __forceinline__ int bvh_visit(const float4 *nodes, int node, float3 o, float3 idir, float tmin,
                                          float tmax, int *stack, int &sp) {
-#if MPG_BVH4
-    const float4 *nd = nodes + NODE_F4 * node;
+  if (W == 4) {
+    const float4 *nd = nodes + NODE_F4(4) * node;
     const float4 lx = __ldg(nd), hx = __ldg(nd + 1), ly = __ldg(nd + 2), hy = __ldg(nd + 3), lz = __ldg(nd + 4),
                  hz = __ldg(nd + 5);
     const int4 ch = __ldg(reinterpret_cast<const int4 *>(nd + 6));
@@ -209,8 +208,8 @@ __device__ __forceinline__ int bvh_visit(const float4 *nodes, int node, float3 o
     if (t[2] != INF) stack[sp++] = c[2];
     if (t[1] != INF) stack[sp++] = c[1];
     return c[0];
-#else
-    const float4 *nd = nodes + NODE_F4 * node;
+  } else {
+    const float4 *nd = nodes + NODE_F4(2) * node;
     float4 a = __ldg(nd), b = __ldg(nd + 1), c = __ldg(nd + 2);
     int4 ch = __ldg(reinterpret_cast<const int4 *>(nd + 3));
     float tx0 = (a.x - o.x) * idir.x, tx1 = (a.w - o.x) * idir.x;
@@ -232,15 +231,16 @@ __device__ __forceinline__ int bvh_visit(const float4 *nodes, int node, float3 o
     if (h0) return ch.x;
     if (h1) return ch.y;
     return stack[--sp];
-#endif
+  }
 }
 
 struct DScene {
     int n_surf, n_light, n_tri, n_nodes;
+    int bvh_w;           // 2 or 4: node layout (see bvh_visit)
     float extent;
     DSurf surf[DS_MAX_SURF];
     DLight light[DS_MAX_LIGHT];
-    const float4 *nodes; // NODE_F4 float4 per node (see bvh_visit)
+    const float4 *nodes; // NODE_F4(bvh_w) float4 per node (see bvh_visit)
     const float4 *tpos;  // BVH order, TSTRIDE float4 per tri; v0.w = original tri id, v1.w = surf id, v2.w = specular flag
     const float4 *tnrm;  // BVH order, 3 float4 per tri: vertex shading normals
     const int4 *oidx;    // original order: vertex indices (w: BVH slot)
@@ -359,6 +359,7 @@ __device__ __forceinline__ bool quad_hit(float3 o, float3 d, float3 q0, float3 e
 #ifdef MPG_NH
 __device__ unsigned long long g_nh[256];   // diagnostic: closest-hit rays by node visits
 #endif
+template <int W>
 __device__ __forceinline__ bool trace(const DScene &S, float3 o, float3 d, float tmin, float tmax, bool spec_only,
                                       const bool ANY, Hit &h, LaneStats &st, int hint = -1) {   // callers count rays
 #ifdef MPG_NH
@@ -407,14 +408,14 @@ __device__ __forceinline__ bool trace(const DScene &S, float3 o, float3 d, float
                 bb0 = c0; bb1 = c1; bb2 = c2;
             }
         }
-        int stack[TRAV_STACK];
+        int stack[TRAV_STACK(W)];
         stack[0] = SENT;
         int sp = 1;
         int node = 0, leaf = NONE;
         while (node != SENT || leaf != NONE) {
             while (node >= 0 && node != SENT) {
                 st.nodes++;
-                node = bvh_visit(S.nodes, node, o, r.idir, tmin, best, stack, sp);
+                node = bvh_visit<W>(S.nodes, node, o, r.idir, tmin, best, stack, sp);
                 if (node < 0 && leaf == NONE) { // postpone the leaf, keep traversing
                     leaf = node;
                     node = stack[--sp];

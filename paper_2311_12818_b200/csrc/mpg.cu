@@ -335,6 +335,7 @@ extern "C" mpg_status mpg_scene_create(const mpg_surface_desc *surfaces, int32_t
                                 (hi[2] - lo[2]) * (hi[2] - lo[2]));
     // BVH
     std::vector<float4> nodes4, tpos, tnrm;
+    d.bvh_w = 2;
     if (d.n_tri > 0) {
         std::vector<BTri> bt(d.n_tri);
         for (int t = 0; t < d.n_tri; t++) {
@@ -361,7 +362,10 @@ extern "C" mpg_status mpg_scene_create(const mpg_surface_desc *surfaces, int32_t
             B.nodes.insert(B.nodes.begin(), nd);
         }
         if (B.max_depth > 60) { mpg_scene_destroy(s); return fail(MPG_ERR_UNSUPPORTED, "BVH too deep"); }
-#if MPG_BVH4
+        int width = d.n_tri >= 65536 ? 4 : 2;
+        if (const char *v = getenv("MPG_BVH_WIDTH")) width = atoi(v) == 4 ? 4 : 2;
+        d.bvh_w = width;
+        if (width == 4) {
         // collapse the binary SAH tree into a 4-wide one (children = grandchildren):
         // half the dependent node fetches per ray; 128-B SoA nodes (NODE_F4 float4)
         std::vector<float> w4;
@@ -385,11 +389,11 @@ extern "C" mpg_status mpg_scene_create(const mpg_surface_desc *surfaces, int32_t
                     cnt++;
                 }
             }
-            const int id = (int)(w4.size() / (4 * NODE_F4));
-            w4.resize(w4.size() + 4 * NODE_F4, 0.f);
+            const int id = (int)(w4.size() / (4 * NODE_F4(4)));
+            w4.resize(w4.size() + 4 * NODE_F4(4), 0.f);
             for (int j = 0; j < cnt; j++)
                 if (ref[j] >= 0) ref[j] = collapse(ref[j]);
-            float *o = w4.data() + (size_t)id * 4 * NODE_F4;
+            float *o = w4.data() + (size_t)id * 4 * NODE_F4(4);
             for (int j = 0; j < 4; j++) {
                 const bool on = j < cnt;
                 for (int a = 0; a < 3; a++) {
@@ -404,10 +408,10 @@ extern "C" mpg_status mpg_scene_create(const mpg_surface_desc *surfaces, int32_t
             return id;
         };
         collapse(0);
-        d.n_nodes = (int)(w4.size() / (4 * NODE_F4));
-        nodes4.resize((size_t)NODE_F4 * d.n_nodes);
+        d.n_nodes = (int)(w4.size() / (4 * NODE_F4(4)));
+        nodes4.resize((size_t)NODE_F4(4) * d.n_nodes);
         memcpy(nodes4.data(), w4.data(), w4.size() * sizeof(float));
-#else
+        } else {
         d.n_nodes = (int)B.nodes.size();
         nodes4.resize(4 * d.n_nodes);
         for (int i = 0; i < d.n_nodes; i++) {
@@ -418,7 +422,7 @@ extern "C" mpg_status mpg_scene_create(const mpg_surface_desc *surfaces, int32_t
             int4 ch = make_int4(nd.c0, nd.c1, 0, 0);
             memcpy(&nodes4[4 * i + 3], &ch, sizeof(int4));
         }
-#endif
+        }
         tpos.assign((size_t)TSTRIDE * d.n_tri, make_float4(0.f, 0.f, 0.f, 0.f));
         tnrm.resize(3 * d.n_tri);
         for (int j = 0; j < d.n_tri; j++) {
@@ -455,6 +459,7 @@ extern "C" mpg_status mpg_scene_get_info(const mpg_scene *scene, mpg_scene_info 
     info->n_light = scene->d.n_light;
     info->n_tri = scene->d.n_tri;
     info->n_nodes = scene->d.n_nodes;
+    info->bvh_width = scene->d.bvh_w;
     info->device_bytes = scene->bytes;
     return MPG_OK;
 }
@@ -462,13 +467,14 @@ extern "C" mpg_status mpg_scene_get_info(const mpg_scene *scene, mpg_scene_info 
 // ----------------------------------------------------------------------------
 // debug trace kernel
 // ----------------------------------------------------------------------------
+template <int W>
 __global__ void k_trace(const DScene S, const float4 *orig, const float4 *dir, int64_t n, float tmin, int spec_only,
                         float *t, int *prim, int *surf) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         LaneStats ls = {0, 0, 0};
         Hit h;
         ls.rays++;
-        bool ok = trace(S, xyz(orig[i]), nrmz(xyz(dir[i])), tmin, 3.0e38f, spec_only != 0, false, h, ls);
+        bool ok = trace<W>(S, xyz(orig[i]), nrmz(xyz(dir[i])), tmin, 3.0e38f, spec_only != 0, false, h, ls);
         t[i] = ok ? h.t : -1.0f;
         prim[i] = ok && h.prim >= 0 ? __float_as_int(S.tpos[TSTRIDE * h.prim].w) : -1;
         surf[i] = ok ? h.surf : -1;
@@ -482,8 +488,12 @@ extern "C" mpg_status mpg_trace_rays(const mpg_scene *scene, const float *orig, 
     if (n == 0) return MPG_OK;
     int blocks = (int)std::min<int64_t>((n + 127) / 128, 148 * 16);
     COUNT_LAUNCH(1);
-    k_trace<<<blocks, 128, 0, as_stream(stream)>>>(scene->d, (const float4 *)orig, (const float4 *)dir, n, tmin,
-                                                   spec_only, t, prim, surf);
+    if (scene->d.bvh_w == 4)
+        k_trace<4><<<blocks, 128, 0, as_stream(stream)>>>(scene->d, (const float4 *)orig, (const float4 *)dir, n, tmin,
+                                                          spec_only, t, prim, surf);
+    else
+        k_trace<2><<<blocks, 128, 0, as_stream(stream)>>>(scene->d, (const float4 *)orig, (const float4 *)dir, n, tmin,
+                                                          spec_only, t, prim, surf);
     CUDA_TRY(cudaPeekAtLastError());
     return MPG_OK;
 }
@@ -1071,13 +1081,12 @@ extern "C" size_t mpg_walk_workspace_size(int64_t n, const mpg_sampler_desc *sam
 template <int KMAX, typename R>
 static mpg_status launch_walk(const DScene &S, const SeedCtx &g, WalkParams P, cudaStream_t st, void *ws,
                               bool sort) {
-    static int occ = 0;
+    const bool wide = S.bvh_w == 4;
+    static int occ2 = 0, occ4 = 0;
+    int &occ = wide ? occ4 : occ2;
     if (!occ) {
-#ifdef MPG_CARVEOUT
-        // unified L1/shared split: this kernel uses 152 B of shared memory; prefer L1
-        CUDA_TRY(cudaFuncSetAttribute(k_walk<KMAX, R>, cudaFuncAttributePreferredSharedMemoryCarveout, MPG_CARVEOUT));
-#endif
-        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_walk<KMAX, R>, 128, 0));
+        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, wide ? k_walk<KMAX, R, 4> : k_walk<KMAX, R, 2>,
+                                                               128, 0));
         if (occ <= 0) occ = 1;
     }
     MKLayout L = mk_layout(P.n);
@@ -1133,7 +1142,8 @@ static mpg_status launch_walk(const DScene &S, const SeedCtx &g, WalkParams P, c
         P.idle_backlog = (uint32_t)(blocks * 128 / div);
     }
     COUNT_LAUNCH(1);
-    k_walk<KMAX, R><<<blocks, 128, 0, st>>>(S, g, P);
+    if (wide) k_walk<KMAX, R, 4><<<blocks, 128, 0, st>>>(S, g, P);
+    else k_walk<KMAX, R, 2><<<blocks, 128, 0, st>>>(S, g, P);
     CUDA_TRY(cudaPeekAtLastError());
     return MPG_OK;
 }
@@ -1189,7 +1199,8 @@ static mpg_status launch_wavefront(const DScene &S, const SeedCtx &g, const Walk
 
     static int occ_t = 0, occ_u = 0;
     if (!occ_t) {
-        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_t, k_wf_rays, 128, 0));
+        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_t, S.bvh_w == 4 ? k_wf_rays<4> : k_wf_rays<2>,
+                                                               128, 0));
         CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_u, k_wf_update<KMAX, R>, 128, 0));
         occ_t = std::max(occ_t, 1); occ_u = std::max(occ_u, 1);
     }
@@ -1212,7 +1223,8 @@ static mpg_status launch_wavefront(const DScene &S, const SeedCtx &g, const Walk
         for (int wave = 0; more; wave++) {
             for (int i = 0; i < nk; i++) {
                 COUNT_LAUNCH(1);
-                k_wf_rays<<<gt, 128, 0, st>>>(S, P, i, ro[i], rd[i]);
+                if (S.bvh_w == 4) k_wf_rays<4><<<gt, 128, 0, st>>>(S, P, i, ro[i], rd[i]);
+                else k_wf_rays<2><<<gt, 128, 0, st>>>(S, P, i, ro[i], rd[i]);
                 COUNT_LAUNCH(1);
                 k_wf_post<<<i == 0 ? gp0 : gp, 128, 0, st>>>(S, P, i, rd[i], ro[i + 1], rd[i + 1]);
             }
@@ -1277,7 +1289,7 @@ static mpg_status launch_wavefront(const DScene &S, const SeedCtx &g, const Walk
             argr[i][0] = &Sv; argr[i][1] = &Pv; argr[i][2] = &subs[i]; argr[i][3] = &ro[i]; argr[i][4] = &rd[i];
             argp[i][0] = &Sv; argp[i][1] = &Pv; argp[i][2] = &subs[i]; argp[i][3] = &rd[i];
             argp[i][4] = &ro[i + 1]; argp[i][5] = &rd[i + 1];
-            CUDA_TRY(add((void *)k_wf_rays, gt, 128, argr[i]));
+            CUDA_TRY(add(S.bvh_w == 4 ? (void *)k_wf_rays<4> : (void *)k_wf_rays<2>, gt, 128, argr[i]));
             CUDA_TRY(add((void *)k_wf_post, i == 0 ? gp0 : gp, 128, argp[i]));
         }
         CUDA_TRY(add((void *)k_wf_update<KMAX, R>, gu, 128, args3));

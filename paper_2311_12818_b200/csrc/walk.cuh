@@ -179,7 +179,7 @@ enum { TR_REPROJ = 0, TR_DEDUCE = 1, TR_VIS = 2 };
 // One traversal call site serves all three modes, so lanes tracing visibility
 // traverse together with warp-mates that reproject (no separate low-occupancy
 // visibility traversal).
-template <int KMAX>
+template <int KMAX, int W>
 __device__ __forceinline__ int trace_chain(const DScene &S, int mode, int k, uint32_t bits, bool learned,
                                            float3 xD, float3 xL, float3 tgt, const double3 (&q)[KMAX],
                                            const double3 (&x)[KMAX], const int (&hint)[KMAX],
@@ -227,7 +227,7 @@ __device__ __forceinline__ int trace_chain(const DScene &S, int mode, int k, uin
         // k_walk -17 % configs[1], -7 % [2], -13 % [3] against a register counter)
         atomicAdd(s_rays, 1u);
         Hit h;
-        const bool hit = trace(S, of, d, eps, tmax, !vis, vis, h, st, mode == TR_REPROJ ? rget(hint, i) : -1);
+        const bool hit = trace<W>(S, of, d, eps, tmax, !vis, vis, h, st, mode == TR_REPROJ ? rget(hint, i) : -1);
         if (vis) {
             if (hit) return 5;
             continue;
@@ -315,7 +315,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
 }
 #endif
 
-template <int KMAX, typename R>
+template <int KMAX, typename R, int W>
 __global__ void __launch_bounds__(128, (KMAX <= 2 ? MPG_WALK_MINB2 : 2)) k_walk(const DScene S, const SeedCtx g, const WalkParams P) {
     __shared__ unsigned long long s_stats[SS_N];
     __shared__ unsigned s_rays[128];   // chain rays per thread (see trace_chain)
@@ -506,7 +506,7 @@ __global__ void __launch_bounds__(128, (KMAX <= 2 ? MPG_WALK_MINB2 : 2)) k_walk(
             for (int i = 0; i < KMAX; i++) sreq |= (uint32_t)(surf[i] & 15) << (4 * i);
             uint32_t tres = tau;
             const int mode = ded ? TR_DEDUCE : (phase == PH_VIS ? TR_VIS : TR_REPROJ);
-            int why = trace_chain<KMAX>(S, mode, k, bits, learned, xD, xL, tgt, q, x, prim, sreq, P.ray_eps, y, yp, ys, ls,
+            int why = trace_chain<KMAX, W>(S, mode, k, bits, learned, xD, xL, tgt, q, x, prim, sreq, P.ray_eps, y, yp, ys, ls,
                                         tres, &s_rays[threadIdx.x]);
             bool ok = why == 0;
             if (mode == TR_VIS) {

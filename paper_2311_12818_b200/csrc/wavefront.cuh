@@ -243,6 +243,7 @@ __global__ void k_wf_init(const DScene S, const SeedCtx g, const WFParams P) {
 // (visibility) -- the operator r(x, w) of Eq. 6 and V of Eq. 2.
 // Same arithmetic as trace<> in device_common.cuh.
 // --------------------------------------------------------------------------
+template <int W>
 __global__ void __launch_bounds__(128, WF_TRACE_MINB) k_wf_rays(const DScene S, const WFParams P, int sub,
                                                                 const float4 *ro_s, const float4 *rd_s) {
     __shared__ unsigned long long s_acc[3];
@@ -274,7 +275,7 @@ __global__ void __launch_bounds__(128, WF_TRACE_MINB) k_wf_rays(const DScene S, 
     r.Sx = r.Sy = r.Sz = 0.f;
     float tmax = 0.f;
     int node = SENT, leaf = NONE, sp = 0;
-    int stack[TRAV_STACK];
+    int stack[TRAV_STACK(W)];
     int bprim = -2, bsurf = -1;
     float bb0 = 0.f, bb1 = 0.f, bb2 = 0.f;   // barycentrics, or the analytic hit point
     LaneStats ls = {0u, 0u, 0u};
@@ -347,7 +348,7 @@ __global__ void __launch_bounds__(128, WF_TRACE_MINB) k_wf_rays(const DScene S, 
             while (node != SENT || leaf != NONE) {
                 while (node >= 0 && node != SENT) {
                     ls.nodes++;
-                    node = bvh_visit(S.nodes, node, o, r.idir, eps, tmax, stack, sp);
+                    node = bvh_visit<W>(S.nodes, node, o, r.idir, eps, tmax, stack, sp);
                     if (node < 0 && leaf == NONE) { // postpone the leaf, keep traversing
                         leaf = node;
                         node = stack[--sp];

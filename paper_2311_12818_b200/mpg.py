@@ -81,7 +81,7 @@ class mpg_walk_stats(C.Structure):
 
 class mpg_scene_info(C.Structure):
     _fields_ = [("extent", C.c_float), ("n_surf", C.c_int32), ("n_light", C.c_int32), ("n_tri", C.c_int32),
-                ("n_nodes", C.c_int32), ("device_bytes", C.c_size_t)]
+                ("n_nodes", C.c_int32), ("bvh_width", C.c_int32), ("device_bytes", C.c_size_t)]
 
 
 EXPORTS = ["mpg_scene_create", "mpg_scene_destroy", "mpg_scene_get_info", "mpg_trace_rays", "mpg_guide_create",
