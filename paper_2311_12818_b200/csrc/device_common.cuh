@@ -170,7 +170,11 @@ template <typename T, int N, int M> __device__ __forceinline__ void rset2(T (&a)
 // overlaps [tmin, tmax] (or pops the stack if none) and pushes the others
 // far-to-near.  Same slab arithmetic for both layouts.
 template <int W>
-__device__ __forceinline__ int bvh_visit(const float4 *nodes, int node, float3 o, float3 idir, float tmin,
+// Slab distances as one FFMA per plane: t = b * idir - oi with oi = o * idir
+// precomputed per ray (Aila & Laine 2009).  The rounding of oi shifts a plane
+// by ~ulp(|o|); node boxes are inflated by extent * 2^-20 at build time, so the
+// test stays conservative (a box the ray truly enters is never culled).
+__device__ __forceinline__ int bvh_visit(const float4 *nodes, int node, float3 oi, float3 idir, float tmin,
                                          float tmax, int *stack, int &sp) {
   if (W == 4) {
     const float4 *nd = nodes + NODE_F4(4) * node;
@@ -182,9 +186,9 @@ __device__ __forceinline__ int bvh_visit(const float4 *nodes, int node, float3 o
     int c[4] = {ch.x, ch.y, ch.z, ch.w};
 #define MPG_SLAB(J, LX, HX, LY, HY, LZ, HZ)                                                         \
     {                                                                                                \
-        float x0 = (LX - o.x) * idir.x, x1 = (HX - o.x) * idir.x;                                    \
-        float y0 = (LY - o.y) * idir.y, y1 = (HY - o.y) * idir.y;                                    \
-        float z0 = (LZ - o.z) * idir.z, z1 = (HZ - o.z) * idir.z;                                    \
+        float x0 = fmaf(LX, idir.x, -oi.x), x1 = fmaf(HX, idir.x, -oi.x);                            \
+        float y0 = fmaf(LY, idir.y, -oi.y), y1 = fmaf(HY, idir.y, -oi.y);                            \
+        float z0 = fmaf(LZ, idir.z, -oi.z), z1 = fmaf(HZ, idir.z, -oi.z);                            \
         float tn = fmaxf(fmaxf(fminf(x0, x1), fminf(y0, y1)), fmaxf(fminf(z0, z1), tmin));           \
         float tf = fminf(fminf(fmaxf(x0, x1), fmaxf(y0, y1)), fminf(fmaxf(z0, z1), tmax));           \
         t[J] = tn <= tf ? tn : INF;                                                                  \
@@ -212,14 +216,14 @@ __device__ __forceinline__ int bvh_visit(const float4 *nodes, int node, float3 o
     const float4 *nd = nodes + NODE_F4(2) * node;
     float4 a = __ldg(nd), b = __ldg(nd + 1), c = __ldg(nd + 2);
     int4 ch = __ldg(reinterpret_cast<const int4 *>(nd + 3));
-    float tx0 = (a.x - o.x) * idir.x, tx1 = (a.w - o.x) * idir.x;
-    float ty0 = (a.y - o.y) * idir.y, ty1 = (b.x - o.y) * idir.y;
-    float tz0 = (a.z - o.z) * idir.z, tz1 = (b.y - o.z) * idir.z;
+    float tx0 = fmaf(a.x, idir.x, -oi.x), tx1 = fmaf(a.w, idir.x, -oi.x);
+    float ty0 = fmaf(a.y, idir.y, -oi.y), ty1 = fmaf(b.x, idir.y, -oi.y);
+    float tz0 = fmaf(a.z, idir.z, -oi.z), tz1 = fmaf(b.y, idir.z, -oi.z);
     float n0 = fmaxf(fmaxf(fminf(tx0, tx1), fminf(ty0, ty1)), fmaxf(fminf(tz0, tz1), tmin));
     float f0 = fminf(fminf(fmaxf(tx0, tx1), fmaxf(ty0, ty1)), fminf(fmaxf(tz0, tz1), tmax));
-    float sx0 = (b.z - o.x) * idir.x, sx1 = (c.y - o.x) * idir.x;
-    float sy0 = (b.w - o.y) * idir.y, sy1 = (c.z - o.y) * idir.y;
-    float sz0 = (c.x - o.z) * idir.z, sz1 = (c.w - o.z) * idir.z;
+    float sx0 = fmaf(b.z, idir.x, -oi.x), sx1 = fmaf(c.y, idir.x, -oi.x);
+    float sy0 = fmaf(b.w, idir.y, -oi.y), sy1 = fmaf(c.z, idir.y, -oi.y);
+    float sz0 = fmaf(c.x, idir.z, -oi.z), sz1 = fmaf(c.w, idir.z, -oi.z);
     float n1 = fmaxf(fmaxf(fminf(sx0, sx1), fminf(sy0, sy1)), fmaxf(fminf(sz0, sz1), tmin));
     float f1 = fminf(fminf(fmaxf(sx0, sx1), fmaxf(sy0, sy1)), fminf(fmaxf(sz0, sz1), tmax));
     bool h0 = n0 <= f0, h1 = n1 <= f1;
@@ -408,6 +412,7 @@ __device__ __forceinline__ bool trace(const DScene &S, float3 o, float3 d, float
                 bb0 = c0; bb1 = c1; bb2 = c2;
             }
         }
+        const float3 oi = f3(o.x * r.idir.x, o.y * r.idir.y, o.z * r.idir.z);
         int stack[TRAV_STACK(W)];
         stack[0] = SENT;
         int sp = 1;
@@ -415,7 +420,7 @@ __device__ __forceinline__ bool trace(const DScene &S, float3 o, float3 d, float
         while (node != SENT || leaf != NONE) {
             while (node >= 0 && node != SENT) {
                 st.nodes++;
-                node = bvh_visit<W>(S.nodes, node, o, r.idir, tmin, best, stack, sp);
+                node = bvh_visit<W>(S.nodes, node, oi, r.idir, tmin, best, stack, sp);
                 if (node < 0 && leaf == NONE) { // postpone the leaf, keep traversing
                     leaf = node;
                     node = stack[--sp];

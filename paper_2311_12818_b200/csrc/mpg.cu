@@ -362,6 +362,15 @@ extern "C" mpg_status mpg_scene_create(const mpg_surface_desc *surfaces, int32_t
             B.nodes.insert(B.nodes.begin(), nd);
         }
         if (B.max_depth > 60) { mpg_scene_destroy(s); return fail(MPG_ERR_UNSUPPORTED, "BVH too deep"); }
+        {   // inflate child boxes by extent * 2^-20: keeps the FFMA slab test conservative (bvh_visit)
+            const float e = d.extent * (1.0f / 1048576.0f);
+            for (BNode &nd : B.nodes)
+                for (int c = 0; c < 2; c++)
+                    for (int a = 0; a < 3; a++) {
+                        nd.b[6 * c + a] -= e;
+                        nd.b[6 * c + 3 + a] += e;
+                    }
+        }
         int width = d.n_tri >= 65536 ? 4 : 2;
         if (const char *v = getenv("MPG_BVH_WIDTH")) width = atoi(v) == 4 ? 4 : 2;
         d.bvh_w = width;
@@ -1138,8 +1147,8 @@ static mpg_status launch_walk(const DScene &S, const SeedCtx &g, WalkParams P, c
     int blocks = (int)std::min<int64_t>(want, (int64_t)num_sms() * occ);
     {
         int div = 8;   // idle: fewer unclaimed items than 1/div of the lanes
-        if (const char *v = getenv("MPG_IDLE_DIV")) div = std::max(1, atoi(v));
-        P.idle_backlog = (uint32_t)(blocks * 128 / div);
+        if (const char *v = getenv("MPG_IDLE_DIV")) div = std::max(0, atoi(v));
+        P.idle_backlog = div ? (uint32_t)(blocks * 128 / div) : 0x7fffffffu;   // 0: any backlog
     }
     COUNT_LAUNCH(1);
     if (wide) k_walk<KMAX, R, 4><<<blocks, 128, 0, st>>>(S, g, P);

@@ -345,10 +345,11 @@ __global__ void __launch_bounds__(128, WF_TRACE_MINB) k_wf_rays(const DScene S, 
         if (rid >= 0) {
             const bool any = (meta & WF_ANY) != 0;
             const float3 o = r.o;
+            const float3 oi = f3(o.x * r.idir.x, o.y * r.idir.y, o.z * r.idir.z);
             while (node != SENT || leaf != NONE) {
                 while (node >= 0 && node != SENT) {
                     ls.nodes++;
-                    node = bvh_visit<W>(S.nodes, node, o, r.idir, eps, tmax, stack, sp);
+                    node = bvh_visit<W>(S.nodes, node, oi, r.idir, eps, tmax, stack, sp);
                     if (node < 0 && leaf == NONE) { // postpone the leaf, keep traversing
                         leaf = node;
                         node = stack[--sp];
