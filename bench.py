@@ -218,9 +218,15 @@ def run_ours(args):
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)   # > 126 MB L2
 
 
+    # configs[4] on N ranks: the guide histogram is summed over ranks before every
+    # rebuild (the method's one exchange step); no-op on one rank
+    gsz = ds.info_guide_size() if progressive else 0
+    hbuf = torch.empty(max(gsz, 1), dtype=torch.float32, device=dev)
+    exchange = (lambda d: D.exchange_guide(d, hbuf)) if (progressive and world > 1) else None
+
     def step():
         if progressive:
-            mpg.run_progressive(ds, b, opts, iterations=iters)
+            mpg.run_progressive(ds, b, opts, iterations=iters, exchange=exchange)
         else:
             mpg.run_step(ds, b, opts, accumulate=guided)
 
@@ -263,6 +269,8 @@ def run_ours(args):
             if guided:
                 mpg.mpg_guide_accumulate(ds.guide, b.query, b.out, b.n)
             if progressive:
+                if exchange is not None:
+                    exchange(ds)
                 mpg.mpg_guide_rebuild(ds.guide)
             ev5[4].record(stream)
             part_ev.append(ev5)

@@ -219,6 +219,12 @@ mpg_status mpg_guide_rebuild(mpg_guide *guide, void *stream);
 /* copies: histogram -> energy (device [cells][n_types][bins] float); tables -> prefix (domain 0:
  * device [cells][bins] u64).  Either may be NULL. */
 mpg_status mpg_guide_download(const mpg_guide *guide, float *energy, uint64_t *prefix, void *stream);
+/* Overwrite the accumulation histogram with `energy` (device [cells][n_types][bins] float), leaving
+ * the sampling tables untouched: the exchange step of a multi-process progressive loop
+ * -- accumulate -> download -> all-reduce(sum) over ranks -> set_histogram ->
+ * rebuild, so every rank fits the next guide from the samples of all ranks (the
+ * samples of the last iteration).  Asynchronous on `stream`; energy must not alias it. */
+mpg_status mpg_guide_set_histogram(mpg_guide *guide, const float *energy, void *stream);
 /* domain 1 tables: n_prefix [cells][6] u64, type_prefix [cells][126] u64, dir_prefix [cells][126][bins] u32. */
 mpg_status mpg_guide_download_dir_tables(const mpg_guide *guide, uint64_t *n_prefix, uint64_t *type_prefix,
                                          uint32_t *dir_prefix, void *stream);

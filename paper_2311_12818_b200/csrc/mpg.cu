@@ -852,6 +852,13 @@ extern "C" mpg_status mpg_guide_download(const mpg_guide *g, float *energy, uint
     return MPG_OK;
 }
 
+extern "C" mpg_status mpg_guide_set_histogram(mpg_guide *g, const float *energy, void *stream) {
+    ARG_CHECK(g && energy, "NULL argument");
+    size_t ne = (size_t)g->n_cells * g->n_types * g->n_bins;
+    CUDA_TRY(cudaMemcpyAsync(g->hist, energy, ne * sizeof(float), cudaMemcpyDeviceToDevice, as_stream(stream)));
+    return MPG_OK;
+}
+
 extern "C" mpg_status mpg_guide_download_dir_tables(const mpg_guide *g, uint64_t *n_prefix, uint64_t *type_prefix,
                                                     uint32_t *dir_prefix, void *stream) {
     ARG_CHECK(g && g->desc.domain == 1, "needs a typed direction guide");

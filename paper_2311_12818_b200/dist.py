@@ -5,9 +5,13 @@ its own batch with walk ids [base + r*n, base + (r+1)*n) -- every random number
 of a walk is drawn from its walk id (Philox counter, R13), so ranks never share
 a draw and no data-path collective is needed ("scaling": "weak").  The only
 cross-rank operations are measurement (max-over-ranks device time, summed
-counts) and, for a render that spreads one receiver set over ranks, the
+counts), for a render that spreads one receiver set over ranks, the
 combination of per-rank estimates (Eq. 3 is a mean over walks, so the global
-estimate is the walk-count-weighted mean of the rank means).
+estimate is the walk-count-weighted mean of the rank means), and the one
+exchange the method itself has: in the progressive loop (configs[4]) the guide
+is fitted from the samples of the last iteration (P:426 footnote) --
+of all ranks -- so the accumulated histograms are summed over ranks before
+every rebuild; every rank then samples from the same guide.
 
 torch.distributed carries these (NCCL on the GPU box, gloo in the CPU tests).
 """
@@ -43,3 +47,23 @@ def combine_estimates(mean: torch.Tensor, spp: int) -> torch.Tensor:
     dist.all_reduce(num, op=dist.ReduceOp.SUM)
     dist.all_reduce(den, op=dist.ReduceOp.SUM)
     return (num / den).to(mean.dtype)
+
+
+def allreduce_histogram(hist: torch.Tensor) -> torch.Tensor:
+    """Sum a guide histogram over ranks in place (identity on one process)."""
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+        dist.all_reduce(hist, op=dist.ReduceOp.SUM)
+    return hist
+
+
+def exchange_guide(ds, buf: torch.Tensor, stream=None):
+    """Exchange step of the multi-process progressive loop (mpg.run_progressive's
+    `exchange`): this rank's accumulated histogram -> buf (device, cells*types*bins
+    float32) -> sum over ranks (NCCL over NVLink on the GPU box) -> back into the
+    guide, before mpg_guide_rebuild."""
+    from . import mpg
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return
+    mpg.mpg_guide_download(ds.guide, buf, None, stream)
+    allreduce_histogram(buf)
+    mpg.mpg_guide_set_histogram(ds.guide, buf, stream)

@@ -85,6 +85,7 @@ class mpg_scene_info(C.Structure):
 
 
 EXPORTS = ["mpg_scene_create", "mpg_scene_destroy", "mpg_scene_get_info", "mpg_trace_rays", "mpg_guide_create",
+           "mpg_guide_set_histogram",
            "mpg_guide_destroy", "mpg_guide_upload", "mpg_guide_reset", "mpg_guide_accumulate", "mpg_guide_rebuild",
            "mpg_guide_download", "mpg_guide_download_dir_tables", "mpg_sample_seeds", "mpg_walk_workspace_size", "mpg_manifold_walk", "mpg_estimate",
            "mpg_debug_trace", "mpg_last_error", "mpg_version", "mpg_kernel_launches"]
@@ -114,6 +115,7 @@ def lib():
             "mpg_guide_accumulate": (st, [P, C.POINTER(mpg_query), C.POINTER(mpg_walk_buf), C.c_int64, P]),
             "mpg_guide_rebuild": (st, [P, P]),
             "mpg_guide_download": (st, [P, P, P, P]),
+            "mpg_guide_set_histogram": (st, [P, P, P]),
             "mpg_guide_download_dir_tables": (st, [P, P, P, P, P]),
             "mpg_sample_seeds": (st, [P, P, C.POINTER(mpg_sampler_desc), C.POINTER(mpg_query),
                                       C.POINTER(mpg_walk_opts), C.POINTER(mpg_seed_buf), P]),
@@ -207,6 +209,10 @@ def mpg_guide_rebuild(h, stream=None):
 
 def mpg_guide_download(h, energy=None, prefix=None, stream=None):
     _check(lib().mpg_guide_download(h, _ptr(energy), _ptr(prefix), _stream_ptr(stream)), "mpg_guide_download")
+
+
+def mpg_guide_set_histogram(h, energy, stream=None):
+    _check(lib().mpg_guide_set_histogram(h, _ptr(energy), _stream_ptr(stream)), "mpg_guide_set_histogram")
 
 
 def mpg_guide_download_dir_tables(h, n_prefix=None, type_prefix=None, dir_prefix=None, stream=None):
@@ -310,6 +316,13 @@ class DeviceScene:
         mpg_guide_upload(self.guide, e, stream)
         torch.cuda.synchronize()
 
+    def info_guide_size(self) -> int:
+        """Floats in the guide histogram ([cells][types][bins]); 0 without a guide."""
+        if self.guide is None:
+            return 0
+        g = self.guide_desc
+        return int(g.cells_x * g.cells_y * max(1, g.n_types) * g.bins_x * g.bins_y)
+
     def opts(self, **over) -> mpg_walk_opts:
         o = self.w.opts
         d = dict(max_iters=o.max_iters, tol=o.tol, beta0=o.beta0, trials=o.trials, k_max=o.k_max,
@@ -398,18 +411,23 @@ class Batch:
 
 
 def run_progressive(ds: DeviceScene, b: Batch, opts: mpg_walk_opts, iterations: int = 8, stream=None,
-                    on_iteration=None):
+                    on_iteration=None, exchange=None, id_stride=None):
     """configs[4] (R22): guide reset (learned branch absent) at iteration 0, then per
-    iteration: seeds -> walk (+trials) -> estimator -> accumulate -> rebuild tables
-    from this iteration only (P:426 footnote).  Iteration it uses
-    walk_id_base = base + it*n so every iteration draws fresh random numbers."""
+    iteration: seeds -> walk (+trials) -> estimator -> accumulate [-> exchange] ->
+    rebuild tables from this iteration only (P:426 footnote).  Iteration it
+    uses walk_id_base = base + it*id_stride (default b.n) so every iteration draws
+    fresh random numbers.  `exchange(ds)` (multi-process runs, dist.exchange_guide)
+    replaces this rank's histogram by the sum over ranks before the rebuild."""
     mpg_guide_reset(ds.guide, stream)
     base = opts.walk_id_base
+    stride = b.n if id_stride is None else id_stride
     for it in range(iterations):
-        opts.walk_id_base = base + it * b.n
+        opts.walk_id_base = base + it * stride
         run_step(ds, b, opts, stream, estimate=True, accumulate=True)
         if on_iteration is not None:
             on_iteration(it)
+        if exchange is not None:
+            exchange(ds)
         mpg_guide_rebuild(ds.guide, stream)
     opts.walk_id_base = base
 

@@ -81,3 +81,66 @@ def test_single_process_is_identity():
     assert torch.equal(D.combine_estimates(m, 4), m)
     assert D.reduce_timing(3.5, [1, 2]) == (3.5, [1.0, 2.0])
     assert D.walk_id_base(3, 100, base=7) == 307
+
+
+# ---- configs[4] progressive loop on 2 ranks: the guide exchange ----
+def _cfg4_small():
+    return W.config4(n_side=6, grid_n=32)
+
+
+def _rank_hist(rank, w, s):
+    """Oracle walks of this rank's partition of iteration 0 (guide reset) and
+    their typed direction histogram (Eq. 9 accumulation, R22)."""
+    from paper_2311_12818_b200 import dist as D
+    base = D.walk_id_base(rank, w.n_walks)
+    o = s.walks(np.arange(w.n_walks), s.opts(walk_id_base=base))
+    return s.accumulate_dir(o["status"], o["w"], o["pos"][:, 0], o["k"], o["tau"])
+
+
+def _worker_guide(rank, world, port, out):
+    import hashlib
+    import torch
+    import torch.distributed as dist
+    from oracle import oracle as O
+    from paper_2311_12818_b200 import dist as D
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    w = _cfg4_small()
+    s = O.OracleScene(w)
+    s.set_dir_hist(np.zeros((256, 126, 1024), np.float32))          # reset: learned branch absent
+    h = torch.from_numpy(_rank_hist(rank, w, s))
+    D.allreduce_histogram(h)                                          # the exchange step
+    npf, tpf, dpf = O.guide_dir_tables(h.numpy())                     # every rank rebuilds from the sum
+    dig = hashlib.sha256(npf.tobytes() + tpf.tobytes() + dpf.tobytes()).hexdigest()
+    digs = [None] * world
+    dist.all_gather_object(digs, dig)
+    if rank == 0:
+        np.save(out, h.numpy())
+        json.dump({"digests": digs}, open(out + ".json", "w"))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_rank_progressive_guide_exchange(tmp_path):
+    """Both ranks end the iteration with the same guide, fitted from the samples of
+    both partitions: the summed histogram equals one process accumulating all
+    walks, and the tables every rank rebuilds from it are identical."""
+    from oracle import oracle as O
+    out = str(tmp_path / "h.npy")
+    mp.spawn(_worker_guide, args=(2, _free_port(), out), nprocs=2, join=True)
+    h = np.load(out)
+    digs = json.load(open(out + ".json"))["digests"]
+    assert digs[0] == digs[1]
+    w = _cfg4_small()
+    s = O.OracleScene(w)
+    s.set_dir_hist(np.zeros((256, 126, 1024), np.float32))
+    ref = sum(_rank_hist(k, w, s) for k in range(2))
+    assert h.sum() > 0 and np.allclose(h, ref, rtol=1e-12, atol=0)
+    # each rank alone would have learned from half the samples: a different guide
+    assert not np.allclose(h, _rank_hist(0, w, s))
+
+
+def test_allreduce_histogram_single_process_identity():
+    import torch
+    from paper_2311_12818_b200 import dist as D
+    h = torch.arange(6, dtype=torch.float32)
+    assert torch.equal(D.allreduce_histogram(h.clone()), h)

@@ -9,8 +9,8 @@ cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 2
 w = W.CONFIGS[cfg]()
 ds = mpg.DeviceScene(w)
 b = mpg.Batch(w.xD, w.nD, w.spp, w.seed.k)
-for trials, kmax in [(0, 1), (1, 4), (1, 8), (1, 32), (1, 1024)]:
-    opts = ds.opts(trials=trials, k_max=kmax)
+for trials, kmax in [(0, 1), (1, 4), (1, 8), (1, 32), (1, 128), (1, 1024)]:
+    opts = ds.opts(trials=trials, k_max=kmax, flags=w.opts.flags | 8)
     mpg.mpg_sample_seeds(ds.h, ds.guide, ds.sampler, b.query, opts, b.seeds)
     ts = []
     for rep in range(4):
