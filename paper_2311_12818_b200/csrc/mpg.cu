@@ -1017,8 +1017,11 @@ static MKLayout mk_layout(int64_t n) {
 }
 
 // MPG_FLAG_SORT keys: receiver cell (4 bits per axis, cells of extent/16, Morton)
-// above the seed direction (octahedral map, 9 bits per axis, Morton); walks
-// without a seed last.  Values: walk indices.
+// above the seed direction (octahedral map, 9 bits per axis, Morton); with a
+// per-sample chain length (configs[4], ctype != NULL) the length goes on top
+// (equal k walk together: the rolled per-vertex loops run the warp's max k) and
+// the direction keeps 8 bits per axis.  Walks without a seed last.  Values: walk
+// indices.
 __device__ __forceinline__ uint32_t mpg_spread2(uint32_t v) { // 9 bits -> every 2nd bit
     v &= 0x1ffu;
     v = (v | (v << 8)) & 0x00ff00ffu;
@@ -1027,8 +1030,8 @@ __device__ __forceinline__ uint32_t mpg_spread2(uint32_t v) { // 9 bits -> every
     v = (v | (v << 1)) & 0x55555555u;
     return v;
 }
-__global__ void k_sort_keys(const float4 *xD, const float4 *tgt, const int *bin, int64_t n, int spp, float cell,
-                            uint32_t *key, uint32_t *val) {
+__global__ void k_sort_keys(const float4 *xD, const float4 *tgt, const int *bin, const uint32_t *ctype, int64_t n,
+                            int spp, float cell, uint32_t *key, uint32_t *val) {
     for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < n; w += (int64_t)gridDim.x * blockDim.x) {
         val[w] = (uint32_t)w;
         if (bin[w] == -2) { key[w] = 0xffffffffu; continue; }
@@ -1048,7 +1051,12 @@ __global__ void k_sort_keys(const float4 *xD, const float4 *tgt, const int *bin,
         uint32_t pos = 0;
         for (int b = 0; b < 4; b++)
             pos |= (((cx >> b) & 1u) << (3 * b)) | (((cy >> b) & 1u) << (3 * b + 1)) | (((cz >> b) & 1u) << (3 * b + 2));
-        key[w] = (pos << 18) | dir;                                            // 30 bits
+        if (ctype) {   // per-sample chain length (configs[4]): group equal lengths first
+            const uint32_t len = min(__ldg(ctype + w) & 15u, 7u);
+            key[w] = (len << 28) | (pos << 16) | (dir >> 2);                     // 31 bits
+        } else {
+            key[w] = (pos << 18) | dir;                                          // 30 bits
+        }
     }
 }
 static size_t mk_ws_bytes(int64_t n) { return mk_layout(n).total; }
@@ -1141,13 +1149,15 @@ static mpg_status launch_walk(const DScene &S, const SeedCtx &g, WalkParams P, c
         uint32_t *v0 = (uint32_t *)(b + L.sval), *v1 = (uint32_t *)(b + L.sval2);
         int gk = (int)std::min<int64_t>((P.n + 255) / 256, (int64_t)num_sms() * 8);
         COUNT_LAUNCH(1);
-        k_sort_keys<<<gk, 256, 0, st>>>(P.xD, P.seed_tgt, P.seed_bin, P.n, P.spp, S.extent / 16.0f, k0, v0);
+        const uint32_t *len = g.mode == MPG_SEED_GUIDE_DIR ? P.seed_ctype : nullptr;   // per-sample n
+        k_sort_keys<<<gk, 256, 0, st>>>(P.xD, P.seed_tgt, P.seed_bin, len, P.n, P.spp, S.extent / 16.0f, k0, v0);
         CUDA_TRY(cudaPeekAtLastError());
         size_t tb = 0;
-        CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, tb, k0, k1, v0, v1, (int)P.n, 0, 30, st));
+        const int kbits = len ? 31 : 30;
+        CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, tb, k0, k1, v0, v1, (int)P.n, 0, kbits, st));
         if (tb > L.stemp_bytes) return fail(MPG_ERR_INVALID_ARG, "sort scratch larger than reserved");
         COUNT_LAUNCH(4);   // cub onesweep: histogram + 3 passes of 10 bits (library launches, counted)
-        CUDA_TRY(cub::DeviceRadixSort::SortPairs(b + L.stemp, tb, k0, k1, v0, v1, (int)P.n, 0, 30, st));
+        CUDA_TRY(cub::DeviceRadixSort::SortPairs(b + L.stemp, tb, k0, k1, v0, v1, (int)P.n, 0, kbits, st));
         P.perm = v1;
     }
     int64_t want = (P.n + 127) / 128;
