@@ -1102,15 +1102,15 @@ extern "C" size_t mpg_walk_workspace_size(int64_t n, const mpg_sampler_desc *sam
     return std::max(wf_layout(n, k).total, mk_ws_bytes(n));
 }
 
-template <int KMAX, typename R>
+template <int KMAX, typename R, int MINB = (KMAX <= 2 ? MPG_WALK_MINB2 : MPG_WALK_MINB_LONG)>
 static mpg_status launch_walk(const DScene &S, const SeedCtx &g, WalkParams P, cudaStream_t st, void *ws,
                               bool sort) {
     const bool wide = S.bvh_w == 4;
     static int occ2 = 0, occ4 = 0;
     int &occ = wide ? occ4 : occ2;
     if (!occ) {
-        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, wide ? k_walk<KMAX, R, 4> : k_walk<KMAX, R, 2>,
-                                                               128, 0));
+        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+            &occ, wide ? k_walk<KMAX, R, 4, MINB> : k_walk<KMAX, R, 2, MINB>, 128, 0));
         if (occ <= 0) occ = 1;
     }
     MKLayout L = mk_layout(P.n);
@@ -1168,8 +1168,8 @@ static mpg_status launch_walk(const DScene &S, const SeedCtx &g, WalkParams P, c
         P.idle_backlog = div ? (uint32_t)(blocks * 128 / div) : 0x7fffffffu;   // 0: any backlog
     }
     COUNT_LAUNCH(1);
-    if (wide) k_walk<KMAX, R, 4><<<blocks, 128, 0, st>>>(S, g, P);
-    else k_walk<KMAX, R, 2><<<blocks, 128, 0, st>>>(S, g, P);
+    if (wide) k_walk<KMAX, R, 4, MINB><<<blocks, 128, 0, st>>>(S, g, P);
+    else k_walk<KMAX, R, 2, MINB><<<blocks, 128, 0, st>>>(S, g, P);
     CUDA_TRY(cudaPeekAtLastError());
     return MPG_OK;
 }
@@ -1409,7 +1409,12 @@ extern "C" mpg_status mpg_manifold_walk(const mpg_scene *scene, const mpg_guide 
         if (k <= 1) return launch_walk<1, double>(scene->d, g, P, s, workspace, (o->flags & MPG_FLAG_SORT) != 0);
         if (k <= 2) return launch_walk<2, double>(scene->d, g, P, s, workspace, (o->flags & MPG_FLAG_SORT) != 0);
         if (k <= 4) return launch_walk<4, double>(scene->d, g, P, s, workspace, (o->flags & MPG_FLAG_SORT) != 0);
-        if (k <= 6) return launch_walk<6, double>(scene->d, g, P, s, workspace, (o->flags & MPG_FLAG_SORT) != 0);
+        if (k <= 6) {
+            if (sd->mode == MPG_SEED_GUIDE_DIR)   // mixed chain lengths: see MPG_WALK_MINB_MIXED
+                return launch_walk<6, double, MPG_WALK_MINB_MIXED>(scene->d, g, P, s, workspace,
+                                                                   (o->flags & MPG_FLAG_SORT) != 0);
+            return launch_walk<6, double>(scene->d, g, P, s, workspace, (o->flags & MPG_FLAG_SORT) != 0);
+        }
         return launch_walk<8, double>(scene->d, g, P, s, workspace, (o->flags & MPG_FLAG_SORT) != 0);
     }
     if (k <= 1) return launch_walk<1, float>(scene->d, g, P, s, workspace, (o->flags & MPG_FLAG_SORT) != 0);

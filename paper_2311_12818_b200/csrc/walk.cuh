@@ -17,15 +17,25 @@
 // analytic GGT by one more back-substitution with the 2-column light RHS (R11),
 // and reciprocal-probability trials (Eq. 15, R13).
 #pragma once
+// Occupancy (blocks of 128 per SM the register budget must allow), measured
+// (k_walk ms): k <= 2: 6 blocks (80 regs) 41.5 / 8 (64) 39.8 / 10 (48) 39.8 /
+// 12 (40) 46.1 on configs[1], 312 / 309 / 334 / 366 on [2] -> 8.  k = 6: 2
+// blocks (200+ regs) / 4 (128) / 6 (80) / 8 (64): configs[3] 232 / 170 / 163 /
+// 180 ms, but the mixed-length loop of configs[4] 256 / 264 / 279 / 292 ms per
+// step -> two instantiations, chosen by the sampler (MINB below).
 #ifndef MPG_WALK_MINB2
-#define MPG_WALK_MINB2 6   // k <= 2: 80 registers (measured best of 64/80/96/148)
+#define MPG_WALK_MINB2 8
+#endif
+#ifndef MPG_WALK_MINB_LONG
+#define MPG_WALK_MINB_LONG 6   // fixed long chains (configs[3])
+#endif
+#ifndef MPG_WALK_MINB_MIXED
+#define MPG_WALK_MINB_MIXED 2  // per-sample chain length (configs[4])
 #endif
 #include "device_common.cuh"
 #include "seed.cuh"
 #include "newton.cuh"
 
-// occupancy: k <= 2 chains are capped at 80 registers (6 blocks of 128 per SM):
-// the spills are cheaper than the latency the extra warps hide (+11% on configs[1])
 enum { PH_FETCH = 0, PH_SEED = 1, PH_DEDUCE = 2, PH_SOLVE = 3, PH_REPROJ = 4, PH_END = 5, PH_IDLE = 6, PH_WAIT = 7,
        PH_VIS = 8 };
 #define HARD_NONE 0xffffffffu
@@ -315,8 +325,8 @@ __device__ __forceinline__ unsigned long long gtimer() {
 }
 #endif
 
-template <int KMAX, typename R, int W>
-__global__ void __launch_bounds__(128, (KMAX <= 2 ? MPG_WALK_MINB2 : 2)) k_walk(const DScene S, const SeedCtx g, const WalkParams P) {
+template <int KMAX, typename R, int W, int MINB>
+__global__ void __launch_bounds__(128, MINB) k_walk(const DScene S, const SeedCtx g, const WalkParams P) {
     __shared__ unsigned long long s_stats[SS_N];
     __shared__ unsigned s_rays[128];   // chain rays per thread (see trace_chain)
     for (int i = threadIdx.x; i < SS_N; i += blockDim.x) s_stats[i] = 0ull;
