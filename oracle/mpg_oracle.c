@@ -66,6 +66,13 @@ typedef struct {
     const uint64_t *n_prefix;    /* [cells][6] defensive length mixture (Eqs. 10, 13)  */
     const uint64_t *type_prefix; /* [cells][126] per-length type weights (Eq. 11)      */
     const uint32_t *dir_prefix;  /* [cells][126][bins] learned direction weights        */
+    /* mode 4 (STree + vMF guide; orc_stree_build): n_prefix / type_prefix
+       above are then per leaf; the tree is descended with (x_D, x_L) */
+    int32_t root_ref, pad_;      /* >= 0 inner node, < 0: ~leaf                          */
+    const void *nodes;           /* orc_snode [n_nodes]                                  */
+    const int32_t *grp_off;      /* [leaves][127] lobe offsets of the (leaf, type) groups */
+    const uint64_t *lobe_prefix; /* [lobes] inclusive per-group prefix of lobe weights   */
+    const float *lobe_mu;        /* [lobes][4] vMF mean direction (xyz), kappa (w)       */
 } orc_seed_cfg;
 
 typedef struct {
@@ -782,8 +789,29 @@ static int guide_cell(const orc_seed_cfg *cfg, const float xD[3]) {
     return cz * cfg->cells_x + cx;
 }
 
+typedef struct { float split; int32_t axis, child[2]; } orc_snode; /* child >= 0 inner node, < 0 ~leaf */
+static float canon0(float x) { return x + 0.0f; } /* -0 -> +0: one ordering of equal keys [R29] */
+
+/* w_D ~ vMF(mu, kappa) on S^2 (Eq. 12, density kappa/(4 pi sinh kappa) e^{kappa mu.w}):
+ * cos theta by the inverse CDF F(c) = (e^{kappa c} - e^{-kappa}) / (2 sinh kappa), written as
+ * c = 1 + log(xi + (1 - xi) e^{-2 kappa}) / kappa with xi = 1 - u1 in (0, 1]; phi = 2 pi u2 [R31] */
+static void vmf_dir(const float mu[3], float kap, float u1, float u2, float out[3]) {
+    float xi = 1.0f - u1;
+    float e2k = expf(-2.0f * kap);
+    float ct = 1.0f + logf(xi + (1.0f - xi) * e2k) / kap;
+    if (ct < -1.0f) ct = -1.0f;
+    if (ct > 1.0f) ct = 1.0f;
+    float st2 = 1.0f - ct * ct;
+    float st = sqrtf(st2 > 0.0f ? st2 : 0.0f);
+    float phi = 6.28318530717958647692f * u2;
+    float cp = cosf(phi), sp = sinf(phi);
+    float b1[3], b2[3];
+    onb_f(mu, b1, b2);
+    for (int j = 0; j < 3; j++) out[j] = ct * mu[j] + st * (cp * b1[j] + sp * b2[j]);
+}
+
 static int seed_target(const orc_scene *sc, const orc_seed_cfg *cfg, const orc_opts *o, uint64_t walk, uint32_t trial,
-                       const float xD[3], seed_res *sr) {
+                       const float xD[3], const float xL[3], seed_res *sr) {
     uint32_t r[4];
     float *tgt = sr->tgt;
     int32_t *bin = &sr->bin;
@@ -866,9 +894,21 @@ static int seed_target(const orc_scene *sc, const orc_seed_cfg *cfg, const orc_o
         tgt[2] = cfg->uv_origin[1] + v * cfg->uv_scale[1];
         return 1;
     }
-    if (cfg->mode == 3) { /* configs[4]: n ~ 1/2 P_0 + 1/2 P_e (Eqs. 10, 13), then one-sample MIS
-                             of the initializer and the learned (tau, w_D) (Eqs. 8, 11, 13) [R22] */
-        int c = guide_cell(cfg, xD);
+    if (cfg->mode == 3 || cfg->mode == 4) {
+        /* configs[4]: n ~ 1/2 P_0 + 1/2 P_e (Eqs. 10, 13), then one-sample MIS of the initializer
+           and the learned (tau, w_D) (Eqs. 8, 11, 13) [R22].  mode 3: P_e from the histogram cell
+           of x_D, w_D from its direction bins; mode 4: P_e from the STree leaf of
+           (x_D, x_L), w_D from the leaf's vMF mixture of type tau (Eq. 12) [R28-R31] */
+        int c;
+        if (cfg->mode == 3) {
+            c = guide_cell(cfg, xD);
+        } else {
+            const orc_snode *nodes = (const orc_snode *)cfg->nodes;
+            float p[6] = {canon0(xD[0]), canon0(xD[1]), canon0(xD[2]), canon0(xL[0]), canon0(xL[1]), canon0(xL[2])};
+            int ref = cfg->root_ref;
+            while (ref >= 0) ref = p[nodes[ref].axis] < nodes[ref].split ? nodes[ref].child[0] : nodes[ref].child[1];
+            c = ~ref;
+        }
         const uint64_t *npf = cfg->n_prefix + (size_t)c * 6;
         draw(o, walk, 1u, 0u, r); /* n reused by every trial */
         uint64_t S = npf[5];
@@ -888,6 +928,21 @@ static int seed_target(const orc_scene *sc, const orc_seed_cfg *cfg, const orc_o
             while (tpf[m] <= tt) m++;
             sr->tau = (uint32_t)m;
             sr->learned = 1;
+            if (cfg->mode == 4) { /* lobe i ~ W_i (Eq. 12 weights w_i), then w_D ~ vMF(mu_i, kappa_i) */
+                int glo = cfg->grp_off[(size_t)c * 127 + g0 + m], ghi = cfg->grp_off[(size_t)c * 127 + g0 + m + 1];
+                uint64_t Sl = cfg->lobe_prefix[ghi - 1];
+                uint64_t tl = mulhi_u64(r[3], Sl);
+                int b = glo;
+                while (cfg->lobe_prefix[b] <= tl) b++;
+                *bin = b;
+                uint32_t r2[4];
+                draw(o, walk, 2u, trial, r2);
+                const float *mu = cfg->lobe_mu + 4 * (size_t)b;
+                float w[3];
+                vmf_dir(mu, mu[3], u01(r2[0]), u01(r2[1]), w);
+                for (int j = 0; j < 3; j++) tgt[j] = xD[j] + w[j];
+                return 1;
+            }
             int nb = cfg->bins_x * cfg->bins_y;
             const uint32_t *dpf = cfg->dir_prefix + ((size_t)c * 126 + g0 + m) * nb;
             uint64_t Sd = dpf[nb - 1];
@@ -989,7 +1044,8 @@ static int attempt(const orc_scene *sc, const orc_seed_cfg *cfg, const orc_opts 
     *iters = 0;
     *k = cfg->k;
     *tau = cfg->tau;
-    if (!seed_target(sc, cfg, o, walk, trial, xD, sr)) return ST_SEED_FAIL;
+    float xLf[3] = {(float)xL.x, (float)xL.y, (float)xL.z}; /* exact: x_L was drawn in fp32 */
+    if (!seed_target(sc, cfg, o, walk, trial, xD, xLf, sr)) return ST_SEED_FAIL;
     *k = sr->n;
     v3 xd = vf(xD);
     double eps = eps_ray(sc, o);
@@ -1181,7 +1237,7 @@ int orc_seed(const void *h, const orc_seed_cfg *cfg, const orc_opts *o, const fl
     uint64_t wid = o->walk_id_base + (uint64_t)walk;
     sample_light(sc, o, wid, xL, pdfL, &lid);
     seed_res sr;
-    int ok = seed_target(sc, cfg, o, wid, trial, xD + 3 * (walk / spp), &sr);
+    int ok = seed_target(sc, cfg, o, wid, trial, xD + 3 * (walk / spp), xL, &sr);
     memcpy(tgt, sr.tgt, sizeof(sr.tgt));
     *bin = sr.bin;
     return ok;
@@ -1193,7 +1249,11 @@ int orc_seed_ex(const void *h, const orc_seed_cfg *cfg, const orc_opts *o, const
                 uint32_t *init_bits, double *Pn) {
     const orc_scene *sc = (const orc_scene *)h;
     seed_res sr;
-    int ok = seed_target(sc, cfg, o, o->walk_id_base + (uint64_t)walk, trial, xD + 3 * (walk / spp), &sr);
+    float xL[3];
+    double pdfL;
+    int lid;
+    sample_light(sc, o, o->walk_id_base + (uint64_t)walk, xL, &pdfL, &lid);
+    int ok = seed_target(sc, cfg, o, o->walk_id_base + (uint64_t)walk, trial, xD + 3 * (walk / spp), xL, &sr);
     memcpy(tgt, sr.tgt, sizeof(sr.tgt));
     *bin = sr.bin; *n = sr.n; *tau = sr.tau; *learned = sr.learned; *init_bits = sr.init_bits; *Pn = sr.Pn;
     return ok;
@@ -1268,6 +1328,50 @@ void orc_accumulate(const orc_seed_cfg *cfg, const float *xD, int32_t spp, int64
     }
 }
 
+/* per-cell (or per-leaf) length and type tables from the per-type energies E[126] (R22):
+ * W_n = E_n>0 ? max(1, floor(E_n/E_max 2^20)) : 0, n_prefix = cumsum(c_n sum W + 119 W_n)
+ * (= 1/2 P_0 + 1/2 P_e, Eqs. 10, 13; no energy -> c_n); type weights per length group
+ * likewise from E_tau (Eq. 11). */
+static void typed_tables(const double *E, uint64_t *n_prefix, uint64_t *type_prefix) {
+    double En[6], emax = 0.0;
+    for (int n = 1; n <= 6; n++) {
+        double e = 0.0;
+        for (int m = 0; m < (1 << n); m++) e += E[(1 << n) - 2 + m];
+        En[n - 1] = e;
+        if (e > emax) emax = e;
+    }
+    uint64_t Wn[6], sumW = 0;
+    for (int n = 0; n < 6; n++) {
+        uint64_t w = 0;
+        if (En[n] > 0.0 && emax > 0.0) {
+            w = (uint64_t)floor((En[n] / emax) * 1048576.0);
+            if (w < 1u) w = 1u;
+        }
+        Wn[n] = w;
+        sumW += w;
+    }
+    uint64_t acc = 0;
+    for (int n = 0; n < 6; n++) {
+        acc += sumW == 0 ? P0_INT[n] : P0_INT[n] * sumW + 119u * Wn[n];
+        n_prefix[n] = acc;
+    }
+    for (int n = 1; n <= 6; n++) {
+        int g0 = (1 << n) - 2, gn = 1 << n;
+        double gmax = 0.0;
+        for (int m = 0; m < gn; m++) if (E[g0 + m] > gmax) gmax = E[g0 + m];
+        uint64_t a2 = 0;
+        for (int m = 0; m < gn; m++) {
+            uint64_t w = 0;
+            if (E[g0 + m] > 0.0 && gmax > 0.0) {
+                w = (uint64_t)floor((E[g0 + m] / gmax) * 1048576.0);
+                if (w < 1u) w = 1u;
+            }
+            a2 += w;
+            type_prefix[g0 + m] = a2;
+        }
+    }
+}
+
 /* configs[4] guide tables from a typed direction histogram hist[cells][126][nb]
  * (R22): per (cell, type) energy E = sum of bins (fp64, bin order); per length
  * E_n = sum of its types (type order); W_n = E_n>0 ? max(1, floor(E_n/E_max 2^20)) : 0,
@@ -1297,43 +1401,7 @@ void orc_guide_dir_tables(const float *hist, int n_cells, int nb, uint64_t *n_pr
                 dp[b] = acc;
             }
         }
-        double En[6], emax = 0.0;
-        for (int n = 1; n <= 6; n++) {
-            double e = 0.0;
-            for (int m = 0; m < (1 << n); m++) e += E[(1 << n) - 2 + m];
-            En[n - 1] = e;
-            if (e > emax) emax = e;
-        }
-        uint64_t Wn[6], sumW = 0;
-        for (int n = 0; n < 6; n++) {
-            uint64_t w = 0;
-            if (En[n] > 0.0 && emax > 0.0) {
-                w = (uint64_t)floor((En[n] / emax) * 1048576.0);
-                if (w < 1u) w = 1u;
-            }
-            Wn[n] = w;
-            sumW += w;
-        }
-        uint64_t acc = 0;
-        for (int n = 0; n < 6; n++) {
-            acc += sumW == 0 ? P0_INT[n] : P0_INT[n] * sumW + 119u * Wn[n];
-            n_prefix[(size_t)c * 6 + n] = acc;
-        }
-        for (int n = 1; n <= 6; n++) {
-            int g0 = (1 << n) - 2, gn = 1 << n;
-            double gmax = 0.0;
-            for (int m = 0; m < gn; m++) if (E[g0 + m] > gmax) gmax = E[g0 + m];
-            uint64_t a2 = 0;
-            for (int m = 0; m < gn; m++) {
-                uint64_t w = 0;
-                if (E[g0 + m] > 0.0 && gmax > 0.0) {
-                    w = (uint64_t)floor((E[g0 + m] / gmax) * 1048576.0);
-                    if (w < 1u) w = 1u;
-                }
-                a2 += w;
-                type_prefix[(size_t)c * 126 + g0 + m] = a2;
-            }
-        }
+        typed_tables(E, n_prefix + (size_t)c * 6, type_prefix + (size_t)c * 126);
     }
     free(E);
 }
@@ -1360,3 +1428,266 @@ void orc_accumulate_dir(const orc_seed_cfg *cfg, const float *xD, int32_t spp, i
         hist[((size_t)c * 126 + type) * nb + bv * cfg->bins_x + bu] += w[i];
     }
 }
+
+/* ------------------------------------------------------------------------ */
+/* STree + vMF guide, §5.5-5.6:                       */
+/*   S = the sub-path samples of the last iteration (P:426 footnote)   */
+/*   w = T <1/P> per sample (Eq. 9)                                */
+/*   6D adaptive binary tree over (x_D, x_L), leaf threshold c sqrt|S|,       */
+/*   eps k overlap copies, far samples discarded (P:518-523 + footnote)       */
+/*   per leaf: P_e(n) (Eq. 10), P_e(tau|n) (Eq. 11), per type a vMF mixture   */
+/*   with mu_i = w_D*_i, kappa_i = sigma_i^-2 from the nearest direction in   */
+/*   the same (leaf, type) set, weights ~ w_i (Eq. 12)             */
+/* Readings R28-R31.  Breadth-first: nodes and leaves are      */
+/* numbered in the order they are created, level by level.                    */
+/* ------------------------------------------------------------------------ */
+typedef struct { float xD[3], xL[3], omega[3], w; int32_t type, pad; } orc_gsample; /* 48 B record */
+
+typedef struct {
+    int32_t n_nodes, n_leaves, root_ref, thr;
+    int64_t n_valid, n_lobes;
+    orc_snode *nodes;
+    int64_t *leaf_begin, *leaf_count; /* into leaf_ids (the leaf's list, in its own order) */
+    int64_t *leaf_ids;
+    int32_t *grp_off;                 /* [leaves][127] */
+    int64_t *lobe_sample;             /* [lobes] record index */
+    uint64_t *lobe_prefix;            /* [lobes] */
+    float *lobe_mu;                   /* [lobes][4] */
+    uint64_t *n_prefix, *type_prefix; /* [leaves][6], [leaves][126] */
+} orc_stree;
+
+static const orc_gsample *g_sort_rec;
+static int g_sort_axis;
+static float skey(const orc_gsample *r, int a) { return canon0(a < 3 ? r->xD[a] : r->xL[a - 3]); }
+static int cmp_axis(const void *A, const void *B) { /* by (coordinate, record index) [R29] */
+    int64_t i = *(const int64_t *)A, j = *(const int64_t *)B;
+    float x = skey(g_sort_rec + i, g_sort_axis), y = skey(g_sort_rec + j, g_sort_axis);
+    if (x < y) return -1;
+    if (x > y) return 1;
+    return i < j ? -1 : (i > j ? 1 : 0);
+}
+
+typedef struct { int64_t *ids; int64_t n; float lo[6], hi[6]; int depth; int parent, side; } orc_qnode;
+
+void orc_stree_free(void *h) {
+    orc_stree *t = (orc_stree *)h;
+    if (!t) return;
+    free(t->nodes); free(t->leaf_begin); free(t->leaf_count); free(t->leaf_ids); free(t->grp_off);
+    free(t->lobe_sample); free(t->lobe_prefix); free(t->lobe_mu); free(t->n_prefix); free(t->type_prefix);
+    free(t);
+}
+
+/* Build the guide from n records; a record is a sample iff w > 0 and 0 <= type < 126.
+ * eps: overlap fraction (0.1, P:523 footnote); c_thr: threshold coefficient (1);
+ * kappa in [kappa_min, kappa_max] (R30). */
+void *orc_stree_build(const orc_gsample *rec, int64_t n, float eps, float c_thr, int32_t max_depth,
+                      float kappa_min, float kappa_max) {
+    orc_stree *t = (orc_stree *)calloc(1, sizeof(orc_stree));
+    int64_t nv = 0;
+    for (int64_t i = 0; i < n; i++) if (rec[i].w > 0.0f && rec[i].type >= 0 && rec[i].type < 126) nv++;
+    t->n_valid = nv;
+    /* threshold c sqrt|S| [R28]: floor in fp64 of c * sqrt(|S|), at least 1 */
+    double thr_d = floor((double)c_thr * sqrt((double)nv));
+    t->thr = thr_d < 1.0 ? 1 : (int32_t)thr_d;
+    /* root: all samples in record order; box = fp32 min/max of their (x_D, x_L) */
+    orc_qnode root;
+    memset(&root, 0, sizeof(root));
+    root.ids = (int64_t *)malloc(sizeof(int64_t) * (nv ? nv : 1));
+    root.n = 0;
+    for (int a = 0; a < 6; a++) { root.lo[a] = INFINITY; root.hi[a] = -INFINITY; }
+    for (int64_t i = 0; i < n; i++) {
+        if (!(rec[i].w > 0.0f && rec[i].type >= 0 && rec[i].type < 126)) continue;
+        root.ids[root.n++] = i;
+        for (int a = 0; a < 6; a++) {
+            float x = skey(rec + i, a);
+            if (x < root.lo[a]) root.lo[a] = x;
+            if (x > root.hi[a]) root.hi[a] = x;
+        }
+    }
+    int active[6], na = 0; /* split axes: those the samples span, in (x_D, x_L) order [R28] */
+    for (int a = 0; a < 6; a++) if (nv > 0 && root.hi[a] > root.lo[a]) active[na++] = a;
+    root.parent = -1;
+    /* breadth-first queue */
+    int64_t qcap = 1024, qh = 0, qt = 0;
+    orc_qnode *q = (orc_qnode *)malloc(sizeof(orc_qnode) * qcap);
+    q[qt++] = root;
+    int64_t ncap = 64, lcap = 64, idcap = nv + 16, idn = 0;
+    t->nodes = (orc_snode *)malloc(sizeof(orc_snode) * ncap);
+    t->leaf_begin = (int64_t *)malloc(sizeof(int64_t) * lcap);
+    t->leaf_count = (int64_t *)malloc(sizeof(int64_t) * lcap);
+    t->leaf_ids = (int64_t *)malloc(sizeof(int64_t) * idcap);
+    while (qh < qt) {
+        orc_qnode nd = q[qh++];
+        int ref;
+        if (nd.n <= t->thr || nd.depth >= max_depth || na == 0) { /* leaf */
+            if (t->n_leaves == lcap) {
+                lcap *= 2;
+                t->leaf_begin = (int64_t *)realloc(t->leaf_begin, sizeof(int64_t) * lcap);
+                t->leaf_count = (int64_t *)realloc(t->leaf_count, sizeof(int64_t) * lcap);
+            }
+            if (idn + nd.n > idcap) {
+                while (idn + nd.n > idcap) idcap *= 2;
+                t->leaf_ids = (int64_t *)realloc(t->leaf_ids, sizeof(int64_t) * idcap);
+            }
+            memcpy(t->leaf_ids + idn, nd.ids, sizeof(int64_t) * nd.n);
+            t->leaf_begin[t->n_leaves] = idn;
+            t->leaf_count[t->n_leaves] = nd.n;
+            idn += nd.n;
+            ref = ~t->n_leaves++;
+            free(nd.ids);
+        } else { /* split at the midpoint of the cycled axis with eps k overlap [R28, R29] */
+            if (t->n_nodes == ncap) { ncap *= 2; t->nodes = (orc_snode *)realloc(t->nodes, sizeof(orc_snode) * ncap); }
+            int me = t->n_nodes++;
+            ref = me;
+            int a = active[nd.depth % na];
+            float c = (nd.lo[a] + nd.hi[a]) * 0.5f;
+            float delta = (nd.hi[a] - nd.lo[a]) * 0.25f; /* copies kept within half a child width */
+            g_sort_rec = rec; g_sort_axis = a;
+            qsort(nd.ids, (size_t)nd.n, sizeof(int64_t), cmp_axis);
+            int64_t m = 0;
+            while (m < nd.n && skey(rec + nd.ids[m], a) < c) m++;
+            int64_t e = (int64_t)floor((double)eps * (double)nd.n);
+            int64_t eR = 0, eL = 0; /* the e nearest samples across the plane, the far ones dropped */
+            while (eR < e && m + eR < nd.n && skey(rec + nd.ids[m + eR], a) - c <= delta) eR++;
+            while (eL < e && m - 1 - eL >= 0 && c - skey(rec + nd.ids[m - 1 - eL], a) <= delta) eL++;
+            /* samples inherited as copies that lie more than half a child width outside the child's
+               box are far from it: discarded (P:523 footnote) [R29] */
+            int64_t s0 = 0, s1 = nd.n;
+            while (s0 < m && nd.lo[a] - skey(rec + nd.ids[s0], a) > delta) s0++;
+            while (s1 > m && skey(rec + nd.ids[s1 - 1], a) - nd.hi[a] > delta) s1--;
+            t->nodes[me].axis = a;
+            t->nodes[me].split = c;
+            t->nodes[me].child[0] = t->nodes[me].child[1] = 0;
+            if (qt + 2 > qcap) {
+                /* compact the consumed head, then grow */
+                memmove(q, q + qh, sizeof(orc_qnode) * (qt - qh));
+                qt -= qh; qh = 0;
+                if (qt + 2 > qcap) { qcap *= 2; q = (orc_qnode *)realloc(q, sizeof(orc_qnode) * qcap); }
+            }
+            for (int side = 0; side < 2; side++) {
+                orc_qnode ch;
+                memcpy(ch.lo, nd.lo, sizeof(ch.lo));
+                memcpy(ch.hi, nd.hi, sizeof(ch.hi));
+                int64_t b0 = side == 0 ? s0 : m - eL, b1 = side == 0 ? m + eR : s1;
+                if (side == 0) ch.hi[a] = c; else ch.lo[a] = c;
+                ch.n = b1 - b0;
+                ch.ids = (int64_t *)malloc(sizeof(int64_t) * (ch.n ? ch.n : 1));
+                memcpy(ch.ids, nd.ids + b0, sizeof(int64_t) * ch.n);
+                ch.depth = nd.depth + 1;
+                ch.parent = me;
+                ch.side = side;
+                q[qt++] = ch;
+            }
+            free(nd.ids);
+        }
+        if (nd.parent < 0) t->root_ref = ref;
+        else t->nodes[nd.parent].child[nd.side] = ref;
+    }
+    free(q);
+    /* per leaf: lobes grouped by type (stable), kappa, weights, tables */
+    int L = t->n_leaves;
+    t->n_lobes = idn;
+    t->grp_off = (int32_t *)malloc(sizeof(int32_t) * 127 * (size_t)L);
+    t->lobe_sample = (int64_t *)malloc(sizeof(int64_t) * (idn ? idn : 1));
+    t->lobe_prefix = (uint64_t *)malloc(sizeof(uint64_t) * (idn ? idn : 1));
+    t->lobe_mu = (float *)malloc(sizeof(float) * 4 * (idn ? idn : 1));
+    t->n_prefix = (uint64_t *)malloc(sizeof(uint64_t) * 6 * (size_t)L);
+    t->type_prefix = (uint64_t *)malloc(sizeof(uint64_t) * 126 * (size_t)L);
+    int64_t pos = 0;
+    double E[126];
+    for (int l = 0; l < L; l++) {
+        const int64_t *ids = t->leaf_ids + t->leaf_begin[l];
+        int64_t cnt = t->leaf_count[l];
+        for (int ty = 0; ty < 126; ty++) {
+            t->grp_off[(size_t)l * 127 + ty] = (int32_t)pos;
+            int64_t g0 = pos;
+            for (int64_t j = 0; j < cnt; j++) if (rec[ids[j]].type == ty) t->lobe_sample[pos++] = ids[j];
+            /* E_tau = sum of w (Eqs. 10-11), in group order */
+            double e = 0.0;
+            float wmax = 0.0f;
+            for (int64_t i = g0; i < pos; i++) {
+                float wi = rec[t->lobe_sample[i]].w;
+                e += (double)wi;
+                if (wi > wmax) wmax = wi;
+            }
+            E[ty] = e;
+            uint64_t acc = 0;
+            for (int64_t i = g0; i < pos; i++) {
+                const orc_gsample *ri = rec + t->lobe_sample[i];
+                /* sigma_i: distance to the nearest other direction of the set (chord) [R30] */
+                float d2min = INFINITY;
+                for (int64_t j = g0; j < pos; j++) {
+                    if (j == i) continue;
+                    const orc_gsample *rj = rec + t->lobe_sample[j];
+                    float dx = ri->omega[0] - rj->omega[0], dy = ri->omega[1] - rj->omega[1],
+                          dz = ri->omega[2] - rj->omega[2];
+                    float d2 = dx * dx + dy * dy + dz * dz;
+                    if (d2 < d2min) d2min = d2;
+                }
+                float kap = pos - g0 == 1 ? kappa_min : (d2min > 0.0f ? 1.0f / d2min : kappa_max);
+                if (kap < kappa_min) kap = kappa_min;
+                if (kap > kappa_max) kap = kappa_max;
+                t->lobe_mu[4 * i] = ri->omega[0];
+                t->lobe_mu[4 * i + 1] = ri->omega[1];
+                t->lobe_mu[4 * i + 2] = ri->omega[2];
+                t->lobe_mu[4 * i + 3] = kap;
+                /* lobe weight ~ w_i, integer as R20 */
+                float qf = floorf((ri->w / wmax) * 1048576.0f);
+                uint64_t W = (uint64_t)qf;
+                if (W < 1u) W = 1u;
+                acc += W;
+                t->lobe_prefix[i] = acc;
+            }
+        }
+        t->grp_off[(size_t)l * 127 + 126] = (int32_t)pos;
+        typed_tables(E, t->n_prefix + (size_t)l * 6, t->type_prefix + (size_t)l * 126);
+    }
+    return t;
+}
+
+/* counts: n_nodes, n_leaves, root_ref, thr, n_valid, n_lobes */
+void orc_stree_info(const void *h, int64_t out[6]) {
+    const orc_stree *t = (const orc_stree *)h;
+    out[0] = t->n_nodes; out[1] = t->n_leaves; out[2] = t->root_ref; out[3] = t->thr;
+    out[4] = t->n_valid; out[5] = t->n_lobes;
+}
+
+/* copy out (caller sizes from orc_stree_info); any pointer may be NULL */
+void orc_stree_get(const void *h, orc_snode *nodes, int64_t *leaf_begin, int64_t *leaf_count, int64_t *leaf_ids,
+                   int32_t *grp_off, int64_t *lobe_sample, uint64_t *lobe_prefix, float *lobe_mu, uint64_t *n_prefix,
+                   uint64_t *type_prefix) {
+    const orc_stree *t = (const orc_stree *)h;
+    int64_t L = t->n_leaves, nl = t->n_lobes;
+    if (nodes) memcpy(nodes, t->nodes, sizeof(orc_snode) * t->n_nodes);
+    if (leaf_begin) memcpy(leaf_begin, t->leaf_begin, sizeof(int64_t) * L);
+    if (leaf_count) memcpy(leaf_count, t->leaf_count, sizeof(int64_t) * L);
+    if (leaf_ids) memcpy(leaf_ids, t->leaf_ids, sizeof(int64_t) * nl);
+    if (grp_off) memcpy(grp_off, t->grp_off, sizeof(int32_t) * 127 * L);
+    if (lobe_sample) memcpy(lobe_sample, t->lobe_sample, sizeof(int64_t) * nl);
+    if (lobe_prefix) memcpy(lobe_prefix, t->lobe_prefix, sizeof(uint64_t) * nl);
+    if (lobe_mu) memcpy(lobe_mu, t->lobe_mu, sizeof(float) * 4 * nl);
+    if (n_prefix) memcpy(n_prefix, t->n_prefix, sizeof(uint64_t) * 6 * L);
+    if (type_prefix) memcpy(type_prefix, t->type_prefix, sizeof(uint64_t) * 126 * L);
+}
+
+/* sample records from walk outputs (Eq. 9 samples of one iteration): x_D of the walk's receiver,
+ * its x_L, w_D* = normalize(x_1* - x_D) (fp32), type = 2^n - 2 + tau, w; non-samples get w = 0 */
+void orc_record_samples(const float *xD, int32_t spp, int64_t n, const int32_t *status, const float *w,
+                        const float *x1, const int32_t *k, const uint32_t *tau, const float *xL, orc_gsample *out) {
+    for (int64_t i = 0; i < n; i++) {
+        orc_gsample *r = out + i;
+        memset(r, 0, sizeof(*r));
+        const float *xd = xD + 3 * (i / spp);
+        for (int j = 0; j < 3; j++) { r->xD[j] = xd[j]; r->xL[j] = xL[3 * i + j]; }
+        r->type = -1;
+        if (status[i] != ST_CONVERGED || !(w[i] > 0.0f) || k[i] < 1 || k[i] > 6) continue;
+        float dx = x1[3 * i] - xd[0], dy = x1[3 * i + 1] - xd[1], dz = x1[3 * i + 2] - xd[2];
+        float l = sqrtf(dx * dx + dy * dy + dz * dz);
+        r->omega[0] = dx / l; r->omega[1] = dy / l; r->omega[2] = dz / l;
+        r->type = (1 << k[i]) - 2 + (int32_t)tau[i];
+        r->w = w[i];
+    }
+}
+
+/* vMF direction draw as seed mode 4 does it (test export) */
+void orc_vmf_sample(const float mu[3], float kap, float u1, float u2, float out[3]) { vmf_dir(mu, kap, u1, u2, out); }

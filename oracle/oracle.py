@@ -47,7 +47,15 @@ class SeedCfg(C.Structure):
                 ("grid_origin", C.c_float * 2), ("grid_extent", C.c_float * 2), ("cells_x", C.c_int32),
                 ("cells_y", C.c_int32), ("bins_x", C.c_int32), ("bins_y", C.c_int32), ("uv_origin", C.c_float * 2),
                 ("uv_scale", C.c_float * 2), ("uv_plane_y", C.c_float), ("prefix", C.POINTER(C.c_uint64)),
-                ("n_prefix", C.c_void_p), ("type_prefix", C.c_void_p), ("dir_prefix", C.c_void_p)]
+                ("n_prefix", C.c_void_p), ("type_prefix", C.c_void_p), ("dir_prefix", C.c_void_p),
+                ("root_ref", C.c_int32), ("pad_", C.c_int32), ("nodes", C.c_void_p), ("grp_off", C.c_void_p),
+                ("lobe_prefix", C.c_void_p), ("lobe_mu", C.c_void_p)]
+
+
+# STree + vMF guide: 48-byte sample record and tree node, as in mpg_oracle.c
+GSAMPLE = np.dtype([("xD", np.float32, (3,)), ("xL", np.float32, (3,)), ("omega", np.float32, (3,)),
+                    ("w", np.float32), ("type", np.int32), ("pad", np.int32)])
+SNODE = np.dtype([("split", np.float32), ("axis", np.int32), ("child", np.int32, (2,))])
 
 
 class Opts(C.Structure):
@@ -116,6 +124,13 @@ def lib():
         _lib.orc_guide_dir_tables.argtypes = [P, C.c_int, C.c_int, P, P, P]
         _lib.orc_accumulate_dir.argtypes = [C.POINTER(SeedCfg), P, C.c_int32, C.c_int64, P, P, P, P, P, P]
         _lib.orc_tangent_basis.argtypes = [P, C.c_int32, C.c_int32, dp, dp, dp]
+        _lib.orc_stree_build.restype = P
+        _lib.orc_stree_build.argtypes = [P, C.c_int64, C.c_float, C.c_float, C.c_int32, C.c_float, C.c_float]
+        _lib.orc_stree_free.argtypes = [P]
+        _lib.orc_stree_info.argtypes = [P, P]
+        _lib.orc_stree_get.argtypes = [P] + [P] * 10
+        _lib.orc_record_samples.argtypes = [P, C.c_int32, C.c_int64, P, P, P, P, P, P, P]
+        _lib.orc_vmf_sample.argtypes = [P, C.c_float, C.c_float, C.c_float, P]
         _lib.orc_scatter.restype = C.c_int
         _lib.orc_scatter.argtypes = [C.c_int, C.c_double, C.c_double, dp, dp, dp]
     return _lib
@@ -167,6 +182,50 @@ def guide_dir_tables(H: np.ndarray):
     dpf = np.zeros((nc, 126, nb), np.uint32)
     lib().orc_guide_dir_tables(_ptr(H), nc, nb, _ptr(npf), _ptr(tpf), _ptr(dpf))
     return npf, tpf, dpf
+
+
+STREE_DEFAULTS = dict(eps=0.1, c_thr=1.0, max_depth=32, kappa_min=1.0, kappa_max=1.0e4)
+
+
+def stree_build(records: np.ndarray, eps=0.1, c_thr=1.0, max_depth=32, kappa_min=1.0, kappa_max=1.0e4) -> dict:
+    """STree + vMF guide from sample records (GSAMPLE array): tree, leaf lists, lobes, tables."""
+    L = lib()
+    rec = np.ascontiguousarray(records, GSAMPLE)
+    h = L.orc_stree_build(_ptr(rec), rec.shape[0], eps, c_thr, max_depth, kappa_min, kappa_max)
+    info = np.zeros(6, np.int64)
+    L.orc_stree_info(h, _ptr(info))
+    nn, nl, root, thr, nv, nlobe = (int(x) for x in info)
+    out = dict(n_nodes=nn, n_leaves=nl, root_ref=root, thr=thr, n_valid=nv, n_lobes=nlobe,
+               nodes=np.zeros(max(nn, 1), SNODE), leaf_begin=np.zeros(nl, np.int64), leaf_count=np.zeros(nl, np.int64),
+               leaf_ids=np.zeros(max(nlobe, 1), np.int64), grp_off=np.zeros((nl, 127), np.int32),
+               lobe_sample=np.zeros(max(nlobe, 1), np.int64), lobe_prefix=np.zeros(max(nlobe, 1), np.uint64),
+               lobe_mu=np.zeros((max(nlobe, 1), 4), np.float32), n_prefix=np.zeros((nl, 6), np.uint64),
+               type_prefix=np.zeros((nl, 126), np.uint64))
+    L.orc_stree_get(h, *(_ptr(out[k]) for k in ("nodes", "leaf_begin", "leaf_count", "leaf_ids", "grp_off",
+                                                "lobe_sample", "lobe_prefix", "lobe_mu", "n_prefix", "type_prefix")))
+    L.orc_stree_free(h)
+    out["nodes"] = out["nodes"][:nn]
+    for k in ("leaf_ids", "lobe_sample", "lobe_prefix", "lobe_mu"):
+        out[k] = out[k][:nlobe]
+    return out
+
+
+def record_samples(xD, spp, status, w, x1, k, tau, xL) -> np.ndarray:
+    """Sample records (GSAMPLE) of one iteration's walks (Eq. 9 samples)."""
+    n = len(status)
+    out = np.zeros(n, GSAMPLE)
+    arrs = [np.ascontiguousarray(a, dt) for a, dt in ((xD, np.float32), (status, np.int32), (w, np.float32),
+                                                      (x1, np.float32), (k, np.int32), (tau, np.uint32),
+                                                      (xL, np.float32))]
+    lib().orc_record_samples(_ptr(arrs[0]), int(spp), n, *(_ptr(a) for a in arrs[1:]), _ptr(out))
+    return out
+
+
+def vmf_sample(mu, kappa, u1, u2) -> np.ndarray:
+    mu = np.ascontiguousarray(mu, np.float32)
+    out = np.zeros(3, np.float32)
+    lib().orc_vmf_sample(_ptr(mu), float(kappa), float(u1), float(u2), _ptr(out))
+    return out
 
 
 def make_opts(w, **over) -> Opts:
@@ -240,6 +299,16 @@ class OracleScene:
         self.dir_tables = guide_dir_tables(H)
         npf, tpf, dpf = self.dir_tables
         c.n_prefix, c.type_prefix, c.dir_prefix = _ptr(npf), _ptr(tpf), _ptr(dpf)
+
+    def set_stree(self, G: dict, c=None):
+        """Seed mode 4: sample from an STree + vMF guide (stree_build output)."""
+        c = c or self.cfg
+        self.stree = G
+        c.mode = 4
+        c.root_ref = G["root_ref"]
+        c.nodes, c.grp_off = _ptr(G["nodes"]), _ptr(G["grp_off"])
+        c.lobe_prefix, c.lobe_mu = _ptr(G["lobe_prefix"]), _ptr(G["lobe_mu"])
+        c.n_prefix, c.type_prefix = _ptr(G["n_prefix"]), _ptr(G["type_prefix"])
 
     def set_energies(self, E, c=None):
         c = c or self.cfg

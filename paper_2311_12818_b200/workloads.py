@@ -452,3 +452,47 @@ def scene_extent(w: Workload) -> float:
             pts.append(c)
     P = np.stack(pts)
     return float(np.linalg.norm(P.max(0) - P.min(0)))
+
+
+# ---------------------------------------------------------------------------
+# STree + vMF guide: seeded sample records shaped like one
+# progressive iteration of configs[4] (inputs only: no method arithmetic).
+# Record = 48 B: x_D[3], x_L[3], w_D*[3] (unit), w, type (2^n - 2 + tau, or -1), pad.
+# ---------------------------------------------------------------------------
+GUIDE_SAMPLE = np.dtype([("xD", np.float32, (3,)), ("xL", np.float32, (3,)), ("omega", np.float32, (3,)),
+                         ("w", np.float32), ("type", np.int32), ("pad", np.int32)])
+
+
+def synthetic_guide_samples(n: int, seed: int = 0, invalid_frac: float = 0.3, n_clusters: int = 24) -> np.ndarray:
+    """x_D uniform on the configs[4] receiver rectangle (y = -2), x_L on one of its
+    three lights (point light or unit squares), w_D* drawn around a few cluster
+    directions per light (caustic-like basins) on the upper hemisphere, type with
+    chain length 1..6 (short chains dominant), w ~ LogNormal(0, 1); a fraction of
+    records are non-samples (w = 0, type = -1), as failed walks are."""
+    rng = np.random.default_rng(seed)
+    r = np.zeros(n, GUIDE_SAMPLE)
+    r["xD"][:, 0] = rng.uniform(-7.5, 10.0, n)
+    r["xD"][:, 1] = -2.0
+    r["xD"][:, 2] = rng.uniform(0.0, 10.0, n)
+    light = rng.integers(0, 3, n)
+    centres = np.array([[-5.0, 4.0, 2.5], [-5.0, 5.0, 7.5], [5.0, 8.0, 5.0]], np.float64)
+    xl = centres[light].copy()
+    area = light > 0
+    xl[area, 0] += rng.uniform(-0.5, 0.5, area.sum())
+    xl[area, 2] += rng.uniform(-0.5, 0.5, area.sum())
+    r["xL"] = xl.astype(np.float32)
+    cdir = rng.normal(size=(n_clusters, 3))
+    cdir[:, 1] = np.abs(cdir[:, 1]) + 0.5
+    cdir /= np.linalg.norm(cdir, axis=1, keepdims=True)
+    cl = rng.integers(0, n_clusters, n)
+    om = cdir[cl] + rng.normal(scale=0.05, size=(n, 3))
+    om /= np.linalg.norm(om, axis=1, keepdims=True)
+    r["omega"] = om.astype(np.float32)
+    length = np.minimum(rng.geometric(0.55, n), 6)
+    tau = (rng.integers(0, 1 << 30, n) & ((1 << length) - 1))
+    r["type"] = ((1 << length) - 2 + tau).astype(np.int32)
+    r["w"] = rng.lognormal(0.0, 1.0, n).astype(np.float32)
+    bad = rng.random(n) < invalid_frac
+    r["w"][bad] = 0.0
+    r["type"][bad] = -1
+    return r
