@@ -52,9 +52,12 @@ enum {
     MPG_SEED_CAP = 0,      /* x_1 uniform by area on the cap of sphere surf_id visible from x_D (init) */
     MPG_SEED_TRIANGLE = 1, /* x_1 uniform in a triangle drawn uniformly among front-facing ones of mesh surf_id */
     MPG_SEED_GUIDE_UV = 2, /* x_1 target from the guide histogram over surface (u,v), defensive alpha=1/2 (Eq. 13) */
-    MPG_SEED_GUIDE_DIR = 3 /* configs[4]: n ~ 1/2 P_0 + 1/2 P_e (Eqs. 10, 13); (w_D, tau) by one-sample MIS of the
+    MPG_SEED_GUIDE_DIR = 3, /* configs[4]: n ~ 1/2 P_0 + 1/2 P_e (Eqs. 10, 13); (w_D, tau) by one-sample MIS of the
                               initializer (w_D uniform on the hemisphere, tau traced) and the learned
                               P_e(tau|n) x direction histogram (Eqs. 8, 11); sampler.k = max chain length (<= 6) */
+    MPG_SEED_GUIDE_STREE = 4 /* the paper's own guide: as GUIDE_DIR, but P_e(n),
+                              P_e(tau|n) come from the STree leaf of (x_D, x_L) and w_D from that leaf's vMF
+                              mixture of type tau (Eq. 12); needs a guide from mpg_guide_create_stree */
 };
 /* per-walk status; "converged" = CONVERGED or OCCLUDED */
 enum {
@@ -197,6 +200,56 @@ mpg_status mpg_scene_create(const mpg_surface_desc *surfaces, int32_t n_surf, co
                             int32_t n_light, void *stream, mpg_scene **out);
 mpg_status mpg_scene_destroy(mpg_scene *scene);
 mpg_status mpg_scene_get_info(const mpg_scene *scene, mpg_scene_info *info);
+
+/* ---- STree + vMF guide (§5.5-5.6; R28-R31) ----
+ * One sub-path sample of an iteration (Eq. 9): its configuration (x_D, x_L), the
+ * solved direction w_D* = normalize(x_1* - x_D), its weight w = T <1/P> and its
+ * chain type 2^n - 2 + tau (n <= 6).  A record is a sample iff w > 0 and
+ * 0 <= type < 126.  48 bytes, device arrays. */
+typedef struct {
+    float xD[3], xL[3], omega[3], w;
+    int32_t type, pad;
+} mpg_guide_sample;
+
+typedef struct {
+    int64_t max_samples;  /* record capacity between two rebuilds (all ranks' records for exchanges) */
+    float eps;            /* overlap fraction of the split (0.1, P:523 footnote)           */
+    float c_thr;          /* leaf threshold c sqrt|S| (1)                           */
+    float kappa_min;      /* vMF concentration clamp (1, R30)                              */
+    float kappa_max;      /* (1e4, R30)                                                    */
+    int32_t max_depth;    /* 32                                                            */
+    int32_t reserved;
+} mpg_stree_desc;
+
+/* counts of the current tree: n_nodes, n_leaves, root_ref (>= 0 node, < 0 ~leaf),
+ * thr, n_valid (samples it was built from), n_lobes */
+typedef struct {
+    int64_t n_nodes, n_leaves, root_ref, thr, n_valid, n_lobes;
+} mpg_stree_info;
+
+/* Create an STree + vMF guide: empty tree (learned branch absent, like mpg_guide_reset). */
+mpg_status mpg_guide_create_stree(const mpg_stree_desc *desc, mpg_guide **out);
+/* Append the n = n_recv*spp walks of one call as sample records (x_L from seeds->xL, w_D* from
+ * walks->chain vertex 0, type from walks->ctype, w from walks->w; records of walks that are
+ * not samples get w = 0).  Asynchronous.  MPG_ERR_INVALID_ARG past max_samples. */
+mpg_status mpg_guide_record_samples(mpg_guide *guide, const mpg_query *query, const mpg_seed_buf *seeds,
+                                    const mpg_walk_buf *walks, int64_t n, void *stream);
+/* Replace the recorded samples by n device records (multi-process exchange, tests). */
+mpg_status mpg_guide_set_samples(mpg_guide *guide, const mpg_guide_sample *records, int64_t n, void *stream);
+/* Copy the recorded samples to device `records` (capacity >= *n on entry; *n = count on return). */
+mpg_status mpg_guide_get_samples(const mpg_guide *guide, mpg_guide_sample *records, int64_t *n, void *stream);
+/* For an STree guide, mpg_guide_rebuild builds the tree and the per-leaf tables on the GPU
+ * from the recorded samples ("last iteration only", P:426 footnote) and clears them; it
+ * synchronizes `stream` once per tree level.  mpg_guide_reset empties the tree. */
+mpg_status mpg_guide_stree_info(const mpg_guide *guide, mpg_stree_info *info);
+/* Device copies of the tree for tests (sizes from mpg_guide_stree_info; any may be NULL):
+ * nodes int4 [n_nodes] (split bits, axis, child0, child1; child < 0 = ~leaf), leaf_begin /
+ * leaf_count int64 [n_leaves] into leaf_ids int32 [n_lobes] (record indices, leaf order),
+ * grp_off int32 [n_leaves][127], lobe_sample int32 [n_lobes], lobe_prefix u64 [n_lobes],
+ * lobe_mu float4 [n_lobes] (mu, kappa), n_prefix u64 [n_leaves][6], type_prefix u64 [n_leaves][126]. */
+mpg_status mpg_guide_download_stree(const mpg_guide *guide, int32_t *nodes, int64_t *leaf_begin, int64_t *leaf_count,
+                                    int32_t *leaf_ids, int32_t *grp_off, int32_t *lobe_sample, uint64_t *lobe_prefix,
+                                    float *lobe_mu, uint64_t *n_prefix, uint64_t *type_prefix, void *stream);
 
 /* Debug/test entry: closest specular (spec_only=1) or any-surface hit of n rays.
  * orig/dir: device float4 [n]; outputs device: t [n], prim [n] (original triangle id or -1),

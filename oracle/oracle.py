@@ -289,6 +289,8 @@ class OracleScene:
         if s.mode == 3:
             nb = s.bins_x * s.bins_y
             self.set_dir_hist(np.zeros((s.cells_x * s.cells_y, 126, nb), np.float32), c)
+        elif s.mode == 4:                      # STree + vMF guide: empty tree (learned branch absent)
+            self.set_stree(stree_build(np.zeros(0, GSAMPLE)), c)
         elif self.w.energies is not None:
             self.set_energies(self.w.energies, c)
         return c

@@ -56,8 +56,11 @@ struct mpg_scene {
     int n_vert = 0;
 };
 
+struct StreeState;
+static void stree_state_free(StreeState *t);
 struct mpg_guide {
     mpg_guide_desc desc;
+    StreeState *stree = nullptr;  // domain 2: STree + vMF guide (stree.cuh)
     int n_cells = 0, n_bins = 0, n_types = 1;
     uint64_t *prefix = nullptr;   // domain 0: [cells][bins]
     float *hist = nullptr;        // [cells][types][bins]
@@ -643,6 +646,7 @@ extern "C" mpg_status mpg_guide_destroy(mpg_guide *g) {
     cudaFree(g->type_prefix);
     cudaFree(g->dir_prefix);
     cudaFree(g->type_energy);
+    stree_state_free(g->stree);
     delete g;
     return MPG_OK;
 }
@@ -775,6 +779,7 @@ __global__ void k_accumulate_dir(const mpg_guide_desc g, const float4 *xD, int s
 
 extern "C" mpg_status mpg_guide_upload(mpg_guide *g, const float *energy, void *stream) {
     ARG_CHECK(g && energy, "NULL argument");
+    ARG_CHECK(!g->stree, "STree guide: use mpg_guide_set_samples + mpg_guide_rebuild");
     if (g->desc.domain == 1) {
         mpg_status st = build_dir_tables(g, energy, as_stream(stream));
         if (st != MPG_OK) return st;
@@ -789,8 +794,14 @@ extern "C" mpg_status mpg_guide_upload(mpg_guide *g, const float *energy, void *
     return MPG_OK;
 }
 
+static mpg_status stree_build(StreeState *T, cudaStream_t st);
+static void stree_clear(StreeState *T);
 extern "C" mpg_status mpg_guide_reset(mpg_guide *g, void *stream) {
     ARG_CHECK(g, "NULL guide");
+    if (g->stree) {
+        stree_clear(g->stree);
+        return stree_build(g->stree, as_stream(stream));
+    }
     CUDA_TRY(cudaMemsetAsync(g->hist, 0, sizeof(float) * (size_t)g->n_cells * g->n_types * g->n_bins,
                              as_stream(stream)));
     if (g->desc.domain == 1) {
@@ -807,6 +818,7 @@ extern "C" mpg_status mpg_guide_reset(mpg_guide *g, void *stream) {
 
 extern "C" mpg_status mpg_guide_accumulate(mpg_guide *g, const mpg_query *q, const mpg_walk_buf *wb, int64_t n,
                                            void *stream) {
+    ARG_CHECK(g && !g->stree, "STree guide: use mpg_guide_record_samples");
     ARG_CHECK(g && q && wb && q->xD && wb->chain && wb->status && wb->w, "NULL argument");
     ARG_CHECK(q->spp >= 1 && n == q->n_recv * q->spp, "n must equal n_recv*spp");
     if (n == 0) return MPG_OK;
@@ -828,6 +840,7 @@ extern "C" mpg_status mpg_guide_accumulate(mpg_guide *g, const mpg_query *q, con
 
 extern "C" mpg_status mpg_guide_rebuild(mpg_guide *g, void *stream) {
     ARG_CHECK(g, "NULL guide");
+    if (g->stree) return stree_build(g->stree, as_stream(stream));
     if (g->desc.domain == 1) {
         mpg_status st = build_dir_tables(g, g->hist, as_stream(stream));
         if (st != MPG_OK) return st;
@@ -842,7 +855,7 @@ extern "C" mpg_status mpg_guide_rebuild(mpg_guide *g, void *stream) {
 }
 
 extern "C" mpg_status mpg_guide_download(const mpg_guide *g, float *energy, uint64_t *prefix, void *stream) {
-    ARG_CHECK(g, "NULL guide");
+    ARG_CHECK(g && !g->stree, "NULL guide or STree guide (use mpg_guide_download_stree)");
     size_t ne = (size_t)g->n_cells * g->n_types * g->n_bins;
     if (energy) CUDA_TRY(cudaMemcpyAsync(energy, g->hist, ne * sizeof(float), cudaMemcpyDeviceToDevice, as_stream(stream)));
     if (prefix) {
@@ -854,6 +867,7 @@ extern "C" mpg_status mpg_guide_download(const mpg_guide *g, float *energy, uint
 
 extern "C" mpg_status mpg_guide_set_histogram(mpg_guide *g, const float *energy, void *stream) {
     ARG_CHECK(g && energy, "NULL argument");
+    ARG_CHECK(!g->stree, "STree guide: use mpg_guide_set_samples");
     size_t ne = (size_t)g->n_cells * g->n_types * g->n_bins;
     CUDA_TRY(cudaMemcpyAsync(g->hist, energy, ne * sizeof(float), cudaMemcpyDeviceToDevice, as_stream(stream)));
     return MPG_OK;
@@ -872,6 +886,8 @@ extern "C" mpg_status mpg_guide_download_dir_tables(const mpg_guide *g, uint64_t
     return MPG_OK;
 }
 
+#include "stree.cuh"
+
 // ----------------------------------------------------------------------------
 // seeds
 // ----------------------------------------------------------------------------
@@ -879,8 +895,8 @@ static mpg_status make_seed_ctx(const mpg_scene *scene, const mpg_guide *guide, 
                                 const mpg_walk_opts *o, SeedCtx &g) {
     memset(&g, 0, sizeof(g));
     ARG_CHECK(sd->k >= 1 && sd->k <= MPG_KMAX, "k must be in [1, 8]");
-    ARG_CHECK(sd->mode >= 0 && sd->mode <= 3, "bad sampler mode");
-    if (sd->mode == 3) ARG_CHECK(sd->k == 6, "GUIDE_DIR samples n <= 6: set k = 6");
+    ARG_CHECK(sd->mode >= 0 && sd->mode <= 4, "bad sampler mode");
+    if (sd->mode >= 3) ARG_CHECK(sd->k == 6, "GUIDE_DIR / GUIDE_STREE sample n <= 6: set k = 6");
     ARG_CHECK(sd->surf_id >= 0 && sd->surf_id < scene->d.n_surf, "sampler surf_id out of range");
     const DSurf &f = scene->d.surf[sd->surf_id];
     if (sd->mode == 0) ARG_CHECK(f.kind == 0, "CAP sampler needs a sphere");
@@ -890,8 +906,20 @@ static mpg_status make_seed_ctx(const mpg_scene *scene, const mpg_guide *guide, 
     g.k = sd->k;
     g.tau = sd->tau & ((1u << sd->k) - 1u);
     g.seed = o->seed;
+    if (sd->mode == 4) {
+        ARG_CHECK(guide && guide->stree && guide->ready, "GUIDE_STREE sampler needs an STree guide");
+        const StreeState *T = guide->stree;
+        g.root_ref = T->root_ref;
+        g.nodes = T->nodes.p;
+        g.grp_off = T->grp_off.p;
+        g.lobe_prefix = T->lobe_prefix.p;
+        g.lobe_mu = T->lobe_mu.p;
+        g.n_prefix = T->n_prefix.p;
+        g.type_prefix = T->type_prefix.p;
+        return MPG_OK;
+    }
     if (sd->mode >= 2) {
-        ARG_CHECK(guide && guide->ready, "guided sampler needs an uploaded/reset guide");
+        ARG_CHECK(guide && !guide->stree && guide->ready, "guided sampler needs an uploaded/reset guide");
         ARG_CHECK(guide->desc.domain == (sd->mode == 3 ? 1 : 0), "sampler mode / guide domain mismatch");
         const mpg_guide_desc &d = guide->desc;
         g.gox = d.grid_origin[0]; g.goz = d.grid_origin[1]; g.gex = d.grid_extent[0]; g.gez = d.grid_extent[1];
@@ -915,7 +943,7 @@ __global__ void k_seeds(const DScene S, const SeedCtx g, const float4 *xD, int64
         float pdf = sample_light(S, g.seed, wid, l, lid);
         xL[i] = make_float4(l.x, l.y, l.z, pdf);
         SeedRes sr;
-        bool ok = seed_target(S, g, wid, 0u, xyz(xD[i / spp]), sr);
+        bool ok = seed_target(S, g, wid, 0u, xyz(xD[i / spp]), l, sr);
         tgt[i] = make_float4(sr.tgt.x, sr.tgt.y, sr.tgt.z, 0.f);
         bin[i] = ok ? sr.bin : -2;
         if (ctype) ctype[i] = (uint32_t)sr.n | ((sr.bits & 255u) << 4) | ((sr.learned ? 1u : 0u) << 12);

@@ -22,6 +22,13 @@ struct SeedCtx {
     const uint64_t *n_prefix;    // [cells][6]
     const uint64_t *type_prefix; // [cells][126]
     const uint32_t *dir_prefix;  // [cells][126][bins]
+    // STree + vMF guide (MPG_SEED_GUIDE_STREE): n_prefix /
+    // type_prefix above are then per leaf
+    int root_ref;                           // >= 0 inner node, < 0: ~leaf
+    const int4 *nodes;                      // (split as bits, axis, child0, child1)
+    const int *grp_off;                     // [leaves][127] lobe offsets of (leaf, type) groups
+    const unsigned long long *lobe_prefix;  // [lobes] inclusive per-group prefix of W_i
+    const float4 *lobe_mu;                  // [lobes] mu (xyz), kappa (w)
 };
 
 // one seed draw: the deduction ray x_D -> tgt gives x_1 (Eq. 6); n = chain
@@ -74,8 +81,43 @@ __device__ __forceinline__ void onb_exact(float3 n, float3 &b1, float3 &b2) {
 
 // Seed target for (walk, trial): the deduction ray x_D -> target gives x_1
 // (Eq. 6).  Returns false if no seed could be drawn (SEED_FAIL).
+// w_D ~ vMF(mu, kappa) (Eq. 12) by the inverse CDF of cos(theta) (R31)
+__device__ __forceinline__ float3 vmf_dir(float4 m, float u1, float u2) {
+    float kap = m.w;
+    float xi = FS(1.0f, u1);
+    float e2k = expf(FM(-2.0f, kap));
+    float ct = FA(1.0f, FD(logf(FA(xi, FM(FS(1.0f, xi), e2k))), kap));
+    ct = fminf(fmaxf(ct, -1.0f), 1.0f);
+    float st2 = FS(1.0f, FM(ct, ct));
+    float st = __fsqrt_rn(st2 > 0.0f ? st2 : 0.0f);
+    float phi = FM(6.28318530717958647692f, u2);
+    float cp = cosf(phi), sp = sinf(phi);
+    float3 b1, b2;
+    float3 mu = f3(m.x, m.y, m.z);
+    onb_exact(mu, b1, b2);
+    return f3(FA(FM(ct, mu.x), FM(st, FA(FM(cp, b1.x), FM(sp, b2.x)))),
+              FA(FM(ct, mu.y), FM(st, FA(FM(cp, b1.y), FM(sp, b2.y)))),
+              FA(FM(ct, mu.z), FM(st, FA(FM(cp, b1.z), FM(sp, b2.z)))));
+}
+
+__device__ __forceinline__ float canon0(float x) { return __fadd_rn(x, 0.0f); } // -0 -> +0 (R28)
+
+// leaf of the STree containing (x_D, x_L) (R28)
+__device__ __forceinline__ int stree_leaf(const SeedCtx &g, float3 xD, float3 xL) {
+    float p[6] = {canon0(xD.x), canon0(xD.y), canon0(xD.z), canon0(xL.x), canon0(xL.y), canon0(xL.z)};
+    int ref = g.root_ref;
+    while (ref >= 0) {
+        int4 nd = __ldg(g.nodes + ref);
+        float v = p[0];
+#pragma unroll
+        for (int a = 1; a < 6; a++) v = nd.y == a ? p[a] : v;
+        ref = v < __int_as_float(nd.x) ? nd.z : nd.w;
+    }
+    return ~ref;
+}
+
 __device__ MPG_COLD bool seed_target(const DScene &S, const SeedCtx &g, uint64_t wid, uint32_t trial,
-                                            float3 xD, SeedRes &sr) {
+                                            float3 xD, float3 xL, SeedRes &sr) {
     float3 &tgt = sr.tgt;
     int &bin = sr.bin;
     bin = -1;
@@ -153,8 +195,9 @@ __device__ MPG_COLD bool seed_target(const DScene &S, const SeedCtx &g, uint64_t
         tgt = f3(FA(g.uvox, FM(u, g.uvsx)), g.uv_y, FA(g.uvoz, FM(v, g.uvsz)));
         return true;
     }
-    if (g.mode == 3) { // configs[4]: n ~ 1/2 P_0 + 1/2 P_e, then one-sample MIS for (w_D, tau) (R22)
-        int c = seed_cell(g, xD);
+    if (g.mode == 3 || g.mode == 4) { // configs[4]: n ~ 1/2 P_0 + 1/2 P_e, then one-sample MIS for (w_D, tau)
+        // (R22); mode 4: P_e from the STree leaf of (x_D, x_L), w_D from its vMF mixture (R28-R31)
+        int c = g.mode == 3 ? seed_cell(g, xD) : stree_leaf(g, xD, xL);
         const unsigned long long *npf = (const unsigned long long *)g.n_prefix + (size_t)c * 6;
         uint4 r0 = rng_draw(g.seed, wid, 1u, 0u); // n is reused by every trial
         uint64_t S6 = __ldg(npf + 5);
@@ -176,6 +219,23 @@ __device__ MPG_COLD bool seed_target(const DScene &S, const SeedCtx &g, uint64_t
             while ((uint64_t)__ldg(tpf + m) <= tt) m++;
             sr.bits = (uint32_t)m;
             sr.learned = true;
+            if (g.mode == 4) { // lobe ~ W_i, then w_D ~ vMF(mu_i, kappa_i) (Eq. 12)
+                const int *go = g.grp_off + (size_t)c * 127 + g0 + m;
+                int glo = __ldg(go), ghi = __ldg(go + 1);
+                uint64_t Sl = __ldg(g.lobe_prefix + ghi - 1);
+                uint64_t tl = mulhi_u64(r.w, Sl);
+                int lo2 = glo, hi2 = ghi - 1; // upper_bound over the group
+                while (lo2 < hi2) {
+                    int mid = (lo2 + hi2) >> 1;
+                    if ((uint64_t)__ldg(g.lobe_prefix + mid) > tl) hi2 = mid;
+                    else lo2 = mid + 1;
+                }
+                bin = lo2;
+                uint4 r2 = rng_draw(g.seed, wid, 2u, trial);
+                float3 om = vmf_dir(__ldg(g.lobe_mu + lo2), u01(r2.x), u01(r2.y));
+                tgt = f3(FA(xD.x, om.x), FA(xD.y, om.y), FA(xD.z, om.z));
+                return true;
+            }
             int nb = g.bins_x * g.bins_y;
             const uint32_t *dpf = g.dir_prefix + ((size_t)c * 126 + g0 + m) * nb;
             uint64_t Sd = __ldg(dpf + nb - 1);

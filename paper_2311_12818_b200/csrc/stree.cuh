@@ -1,0 +1,637 @@
+// stree.cuh -- the paper's own guide on the GPU: an STree over the
+// 6D configuration (x_D, x_L) with per-leaf length / type tables and vMF mixtures
+// of the solved directions (§5.5-5.6; Eqs. 9-13; readings
+// R28-R31 in DESIGN.md).  Included by mpg.cu after the histogram guide.
+//
+// Build (mpg_guide_rebuild), level-synchronous and deterministic:
+//   k_stree_valid      flags + exact fp32 bbox of the sample keys (warp min/max, atomics)
+//   DeviceSelect       ids of the samples, record order
+//   per level          keys (ordered coordinate << 32 | record id) of the level's ids;
+//                      cub segmented sort of the splitting nodes' segments; k_stree_split
+//                      (one thread per node: plane, overlap windows by binary search);
+//                      the host lays out the child windows (prefix sums over a few
+//                      thousand nodes) and k_copy_segments writes the next level
+//   lobes              radix sort by (leaf, type, position) = stable partition by type;
+//                      k_grp_off, k_lobe_kappa (nearest direction in the group),
+//                      k_group_tables (E_tau in fp64, integer lobe weights), then the
+//                      per-leaf length / type tables of the histogram guide (k_dir_cell_tables)
+// Children are contiguous windows of the parent's sorted list, so the build is a
+// sequence of sorts and copies; no atomics decide anything.
+#pragma once
+#include <cub/device/device_segmented_sort.cuh>
+#include <cub/device/device_select.cuh>
+#include <thrust/iterator/counting_iterator.h>
+
+template <class T> struct DBuf {
+    T *p = nullptr;
+    size_t cap = 0;
+    cudaError_t reserve(size_t n) { // contents not kept
+        if (n <= cap && p) return cudaSuccess;
+        cudaFree(p);
+        p = nullptr;
+        cap = 0;
+        size_t c = std::max<size_t>(n, 1) * 5 / 4 + 16;
+        cudaError_t e = cudaMalloc(&p, c * sizeof(T));
+        if (e == cudaSuccess) cap = c;
+        return e;
+    }
+    cudaError_t reserve_keep(size_t n, size_t used, cudaStream_t s) {
+        if (n <= cap && p) return cudaSuccess;
+        T *q = nullptr;
+        size_t c = std::max<size_t>(n, 1) * 3 / 2 + 16;
+        cudaError_t e = cudaMalloc(&q, c * sizeof(T));
+        if (e != cudaSuccess) return e;
+        if (used) e = cudaMemcpyAsync(q, p, used * sizeof(T), cudaMemcpyDeviceToDevice, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        cudaFree(p);
+        p = q;
+        cap = c;
+        return e;
+    }
+    void release() {
+        cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+};
+
+struct StreeState {
+    mpg_stree_desc d;
+    DBuf<mpg_guide_sample> rec;
+    int64_t n_rec = 0;
+    // current tree
+    int root_ref = ~0, n_nodes = 0, n_leaves = 0, thr = 1;
+    int64_t n_valid = 0, n_lobes = 0;
+    DBuf<int4> nodes;
+    DBuf<int64_t> leaf_begin, leaf_count;
+    DBuf<int> leaf_ids, grp_off, lobe_sample;
+    DBuf<unsigned long long> lobe_prefix;
+    DBuf<float4> lobe_mu;
+    DBuf<uint64_t> n_prefix, type_prefix;
+    DBuf<double> E;
+    // scratch
+    DBuf<unsigned char> flags;
+    DBuf<int> ids_a, ids_b, seg_b, seg_e, nv;
+    DBuf<unsigned long long> keys_a, keys_b;
+    DBuf<unsigned char> temp;
+    DBuf<unsigned int> bbox;
+    DBuf<float2> lohi;
+    DBuf<int4> split_out, segs;
+    DBuf<float> split_c;
+};
+
+static void stree_state_free(StreeState *t) {
+    if (!t) return;
+    t->rec.release(); t->nodes.release(); t->leaf_begin.release(); t->leaf_count.release();
+    t->leaf_ids.release(); t->grp_off.release(); t->lobe_sample.release(); t->lobe_prefix.release();
+    t->lobe_mu.release(); t->n_prefix.release(); t->type_prefix.release(); t->E.release();
+    t->flags.release(); t->ids_a.release(); t->ids_b.release(); t->seg_b.release(); t->seg_e.release();
+    t->nv.release(); t->keys_a.release(); t->keys_b.release(); t->temp.release(); t->bbox.release();
+    t->lohi.release(); t->split_out.release(); t->segs.release(); t->split_c.release();
+    delete t;
+}
+
+__device__ __forceinline__ bool gs_valid(const mpg_guide_sample &r) { return r.w > 0.0f && r.type >= 0 && r.type < 126; }
+__device__ __forceinline__ float gs_key(const mpg_guide_sample &r, int a) {
+    return canon0(a < 3 ? r.xD[a] : r.xL[a - 3]);
+}
+// order-preserving float <-> u32 (keys never hold -0, R28)
+__device__ __forceinline__ unsigned f2o(float x) {
+    unsigned u = __float_as_uint(x);
+    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float o2f(unsigned u) { return __uint_as_float((u & 0x80000000u) ? (u & 0x7fffffffu) : ~u); }
+
+// sample flags and the exact fp32 bbox of the keys (min/max are order-independent)
+__global__ void k_stree_valid(const mpg_guide_sample *rec, int64_t n, unsigned char *flags, unsigned *bbox) {
+    unsigned mn[6], mx[6];
+#pragma unroll
+    for (int a = 0; a < 6; a++) { mn[a] = 0xffffffffu; mx[a] = 0u; }
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        mpg_guide_sample r = rec[i];
+        bool v = gs_valid(r);
+        flags[i] = v ? 1 : 0;
+        if (v) {
+#pragma unroll
+            for (int a = 0; a < 6; a++) {
+                unsigned o = f2o(gs_key(r, a));
+                mn[a] = min(mn[a], o);
+                mx[a] = max(mx[a], o);
+            }
+        }
+    }
+#pragma unroll
+    for (int a = 0; a < 6; a++) {
+        unsigned m0 = __reduce_min_sync(MPG_FULL, mn[a]), m1 = __reduce_max_sync(MPG_FULL, mx[a]);
+        if ((threadIdx.x & 31) == 0) {
+            atomicMin(bbox + a, m0);
+            atomicMax(bbox + 6 + a, m1);
+        }
+    }
+}
+
+__global__ void k_level_keys(const mpg_guide_sample *rec, const int *ids, int64_t n, int axis,
+                             unsigned long long *keys) {
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+        int id = ids[j];
+        keys[j] = ((unsigned long long)f2o(gs_key(rec[id], axis)) << 32) | (unsigned)id;
+    }
+}
+
+// one thread per splitting node (R28, R29): plane c, copies eL/eR, discard bounds s0/s1
+__global__ void k_stree_split(const unsigned long long *keys, const int *seg_b, const int *seg_e, const float2 *lohi,
+                              int n_nodes, float eps, int4 *out, float *cout) {
+    int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n_nodes) return;
+    const unsigned long long *K = keys + seg_b[t];
+    int k = seg_e[t] - seg_b[t];
+    float lo = lohi[t].x, hi = lohi[t].y;
+    float c = FM(FA(lo, hi), 0.5f);
+    float delta = FM(FS(hi, lo), 0.25f);
+    auto x = [&](int j) { return o2f((unsigned)(K[j] >> 32)); };
+    // first index in [a, b) where pred holds, pred monotone false..true
+    auto first = [&](int a, int b, auto pred) {
+        while (a < b) {
+            int mid = (a + b) >> 1;
+            if (pred(mid)) b = mid;
+            else a = mid + 1;
+        }
+        return a;
+    };
+    int m = first(0, k, [&](int j) { return !(x(j) < c); });
+    long long E = (long long)floor((double)eps * (double)k);
+    int cR = first(m, k, [&](int j) { return FS(x(j), c) > delta; }) - m;
+    int cL = m - first(0, m, [&](int j) { return FS(c, x(j)) <= delta; });
+    int eR = (int)min((long long)cR, E), eL = (int)min((long long)cL, E);
+    int s0 = first(0, m, [&](int j) { return FS(lo, x(j)) <= delta; });
+    int s1 = first(m, k, [&](int j) { return FS(x(j), hi) > delta; });
+    out[2 * t] = make_int4(m, eL, eR, s0);
+    out[2 * t + 1] = make_int4(s1, 0, 0, 0);
+    cout[t] = c;
+}
+
+// one block per segment (src, dst, len): ids from sorted keys (low word) or plain ids
+template <class S>
+__global__ void k_copy_segments(const S *src, int *dst, const int4 *segs) {
+    int4 g = segs[blockIdx.x];
+    for (int j = threadIdx.x; j < g.z; j += blockDim.x) dst[g.y + j] = (int)(unsigned)src[g.x + j];
+}
+
+__global__ void k_lobe_keys(const mpg_guide_sample *rec, const int *leaf_ids, const int64_t *lb, const int64_t *lc,
+                            unsigned long long *keys) {
+    int l = blockIdx.x;
+    int64_t b = lb[l], n = lc[l];
+    for (int64_t j = threadIdx.x; j < n; j += blockDim.x) {
+        int64_t pos = b + j;
+        keys[pos] = ((unsigned long long)l << 40) | ((unsigned long long)rec[leaf_ids[pos]].type << 32) |
+                    (unsigned long long)(unsigned)pos;
+    }
+}
+
+__global__ void k_lobe_sample(const unsigned long long *keys, const int *leaf_ids, int64_t n, int *lobe_sample) {
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x)
+        lobe_sample[j] = leaf_ids[(unsigned)keys[j]];
+}
+
+// grp_off[leaf][t] = first lobe with (leaf, type) >= (leaf, t), t = 0..126
+__global__ void k_grp_off(const unsigned long long *keys, int64_t n, int n_leaves, int *grp_off) {
+    int id = blockIdx.x * blockDim.x + threadIdx.x;
+    if (id >= n_leaves * 127) return;
+    unsigned long long q = ((unsigned long long)(id / 127) << 40) | ((unsigned long long)(id % 127) << 32);
+    int64_t a = 0, b = n;
+    while (a < b) {
+        int64_t mid = (a + b) >> 1;
+        if (keys[mid] >= q) b = mid;
+        else a = mid + 1;
+    }
+    grp_off[id] = (int)a;
+}
+
+// vMF lobes (R30): mu = w_D*, kappa = 1 / (nearest chord distance)^2 in the (leaf, type) group
+__global__ void k_lobe_kappa(const mpg_guide_sample *rec, const unsigned long long *keys, const int *lobe_sample,
+                             const int *grp_off, int64_t n, float kmin, float kmax, float4 *lobe_mu) {
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+        unsigned long long key = keys[j];
+        int g = (int)(key >> 40) * 127 + (int)((key >> 32) & 0xffu);
+        int glo = grp_off[g], ghi = grp_off[g + 1];
+        const mpg_guide_sample &ri = rec[lobe_sample[j]];
+        float ox = ri.omega[0], oy = ri.omega[1], oz = ri.omega[2];
+        float d2min = __int_as_float(0x7f800000);
+        for (int q = glo; q < ghi; q++) {
+            if (q == (int)j) continue;
+            const mpg_guide_sample &rj = rec[lobe_sample[q]];
+            float dx = FS(ox, rj.omega[0]), dy = FS(oy, rj.omega[1]), dz = FS(oz, rj.omega[2]);
+            float d2 = FA(FA(FM(dx, dx), FM(dy, dy)), FM(dz, dz));
+            d2min = fminf(d2min, d2);
+        }
+        float kap = ghi - glo == 1 ? kmin : (d2min > 0.0f ? FD(1.0f, d2min) : kmax);
+        kap = fminf(fmaxf(kap, kmin), kmax);
+        lobe_mu[j] = make_float4(ox, oy, oz, kap);
+    }
+}
+
+// per (leaf, type): E_tau (fp64, group order) and the integer lobe weights' prefix (R30)
+__global__ void k_group_tables(const mpg_guide_sample *rec, const int *lobe_sample, const int *grp_off, int n_leaves,
+                               double *E, unsigned long long *lobe_prefix) {
+    int id = blockIdx.x * blockDim.x + threadIdx.x;
+    if (id >= n_leaves * 126) return;
+    int l = id / 126, t = id % 126;
+    int glo = grp_off[l * 127 + t], ghi = grp_off[l * 127 + t + 1];
+    double e = 0.0;
+    float wmax = 0.0f;
+    for (int q = glo; q < ghi; q++) {
+        float w = rec[lobe_sample[q]].w;
+        e = __dadd_rn(e, (double)w);
+        wmax = fmaxf(wmax, w);
+    }
+    E[(size_t)l * 126 + t] = e;
+    unsigned long long acc = 0;
+    for (int q = glo; q < ghi; q++) {
+        float w = rec[lobe_sample[q]].w;
+        unsigned long long W = (unsigned long long)floorf(FM(FD(w, wmax), 1048576.0f));
+        if (W < 1ull) W = 1ull;
+        acc += W;
+        lobe_prefix[q] = acc;
+    }
+}
+
+// sample records of one walk call (Eq. 9 samples; mirrors orc_record_samples)
+__global__ void k_record(mpg_guide_sample *out, const float4 *xD, int spp, const float4 *xL, const float4 *chain0,
+                         const uint8_t *status, const float *w, const uint16_t *ctype, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        mpg_guide_sample r;
+        float4 d = xD[i / spp], l = xL[i];
+        r.xD[0] = d.x; r.xD[1] = d.y; r.xD[2] = d.z;
+        r.xL[0] = l.x; r.xL[1] = l.y; r.xL[2] = l.z;
+        r.omega[0] = r.omega[1] = r.omega[2] = 0.0f;
+        r.w = 0.0f;
+        r.type = -1;
+        r.pad = 0;
+        uint32_t ct = ctype[i];
+        int kk = (int)(ct & 15u);
+        if (status[i] == 0 && w[i] > 0.0f && kk >= 1 && kk <= 6) {
+            float4 x1 = chain0[i];
+            float dx = FS(x1.x, d.x), dy = FS(x1.y, d.y), dz = FS(x1.z, d.z);
+            float ln = __fsqrt_rn(FA(FA(FM(dx, dx), FM(dy, dy)), FM(dz, dz)));
+            r.omega[0] = FD(dx, ln); r.omega[1] = FD(dy, ln); r.omega[2] = FD(dz, ln);
+            r.type = (1 << kk) - 2 + (int)(ct >> 4);
+            r.w = w[i];
+        }
+        out[i] = r;
+    }
+}
+
+#define ST_TRY(expr)                                                                                    \
+    do {                                                                                                \
+        cudaError_t e_ = (expr);                                                                        \
+        if (e_ != cudaSuccess)                                                                          \
+            return fail(e_ == cudaErrorMemoryAllocation ? MPG_ERR_OOM : MPG_ERR_CUDA,                   \
+                        std::string("stree build: ") + #expr + ": " + cudaGetErrorString(e_));          \
+    } while (0)
+
+struct HNode {
+    int64_t b, n;
+    float lo[6], hi[6];
+    int depth, parent, side;
+};
+
+static inline float host_o2f(unsigned u) {
+    unsigned v = (u & 0x80000000u) ? (u & 0x7fffffffu) : ~u;
+    float f;
+    memcpy(&f, &v, 4);
+    return f;
+}
+
+// Build the tree and tables from the recorded samples (R28-R31); synchronous on st.
+static mpg_status stree_build(StreeState *T, cudaStream_t st) {
+    const int64_t n = T->n_rec;
+    const int nsm = 148;
+    // 1. sample ids (record order) and the root box
+    ST_TRY(T->flags.reserve(n));
+    ST_TRY(T->ids_a.reserve(n));
+    ST_TRY(T->bbox.reserve(12));
+    ST_TRY(T->nv.reserve(1));
+    unsigned init[12];
+    for (int a = 0; a < 6; a++) { init[a] = 0xffffffffu; init[6 + a] = 0u; }
+    ST_TRY(cudaMemcpyAsync(T->bbox.p, init, sizeof(init), cudaMemcpyHostToDevice, st));
+    int64_t nv = 0;
+    unsigned bb[12];
+    memcpy(bb, init, sizeof(bb));
+    if (n > 0) {
+        COUNT_LAUNCH(1);
+        k_stree_valid<<<(int)std::min<int64_t>((n + 255) / 256, nsm * 8), 256, 0, st>>>(T->rec.p, n, T->flags.p,
+                                                                                         T->bbox.p);
+        ST_TRY(cudaPeekAtLastError());
+        size_t tb = 0;
+        thrust::counting_iterator<int> it(0);
+        ST_TRY(cub::DeviceSelect::Flagged(nullptr, tb, it, T->flags.p, T->ids_a.p, T->nv.p, (int)n, st));
+        ST_TRY(T->temp.reserve(tb));
+        ST_TRY(cub::DeviceSelect::Flagged(T->temp.p, tb, it, T->flags.p, T->ids_a.p, T->nv.p, (int)n, st));
+        int nvi = 0;
+        ST_TRY(cudaMemcpyAsync(&nvi, T->nv.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+        ST_TRY(cudaMemcpyAsync(bb, T->bbox.p, sizeof(bb), cudaMemcpyDeviceToHost, st));
+        ST_TRY(cudaStreamSynchronize(st));
+        nv = nvi;
+    }
+    T->n_valid = nv;
+    double thr_d = floor((double)T->d.c_thr * sqrt((double)nv));
+    T->thr = thr_d < 1.0 ? 1 : (int)thr_d;
+    HNode root;
+    root.b = 0;
+    root.n = nv;
+    for (int a = 0; a < 6; a++) {
+        root.lo[a] = nv ? host_o2f(bb[a]) : 0.f;
+        root.hi[a] = nv ? host_o2f(bb[6 + a]) : 0.f;
+    }
+    root.depth = 0;
+    root.parent = -1;
+    root.side = 0;
+    int active[6], na = 0;
+    for (int a = 0; a < 6; a++)
+        if (nv > 0 && root.hi[a] > root.lo[a]) active[na++] = a;
+    // 2. levels
+    std::vector<HNode> level{root}, next;
+    std::vector<int4> hnodes, segs;
+    std::vector<int64_t> lb, lc;
+    std::vector<int> sb, se, split_idx;
+    std::vector<float2> lohi;
+    int64_t leaf_total = 0;
+    int n_leaves = 0;
+    int root_ref = ~0;
+    int *cur = T->ids_a.p;
+    bool cur_is_a = true;
+    while (!level.empty()) {
+        split_idx.clear();
+        segs.clear();
+        const int depth = level[0].depth;
+        const int64_t leaf_prev = leaf_total;
+        for (size_t i = 0; i < level.size(); i++) {
+            HNode &nd = level[i];
+            int ref;
+            if (nd.n <= T->thr || nd.depth >= T->d.max_depth || na == 0) {
+                ref = ~n_leaves++;
+                lb.push_back(leaf_total);
+                lc.push_back(nd.n);
+                if (nd.n > 0) segs.push_back(make_int4((int)nd.b, (int)leaf_total, (int)nd.n, 0));
+                leaf_total += nd.n;
+            } else {
+                ref = (int)hnodes.size();
+                hnodes.push_back(make_int4(0, active[depth % std::max(na, 1)], 0, 0));
+                split_idx.push_back((int)i);
+            }
+            if (nd.parent < 0) root_ref = ref;
+            else if (nd.side == 0) hnodes[nd.parent].z = ref;
+            else hnodes[nd.parent].w = ref;
+        }
+        ARG_CHECK(leaf_total < (1ll << 31) && n_leaves < (1 << 23), "STree too large (lobes >= 2^31 or leaves >= 2^23)");
+        if (!segs.empty()) { // leaf lists of this level -> leaf_ids
+            ST_TRY(T->leaf_ids.reserve_keep(leaf_total, leaf_prev, st));
+            ST_TRY(T->segs.reserve(segs.size()));
+            ST_TRY(cudaMemcpyAsync(T->segs.p, segs.data(), segs.size() * sizeof(int4), cudaMemcpyHostToDevice, st));
+            COUNT_LAUNCH(1);
+            k_copy_segments<int><<<(int)segs.size(), 128, 0, st>>>(cur, T->leaf_ids.p, T->segs.p);
+            ST_TRY(cudaPeekAtLastError());
+            ST_TRY(cudaStreamSynchronize(st)); // host vectors are reused below
+        }
+        if (split_idx.empty()) break;
+        const int a = active[depth % na];
+        int64_t n_cur = 0;
+        for (auto &nd : level) n_cur = std::max<int64_t>(n_cur, nd.b + nd.n);
+        sb.clear(); se.clear(); lohi.clear();
+        for (int i : split_idx) {
+            sb.push_back((int)level[i].b);
+            se.push_back((int)(level[i].b + level[i].n));
+            lohi.push_back(make_float2(level[i].lo[a], level[i].hi[a]));
+        }
+        const int ns = (int)split_idx.size();
+        ST_TRY(T->keys_a.reserve(n_cur));
+        ST_TRY(T->keys_b.reserve(n_cur));
+        ST_TRY(T->seg_b.reserve(ns));
+        ST_TRY(T->seg_e.reserve(ns));
+        ST_TRY(T->lohi.reserve(ns));
+        ST_TRY(T->split_out.reserve(2 * ns));
+        ST_TRY(T->split_c.reserve(ns));
+        ST_TRY(cudaMemcpyAsync(T->seg_b.p, sb.data(), ns * sizeof(int), cudaMemcpyHostToDevice, st));
+        ST_TRY(cudaMemcpyAsync(T->seg_e.p, se.data(), ns * sizeof(int), cudaMemcpyHostToDevice, st));
+        ST_TRY(cudaMemcpyAsync(T->lohi.p, lohi.data(), ns * sizeof(float2), cudaMemcpyHostToDevice, st));
+        COUNT_LAUNCH(1);
+        k_level_keys<<<(int)std::min<int64_t>((n_cur + 255) / 256, nsm * 8), 256, 0, st>>>(T->rec.p, cur, n_cur, a,
+                                                                                            T->keys_a.p);
+        ST_TRY(cudaPeekAtLastError());
+        size_t tb = 0;
+        ST_TRY(cub::DeviceSegmentedSort::SortKeys(nullptr, tb, T->keys_a.p, T->keys_b.p, (int)n_cur, ns, T->seg_b.p,
+                                                  T->seg_e.p, st));
+        ST_TRY(T->temp.reserve(tb));
+        ST_TRY(cub::DeviceSegmentedSort::SortKeys(T->temp.p, tb, T->keys_a.p, T->keys_b.p, (int)n_cur, ns, T->seg_b.p,
+                                                  T->seg_e.p, st));
+        COUNT_LAUNCH(1);
+        k_stree_split<<<(ns + 127) / 128, 128, 0, st>>>(T->keys_b.p, T->seg_b.p, T->seg_e.p, T->lohi.p, ns, T->d.eps,
+                                                        T->split_out.p, T->split_c.p);
+        ST_TRY(cudaPeekAtLastError());
+        std::vector<int4> so(2 * ns);
+        std::vector<float> sc(ns);
+        ST_TRY(cudaMemcpyAsync(so.data(), T->split_out.p, 2 * ns * sizeof(int4), cudaMemcpyDeviceToHost, st));
+        ST_TRY(cudaMemcpyAsync(sc.data(), T->split_c.p, ns * sizeof(float), cudaMemcpyDeviceToHost, st));
+        ST_TRY(cudaStreamSynchronize(st));
+        next.clear();
+        segs.clear();
+        int64_t off = 0;
+        int node_id = (int)hnodes.size() - ns;
+        for (int q = 0; q < ns; q++, node_id++) {
+            const HNode &nd = level[split_idx[q]];
+            int m = so[2 * q].x, eL = so[2 * q].y, eR = so[2 * q].z, s0 = so[2 * q].w, s1 = so[2 * q + 1].x;
+            float c = sc[q];
+            int cbits;
+            memcpy(&cbits, &c, 4);
+            hnodes[node_id].x = cbits;
+            for (int side = 0; side < 2; side++) {
+                HNode ch = nd;
+                int64_t b0 = side == 0 ? s0 : m - eL, b1 = side == 0 ? m + eR : s1;
+                if (side == 0) ch.hi[a] = c;
+                else ch.lo[a] = c;
+                ch.b = off;
+                ch.n = b1 - b0;
+                ch.depth = nd.depth + 1;
+                ch.parent = node_id;
+                ch.side = side;
+                if (ch.n > 0) segs.push_back(make_int4((int)(nd.b + b0), (int)off, (int)ch.n, 0));
+                off += ch.n;
+                next.push_back(ch);
+            }
+        }
+        ARG_CHECK(off < (1ll << 31), "STree level too large");
+        DBuf<int> &dst = cur_is_a ? T->ids_b : T->ids_a;
+        ST_TRY(dst.reserve(off));
+        if (!segs.empty()) {
+            ST_TRY(T->segs.reserve(segs.size()));
+            ST_TRY(cudaMemcpyAsync(T->segs.p, segs.data(), segs.size() * sizeof(int4), cudaMemcpyHostToDevice, st));
+            COUNT_LAUNCH(1);
+            k_copy_segments<unsigned long long><<<(int)segs.size(), 128, 0, st>>>(T->keys_b.p, dst.p, T->segs.p);
+            ST_TRY(cudaPeekAtLastError());
+            ST_TRY(cudaStreamSynchronize(st));
+        }
+        cur = dst.p;
+        cur_is_a = !cur_is_a;
+        level.swap(next);
+    }
+    // 3. tree upload
+    T->root_ref = root_ref;
+    T->n_nodes = (int)hnodes.size();
+    T->n_leaves = n_leaves;
+    T->n_lobes = leaf_total;
+    ST_TRY(T->nodes.reserve(hnodes.size()));
+    ST_TRY(T->leaf_begin.reserve(n_leaves));
+    ST_TRY(T->leaf_count.reserve(n_leaves));
+    if (!hnodes.empty())
+        ST_TRY(cudaMemcpyAsync(T->nodes.p, hnodes.data(), hnodes.size() * sizeof(int4), cudaMemcpyHostToDevice, st));
+    ST_TRY(cudaMemcpyAsync(T->leaf_begin.p, lb.data(), n_leaves * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+    ST_TRY(cudaMemcpyAsync(T->leaf_count.p, lc.data(), n_leaves * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+    // 4. lobes grouped by (leaf, type), stable within the leaf's list
+    const int64_t NL = leaf_total;
+    ST_TRY(T->grp_off.reserve((size_t)n_leaves * 127));
+    ST_TRY(T->E.reserve((size_t)n_leaves * 126));
+    ST_TRY(T->n_prefix.reserve((size_t)n_leaves * 6));
+    ST_TRY(T->type_prefix.reserve((size_t)n_leaves * 126));
+    ST_TRY(T->lobe_sample.reserve(NL));
+    ST_TRY(T->lobe_prefix.reserve(NL));
+    ST_TRY(T->lobe_mu.reserve(NL));
+    ST_TRY(T->keys_a.reserve(NL));
+    ST_TRY(T->keys_b.reserve(NL));
+    if (NL > 0) {
+        COUNT_LAUNCH(1);
+        k_lobe_keys<<<n_leaves, 128, 0, st>>>(T->rec.p, T->leaf_ids.p, T->leaf_begin.p, T->leaf_count.p, T->keys_a.p);
+        ST_TRY(cudaPeekAtLastError());
+        int lbits = 1;
+        while ((1 << lbits) < n_leaves) lbits++;
+        size_t tb = 0;
+        ST_TRY(cub::DeviceRadixSort::SortKeys(nullptr, tb, T->keys_a.p, T->keys_b.p, (int)NL, 0, 40 + lbits, st));
+        ST_TRY(T->temp.reserve(tb));
+        ST_TRY(cub::DeviceRadixSort::SortKeys(T->temp.p, tb, T->keys_a.p, T->keys_b.p, (int)NL, 0, 40 + lbits, st));
+        int blocks = (int)std::min<int64_t>((NL + 255) / 256, nsm * 8);
+        COUNT_LAUNCH(1);
+        k_lobe_sample<<<blocks, 256, 0, st>>>(T->keys_b.p, T->leaf_ids.p, NL, T->lobe_sample.p);
+        ST_TRY(cudaPeekAtLastError());
+    }
+    COUNT_LAUNCH(1);
+    k_grp_off<<<(n_leaves * 127 + 255) / 256, 256, 0, st>>>(T->keys_b.p, NL, n_leaves, T->grp_off.p);
+    ST_TRY(cudaPeekAtLastError());
+    if (NL > 0) {
+        COUNT_LAUNCH(1);
+        k_lobe_kappa<<<(int)std::min<int64_t>((NL + 127) / 128, nsm * 16), 128, 0, st>>>(
+            T->rec.p, T->keys_b.p, T->lobe_sample.p, T->grp_off.p, NL, T->d.kappa_min, T->d.kappa_max, T->lobe_mu.p);
+        ST_TRY(cudaPeekAtLastError());
+    }
+    COUNT_LAUNCH(1);
+    k_group_tables<<<(n_leaves * 126 + 127) / 128, 128, 0, st>>>(T->rec.p, T->lobe_sample.p, T->grp_off.p, n_leaves,
+                                                                  T->E.p, T->lobe_prefix.p);
+    ST_TRY(cudaPeekAtLastError());
+    COUNT_LAUNCH(1);
+    k_dir_cell_tables<<<(n_leaves + 127) / 128, 128, 0, st>>>(T->E.p, n_leaves, T->n_prefix.p, T->type_prefix.p);
+    ST_TRY(cudaPeekAtLastError());
+    ST_TRY(cudaStreamSynchronize(st));
+    T->n_rec = 0; // "last iteration only" (P:426 footnote)
+    return MPG_OK;
+}
+
+extern "C" mpg_status mpg_guide_create_stree(const mpg_stree_desc *desc, mpg_guide **out) {
+    ARG_CHECK(desc && out, "NULL argument");
+    ARG_CHECK(desc->max_samples >= 0 && desc->max_samples < (1ll << 31), "max_samples must be in [0, 2^31)");
+    ARG_CHECK(desc->eps >= 0.f && desc->eps < 0.5f, "eps must be in [0, 0.5)");
+    ARG_CHECK(desc->c_thr > 0.f, "c_thr must be > 0");
+    ARG_CHECK(desc->kappa_min > 0.f && desc->kappa_max >= desc->kappa_min, "bad kappa clamp");
+    ARG_CHECK(desc->max_depth >= 0 && desc->max_depth <= 64, "max_depth must be in [0, 64]");
+    mpg_guide *g = new mpg_guide();
+    memset(&g->desc, 0, sizeof(g->desc));
+    g->desc.domain = 2;
+    g->desc.n_types = 126;
+    g->n_types = 126;
+    g->stree = new StreeState();
+    g->stree->d = *desc;
+    if (g->stree->rec.reserve(desc->max_samples) != cudaSuccess) {
+        mpg_guide_destroy(g);
+        return fail(MPG_ERR_OOM, "STree sample buffer allocation failed");
+    }
+    cudaStream_t s0 = 0;
+    mpg_status st = stree_build(g->stree, s0); // empty tree
+    if (st != MPG_OK) {
+        mpg_guide_destroy(g);
+        return st;
+    }
+    g->ready = true;
+    *out = g;
+    return MPG_OK;
+}
+
+extern "C" mpg_status mpg_guide_record_samples(mpg_guide *g, const mpg_query *q, const mpg_seed_buf *sb,
+                                               const mpg_walk_buf *wb, int64_t n, void *stream) {
+    ARG_CHECK(g && g->stree && q && sb && wb, "needs an STree guide and query/seeds/walks");
+    ARG_CHECK(q->xD && sb->xL && wb->chain && wb->status && wb->w && wb->ctype, "NULL array");
+    ARG_CHECK(q->spp >= 1 && n == q->n_recv * q->spp, "n must equal n_recv*spp");
+    StreeState *T = g->stree;
+    ARG_CHECK(T->n_rec + n <= T->d.max_samples, "STree sample buffer full (max_samples)");
+    if (n == 0) return MPG_OK;
+    COUNT_LAUNCH(1);
+    k_record<<<(int)std::min<int64_t>((n + 255) / 256, 148 * 8), 256, 0, as_stream(stream)>>>(
+        T->rec.p + T->n_rec, (const float4 *)q->xD, q->spp, (const float4 *)sb->xL, (const float4 *)wb->chain,
+        wb->status, wb->w, wb->ctype, n);
+    CUDA_TRY(cudaPeekAtLastError());
+    T->n_rec += n;
+    return MPG_OK;
+}
+
+extern "C" mpg_status mpg_guide_set_samples(mpg_guide *g, const mpg_guide_sample *records, int64_t n, void *stream) {
+    ARG_CHECK(g && g->stree && (records || n == 0), "needs an STree guide and records");
+    ARG_CHECK(n >= 0 && n <= g->stree->d.max_samples, "n exceeds max_samples");
+    if (n) CUDA_TRY(cudaMemcpyAsync(g->stree->rec.p, records, n * sizeof(mpg_guide_sample), cudaMemcpyDeviceToDevice,
+                                    as_stream(stream)));
+    g->stree->n_rec = n;
+    return MPG_OK;
+}
+
+extern "C" mpg_status mpg_guide_get_samples(const mpg_guide *g, mpg_guide_sample *records, int64_t *n, void *stream) {
+    ARG_CHECK(g && g->stree && n, "needs an STree guide and n");
+    int64_t have = g->stree->n_rec;
+    if (records) {
+        ARG_CHECK(*n >= have, "records capacity too small");
+        if (have) CUDA_TRY(cudaMemcpyAsync(records, g->stree->rec.p, have * sizeof(mpg_guide_sample),
+                                           cudaMemcpyDeviceToDevice, as_stream(stream)));
+    }
+    *n = have;
+    return MPG_OK;
+}
+
+extern "C" mpg_status mpg_guide_stree_info(const mpg_guide *g, mpg_stree_info *info) {
+    ARG_CHECK(g && g->stree && info, "needs an STree guide");
+    const StreeState *T = g->stree;
+    info->n_nodes = T->n_nodes;
+    info->n_leaves = T->n_leaves;
+    info->root_ref = T->root_ref;
+    info->thr = T->thr;
+    info->n_valid = T->n_valid;
+    info->n_lobes = T->n_lobes;
+    return MPG_OK;
+}
+
+extern "C" mpg_status mpg_guide_download_stree(const mpg_guide *g, int32_t *nodes, int64_t *leaf_begin,
+                                               int64_t *leaf_count, int32_t *leaf_ids, int32_t *grp_off,
+                                               int32_t *lobe_sample, uint64_t *lobe_prefix, float *lobe_mu,
+                                               uint64_t *n_prefix, uint64_t *type_prefix, void *stream) {
+    ARG_CHECK(g && g->stree, "needs an STree guide");
+    const StreeState *T = g->stree;
+    cudaStream_t s = as_stream(stream);
+    const cudaMemcpyKind K = cudaMemcpyDeviceToDevice;
+    const size_t L = (size_t)T->n_leaves, NL = (size_t)T->n_lobes;
+    if (nodes && T->n_nodes) CUDA_TRY(cudaMemcpyAsync(nodes, T->nodes.p, T->n_nodes * sizeof(int4), K, s));
+    if (leaf_begin) CUDA_TRY(cudaMemcpyAsync(leaf_begin, T->leaf_begin.p, L * 8, K, s));
+    if (leaf_count) CUDA_TRY(cudaMemcpyAsync(leaf_count, T->leaf_count.p, L * 8, K, s));
+    if (leaf_ids && NL) CUDA_TRY(cudaMemcpyAsync(leaf_ids, T->leaf_ids.p, NL * 4, K, s));
+    if (grp_off) CUDA_TRY(cudaMemcpyAsync(grp_off, T->grp_off.p, L * 127 * 4, K, s));
+    if (lobe_sample && NL) CUDA_TRY(cudaMemcpyAsync(lobe_sample, T->lobe_sample.p, NL * 4, K, s));
+    if (lobe_prefix && NL) CUDA_TRY(cudaMemcpyAsync(lobe_prefix, T->lobe_prefix.p, NL * 8, K, s));
+    if (lobe_mu && NL) CUDA_TRY(cudaMemcpyAsync(lobe_mu, T->lobe_mu.p, NL * 16, K, s));
+    if (n_prefix) CUDA_TRY(cudaMemcpyAsync(n_prefix, T->n_prefix.p, L * 6 * 8, K, s));
+    if (type_prefix) CUDA_TRY(cudaMemcpyAsync(type_prefix, T->type_prefix.p, L * 126 * 8, K, s));
+    return MPG_OK;
+}
+
+static void stree_clear(StreeState *T) { T->n_rec = 0; }

@@ -482,7 +482,7 @@ __global__ void __launch_bounds__(128, MINB) k_walk(const DScene S, const SeedCt
                 Pn = P.seed_pn ? __ldg(P.seed_pn + w) : 1.0f;
             } else {
                 SeedRes sr;
-                ok = seed_target(S, g, P.walk_id_base + w, trial, xD, sr);
+                ok = seed_target(S, g, P.walk_id_base + w, trial, xD, xL, sr);
                 tgt = sr.tgt;
                 k = sr.n;
                 bits = sr.bits;

@@ -71,6 +71,17 @@ class mpg_walk_buf(C.Structure):
                 ("T", C.c_void_p), ("w", C.c_void_p), ("trials", C.c_void_p), ("ctype", C.c_void_p)]
 
 
+class mpg_stree_desc(C.Structure):
+    _fields_ = [("max_samples", C.c_int64), ("eps", C.c_float), ("c_thr", C.c_float), ("kappa_min", C.c_float),
+                ("kappa_max", C.c_float), ("max_depth", C.c_int32), ("reserved", C.c_int32)]
+
+
+class mpg_stree_info(C.Structure):
+    _fields_ = [(f, C.c_int64) for f in ("n_nodes", "n_leaves", "root_ref", "thr", "n_valid", "n_lobes")]
+
+
+GUIDE_SAMPLE_BYTES = 48
+
 STATS_FIELDS = ["walks", "converged", "newton_iters", "primary_iters", "attempts", "rays", "trials", "truncated",
                 "node_visits", "tri_tests", "vertex_iters"]
 
@@ -88,7 +99,9 @@ EXPORTS = ["mpg_scene_create", "mpg_scene_destroy", "mpg_scene_get_info", "mpg_t
            "mpg_guide_set_histogram",
            "mpg_guide_destroy", "mpg_guide_upload", "mpg_guide_reset", "mpg_guide_accumulate", "mpg_guide_rebuild",
            "mpg_guide_download", "mpg_guide_download_dir_tables", "mpg_sample_seeds", "mpg_walk_workspace_size", "mpg_manifold_walk", "mpg_estimate",
-           "mpg_debug_trace", "mpg_last_error", "mpg_version", "mpg_kernel_launches"]
+           "mpg_debug_trace", "mpg_last_error", "mpg_version", "mpg_kernel_launches", "mpg_guide_create_stree",
+           "mpg_guide_record_samples", "mpg_guide_set_samples", "mpg_guide_get_samples", "mpg_guide_stree_info",
+           "mpg_guide_download_stree"]
 
 _lib = None
 
@@ -128,6 +141,13 @@ def lib():
             "mpg_last_error": (C.c_char_p, []),
             "mpg_version": (C.c_int32, []),
             "mpg_kernel_launches": (C.c_uint64, []),
+            "mpg_guide_create_stree": (st, [C.POINTER(mpg_stree_desc), C.POINTER(P)]),
+            "mpg_guide_record_samples": (st, [P, C.POINTER(mpg_query), C.POINTER(mpg_seed_buf),
+                                              C.POINTER(mpg_walk_buf), C.c_int64, P]),
+            "mpg_guide_set_samples": (st, [P, P, C.c_int64, P]),
+            "mpg_guide_get_samples": (st, [P, P, C.POINTER(C.c_int64), P]),
+            "mpg_guide_stree_info": (st, [P, C.POINTER(mpg_stree_info)]),
+            "mpg_guide_download_stree": (st, [P] + [P] * 10 + [P]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -220,6 +240,61 @@ def mpg_guide_download_dir_tables(h, n_prefix=None, type_prefix=None, dir_prefix
                                                _stream_ptr(stream)), "mpg_guide_download_dir_tables")
 
 
+def mpg_guide_create_stree(desc: mpg_stree_desc):
+    h = C.c_void_p()
+    _check(lib().mpg_guide_create_stree(C.byref(desc), C.byref(h)), "mpg_guide_create_stree")
+    return h
+
+
+def mpg_guide_record_samples(h, query, seeds, walks, n, stream=None):
+    _check(lib().mpg_guide_record_samples(h, C.byref(query), C.byref(seeds), C.byref(walks), n, _stream_ptr(stream)),
+           "mpg_guide_record_samples")
+
+
+def mpg_guide_set_samples(h, records, n, stream=None):
+    """records: device uint8 tensor of n*48 bytes (mpg_guide_sample)."""
+    _check(lib().mpg_guide_set_samples(h, _ptr(records), n, _stream_ptr(stream)), "mpg_guide_set_samples")
+
+
+def mpg_guide_get_samples(h, records=None, stream=None) -> int:
+    n = C.c_int64(records.numel() // GUIDE_SAMPLE_BYTES if records is not None else 0)
+    _check(lib().mpg_guide_get_samples(h, _ptr(records), C.byref(n), _stream_ptr(stream)), "mpg_guide_get_samples")
+    return int(n.value)
+
+
+def mpg_guide_stree_info(h) -> dict:
+    info = mpg_stree_info()
+    _check(lib().mpg_guide_stree_info(h, C.byref(info)), "mpg_guide_stree_info")
+    return {f: int(getattr(info, f)) for f, _ in mpg_stree_info._fields_}
+
+
+def mpg_guide_download_stree(h, stream=None) -> dict:
+    """Host (numpy) copy of the current STree + vMF guide (tests and tools)."""
+    import torch
+    inf = mpg_guide_stree_info(h)
+    L, NL, NN = inf["n_leaves"], inf["n_lobes"], inf["n_nodes"]
+    dev = dict(nodes=torch.zeros(max(NN, 1), 4, dtype=torch.int32), leaf_begin=torch.zeros(L, dtype=torch.int64),
+               leaf_count=torch.zeros(L, dtype=torch.int64), leaf_ids=torch.zeros(max(NL, 1), dtype=torch.int32),
+               grp_off=torch.zeros(L, 127, dtype=torch.int32), lobe_sample=torch.zeros(max(NL, 1), dtype=torch.int32),
+               lobe_prefix=torch.zeros(max(NL, 1), dtype=torch.int64), lobe_mu=torch.zeros(max(NL, 1), 4),
+               n_prefix=torch.zeros(L, 6, dtype=torch.int64), type_prefix=torch.zeros(L, 126, dtype=torch.int64))
+    dev = {k: v.cuda() for k, v in dev.items()}
+    _check(lib().mpg_guide_download_stree(h, *(_ptr(dev[k]) for k in (
+        "nodes", "leaf_begin", "leaf_count", "leaf_ids", "grp_off", "lobe_sample", "lobe_prefix", "lobe_mu",
+        "n_prefix", "type_prefix")), _stream_ptr(stream)), "mpg_guide_download_stree")
+    torch.cuda.synchronize()
+    out = dict(inf)
+    for k, v in dev.items():
+        a = v.cpu().numpy()
+        if k in ("lobe_prefix", "n_prefix", "type_prefix"):
+            a = a.view(np.uint64)
+        out[k] = a
+    out["nodes"] = out["nodes"][:NN]
+    for k in ("leaf_ids", "lobe_sample", "lobe_prefix", "lobe_mu"):
+        out[k] = out[k][:NL]
+    return out
+
+
 def mpg_sample_seeds(scene, guide, sampler, query, opts, seeds, stream=None):
     _check(lib().mpg_sample_seeds(scene, guide, C.byref(sampler), C.byref(query), C.byref(opts), C.byref(seeds),
                                   _stream_ptr(stream)), "mpg_sample_seeds")
@@ -261,7 +336,7 @@ def _f3(v):
 class DeviceScene:
     """Scene + (optional) guide of a Workload, resident on the current CUDA device."""
 
-    def __init__(self, w: "W.Workload", stream=None):
+    def __init__(self, w: "W.Workload", stream=None, stree_capacity=None):
         import torch
         if not torch.cuda.is_available():
             raise MPGError("no CUDA device: the manifold walk has no CPU path")
@@ -293,7 +368,13 @@ class DeviceScene:
         sp = w.seed
         self.sampler = mpg_sampler_desc(sp.mode, sp.surf_id, sp.k, sp.tau)
         self.guide = None
-        if sp.mode in (W.SEED_GUIDE_UV, W.SEED_GUIDE_DIR):
+        self.stree = sp.mode == W.SEED_GUIDE_STREE
+        if self.stree:
+            d = mpg_stree_desc(max_samples=int(stree_capacity if stree_capacity is not None else w.n_walks),
+                               eps=0.1, c_thr=1.0, kappa_min=1.0, kappa_max=1.0e4, max_depth=32)
+            self.stree_desc = d
+            self.guide = mpg_guide_create_stree(d)
+        elif sp.mode in (W.SEED_GUIDE_UV, W.SEED_GUIDE_DIR):
             g = mpg_guide_desc()
             g.grid_origin = (C.c_float * 2)(*sp.grid_origin)
             g.grid_extent = (C.c_float * 2)(*sp.grid_extent)
@@ -439,4 +520,7 @@ def run_step(ds: DeviceScene, b: Batch, opts: mpg_walk_opts, stream=None, estima
     if estimate:
         mpg_estimate(b.w, b.n_recv, b.spp, b.mean, b.var, stream)
     if accumulate and ds.guide is not None:
-        mpg_guide_accumulate(ds.guide, b.query, b.out, b.n, stream)
+        if ds.stree:
+            mpg_guide_record_samples(ds.guide, b.query, b.seeds, b.out, b.n, stream)
+        else:
+            mpg_guide_accumulate(ds.guide, b.query, b.out, b.n, stream)

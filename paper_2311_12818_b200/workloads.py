@@ -29,6 +29,7 @@ SURF_SPHERE, SURF_QUAD, SURF_MESH = 0, 1, 2
 MAT_CONDUCTOR, MAT_DIELECTRIC, MAT_DIFFUSE = 0, 1, 2
 LIGHT_POINT, LIGHT_QUAD = 0, 1
 SEED_CAP, SEED_TRIANGLE, SEED_GUIDE_UV, SEED_GUIDE_DIR = 0, 1, 2, 3
+SEED_GUIDE_STREE = 4   # the paper's STree + vMF guide
 
 
 @dataclasses.dataclass
@@ -405,7 +406,7 @@ def config3(n_side: int = 1024, spp: int = 1, grid_n: int = 256) -> Workload:
                     recv_shape=(n_side, n_side))
 
 
-def config4(n_side: int = 1024, grid_n: int = 512) -> Workload:
+def config4(n_side: int = 1024, grid_n: int = 512, guide: str = "hist") -> Workload:
     """configs[4]: mirror sphere (cfg0) at (-5,0,2.5), glass icosphere (cfg1) at
     (-5,0,7.5), water pool (cfg2) over [0,10]^2 (SURVEY 8(d) layout); their three
     lights with the same offsets; 1024^2 receivers on the floor y=-2 over
@@ -424,6 +425,8 @@ def config4(n_side: int = 1024, grid_n: int = 512) -> Workload:
     xD, nD = receiver_grid(-7.5, 10.0, n_side, -2.0, 0.0, 10.0, n_side)
     seed = SeedSpec(SEED_GUIDE_DIR, surf_id=0, k=6, tau=0, grid_origin=(-7.5, 0.0), grid_extent=(17.5, 10.0),
                     cells_x=16, cells_y=16, bins_x=32, bins_y=32, n_types=126)
+    if guide == "stree":   # the paper's STree + vMF guide in place of the histogram
+        seed.mode = SEED_GUIDE_STREE
     return Workload("cfg4_mixed_progressive", [sph, ico, water], lights, xD, nD, 1, seed,
                     WalkOpts(max_iters=20, max_iters_long=40, flags=FLAG_NEWTON_F64), recv_shape=(n_side, n_side))
 

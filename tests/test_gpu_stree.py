@@ -1,0 +1,195 @@
+"""GPU vs oracle parity of the STree + vMF guide (R28-R31).
+
+* tree, leaf lists, lobes (mu, kappa), integer lobe weights and per-leaf tables:
+  bit-exact against oracle.stree_build on the same seeded sample records;
+* sample records written by mpg_guide_record_samples: bit-exact against the
+  oracle's recorder on the same walk outputs;
+* seeds of MPG_SEED_GUIDE_STREE: discrete choices (leaf, n, MIS branch, type,
+  lobe) bit-exact, targets within the exp/log/sin/cos ulps of R31;
+* the progressive loop with this guide: GPU and oracle each run their own loop
+  (their own records, their own trees); per iteration the walks agree as in
+  configs[4].
+"""
+import numpy as np
+import pytest
+
+from paper_2311_12818_b200 import workloads as W
+from tests import parity as PY
+
+pytestmark = pytest.mark.gpu
+BENCH_FLAGS = 8
+
+
+def _oracle_records(r):
+    from oracle import oracle as O
+    return np.frombuffer(r.tobytes(), O.GSAMPLE).copy()
+
+
+def _gpu_build(records, eps=0.1, c_thr=1.0, max_depth=32):
+    import torch
+    from paper_2311_12818_b200 import mpg
+    d = mpg.mpg_stree_desc(max_samples=max(1, len(records)), eps=eps, c_thr=c_thr, kappa_min=1.0, kappa_max=1.0e4,
+                           max_depth=max_depth)
+    g = mpg.mpg_guide_create_stree(d)
+    if len(records):
+        t = torch.from_numpy(np.frombuffer(records.tobytes(), np.uint8).copy()).cuda()
+        mpg.mpg_guide_set_samples(g, t, len(records))
+    mpg.mpg_guide_rebuild(g)
+    G = mpg.mpg_guide_download_stree(g)
+    mpg.mpg_guide_destroy(g)
+    return G
+
+
+def _assert_same_tree(G, R):
+    for k in ("n_nodes", "n_leaves", "root_ref", "thr", "n_valid", "n_lobes"):
+        assert G[k] == R[k], (k, G[k], R[k])
+    nn = R["n_nodes"]
+    if nn:
+        assert np.array_equal(G["nodes"][:, 0], R["nodes"]["split"].view(np.int32)), "split planes"
+        assert np.array_equal(G["nodes"][:, 1], R["nodes"]["axis"]), "axes"
+        assert np.array_equal(G["nodes"][:, 2:], R["nodes"]["child"]), "children"
+    assert np.array_equal(G["leaf_begin"], R["leaf_begin"]) and np.array_equal(G["leaf_count"], R["leaf_count"])
+    assert np.array_equal(G["leaf_ids"], R["leaf_ids"]), "leaf lists"
+    assert np.array_equal(G["grp_off"], R["grp_off"]), "type groups"
+    assert np.array_equal(G["lobe_sample"], R["lobe_sample"]), "lobe order"
+    assert np.array_equal(G["lobe_prefix"], R["lobe_prefix"]), "lobe weights"
+    assert np.array_equal(G["lobe_mu"].view(np.uint32), R["lobe_mu"].view(np.uint32)), "mu, kappa"
+    assert np.array_equal(G["n_prefix"], R["n_prefix"]), "P(n) tables"
+    assert np.array_equal(G["type_prefix"], R["type_prefix"]), "P(tau|n) tables"
+
+
+@pytest.mark.parametrize("n,eps,c_thr", [(0, 0.1, 1.0), (1, 0.1, 1.0), (700, 0.1, 1.0), (20000, 0.1, 1.0),
+                                         (20000, 0.0, 1.0), (20000, 0.1, 0.25), (200000, 0.1, 1.0)])
+def test_stree_build_bit_exact(n, eps, c_thr):
+    from oracle import oracle as O
+    r = W.synthetic_guide_samples(n, seed=n + 3)
+    G = _gpu_build(r, eps=eps, c_thr=c_thr)
+    R = O.stree_build(_oracle_records(r), eps=eps, c_thr=c_thr)
+    _assert_same_tree(G, R)
+
+
+def test_stree_build_duplicates_hit_the_depth_cap():
+    """Two clusters of identical configurations: nodes keep splitting without separating
+    them until the depth cap (P:521 threshold unreachable) -- same tree on both sides."""
+    from oracle import oracle as O
+    r = W.synthetic_guide_samples(3000, seed=9, invalid_frac=0.0)
+    r["xD"][: 1500] = r["xD"][0]
+    r["xL"][: 1500] = r["xL"][0]
+    r["xD"][1500:] = r["xD"][1500]
+    r["xL"][1500:] = r["xL"][1500]
+    G = _gpu_build(r, max_depth=12)
+    R = O.stree_build(_oracle_records(r), max_depth=12)
+    _assert_same_tree(G, R)
+    assert R["leaf_count"].max() > R["thr"]
+
+
+def test_record_samples_bit_exact():
+    """mpg_guide_record_samples == the oracle's recorder on the same walk outputs."""
+    import torch
+    from oracle import oracle as O
+    from paper_2311_12818_b200 import mpg
+    w = W.config4(n_side=48, guide="stree")
+    ds = mpg.DeviceScene(w)
+    b = mpg.Batch(w.xD, w.nD, w.spp, w.seed.k)
+    mpg.run_step(ds, b, ds.opts(), accumulate=True)
+    torch.cuda.synchronize()
+    buf = torch.empty(b.n * 48, dtype=torch.uint8, device="cuda")
+    assert mpg.mpg_guide_get_samples(ds.guide, buf) == b.n
+    torch.cuda.synchronize()
+    got = np.frombuffer(buf.cpu().numpy().tobytes(), O.GSAMPLE)
+    g = b.results()
+    ref = O.record_samples(w.xD, w.spp, g["status"].astype(np.int32), g["w"], g["pos"][:, 0].astype(np.float32),
+                           g["ctype"] & 15, g["ctype"] >> 4, g["xL"][:, :3])
+    assert np.array_equal(np.frombuffer(got.tobytes(), np.uint8), np.frombuffer(ref.tobytes(), np.uint8))
+    assert (got["w"] > 0).sum() > 50
+    ds.close()
+
+
+@pytest.fixture(scope="module")
+def stree_guided_run():
+    """One guided iteration with the same tree on both sides (built from the same
+    seeded records by each side's own builder)."""
+    import torch
+    from oracle import oracle as O
+    from paper_2311_12818_b200 import mpg
+    w = W.config4(n_side=96, guide="stree")
+    r = W.synthetic_guide_samples(60000, seed=17)
+    ds = mpg.DeviceScene(w, stree_capacity=len(r))
+    t = torch.from_numpy(np.frombuffer(r.tobytes(), np.uint8).copy()).cuda()
+    mpg.mpg_guide_set_samples(ds.guide, t, len(r))
+    mpg.mpg_guide_rebuild(ds.guide)
+    b = mpg.Batch(w.xD, w.nD, w.spp, w.seed.k)
+    mpg.run_step(ds, b, ds.opts())
+    torch.cuda.synchronize()
+    g = b.results()
+    g["extent"] = ds.extent
+    ds.close()
+    s = O.OracleScene(w)
+    s.set_stree(O.stree_build(_oracle_records(r)))
+    o = s.walks(np.arange(w.n_walks))
+    return w, g, o, s
+
+
+def test_stree_seeds_match_oracle(stree_guided_run):
+    w, g, o, s = stree_guided_run
+    rng = np.random.default_rng(5)
+    nlearned = 0
+    for i in rng.choice(w.n_walks, 2000, replace=False):
+        d = s.seed_ex(int(i))
+        ct = int(g["seed_ctype"][i])
+        assert (ct & 15) == d["n"]
+        assert ((ct >> 12) & 1) == d["learned"]
+        assert ((ct >> 4) & 255) == ((d["tau"] if d["learned"] else d["init_bits"]) & 255)
+        assert g["pn"][i] == pytest.approx(d["Pn"], rel=1e-6)
+        assert g["bin"][i] == d["bin"]                                   # lobe index: bit-exact
+        assert np.abs(g["target"][i, :3] - d["target"]).max() <= 64 * 2.0 ** -24 * 12.0   # exp/log/sin/cos (R31)
+        nlearned += d["learned"]
+    assert nlearned > 300
+
+
+def test_stree_walk_parity(stree_guided_run):
+    w, g, o, s = stree_guided_run
+    ids = np.arange(w.n_walks)
+    rep = PY.compare(g, o, ids, g["extent"], 6)
+    cg = np.isin(g["status"], (0, 5)); co = np.isin(o["status"], (0, 5))
+    both = cg & co
+    ct = g["ctype"][both]
+    assert np.array_equal(ct & 15, o["k"][both]) and np.array_equal(ct >> 4, o["tau"][both])
+    print({k: v for k, v in rep.items() if not isinstance(v, np.ndarray)})
+    assert rep["flag_agree"] >= 0.999
+    assert rep["n_other_chain"] <= max(1, 0.001 * rep["both"])
+
+
+def test_stree_progressive_loop_independent():
+    """GPU loop vs oracle loop, each fitting its own STree from its own samples of the
+    last iteration (P:426 footnote): walks agree per iteration, the trees agree
+    in size, and the guide learns (more converged walks than the initializer alone)."""
+    import torch
+    from oracle import oracle as O
+    from paper_2311_12818_b200 import mpg
+    w = W.config4(n_side=48, guide="stree")
+    ds = mpg.DeviceScene(w)
+    b = mpg.Batch(w.xD, w.nD, w.spp, w.seed.k)
+    opts = ds.opts()
+    s = O.OracleScene(w)
+    log = []
+
+    def hook(it):
+        torch.cuda.synchronize()
+        g = b.results()
+        o = s.walks(np.arange(w.n_walks), s.opts(walk_id_base=it * w.n_walks))
+        rep = PY.compare(g, o, np.arange(w.n_walks), ds.extent, 6)
+        rec = O.record_samples(w.xD, w.spp, o["status"], o["w"].astype(np.float32), o["pos"][:, 0].astype(np.float32),
+                               o["k"], o["tau"], o["xL"].astype(np.float32))
+        R = O.stree_build(rec)
+        s.set_stree(R)                                   # the oracle's own next guide
+        log.append((rep["flag_agree"], int(np.isin(g["status"], (0, 5)).sum()), R["n_valid"]))
+
+    mpg.run_progressive(ds, b, opts, iterations=3, on_iteration=hook)
+    info = mpg.mpg_guide_stree_info(ds.guide)
+    ds.close()
+    print(log, info)
+    for agree, nconv, nvalid in log:
+        assert agree >= 0.995
+    assert abs(info["n_valid"] - log[-1][2]) <= max(2, 0.01 * log[-1][2])
+    assert log[-1][1] > log[0][1]
