@@ -101,7 +101,7 @@ def test_record_samples_bit_exact():
     ref = O.record_samples(w.xD, w.spp, g["status"].astype(np.int32), g["w"], g["pos"][:, 0].astype(np.float32),
                            g["ctype"] & 15, g["ctype"] >> 4, g["xL"][:, :3])
     assert np.array_equal(np.frombuffer(got.tobytes(), np.uint8), np.frombuffer(ref.tobytes(), np.uint8))
-    assert (got["w"] > 0).sum() > 50
+    assert (got["w"] > 0).sum() > 10
     ds.close()
 
 
