@@ -97,8 +97,10 @@ def dist_env():
     return rank, world, local
 
 
-def make_workload(cfg):
+def make_workload(cfg, guide="hist"):
     from paper_2311_12818_b200 import workloads as W
+    if cfg == 4:
+        return W.config4(guide=guide)
     return W.CONFIGS[cfg]()
 
 
@@ -204,12 +206,13 @@ def run_ours(args):
         dist.init_process_group("nccl")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    w = make_workload(args.config)
-    progressive = w.seed.mode == 3      # configs[4]: one step = the whole 8-iteration loop (R22)
+    w = make_workload(args.config, args.guide)
+    progressive = w.seed.mode in (3, 4)  # configs[4]: one step = the whole 8-iteration loop (R22)
+    stree = w.seed.mode == 4             # --guide stree: the paper's STree + vMF guide
     iters = 8 if progressive else 1
     # independent partitions (weak scaling): rank r owns walk ids [r*n*iters, (r+1)*n*iters)
     w.opts.walk_id_base = D.walk_id_base(rank, w.n_walks * iters)
-    ds = mpg.DeviceScene(w)
+    ds = mpg.DeviceScene(w, stree_capacity=w.n_walks * world)
     b = mpg.Batch(w.xD, w.nD, w.spp, w.seed.k)
     opts = ds.opts(flags=w.opts.flags | (1 if args.wavefront else 0) | (2 if args.hostloop else 0) |
                    (4 if args.f64 else 0) | (0 if args.no_sort else 8))
@@ -220,9 +223,15 @@ def run_ours(args):
 
     # configs[4] on N ranks: the guide histogram is summed over ranks before every
     # rebuild (the method's one exchange step); no-op on one rank
-    gsz = ds.info_guide_size() if progressive else 0
+    gsz = ds.info_guide_size() if (progressive and not stree) else 0
     hbuf = torch.empty(max(gsz, 1), dtype=torch.float32, device=dev)
-    exchange = (lambda d: D.exchange_guide(d, hbuf)) if (progressive and world > 1) else None
+    exchange = None
+    if progressive and world > 1:
+        if stree:   # STree: the sample records of all ranks are gathered (the tree is fitted from all of them)
+            sbuf = torch.empty(b.n * world * mpg.GUIDE_SAMPLE_BYTES, dtype=torch.uint8, device=dev)
+            exchange = lambda d: D.exchange_samples(d, sbuf, b.n)
+        else:
+            exchange = lambda d: D.exchange_guide(d, hbuf)
 
     def step():
         if progressive:
@@ -266,7 +275,9 @@ def run_ours(args):
             walk_ev.append((ev5[1], ev5[2]))
             mpg.mpg_estimate(b.w, b.n_recv, b.spp, b.mean, b.var)
             ev5[3].record(stream)
-            if guided:
+            if stree:
+                mpg.mpg_guide_record_samples(ds.guide, b.query, b.seeds, b.out, b.n)
+            elif guided:
                 mpg.mpg_guide_accumulate(ds.guide, b.query, b.out, b.n)
             if progressive:
                 if exchange is not None:
@@ -370,7 +381,9 @@ def run_ours(args):
         line = {"metric": METRIC, "value": value, "unit": "walks/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "f32+f64" if opts.flags & 4 else "f32", "data": "synthetic",
-                "config": {"workload": CONFIG_NAMES[args.config], "n_walks_per_gpu": b.n, "k": w.seed.k,
+                "config": {"workload": CONFIG_NAMES[args.config] + (
+                               " -- guide: STree over (x_D, x_L) + per-type vMF mixtures (SURVEY 8(f)1) in place of "
+                               "the histogram" if stree else ""), "n_walks_per_gpu": b.n, "k": w.seed.k,
                            "max_iters": w.opts.max_iters, "trials": "on (k_max 1024)",
                            "l2": "256 MB buffer written before every timed step (inputs < 126 MB L2)",
                            "order": ("primaries in walk order" if not opts.flags & 8 else
@@ -413,6 +426,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=1)
     ap.add_argument("--ref-walks", type=int, default=100000)
+    ap.add_argument("--guide", default="hist", choices=["hist", "stree"],
+                    help="configs[4] guide: BASELINE's histogram (default) or the paper's STree + vMF (SURVEY 8(f)1)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--wavefront", action="store_true", help="wavefront path (MPG_FLAG_WAVEFRONT)")

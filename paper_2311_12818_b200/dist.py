@@ -67,3 +67,29 @@ def exchange_guide(ds, buf: torch.Tensor, stream=None):
     mpg.mpg_guide_download(ds.guide, buf, None, stream)
     allreduce_histogram(buf)
     mpg.mpg_guide_set_histogram(ds.guide, buf, stream)
+
+
+def exchange_samples(ds, buf: torch.Tensor, n_local: int, stream=None):
+    """Exchange step of the multi-process progressive loop with the STree + vMF guide:
+    every rank's sample records of this iteration are gathered on every rank (NCCL
+    all-gather; 48 B per walk), in rank order, and replace the local records before
+    mpg_guide_rebuild, so every rank fits the same tree from the samples of all ranks
+    (P:426 footnote).  buf: device uint8 of world * n_local * 48 bytes."""
+    from . import mpg
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return
+    world = dist.get_world_size()
+    B = mpg.GUIDE_SAMPLE_BYTES
+    mine = torch.empty(n_local * B, dtype=torch.uint8, device=buf.device)
+    got = mpg.mpg_guide_get_samples(ds.guide, mine, stream)
+    assert got == n_local, (got, n_local)
+    gather_records(mine, buf[: world * n_local * B])
+    mpg.mpg_guide_set_samples(ds.guide, buf, world * n_local, stream)
+
+
+def gather_records(mine: torch.Tensor, out: torch.Tensor) -> torch.Tensor:
+    """All-gather of equal-sized per-rank record buffers into out (rank order); NCCL or gloo."""
+    world = dist.get_world_size()
+    parts = list(out.view(world, -1).unbind(0))
+    dist.all_gather(parts, mine)
+    return out

@@ -144,3 +144,54 @@ def test_allreduce_histogram_single_process_identity():
     from paper_2311_12818_b200 import dist as D
     h = torch.arange(6, dtype=torch.float32)
     assert torch.equal(D.allreduce_histogram(h.clone()), h)
+
+
+# ---- the STree + vMF guide on 2 ranks: sample records gathered ----
+def _rank_records(rank, w, s):
+    """Oracle walks of this rank's partition of iteration 0 (empty tree) as sample records."""
+    from oracle import oracle as O
+    from paper_2311_12818_b200 import dist as D
+    base = D.walk_id_base(rank, w.n_walks)
+    o = s.walks(np.arange(w.n_walks), s.opts(walk_id_base=base))
+    return O.record_samples(w.xD, w.spp, o["status"], o["w"].astype(np.float32), o["pos"][:, 0].astype(np.float32),
+                            o["k"], o["tau"], o["xL"].astype(np.float32))
+
+
+def _worker_stree(rank, world, port, out):
+    import hashlib
+    import torch
+    import torch.distributed as dist
+    from oracle import oracle as O
+    from paper_2311_12818_b200 import dist as D
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    w = W.config4(n_side=8, grid_n=32, guide="stree")
+    s = O.OracleScene(w)
+    mine = torch.from_numpy(np.frombuffer(_rank_records(rank, w, s).tobytes(), np.uint8).copy())
+    allr = torch.empty(world * mine.numel(), dtype=torch.uint8)
+    D.gather_records(mine, allr)                                       # the exchange step
+    G = O.stree_build(np.frombuffer(allr.numpy().tobytes(), O.GSAMPLE))  # every rank fits from all samples
+    dig = hashlib.sha256(G["nodes"].tobytes() + G["leaf_ids"].tobytes() + G["lobe_mu"].tobytes() +
+                         G["lobe_prefix"].tobytes() + G["n_prefix"].tobytes()).hexdigest()
+    digs = [None] * world
+    dist.all_gather_object(digs, dig)
+    if rank == 0:
+        np.save(out, allr.numpy())
+        json.dump({"digests": digs}, open(out + ".json", "w"))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_rank_stree_sample_exchange(tmp_path):
+    """Both ranks fit the same STree from the records of both partitions, in rank order,
+    equal to one process concatenating the two partitions' records."""
+    from oracle import oracle as O
+    out = str(tmp_path / "r.npy")
+    mp.spawn(_worker_stree, args=(2, _free_port(), out), nprocs=2, join=True)
+    got = np.load(out)
+    digs = json.load(open(out + ".json"))["digests"]
+    assert digs[0] == digs[1]
+    w = W.config4(n_side=8, grid_n=32, guide="stree")
+    s = O.OracleScene(w)
+    ref = np.concatenate([_rank_records(k, w, s) for k in range(2)])
+    assert np.array_equal(got, np.frombuffer(ref.tobytes(), np.uint8))
+    assert (ref["w"] > 0).sum() > 0
