@@ -1456,15 +1456,20 @@ typedef struct {
     uint64_t *n_prefix, *type_prefix; /* [leaves][6], [leaves][126] */
 } orc_stree;
 
-static const orc_gsample *g_sort_rec;
-static int g_sort_axis;
 static float skey(const orc_gsample *r, int a) { return canon0(a < 3 ? r->xD[a] : r->xL[a - 3]); }
-static int cmp_axis(const void *A, const void *B) { /* by (coordinate, record index) [R29] */
-    int64_t i = *(const int64_t *)A, j = *(const int64_t *)B;
-    float x = skey(g_sort_rec + i, g_sort_axis), y = skey(g_sort_rec + j, g_sort_axis);
-    if (x < y) return -1;
-    if (x > y) return 1;
-    return i < j ? -1 : (i > j ? 1 : 0);
+
+/* stable sort of a node's list by one coordinate (equal coordinates keep the list's
+ * order; the root list is in record order) [R29] -- a plain merge sort */
+static void sort_by_axis(const orc_gsample *rec, int a, int64_t *ids, int64_t n, int64_t *tmp) {
+    if (n < 2) return;
+    int64_t h = n / 2;
+    sort_by_axis(rec, a, ids, h, tmp);
+    sort_by_axis(rec, a, ids + h, n - h, tmp);
+    int64_t i = 0, j = h, k = 0;
+    while (i < h && j < n) tmp[k++] = skey(rec + ids[j], a) < skey(rec + ids[i], a) ? ids[j++] : ids[i++];
+    while (i < h) tmp[k++] = ids[i++];
+    while (j < n) tmp[k++] = ids[j++];
+    memcpy(ids, tmp, sizeof(int64_t) * n);
 }
 
 typedef struct { int64_t *ids; int64_t n; float lo[6], hi[6]; int depth; int parent, side; } orc_qnode;
@@ -1542,8 +1547,9 @@ void *orc_stree_build(const orc_gsample *rec, int64_t n, float eps, float c_thr,
             int a = active[nd.depth % na];
             float c = (nd.lo[a] + nd.hi[a]) * 0.5f;
             float delta = (nd.hi[a] - nd.lo[a]) * 0.25f; /* copies kept within half a child width */
-            g_sort_rec = rec; g_sort_axis = a;
-            qsort(nd.ids, (size_t)nd.n, sizeof(int64_t), cmp_axis);
+            int64_t *tmp = (int64_t *)malloc(sizeof(int64_t) * (nd.n ? nd.n : 1));
+            sort_by_axis(rec, a, nd.ids, nd.n, tmp);
+            free(tmp);
             int64_t m = 0;
             while (m < nd.n && skey(rec + nd.ids[m], a) < c) m++;
             int64_t e = (int64_t)floor((double)eps * (double)nd.n);

@@ -6,11 +6,12 @@
 // Build (mpg_guide_rebuild), level-synchronous and deterministic:
 //   k_stree_valid      flags + exact fp32 bbox of the sample keys (warp min/max, atomics)
 //   DeviceSelect       ids of the samples, record order
-//   per level          keys (ordered coordinate << 32 | record id) of the level's ids;
-//                      cub segmented sort of the splitting nodes' segments; k_stree_split
-//                      (one thread per node: plane, overlap windows by binary search);
-//                      the host lays out the child windows (prefix sums over a few
-//                      thousand nodes) and k_copy_segments writes the next level
+//   per level          one pinned upload of the level's node table; keys (node index << 32 |
+//                      ordered coordinate) and one stable cub radix sort of (key, id) = every
+//                      node's list stably sorted by the split axis; k_stree_split (one thread
+//                      per node: plane, overlap windows by binary search); one D2H + sync;
+//                      the host lays out the child windows (prefix sums over a few thousand
+//                      nodes) and k_copy_segments (element-parallel) writes the next level
 //   lobes              radix sort by (leaf, type, position) = stable partition by type;
 //                      k_grp_off, k_lobe_kappa (nearest direction in the group),
 //                      k_group_tables (E_tau in fp64, integer lobe weights), then the
@@ -18,6 +19,7 @@
 // Children are contiguous windows of the parent's sorted list, so the build is a
 // sequence of sorts and copies; no atomics decide anything.
 #pragma once
+#include <chrono>
 #include <cub/device/device_segmented_sort.cuh>
 #include <cub/device/device_select.cuh>
 #include <thrust/iterator/counting_iterator.h>
@@ -55,6 +57,26 @@ template <class T> struct DBuf {
     }
 };
 
+template <class T> struct PinBuf { // pinned host staging (reused; rewritten only after a stream sync)
+    T *p = nullptr;
+    size_t cap = 0;
+    cudaError_t reserve(size_t n) {
+        if (n <= cap && p) return cudaSuccess;
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        cap = 0;
+        size_t c = std::max<size_t>(n, 1) * 3 / 2 + 64;
+        cudaError_t e = cudaHostAlloc((void **)&p, c * sizeof(T), cudaHostAllocDefault);
+        if (e == cudaSuccess) cap = c;
+        return e;
+    }
+    void release() {
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        cap = 0;
+    }
+};
+
 struct StreeState {
     mpg_stree_desc d;
     DBuf<mpg_guide_sample> rec;
@@ -71,13 +93,14 @@ struct StreeState {
     DBuf<double> E;
     // scratch
     DBuf<unsigned char> flags;
-    DBuf<int> ids_a, ids_b, seg_b, seg_e, nv;
+    DBuf<int> ids_a, ids_b, ids_c, nv;
     DBuf<unsigned long long> keys_a, keys_b;
     DBuf<unsigned char> temp;
     DBuf<unsigned int> bbox;
-    DBuf<float2> lohi;
-    DBuf<int4> split_out, segs;
-    DBuf<float> split_c;
+    DBuf<int4> split_out;
+    DBuf<int4> dstage_a, dstage_b;    // per-level device staging (level data, child segments)
+    PinBuf<int4> hstage_a, hstage_b;  // pinned host staging of the same
+    PinBuf<int4> hsplit;              // split results (m, eL, eR, s0 | s1, c bits)
 };
 
 static void stree_state_free(StreeState *t) {
@@ -85,9 +108,10 @@ static void stree_state_free(StreeState *t) {
     t->rec.release(); t->nodes.release(); t->leaf_begin.release(); t->leaf_count.release();
     t->leaf_ids.release(); t->grp_off.release(); t->lobe_sample.release(); t->lobe_prefix.release();
     t->lobe_mu.release(); t->n_prefix.release(); t->type_prefix.release(); t->E.release();
-    t->flags.release(); t->ids_a.release(); t->ids_b.release(); t->seg_b.release(); t->seg_e.release();
+    t->flags.release(); t->ids_a.release(); t->ids_b.release(); t->ids_c.release();
     t->nv.release(); t->keys_a.release(); t->keys_b.release(); t->temp.release(); t->bbox.release();
-    t->lohi.release(); t->split_out.release(); t->segs.release(); t->split_c.release();
+    t->split_out.release();
+    t->dstage_a.release(); t->dstage_b.release(); t->hstage_a.release(); t->hstage_b.release(); t->hsplit.release();
     delete t;
 }
 
@@ -130,25 +154,35 @@ __global__ void k_stree_valid(const mpg_guide_sample *rec, int64_t n, unsigned c
     }
 }
 
-__global__ void k_level_keys(const mpg_guide_sample *rec, const int *ids, int64_t n, int axis,
-                             unsigned long long *keys) {
+// element-parallel: key = (node index in the level) << 32 | ordered coordinate; a stable
+// radix sort of (key, id) then orders every node's list by the coordinate, equal
+// coordinates keeping the list's order (R29).  nodes: (begin, count), contiguous.
+__global__ void k_level_keys(const mpg_guide_sample *rec, const int *ids, int64_t n, const int2 *nodes, int nl,
+                             int axis, unsigned long long *keys) {
     for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+        int lo = 0, hi = nl - 1; // last node with begin <= j
+        while (lo < hi) {
+            int mid = (lo + hi + 1) >> 1;
+            if (nodes[mid].x <= (int)j) lo = mid;
+            else hi = mid - 1;
+        }
         int id = ids[j];
-        keys[j] = ((unsigned long long)f2o(gs_key(rec[id], axis)) << 32) | (unsigned)id;
+        keys[j] = ((unsigned long long)lo << 32) | f2o(gs_key(rec[id], axis));
     }
 }
 
 // one thread per splitting node (R28, R29): plane c, copies eL/eR, discard bounds s0/s1
-__global__ void k_stree_split(const unsigned long long *keys, const int *seg_b, const int *seg_e, const float2 *lohi,
-                              int n_nodes, float eps, int4 *out, float *cout) {
+__global__ void k_stree_split(const unsigned long long *keys, const int2 *sbe, const float2 *lohi, int n_nodes,
+                              float eps, int4 *out) {
     int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= n_nodes) return;
-    const unsigned long long *K = keys + seg_b[t];
-    int k = seg_e[t] - seg_b[t];
+    const unsigned long long *K = keys + sbe[t].x;
+    int k = sbe[t].y - sbe[t].x;
+    // keys: low word = ordered coordinate
     float lo = lohi[t].x, hi = lohi[t].y;
     float c = FM(FA(lo, hi), 0.5f);
     float delta = FM(FS(hi, lo), 0.25f);
-    auto x = [&](int j) { return o2f((unsigned)(K[j] >> 32)); };
+    auto x = [&](int j) { return o2f((unsigned)K[j]); };
     // first index in [a, b) where pred holds, pred monotone false..true
     auto first = [&](int a, int b, auto pred) {
         while (a < b) {
@@ -166,15 +200,24 @@ __global__ void k_stree_split(const unsigned long long *keys, const int *seg_b, 
     int s0 = first(0, m, [&](int j) { return FS(lo, x(j)) <= delta; });
     int s1 = first(m, k, [&](int j) { return FS(x(j), hi) > delta; });
     out[2 * t] = make_int4(m, eL, eR, s0);
-    out[2 * t + 1] = make_int4(s1, 0, 0, 0);
-    cout[t] = c;
+    out[2 * t + 1] = make_int4(s1, __float_as_int(c), 0, 0);
 }
 
-// one block per segment (src, dst, len): ids from sorted keys (low word) or plain ids
-template <class S>
-__global__ void k_copy_segments(const S *src, int *dst, const int4 *segs) {
-    int4 g = segs[blockIdx.x];
-    for (int j = threadIdx.x; j < g.z; j += blockDim.x) dst[g.y + j] = (int)(unsigned)src[g.x + j];
+// element-parallel copy of segments (src, dst, len) whose dst ranges are contiguous and
+// increasing from segs[0].y: total elements n
+__global__ void k_copy_segments(const int *src, int *dst, const int4 *segs, int nseg, int64_t n) {
+    const int d0 = segs[0].y;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+        int d = d0 + (int)e;
+        int lo = 0, hi = nseg - 1; // last segment with dst <= d
+        while (lo < hi) {
+            int mid = (lo + hi + 1) >> 1;
+            if (segs[mid].y <= d) lo = mid;
+            else hi = mid - 1;
+        }
+        int4 g = segs[lo];
+        dst[d] = src[g.x + (d - g.y)];
+    }
 }
 
 __global__ void k_lobe_keys(const mpg_guide_sample *rec, const int *leaf_ids, const int64_t *lb, const int64_t *lc,
@@ -302,8 +345,35 @@ static inline float host_o2f(unsigned u) {
     return f;
 }
 
+// MPG_STREE_PROFILE=1: per-phase wall times of the build (synchronising after each phase), on stderr
+struct StreeProf {
+    bool on = getenv("MPG_STREE_PROFILE") != nullptr;
+    std::vector<std::pair<std::string, double>> acc;
+    std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+    void mark(const char *phase, cudaStream_t st) {
+        if (!on) return;
+        cudaStreamSynchronize(st);
+        auto now = std::chrono::steady_clock::now();
+        double ms = std::chrono::duration<double, std::milli>(now - t).count();
+        t = now;
+        for (auto &a : acc)
+            if (a.first == phase) { a.second += ms; return; }
+        acc.emplace_back(phase, ms);
+    }
+    ~StreeProf() {
+        if (!on) return;
+        double tot = 0;
+        for (auto &a : acc) tot += a.second;
+        fprintf(stderr, "stree_build %.3f ms:", tot);
+        for (auto &a : acc) fprintf(stderr, " %s=%.3f", a.first.c_str(), a.second);
+        fprintf(stderr, "\n");
+    }
+};
+
 // Build the tree and tables from the recorded samples (R28-R31); synchronous on st.
 static mpg_status stree_build(StreeState *T, cudaStream_t st) {
+    StreeProf prof;
+    prof.mark("start", st);
     const int64_t n = T->n_rec;
     const int nsm = 148;
     // 1. sample ids (record order) and the root box
@@ -333,6 +403,7 @@ static mpg_status stree_build(StreeState *T, cudaStream_t st) {
         ST_TRY(cudaStreamSynchronize(st));
         nv = nvi;
     }
+    prof.mark("select", st);
     T->n_valid = nv;
     double thr_d = floor((double)T->d.c_thr * sqrt((double)nv));
     T->thr = thr_d < 1.0 ? 1 : (int)thr_d;
@@ -353,9 +424,9 @@ static mpg_status stree_build(StreeState *T, cudaStream_t st) {
     std::vector<HNode> level{root}, next;
     std::vector<int4> hnodes, segs;
     std::vector<int64_t> lb, lc;
-    std::vector<int> sb, se, split_idx;
-    std::vector<float2> lohi;
+    std::vector<int> split_idx;
     int64_t leaf_total = 0;
+    ST_TRY(T->leaf_ids.reserve_keep((size_t)nv * 4, 0, st)); // overlap copies grow the lists (measured ~5x)
     int n_leaves = 0;
     int root_ref = ~0;
     int *cur = T->ids_a.p;
@@ -384,55 +455,67 @@ static mpg_status stree_build(StreeState *T, cudaStream_t st) {
             else hnodes[nd.parent].w = ref;
         }
         ARG_CHECK(leaf_total < (1ll << 31) && n_leaves < (1 << 23), "STree too large (lobes >= 2^31 or leaves >= 2^23)");
-        if (!segs.empty()) { // leaf lists of this level -> leaf_ids
-            ST_TRY(T->leaf_ids.reserve_keep(leaf_total, leaf_prev, st));
-            ST_TRY(T->segs.reserve(segs.size()));
-            ST_TRY(cudaMemcpyAsync(T->segs.p, segs.data(), segs.size() * sizeof(int4), cudaMemcpyHostToDevice, st));
-            COUNT_LAUNCH(1);
-            k_copy_segments<int><<<(int)segs.size(), 128, 0, st>>>(cur, T->leaf_ids.p, T->segs.p);
-            ST_TRY(cudaPeekAtLastError());
-            ST_TRY(cudaStreamSynchronize(st)); // host vectors are reused below
+        // one pinned upload per level: [leaf segments | level nodes (b, n) | split nodes (b, e) | (lo, hi)]
+        const int n_ls = (int)segs.size(), nl = (int)level.size(), ns = (int)split_idx.size();
+        const int a = ns ? active[depth % na] : 0;
+        const size_t n4 = n_ls + (nl + 1) / 2 + (ns + 1) / 2 + (ns + 1) / 2;
+        ST_TRY(T->hstage_a.reserve(n4));
+        ST_TRY(T->dstage_a.reserve(n4));
+        int4 *h4 = T->hstage_a.p;
+        memcpy(h4, segs.data(), n_ls * sizeof(int4));
+        int2 *h_lvl = (int2 *)(h4 + n_ls);
+        for (int i = 0; i < nl; i++) h_lvl[i] = make_int2((int)level[i].b, (int)level[i].n);
+        int2 *h_sbe = (int2 *)(h4 + n_ls + (nl + 1) / 2);
+        float2 *h_lohi = (float2 *)(h4 + n_ls + (nl + 1) / 2 + (ns + 1) / 2);
+        for (int q = 0; q < ns; q++) {
+            const HNode &nd = level[split_idx[q]];
+            h_sbe[q] = make_int2((int)nd.b, (int)(nd.b + nd.n));
+            h_lohi[q] = make_float2(nd.lo[a], nd.hi[a]);
         }
+        ST_TRY(cudaMemcpyAsync(T->dstage_a.p, h4, n4 * sizeof(int4), cudaMemcpyHostToDevice, st));
+        const int4 *d_ls = T->dstage_a.p;
+        const int2 *d_lvl = (const int2 *)(T->dstage_a.p + n_ls);
+        const int2 *d_sbe = (const int2 *)(T->dstage_a.p + n_ls + (nl + 1) / 2);
+        const float2 *d_lohi = (const float2 *)(T->dstage_a.p + n_ls + (nl + 1) / 2 + (ns + 1) / 2);
+        if (n_ls) { // leaf lists of this level -> leaf_ids
+            ST_TRY(T->leaf_ids.reserve_keep(leaf_total, leaf_prev, st));
+            COUNT_LAUNCH(1);
+            const int64_t ne = leaf_total - leaf_prev;
+            k_copy_segments<<<(int)std::min<int64_t>((ne + 255) / 256, nsm * 8), 256, 0, st>>>(cur, T->leaf_ids.p, d_ls,
+                                                                                              n_ls, ne);
+            ST_TRY(cudaPeekAtLastError());
+        }
+        prof.mark("leafcopy", st);
         if (split_idx.empty()) break;
-        const int a = active[depth % na];
         int64_t n_cur = 0;
         for (auto &nd : level) n_cur = std::max<int64_t>(n_cur, nd.b + nd.n);
-        sb.clear(); se.clear(); lohi.clear();
-        for (int i : split_idx) {
-            sb.push_back((int)level[i].b);
-            se.push_back((int)(level[i].b + level[i].n));
-            lohi.push_back(make_float2(level[i].lo[a], level[i].hi[a]));
-        }
-        const int ns = (int)split_idx.size();
         ST_TRY(T->keys_a.reserve(n_cur));
         ST_TRY(T->keys_b.reserve(n_cur));
-        ST_TRY(T->seg_b.reserve(ns));
-        ST_TRY(T->seg_e.reserve(ns));
-        ST_TRY(T->lohi.reserve(ns));
         ST_TRY(T->split_out.reserve(2 * ns));
-        ST_TRY(T->split_c.reserve(ns));
-        ST_TRY(cudaMemcpyAsync(T->seg_b.p, sb.data(), ns * sizeof(int), cudaMemcpyHostToDevice, st));
-        ST_TRY(cudaMemcpyAsync(T->seg_e.p, se.data(), ns * sizeof(int), cudaMemcpyHostToDevice, st));
-        ST_TRY(cudaMemcpyAsync(T->lohi.p, lohi.data(), ns * sizeof(float2), cudaMemcpyHostToDevice, st));
+        ST_TRY(T->hsplit.reserve(2 * ns));
+        DBuf<int> &sorted_ids = T->ids_c; // this level's ids, each node's list sorted
+        ST_TRY(sorted_ids.reserve(n_cur));
         COUNT_LAUNCH(1);
-        k_level_keys<<<(int)std::min<int64_t>((n_cur + 255) / 256, nsm * 8), 256, 0, st>>>(T->rec.p, cur, n_cur, a,
-                                                                                            T->keys_a.p);
+        k_level_keys<<<(int)std::min<int64_t>((n_cur + 255) / 256, nsm * 8), 256, 0, st>>>(T->rec.p, cur, n_cur, d_lvl,
+                                                                                            nl, a, T->keys_a.p);
         ST_TRY(cudaPeekAtLastError());
+        prof.mark("keys", st);
+        int nbits = 1;
+        while ((1 << nbits) < nl) nbits++;
         size_t tb = 0;
-        ST_TRY(cub::DeviceSegmentedSort::SortKeys(nullptr, tb, T->keys_a.p, T->keys_b.p, (int)n_cur, ns, T->seg_b.p,
-                                                  T->seg_e.p, st));
+        ST_TRY(cub::DeviceRadixSort::SortPairs(nullptr, tb, T->keys_a.p, T->keys_b.p, cur, sorted_ids.p, (int)n_cur, 0,
+                                               32 + nbits, st));
         ST_TRY(T->temp.reserve(tb));
-        ST_TRY(cub::DeviceSegmentedSort::SortKeys(T->temp.p, tb, T->keys_a.p, T->keys_b.p, (int)n_cur, ns, T->seg_b.p,
-                                                  T->seg_e.p, st));
+        ST_TRY(cub::DeviceRadixSort::SortPairs(T->temp.p, tb, T->keys_a.p, T->keys_b.p, cur, sorted_ids.p, (int)n_cur,
+                                               0, 32 + nbits, st));
+        prof.mark("sort", st);
         COUNT_LAUNCH(1);
-        k_stree_split<<<(ns + 127) / 128, 128, 0, st>>>(T->keys_b.p, T->seg_b.p, T->seg_e.p, T->lohi.p, ns, T->d.eps,
-                                                        T->split_out.p, T->split_c.p);
+        k_stree_split<<<(ns + 127) / 128, 128, 0, st>>>(T->keys_b.p, d_sbe, d_lohi, ns, T->d.eps, T->split_out.p);
         ST_TRY(cudaPeekAtLastError());
-        std::vector<int4> so(2 * ns);
-        std::vector<float> sc(ns);
-        ST_TRY(cudaMemcpyAsync(so.data(), T->split_out.p, 2 * ns * sizeof(int4), cudaMemcpyDeviceToHost, st));
-        ST_TRY(cudaMemcpyAsync(sc.data(), T->split_c.p, ns * sizeof(float), cudaMemcpyDeviceToHost, st));
+        ST_TRY(cudaMemcpyAsync(T->hsplit.p, T->split_out.p, 2 * ns * sizeof(int4), cudaMemcpyDeviceToHost, st));
         ST_TRY(cudaStreamSynchronize(st));
+        const int4 *so = T->hsplit.p;
+        prof.mark("split", st);
         next.clear();
         segs.clear();
         int64_t off = 0;
@@ -440,9 +523,9 @@ static mpg_status stree_build(StreeState *T, cudaStream_t st) {
         for (int q = 0; q < ns; q++, node_id++) {
             const HNode &nd = level[split_idx[q]];
             int m = so[2 * q].x, eL = so[2 * q].y, eR = so[2 * q].z, s0 = so[2 * q].w, s1 = so[2 * q + 1].x;
-            float c = sc[q];
-            int cbits;
-            memcpy(&cbits, &c, 4);
+            int cbits = so[2 * q + 1].y;
+            float c;
+            memcpy(&c, &cbits, 4);
             hnodes[node_id].x = cbits;
             for (int side = 0; side < 2; side++) {
                 HNode ch = nd;
@@ -463,13 +546,16 @@ static mpg_status stree_build(StreeState *T, cudaStream_t st) {
         DBuf<int> &dst = cur_is_a ? T->ids_b : T->ids_a;
         ST_TRY(dst.reserve(off));
         if (!segs.empty()) {
-            ST_TRY(T->segs.reserve(segs.size()));
-            ST_TRY(cudaMemcpyAsync(T->segs.p, segs.data(), segs.size() * sizeof(int4), cudaMemcpyHostToDevice, st));
+            ST_TRY(T->hstage_b.reserve(segs.size()));
+            ST_TRY(T->dstage_b.reserve(segs.size()));
+            memcpy(T->hstage_b.p, segs.data(), segs.size() * sizeof(int4));
+            ST_TRY(cudaMemcpyAsync(T->dstage_b.p, T->hstage_b.p, segs.size() * sizeof(int4), cudaMemcpyHostToDevice, st));
             COUNT_LAUNCH(1);
-            k_copy_segments<unsigned long long><<<(int)segs.size(), 128, 0, st>>>(T->keys_b.p, dst.p, T->segs.p);
+            k_copy_segments<<<(int)std::min<int64_t>((off + 255) / 256, nsm * 8), 256, 0, st>>>(
+                sorted_ids.p, dst.p, T->dstage_b.p, (int)segs.size(), off);
             ST_TRY(cudaPeekAtLastError());
-            ST_TRY(cudaStreamSynchronize(st));
         }
+        prof.mark("childcopy", st);
         cur = dst.p;
         cur_is_a = !cur_is_a;
         level.swap(next);
@@ -486,6 +572,7 @@ static mpg_status stree_build(StreeState *T, cudaStream_t st) {
         ST_TRY(cudaMemcpyAsync(T->nodes.p, hnodes.data(), hnodes.size() * sizeof(int4), cudaMemcpyHostToDevice, st));
     ST_TRY(cudaMemcpyAsync(T->leaf_begin.p, lb.data(), n_leaves * sizeof(int64_t), cudaMemcpyHostToDevice, st));
     ST_TRY(cudaMemcpyAsync(T->leaf_count.p, lc.data(), n_leaves * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+    prof.mark("upload", st);
     // 4. lobes grouped by (leaf, type), stable within the leaf's list
     const int64_t NL = leaf_total;
     ST_TRY(T->grp_off.reserve((size_t)n_leaves * 127));
@@ -512,6 +599,7 @@ static mpg_status stree_build(StreeState *T, cudaStream_t st) {
         k_lobe_sample<<<blocks, 256, 0, st>>>(T->keys_b.p, T->leaf_ids.p, NL, T->lobe_sample.p);
         ST_TRY(cudaPeekAtLastError());
     }
+    prof.mark("lobesort", st);
     COUNT_LAUNCH(1);
     k_grp_off<<<(n_leaves * 127 + 255) / 256, 256, 0, st>>>(T->keys_b.p, NL, n_leaves, T->grp_off.p);
     ST_TRY(cudaPeekAtLastError());
@@ -521,14 +609,17 @@ static mpg_status stree_build(StreeState *T, cudaStream_t st) {
             T->rec.p, T->keys_b.p, T->lobe_sample.p, T->grp_off.p, NL, T->d.kappa_min, T->d.kappa_max, T->lobe_mu.p);
         ST_TRY(cudaPeekAtLastError());
     }
+    prof.mark("kappa", st);
     COUNT_LAUNCH(1);
     k_group_tables<<<(n_leaves * 126 + 127) / 128, 128, 0, st>>>(T->rec.p, T->lobe_sample.p, T->grp_off.p, n_leaves,
                                                                   T->E.p, T->lobe_prefix.p);
     ST_TRY(cudaPeekAtLastError());
+    prof.mark("groups", st);
     COUNT_LAUNCH(1);
     k_dir_cell_tables<<<(n_leaves + 127) / 128, 128, 0, st>>>(T->E.p, n_leaves, T->n_prefix.p, T->type_prefix.p);
     ST_TRY(cudaPeekAtLastError());
     ST_TRY(cudaStreamSynchronize(st));
+    prof.mark("tables", st);
     T->n_rec = 0; // "last iteration only" (P:426 footnote)
     return MPG_OK;
 }

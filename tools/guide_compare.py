@@ -55,10 +55,13 @@ def main():
     n_side = int(sys.argv[1]) if len(sys.argv) > 1 else 1024
     iters = int(sys.argv[2]) if len(sys.argv) > 2 else 8
     out = {"n_side": n_side, "walks_per_iteration": n_side * n_side, "iterations": iters}
-    for g in ("hist", "stree"):
+    guides = sys.argv[3].split(",") if len(sys.argv) > 3 else ["hist", "stree"]
+    for g in guides:
         t0 = time.time()
         out[g] = run(g, n_side, iters)
         out[g + "_wall_s"] = time.time() - t0
+    if len(guides) < 2:
+        return
     last = {g: out[g][-1] for g in ("hist", "stree")}
     out["summary"] = {
         "mean_w": {g: last[g]["mean_w"] for g in last},
