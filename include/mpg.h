@@ -137,7 +137,12 @@ typedef struct {
     uint64_t seed;         /* Philox key                                              */
     uint64_t walk_id_base; /* added to the walk index in the Philox counter          */
     int32_t max_iters_long;/* Newton cap for chains with k >= 3 (0: max_iters)        */
-    int32_t reserved;
+    int32_t recip_repeats; /* M >= 2: the reciprocal probability is estimated M times and averaged
+                              (R x M / TR x M, Fig. "repber"): repetition r runs its trials
+                              with Philox trial counter r*2^20 + t; trials[w] = sum of the M counts,
+                              w = T * (sum/M) / (P(n) pdf_L).  0 or 1: one estimate.  Needs k_max < 2^20;
+                              the walk is re-run once per repetition (outputs identical; stats: walks,
+                              converged, primary_iters and by_status count one pass, work counters all) */
 } mpg_walk_opts;
 
 /* Configurations (x_D, x_L): receivers; walk w uses receiver w / spp. */

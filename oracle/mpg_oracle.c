@@ -82,6 +82,8 @@ typedef struct {
     int32_t max_iters_long; /* cap for chains with k >= 3 (0: max_iters) */
     double tol, beta0, same_chain_eps, ray_eps;
     uint64_t seed, walk_id_base;
+    int32_t recip_repeats;  /* M >= 2: M independent reciprocal estimates averaged [R32] */
+    int32_t pad_;
 } orc_opts;
 
 typedef struct {
@@ -1113,21 +1115,28 @@ int orc_walks(const void *h, const orc_seed_cfg *cfg, const orc_opts *o, const f
             }
         }
         if (st == ST_CONVERGED && r->T > 0.0 && o->trials) {
-            uint32_t kk = 0;
+            /* R x M: repetition rep draws its trials with counter rep*2^20 + t [R32] */
+            int M = o->recip_repeats > 1 ? o->recip_repeats : 1;
+            uint32_t ksum = 0;
             double es = eps_same(sc, o);
-            for (uint32_t t = 1; t <= o->k_max; t++) {
-                cvtx y[KMAX];
-                int it2, k2;
-                uint32_t tau2;
-                seed_res s2r;
-                int s2 = attempt(sc, cfg, o, wid, t, xd, xL, y, &it2, &s2r, &k2, &tau2);
-                r->attempts++;
-                r->total_iters += it2;
-                if (s2 == ST_CONVERGED && k2 == k && tau2 == tau && same_chain(k, y, x, es)) { kk = t; break; }
+            for (int rep = 0; rep < M; rep++) {
+                uint32_t kk = 0;
+                for (uint32_t t = 1; t <= o->k_max; t++) {
+                    cvtx y[KMAX];
+                    int it2, k2;
+                    uint32_t tau2;
+                    seed_res s2r;
+                    int s2 = attempt(sc, cfg, o, wid, ((uint32_t)rep << 20) + t, xd, xL, y, &it2, &s2r, &k2, &tau2);
+                    r->attempts++;
+                    r->total_iters += it2;
+                    if (s2 == ST_CONVERGED && k2 == k && tau2 == tau && same_chain(k, y, x, es)) { kk = t; break; }
+                }
+                if (kk == 0) { kk = o->k_max; r->truncated = 1; }
+                ksum += kk;
             }
-            if (kk == 0) { kk = o->k_max; r->truncated = 1; }
-            r->trials = kk;
-            r->w = r->T * (double)kk / (r->Pn * r->pdfL); /* Eq. 15: w = T k / (P(n) pdf_L) */
+            r->trials = ksum;
+            /* Eq. 15: w = T <1/P> / (P(n) pdf_L), <1/P> = mean of the M geometric counts */
+            r->w = r->T * ((double)ksum / (double)M) / (r->Pn * r->pdfL);
         }
     }
     return 0;

@@ -61,7 +61,8 @@ SNODE = np.dtype([("split", np.float32), ("axis", np.int32), ("child", np.int32,
 class Opts(C.Structure):
     _fields_ = [("max_iters", C.c_int32), ("trials", C.c_int32), ("k_max", C.c_uint32), ("max_iters_long", C.c_int32),
                 ("tol", C.c_double), ("beta0", C.c_double), ("same_chain_eps", C.c_double), ("ray_eps", C.c_double),
-                ("seed", C.c_uint64), ("walk_id_base", C.c_uint64)]
+                ("seed", C.c_uint64), ("walk_id_base", C.c_uint64), ("recip_repeats", C.c_int32),
+                ("pad_", C.c_int32)]
 
 
 class WalkOut(C.Structure):
@@ -232,7 +233,7 @@ def make_opts(w, **over) -> Opts:
     o = w.opts
     d = dict(max_iters=o.max_iters, trials=o.trials, k_max=o.k_max, tol=o.tol, beta0=o.beta0, seed=o.seed,
              walk_id_base=o.walk_id_base, same_chain_eps=0.0, ray_eps=0.0,
-             max_iters_long=getattr(o, "max_iters_long", 0))
+             max_iters_long=getattr(o, "max_iters_long", 0), recip_repeats=getattr(o, "recip_repeats", 1))
     d.update(over)
     r = Opts()
     for k, v in d.items():

@@ -1088,6 +1088,8 @@ __global__ void k_sort_keys(const float4 *xD, const float4 *tgt, const int *bin,
     }
 }
 static size_t mk_ws_bytes(int64_t n) { return mk_layout(n).total; }
+// recip_repeats scratch after the walk workspace: w_r [n] f32, trials_r [n] u32, stats
+static size_t rep_bytes(int64_t n) { return ((size_t)n * 8 + sizeof(mpg_walk_stats) + 511) & ~(size_t)255; }
 
 // wavefront workspace layout: header, slot lists, free stack,
 // per-slot SoA state, ray lists, hits, hard entries, trial items
@@ -1124,10 +1126,33 @@ static WFLayout wf_layout(int64_t n, int k) {
     return L;
 }
 
+static size_t rep_offset(int64_t n, int k) {
+    return (std::max(wf_layout(n, k).total, mk_ws_bytes(n)) + 255) & ~(size_t)255;
+}
+// R x M: w += w_r, trials += trials_r (then w *= scale on the last repetition); work
+// counters of the repetition added to the caller's stats (walks/converged count one pass)
+__global__ void k_repeat_accum(float *w, uint32_t *trials, const float *w_r, const uint32_t *t_r, int64_t n,
+                               unsigned long long *stats, const unsigned long long *s_r, float scale) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        w[i] = __fmul_rn(__fadd_rn(w[i], w_r[i]), scale);
+        trials[i] += t_r[i];
+    }
+    if (stats && blockIdx.x == 0 && threadIdx.x < 11) {
+        // mpg_walk_stats: walks, converged, newton_iters, primary_iters, attempts, rays, trials, truncated,
+        // node_visits, tri_tests, vertex_iters
+        const int f = threadIdx.x;
+        if (f != 0 && f != 1 && f != 3) atomicAdd(stats + f, s_r[f]);
+    }
+}
+
+static mpg_status walk_dispatch(const mpg_scene *scene, const SeedCtx &g, const mpg_sampler_desc *sd,
+                                const mpg_walk_opts *o, const WalkParams &P, void *workspace, size_t workspace_bytes,
+                                cudaStream_t s);
+
 extern "C" size_t mpg_walk_workspace_size(int64_t n, const mpg_sampler_desc *sampler, const mpg_walk_opts *opts) {
     int k = sampler ? std::max(1, std::min(MPG_KMAX, (int)sampler->k)) : MPG_KMAX;
-    (void)opts; // one size serves both paths
-    return std::max(wf_layout(n, k).total, mk_ws_bytes(n));
+    (void)opts; // one size serves both paths (+ the per-repetition buffers of recip_repeats)
+    return rep_offset(n, k) + rep_bytes(n);
 }
 
 template <int KMAX, typename R, int MINB = (KMAX <= 2 ? MPG_WALK_MINB2 : MPG_WALK_MINB_LONG)>
@@ -1219,6 +1244,7 @@ static mpg_status launch_wavefront(const DScene &S, const SeedCtx &g, const Walk
     WFParams P;
     memset(&P, 0, sizeof(P));
     P.xD = MP.xD; P.nD = MP.nD; P.n = MP.n; P.spp = MP.spp;
+    P.trial_base = MP.trial_base;
     P.seed_xL = MP.seed_xL; P.seed_tgt = MP.seed_tgt; P.seed_bin = MP.seed_bin;
     P.chain = MP.chain; P.status = MP.status; P.iters = MP.iters; P.G = MP.G; P.T = MP.T; P.w = MP.w;
     P.trials = MP.trials; P.stats = MP.stats;
@@ -1417,8 +1443,40 @@ extern "C" mpg_status mpg_manifold_walk(const mpg_scene *scene, const mpg_guide 
     P.n_dbg = g_dbg_n;
     P.dbg_stride = g_dbg_stride;
     int k = g.k;
-    if (sd->mode == MPG_SEED_GUIDE_DIR)
-        ARG_CHECK(sb->ctype && sb->pn && out->ctype, "GUIDE_DIR needs seed ctype/pn and walk ctype arrays");
+    if (sd->mode >= MPG_SEED_GUIDE_DIR)
+        ARG_CHECK(sb->ctype && sb->pn && out->ctype, "GUIDE_DIR/STREE need seed ctype/pn and walk ctype arrays");
+    const int M = std::max(1, (int)o->recip_repeats);
+    ARG_CHECK(M == 1 || (o->trials && o->k_max < (1u << 20) && M <= 4096), "recip_repeats needs trials, k_max < 2^20, M <= 4096");
+    if (M == 1) return walk_dispatch(scene, g, sd, o, P, workspace, workspace_bytes, s);
+    // R x M: M independent trial sequences, averaged
+    char *rb = (char *)workspace + rep_offset(P.n, k);
+    float *w_r = (float *)rb;
+    uint32_t *t_r = (uint32_t *)(rb + (size_t)P.n * 4);
+    mpg_walk_stats *s_r = (mpg_walk_stats *)(((uintptr_t)(rb + (size_t)P.n * 8) + 255) & ~(uintptr_t)255);
+    st = walk_dispatch(scene, g, sd, o, P, workspace, workspace_bytes, s);
+    if (st != MPG_OK) return st;
+    for (int r = 1; r < M; r++) {
+        WalkParams Pr = P;
+        Pr.trial_base = (uint32_t)r << 20;
+        Pr.w = w_r;
+        Pr.trials = t_r;
+        Pr.stats = (unsigned long long *)s_r;
+        CUDA_TRY(cudaMemsetAsync(s_r, 0, sizeof(mpg_walk_stats), s));
+        st = walk_dispatch(scene, g, sd, o, Pr, workspace, workspace_bytes, s);
+        if (st != MPG_OK) return st;
+        COUNT_LAUNCH(1);
+        k_repeat_accum<<<(int)std::min<int64_t>((P.n + 255) / 256, (int64_t)num_sms() * 8), 256, 0, s>>>(
+            out->w, out->trials, w_r, t_r, P.n, (unsigned long long *)stats, (const unsigned long long *)s_r,
+            r == M - 1 ? 1.0f / (float)M : 1.0f);
+        CUDA_TRY(cudaPeekAtLastError());
+    }
+    return MPG_OK;
+}
+
+static mpg_status walk_dispatch(const mpg_scene *scene, const SeedCtx &g, const mpg_sampler_desc *sd,
+                                const mpg_walk_opts *o, const WalkParams &P, void *workspace, size_t workspace_bytes,
+                                cudaStream_t s) {
+    const int k = g.k;
     if (o->flags & MPG_FLAG_WAVEFRONT) {
         if (o->flags & MPG_FLAG_NEWTON_F64) {
             if (k <= 1) return launch_wavefront<1, double>(scene->d, g, P, workspace, workspace_bytes, s);
@@ -1438,7 +1496,7 @@ extern "C" mpg_status mpg_manifold_walk(const mpg_scene *scene, const mpg_guide 
         if (k <= 2) return launch_walk<2, double>(scene->d, g, P, s, workspace, (o->flags & MPG_FLAG_SORT) != 0);
         if (k <= 4) return launch_walk<4, double>(scene->d, g, P, s, workspace, (o->flags & MPG_FLAG_SORT) != 0);
         if (k <= 6) {
-            if (sd->mode == MPG_SEED_GUIDE_DIR)   // mixed chain lengths: see MPG_WALK_MINB_MIXED
+            if (sd->mode >= MPG_SEED_GUIDE_DIR)   // mixed chain lengths: see MPG_WALK_MINB_MIXED
                 return launch_walk<6, double, MPG_WALK_MINB_MIXED>(scene->d, g, P, s, workspace,
                                                                    (o->flags & MPG_FLAG_SORT) != 0);
             return launch_walk<6, double>(scene->d, g, P, s, workspace, (o->flags & MPG_FLAG_SORT) != 0);

@@ -79,6 +79,7 @@ struct WalkParams {
     // items (entry e, trial t) in doubling batches; lanes whose primary queue is
     // exhausted take items by ticket from a ring, in the same launch.  k = the
     // smallest successful trial: every trial below it has run (batch order).
+    uint32_t trial_base;        // Philox trial counter offset of trials t >= 1 (recip_repeats)
     uint32_t local_trials;
     uint32_t item_b0;           // first item batch of a hard entry
     uint32_t item_grow;         // later batches: previous << item_grow
@@ -482,7 +483,7 @@ __global__ void __launch_bounds__(128, MINB) k_walk(const DScene S, const SeedCt
                 Pn = P.seed_pn ? __ldg(P.seed_pn + w) : 1.0f;
             } else {
                 SeedRes sr;
-                ok = seed_target(S, g, P.walk_id_base + w, trial, xD, xL, sr);
+                ok = seed_target(S, g, P.walk_id_base + w, trial + P.trial_base, xD, xL, sr);
                 tgt = sr.tgt;
                 k = sr.n;
                 bits = sr.bits;

@@ -75,6 +75,7 @@ struct WFHeader {                 // device counters (in the workspace; zeroed b
 };
 
 struct WFParams {
+    uint32_t trial_base; // Philox trial counter offset of trials t >= 1 (recip_repeats)
     // inputs / outputs (as the persistent kernel)
     const float4 *xD, *nD;
     int64_t n;
@@ -195,7 +196,7 @@ __device__ __forceinline__ void wf_start(const DScene &S, const SeedCtx &g, cons
         pn = P.seed_pn ? __ldg(P.seed_pn + w) : 1.0f;
     } else {
         SeedRes sr;
-        ok = seed_target(S, g, P.walk_id_base + w, trial, xD, xyz(__ldg(P.seed_xL + w)), sr);
+        ok = seed_target(S, g, P.walk_id_base + w, trial + P.trial_base, xD, xyz(__ldg(P.seed_xL + w)), sr);
         tgt = sr.tgt;
         ct = (uint32_t)sr.n | ((sr.bits & 255u) << 4) | ((sr.learned ? 1u : 0u) << 12);
         pn = sr.Pn;

@@ -54,7 +54,7 @@ class mpg_walk_opts(C.Structure):
     _fields_ = [("max_iters", C.c_int32), ("tol", C.c_float), ("beta0", C.c_float), ("trials", C.c_int32),
                 ("k_max", C.c_uint32), ("same_chain_eps", C.c_float), ("ray_eps", C.c_float), ("flags", C.c_uint32),
                 ("seed", C.c_uint64), ("walk_id_base", C.c_uint64), ("max_iters_long", C.c_int32),
-                ("reserved", C.c_int32)]
+                ("recip_repeats", C.c_int32)]
 
 
 class mpg_query(C.Structure):
@@ -408,7 +408,7 @@ class DeviceScene:
         o = self.w.opts
         d = dict(max_iters=o.max_iters, tol=o.tol, beta0=o.beta0, trials=o.trials, k_max=o.k_max,
                  same_chain_eps=0.0, ray_eps=0.0, flags=o.flags, seed=o.seed, walk_id_base=o.walk_id_base,
-                 max_iters_long=o.max_iters_long)
+                 max_iters_long=o.max_iters_long, recip_repeats=o.recip_repeats)
         d.update(over)
         r = mpg_walk_opts()
         for k, v in d.items():

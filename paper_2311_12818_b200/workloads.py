@@ -90,6 +90,7 @@ class WalkOpts:
     walk_id_base: int = 0
     flags: int = 0                   # MPG_FLAG_* (4 = MPG_FLAG_NEWTON_F64)
     max_iters_long: int = 0          # Newton cap for chains with k >= 3 (0: max_iters)
+    recip_repeats: int = 1           # M reciprocal-probability estimates averaged (R x M)
 
 
 FLAG_NEWTON_F64 = 4

@@ -545,3 +545,29 @@ def test_trial_fallbacks_give_identical_walks(caps, monkeypatch):
         for k in ("status", "trials", "w"):
             assert np.array_equal(a[k], b[k]), (w.name, k)
         assert sa["trials"] == sb["trials"] and sa["truncated"] == sb["truncated"]
+
+
+@pytest.mark.parametrize("which,flags", [("cfg0", 0), ("cfg1", BENCH_FLAGS), ("cfg1wf", 1)])
+def test_repeated_reciprocal_estimates(which, flags):
+    """recip_repeats = 4 (R x 4, R32): the summed trial counts equal the oracle's
+    (walks both sides converge to the same chain), w agrees, and repetition 0 of the GPU
+    run is the single-estimate run (trials4 - trials1 = counts of repetitions 1..3 >= 3)."""
+    w = {"cfg0": lambda: W.config0(n_side=16, spp=8), "cfg1": lambda: W.config1(n_side=64, spp=1),
+         "cfg1wf": lambda: W.config1(n_side=64, spp=1)}[which]()
+    g1, s1, ext = PY.run_gpu(w, flags=w.opts.flags | flags)
+    g4, s4, _ = PY.run_gpu(w, flags=w.opts.flags | flags, recip_repeats=4)
+    for k in ("status", "iters", "G", "T"):
+        assert np.array_equal(g1[k], g4[k]), k
+    conv = (g1["status"] == 0) & (g1["T"] > 0)
+    assert (g4["trials"][conv] - g1["trials"][conv] >= 3).all()
+    assert s4["walks"] == s1["walks"] and s4["converged"] == s1["converged"]
+    assert s4["trials"] == int(g4["trials"].sum()) and s4["attempts"] > s1["attempts"]
+    ids = np.arange(w.n_walks)
+    o, s = PY.run_oracle(w, ids, recip_repeats=4)
+    rep = PY.compare(g4, o, ids, ext, w.seed.k)
+    both = (g4["status"] == 0) & (o["status"] == 0) & (g4["T"] > 0)
+    agree = (g4["trials"][both] == o["trials"][both]).mean()
+    print(which, rep["flag_agree"], agree)
+    assert rep["flag_agree"] >= 0.999 and agree >= 0.98
+    same = both & (g4["trials"] == o["trials"])
+    assert np.median(np.abs(g4["w"][same] - o["w"][same]) / np.maximum(o["w"][same], 1e-30)) < 1e-4

@@ -690,3 +690,28 @@ def test_progressive_loop_learns():
     tri = [r["trials"][r["trials"] > 0].mean() for r in res]
     assert conv[2] > 2 * conv[0], conv
     assert tri[2] < tri[0], tri
+
+
+# ---------------------------------------------------------------------------
+# R x M: M reciprocal-probability estimates averaged [R32]
+# ---------------------------------------------------------------------------
+def test_repeated_reciprocal_estimates_unbiased_and_lower_variance():
+    """Averaging M independent geometric counts keeps E[w] (Eq. 15 stays unbiased) and cuts
+    the variance of w; the solved chains (trial 0) are unchanged and every count is >= M."""
+    w = dataclasses.replace(W.config0(n_side=8, spp=64))
+    s = O.OracleScene(w)
+    ids = np.arange(w.n_walks)
+    a = s.walks(ids, s.opts())
+    b = s.walks(ids, s.opts(recip_repeats=4))
+    assert np.array_equal(a["status"], b["status"]) and np.array_equal(a["pos"], b["pos"])
+    conv = (a["status"] == 0) & (a["T"] > 0)
+    assert (b["trials"][conv] >= 4).all() and (a["trials"][conv] >= 1).all()
+    # per receiver: same mean within the standard errors, lower variance
+    wa = a["w"].reshape(-1, w.spp)
+    wb = b["w"].reshape(-1, w.spp)
+    se = np.sqrt(wa.var(1, ddof=1) / w.spp + wb.var(1, ddof=1) / w.spp)
+    ok = se > 0
+    z = np.abs(wa.mean(1) - wb.mean(1))[ok] / se[ok]
+    assert (z < 3).mean() >= 0.95 and z.max() < 5
+    assert abs(wa.mean() - wb.mean()) < 3 * np.sqrt(wa.var() / wa.size + wb.var() / wb.size)
+    assert wb.var(1).mean() < 0.8 * wa.var(1).mean()
