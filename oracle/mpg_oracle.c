@@ -1706,3 +1706,140 @@ void orc_record_samples(const float *xD, int32_t spp, int64_t n, const int32_t *
 
 /* vMF direction draw as seed mode 4 does it (test export) */
 void orc_vmf_sample(const float mu[3], float kap, float u1, float u2, float out[3]) { vmf_dir(mu, kap, u1, u2, out); }
+
+/* ------------------------------------------------------------------------ */
+/* Photon-based initial distribution: photons   */
+/* traced from the emitters through the specular surfaces until they cross   */
+/* the receiver plane; each landed photon with n >= 1 specular vertices is a */
+/* sub-path sample (x_D, x_L, w_D*, type, w = its power) from which the      */
+/* STree + vMF guide of iteration 0 is fitted instead of the empty guide.    */
+/* Reading R33: emission, R/T by Fresnel, plane landing.         */
+/* ------------------------------------------------------------------------ */
+typedef struct {
+    int64_t n_photons;      /* N: power of a photon = n_light * Phi_light / N */
+    uint64_t seed, photon_id_base;
+    float plane_point[3], plane_normal[3]; /* receiver plane; photons land crossing it against the normal */
+    int32_t max_vertices;   /* <= 6 */
+    float ray_eps;          /* 0: 1e-4 * extent */
+} orc_photon_desc;
+
+/* one photon: record (w = 0, type = -1 if it does not land after >= 1 specular vertex);
+ * nv, vertices (x_D order), prims, surfs for the pins */
+static void trace_photon(const orc_scene *sc, const orc_photon_desc *pd, int64_t p, orc_gsample *rec, int *nv_out,
+                         double *verts, int32_t *prims, int32_t *surfs) {
+    orc_opts o;
+    memset(&o, 0, sizeof(o));
+    o.seed = pd->seed;
+    uint64_t wid = pd->photon_id_base + (uint64_t)p;
+    double eps = pd->ray_eps > 0.0f ? pd->ray_eps : 1e-4 * sc->extent;
+    memset(rec, 0, sizeof(*rec));
+    rec->type = -1;
+    *nv_out = 0;
+    uint32_t r[4];
+    /* emission: light uniformly, position on it (as sample_light, purpose 8), direction (purpose 9) */
+    draw(&o, wid, 8u, 0u, r);
+    int li = sc->n_light > 1 ? (int)uidx(r[2], (uint32_t)sc->n_light) : 0;
+    const orc_light *L = &sc->light[li];
+    float xLf[3];
+    double phi_light;
+    v3 d;
+    uint32_t q[4];
+    draw(&o, wid, 9u, 0u, q);
+    double u1 = (double)u01(q[0]), u2 = (double)u01(q[1]);
+    double ph = 6.28318530717958647692 * u2;
+    if (L->kind == 1) {
+        float a = u01(r[0]) - 0.5f, b = u01(r[1]) - 0.5f;
+        for (int j = 0; j < 3; j++) xLf[j] = L->position[j] + (a * L->edge_u[j] + b * L->edge_v[j]);
+        v3 nl = cross(vf(L->edge_u), vf(L->edge_v));
+        double area = len(nl);
+        nl = mul(nl, 1.0 / area);
+        phi_light = (double)L->emit * area * 3.14159265358979323846; /* Lambertian one-sided: L A pi */
+        v3 b1, b2;
+        onb(nl, &b1, &b2);
+        double st = sqrt(u1), ct = sqrt(1.0 - u1);   /* cosine-weighted about n_L */
+        d = add(mul(nl, ct), add(mul(b1, st * cos(ph)), mul(b2, st * sin(ph))));
+    } else {
+        for (int j = 0; j < 3; j++) xLf[j] = L->position[j];
+        phi_light = 4.0 * 3.14159265358979323846 * (double)L->emit; /* isotropic point: 4 pi I */
+        double z = 1.0 - 2.0 * u1, st = sqrt(fmax(0.0, 1.0 - z * z));
+        d = V(st * cos(ph), z, st * sin(ph));
+    }
+    double w = (double)sc->n_light * phi_light / (double)pd->n_photons;
+    v3 o3 = vf(xLf);
+    v3 pp = vf(pd->plane_point), pn = nrmz(vf(pd->plane_normal));
+    cvtx x[KMAX];
+    int isT[KMAX];
+    int nv = 0;
+    uint32_t rt[4];
+    for (;;) {
+        hit_t h = closest(sc, o3, d, eps, 1e300, 0, 1);
+        double den = dot(d, pn);
+        double tp = den < 0.0 ? dot(sub(pp, o3), pn) / den : -1.0;
+        if (tp > eps && (h.surf < 0 || tp < h.t)) { /* lands on the receiver plane */
+            if (nv >= 1) {
+                v3 xd = add(o3, mul(d, tp));
+                float xD[3] = {(float)xd.x, (float)xd.y, (float)xd.z};
+                for (int j = 0; j < 3; j++) { rec->xD[j] = xD[j]; rec->xL[j] = xLf[j]; }
+                float v1[3] = {(float)x[nv - 1].p.x, (float)x[nv - 1].p.y, (float)x[nv - 1].p.z};
+                float dx = v1[0] - xD[0], dy = v1[1] - xD[1], dz = v1[2] - xD[2];
+                float l = sqrtf(dx * dx + dy * dy + dz * dz);
+                rec->omega[0] = dx / l; rec->omega[1] = dy / l; rec->omega[2] = dz / l;
+                uint32_t tau = 0;
+                for (int i = 0; i < nv; i++) tau |= (uint32_t)isT[nv - 1 - i] << i; /* x_D order */
+                rec->type = (1 << nv) - 2 + (int32_t)tau;
+                rec->w = (float)w;
+                *nv_out = nv;
+                for (int i = 0; i < nv; i++) {
+                    const cvtx *v = &x[nv - 1 - i];
+                    verts[3 * i] = v->p.x; verts[3 * i + 1] = v->p.y; verts[3 * i + 2] = v->p.z;
+                    prims[i] = v->prim; surfs[i] = v->surf;
+                }
+            }
+            return;
+        }
+        if (h.surf < 0 || nv == pd->max_vertices) return;      /* escaped, or chain too long */
+        const orc_surface *f = &sc->surf[h.surf];
+        if (f->mat == 2) return;                                  /* absorbed by a diffuse occluder */
+        x[nv].p = h.p; x[nv].prim = h.prim; x[nv].surf = h.surf;
+        v3 ng = geo_normal(sc, &x[nv]);
+        v3 dummy[1];
+        v3 n = shading_normal(sc, &x[nv], 0, NULL, dummy);
+        int outside = dot(d, ng) < 0.0;
+        if (dot(d, n) > 0.0) n = mul(n, -1.0);
+        double ci = -dot(d, n);
+        if (!(ci > 0.0)) return;
+        int t = 0;
+        if (f->mat == 0) {
+            w *= (double)f->reflectance;
+        } else {                                                  /* R with probability F (Fresnel), else T */
+            double e1 = outside ? f->eta_out : f->eta_in, e2 = outside ? f->eta_in : f->eta_out;
+            double F = orc_fresnel(ci, e1, e2);
+            if ((nv & 3) == 0) draw(&o, wid, 10u, (uint32_t)(nv >> 2), rt);
+            t = (double)u01(rt[nv & 3]) >= F;
+            if (t) {
+                double eta = e1 / e2;
+                double k2 = 1.0 - eta * eta * (1.0 - ci * ci);
+                if (k2 < 0.0) return;
+                d = nrmz(add(mul(d, eta), mul(n, eta * ci - sqrt(k2))));
+            }
+        }
+        if (!t) d = add(d, mul(n, 2.0 * ci));
+        isT[nv] = t;
+        o3 = h.p;
+        nv++;
+    }
+}
+
+void orc_trace_photons(const void *h, const orc_photon_desc *pd, int64_t first, int64_t count, orc_gsample *rec,
+                       int32_t *nv, double *verts, int32_t *prims, int32_t *surfs) {
+    for (int64_t i = 0; i < count; i++) {
+        int n_v = 0;
+        double vv[3 * KMAX];
+        int32_t pr[KMAX], su[KMAX];
+        trace_photon((const orc_scene *)h, pd, first + i, rec + i, &n_v, vv, pr, su);
+        if (nv) nv[i] = n_v;
+        if (verts) memcpy(verts + 3 * KMAX * i, vv, sizeof(vv));
+        if (prims) memcpy(prims + KMAX * i, pr, sizeof(pr));
+        if (surfs) memcpy(surfs + KMAX * i, su, sizeof(su));
+    }
+}

@@ -55,6 +55,12 @@ class SeedCfg(C.Structure):
 # STree + vMF guide: 48-byte sample record and tree node, as in mpg_oracle.c
 GSAMPLE = np.dtype([("xD", np.float32, (3,)), ("xL", np.float32, (3,)), ("omega", np.float32, (3,)),
                     ("w", np.float32), ("type", np.int32), ("pad", np.int32)])
+class PhotonDesc(C.Structure):
+    _fields_ = [("n_photons", C.c_int64), ("seed", C.c_uint64), ("photon_id_base", C.c_uint64),
+                ("plane_point", C.c_float * 3), ("plane_normal", C.c_float * 3), ("max_vertices", C.c_int32),
+                ("ray_eps", C.c_float)]
+
+
 SNODE = np.dtype([("split", np.float32), ("axis", np.int32), ("child", np.int32, (2,))])
 
 
@@ -132,6 +138,7 @@ def lib():
         _lib.orc_stree_get.argtypes = [P] + [P] * 10
         _lib.orc_record_samples.argtypes = [P, C.c_int32, C.c_int64, P, P, P, P, P, P, P]
         _lib.orc_vmf_sample.argtypes = [P, C.c_float, C.c_float, C.c_float, P]
+        _lib.orc_trace_photons.argtypes = [P, C.POINTER(PhotonDesc), C.c_int64, C.c_int64, P, P, P, P, P]
         _lib.orc_scatter.restype = C.c_int
         _lib.orc_scatter.argtypes = [C.c_int, C.c_double, C.c_double, dp, dp, dp]
     return _lib
@@ -312,6 +319,23 @@ class OracleScene:
         c.nodes, c.grp_off = _ptr(G["nodes"]), _ptr(G["grp_off"])
         c.lobe_prefix, c.lobe_mu = _ptr(G["lobe_prefix"]), _ptr(G["lobe_mu"])
         c.n_prefix, c.type_prefix = _ptr(G["n_prefix"]), _ptr(G["type_prefix"])
+
+    def trace_photons(self, n_photons, plane_point, plane_normal, first=0, count=None, seed=0, base=0,
+                      max_vertices=6):
+        """Photon records (GSAMPLE) of photons first..first+count of an N = n_photons run, plus
+        per photon: vertex count, vertices / prims / surfs in x_D order."""
+        count = n_photons - first if count is None else count
+        d = PhotonDesc(n_photons=n_photons, seed=seed, photon_id_base=base, max_vertices=max_vertices, ray_eps=0.0)
+        d.plane_point[:] = [float(v) for v in plane_point]
+        d.plane_normal[:] = [float(v) for v in plane_normal]
+        rec = np.zeros(count, GSAMPLE)
+        nv = np.zeros(count, np.int32)
+        verts = np.zeros((count, KMAX, 3), np.float64)
+        prims = np.zeros((count, KMAX), np.int32)
+        surfs = np.zeros((count, KMAX), np.int32)
+        lib().orc_trace_photons(self.h, C.byref(d), first, count, _ptr(rec), _ptr(nv), _ptr(verts), _ptr(prims),
+                                _ptr(surfs))
+        return rec, nv, verts, prims, surfs
 
     def set_energies(self, E, c=None):
         c = c or self.cfg
