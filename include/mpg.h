@@ -256,6 +256,25 @@ mpg_status mpg_guide_download_stree(const mpg_guide *guide, int32_t *nodes, int6
                                     int32_t *leaf_ids, int32_t *grp_off, int32_t *lobe_sample, uint64_t *lobe_prefix,
                                     float *lobe_mu, uint64_t *n_prefix, uint64_t *type_prefix, void *stream);
 
+/* ---- photon-based initial distribution (R33) ----
+ * Trace n_photons photons from the emitters (uniform light choice, cosine-weighted area
+ * lights, isotropic point lights; power n_lights * Phi / n_photons) through the specular
+ * surfaces (R with probability F at dielectrics, conductors R with weight rho; diffuse
+ * surfaces absorb) until they cross the receiver plane against its normal.  records
+ * (device, n_photons) gets one mpg_guide_sample per photon: landed after 1..max_vertices
+ * specular vertices -> (x_D, x_L, w_D*, type, w = power), else w = 0, type = -1.  Feed them
+ * to an STree guide (mpg_guide_set_samples + mpg_guide_rebuild) as the initial guide.
+ * Philox counters (photon_id_base + p, purpose 8 / 9 / 10, trial). Asynchronous. */
+typedef struct {
+    int64_t n_photons;
+    uint64_t seed, photon_id_base;
+    float plane_point[3], plane_normal[3];
+    int32_t max_vertices;  /* 1..6 */
+    float ray_eps;         /* 0 => 1e-4 * scene extent */
+} mpg_photon_desc;
+mpg_status mpg_trace_photons(const mpg_scene *scene, const mpg_photon_desc *desc, mpg_guide_sample *records,
+                             void *stream);
+
 /* Debug/test entry: closest specular (spec_only=1) or any-surface hit of n rays.
  * orig/dir: device float4 [n]; outputs device: t [n], prim [n] (original triangle id or -1),
  * surf [n] (-1 = miss). */

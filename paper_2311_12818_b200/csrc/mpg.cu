@@ -887,6 +887,7 @@ extern "C" mpg_status mpg_guide_download_dir_tables(const mpg_guide *g, uint64_t
 }
 
 #include "stree.cuh"
+#include "photons.cuh"
 
 // ----------------------------------------------------------------------------
 // seeds

@@ -80,6 +80,12 @@ class mpg_stree_info(C.Structure):
     _fields_ = [(f, C.c_int64) for f in ("n_nodes", "n_leaves", "root_ref", "thr", "n_valid", "n_lobes")]
 
 
+class mpg_photon_desc(C.Structure):
+    _fields_ = [("n_photons", C.c_int64), ("seed", C.c_uint64), ("photon_id_base", C.c_uint64),
+                ("plane_point", C.c_float * 3), ("plane_normal", C.c_float * 3), ("max_vertices", C.c_int32),
+                ("ray_eps", C.c_float)]
+
+
 GUIDE_SAMPLE_BYTES = 48
 
 STATS_FIELDS = ["walks", "converged", "newton_iters", "primary_iters", "attempts", "rays", "trials", "truncated",
@@ -101,7 +107,7 @@ EXPORTS = ["mpg_scene_create", "mpg_scene_destroy", "mpg_scene_get_info", "mpg_t
            "mpg_guide_download", "mpg_guide_download_dir_tables", "mpg_sample_seeds", "mpg_walk_workspace_size", "mpg_manifold_walk", "mpg_estimate",
            "mpg_debug_trace", "mpg_last_error", "mpg_version", "mpg_kernel_launches", "mpg_guide_create_stree",
            "mpg_guide_record_samples", "mpg_guide_set_samples", "mpg_guide_get_samples", "mpg_guide_stree_info",
-           "mpg_guide_download_stree"]
+           "mpg_guide_download_stree", "mpg_trace_photons"]
 
 _lib = None
 
@@ -147,6 +153,7 @@ def lib():
             "mpg_guide_set_samples": (st, [P, P, C.c_int64, P]),
             "mpg_guide_get_samples": (st, [P, P, C.POINTER(C.c_int64), P]),
             "mpg_guide_stree_info": (st, [P, C.POINTER(mpg_stree_info)]),
+            "mpg_trace_photons": (st, [P, C.POINTER(mpg_photon_desc), P, P]),
             "mpg_guide_download_stree": (st, [P] + [P] * 10 + [P]),
         }
         for name, (res, args) in sig.items():
@@ -293,6 +300,28 @@ def mpg_guide_download_stree(h, stream=None) -> dict:
     for k in ("leaf_ids", "lobe_sample", "lobe_prefix", "lobe_mu"):
         out[k] = out[k][:NL]
     return out
+
+
+def mpg_trace_photons(scene, desc: mpg_photon_desc, records, stream=None):
+    """records: device uint8 tensor of desc.n_photons * 48 bytes (mpg_guide_sample)."""
+    _check(lib().mpg_trace_photons(scene, C.byref(desc), _ptr(records), _stream_ptr(stream)), "mpg_trace_photons")
+
+
+def photon_init(ds, n_photons: int, plane_point, plane_normal, seed: int = 0, base: int = 0, stream=None):
+    """Photon-based p_0: trace photons on the GPU and fit the STree guide from
+    them (replaces the empty iteration-0 guide).  Returns the number of landed photons."""
+    import torch
+    d = mpg_photon_desc(n_photons=n_photons, seed=seed, photon_id_base=base, max_vertices=6, ray_eps=0.0)
+    d.plane_point = (C.c_float * 3)(*[float(v) for v in plane_point])
+    d.plane_normal = (C.c_float * 3)(*[float(v) for v in plane_normal])
+    cap = ds.stree_desc.max_samples
+    rec = torch.empty(n_photons * GUIDE_SAMPLE_BYTES, dtype=torch.uint8, device="cuda")
+    mpg_trace_photons(ds.h, d, rec, stream)
+    landed = int((rec.view(-1, 12)[:, 9].view(torch.float32) > 0).sum())   # w > 0
+    assert n_photons <= cap, "photon records exceed the STree guide's max_samples"
+    mpg_guide_set_samples(ds.guide, rec, n_photons, stream)
+    mpg_guide_rebuild(ds.guide, stream)
+    return landed
 
 
 def mpg_sample_seeds(scene, guide, sampler, query, opts, seeds, stream=None):
