@@ -212,7 +212,7 @@ def run_ours(args):
     iters = 8 if progressive else 1
     # independent partitions (weak scaling): rank r owns walk ids [r*n*iters, (r+1)*n*iters)
     w.opts.walk_id_base = D.walk_id_base(rank, w.n_walks * iters)
-    ds = mpg.DeviceScene(w, stree_capacity=w.n_walks * world)
+    ds = mpg.DeviceScene(w, stree_capacity=max(w.n_walks * world, args.photons))
     b = mpg.Batch(w.xD, w.nD, w.spp, w.seed.k)
     opts = ds.opts(flags=w.opts.flags | (1 if args.wavefront else 0) | (2 if args.hostloop else 0) |
                    (4 if args.f64 else 0) | (0 if args.no_sort else 8))
@@ -233,9 +233,17 @@ def run_ours(args):
         else:
             exchange = lambda d: D.exchange_guide(d, hbuf)
 
+    plane = (w.xD[0].tolist(), w.nD[0].tolist())   # receiver plane (photon landing, R33)
+
+    def photon_init():
+        if stree and args.photons:      # photon-based p_0: iteration 0 from photons
+            mpg.photon_init(ds, args.photons, plane[0], plane[1], seed=1, base=rank * args.photons)
+
     def step():
         if progressive:
-            mpg.run_progressive(ds, b, opts, iterations=iters, exchange=exchange)
+            mpg.mpg_guide_reset(ds.guide)
+            photon_init()
+            mpg.run_progressive(ds, b, opts, iterations=iters, exchange=exchange, reset=False)
         else:
             mpg.run_step(ds, b, opts, accumulate=guided)
 
@@ -263,6 +271,7 @@ def run_ours(args):
         e0.record(stream)
         if progressive:
             mpg.mpg_guide_reset(ds.guide)
+            photon_init()
         base = opts.walk_id_base
         for it in range(iters):
             opts.walk_id_base = base + it * b.n
@@ -383,7 +392,9 @@ def run_ours(args):
                 "scaling": "weak", "vs_baseline": None, "dtype": "f32+f64" if opts.flags & 4 else "f32", "data": "synthetic",
                 "config": {"workload": CONFIG_NAMES[args.config] + (
                                " -- guide: STree over (x_D, x_L) + per-type vMF mixtures (SURVEY 8(f)1) in place of "
-                               "the histogram" if stree else ""), "n_walks_per_gpu": b.n, "k": w.seed.k,
+                               "the histogram" if stree else "") + (
+                               f"; iteration 0 from {args.photons} photons (SURVEY 8(f)4)" if stree and args.photons
+                               else ""), "n_walks_per_gpu": b.n, "k": w.seed.k,
                            "max_iters": w.opts.max_iters, "trials": "on (k_max 1024)",
                            "l2": "256 MB buffer written before every timed step (inputs < 126 MB L2)",
                            "order": ("primaries in walk order" if not opts.flags & 8 else
@@ -428,6 +439,8 @@ def main():
     ap.add_argument("--ref-walks", type=int, default=100000)
     ap.add_argument("--guide", default="hist", choices=["hist", "stree"],
                     help="configs[4] guide: BASELINE's histogram (default) or the paper's STree + vMF (SURVEY 8(f)1)")
+    ap.add_argument("--photons", type=int, default=0,
+                    help="with --guide stree: photon-based initial guide from this many photons (SURVEY 8(f)4)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--wavefront", action="store_true", help="wavefront path (MPG_FLAG_WAVEFRONT)")

@@ -317,7 +317,7 @@ def photon_init(ds, n_photons: int, plane_point, plane_normal, seed: int = 0, ba
     cap = ds.stree_desc.max_samples
     rec = torch.empty(n_photons * GUIDE_SAMPLE_BYTES, dtype=torch.uint8, device="cuda")
     mpg_trace_photons(ds.h, d, rec, stream)
-    landed = int((rec.view(-1, 12)[:, 9].view(torch.float32) > 0).sum())   # w > 0
+    landed = int((rec.view(torch.float32).view(-1, 12)[:, 9] > 0).sum())   # w > 0
     assert n_photons <= cap, "photon records exceed the STree guide's max_samples"
     mpg_guide_set_samples(ds.guide, rec, n_photons, stream)
     mpg_guide_rebuild(ds.guide, stream)
@@ -521,14 +521,16 @@ class Batch:
 
 
 def run_progressive(ds: DeviceScene, b: Batch, opts: mpg_walk_opts, iterations: int = 8, stream=None,
-                    on_iteration=None, exchange=None, id_stride=None):
+                    on_iteration=None, exchange=None, id_stride=None, reset=True):
     """configs[4] (R22): guide reset (learned branch absent) at iteration 0, then per
     iteration: seeds -> walk (+trials) -> estimator -> accumulate [-> exchange] ->
     rebuild tables from this iteration only (P:426 footnote).  Iteration it
     uses walk_id_base = base + it*id_stride (default b.n) so every iteration draws
     fresh random numbers.  `exchange(ds)` (multi-process runs, dist.exchange_guide)
-    replaces this rank's histogram by the sum over ranks before the rebuild."""
-    mpg_guide_reset(ds.guide, stream)
+    replaces this rank's histogram by the sum over ranks before the rebuild.
+    reset=False keeps the caller's initial guide (e.g. photon_init)."""
+    if reset:
+        mpg_guide_reset(ds.guide, stream)
     base = opts.walk_id_base
     stride = b.n if id_stride is None else id_stride
     for it in range(iterations):

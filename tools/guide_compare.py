@@ -23,12 +23,21 @@ from paper_2311_12818_b200 import mpg, workloads as W  # noqa: E402
 
 
 def run(guide, n_side, iters):
-    w = W.config4(n_side=n_side, guide=guide)
-    ds = mpg.DeviceScene(w)
+    photons = guide.endswith("+photons")          # photon-based p_0
+    w = W.config4(n_side=n_side, guide=guide.split("+")[0])
+    ds = mpg.DeviceScene(w, stree_capacity=max(n_side * n_side, 1 << 20))
     b = mpg.Batch(w.xD, w.nD, w.spp, w.seed.k)
     opts = ds.opts(flags=w.opts.flags | 8)
     rows = []
     mpg.mpg_guide_reset(ds.guide)
+    if photons:
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        e[0].record()
+        landed = mpg.photon_init(ds, 1 << 20, (0, -2, 0), (0, 1, 0), seed=1)
+        e[1].record()
+        torch.cuda.synchronize()
+        print(guide, json.dumps({"photons": 1 << 20, "landed": landed, "ms": e[0].elapsed_time(e[1]),
+                                 "tree": mpg.mpg_guide_stree_info(ds.guide)}), flush=True)
     for it in range(iters):
         opts.walk_id_base = it * b.n
         e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
@@ -43,12 +52,15 @@ def run(guide, n_side, iters):
         row = dict(it=it, converged=st["converged"], mean_w=float(wv.mean()), second_moment=float((wv * wv).mean()),
                    var_w=float(wv.var()), step_ms=e[0].elapsed_time(e[1]), rebuild_ms=e[1].elapsed_time(e[2]),
                    trials_per_conv=st["trials"] / max(1, st["converged"]), newton_iters=st["newton_iters"])
-        if guide == "stree":
+        if guide.startswith("stree"):
             row["tree"] = mpg.mpg_guide_stree_info(ds.guide)
         rows.append(row)
         print(guide, json.dumps(row), flush=True)
     ds.close()
     return rows
+
+
+os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
 
 
 def main():
@@ -60,7 +72,9 @@ def main():
         t0 = time.time()
         out[g] = run(g, n_side, iters)
         out[g + "_wall_s"] = time.time() - t0
-    if len(guides) < 2:
+    if "hist" not in guides or "stree" not in guides:
+        json.dump(out, open(os.path.join(ROOT, "gpurun_out", f"guide_compare_{n_side}_{'_'.join(guides)}.json"), "w"),
+                  indent=1)
         return
     last = {g: out[g][-1] for g in ("hist", "stree")}
     out["summary"] = {
@@ -71,6 +85,9 @@ def main():
         "mean_rebuild_ms": {g: float(np.mean([r["rebuild_ms"] for r in out[g][1:]])) for g in last},
     }
     print(json.dumps(out["summary"]), flush=True)
+    for g in guides:
+        if g not in ("hist", "stree"):
+            out["summary"]["converged_per_iteration_" + g] = [r["converged"] for r in out[g]]
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
     json.dump(out, open(os.path.join(ROOT, "gpurun_out", f"guide_compare_{n_side}.json"), "w"), indent=1)
 
