@@ -80,6 +80,7 @@ struct WalkParams {
     // exhausted take items by ticket from a ring, in the same launch.  k = the
     // smallest successful trial: every trial below it has run (batch order).
     uint32_t trial_base;        // Philox trial counter offset of trials t >= 1 (recip_repeats)
+    size_t trav_bytes;          // host side: bytes of nodes + triangle positions (L2 window)
     uint32_t local_trials;
     uint32_t item_b0;           // first item batch of a hard entry
     uint32_t item_grow;         // later batches: previous << item_grow
