@@ -102,8 +102,10 @@ __device__ __forceinline__ float3 vmf_dir(float4 m, float u1, float u2) {
 
 __device__ __forceinline__ float canon0(float x) { return __fadd_rn(x, 0.0f); } // -0 -> +0 (R28)
 
-// leaf of the STree containing (x_D, x_L) (R28)
-__device__ __forceinline__ int stree_leaf(const SeedCtx &g, float3 xD, float3 xL) {
+// leaf of the STree containing (x_D, x_L) (R28).  Out of line, like the lobe draw
+// below: seed_target is inlined into k_walk, whose instruction-cache footprint is a
+// measured limiter (configs[4] +4 % with these paths inlined)
+__device__ __noinline__ int stree_leaf(const SeedCtx &g, float3 xD, float3 xL) {
     float p[6] = {canon0(xD.x), canon0(xD.y), canon0(xD.z), canon0(xL.x), canon0(xL.y), canon0(xL.z)};
     int ref = g.root_ref;
     while (ref >= 0) {
@@ -114,6 +116,26 @@ __device__ __forceinline__ int stree_leaf(const SeedCtx &g, float3 xD, float3 xL
         ref = v < __int_as_float(nd.x) ? nd.z : nd.w;
     }
     return ~ref;
+}
+
+// mode 4, learned branch: lobe i of group (leaf, type) by the integer CDF of W_i, then
+// w_D ~ vMF(mu_i, kappa_i) (Eq. 12, R30-R31); returns the deduction target x_D + w_D
+__device__ __noinline__ float3 stree_lobe_target(const SeedCtx &g, int grp, uint32_t rw, uint64_t wid, uint32_t trial,
+                                                 float3 xD, int &bin) {
+    const int *go = g.grp_off + grp;
+    int glo = __ldg(go), ghi = __ldg(go + 1);
+    uint64_t Sl = __ldg(g.lobe_prefix + ghi - 1);
+    uint64_t tl = mulhi_u64(rw, Sl);
+    int lo2 = glo, hi2 = ghi - 1; // upper_bound over the group
+    while (lo2 < hi2) {
+        int mid = (lo2 + hi2) >> 1;
+        if ((uint64_t)__ldg(g.lobe_prefix + mid) > tl) hi2 = mid;
+        else lo2 = mid + 1;
+    }
+    bin = lo2;
+    uint4 r2 = rng_draw(g.seed, wid, 2u, trial);
+    float3 om = vmf_dir(__ldg(g.lobe_mu + lo2), u01(r2.x), u01(r2.y));
+    return f3(FA(xD.x, om.x), FA(xD.y, om.y), FA(xD.z, om.z));
 }
 
 __device__ MPG_COLD bool seed_target(const DScene &S, const SeedCtx &g, uint64_t wid, uint32_t trial,
@@ -220,20 +242,7 @@ __device__ MPG_COLD bool seed_target(const DScene &S, const SeedCtx &g, uint64_t
             sr.bits = (uint32_t)m;
             sr.learned = true;
             if (g.mode == 4) { // lobe ~ W_i, then w_D ~ vMF(mu_i, kappa_i) (Eq. 12)
-                const int *go = g.grp_off + (size_t)c * 127 + g0 + m;
-                int glo = __ldg(go), ghi = __ldg(go + 1);
-                uint64_t Sl = __ldg(g.lobe_prefix + ghi - 1);
-                uint64_t tl = mulhi_u64(r.w, Sl);
-                int lo2 = glo, hi2 = ghi - 1; // upper_bound over the group
-                while (lo2 < hi2) {
-                    int mid = (lo2 + hi2) >> 1;
-                    if ((uint64_t)__ldg(g.lobe_prefix + mid) > tl) hi2 = mid;
-                    else lo2 = mid + 1;
-                }
-                bin = lo2;
-                uint4 r2 = rng_draw(g.seed, wid, 2u, trial);
-                float3 om = vmf_dir(__ldg(g.lobe_mu + lo2), u01(r2.x), u01(r2.y));
-                tgt = f3(FA(xD.x, om.x), FA(xD.y, om.y), FA(xD.z, om.z));
+                tgt = stree_lobe_target(g, c * 127 + g0 + m, r.w, wid, trial, xD, bin);
                 return true;
             }
             int nb = g.bins_x * g.bins_y;

@@ -157,6 +157,8 @@ def lib():
             "mpg_guide_download_stree": (st, [P] + [P] * 10 + [P]),
         }
         for name, (res, args) in sig.items():
+            if "MPG_LIB" in os.environ and not hasattr(L, name):
+                continue      # an older experiment build (tools/minb_sweep.sh) lacks newer entry points
             fn = getattr(L, name)
             fn.restype = res
             fn.argtypes = args
