@@ -139,3 +139,32 @@ def test_wavefront_cfg4_guided():
     assert rep["n_other_chain"] <= max(1, 0.001 * rep["both"])
     vis = both & (g["status"] == 0)
     assert np.median(np.abs(g["w"][vis] - o["w"][vis]) / np.maximum(o["w"][vis], 1e-30)) < 1e-3
+
+
+def test_wavefront_stree_guided_matches_persistent_kernel():
+    """The STree + vMF sampler (MPG_SEED_GUIDE_STREE) on the wavefront path:
+    the same walks as the persistent kernel (every draw depends on the walk id alone)."""
+    import torch
+    from paper_2311_12818_b200 import mpg
+    w = W.config4(n_side=96, guide="stree")
+    r = W.synthetic_guide_samples(60000, seed=17)
+    out = []
+    for flags in (8, WF):
+        ds = mpg.DeviceScene(w, stree_capacity=len(r))
+        t = torch.from_numpy(np.frombuffer(r.tobytes(), np.uint8).copy()).cuda()
+        mpg.mpg_guide_set_samples(ds.guide, t, len(r))
+        mpg.mpg_guide_rebuild(ds.guide)
+        b = mpg.Batch(w.xD, w.nD, w.spp, w.seed.k)
+        mpg.run_step(ds, b, ds.opts(flags=w.opts.flags | flags))
+        torch.cuda.synchronize()
+        out.append(b.results())
+        ext = ds.extent
+        ds.close()
+    a, g = out
+    assert np.array_equal(a["seed_ctype"], g["seed_ctype"]) and np.array_equal(a["bin"], g["bin"])
+    both = _paths_agree(a, g)
+    assert both.sum() > 100
+    n = a["ctype"][both] & 15
+    used = np.arange(a["pos"].shape[1])[None, :] < n[:, None]           # each chain's own vertices
+    d = np.where(used, np.linalg.norm(a["pos"][both] - g["pos"][both], axis=2), 0.0).max(1)
+    assert (d < 1e-4 * ext).mean() >= 0.999
