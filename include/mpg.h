@@ -141,8 +141,9 @@ typedef struct {
                               (R x M / TR x M, Fig. "repber"): repetition r runs its trials
                               with Philox trial counter r*2^20 + t; trials[w] = sum of the M counts,
                               w = T * (sum/M) / (P(n) pdf_L).  0 or 1: one estimate.  Needs k_max < 2^20;
-                              the walk is re-run once per repetition (outputs identical; stats: walks,
-                              converged, primary_iters and by_status count one pass, work counters all) */
+                              repetitions r >= 1 run only the trials of walks that converged (persistent
+                              kernel; the wavefront path re-runs the primaries); stats: walks, converged,
+                              primary_iters and by_status count one pass, work counters all passes */
 } mpg_walk_opts;
 
 /* Configurations (x_D, x_L): receivers; walk w uses receiver w / spp. */

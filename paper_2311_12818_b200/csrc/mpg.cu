@@ -1108,7 +1108,7 @@ __global__ void k_sort_keys(const float4 *xD, const float4 *tgt, const int *bin,
 }
 static size_t mk_ws_bytes(int64_t n) { return mk_layout(n).total; }
 // recip_repeats scratch after the walk workspace: w_r [n] f32, trials_r [n] u32, stats
-static size_t rep_bytes(int64_t n) { return ((size_t)n * 8 + sizeof(mpg_walk_stats) + 511) & ~(size_t)255; }
+static size_t rep_bytes(int64_t n) { return ((size_t)n * 12 + sizeof(mpg_walk_stats) + 767) & ~(size_t)255; }
 
 // wavefront workspace layout: header, slot lists, free stack,
 // per-slot SoA state, ray lists, hits, hard entries, trial items
@@ -1524,7 +1524,10 @@ extern "C" mpg_status mpg_manifold_walk(const mpg_scene *scene, const mpg_guide 
     float *w_r = (float *)rb;
     uint32_t *t_r = (uint32_t *)(rb + (size_t)P.n * 4);
     mpg_walk_stats *s_r = (mpg_walk_stats *)(((uintptr_t)(rb + (size_t)P.n * 8) + 255) & ~(uintptr_t)255);
-    st = walk_dispatch(scene, g, sd, o, P, workspace, workspace_bytes, s);
+    uint32_t *ps_r = (uint32_t *)(((uintptr_t)(s_r + 1) + 255) & ~(uintptr_t)255);
+    WalkParams P0 = P;
+    P0.psurf_out = ps_r;
+    st = walk_dispatch(scene, g, sd, o, P0, workspace, workspace_bytes, s);
     if (st != MPG_OK) return st;
     for (int r = 1; r < M; r++) {
         WalkParams Pr = P;
@@ -1532,6 +1535,8 @@ extern "C" mpg_status mpg_manifold_walk(const mpg_scene *scene, const mpg_guide 
         Pr.w = w_r;
         Pr.trials = t_r;
         Pr.stats = (unsigned long long *)s_r;
+        Pr.psurf_out = ps_r;
+        Pr.trials_only = (o->flags & MPG_FLAG_WAVEFRONT) ? 0 : 1;   // the wavefront path re-runs primaries
         CUDA_TRY(cudaMemsetAsync(s_r, 0, sizeof(mpg_walk_stats), s));
         st = walk_dispatch(scene, g, sd, o, Pr, workspace, workspace_bytes, s);
         if (st != MPG_OK) return st;

@@ -80,6 +80,8 @@ struct WalkParams {
     // exhausted take items by ticket from a ring, in the same launch.  k = the
     // smallest successful trial: every trial below it has run (batch order).
     uint32_t trial_base;        // Philox trial counter offset of trials t >= 1 (recip_repeats)
+    uint32_t *psurf_out;        // recip_repeats: primary surface ids per walk (written by repetition 0)
+    int trials_only;            // recip_repeats r >= 1: primaries are final (outputs of repetition 0); run trials only
     size_t trav_bytes;          // host side: bytes of nodes + triangle positions (L2 window)
     uint32_t local_trials;
     uint32_t item_b0;           // first item batch of a hard entry
@@ -402,6 +404,24 @@ __global__ void __launch_bounds__(128, MINB) k_walk(const DScene S, const SeedCt
                     lid = 0;
                     if (S.n_light > 1) lid = (int)uidx(rng_draw(g.seed, P.walk_id_base + w, 0u, 0u).z, (uint32_t)S.n_light);
                     phase = PH_SEED;
+                    if (P.trials_only) {
+                        // R x M repetition r >= 1 (R32): the primary chain, its type, surfaces and T
+                        // are the outputs of repetition 0; only the trial sequence r*2^20 + t runs
+                        const float T0 = P.T[w];
+                        if (P.status[w] == ST_CONVERGED && T0 > 0.0f && P.trials_on) {
+                            const uint32_t ct = P.out_ctype ? (uint32_t)P.out_ctype[w] : ((uint32_t)g.k | (g.tau << 4));
+                            pk = (int)(ct & 15u);
+                            ptau = ct >> 4;
+                            psurf = P.psurf_out[w];
+                            Tprim = T0;
+                            trial = 1;
+                        } else {
+                            P.trials[w] = 0;
+                            P.w[w] = 0.0f;
+                            walk_resolved(P);
+                            phase = PH_FETCH;
+                        }
+                    }
                 } else {
                     phase = PH_WAIT;   // primaries exhausted: trial items
                 }
@@ -634,6 +654,7 @@ __global__ void __launch_bounds__(128, MINB) k_walk(const DScene S, const SeedCt
                         if (i >= k) break;
                         psurf |= (uint32_t)(surf[i] & 15) << (4 * i);
                     }
+                    if (P.psurf_out) P.psurf_out[w] = psurf;
                     if (queue_drained(P, drained) && P.items && hard_publish(P, w, psurf, pk, ptau, 0u, seq_only))
                         phase = PH_FETCH;
                     else {
