@@ -328,6 +328,11 @@ mpg_status mpg_manifold_walk(const mpg_scene *scene, const mpg_guide *guide, con
 /* Estimator (Eq. 3): mean[r] = (1/spp) sum_s w[r*spp+s]; var (nullable) = sample variance. */
 mpg_status mpg_estimate(const float *w, int64_t n_recv, int32_t spp, float *mean, float *var, void *stream);
 
+/* Render-pass splat (Eq. 3 across passes, "never splat the samples
+ * produced in the training stage"): sum[r] += mean_j w[r*spp+j] and (nullable) sumsq[r] += its
+ * square, fp64 device arrays [n_recv] the caller zeroes; image = sum / passes. */
+mpg_status mpg_splat(const float *w, int64_t n_recv, int32_t spp, double *sum, double *sumsq, void *stream);
+
 /* Debug: for the next mpg_manifold_walk calls, record (||C||_inf, beta) of every
  * primary Newton iteration of walks w < n_walks into buf[w*stride + 2*it + {0,1}]
  * (device float); buf = NULL disables.  Not thread-safe; for tests and tools. */

@@ -1612,6 +1612,27 @@ extern "C" mpg_status mpg_estimate(const float *w, int64_t n_recv, int32_t spp, 
     return MPG_OK;
 }
 
+// splat (Eq. 3 over render passes): sum[r] += sum_j w[r*spp+j], sumsq[r] += (that pass mean)^2, fp64
+__global__ void k_splat(const float *w, int64_t n_recv, int spp, double *sum, double *sumsq) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n_recv; r += (int64_t)gridDim.x * blockDim.x) {
+        double s = 0.0;
+        for (int j = 0; j < spp; j++) s += (double)w[r * spp + j];
+        s /= spp;
+        sum[r] += s;
+        if (sumsq) sumsq[r] += s * s;
+    }
+}
+
+extern "C" mpg_status mpg_splat(const float *w, int64_t n_recv, int32_t spp, double *sum, double *sumsq, void *stream) {
+    ARG_CHECK(w && sum && n_recv >= 0 && spp >= 1, "bad argument");
+    if (n_recv == 0) return MPG_OK;
+    int blocks = (int)std::min<int64_t>((n_recv + 255) / 256, (int64_t)num_sms() * 8);
+    COUNT_LAUNCH(1);
+    k_splat<<<blocks, 256, 0, as_stream(stream)>>>(w, n_recv, spp, sum, sumsq);
+    CUDA_TRY(cudaPeekAtLastError());
+    return MPG_OK;
+}
+
 extern "C" const char *mpg_last_error(void) { return g_err.c_str(); }
 extern "C" int32_t mpg_version(void) { return 1; }
 extern "C" uint64_t mpg_kernel_launches(void) { return g_launches.load(std::memory_order_relaxed); }

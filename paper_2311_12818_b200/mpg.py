@@ -107,7 +107,7 @@ EXPORTS = ["mpg_scene_create", "mpg_scene_destroy", "mpg_scene_get_info", "mpg_t
            "mpg_guide_download", "mpg_guide_download_dir_tables", "mpg_sample_seeds", "mpg_walk_workspace_size", "mpg_manifold_walk", "mpg_estimate",
            "mpg_debug_trace", "mpg_last_error", "mpg_version", "mpg_kernel_launches", "mpg_guide_create_stree",
            "mpg_guide_record_samples", "mpg_guide_set_samples", "mpg_guide_get_samples", "mpg_guide_stree_info",
-           "mpg_guide_download_stree", "mpg_trace_photons"]
+           "mpg_guide_download_stree", "mpg_trace_photons", "mpg_splat"]
 
 _lib = None
 
@@ -154,6 +154,7 @@ def lib():
             "mpg_guide_get_samples": (st, [P, P, C.POINTER(C.c_int64), P]),
             "mpg_guide_stree_info": (st, [P, C.POINTER(mpg_stree_info)]),
             "mpg_trace_photons": (st, [P, C.POINTER(mpg_photon_desc), P, P]),
+            "mpg_splat": (st, [P, C.c_int64, C.c_int32, P, P, P]),
             "mpg_guide_download_stree": (st, [P] + [P] * 10 + [P]),
         }
         for name, (res, args) in sig.items():
@@ -343,6 +344,10 @@ def mpg_manifold_walk(scene, guide, sampler, query, seeds, opts, out, stats, wor
 
 def mpg_estimate(w, n_recv, spp, mean, var=None, stream=None):
     _check(lib().mpg_estimate(_ptr(w), n_recv, spp, _ptr(mean), _ptr(var), _stream_ptr(stream)), "mpg_estimate")
+
+
+def mpg_splat(w, n_recv, spp, sum_, sumsq=None, stream=None):
+    _check(lib().mpg_splat(_ptr(w), n_recv, spp, _ptr(sum_), _ptr(sumsq), _stream_ptr(stream)), "mpg_splat")
 
 
 def mpg_debug_trace(buf=None, n_walks=0, stride=0):
@@ -557,3 +562,69 @@ def run_step(ds: DeviceScene, b: Batch, opts: mpg_walk_opts, stream=None, estima
             mpg_guide_record_samples(ds.guide, b.query, b.seeds, b.out, b.n, stream)
         else:
             mpg_guide_accumulate(ds.guide, b.query, b.out, b.n, stream)
+
+
+def training_schedule(budget_passes: int, train_frac: float = 0.3):
+    """The paper's online training schedule (reading R34), in passes of one walk
+    per receiver: training iterations of 1, 2, 4, ... passes (doubling, Mueller 17); after an
+    iteration, a new (doubled) one starts only while less than half of the training budget
+    floor(train_frac * budget) is used, otherwise the current iteration continues until the
+    training budget is used up; training stops at that budget.  Returns (passes per training
+    iteration, render passes)."""
+    T = int(train_frac * budget_passes)
+    iters, used, i = [], 0, 0
+    while used < T:
+        n = min(1 << i, T - used)
+        iters.append(n)
+        used += n
+        if used >= T:
+            break
+        if 2 * used < T:
+            i += 1
+        else:                       # continue the current iteration to the end of training
+            iters[-1] += T - used
+            used = T
+    return iters, budget_passes - T
+
+
+def run_train_render(ds: DeviceScene, b: Batch, opts: mpg_walk_opts, budget_passes: int, stream=None,
+                     photons=None, on_iteration=None, train_frac: float = 0.3):
+    """Progressive train/render loop at walk level: training
+    iterations by training_schedule (each guide fitted from the last iteration's samples
+    only), then render passes with the final guide, splatted into a per-receiver fp64
+    sum; training samples are never splatted.  photons = (n, plane_point, plane_normal)
+    starts an STree guide from photons.  Returns (image, per-receiver
+    variance of the pass means, schedule)."""
+    import torch
+    iters, render = training_schedule(budget_passes, train_frac)
+    if ds.stree and iters:
+        need = max(max(iters) * b.n, photons[0] if photons else 0)
+        if need > ds.stree_desc.max_samples:
+            raise MPGError(f"STree guide holds {ds.stree_desc.max_samples} records; this schedule needs {need} "
+                           f"(DeviceScene(..., stree_capacity={need}))")
+    mpg_guide_reset(ds.guide, stream)
+    if photons is not None and ds.stree:
+        photon_init(ds, photons[0], photons[1], photons[2], stream=stream)
+    base = opts.walk_id_base
+    p = 0
+    for it, n_pass in enumerate(iters):
+        for _ in range(n_pass):
+            opts.walk_id_base = base + p * b.n
+            run_step(ds, b, opts, stream, estimate=False, accumulate=True)
+            p += 1
+        mpg_guide_rebuild(ds.guide, stream)
+        if on_iteration is not None:
+            on_iteration(it, n_pass)
+    dev = b.w.device
+    s = torch.zeros(b.n_recv, dtype=torch.float64, device=dev)
+    s2 = torch.zeros(b.n_recv, dtype=torch.float64, device=dev)
+    for _ in range(render):
+        opts.walk_id_base = base + p * b.n
+        run_step(ds, b, opts, stream, estimate=False, accumulate=False)
+        mpg_splat(b.w, b.n_recv, b.spp, s, s2, stream)
+        p += 1
+    opts.walk_id_base = base
+    n = max(render, 1)
+    img = s / n
+    var = (s2 / n - img * img) * n / max(n - 1, 1)
+    return img, var, (iters, render)

@@ -1,0 +1,52 @@
+"""configs[4] at full size: the progressive train/render loop at equal
+budget -- untrained render vs the paper's schedule with the histogram guide, the STree
+guide and the photon-started STree guide.  Reports the variance of the final image
+(mean over receivers of the pass variance / render passes), the time, and the
+efficiency 1 / (variance x time).  Usage (GPU box): python tools/train_render.py [budget]"""
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+from paper_2311_12818_b200 import mpg, workloads as W  # noqa: E402
+
+
+def main():
+    budget = int(sys.argv[1]) if len(sys.argv) > 1 else 32
+    rows = []
+    for name, guide, frac, photons in (("untrained", "hist", 0.0, None), ("hist", "hist", 0.3, None),
+                                       ("stree", "stree", 0.3, None),
+                                       ("stree+photons", "stree", 0.3, (1 << 20, (0, -2, 0), (0, 1, 0)))):
+        w = W.config4(guide=guide)
+        iters, _ = mpg.training_schedule(budget, frac)
+        ds = mpg.DeviceScene(w, stree_capacity=max([1] + iters) * w.n_walks)
+        b = mpg.Batch(w.xD, w.nD, w.spp, w.seed.k)
+        opts = ds.opts(flags=w.opts.flags | 8)
+        mpg.run_train_render(ds, b, opts, 4, train_frac=frac, photons=photons)     # warm-up (allocations)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        img, var, sched = mpg.run_train_render(ds, b, opts, budget, train_frac=frac, photons=photons)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        v_img = float(var.mean()) / max(sched[1], 1)
+        row = dict(run=name, schedule=sched, ms=ms, image_mean=float(img.mean()), image_variance=v_img,
+                   efficiency=1.0 / (v_img * ms))
+        rows.append(row)
+        print(json.dumps(row), flush=True)
+        ds.close()
+    for r in rows:
+        r["efficiency_vs_untrained"] = r["efficiency"] / rows[0]["efficiency"]
+        r["variance_vs_untrained"] = r["image_variance"] / rows[0]["image_variance"]
+    out = {"budget_passes": budget, "walks_per_pass": 1 << 20, "rows": rows}
+    print(json.dumps(out), flush=True)
+    os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+    json.dump(out, open(os.path.join(ROOT, "gpurun_out", f"train_render_{budget}.json"), "w"), indent=1)
+
+
+if __name__ == "__main__":
+    main()
