@@ -222,7 +222,7 @@ typedef struct {
     float eps;            /* overlap fraction of the split (0.1, P:523 footnote)           */
     float c_thr;          /* leaf threshold c sqrt|S| (1)                           */
     float kappa_min;      /* vMF concentration clamp (1, R30)                              */
-    float kappa_max;      /* (1e4, R30)                                                    */
+    float kappa_max;      /* (300, R30: measured, fewer fireflies than 3e3 / 1e4)          */
     int32_t max_depth;    /* 32                                                            */
     int32_t reserved;
 } mpg_stree_desc;

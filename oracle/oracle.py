@@ -192,10 +192,10 @@ def guide_dir_tables(H: np.ndarray):
     return npf, tpf, dpf
 
 
-STREE_DEFAULTS = dict(eps=0.1, c_thr=1.0, max_depth=32, kappa_min=1.0, kappa_max=1.0e4)
+STREE_DEFAULTS = dict(eps=0.1, c_thr=1.0, max_depth=32, kappa_min=1.0, kappa_max=300.0)
 
 
-def stree_build(records: np.ndarray, eps=0.1, c_thr=1.0, max_depth=32, kappa_min=1.0, kappa_max=1.0e4) -> dict:
+def stree_build(records: np.ndarray, eps=0.1, c_thr=1.0, max_depth=32, kappa_min=1.0, kappa_max=300.0) -> dict:
     """STree + vMF guide from sample records (GSAMPLE array): tree, leaf lists, lobes, tables."""
     L = lib()
     rec = np.ascontiguousarray(records, GSAMPLE)

@@ -372,7 +372,7 @@ def _f3(v):
 class DeviceScene:
     """Scene + (optional) guide of a Workload, resident on the current CUDA device."""
 
-    def __init__(self, w: "W.Workload", stream=None, stree_capacity=None):
+    def __init__(self, w: "W.Workload", stream=None, stree_capacity=None, stree_kappa_max=300.0):
         import torch
         if not torch.cuda.is_available():
             raise MPGError("no CUDA device: the manifold walk has no CPU path")
@@ -407,7 +407,7 @@ class DeviceScene:
         self.stree = sp.mode == W.SEED_GUIDE_STREE
         if self.stree:
             d = mpg_stree_desc(max_samples=int(stree_capacity if stree_capacity is not None else w.n_walks),
-                               eps=0.1, c_thr=1.0, kappa_min=1.0, kappa_max=1.0e4, max_depth=32)
+                               eps=0.1, c_thr=1.0, kappa_min=1.0, kappa_max=float(stree_kappa_max), max_depth=32)
             self.stree_desc = d
             self.guide = mpg_guide_create_stree(d)
         elif sp.mode in (W.SEED_GUIDE_UV, W.SEED_GUIDE_DIR):

@@ -28,7 +28,7 @@ def _oracle_records(r):
 def _gpu_build(records, eps=0.1, c_thr=1.0, max_depth=32):
     import torch
     from paper_2311_12818_b200 import mpg
-    d = mpg.mpg_stree_desc(max_samples=max(1, len(records)), eps=eps, c_thr=c_thr, kappa_min=1.0, kappa_max=1.0e4,
+    d = mpg.mpg_stree_desc(max_samples=max(1, len(records)), eps=eps, c_thr=c_thr, kappa_min=1.0, kappa_max=300.0,
                            max_depth=max_depth)
     g = mpg.mpg_guide_create_stree(d)
     if len(records):
