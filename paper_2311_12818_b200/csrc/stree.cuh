@@ -638,7 +638,17 @@ extern "C" mpg_status mpg_guide_create_stree(const mpg_stree_desc *desc, mpg_gui
     g->n_types = 126;
     g->stree = new StreeState();
     g->stree->d = *desc;
-    if (g->stree->rec.reserve(desc->max_samples) != cudaSuccess) {
+    // pre-size the build's buffers for max_samples (measured: ~22 % of records are samples on
+    // configs[4], lobes ~5x the samples, a level ~1.2x its parent): growth inside a rebuild
+    // costs cudaMalloc/cudaFree device syncs (~1 s on the first full-size rebuild otherwise)
+    StreeState *T0 = g->stree;
+    const size_t ms = (size_t)std::max<int64_t>(desc->max_samples, 1);
+    bool okr = T0->flags.reserve(ms) == cudaSuccess && T0->ids_a.reserve(ms) == cudaSuccess &&
+               T0->ids_b.reserve(ms) == cudaSuccess && T0->ids_c.reserve(ms) == cudaSuccess &&
+               T0->keys_a.reserve(ms * 3 / 2) == cudaSuccess && T0->keys_b.reserve(ms * 3 / 2) == cudaSuccess &&
+               T0->leaf_ids.reserve(ms * 3 / 2) == cudaSuccess && T0->lobe_sample.reserve(ms * 3 / 2) == cudaSuccess &&
+               T0->lobe_prefix.reserve(ms * 3 / 2) == cudaSuccess && T0->lobe_mu.reserve(ms * 3 / 2) == cudaSuccess;
+    if (!okr || g->stree->rec.reserve(desc->max_samples) != cudaSuccess) {
         mpg_guide_destroy(g);
         return fail(MPG_ERR_OOM, "STree sample buffer allocation failed");
     }
