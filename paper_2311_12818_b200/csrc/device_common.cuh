@@ -164,6 +164,11 @@ template <typename T, int N, int M> __device__ __forceinline__ void rset2(T (&a)
 // Child ref: >= 0 node index, < 0 leaf ~(first_tri << 3 | count - 1),
 // 0x7fffffff empty slot (point box at 3e38: never entered).
 #define NODE_F4(W) ((W) == 4 ? 8 : 4)
+// load path of BVH nodes and leaf triangles in the traversal loop (experiment knob:
+// __ldcg keeps them out of L1, leaving L1 to the lanes' local memory)
+#ifndef MPG_LDN
+#define MPG_LDN __ldg
+#endif
 #define TRAV_STACK(W) ((W) == 4 ? 96 : 64)
 
 // One node visit of the ordered traversal: returns the nearest child whose box
@@ -178,9 +183,9 @@ __device__ __forceinline__ int bvh_visit(const float4 *nodes, int node, float3 o
                                          float tmax, int *stack, int &sp) {
   if (W == 4) {
     const float4 *nd = nodes + NODE_F4(4) * node;
-    const float4 lx = __ldg(nd), hx = __ldg(nd + 1), ly = __ldg(nd + 2), hy = __ldg(nd + 3), lz = __ldg(nd + 4),
-                 hz = __ldg(nd + 5);
-    const int4 ch = __ldg(reinterpret_cast<const int4 *>(nd + 6));
+    const float4 lx = MPG_LDN(nd), hx = MPG_LDN(nd + 1), ly = MPG_LDN(nd + 2), hy = MPG_LDN(nd + 3), lz = MPG_LDN(nd + 4),
+                 hz = MPG_LDN(nd + 5);
+    const int4 ch = MPG_LDN(reinterpret_cast<const int4 *>(nd + 6));
     const float INF = __int_as_float(0x7f800000);
     float t[4];
     int c[4] = {ch.x, ch.y, ch.z, ch.w};
@@ -214,8 +219,8 @@ __device__ __forceinline__ int bvh_visit(const float4 *nodes, int node, float3 o
     return c[0];
   } else {
     const float4 *nd = nodes + NODE_F4(2) * node;
-    float4 a = __ldg(nd), b = __ldg(nd + 1), c = __ldg(nd + 2);
-    int4 ch = __ldg(reinterpret_cast<const int4 *>(nd + 3));
+    float4 a = MPG_LDN(nd), b = MPG_LDN(nd + 1), c = MPG_LDN(nd + 2);
+    int4 ch = MPG_LDN(reinterpret_cast<const int4 *>(nd + 3));
     float tx0 = fmaf(a.x, idir.x, -oi.x), tx1 = fmaf(a.w, idir.x, -oi.x);
     float ty0 = fmaf(a.y, idir.y, -oi.y), ty1 = fmaf(b.x, idir.y, -oi.y);
     float tz0 = fmaf(a.z, idir.z, -oi.z), tz1 = fmaf(b.y, idir.z, -oi.z);
@@ -432,8 +437,8 @@ __device__ __forceinline__ bool trace(const DScene &S, float3 o, float3 d, float
                 int start = v >> 3, cnt = (v & 7) + 1;
                 for (int j = start; j < start + cnt; j++) {
                     st.tris++;
-                    float4 p0 = __ldg(S.tpos + TSTRIDE * j), p1 = __ldg(S.tpos + TSTRIDE * j + 1),
-                           p2 = __ldg(S.tpos + TSTRIDE * j + 2);
+                    float4 p0 = MPG_LDN(S.tpos + TSTRIDE * j), p1 = MPG_LDN(S.tpos + TSTRIDE * j + 1),
+                           p2 = MPG_LDN(S.tpos + TSTRIDE * j + 2);
                     if (spec_only && __float_as_int(p2.w) == 0) continue;
                     float t, c0, c1, c2;
                     if (tri_hit(r, xyz(p0), xyz(p1), xyz(p2), tmin, best, t, c0, c1, c2)) {
