@@ -1210,6 +1210,14 @@ static mpg_status launch_walk(const DScene &S, const SeedCtx &g, WalkParams P, c
     static int occ2 = 0, occ4 = 0;
     int &occ = wide ? occ4 : occ2;
     if (!occ) {
+        // shared-memory carve-out preference (MPG_CARVEOUT percent, unset: driver default);
+        // the kernel needs 1.7 KB of shared memory per block, the rest of the unified
+        // L1/shared array can cache nodes and the lanes' local memory
+        if (const char *e = getenv("MPG_CARVEOUT")) {
+            int pc = atoi(e);
+            CUDA_TRY(cudaFuncSetAttribute(k_walk<KMAX, R, 4, MINB>, cudaFuncAttributePreferredSharedMemoryCarveout, pc));
+            CUDA_TRY(cudaFuncSetAttribute(k_walk<KMAX, R, 2, MINB>, cudaFuncAttributePreferredSharedMemoryCarveout, pc));
+        }
         CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
             &occ, wide ? k_walk<KMAX, R, 4, MINB> : k_walk<KMAX, R, 2, MINB>, 128, 0));
         if (occ <= 0) occ = 1;
