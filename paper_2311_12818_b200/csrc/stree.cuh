@@ -463,8 +463,10 @@ static mpg_status stree_build(StreeState *T, cudaStream_t st) {
         ST_TRY(T->dstage_a.reserve(n4));
         int4 *h4 = T->hstage_a.p;
         memcpy(h4, segs.data(), n_ls * sizeof(int4));
+        // split nodes come first in the level array (children are laid out split-first):
+        // only they are keyed and sorted
         int2 *h_lvl = (int2 *)(h4 + n_ls);
-        for (int i = 0; i < nl; i++) h_lvl[i] = make_int2((int)level[i].b, (int)level[i].n);
+        for (int q = 0; q < ns; q++) h_lvl[q] = make_int2((int)level[split_idx[q]].b, (int)level[split_idx[q]].n);
         int2 *h_sbe = (int2 *)(h4 + n_ls + (nl + 1) / 2);
         float2 *h_lohi = (float2 *)(h4 + n_ls + (nl + 1) / 2 + (ns + 1) / 2);
         for (int q = 0; q < ns; q++) {
@@ -487,8 +489,8 @@ static mpg_status stree_build(StreeState *T, cudaStream_t st) {
         }
         prof.mark("leafcopy", st);
         if (split_idx.empty()) break;
-        int64_t n_cur = 0;
-        for (auto &nd : level) n_cur = std::max<int64_t>(n_cur, nd.b + nd.n);
+        int64_t n_cur = 0;   // elements of the split nodes: [0, n_cur) of the level array
+        for (int q = 0; q < ns; q++) n_cur = std::max<int64_t>(n_cur, level[split_idx[q]].b + level[split_idx[q]].n);
         ST_TRY(T->keys_a.reserve(n_cur));
         ST_TRY(T->keys_b.reserve(n_cur));
         ST_TRY(T->split_out.reserve(2 * ns));
@@ -497,11 +499,11 @@ static mpg_status stree_build(StreeState *T, cudaStream_t st) {
         ST_TRY(sorted_ids.reserve(n_cur));
         COUNT_LAUNCH(1);
         k_level_keys<<<(int)std::min<int64_t>((n_cur + 255) / 256, nsm * 8), 256, 0, st>>>(T->rec.p, cur, n_cur, d_lvl,
-                                                                                            nl, a, T->keys_a.p);
+                                                                                            ns, a, T->keys_a.p);
         ST_TRY(cudaPeekAtLastError());
         prof.mark("keys", st);
         int nbits = 1;
-        while ((1 << nbits) < nl) nbits++;
+        while ((1 << nbits) < ns) nbits++;
         size_t tb = 0;
         ST_TRY(cub::DeviceRadixSort::SortPairs(nullptr, tb, T->keys_a.p, T->keys_b.p, cur, sorted_ids.p, (int)n_cur, 0,
                                                32 + nbits, st));
@@ -532,14 +534,23 @@ static mpg_status stree_build(StreeState *T, cudaStream_t st) {
                 int64_t b0 = side == 0 ? s0 : m - eL, b1 = side == 0 ? m + eR : s1;
                 if (side == 0) ch.hi[a] = c;
                 else ch.lo[a] = c;
-                ch.b = off;
+                ch.b = nd.b + b0;   // source position in this level's sorted ids (laid out below)
                 ch.n = b1 - b0;
                 ch.depth = nd.depth + 1;
                 ch.parent = node_id;
                 ch.side = side;
-                if (ch.n > 0) segs.push_back(make_int4((int)(nd.b + b0), (int)off, (int)ch.n, 0));
-                off += ch.n;
                 next.push_back(ch);
+            }
+        }
+        // lay out the next level split-first (the children that will split, in order, then
+        // the future leaves): the next level sorts only [0, split elements)
+        for (int pass = 0; pass < 2; pass++) {
+            for (auto &ch : next) {
+                const bool will_leaf = ch.n <= T->thr || ch.depth >= T->d.max_depth || na == 0;
+                if (will_leaf != (pass == 1)) continue;
+                if (ch.n > 0) segs.push_back(make_int4((int)ch.b, (int)off, (int)ch.n, 0));
+                ch.b = off;
+                off += ch.n;
             }
         }
         ARG_CHECK(off < (1ll << 31), "STree level too large");
