@@ -500,3 +500,31 @@ def synthetic_guide_samples(n: int, seed: int = 0, invalid_frac: float = 0.3, n_
     r["w"][bad] = 0.0
     r["type"][bad] = -1
     return r
+
+
+def synthetic_walk_outputs(xD: np.ndarray, spp: int, seed: int = 0, k_max: int = 6, x1_plane_y=None,
+                           x1_extent=None):
+    """Seeded stand-ins for one walk call's outputs (inputs of the accumulate / record unit
+    tests, so neither side's expected values come from the other): per walk a status
+    (60 % CONVERGED, the rest MAXITER / SEED_FAIL / OCCLUDED), w ~ LogNormal(0, 1) (0 unless
+    CONVERGED), chain length n in 1..k_max and type bits, x_L on a unit square at y = 5, and
+    the first vertex x_1: on the plane y = x1_plane_y over x1_extent = (x0, z0, x1, z1) if
+    given (surface-(u,v) guides), else x_D + a unit upper-hemisphere direction."""
+    rng = np.random.default_rng(seed)
+    n = xD.shape[0] * spp
+    status = rng.choice(np.array([0, 1, 2, 5], np.uint8), size=n, p=[0.6, 0.15, 0.15, 0.1])
+    w = np.where(status == 0, rng.lognormal(0.0, 1.0, n), 0.0).astype(np.float32)
+    k = rng.integers(1, k_max + 1, n)
+    tau = rng.integers(0, 1 << 30, n) & ((1 << k) - 1)
+    ctype = (k | (tau << 4)).astype(np.uint16)
+    xd = np.repeat(np.asarray(xD, np.float64), spp, axis=0)
+    if x1_plane_y is not None:
+        x0, z0, x1e, z1e = x1_extent
+        x1 = np.stack([rng.uniform(x0, x1e, n), np.full(n, x1_plane_y), rng.uniform(z0, z1e, n)], 1)
+    else:
+        d = rng.normal(size=(n, 3))
+        d[:, 1] = np.abs(d[:, 1]) + 1e-3
+        d /= np.linalg.norm(d, axis=1, keepdims=True)
+        x1 = xd + d * rng.uniform(0.5, 3.0, (n, 1))
+    xL = np.stack([rng.uniform(-0.5, 0.5, n), np.full(n, 5.0), rng.uniform(-0.5, 0.5, n)], 1)
+    return dict(status=status, w=w, ctype=ctype, x1=x1.astype(np.float32), xL=xL.astype(np.float32))

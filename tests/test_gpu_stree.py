@@ -84,24 +84,26 @@ def test_stree_build_duplicates_hit_the_depth_cap():
 
 
 def test_record_samples_bit_exact():
-    """mpg_guide_record_samples == the oracle's recorder on the same walk outputs."""
+    """mpg_guide_record_samples == the oracle's recorder on the same seeded synthetic walk
+    outputs (workloads.synthetic_walk_outputs)."""
     import torch
     from oracle import oracle as O
     from paper_2311_12818_b200 import mpg
+    from tests.test_gpu_parity import _load_outputs
     w = W.config4(n_side=48, guide="stree")
     ds = mpg.DeviceScene(w)
     b = mpg.Batch(w.xD, w.nD, w.spp, w.seed.k)
-    mpg.run_step(ds, b, ds.opts(), accumulate=True)
-    torch.cuda.synchronize()
+    o = W.synthetic_walk_outputs(w.xD, w.spp, seed=3)
+    _load_outputs(b, o)
+    mpg.mpg_guide_record_samples(ds.guide, b.query, b.seeds, b.out, b.n)
     buf = torch.empty(b.n * 48, dtype=torch.uint8, device="cuda")
     assert mpg.mpg_guide_get_samples(ds.guide, buf) == b.n
     torch.cuda.synchronize()
     got = np.frombuffer(buf.cpu().numpy().tobytes(), O.GSAMPLE)
-    g = b.results()
-    ref = O.record_samples(w.xD, w.spp, g["status"].astype(np.int32), g["w"], g["pos"][:, 0].astype(np.float32),
-                           g["ctype"] & 15, g["ctype"] >> 4, g["xL"][:, :3])
+    ref = O.record_samples(w.xD, w.spp, o["status"].astype(np.int32), o["w"], o["x1"], o["ctype"] & 15,
+                           o["ctype"] >> 4, o["xL"])
     assert np.array_equal(np.frombuffer(got.tobytes(), np.uint8), np.frombuffer(ref.tobytes(), np.uint8))
-    assert (got["w"] > 0).sum() > 10
+    assert (got["w"] > 0).sum() > 500
     ds.close()
 
 
