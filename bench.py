@@ -212,7 +212,7 @@ def run_ours(args):
     iters = 8 if progressive else 1
     # independent partitions (weak scaling): rank r owns walk ids [r*n*iters, (r+1)*n*iters)
     w.opts.walk_id_base = D.walk_id_base(rank, w.n_walks * iters)
-    ds = mpg.DeviceScene(w, stree_capacity=max(w.n_walks * world, args.photons))
+    ds = mpg.DeviceScene(w, stree_capacity=max(w.n_walks, args.photons) * world)
     b = mpg.Batch(w.xD, w.nD, w.spp, w.seed.k)
     opts = ds.opts(flags=w.opts.flags | (1 if args.wavefront else 0) | (2 if args.hostloop else 0) |
                    (4 if args.f64 else 0) | (0 if args.no_sort else 8))
@@ -235,9 +235,14 @@ def run_ours(args):
 
     plane = (w.xD[0].tolist(), w.nD[0].tolist())   # receiver plane (photon landing, R33)
 
+    pbuf = None
+    if stree and args.photons and world > 1:
+        pbuf = torch.empty(args.photons * world * mpg.GUIDE_SAMPLE_BYTES, dtype=torch.uint8, device=dev)
+
     def photon_init():
         if stree and args.photons:      # photon-based p_0: iteration 0 from photons
-            mpg.photon_init(ds, args.photons, plane[0], plane[1], seed=1, base=rank * args.photons)
+            ex = (lambda d: D.exchange_samples(d, pbuf, args.photons)) if pbuf is not None else None
+            mpg.photon_init(ds, args.photons, plane[0], plane[1], seed=1, base=rank * args.photons, exchange=ex)
 
     def step():
         if progressive:

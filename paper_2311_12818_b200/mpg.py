@@ -310,9 +310,12 @@ def mpg_trace_photons(scene, desc: mpg_photon_desc, records, stream=None):
     _check(lib().mpg_trace_photons(scene, C.byref(desc), _ptr(records), _stream_ptr(stream)), "mpg_trace_photons")
 
 
-def photon_init(ds, n_photons: int, plane_point, plane_normal, seed: int = 0, base: int = 0, stream=None):
+def photon_init(ds, n_photons: int, plane_point, plane_normal, seed: int = 0, base: int = 0, stream=None,
+                exchange=None):
     """Photon-based p_0: trace photons on the GPU and fit the STree guide from
-    them (replaces the empty iteration-0 guide).  Returns the number of landed photons."""
+    them (replaces the empty iteration-0 guide).  exchange(ds) (multi-process runs,
+    dist.exchange_samples) gathers every rank's photon records before the fit, so all ranks
+    start from the same guide.  Returns the number of landed photons (this rank's)."""
     import torch
     d = mpg_photon_desc(n_photons=n_photons, seed=seed, photon_id_base=base, max_vertices=6, ray_eps=0.0)
     d.plane_point = (C.c_float * 3)(*[float(v) for v in plane_point])
@@ -323,6 +326,8 @@ def photon_init(ds, n_photons: int, plane_point, plane_normal, seed: int = 0, ba
     landed = int((rec.view(torch.float32).view(-1, 12)[:, 9] > 0).sum())   # w > 0
     assert n_photons <= cap, "photon records exceed the STree guide's max_samples"
     mpg_guide_set_samples(ds.guide, rec, n_photons, stream)
+    if exchange is not None:
+        exchange(ds)
     mpg_guide_rebuild(ds.guide, stream)
     return landed
 
