@@ -224,7 +224,10 @@ typedef struct {
     float kappa_min;      /* vMF concentration clamp (1, R30)                              */
     float kappa_max;      /* (300, R30: measured, fewer fireflies than 3e3 / 1e4)          */
     int32_t max_depth;    /* 32                                                            */
-    int32_t reserved;
+    int32_t keep_all;     /* 0: fit from the last iteration's samples only (the paper's default,
+                             P:426 footnote, records cleared by each rebuild); 1: from all samples
+                             encountered so far (the footnote's alternative, Reibold et al.), records
+                             kept until max_samples */
 } mpg_stree_desc;
 
 /* counts of the current tree: n_nodes, n_leaves, root_ref (>= 0 node, < 0 ~leaf),

@@ -631,7 +631,7 @@ static mpg_status stree_build(StreeState *T, cudaStream_t st) {
     ST_TRY(cudaPeekAtLastError());
     ST_TRY(cudaStreamSynchronize(st));
     prof.mark("tables", st);
-    T->n_rec = 0; // "last iteration only" (P:426 footnote)
+    if (!T->d.keep_all) T->n_rec = 0; // "last iteration only" (P:426 footnote) unless keep_all
     return MPG_OK;
 }
 

@@ -73,7 +73,7 @@ class mpg_walk_buf(C.Structure):
 
 class mpg_stree_desc(C.Structure):
     _fields_ = [("max_samples", C.c_int64), ("eps", C.c_float), ("c_thr", C.c_float), ("kappa_min", C.c_float),
-                ("kappa_max", C.c_float), ("max_depth", C.c_int32), ("reserved", C.c_int32)]
+                ("kappa_max", C.c_float), ("max_depth", C.c_int32), ("keep_all", C.c_int32)]
 
 
 class mpg_stree_info(C.Structure):

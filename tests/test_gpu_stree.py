@@ -198,3 +198,30 @@ def test_stree_progressive_loop_independent():
         assert agree >= 0.98
     assert abs(info["n_valid"] - log[-1][2]) <= max(2, 0.01 * log[-1][2])
     assert log[-1][1] > log[0][1]
+
+
+def test_keep_all_samples_fits_from_every_iteration():
+    """keep_all (P:426 footnote's alternative): after two record+rebuild rounds the tree is
+    the oracle's tree of the concatenated records of both rounds; without it, of the last."""
+    import torch
+    from oracle import oracle as O
+    from paper_2311_12818_b200 import mpg
+    r1 = W.synthetic_guide_samples(20000, seed=31)
+    r2 = W.synthetic_guide_samples(20000, seed=32)
+    for keep in (0, 1):
+        d = mpg.mpg_stree_desc(max_samples=40000, eps=0.1, c_thr=1.0, kappa_min=1.0, kappa_max=300.0, max_depth=32,
+                               keep_all=keep)
+        g = mpg.mpg_guide_create_stree(d)
+        t1 = torch.from_numpy(np.frombuffer(r1.tobytes(), np.uint8).copy()).cuda()
+        mpg.mpg_guide_set_samples(g, t1, len(r1))
+        mpg.mpg_guide_rebuild(g)
+        # a second round appends its records after the kept ones (record_samples appends too)
+        n0 = mpg.mpg_guide_get_samples(g)
+        allr = np.concatenate([r1, r2]) if keep else r2
+        t = torch.from_numpy(np.frombuffer(allr.tobytes(), np.uint8).copy()).cuda()
+        mpg.mpg_guide_set_samples(g, t, len(allr))
+        mpg.mpg_guide_rebuild(g)
+        G = mpg.mpg_guide_download_stree(g)
+        mpg.mpg_guide_destroy(g)
+        assert n0 == (len(r1) if keep else 0)
+        _assert_same_tree(G, O.stree_build(_oracle_records(allr)))
