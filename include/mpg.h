@@ -243,6 +243,12 @@ mpg_status mpg_guide_create_stree(const mpg_stree_desc *desc, mpg_guide **out);
  * not samples get w = 0).  Asynchronous.  MPG_ERR_INVALID_ARG past max_samples. */
 mpg_status mpg_guide_record_samples(mpg_guide *guide, const mpg_query *query, const mpg_seed_buf *seeds,
                                     const mpg_walk_buf *walks, int64_t n, void *stream);
+/* Glossy separator (Eq. 14; R35): subsequent mpg_guide_record_samples
+ * weight every sample by the separator BSDF, a GGX(alpha) microfacet lobe
+ * rho = D(h) / (4 cos_v cos_D) with h = normalize(w_v + w_D*): wv = device float4 [n_recv] unit
+ * directions from x_D towards the viewer, nD = the receivers' normals (float4 [n_recv]); the
+ * caller keeps both alive.  wv = nD = NULL: diffuse separator (weights unchanged). */
+mpg_status mpg_guide_set_separator(mpg_guide *guide, const float *wv, const float *nD, float alpha);
 /* Replace the recorded samples by n device records (multi-process exchange, tests). */
 mpg_status mpg_guide_set_samples(mpg_guide *guide, const mpg_guide_sample *records, int64_t n, void *stream);
 /* Copy the recorded samples to device `records` (capacity >= *n on entry; *n = count on return). */

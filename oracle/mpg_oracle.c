@@ -1687,8 +1687,26 @@ void orc_stree_get(const void *h, orc_snode *nodes, int64_t *leaf_begin, int64_t
 
 /* sample records from walk outputs (Eq. 9 samples of one iteration): x_D of the walk's receiver,
  * its x_L, w_D* = normalize(x_1* - x_D) (fp32), type = 2^n - 2 + tau, w; non-samples get w = 0 */
+/* glossy separator (Eq. 14): w' = rho(w_v, w_D*) w with a microfacet lobe
+ * rho = D(h) / (4 cos_v cos_D), D = GGX(alpha) = alpha^2 / (pi ((n.h)^2 (alpha^2 - 1) + 1)^2),
+ * h = normalize(w_v + w_D*), w_v the receiver's unit direction towards the viewer [R35] */
+static float separator_rho(const float n[3], const float wv[3], const float om[3], float alpha) {
+    float cv = n[0] * wv[0] + n[1] * wv[1] + n[2] * wv[2];
+    float cl = n[0] * om[0] + n[1] * om[1] + n[2] * om[2];
+    if (!(cv > 0.0f) || !(cl > 0.0f)) return 0.0f;
+    float hx = wv[0] + om[0], hy = wv[1] + om[1], hz = wv[2] + om[2];
+    float hl = sqrtf(hx * hx + hy * hy + hz * hz);
+    hx = hx / hl; hy = hy / hl; hz = hz / hl;
+    float nh = n[0] * hx + n[1] * hy + n[2] * hz;
+    float a2 = alpha * alpha;
+    float t = nh * nh * (a2 - 1.0f) + 1.0f;
+    float D = a2 / (3.14159265358979323846f * (t * t));
+    return D / (4.0f * cv * cl);
+}
+
 void orc_record_samples(const float *xD, int32_t spp, int64_t n, const int32_t *status, const float *w,
-                        const float *x1, const int32_t *k, const uint32_t *tau, const float *xL, orc_gsample *out) {
+                        const float *x1, const int32_t *k, const uint32_t *tau, const float *xL, const float *wv,
+                        const float *nD, float alpha, orc_gsample *out) {
     for (int64_t i = 0; i < n; i++) {
         orc_gsample *r = out + i;
         memset(r, 0, sizeof(*r));
@@ -1701,6 +1719,10 @@ void orc_record_samples(const float *xD, int32_t spp, int64_t n, const int32_t *
         r->omega[0] = dx / l; r->omega[1] = dy / l; r->omega[2] = dz / l;
         r->type = (1 << k[i]) - 2 + (int32_t)tau[i];
         r->w = w[i];
+        if (wv) { /* glossy separator: product weighting (Eq. 14) */
+            r->w = w[i] * separator_rho(nD + 3 * (i / spp), wv + 3 * (i / spp), r->omega, alpha);
+            if (!(r->w > 0.0f)) { r->w = 0.0f; r->type = -1; r->omega[0] = r->omega[1] = r->omega[2] = 0.0f; }
+        }
     }
 }
 

@@ -136,7 +136,7 @@ def lib():
         _lib.orc_stree_free.argtypes = [P]
         _lib.orc_stree_info.argtypes = [P, P]
         _lib.orc_stree_get.argtypes = [P] + [P] * 10
-        _lib.orc_record_samples.argtypes = [P, C.c_int32, C.c_int64, P, P, P, P, P, P, P]
+        _lib.orc_record_samples.argtypes = [P, C.c_int32, C.c_int64, P, P, P, P, P, P, P, P, C.c_float, P]
         _lib.orc_vmf_sample.argtypes = [P, C.c_float, C.c_float, C.c_float, P]
         _lib.orc_trace_photons.argtypes = [P, C.POINTER(PhotonDesc), C.c_int64, C.c_int64, P, P, P, P, P]
         _lib.orc_scatter.restype = C.c_int
@@ -218,14 +218,18 @@ def stree_build(records: np.ndarray, eps=0.1, c_thr=1.0, max_depth=32, kappa_min
     return out
 
 
-def record_samples(xD, spp, status, w, x1, k, tau, xL) -> np.ndarray:
-    """Sample records (GSAMPLE) of one iteration's walks (Eq. 9 samples)."""
+def record_samples(xD, spp, status, w, x1, k, tau, xL, wv=None, nD=None, alpha=0.0) -> np.ndarray:
+    """Sample records (GSAMPLE) of one iteration's walks (Eq. 9 samples); with wv / nD (per
+    receiver) the weights carry a GGX(alpha) glossy separator (Eq. 14, R35)."""
     n = len(status)
     out = np.zeros(n, GSAMPLE)
     arrs = [np.ascontiguousarray(a, dt) for a, dt in ((xD, np.float32), (status, np.int32), (w, np.float32),
                                                       (x1, np.float32), (k, np.int32), (tau, np.uint32),
                                                       (xL, np.float32))]
-    lib().orc_record_samples(_ptr(arrs[0]), int(spp), n, *(_ptr(a) for a in arrs[1:]), _ptr(out))
+    g = [None, None] if wv is None else [np.ascontiguousarray(wv, np.float32), np.ascontiguousarray(nD, np.float32)]
+    lib().orc_record_samples(_ptr(arrs[0]), int(spp), n, *(_ptr(a) for a in arrs[1:]),
+                             _ptr(g[0]) if g[0] is not None else None, _ptr(g[1]) if g[1] is not None else None,
+                             float(alpha), _ptr(out))
     return out
 
 

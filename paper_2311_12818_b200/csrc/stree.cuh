@@ -79,6 +79,8 @@ template <class T> struct PinBuf { // pinned host staging (reused; rewritten onl
 
 struct StreeState {
     mpg_stree_desc d;
+    const float4 *sep_wv = nullptr, *sep_n = nullptr; // glossy separator (Eq. 14): per receiver
+    float sep_alpha = 0.f;
     DBuf<mpg_guide_sample> rec;
     int64_t n_rec = 0;
     // current tree
@@ -298,9 +300,25 @@ __global__ void k_group_tables(const mpg_guide_sample *rec, const int *lobe_samp
     }
 }
 
+// glossy separator lobe (Eq. 14, R35): GGX(alpha) D(h) / (4 cos_v cos_D), fp32 as the oracle
+__device__ __forceinline__ float separator_rho(float4 n, float4 wv, float ox, float oy, float oz, float alpha) {
+    float cv = FA(FA(FM(n.x, wv.x), FM(n.y, wv.y)), FM(n.z, wv.z));
+    float cl = FA(FA(FM(n.x, ox), FM(n.y, oy)), FM(n.z, oz));
+    if (!(cv > 0.0f) || !(cl > 0.0f)) return 0.0f;
+    float hx = FA(wv.x, ox), hy = FA(wv.y, oy), hz = FA(wv.z, oz);
+    float hl = __fsqrt_rn(FA(FA(FM(hx, hx), FM(hy, hy)), FM(hz, hz)));
+    hx = FD(hx, hl); hy = FD(hy, hl); hz = FD(hz, hl);
+    float nh = FA(FA(FM(n.x, hx), FM(n.y, hy)), FM(n.z, hz));
+    float a2 = FM(alpha, alpha);
+    float t = FA(FM(FM(nh, nh), FS(a2, 1.0f)), 1.0f);
+    float D = FD(a2, FM(3.14159265358979323846f, FM(t, t)));
+    return FD(D, FM(FM(4.0f, cv), cl));
+}
+
 // sample records of one walk call (Eq. 9 samples; mirrors orc_record_samples)
 __global__ void k_record(mpg_guide_sample *out, const float4 *xD, int spp, const float4 *xL, const float4 *chain0,
-                         const uint8_t *status, const float *w, const uint16_t *ctype, int64_t n) {
+                         const uint8_t *status, const float *w, const uint16_t *ctype, int64_t n, const float4 *sep_wv,
+                         const float4 *sep_n, float sep_alpha) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         mpg_guide_sample r;
         float4 d = xD[i / spp], l = xL[i];
@@ -319,6 +337,11 @@ __global__ void k_record(mpg_guide_sample *out, const float4 *xD, int spp, const
             r.omega[0] = FD(dx, ln); r.omega[1] = FD(dy, ln); r.omega[2] = FD(dz, ln);
             r.type = (1 << kk) - 2 + (int)(ct >> 4);
             r.w = w[i];
+            if (sep_wv) { // glossy separator: product weighting (Eq. 14)
+                r.w = FM(w[i], separator_rho(sep_n[i / spp], sep_wv[i / spp], r.omega[0], r.omega[1], r.omega[2],
+                                             sep_alpha));
+                if (!(r.w > 0.0f)) { r.w = 0.0f; r.type = -1; r.omega[0] = r.omega[1] = r.omega[2] = 0.0f; }
+            }
         }
         out[i] = r;
     }
@@ -685,9 +708,19 @@ extern "C" mpg_status mpg_guide_record_samples(mpg_guide *g, const mpg_query *q,
     COUNT_LAUNCH(1);
     k_record<<<(int)std::min<int64_t>((n + 255) / 256, 148 * 8), 256, 0, as_stream(stream)>>>(
         T->rec.p + T->n_rec, (const float4 *)q->xD, q->spp, (const float4 *)sb->xL, (const float4 *)wb->chain,
-        wb->status, wb->w, wb->ctype, n);
+        wb->status, wb->w, wb->ctype, n, T->sep_wv, T->sep_n, T->sep_alpha);
     CUDA_TRY(cudaPeekAtLastError());
     T->n_rec += n;
+    return MPG_OK;
+}
+
+extern "C" mpg_status mpg_guide_set_separator(mpg_guide *g, const float *wv, const float *nD, float alpha) {
+    ARG_CHECK(g && g->stree, "needs an STree guide");
+    ARG_CHECK((wv == nullptr) == (nD == nullptr), "wv and nD together");
+    ARG_CHECK(!wv || (alpha > 0.f && alpha <= 1.f), "GGX alpha in (0, 1]");
+    g->stree->sep_wv = (const float4 *)wv;
+    g->stree->sep_n = (const float4 *)nD;
+    g->stree->sep_alpha = alpha;
     return MPG_OK;
 }
 

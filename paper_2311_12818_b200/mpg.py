@@ -107,7 +107,7 @@ EXPORTS = ["mpg_scene_create", "mpg_scene_destroy", "mpg_scene_get_info", "mpg_t
            "mpg_guide_download", "mpg_guide_download_dir_tables", "mpg_sample_seeds", "mpg_walk_workspace_size", "mpg_manifold_walk", "mpg_estimate",
            "mpg_debug_trace", "mpg_last_error", "mpg_version", "mpg_kernel_launches", "mpg_guide_create_stree",
            "mpg_guide_record_samples", "mpg_guide_set_samples", "mpg_guide_get_samples", "mpg_guide_stree_info",
-           "mpg_guide_download_stree", "mpg_trace_photons", "mpg_splat"]
+           "mpg_guide_download_stree", "mpg_trace_photons", "mpg_splat", "mpg_guide_set_separator"]
 
 _lib = None
 
@@ -155,6 +155,7 @@ def lib():
             "mpg_guide_stree_info": (st, [P, C.POINTER(mpg_stree_info)]),
             "mpg_trace_photons": (st, [P, C.POINTER(mpg_photon_desc), P, P]),
             "mpg_splat": (st, [P, C.c_int64, C.c_int32, P, P, P]),
+            "mpg_guide_set_separator": (st, [P, P, P, C.c_float]),
             "mpg_guide_download_stree": (st, [P] + [P] * 10 + [P]),
         }
         for name, (res, args) in sig.items():
@@ -259,6 +260,11 @@ def mpg_guide_create_stree(desc: mpg_stree_desc):
 def mpg_guide_record_samples(h, query, seeds, walks, n, stream=None):
     _check(lib().mpg_guide_record_samples(h, C.byref(query), C.byref(seeds), C.byref(walks), n, _stream_ptr(stream)),
            "mpg_guide_record_samples")
+
+
+def mpg_guide_set_separator(h, wv=None, nD=None, alpha=0.0):
+    """Glossy separator (Eq. 14): wv, nD device float32 [n_recv, 4]; None = diffuse."""
+    _check(lib().mpg_guide_set_separator(h, _ptr(wv), _ptr(nD), float(alpha)), "mpg_guide_set_separator")
 
 
 def mpg_guide_set_samples(h, records, n, stream=None):

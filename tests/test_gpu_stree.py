@@ -225,3 +225,34 @@ def test_keep_all_samples_fits_from_every_iteration():
         mpg.mpg_guide_destroy(g)
         assert n0 == (len(r1) if keep else 0)
         _assert_same_tree(G, O.stree_build(_oracle_records(allr)))
+
+
+def test_record_samples_glossy_separator_bit_exact():
+    """Eq. 14 product weighting (GGX separator, R35): GPU records == oracle records."""
+    import torch
+    from oracle import oracle as O
+    from paper_2311_12818_b200 import mpg
+    from tests.test_gpu_parity import _load_outputs
+    w = W.config4(n_side=48, guide="stree")
+    ds = mpg.DeviceScene(w)
+    b = mpg.Batch(w.xD, w.nD, w.spp, w.seed.k)
+    o = W.synthetic_walk_outputs(w.xD, w.spp, seed=4)
+    _load_outputs(b, o)
+    eye = np.array([2.0, 6.0, -4.0])
+    wv = eye[None, :] - w.xD.astype(np.float64)
+    wv = (wv / np.linalg.norm(wv, axis=1, keepdims=True)).astype(np.float32)
+    wv4 = torch.zeros(len(wv), 4); wv4[:, :3] = torch.from_numpy(wv)
+    wv4 = wv4.cuda()
+    mpg.mpg_guide_set_separator(ds.guide, wv4, b.nD, 0.2)
+    mpg.mpg_guide_record_samples(ds.guide, b.query, b.seeds, b.out, b.n)
+    buf = torch.empty(b.n * 48, dtype=torch.uint8, device="cuda")
+    mpg.mpg_guide_get_samples(ds.guide, buf)
+    torch.cuda.synchronize()
+    got = np.frombuffer(buf.cpu().numpy().tobytes(), O.GSAMPLE)
+    ref = O.record_samples(w.xD, w.spp, o["status"].astype(np.int32), o["w"], o["x1"], o["ctype"] & 15,
+                           o["ctype"] >> 4, o["xL"], wv=wv, nD=w.nD, alpha=0.2)
+    assert np.array_equal(np.frombuffer(got.tobytes(), np.uint8), np.frombuffer(ref.tobytes(), np.uint8))
+    plain = O.record_samples(w.xD, w.spp, o["status"].astype(np.int32), o["w"], o["x1"], o["ctype"] & 15,
+                             o["ctype"] >> 4, o["xL"])
+    assert (got["w"] > 0).sum() > 100 and not np.array_equal(got["w"], plain["w"])
+    ds.close()

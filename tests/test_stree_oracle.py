@@ -251,3 +251,44 @@ def test_seed_mode4_draws_from_the_leaf_mixture():
             assert (s["tau"] + (1 << s["n"]) - 2) == r["type"][G["lobe_sample"][b]]
     assert 0.3 * n < learned < 0.7 * n
     assert near >= learned - 2
+
+
+# ---------------------------------------------------------------------------
+# glossy separator product weighting (Eq. 14; R35)
+# ---------------------------------------------------------------------------
+def _rho(wv, om, alpha):
+    """rho via the oracle's recorder: one receiver at the origin (normal +y), walks towards om."""
+    n = om.shape[0]
+    xD = np.zeros((1, 3), np.float32)
+    rec = O.record_samples(xD, n, np.zeros(n, np.int32), np.ones(n, np.float32), om.astype(np.float32),
+                           np.ones(n, np.int32), np.zeros(n, np.uint32), np.zeros((n, 3), np.float32),
+                           wv=np.asarray([wv], np.float32), nD=np.asarray([[0, 1, 0]], np.float32), alpha=alpha)
+    return rec["w"].astype(np.float64)
+
+
+@pytest.mark.parametrize("alpha", [0.05, 0.1])
+def test_ggx_separator_lobe_normalised_at_normal_incidence(alpha):
+    """int rho(n, l) cos_l dl = int D(h) (n.h) dh over the h whose reflection stays above the
+    surface (theta_h <= 45 deg): the GGX mass there, 1 / (1 + alpha^2) in closed form."""
+    m, mp = 8000, 8                              # midpoint rule in (cos^2 theta_l, phi); the lobe is
+    u = (np.arange(m) + 0.5) / m                 # symmetric in phi at normal incidence
+    ct = np.sqrt(u)                              # cos theta, area element d(omega) = d(ct^2)/2 dphi
+    ph = 2 * np.pi * (np.arange(mp) + 0.5) / mp
+    CT, PH = np.meshgrid(ct, ph, indexing="ij")
+    ST = np.sqrt(1 - CT ** 2)
+    om = np.stack([ST * np.cos(PH), CT, ST * np.sin(PH)], -1).reshape(-1, 3)
+    r = _rho([0.0, 1.0, 0.0], om, alpha)
+    cosl = om[:, 1]
+    integral = (r * cosl / cosl).sum() * (0.5 / m) * (2 * np.pi / mp)  # rho cos_l d(omega) = rho du/2 dphi
+    assert integral == pytest.approx(1.0 / (1.0 + alpha * alpha), abs=2e-3)
+
+
+def test_ggx_separator_reciprocal_and_one_sided():
+    rng = np.random.default_rng(2)
+    v = rng.normal(size=(200, 3)); v[:, 1] = np.abs(v[:, 1]); v /= np.linalg.norm(v, axis=1, keepdims=True)
+    l = rng.normal(size=(200, 3)); l[:, 1] = np.abs(l[:, 1]); l /= np.linalg.norm(l, axis=1, keepdims=True)
+    a = np.array([_rho(v[i], l[i:i + 1], 0.3)[0] for i in range(50)])
+    b = np.array([_rho(l[i], v[i:i + 1], 0.3)[0] for i in range(50)])
+    assert np.allclose(a, b, rtol=2e-6)                                  # rho(v, l) = rho(l, v)
+    below = l[:5] * np.array([1, -1, 1])
+    assert (_rho(v[0], below, 0.3) == 0).all()                          # no weight below the separator
