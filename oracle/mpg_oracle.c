@@ -14,7 +14,11 @@
  *   reciprocal probability      PAPER.md:582-591 (Eq. 15, trials reuse n)
  *   sample weight w = T <1/P>   PAPER.md:427-432 (Eq. 9), estimator Eq. 3 (:267-277)
  *   guide tables                PAPER.md:434-466 (Eqs. 10-11) as the BASELINE.json histogram
- * Every choice the paper leaves open is a numbered reading (R1..R27) in
+ *   STree + vMF guide           PAPER.md:424-530 (Eqs. 9-12, STree P:518-523)      [R28-R31]
+ *   repeated reciprocal est.    PAPER.md:906-915 (R x M)                            [R32]
+ *   photon-based p_0            PAPER.md:398, :883                                   [R33]
+ *   glossy separator weighting  PAPER.md:550-556 (Eq. 14)                            [R35]
+ * Every choice the paper leaves open is a numbered reading (R1..R35) in
  * DESIGN.md §3; the code cites them as [Rn].
  *
  * It shares no code, header, table or constant generator with the CUDA
