@@ -64,3 +64,29 @@ def test_struct_layouts():
     assert C.sizeof(mpg.mpg_walk_stats) == 19 * 8
     assert C.sizeof(mpg.mpg_query) == 32
     assert C.sizeof(mpg.mpg_sampler_desc) == 16
+
+
+def test_stree_photon_splat_arguments_rejected_synchronously(L):
+    """The 8(f) entry points check their arguments before touching the device."""
+    h = C.c_void_p()
+    d = mpg.mpg_stree_desc(max_samples=10, eps=0.6, c_thr=1.0, kappa_min=1.0, kappa_max=300.0, max_depth=32)
+    assert L.mpg_guide_create_stree(C.byref(d), C.byref(h)) == 1 and b"eps" in L.mpg_last_error()
+    d.eps, d.kappa_min, d.kappa_max = 0.1, 5.0, 1.0
+    assert L.mpg_guide_create_stree(C.byref(d), C.byref(h)) == 1 and b"kappa" in L.mpg_last_error()
+    d.kappa_min, d.kappa_max, d.max_depth = 1.0, 300.0, 99
+    assert L.mpg_guide_create_stree(C.byref(d), C.byref(h)) == 1
+    assert L.mpg_guide_create_stree(None, C.byref(h)) == 1
+    assert L.mpg_guide_set_separator(None, None, None, C.c_float(0.1)) == 1
+    assert L.mpg_guide_set_samples(None, None, 0, None) == 1
+    info = mpg.mpg_stree_info()
+    assert L.mpg_guide_stree_info(None, C.byref(info)) == 1
+    p = mpg.mpg_photon_desc(n_photons=10, max_vertices=7)
+    assert L.mpg_trace_photons(None, C.byref(p), None, None) == 1
+    assert L.mpg_splat(None, 1, 1, None, None, None) == 1
+
+
+def test_new_struct_layouts():
+    assert C.sizeof(mpg.mpg_stree_desc) == 32
+    assert C.sizeof(mpg.mpg_stree_info) == 48
+    assert C.sizeof(mpg.mpg_photon_desc) == 56
+    assert mpg.GUIDE_SAMPLE_BYTES == 48
