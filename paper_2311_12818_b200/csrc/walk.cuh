@@ -30,7 +30,7 @@
 #define MPG_WALK_MINB_LONG 6   // fixed long chains (configs[3])
 #endif
 #ifndef MPG_WALK_MINB_MIXED
-#define MPG_WALK_MINB_MIXED 2  // per-sample chain length (configs[4])
+#define MPG_WALK_MINB_MIXED 3  // per-sample chain length (configs[4]; 2/3/4: 261/255/271 ms)
 #endif
 #include "device_common.cuh"
 #include "seed.cuh"
