@@ -296,8 +296,10 @@ class _Perlin2:
         return val, dx, dz
 
 
-def glass_slabs(n: int = 256, seed: int = 0):
+def glass_slabs(n: int = 256, seed: int = 0, flat: bool = False):
     """Config 3 geometry: three curved bumpy glass slabs (frozen here).
+    `flat=True` drops the curvature and noise terms (twin 3a: planar interfaces
+    at y_j and y_j + 0.1, where the k=6 chain has a closed form).
 
     slab j in {0,1,2}, y_j = 0, 0.35, 0.7, over (x,z) in [-1,1]^2:
       bottom_j = y_j + 0.1(x^2+z^2) + 0.02 N_j(4x,4z)          (outward normal down)
@@ -313,9 +315,10 @@ def glass_slabs(n: int = 256, seed: int = 0):
         for side in (0, 1):
             noise = _Perlin2(seed + 2 * j + side)
             nv, ndx, ndz = noise(4 * X, 4 * Z)
-            y = yj + 0.1 * (X * X + Z * Z) + 0.1 * side + 0.02 * nv
-            fx = 0.2 * X + 0.02 * 4 * ndx
-            fz = 0.2 * Z + 0.02 * 4 * ndz
+            c = 0.0 if flat else 1.0
+            y = yj + c * 0.1 * (X * X + Z * Z) + 0.1 * side + c * 0.02 * nv
+            fx = c * (0.2 * X + 0.02 * 4 * ndx)
+            fz = c * (0.2 * Z + 0.02 * 4 * ndz)
             ny = np.stack([-fx, np.ones_like(y), -fz], -1)
             out.append(grid_mesh(xs, zs, y, ny, up=(side == 1)))
     return out
@@ -388,12 +391,13 @@ def config2(n_side: int = 2048, spp: int = 4, flat: bool = False, grid_n: int = 
                     recv_shape=(n_side, n_side))
 
 
-def config3(n_side: int = 1024, spp: int = 1, grid_n: int = 256) -> Workload:
+def config3(n_side: int = 1024, spp: int = 1, grid_n: int = 256, flat: bool = False) -> Workload:
     """configs[3]: k=6 TTTTTT through three stacked bumpy glass slabs, point light
     (0,2.5,0), receivers on y=-1 over [-1.5,1.5]^2, guide 8x8 cells x 64x64 bins on
-    the first interface, Dirichlet(0.3) energies, max 40 Newton iterations."""
+    the first interface, Dirichlet(0.3) energies, max 40 Newton iterations.
+    `flat=True` is twin 3a (planar slabs) for the closed-form k=6 pin."""
     surfs = []
-    for (P, N, F) in glass_slabs(grid_n, 0):
+    for (P, N, F) in glass_slabs(grid_n, 0, flat):
         surfs.append(Surface(SURF_MESH, MAT_DIELECTRIC, eta_in=1.5, eta_out=1.0, positions=P, normals=N, indices=F))
     light = Light(LIGHT_POINT, 1.0, position=(0.0, 2.5, 0.0))
     xD, nD = receiver_grid(-1.5, 1.5, n_side, -1.0)
@@ -402,7 +406,7 @@ def config3(n_side: int = 1024, spp: int = 1, grid_n: int = 256) -> Workload:
                     uv_plane_y=0.0)
     rng = np.random.default_rng(0)
     E = rng.dirichlet(np.full(64 * 64, 0.3), size=64).astype(np.float32)
-    return Workload("cfg3_glass_slabs_k6", surfs, [light], xD, nD, spp, seed,
+    return Workload("cfg3_glass_slabs_k6" + ("_flat" if flat else ""), surfs, [light], xD, nD, spp, seed,
                     WalkOpts(max_iters=40, flags=FLAG_NEWTON_F64), energies=np.ascontiguousarray(E),
                     recv_shape=(n_side, n_side))
 

@@ -182,3 +182,34 @@ def snell_plane(xD, xL, eta1, eta2, y_surf=0.0):
     drho = h1 / np.cos(t1) ** 2 + h2 / np.cos(t2) ** 2 * (eta1 * np.cos(t1)) / (eta2 * np.cos(t2))
     G = np.cos(t1) * np.sin(t1) / (rho * drho)
     return x1, G
+
+
+def snell_layers(xD, xL, ys, etas):
+    """Refraction points of the straight-up chain from x_D through horizontal
+    interfaces y = ys[0] < ys[1] < ... to x_L; etas[i] is the index of the
+    medium below ys[i] (etas[-1] the medium above the last interface).
+    Snell's invariant p = eta sin(t) is the same in every layer, so the lateral
+    offset is rho = sum_i h_i p / sqrt(eta_i^2 - p^2) (layer heights h_i);
+    p is found by bisection (rho is increasing in p).  Returns [len(ys), 3]."""
+    xD, xL = np.asarray(xD, np.float64), np.asarray(xL, np.float64)
+    yy = np.concatenate([[xD[1]], np.asarray(ys, np.float64), [xL[1]]])
+    h = np.diff(yy)
+    eta = np.asarray(etas, np.float64)
+    assert np.all(h > 0) and len(eta) == len(h)
+    dvec = np.array([xL[0] - xD[0], 0.0, xL[2] - xD[2]])
+    rho = np.linalg.norm(dvec)
+    pmax = eta.min()
+
+    def offsets(p):
+        return h * p / np.sqrt(eta * eta - p * p)
+
+    a, b = 0.0, pmax * (1 - 1e-15)
+    for _ in range(200):
+        m = 0.5 * (a + b)
+        if offsets(m).sum() > rho:
+            b = m
+        else:
+            a = m
+    off = np.cumsum(offsets(0.5 * (a + b)))[:-1]
+    u = dvec / rho if rho > 0 else np.array([1.0, 0.0, 0.0])
+    return np.array([xD + u * o + np.array([0.0, y - xD[1], 0.0]) for o, y in zip(off, ys)])

@@ -300,6 +300,26 @@ def test_twin2a_snell_point_and_G():
         assert r["G"][q] == pytest.approx(G, rel=1e-9)
 
 
+def test_twin3a_k6_chains_are_layered_snell_points():
+    """k = 6 TTTTTT through three planar glass slabs (twin of configs[3]): every
+    converged chain is the unique straight-up refraction path fixed by Snell's
+    invariant eta sin t (closed form tests/closed_forms.snell_layers).  Pins the
+    6-block tridiagonal elimination and back-substitution and
+    the sequential reprojection through six interfaces (reading R5)."""
+    w = W.config3(24, 1, grid_n=16, flat=True)
+    w.opts.tol, w.opts.max_iters = 1e-11, 60
+    s = O.OracleScene(w)
+    ys = [float(srf.positions[0, 1]) for srf in w.surfaces]   # fp32 planes, bottom to top
+    assert ys == sorted(ys) and len(ys) == 6
+    etas = [1.0, 1.5, 1.0, 1.5, 1.0, 1.5, 1.0]
+    r, idx = _converged_chains(s, w, w.n_walks)
+    assert len(idx) > 50
+    for q in idx:
+        xD = w.xD[r["walk"][q] // w.spp]
+        ref = CF.snell_layers(xD, r["xL"][q], ys, etas)
+        assert np.abs(np.asarray(r["pos"][q][:6]) - ref).max() < 1e-9 * s.extent
+
+
 # ---------------------------------------------------------------------------
 # GGT (Eq. 2, PAPER.md:237): unfold, Coddington, FD re-convergence, reciprocity
 # ---------------------------------------------------------------------------
