@@ -184,13 +184,18 @@ def snell_plane(xD, xL, eta1, eta2, y_surf=0.0):
     return x1, G
 
 
-def snell_layers(xD, xL, ys, etas):
+def snell_layers(xD, xL, ys, etas, with_G=False):
     """Refraction points of the straight-up chain from x_D through horizontal
     interfaces y = ys[0] < ys[1] < ... to x_L; etas[i] is the index of the
     medium below ys[i] (etas[-1] the medium above the last interface).
     Snell's invariant p = eta sin(t) is the same in every layer, so the lateral
     offset is rho = sum_i h_i p / sqrt(eta_i^2 - p^2) (layer heights h_i);
-    p is found by bisection (rho is increasing in p).  Returns [len(ys), 3]."""
+    p is found by bisection (rho is increasing in p).  Returns [len(ys), 3], or
+    with `with_G` also (G, kappa): G = d omega_L / dA_D for a point light at x_L
+    in a medium of index 1 over a horizontal receiver,
+    G = p / (cos t_L rho drho/dp), drho/dp = sum_i h_i eta_i^2 / (eta_i^2 - p^2)^(3/2),
+    and kappa = prod over interfaces of (1 - F), F the unpolarised Fresnel
+    reflectance (Hecht, Optics, §4.6.2) at that interface's angles."""
     xD, xL = np.asarray(xD, np.float64), np.asarray(xL, np.float64)
     yy = np.concatenate([[xD[1]], np.asarray(ys, np.float64), [xL[1]]])
     h = np.diff(yy)
@@ -210,6 +215,19 @@ def snell_layers(xD, xL, ys, etas):
             b = m
         else:
             a = m
-    off = np.cumsum(offsets(0.5 * (a + b)))[:-1]
+    p = 0.5 * (a + b)
+    off = np.cumsum(offsets(p))[:-1]
     u = dvec / rho if rho > 0 else np.array([1.0, 0.0, 0.0])
-    return np.array([xD + u * o + np.array([0.0, y - xD[1], 0.0]) for o, y in zip(off, ys)])
+    pts = np.array([xD + u * o + np.array([0.0, y - xD[1], 0.0]) for o, y in zip(off, ys)])
+    if not with_G:
+        return pts
+    assert eta[-1] == 1.0
+    drho = (h * eta * eta / (eta * eta - p * p) ** 1.5).sum()
+    G = p / (np.sqrt(1.0 - p * p) * rho * drho)
+    kappa = 1.0
+    for e1, e2 in zip(eta[:-1], eta[1:]):
+        ci, ct = np.sqrt(1 - (p / e1) ** 2), np.sqrt(1 - (p / e2) ** 2)
+        rs = (e1 * ci - e2 * ct) / (e1 * ci + e2 * ct)
+        rp = (e2 * ci - e1 * ct) / (e2 * ci + e1 * ct)
+        kappa *= 1.0 - 0.5 * (rs * rs + rp * rp)
+    return pts, G, kappa

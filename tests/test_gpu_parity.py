@@ -266,9 +266,11 @@ def test_twin3a_walk_parity_and_closed_form():
     both = np.nonzero((g["status"][ids] == 0) & (o["status"] == 0))[0]
     assert len(both) > 200
     for q in both[::7]:
-        ref = CF.snell_layers(w.xD[o["walk"][q] // w.spp], o["xL"][q], ys, etas)
+        ref, G, kappa = CF.snell_layers(w.xD[o["walk"][q] // w.spp], o["xL"][q], ys, etas, with_G=True)
         gp = np.asarray(g["pos"][ids[q]][:6], np.float64)
         assert np.abs(gp - ref).max() < 1e-4 * ext
+        assert g["G"][ids[q]] == pytest.approx(G, rel=1e-5)
+        assert g["T"][ids[q]] == pytest.approx(kappa * G, rel=1e-5)
 
 
 def test_cfg2_full_size_sampled():

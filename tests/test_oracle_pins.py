@@ -304,8 +304,9 @@ def test_twin3a_k6_chains_are_layered_snell_points():
     """k = 6 TTTTTT through three planar glass slabs (twin of configs[3]): every
     converged chain is the unique straight-up refraction path fixed by Snell's
     invariant eta sin t (closed form tests/closed_forms.snell_layers).  Pins the
-    6-block tridiagonal elimination and back-substitution and
-    the sequential reprojection through six interfaces (reading R5)."""
+    6-block tridiagonal elimination and back-substitution, the
+    sequential reprojection through six interfaces (reading R5), the analytic GGT
+    (Eq. 2) and kappa = product of six Fresnel transmittances."""
     w = W.config3(24, 1, grid_n=16, flat=True)
     w.opts.tol, w.opts.max_iters = 1e-11, 60
     s = O.OracleScene(w)
@@ -316,8 +317,10 @@ def test_twin3a_k6_chains_are_layered_snell_points():
     assert len(idx) > 50
     for q in idx:
         xD = w.xD[r["walk"][q] // w.spp]
-        ref = CF.snell_layers(xD, r["xL"][q], ys, etas)
+        ref, G, kappa = CF.snell_layers(xD, r["xL"][q], ys, etas, with_G=True)
         assert np.abs(np.asarray(r["pos"][q][:6]) - ref).max() < 1e-9 * s.extent
+        assert r["G"][q] == pytest.approx(G, rel=1e-9)                # Eq. 2 GGT, k = 6
+        assert r["T"][q] == pytest.approx(kappa * G, rel=1e-9)        # T = kappa G I, I = 1
 
 
 # ---------------------------------------------------------------------------
