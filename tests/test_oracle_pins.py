@@ -479,6 +479,24 @@ def test_estimator_unbiased_cfg0(cfg0):
         assert abs(m - T) < 3.5 * se, (m, T, se)
 
 
+def test_estimator_unbiased_twin3a_k6():
+    """Eq. 3 with the reciprocal-probability weight (Eq. 15) on
+    k = 6 guided seeds: mean w over seeds = T = kappa G I of the one layered-Snell
+    chain (closed form), whatever the guide's seed density."""
+    w = W.config3(8, 1, grid_n=16, flat=True)
+    ys = [float(srf.positions[0, 1]) for srf in w.surfaces]
+    etas = [1.0, 1.5, 1.0, 1.5, 1.0, 1.5, 1.0]
+    for ri in (8 * 3 + 3, 8 * 4 + 2, 8 * 2 + 5):
+        ws = O.OracleScene(_single_receiver(w, ri, 2000))
+        r = ws.walks(np.arange(2000))
+        assert r["truncated"].sum() == 0
+        pts, G, kappa = CF.snell_layers(w.xD[ri], r["xL"][0], ys, etas, with_G=True)
+        assert np.all(np.abs(pts[:, [0, 2]]) < 0.95)        # chain inside the meshes
+        m, se = r["w"].mean(), r["w"].std() / np.sqrt(len(r["w"]))
+        assert se < 0.2 * kappa * G
+        assert abs(m - kappa * G) < 3.5 * se, (m, kappa * G, se)
+
+
 def test_dense_grid_enumeration_is_complete(cfg0):
     """dense seed grid, dedupe by same_chain, count stable under
     resolution doubling; equals the Alhazen root count."""
