@@ -273,6 +273,29 @@ def test_twin3a_walk_parity_and_closed_form():
         assert g["T"][ids[q]] == pytest.approx(kappa * G, rel=1e-5)
 
 
+def test_twin3a_gpu_estimator_unbiased():
+    """GPU estimator (Eq. 3 with the Eq. 15 weight) on twin 3a, k = 6: the
+    per-receiver mean over 20,000 guided seeds equals the closed-form kappa G I."""
+    from tests import closed_forms as CF
+    w = W.config3(n_side=8, spp=20000, grid_n=16, flat=True)
+    g, st, ext = PY.run_gpu(w)
+    assert st["truncated"] == 0
+    ys = [float(srf.positions[0, 1]) for srf in w.surfaces]
+    etas = [1.0, 1.5, 1.0, 1.5, 1.0, 1.5, 1.0]
+    xL = np.array([0.0, 2.5, 0.0])
+    z, n = [], 0
+    for ri in range(w.n_recv):
+        pts, G, kappa = CF.snell_layers(w.xD[ri], xL, ys, etas, with_G=True)
+        if np.abs(pts[:, [0, 2]]).max() > 0.95:              # chain leaves the meshes
+            continue
+        se = np.sqrt(g["var"][ri] / w.spp)
+        z.append((g["mean"][ri] - kappa * G) / se)
+        n += 1
+    z = np.array(z)
+    print(n, np.abs(z).max(), z.mean())
+    assert n >= 16 and np.abs(z).max() < 4.5 and abs(z.mean()) < 4.0 / np.sqrt(n)
+
+
 def test_cfg2_full_size_sampled():
     """configs[2] at full size (16,777,216 walks, bench launch configuration) vs 2,000 sampled oracle walks."""
     w = W.config2()
