@@ -231,3 +231,12 @@ def snell_layers(xD, xL, ys, etas, with_G=False):
         rp = (e2 * ci - e1 * ct) / (e2 * ci + e1 * ct)
         kappa *= 1.0 - 0.5 * (rs * rs + rp * rp)
     return pts, G, kappa
+
+
+def mirror_sphere_G(c, R, xD, nD, xL, p, light_normal=None):
+    """GGT of a k = 1 reflection off a sphere mirror: the point-light form
+    (coddington_G) times cos t_L at an area light of normal `light_normal`."""
+    G = coddington_G(c, R, xD, nD, xL, p)
+    if light_normal is not None:
+        G *= abs(np.dot(nz(np.asarray(p, np.float64) - np.asarray(xL, np.float64)), light_normal))
+    return G

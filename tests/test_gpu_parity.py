@@ -579,6 +579,35 @@ def test_cfg3_full_size_sampled():
     _check_walk_parity(rep, min_agree=0.99, w=w, s=s, o=o, ext=ext, max_non_boundary=2)
 
 
+def test_cfg4_mirror_sphere_chains_closed_form():
+    """configs[4] on the GPU (262,144 walks, bench flags): every converged k = 1
+    chain on the mirror sphere is at the Alhazen point of its light sample and has
+    the closed-form G = T (Coddington, x cos t_L for the quad lights)."""
+    from tests import closed_forms as CF
+    w = W.config4(n_side=512)
+    g, st, ext = PY.run_gpu(w, flags=w.opts.flags | BENCH_FLAGS)
+    c = np.array([-5.0, 0.0, 2.5])
+    on_sphere = np.abs(np.linalg.norm(g["pos"][:, 0] - c, axis=1) - 1.0) < 1e-4
+    sel = np.nonzero((g["status"] == 0) & ((g["ctype"] & 15) == 1) & on_sphere)[0]
+    assert len(sel) > 500
+    # G's sensitivity to a residual of tol grows as 1/cos at grazing reflection (the
+    # oracle at tol 1e-5 shows 6.6e-4 at cos 0.02), so the 1e-3 bound is on cos > 0.1
+    worst_p = worst_g = 0.0
+    errs = []
+    for q in sel[:: max(1, len(sel) // 400)]:
+        xD, xL, p = w.xD[q // w.spp].astype(np.float64), g["xL"][q][:3].astype(np.float64), g["pos"][q][0]
+        pts = CF.alhazen_points(c, 1.0, xD, xL)
+        worst_p = max(worst_p, min(np.linalg.norm(p - a) for a in pts) / ext)
+        point = np.allclose(xL, [-5.0, 4.0, 2.5])
+        G = CF.mirror_sphere_G(c, 1.0, xD, [0, 1, 0], xL, p, None if point else [0, 1, 0])
+        e = max(abs(g["G"][q] / G - 1), abs(g["T"][q] / G - 1))
+        errs.append(e)
+        if abs(np.dot(p - c, CF.nz(xL - p))) > 0.1:
+            worst_g = max(worst_g, e)
+    print(len(sel), worst_p, worst_g, np.median(errs), np.quantile(errs, 0.99))
+    assert worst_p < 1e-4 and worst_g < 1e-3 and np.median(errs) < 1e-4
+
+
 def test_cfg4_full_size_first_iterations():
     """configs[4] at full size (1,048,576 walks, the bench's flags): the initial iteration
     (empty guide) and a guided iteration (the seeded typed histogram uploaded to both

@@ -497,6 +497,30 @@ def test_estimator_unbiased_twin3a_k6():
         assert abs(m - kappa * G) < 3.5 * se, (m, kappa * G, se)
 
 
+def test_cfg4_mirror_sphere_chains_closed_form():
+    """configs[4] (mixed scene, three lights, chain length and type drawn per walk):
+    every converged k = 1 chain on the mirror sphere lies at the Alhazen point for
+    its light sample, with G = Coddington (point light) or Coddington x cos t_L
+    (quad lights), and T = G (rho = 1, L_e = I = 1, unit-area lights; Eq. 2)."""
+    w = W.config4(n_side=160, grid_n=32)
+    w.opts.tol, w.opts.max_iters, w.opts.max_iters_long = 1e-11, 40, 60
+    s = O.OracleScene(w)
+    r = s.walks(np.arange(w.n_walks))
+    sel = np.nonzero((r["status"] == 0) & (r["k"] == 1) & (r["surf"][:, 0] == 0))[0]
+    n_point = 0
+    for q in sel:
+        xD, xL = w.xD[r["walk"][q] // w.spp], r["xL"][q]
+        pts = CF.alhazen_points([-5, 0, 2.5], 1.0, xD, xL)
+        p = r["pos"][q][0]
+        assert min(np.linalg.norm(p - a) for a in pts) < 1e-10 * s.extent
+        point = np.allclose(xL, [-5.0, 4.0, 2.5])
+        n_point += point
+        G = CF.mirror_sphere_G([-5, 0, 2.5], 1.0, xD, [0, 1, 0], xL, p, None if point else [0, 1, 0])
+        assert r["G"][q] == pytest.approx(G, rel=1e-8)
+        assert r["T"][q] == pytest.approx(G, rel=1e-8)
+    assert len(sel) > 30 and 5 < n_point < len(sel)
+
+
 def test_dense_grid_enumeration_is_complete(cfg0):
     """dense seed grid, dedupe by same_chain, count stable under
     resolution doubling; equals the Alhazen root count."""
