@@ -273,6 +273,26 @@ def test_twin3a_walk_parity_and_closed_form():
         assert g["T"][ids[q]] == pytest.approx(kappa * G, rel=1e-5)
 
 
+def test_twin3a_full_size_closed_form():
+    """Twin 3a at configs[3]'s full size (1,048,576 k = 6 walks, 256^2-vertex slabs,
+    the bench's flags): 2,000 sampled converged chains on the layered Snell path
+    with closed-form G and T (property that holds at any size)."""
+    from tests import closed_forms as CF
+    w = W.config3(flat=True)
+    g, st, ext = PY.run_gpu(w, flags=w.opts.flags | BENCH_FLAGS)
+    ys = [float(srf.positions[0, 1]) for srf in w.surfaces]
+    etas = [1.0, 1.5, 1.0, 1.5, 1.0, 1.5, 1.0]
+    conv = np.nonzero(g["status"] == 0)[0]
+    assert len(conv) > 100000
+    worst_p = worst_g = 0.0
+    for q in np.random.default_rng(5).choice(conv, 2000, replace=False):
+        ref, G, kappa = CF.snell_layers(w.xD[q // w.spp], g["xL"][q][:3], ys, etas, with_G=True)
+        worst_p = max(worst_p, np.abs(g["pos"][q][:6] - ref).max() / ext)
+        worst_g = max(worst_g, abs(g["G"][q] / G - 1), abs(g["T"][q] / (kappa * G) - 1))
+    print(len(conv), worst_p, worst_g)
+    assert worst_p < 1e-4 and worst_g < 1e-4
+
+
 def test_twin3a_gpu_estimator_unbiased():
     """GPU estimator (Eq. 3 with the Eq. 15 weight) on twin 3a, k = 6: the
     per-receiver mean over 20,000 guided seeds equals the closed-form kappa G I."""
