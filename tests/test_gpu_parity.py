@@ -316,6 +316,25 @@ def test_twin3a_gpu_estimator_unbiased():
     assert n >= 16 and np.abs(z).max() < 4.5 and abs(z.mean()) < 4.0 / np.sqrt(n)
 
 
+def test_twin2a_full_size_closed_form():
+    """Flat-water twin of configs[2] at full size (16,777,216 k = 1 T walks, 512^2-vertex
+    pool, the bench's flags): 2,000 sampled converged chains at the Snell point with
+    the closed-form planar-refraction G (tests/closed_forms.snell_plane)."""
+    from tests import closed_forms as CF
+    w = W.config2(flat=True)
+    g, st, ext = PY.run_gpu(w, flags=w.opts.flags | BENCH_FLAGS)
+    eta = float(np.float32(1.33))
+    conv = np.nonzero(g["status"] == 0)[0]
+    assert len(conv) > 1000000
+    worst_p = worst_g = 0.0
+    for q in np.random.default_rng(6).choice(conv, 2000, replace=False):
+        x1, G = CF.snell_plane(w.xD[q // w.spp], g["xL"][q][:3], eta, 1.0)
+        worst_p = max(worst_p, np.abs(g["pos"][q][0] - x1).max() / ext)
+        worst_g = max(worst_g, abs(g["G"][q] / G - 1))
+    print(len(conv), worst_p, worst_g)
+    assert worst_p < 1e-4 and worst_g < 1e-4
+
+
 def test_cfg2_full_size_sampled():
     """configs[2] at full size (16,777,216 walks, bench launch configuration) vs 2,000 sampled oracle walks."""
     w = W.config2()
