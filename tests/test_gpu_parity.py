@@ -151,6 +151,25 @@ def test_twin1a_walk_parity():
                        max_non_boundary=3)
 
 
+def test_twin1a_full_size_closed_form():
+    """Analytic-glass-sphere twin of configs[1] at full size (1,048,576 k = 2 TT walks,
+    the bench's flags): 500 sampled converged chains equal an in-plane TT root of
+    tests/closed_forms.tt_sphere_chains."""
+    from tests import closed_forms as CF
+    w = W.config1(analytic=True)
+    g, st, ext = PY.run_gpu(w, flags=BENCH_FLAGS)
+    conv = np.nonzero(g["status"] == 0)[0]
+    assert len(conv) > 100000
+    worst = 0.0
+    for q in np.random.default_rng(7).choice(conv, 500, replace=False):
+        xD, p = w.xD[q // w.spp], g["pos"][q]
+        sols = CF.tt_sphere_chains([0, 0, 0], 1.0, 1.5, xD, g["xL"][q][:3], near=p[0])
+        assert sols
+        worst = max(worst, min(np.linalg.norm(p[0] - a) + np.linalg.norm(p[1] - b) for a, b in sols) / ext)
+    print(len(conv), worst)
+    assert worst < 1e-4
+
+
 def test_ragged_and_empty_batches():
     w = W.config0(n_side=8, spp=13)          # 832 walks: not a multiple of the 128-thread block
     g, st, ext = PY.run_gpu(w)
