@@ -300,6 +300,26 @@ def test_twin2a_snell_point_and_G():
         assert r["G"][q] == pytest.approx(G, rel=1e-9)
 
 
+def test_snell_layers_closed_form_special_cases():
+    """The layered closed form reduces to the textbook cases: one interface is
+    tests/closed_forms.snell_plane's Snell point; index-matched layers give a
+    straight segment with G = cos^3 t / H^2 (= cos/r^2) and kappa = 1; normal
+    incidence gives kappa = (1 - 0.04)^2 per slab."""
+    xD, xL = np.array([0.2, -1.0, -0.3]), np.array([0.9, 2.5, 0.4])
+    pts = CF.snell_layers(xD, xL, [0.0], [1.33, 1.0])
+    x1, _ = CF.snell_plane(xD, xL, 1.33, 1.0)
+    assert np.allclose(pts[0], x1, atol=1e-12)
+    pts, G, kappa = CF.snell_layers(xD, xL, [0.0, 0.1, 0.7], [1.0] * 4, with_G=True)
+    d = xL - xD
+    for p in pts:                                             # on the segment x_D x_L
+        assert np.linalg.norm(np.cross(p - xD, d)) < 1e-12
+    r = np.linalg.norm(d)
+    assert G == pytest.approx((d[1] / r) / r ** 2, rel=1e-12) and kappa == pytest.approx(1.0, abs=1e-15)
+    _, _, kappa = CF.snell_layers(xD, xD + [1e-9, 3.5, 0.0], [0.0, 0.1, 0.35, 0.45], [1.0, 1.5, 1.0, 1.5, 1.0],
+                                  with_G=True)
+    assert kappa == pytest.approx(0.9216 ** 2, rel=1e-9)
+
+
 def test_twin3a_k6_chains_are_layered_snell_points():
     """k = 6 TTTTTT through three planar glass slabs (twin of configs[3]): every
     converged chain is the unique straight-up refraction path fixed by Snell's
