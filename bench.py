@@ -214,8 +214,7 @@ def run_ours(args):
     w.opts.walk_id_base = D.walk_id_base(rank, w.n_walks * iters)
     ds = mpg.DeviceScene(w, stree_capacity=max(w.n_walks, args.photons) * world)
     b = mpg.Batch(w.xD, w.nD, w.spp, w.seed.k)
-    opts = ds.opts(flags=w.opts.flags | (1 if args.wavefront else 0) | (2 if args.hostloop else 0) |
-                   (4 if args.f64 else 0) | (0 if args.no_sort else 8))
+    opts = ds.opts(flags=w.opts.flags | (4 if args.f64 else 0) | (0 if args.no_sort else 8))
     stream = torch.cuda.current_stream()
     guided = ds.guide is not None
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)   # > 126 MB L2
@@ -404,7 +403,7 @@ def run_ours(args):
                            "l2": "256 MB buffer written before every timed step (inputs < 126 MB L2)",
                            "order": ("primaries in walk order" if not opts.flags & 8 else
                                      "primaries in (receiver cell, seed direction) order, MPG_FLAG_SORT"),
-                           "path": "wavefront" if opts.flags & 1 else "persistent kernel",
+                           "path": "persistent kernel",
                            "bvh": (f"{ds.info.bvh_width}-wide SAH, {ds.info.n_nodes} nodes, {ds.info.n_tri} triangles"
                                    if ds.info.n_tri else "analytic surfaces only"),
                            "precision": ("fp32 scene/traversal; fp64 positions, residual, hit refinement" +
@@ -448,8 +447,6 @@ def main():
                     help="with --guide stree: photon-based initial guide from this many photons (SURVEY 8(f)4)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--wavefront", action="store_true", help="wavefront path (MPG_FLAG_WAVEFRONT)")
-    ap.add_argument("--hostloop", action="store_true", help="wavefront with host-driven waves (profiling)")
     ap.add_argument("--no-sort", action="store_true",
                     help="walk-order primaries (default: coherence-sorted order, MPG_FLAG_SORT; same results)")
     ap.add_argument("--f64", action="store_true", help="MPG_FLAG_NEWTON_F64")

@@ -116,9 +116,8 @@ typedef struct {
     int32_t n_types; /* 1 (domain 0) or 126 (domain 1) */
 } mpg_guide_desc;
 
-#define MPG_FLAG_WAVEFRONT 1u /* wavefront path (slots + CUDA-graph wave loop) instead of the default
-                                  persistent one-chain-per-lane kernel */
-#define MPG_FLAG_HOSTLOOP 2u  /* wavefront waves launched from the host (blocking; for profilers) */
+/* flag bits 1 and 2 are reserved (a wavefront variant of round 1, removed: slower on every
+   config); any bit other than the two below -> MPG_ERR_INVALID_ARG */
 #define MPG_FLAG_NEWTON_F64 4u /* Jacobian blocks, frames and steps in fp64 (default fp32; positions and
                                   the residual are always fp64, R24) */
 #define MPG_FLAG_SORT 8u      /* persistent kernel: process the primaries in the order of a key built from
@@ -141,8 +140,8 @@ typedef struct {
                               (R x M / TR x M, Fig. "repber"): repetition r runs its trials
                               with Philox trial counter r*2^20 + t; trials[w] = sum of the M counts,
                               w = T * (sum/M) / (P(n) pdf_L).  0 or 1: one estimate.  Needs k_max < 2^20;
-                              repetitions r >= 1 run only the trials of walks that converged (persistent
-                              kernel; the wavefront path re-runs the primaries); stats: walks, converged,
+                              repetitions r >= 1 run only the trials of walks that converged; stats:
+                              walks, converged,
                               primary_iters and by_status count one pass, work counters all passes */
 } mpg_walk_opts;
 
@@ -221,8 +220,12 @@ typedef struct {
     int64_t max_samples;  /* record capacity between two rebuilds (all ranks' records for exchanges) */
     float eps;            /* overlap fraction of the split (0.1, P:523 footnote)           */
     float c_thr;          /* leaf threshold c sqrt|S| (1)                           */
-    float kappa_min;      /* vMF concentration clamp (1, R30)                              */
-    float kappa_max;      /* (300, R30: measured, fewer fireflies than 3e3 / 1e4)          */
+    float kappa_min;      /* vMF concentration kappa_i = sigma_i'^-2 (Eq. 12) is   */
+    float kappa_max;      /* clamped to [kappa_min, kappa_max]; the paper's Eq. 12 is 0 /
+                             FLT_MAX (no clamp; sigma' = 0 -> kappa_max; a lone lobe -> 1, R30).
+                             [1, 300] is the measured product option (R30b: fewer fireflies
+                             on configs[4] than 3e3 / 1e4 / unclamped).  kappa_min < 0 or
+                             kappa_max < kappa_min -> MPG_ERR_INVALID_ARG                  */
     int32_t max_depth;    /* 32                                                            */
     int32_t keep_all;     /* 0: fit from the last iteration's samples only (the paper's default,
                              P:426 footnote, records cleared by each rebuild); 1: from all samples
@@ -321,7 +324,7 @@ mpg_status mpg_sample_seeds(const mpg_scene *scene, const mpg_guide *guide, cons
                             const mpg_query *query, const mpg_walk_opts *opts, mpg_seed_buf *seeds, void *stream);
 
 /* Workspace bytes mpg_manifold_walk needs for n walks of chain length sampler->k
- * (wavefront slots, ray lists, trial entries/items). */
+ * (coherence-sort keys and permutation, trial entries/items, R x M buffers). */
 size_t mpg_walk_workspace_size(int64_t n, const mpg_sampler_desc *sampler, const mpg_walk_opts *opts);
 
 /* The batched manifold walk: per walk, deduce the seed chain
@@ -350,8 +353,7 @@ mpg_status mpg_debug_trace(float *buf, int64_t n_walks, int32_t stride);
 const char *mpg_last_error(void);
 int32_t mpg_version(void);
 /* Number of kernel launches this library has enqueued since load (host-side
- * counter, all threads; a CUDA-graph launch of the wavefront loop counts each
- * node of its body once per wave only in host-loop mode, else as 1). */
+ * counter, all threads; library launches such as cub's radix-sort passes are counted too). */
 uint64_t mpg_kernel_launches(void);
 
 #ifdef __cplusplus

@@ -1497,7 +1497,8 @@ void orc_stree_free(void *h) {
 
 /* Build the guide from n records; a record is a sample iff w > 0 and 0 <= type < 126.
  * eps: overlap fraction (0.1, P:523 footnote); c_thr: threshold coefficient (1);
- * kappa in [kappa_min, kappa_max] (R30). */
+ * kappa = sigma'^-2 (Eq. 12), optionally clamped to [kappa_min, kappa_max]; the paper's
+ * default is no clamp: kappa_min = 0, kappa_max = FLT_MAX (R30). */
 void *orc_stree_build(const orc_gsample *rec, int64_t n, float eps, float c_thr, int32_t max_depth,
                       float kappa_min, float kappa_max) {
     orc_stree *t = (orc_stree *)calloc(1, sizeof(orc_stree));
@@ -1643,7 +1644,9 @@ void *orc_stree_build(const orc_gsample *rec, int64_t n, float eps, float c_thr,
                     float d2 = dx * dx + dy * dy + dz * dz;
                     if (d2 < d2min) d2min = d2;
                 }
-                float kap = pos - g0 == 1 ? kappa_min : (d2min > 0.0f ? 1.0f / d2min : kappa_max);
+                /* Eq. 12: kappa = sigma'^-2; a lone lobe (no neighbour to measure a footprint,
+                 * P:474 silent) takes kappa = 1; sigma' = 0 takes kappa_max [R30] */
+                float kap = pos - g0 == 1 ? 1.0f : (d2min > 0.0f ? 1.0f / d2min : kappa_max);
                 if (kap < kappa_min) kap = kappa_min;
                 if (kap > kappa_max) kap = kappa_max;
                 t->lobe_mu[4 * i] = ri->omega[0];
@@ -1796,7 +1799,7 @@ static void trace_photon(const orc_scene *sc, const orc_photon_desc *pd, int64_t
     cvtx x[KMAX];
     int isT[KMAX];
     int nv = 0;
-    uint32_t rt[4];
+    uint32_t rt[4] = {0u, 0u, 0u, 0u};
     for (;;) {
         hit_t h = closest(sc, o3, d, eps, 1e300, 0, 1);
         double den = dot(d, pn);
@@ -1835,12 +1838,13 @@ static void trace_photon(const orc_scene *sc, const orc_photon_desc *pd, int64_t
         double ci = -dot(d, n);
         if (!(ci > 0.0)) return;
         int t = 0;
+        /* vertex nv owns word nv&3 of draw (10, nv>>2), whatever its material [R33] */
+        if ((nv & 3) == 0) draw(&o, wid, 10u, (uint32_t)(nv >> 2), rt);
         if (f->mat == 0) {
             w *= (double)f->reflectance;
         } else {                                                  /* R with probability F (Fresnel), else T */
             double e1 = outside ? f->eta_out : f->eta_in, e2 = outside ? f->eta_in : f->eta_out;
             double F = orc_fresnel(ci, e1, e2);
-            if ((nv & 3) == 0) draw(&o, wid, 10u, (uint32_t)(nv >> 2), rt);
             t = (double)u01(rt[nv & 3]) >= F;
             if (t) {
                 double eta = e1 / e2;

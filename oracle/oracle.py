@@ -192,10 +192,13 @@ def guide_dir_tables(H: np.ndarray):
     return npf, tpf, dpf
 
 
-STREE_DEFAULTS = dict(eps=0.1, c_thr=1.0, max_depth=32, kappa_min=1.0, kappa_max=300.0)
+FLT_MAX = float(np.finfo(np.float32).max)
+# Eq. 12 (kappa = sigma'^-2) unclamped; KAPPA_CLAMP_R30B is the measured product option
+STREE_DEFAULTS = dict(eps=0.1, c_thr=1.0, max_depth=32, kappa_min=0.0, kappa_max=FLT_MAX)
+KAPPA_CLAMP_R30B = (1.0, 300.0)
 
 
-def stree_build(records: np.ndarray, eps=0.1, c_thr=1.0, max_depth=32, kappa_min=1.0, kappa_max=300.0) -> dict:
+def stree_build(records: np.ndarray, eps=0.1, c_thr=1.0, max_depth=32, kappa_min=0.0, kappa_max=FLT_MAX) -> dict:
     """STree + vMF guide from sample records (GSAMPLE array): tree, leaf lists, lobes, tables."""
     L = lib()
     rec = np.ascontiguousarray(records, GSAMPLE)

@@ -20,7 +20,6 @@
 #include "device_common.cuh"
 #include "seed.cuh"
 #include "walk.cuh"
-#include "wavefront.cuh"
 
 // ----------------------------------------------------------------------------
 // error plumbing
@@ -1110,43 +1109,9 @@ static size_t mk_ws_bytes(int64_t n) { return mk_layout(n).total; }
 // recip_repeats scratch after the walk workspace: w_r [n] f32, trials_r [n] u32, stats
 static size_t rep_bytes(int64_t n) { return ((size_t)n * 12 + sizeof(mpg_walk_stats) + 767) & ~(size_t)255; }
 
-// wavefront workspace layout: header, slot lists, free stack,
-// per-slot SoA state, ray lists, hits, hard entries, trial items
-struct WFLayout {
-    uint32_t S, H, C;
-    size_t hdr, list0, list1, fstack, rec, s_psurf, s_entry, s_tgt, s_x, s_dq, s_y, s_pct, s_pn, r0o0, r0d0, r0o1, r0d1, ro[WF_KMAX], rd[WF_KMAX], h_p, h_s,
-        e_walk, e_psurf, e_pct, e_best, e_issued, e_pending, e_batch, it_entry, it_trial, total;
-};
-static WFLayout wf_layout(int64_t n, int k) {
-    WFLayout L;
-    int64_t nn = std::max<int64_t>(n, 1);
-    L.S = (uint32_t)std::min<int64_t>(nn, 1 << 20);
-    L.H = (uint32_t)std::min<int64_t>(nn, 1 << 22);
-    L.C = 4u * L.H + 65536u;
-    size_t o = 0;
-    auto take = [&](size_t bytes) { size_t r = o; o += (bytes + 255) & ~(size_t)255; return r; };
-    L.hdr = take(sizeof(WFHeader));
-    L.list0 = take(4ull * L.S); L.list1 = take(4ull * L.S); L.fstack = take(4ull * L.S);
-    L.rec = take(32ull * L.S); L.s_psurf = take(4ull * L.S);
-    L.s_entry = take(4ull * L.S); L.s_tgt = take(16ull * L.S);
-    L.s_x = take(32ull * L.S * k); L.s_dq = take(32ull * L.S * k); L.s_y = take(32ull * L.S * k);
-    L.s_pct = take(4ull * L.S); L.s_pn = take(4ull * L.S);
-    const size_t r0 = 16ull * L.S * (k + 1);
-    L.r0o0 = take(r0); L.r0d0 = take(r0); L.r0o1 = take(r0); L.r0d1 = take(r0);
-    for (int i = 0; i < WF_KMAX; i++) {
-        L.ro[i] = i >= 1 && i < k ? take(16ull * L.S) : 0;
-        L.rd[i] = i >= 1 && i < k ? take(16ull * L.S) : 0;
-    }
-    L.h_p = take(16ull * L.S); L.h_s = take(4ull * L.S);
-    L.e_walk = take(4ull * L.H); L.e_psurf = take(4ull * L.H); L.e_pct = take(4ull * L.H); L.e_best = take(4ull * L.H);
-    L.e_issued = take(4ull * L.H); L.e_pending = take(4ull * L.H); L.e_batch = take(4ull * L.H);
-    L.it_entry = take(4ull * L.C); L.it_trial = take(4ull * L.C);
-    L.total = o;
-    return L;
-}
-
 static size_t rep_offset(int64_t n, int k) {
-    return (std::max(wf_layout(n, k).total, mk_ws_bytes(n)) + 255) & ~(size_t)255;
+    (void)k;
+    return (mk_ws_bytes(n) + 255) & ~(size_t)255;
 }
 // R x M: w += w_r, trials += trials_r (then w *= scale on the last repetition); work
 // counters of the repetition added to the caller's stats (walks/converged count one pass)
@@ -1305,168 +1270,6 @@ static mpg_status launch_walk(const DScene &S, const SeedCtx &g, WalkParams P, c
     return MPG_OK;
 }
 
-// ---- wavefront launch: init + CUDA graph { while (more) { trace; update; plan; refill } } ----
-struct WFGraphCache {
-    std::vector<char> key;
-    cudaGraph_t graph = nullptr;
-    cudaGraphExec_t exec = nullptr;
-};
-static WFGraphCache g_wfcache;
-
-template <int KMAX, typename R>
-static mpg_status launch_wavefront(const DScene &S, const SeedCtx &g, const WalkParams &MP, void *ws, size_t wsb,
-                                   cudaStream_t st) {
-    WFLayout L = wf_layout(MP.n, g.k);
-    if (wsb < L.total) return fail(MPG_ERR_INVALID_ARG, "workspace too small for the wavefront walk");
-    char *b = (char *)ws;
-    WFParams P;
-    memset(&P, 0, sizeof(P));
-    P.xD = MP.xD; P.nD = MP.nD; P.n = MP.n; P.spp = MP.spp;
-    P.trial_base = MP.trial_base;
-    P.seed_xL = MP.seed_xL; P.seed_tgt = MP.seed_tgt; P.seed_bin = MP.seed_bin;
-    P.chain = MP.chain; P.status = MP.status; P.iters = MP.iters; P.G = MP.G; P.T = MP.T; P.w = MP.w;
-    P.trials = MP.trials; P.stats = MP.stats;
-    P.max_iters = MP.max_iters; P.trials_on = MP.trials_on; P.k_max = MP.k_max;
-    P.tol = MP.tol; P.beta0 = MP.beta0; P.same_eps = MP.same_eps; P.ray_eps = MP.ray_eps;
-    P.walk_id_base = MP.walk_id_base;
-    P.seed_ctype = MP.seed_ctype; P.seed_pn = MP.seed_pn; P.out_ctype = MP.out_ctype;
-    P.max_iters_long = MP.max_iters_long;
-    P.hdr = (WFHeader *)(b + L.hdr);
-    P.S = L.S; P.H = L.H; P.C = L.C;
-    P.list[0] = (uint32_t *)(b + L.list0); P.list[1] = (uint32_t *)(b + L.list1);
-    P.free_stack = (uint32_t *)(b + L.fstack);
-    P.rec = (uint32_t *)(b + L.rec); P.s_psurf = (uint32_t *)(b + L.s_psurf);
-    P.s_entry = (int32_t *)(b + L.s_entry);
-    P.s_tgt = (float4 *)(b + L.s_tgt); P.s_x = (double4 *)(b + L.s_x); P.s_dq = (double4 *)(b + L.s_dq);
-    P.s_y = (double4 *)(b + L.s_y);
-    
-    P.s_pct = (uint32_t *)(b + L.s_pct); P.s_pn = (float *)(b + L.s_pn);
-    P.r0o0 = (float4 *)(b + L.r0o0); P.r0d0 = (float4 *)(b + L.r0d0);
-    P.r0o1 = (float4 *)(b + L.r0o1); P.r0d1 = (float4 *)(b + L.r0d1);
-    P.h_p = (float4 *)(b + L.h_p); P.h_s = (int32_t *)(b + L.h_s);
-    P.e_walk = (int32_t *)(b + L.e_walk); P.e_psurf = (uint32_t *)(b + L.e_psurf); P.e_pct = (uint32_t *)(b + L.e_pct);
-    P.e_best = (uint32_t *)(b + L.e_best); P.e_issued = (uint32_t *)(b + L.e_issued);
-    P.e_pending = (uint32_t *)(b + L.e_pending); P.e_batch = (uint32_t *)(b + L.e_batch);
-    P.it_entry = (int32_t *)(b + L.it_entry); P.it_trial = (uint32_t *)(b + L.it_trial);
-    const int nk = std::max(1, std::min(g.k, KMAX));   // sub-steps per wave
-    float4 *ro[WF_KMAX + 1], *rd[WF_KMAX + 1];
-    for (int i = 0; i <= WF_KMAX; i++) {
-        ro[i] = i >= 1 && i < nk ? (float4 *)(b + L.ro[i]) : nullptr;
-        rd[i] = i >= 1 && i < nk ? (float4 *)(b + L.rd[i]) : nullptr;
-    }
-
-    static int occ_t = 0, occ_u = 0;
-    if (!occ_t) {
-        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_t, S.bvh_w == 4 ? k_wf_rays<4> : k_wf_rays<2>,
-                                                               128, 0));
-        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_u, k_wf_update<KMAX, R>, 128, 0));
-        occ_t = std::max(occ_t, 1); occ_u = std::max(occ_u, 1);
-    }
-    int gt = num_sms() * occ_t;
-    // grid-stride kernels sized to one resident wave of blocks: most waves are far
-    // smaller than S, and every block pays its stats flush and launch share
-    int gp0 = (int)std::min<int64_t>(((int64_t)L.S * (nk + 1) + 127) / 128, (int64_t)num_sms() * 8);
-    int gp = (int)std::min<int64_t>((L.S + 127) / 128, (int64_t)num_sms() * 8);
-    int gu = (int)std::min<int64_t>((L.S + 127) / 128, (int64_t)num_sms() * occ_u);
-    int gr = (int)std::min<int64_t>((L.S + 255) / 256, (int64_t)num_sms() * 2);
-    int gi = (int)std::min<int64_t>((L.S + 255) / 256, (int64_t)num_sms() * 8);
-
-    CUDA_TRY(cudaMemsetAsync(P.hdr, 0, sizeof(WFHeader), st));
-    if (MP.host_loop) { // host-driven waves (profilers cannot see kernels inside conditional graphs)
-        P.use_cond = 0;
-        COUNT_LAUNCH(1);
-        k_wf_init<KMAX><<<gi, 256, 0, st>>>(S, g, P);
-        CUDA_TRY(cudaPeekAtLastError());
-        unsigned int more = 1;
-        for (int wave = 0; more; wave++) {
-            for (int i = 0; i < nk; i++) {
-                COUNT_LAUNCH(1);
-                if (S.bvh_w == 4) k_wf_rays<4><<<gt, 128, 0, st>>>(S, P, i, ro[i], rd[i]);
-                else k_wf_rays<2><<<gt, 128, 0, st>>>(S, P, i, ro[i], rd[i]);
-                COUNT_LAUNCH(1);
-                k_wf_post<<<i == 0 ? gp0 : gp, 128, 0, st>>>(S, P, i, rd[i], ro[i + 1], rd[i + 1]);
-            }
-            COUNT_LAUNCH(1);
-            k_wf_update<KMAX, R><<<gu, 128, 0, st>>>(S, g, P);
-            COUNT_LAUNCH(1);
-            k_wf_plan<<<1, 1, 0, st>>>(P);
-            COUNT_LAUNCH(1);
-            k_wf_refill<KMAX><<<gr, 256, 0, st>>>(S, g, P);
-            CUDA_TRY(cudaPeekAtLastError());
-            if ((wave & 7) == 7) {
-                CUDA_TRY(cudaMemcpyAsync(&more, &P.hdr->more, 4, cudaMemcpyDeviceToHost, st));
-                CUDA_TRY(cudaStreamSynchronize(st));
-            }
-        }
-        return MPG_OK;
-    }
-    P.use_cond = 1;
-    // graph cache key: every byte the graph depends on
-    std::vector<char> key(sizeof(DScene) + sizeof(SeedCtx) + sizeof(WFParams) + 8 * sizeof(int));
-    {
-        char *kp = key.data();
-        memcpy(kp, &S, sizeof(DScene)); kp += sizeof(DScene);
-        memcpy(kp, &g, sizeof(SeedCtx)); kp += sizeof(SeedCtx);
-        WFParams Pk = P; Pk.cond = 0;
-        memcpy(kp, &Pk, sizeof(WFParams)); kp += sizeof(WFParams);
-        int dims[8] = {gt, gu, gr, KMAX * 16 + (int)sizeof(R), nk, gp0, gp, 0};
-        memcpy(kp, dims, sizeof(dims));
-    }
-    if (!g_wfcache.exec || g_wfcache.key != key) {
-        if (g_wfcache.exec) { cudaGraphExecDestroy(g_wfcache.exec); g_wfcache.exec = nullptr; }
-        if (g_wfcache.graph) { cudaGraphDestroy(g_wfcache.graph); g_wfcache.graph = nullptr; }
-        cudaGraph_t graph;
-        CUDA_TRY(cudaGraphCreate(&graph, 0));
-        cudaGraphConditionalHandle h;
-        CUDA_TRY(cudaGraphConditionalHandleCreate(&h, graph, 1, cudaGraphCondAssignDefault));
-        P.cond = h;
-        cudaGraphNodeParams cp = {};
-        cp.type = cudaGraphNodeTypeConditional;
-        cp.conditional.handle = h;
-        cp.conditional.type = cudaGraphCondTypeWhile;
-        cp.conditional.size = 1;
-        cudaGraphNode_t cnode;
-        CUDA_TRY(cudaGraphAddNode(&cnode, graph, nullptr, 0, &cp));
-        cudaGraph_t body = cp.conditional.phGraph_out[0];
-        DScene Sv = S; SeedCtx gv = g; WFParams Pv = P;
-        int subs[WF_KMAX];
-        void *args3[] = {&Sv, &gv, &Pv};
-        void *args1[] = {&Pv};
-        void *argr[WF_KMAX][5], *argp[WF_KMAX][6];
-        cudaGraphNode_t prev = nullptr;
-        auto add = [&](void *fn, int grid, int block, void **args) -> cudaError_t {
-            cudaKernelNodeParams kn = {};
-            kn.func = fn; kn.gridDim = dim3(grid); kn.blockDim = dim3(block); kn.kernelParams = args;
-            cudaGraphNode_t nd;
-            cudaError_t e = cudaGraphAddKernelNode(&nd, body, prev ? &prev : nullptr, prev ? 1 : 0, &kn);
-            prev = nd;
-            return e;
-        };
-        for (int i = 0; i < nk; i++) {
-            subs[i] = i;
-            argr[i][0] = &Sv; argr[i][1] = &Pv; argr[i][2] = &subs[i]; argr[i][3] = &ro[i]; argr[i][4] = &rd[i];
-            argp[i][0] = &Sv; argp[i][1] = &Pv; argp[i][2] = &subs[i]; argp[i][3] = &rd[i];
-            argp[i][4] = &ro[i + 1]; argp[i][5] = &rd[i + 1];
-            CUDA_TRY(add(S.bvh_w == 4 ? (void *)k_wf_rays<4> : (void *)k_wf_rays<2>, gt, 128, argr[i]));
-            CUDA_TRY(add((void *)k_wf_post, i == 0 ? gp0 : gp, 128, argp[i]));
-        }
-        CUDA_TRY(add((void *)k_wf_update<KMAX, R>, gu, 128, args3));
-        CUDA_TRY(add((void *)k_wf_plan, 1, 1, args1));
-        CUDA_TRY(add((void *)k_wf_refill<KMAX>, gr, 256, args3));
-        cudaGraphExec_t ex;
-        CUDA_TRY(cudaGraphInstantiate(&ex, graph, 0));
-        g_wfcache.graph = graph;
-        g_wfcache.exec = ex;
-        g_wfcache.key = key;
-    }
-    COUNT_LAUNCH(1);
-    k_wf_init<KMAX><<<gi, 256, 0, st>>>(S, g, P);
-    CUDA_TRY(cudaPeekAtLastError());
-    COUNT_LAUNCH(1);
-    CUDA_TRY(cudaGraphLaunch(g_wfcache.exec, st));
-    return MPG_OK;
-}
-
 extern "C" mpg_status mpg_manifold_walk(const mpg_scene *scene, const mpg_guide *guide, const mpg_sampler_desc *sd,
                                         const mpg_query *q, const mpg_seed_buf *sb, const mpg_walk_opts *o,
                                         mpg_walk_buf *out, mpg_walk_stats *stats, void *workspace,
@@ -1482,6 +1285,7 @@ extern "C" mpg_status mpg_manifold_walk(const mpg_scene *scene, const mpg_guide 
     ARG_CHECK(q->n_recv * (int64_t)q->spp < (int64_t)1 << 31, "at most 2^31-1 walks per call");
     ARG_CHECK(o->max_iters >= 0 && o->max_iters < 65536 && o->tol > 0.f && o->beta0 > 0.f, "bad walk options");
     ARG_CHECK(!o->trials || o->k_max >= 1, "k_max must be >= 1");
+    ARG_CHECK((o->flags & ~(MPG_FLAG_NEWTON_F64 | MPG_FLAG_SORT)) == 0, "unknown walk flag");
     SeedCtx g;
     mpg_status st = make_seed_ctx(scene, guide, sd, o, g);
     if (st != MPG_OK) return st;
@@ -1517,7 +1321,6 @@ extern "C" mpg_status mpg_manifold_walk(const mpg_scene *scene, const mpg_guide 
     P.ray_eps = o->ray_eps > 0.f ? o->ray_eps : 1e-4f * scene->d.extent;
     P.walk_id_base = o->walk_id_base;
     P.trav_bytes = scene->trav_bytes;
-    P.host_loop = (o->flags & MPG_FLAG_HOSTLOOP) != 0;
     P.dbg = g_dbg;
     P.n_dbg = g_dbg_n;
     P.dbg_stride = g_dbg_stride;
@@ -1544,7 +1347,7 @@ extern "C" mpg_status mpg_manifold_walk(const mpg_scene *scene, const mpg_guide 
         Pr.trials = t_r;
         Pr.stats = (unsigned long long *)s_r;
         Pr.psurf_out = ps_r;
-        Pr.trials_only = (o->flags & MPG_FLAG_WAVEFRONT) ? 0 : 1;   // the wavefront path re-runs primaries
+        Pr.trials_only = 1;
         CUDA_TRY(cudaMemsetAsync(s_r, 0, sizeof(mpg_walk_stats), s));
         st = walk_dispatch(scene, g, sd, o, Pr, workspace, workspace_bytes, s);
         if (st != MPG_OK) return st;
@@ -1561,20 +1364,6 @@ static mpg_status walk_dispatch(const mpg_scene *scene, const SeedCtx &g, const 
                                 const mpg_walk_opts *o, const WalkParams &P, void *workspace, size_t workspace_bytes,
                                 cudaStream_t s) {
     const int k = g.k;
-    if (o->flags & MPG_FLAG_WAVEFRONT) {
-        if (o->flags & MPG_FLAG_NEWTON_F64) {
-            if (k <= 1) return launch_wavefront<1, double>(scene->d, g, P, workspace, workspace_bytes, s);
-            if (k <= 2) return launch_wavefront<2, double>(scene->d, g, P, workspace, workspace_bytes, s);
-            if (k <= 4) return launch_wavefront<4, double>(scene->d, g, P, workspace, workspace_bytes, s);
-            if (k <= 6) return launch_wavefront<6, double>(scene->d, g, P, workspace, workspace_bytes, s);
-            return launch_wavefront<8, double>(scene->d, g, P, workspace, workspace_bytes, s);
-        }
-        if (k <= 1) return launch_wavefront<1, float>(scene->d, g, P, workspace, workspace_bytes, s);
-        if (k <= 2) return launch_wavefront<2, float>(scene->d, g, P, workspace, workspace_bytes, s);
-        if (k <= 4) return launch_wavefront<4, float>(scene->d, g, P, workspace, workspace_bytes, s);
-        if (k <= 6) return launch_wavefront<6, float>(scene->d, g, P, workspace, workspace_bytes, s);
-        return launch_wavefront<8, float>(scene->d, g, P, workspace, workspace_bytes, s);
-    }
     if (o->flags & MPG_FLAG_NEWTON_F64) {
         if (k <= 1) return launch_walk<1, double>(scene->d, g, P, s, workspace, (o->flags & MPG_FLAG_SORT) != 0);
         if (k <= 2) return launch_walk<2, double>(scene->d, g, P, s, workspace, (o->flags & MPG_FLAG_SORT) != 0);

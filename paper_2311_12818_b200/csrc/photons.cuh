@@ -108,12 +108,13 @@ __global__ void k_photons(const DScene S, const PhotonDev P, int64_t first, int6
             const double ci = -ddot(d, n);
             if (!(ci > 0.0)) break;
             uint32_t t = 0;
+            // vertex nv owns word nv&3 of draw (10, nv>>2), whatever its material (R33)
+            if ((nv & 3) == 0) rt = rng_draw(P.seed, wid, 10u, (uint32_t)(nv >> 2));
             if (f.mat == 0) {
                 w *= (double)f.refl;
             } else {
                 const double e1 = outside ? f.eta_out : f.eta_in, e2 = outside ? f.eta_in : f.eta_out;
                 const double F = fresnel_d(ci, e1, e2);
-                if ((nv & 3) == 0) rt = rng_draw(P.seed, wid, 10u, (uint32_t)(nv >> 2));
                 const uint32_t ru = (nv & 3) == 0 ? rt.x : (nv & 3) == 1 ? rt.y : (nv & 3) == 2 ? rt.z : rt.w;
                 t = (double)u01(ru) >= F ? 1u : 0u;
                 if (t) {

@@ -269,7 +269,8 @@ __global__ void k_lobe_kappa(const mpg_guide_sample *rec, const unsigned long lo
             float d2 = FA(FA(FM(dx, dx), FM(dy, dy)), FM(dz, dz));
             d2min = fminf(d2min, d2);
         }
-        float kap = ghi - glo == 1 ? kmin : (d2min > 0.0f ? FD(1.0f, d2min) : kmax);
+        // Eq. 12: kappa = sigma'^-2; a lone lobe takes 1, sigma' = 0 takes kmax (R30)
+        float kap = ghi - glo == 1 ? 1.0f : (d2min > 0.0f ? FD(1.0f, d2min) : kmax);
         kap = fminf(fmaxf(kap, kmin), kmax);
         lobe_mu[j] = make_float4(ox, oy, oz, kap);
     }
@@ -663,7 +664,7 @@ extern "C" mpg_status mpg_guide_create_stree(const mpg_stree_desc *desc, mpg_gui
     ARG_CHECK(desc->max_samples >= 0 && desc->max_samples < (1ll << 31), "max_samples must be in [0, 2^31)");
     ARG_CHECK(desc->eps >= 0.f && desc->eps < 0.5f, "eps must be in [0, 0.5)");
     ARG_CHECK(desc->c_thr > 0.f, "c_thr must be > 0");
-    ARG_CHECK(desc->kappa_min > 0.f && desc->kappa_max >= desc->kappa_min, "bad kappa clamp");
+    ARG_CHECK(desc->kappa_min >= 0.f && desc->kappa_max >= desc->kappa_min, "bad kappa clamp");
     ARG_CHECK(desc->max_depth >= 0 && desc->max_depth <= 64, "max_depth must be in [0, 64]");
     mpg_guide *g = new mpg_guide();
     memset(&g->desc, 0, sizeof(g->desc));

@@ -97,7 +97,6 @@ struct WalkParams {
     int64_t *e_walk;
     uint32_t *e_psurf, *e_pct, *e_best, *e_pending, *e_issued, *e_batch;
     unsigned long long *items;  // (e << 32 | t); ~0 = not yet written (ring memset to 0xff)
-    int host_loop;      // wavefront: host-driven waves (MPG_FLAG_HOSTLOOP)
 };
 
 // stats slots (mirror mpg_walk_stats field order)
@@ -295,11 +294,15 @@ __device__ __forceinline__ bool queue_drained(const WalkParams &P, bool drained)
     return drained || __ldcg(&P.th->queue) >= (unsigned long long)P.n;
 }
 // make walk w a hard entry whose trials last+1 .. run as items (first batch
-// item_b0); false (and seq_only) if the entry table or the ring is full
+// item_b0); false (and seq_only: the walk's remaining trials stay in this lane,
+// it never asks again) if the entry table or the ring is full.  A full table is
+// seen with a plain load first, so the 32-bit counter stops growing once it
+// reaches hard_cap (no wrap-around onto live entries, no atomic per trial).
 __device__ __forceinline__ bool hard_publish(const WalkParams &P, int64_t w, uint32_t psurf, int pk, uint32_t ptau,
                                              uint32_t last, bool &seq_only) {
+    if (*(volatile unsigned int *)&P.th->n_entries >= P.hard_cap) { seq_only = true; return false; }
     unsigned int e = atomicAdd(&P.th->n_entries, 1u);
-    if (e >= P.hard_cap) return false;
+    if (e >= P.hard_cap) { seq_only = true; return false; }
     const unsigned backlog = *(volatile unsigned *)&P.th->item_tail - *(volatile unsigned *)&P.th->item_head;
     const bool idle = (int)backlog < (int)P.idle_backlog && __ldcg(&P.th->queue) >= (unsigned long long)P.n;
     const uint32_t B = min(idle ? P.item_b0_idle : P.item_b0, P.k_max - last);

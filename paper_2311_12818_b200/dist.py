@@ -74,10 +74,20 @@ def exchange_samples(ds, buf: torch.Tensor, n_local: int, stream=None):
     every rank's sample records of this iteration are gathered on every rank (NCCL
     all-gather; 48 B per walk), in rank order, and replace the local records before
     mpg_guide_rebuild, so every rank fits the same tree from the samples of all ranks
-    (P:426 footnote).  buf: device uint8 of world * n_local * 48 bytes."""
+    (P:426 footnote).  buf: device uint8 of world * n_local * 48 bytes.
+
+    Only the paper's default (fit from the last iteration's samples, keep_all = 0) is
+    exchangeable: with keep_all the guide keeps earlier records across rebuilds, so the
+    local record count is not this iteration's n_local and gathering them again would
+    duplicate every earlier rank's records -- rejected up front."""
     from . import mpg
     if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
         return
+    desc = getattr(ds, "stree_desc", None)
+    if desc is not None and desc.keep_all:
+        raise ValueError("exchange_samples: keep_all guides cannot be exchanged (records persist across rebuilds)")
+    if desc is not None and desc.max_samples < dist.get_world_size() * n_local:
+        raise ValueError("exchange_samples: guide capacity below world * n_local records")
     world = dist.get_world_size()
     B = mpg.GUIDE_SAMPLE_BYTES
     mine = torch.empty(n_local * B, dtype=torch.uint8, device=buf.device)

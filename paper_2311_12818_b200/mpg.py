@@ -17,6 +17,8 @@ from . import workloads as W
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("MPG_LIB", os.path.join(HERE, "libmpg.so"))   # MPG_LIB: experiment variants
 KMAX = 8
+FLT_MAX = float(np.finfo(np.float32).max)   # unclamped vMF concentration (Eq. 12, R30)
+KAPPA_CLAMP_R30B = (1.0, 300.0)             # the measured product option (R30b)
 STATUS_NAMES = ["CONVERGED", "MAXITER", "SEED_FAIL", "BAD_SIDE", "DEGENERATE", "OCCLUDED"]
 
 
@@ -383,7 +385,7 @@ def _f3(v):
 class DeviceScene:
     """Scene + (optional) guide of a Workload, resident on the current CUDA device."""
 
-    def __init__(self, w: "W.Workload", stream=None, stree_capacity=None, stree_kappa_max=300.0):
+    def __init__(self, w: "W.Workload", stream=None, stree_capacity=None, stree_kappa=(0.0, FLT_MAX)):
         import torch
         if not torch.cuda.is_available():
             raise MPGError("no CUDA device: the manifold walk has no CPU path")
@@ -418,7 +420,8 @@ class DeviceScene:
         self.stree = sp.mode == W.SEED_GUIDE_STREE
         if self.stree:
             d = mpg_stree_desc(max_samples=int(stree_capacity if stree_capacity is not None else w.n_walks),
-                               eps=0.1, c_thr=1.0, kappa_min=1.0, kappa_max=float(stree_kappa_max), max_depth=32)
+                               eps=0.1, c_thr=1.0, kappa_min=float(stree_kappa[0]),
+                               kappa_max=float(stree_kappa[1]), max_depth=32)
             self.stree_desc = d
             self.guide = mpg_guide_create_stree(d)
         elif sp.mode in (W.SEED_GUIDE_UV, W.SEED_GUIDE_DIR):

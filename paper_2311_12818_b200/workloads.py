@@ -341,13 +341,26 @@ def receiver_grid(lo: float, hi: float, n: int, y: float, lo_z: Optional[float] 
 # ----------------------------------------------------------------------------
 # the BASELINE.json configurations (and their closed-form test twins)
 # ----------------------------------------------------------------------------
-def config0(n_side: int = 64, spp: int = 16) -> Workload:
+# opaque diffuse occluders of the visibility twin "0v" (test-only): axis-aligned
+# horizontal rectangles (origin, edge_u, edge_v); one between the sphere and the
+# light (cuts x_1 -> x_L segments), one just above the receivers (cuts x_D -> x_1)
+OCCLUDERS_0V = (((-0.2, 2.5, -1.0), (1.6, 0.0, 0.0), (0.0, 0.0, 1.4)),
+                ((1.0, -1.25, 0.5), (1.5, 0.0, 0.0), (0.0, 0.0, 1.5)))
+
+
+def config0(n_side: int = 64, spp: int = 16, occluders: bool = False) -> Workload:
     """configs[0]: k=1 R off an analytic mirror sphere r=1 at the origin, point
-    light (0,4,0), 64x64 receivers on y=-1.5 over [-3,3]^2, 16 cap seeds each."""
+    light (0,4,0), 64x64 receivers on y=-1.5 over [-3,3]^2, 16 cap seeds each.
+    `occluders=True` is twin 0v: the same scene plus the two opaque diffuse
+    rectangles OCCLUDERS_0V, where visibility has a closed form (an
+    Alhazen chain is occluded iff one of its two segments crosses a rectangle)."""
     sph = Surface(SURF_SPHERE, MAT_CONDUCTOR, reflectance=1.0, center=(0.0, 0.0, 0.0), radius=1.0)
+    surfs = [sph]
+    if occluders:
+        surfs += [Surface(SURF_QUAD, MAT_DIFFUSE, origin=o, edge_u=u, edge_v=v) for o, u, v in OCCLUDERS_0V]
     light = Light(LIGHT_POINT, 1.0, position=(0.0, 4.0, 0.0))
     xD, nD = receiver_grid(-3.0, 3.0, n_side, -1.5)
-    return Workload("cfg0_sphere_mirror_k1", [sph], [light], xD, nD, spp,
+    return Workload("cfg0_sphere_mirror_k1" + ("_occluded" if occluders else ""), surfs, [light], xD, nD, spp,
                     SeedSpec(SEED_CAP, surf_id=0, k=1, tau=0b0),
                     WalkOpts(max_iters=20), recv_shape=(n_side, n_side))
 

@@ -240,3 +240,56 @@ def mirror_sphere_G(c, R, xD, nD, xL, p, light_normal=None):
     if light_normal is not None:
         G *= abs(np.dot(nz(np.asarray(p, np.float64) - np.asarray(xL, np.float64)), light_normal))
     return G
+
+
+def segment_hits_rect(a, b, rect, margin):
+    """Does the open segment a -> b cross the axis-aligned horizontal rectangle
+    rect = (origin, edge_u, edge_v) (edges along +x and +z, y constant)?  Returns
+    True / False, or None when the crossing lies within `margin` of the rectangle's
+    border (too close to call in floating point)."""
+    a, b = np.asarray(a, np.float64), np.asarray(b, np.float64)
+    o, u, v = (np.asarray(x, np.float64) for x in rect)
+    y = o[1]
+    if (a[1] - y) * (b[1] - y) >= 0:
+        return False
+    t = (y - a[1]) / (b[1] - a[1])
+    p = a + t * (b - a)
+    dx = min(p[0] - o[0], o[0] + u[0] - p[0])
+    dz = min(p[2] - o[2], o[2] + v[2] - p[2])
+    d = min(dx, dz)                     # > 0 inside, < 0 outside
+    if abs(d) < margin:
+        return None
+    return bool(d > 0)
+
+
+def any_hit_brute_force(a, b, tri_v0, tri_v1, tri_v2, spheres=(), eps=0.0):
+    """Any intersection of the segment a -> b with t in (eps, |b-a| - eps) against
+    every triangle (Moller-Trumbore over all of them, numpy fp64) and analytic
+    spheres (c, R): the visibility V of Eq. 2 by brute force."""
+    a, b = np.asarray(a, np.float64), np.asarray(b, np.float64)
+    d = b - a
+    L = np.linalg.norm(d)
+    d = d / L
+    for c, R in spheres:
+        oc = a - np.asarray(c, np.float64)
+        bb = np.dot(oc, d)
+        disc = bb * bb - (np.dot(oc, oc) - R * R)
+        if disc >= 0:
+            for t in (-bb - np.sqrt(disc), -bb + np.sqrt(disc)):
+                if eps < t < L - eps:
+                    return True
+    if len(tri_v0) == 0:
+        return False
+    e1 = tri_v1 - tri_v0
+    e2 = tri_v2 - tri_v0
+    p = np.cross(d, e2)
+    det = np.einsum("ij,ij->i", e1, p)
+    with np.errstate(divide="ignore", invalid="ignore"):
+        inv = 1.0 / det
+        tv = a - tri_v0
+        u = np.einsum("ij,ij->i", tv, p) * inv
+        q = np.cross(tv, e1)
+        v = (q @ d) * inv
+        t = np.einsum("ij,ij->i", e2, q) * inv
+    hit = (det != 0) & (u >= 0) & (v >= 0) & (u + v <= 1) & (t > eps) & (t < L - eps)
+    return bool(hit.any())

@@ -36,6 +36,11 @@ def compare(g, o, ids, extent, k):
     rep = {"n": len(ids), "conv_gpu": int(cg.sum()), "conv_orc": int(co.sum()),
            "flag_agree": float((cg == co).mean()), "status_agree": float((gs == os_).mean()),
            "both": int(both.sum())}
+    # visibility: among walks both sides converge, CONVERGED (V = 1) vs OCCLUDED (V = 0)
+    rep["n_occluded_gpu"] = int((gs == 5).sum())
+    rep["n_occluded_orc"] = int((os_ == 5).sum())
+    rep["vis_mismatch"] = int((both & (gs != os_)).sum())
+    rep["vis_agree"] = float((gs[both] == os_[both]).mean()) if both.any() else 1.0
     gp = g["pos"][ids][:, :k]
     dv = np.linalg.norm(gp - o["pos"][:, :k], axis=2)
     if "k" in o:                       # per-walk chain length (configs[4]): vertices beyond n are unused

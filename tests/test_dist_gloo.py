@@ -195,3 +195,33 @@ def test_two_rank_stree_sample_exchange(tmp_path):
     ref = np.concatenate([_rank_records(k, w, s) for k in range(2)])
     assert np.array_equal(got, np.frombuffer(ref.tobytes(), np.uint8))
     assert (ref["w"] > 0).sum() > 0
+
+
+def _keep_all_worker(rank, world, port, out):
+    import types
+    import torch
+    import torch.distributed as dist
+    from paper_2311_12818_b200 import dist as D
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    res = {}
+    for keep, cap in ((1, 100), (0, 10)):
+        ds = types.SimpleNamespace(stree_desc=types.SimpleNamespace(keep_all=keep, max_samples=cap))
+        try:
+            D.exchange_samples(ds, torch.empty(0, dtype=torch.uint8), 10)
+            res[f"{keep}_{cap}"] = "ok"
+        except ValueError as e:
+            res[f"{keep}_{cap}"] = str(e)
+    if rank == 0:
+        json.dump(res, open(out, "w"))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_sample_exchange_rejects_keep_all_and_small_capacity(tmp_path):
+    """keep_all guides keep records across rebuilds, so gathering 'this iteration's'
+    records again would duplicate them; a capacity below world * n_local would
+    overflow: both are rejected before any collective."""
+    out = str(tmp_path / "r.json")
+    mp.spawn(_keep_all_worker, args=(2, _free_port(), out), nprocs=2, join=True)
+    r = json.load(open(out))
+    assert "keep_all" in r["1_100"] and "capacity" in r["0_10"]

@@ -1,9 +1,9 @@
 """GPU photon tracer (mpg_trace_photons) vs the oracle's, on the
 same counter-based draws; and the photon-initialised STree guide on configs[4].
 
-Bars: landed flag and chain type agree on >= 99 % of photons (R/T choices compare a
-uniform with F computed in fp64 on both sides; a photon grazing a shared edge may
-take the other triangle, R17); on photons whose types agree x_D within 1e-4 x
+Bars: landed flag and chain type agree on all photons but at most 2 of 20,000 (R/T
+choices compare the same uniform with F computed in fp64 on both sides; a photon
+grazing a shared edge may take the other triangle, R17); on photons whose types agree x_D within 1e-4 x
 extent and w_D* within 1e-4 for >= 99.5 % of them (long internal-reflection chains
 amplify fp32/fp64 differences), w relative 1e-6; records bit-exact in x_L."""
 import numpy as np
@@ -30,11 +30,12 @@ def _gpu_photons(w, n, plane_y):
     return np.frombuffer(rec.cpu().numpy().tobytes(), O.GSAMPLE), ext
 
 
-@pytest.mark.parametrize("cfg", ["cfg0", "cfg1", "cfg4"])
+@pytest.mark.parametrize("cfg", ["cfg0", "cfg1", "cfg4", "mirror_over_glass"])
 def test_photons_match_oracle(cfg):
     from oracle import oracle as O
-    w, y = {"cfg0": (W.config0(n_side=8, spp=1), -1.5), "cfg1": (W.config1(n_side=8), -1.2),
-            "cfg4": (W.config4(n_side=8), -2.0)}[cfg]
+    from tests.test_photon_oracle import _mirror_over_glass
+    w, y = {"cfg0": lambda: (W.config0(n_side=8, spp=1), -1.5), "cfg1": lambda: (W.config1(n_side=8), -1.2),
+            "cfg4": lambda: (W.config4(n_side=8), -2.0), "mirror_over_glass": lambda: (_mirror_over_glass(), -1.0)}[cfg]()
     n = 20000
     g, ext = _gpu_photons(w, n, y)
     s = O.OracleScene(w)
@@ -42,7 +43,7 @@ def test_photons_match_oracle(cfg):
     lg, lo = g["w"] > 0, o["w"] > 0
     agree = ((g["type"] == o["type"]) & (lg == lo)).mean()
     print(cfg, int(lo.sum()), agree)
-    assert lo.sum() > 100 and agree >= 0.99
+    assert lo.sum() > 100 and n - int(round(agree * n)) <= 2
     both = lg & lo & (g["type"] == o["type"])
     assert np.array_equal(g["xL"][both], o["xL"][both])
     # fp32 traversal + fp64 refinement vs fp64 throughout: differences grow along long

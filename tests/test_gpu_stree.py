@@ -25,11 +25,11 @@ def _oracle_records(r):
     return np.frombuffer(r.tobytes(), O.GSAMPLE).copy()
 
 
-def _gpu_build(records, eps=0.1, c_thr=1.0, max_depth=32):
+def _gpu_build(records, eps=0.1, c_thr=1.0, max_depth=32, kappa=(0.0, np.finfo(np.float32).max)):
     import torch
     from paper_2311_12818_b200 import mpg
-    d = mpg.mpg_stree_desc(max_samples=max(1, len(records)), eps=eps, c_thr=c_thr, kappa_min=1.0, kappa_max=300.0,
-                           max_depth=max_depth)
+    d = mpg.mpg_stree_desc(max_samples=max(1, len(records)), eps=eps, c_thr=c_thr, kappa_min=kappa[0],
+                           kappa_max=kappa[1], max_depth=max_depth)
     g = mpg.mpg_guide_create_stree(d)
     if len(records):
         t = torch.from_numpy(np.frombuffer(records.tobytes(), np.uint8).copy()).cuda()
@@ -60,12 +60,19 @@ def _assert_same_tree(G, R):
 
 @pytest.mark.parametrize("n,eps,c_thr", [(0, 0.1, 1.0), (1, 0.1, 1.0), (700, 0.1, 1.0), (20000, 0.1, 1.0),
                                          (20000, 0.0, 1.0), (20000, 0.1, 0.25), (200000, 0.1, 1.0)])
-def test_stree_build_bit_exact(n, eps, c_thr):
+@pytest.mark.parametrize("clamp", [False, True])
+def test_stree_build_bit_exact(n, eps, c_thr, clamp):
+    """Both kappa settings: Eq. 12 unclamped (the default) and the [1, 300] product option (R30b)."""
     from oracle import oracle as O
     r = W.synthetic_guide_samples(n, seed=n + 3)
-    G = _gpu_build(r, eps=eps, c_thr=c_thr)
-    R = O.stree_build(_oracle_records(r), eps=eps, c_thr=c_thr)
+    kap = O.KAPPA_CLAMP_R30B if clamp else (O.STREE_DEFAULTS["kappa_min"], O.STREE_DEFAULTS["kappa_max"])
+    G = _gpu_build(r, eps=eps, c_thr=c_thr, kappa=kap)
+    R = O.stree_build(_oracle_records(r), eps=eps, c_thr=c_thr, kappa_min=kap[0], kappa_max=kap[1])
     _assert_same_tree(G, R)
+    if clamp and R["n_lobes"] > 100:
+        assert R["lobe_mu"][:, 3].max() <= 300.0
+    elif R["n_lobes"] > 100:
+        assert R["lobe_mu"][:, 3].max() > 300.0          # Eq. 12 concentrations beyond the clamp occur
 
 
 def test_stree_build_duplicates_hit_the_depth_cap():
@@ -209,8 +216,8 @@ def test_keep_all_samples_fits_from_every_iteration():
     r1 = W.synthetic_guide_samples(20000, seed=31)
     r2 = W.synthetic_guide_samples(20000, seed=32)
     for keep in (0, 1):
-        d = mpg.mpg_stree_desc(max_samples=40000, eps=0.1, c_thr=1.0, kappa_min=1.0, kappa_max=300.0, max_depth=32,
-                               keep_all=keep)
+        d = mpg.mpg_stree_desc(max_samples=40000, eps=0.1, c_thr=1.0, kappa_min=0.0, kappa_max=mpg.FLT_MAX,
+                               max_depth=32, keep_all=keep)
         g = mpg.mpg_guide_create_stree(d)
         t1 = torch.from_numpy(np.frombuffer(r1.tobytes(), np.uint8).copy()).cuda()
         mpg.mpg_guide_set_samples(g, t1, len(r1))

@@ -800,3 +800,74 @@ def test_repeated_reciprocal_estimates_unbiased_and_lower_variance():
     assert (z < 3).mean() >= 0.95 and z.max() < 5
     assert abs(wa.mean() - wb.mean()) < 3 * np.sqrt(wa.var() / wa.size + wb.var() / wb.size)
     assert wb.var(1).mean() < 0.8 * wa.var(1).mean()
+
+
+# ---------------------------------------------------------------------------
+# visibility V (Eq. 2, "including the visibility function"; O8):
+# closed-form occluders and brute-force any-hit
+# ---------------------------------------------------------------------------
+def _occlusion_closed_form(xD, p, xL, margin):
+    """Twin 0v: the Alhazen chain x_D -> p -> x_L is occluded iff one of its two
+    segments crosses one of the rectangles OCCLUDERS_0V (None: too close to call)."""
+    hits = [CF.segment_hits_rect(a, b, R, margin) for R in W.OCCLUDERS_0V for a, b in ((xD, p), (p, xL))]
+    if any(h is None for h in hits):
+        return None
+    return any(hits)
+
+
+def test_visibility_closed_form_occluders():
+    """Twin 0v (configs[0] plus two opaque diffuse rectangles): every converged walk
+    is OCCLUDED with G = T = 0 exactly when a segment of its (unique) Alhazen chain
+    crosses a rectangle, else CONVERGED with the Coddington G; the rectangles do not
+    take part in deduction or reprojection (specular surfaces only, Eq. 6)."""
+    w = W.config0(n_side=48, spp=4, occluders=True)
+    s = O.OracleScene(w)
+    r = s.walks(np.arange(w.n_walks), s.opts(tol=1e-11, max_iters=40))   # tight tol: G to 1e-6
+    ext = s.extent
+    n = {True: 0, False: 0}
+    for q in np.nonzero(np.isin(r["status"], (0, 5)))[0]:
+        xD, xL = w.xD[q // w.spp].astype(np.float64), r["xL"][q]
+        pts = CF.alhazen_points([0, 0, 0], 1.0, xD, xL)
+        assert len(pts) == 1
+        p = pts[0]
+        assert np.linalg.norm(r["pos"][q][0] - p) < 1e-4 * ext
+        occ = _occlusion_closed_form(xD, p, xL, 1e-3)
+        if occ is None:
+            continue
+        n[occ] += 1
+        if occ:
+            assert r["status"][q] == 5 and r["G"][q] == 0.0 and r["T"][q] == 0.0 and r["w"][q] == 0.0
+        else:
+            assert r["status"][q] == 0
+            assert r["G"][q] == pytest.approx(CF.coddington_G([0, 0, 0], 1.0, xD, [0, 1, 0], xL, p), rel=1e-6)
+    print(n)
+    assert n[True] > 150 and n[False] > 500
+    # the same walks without the rectangles: every OCCLUDED one converges (V is the only difference)
+    s0 = O.OracleScene(W.config0(n_side=48, spp=4))
+    r0 = s0.walks(np.nonzero(r["status"] == 5)[0], s0.opts(tol=1e-11, max_iters=40))
+    assert (r0["status"] == 0).mean() > 0.99
+
+
+def test_visibility_equals_brute_force_any_hit_cfg4():
+    """configs[4] (cross-object occlusion between the sphere, the icosphere and the
+    pool): the oracle's status of converged chains (CONVERGED vs OCCLUDED) equals a
+    brute-force any-hit of every segment x_D -> x_1 -> ... -> x_k -> x_L against all
+    surfaces (numpy Moller-Trumbore over every triangle, analytic sphere)."""
+    w = W.config4(n_side=128, grid_n=64)
+    s = O.OracleScene(w)
+    r = s.walks(np.arange(w.n_walks))
+    pos, _, idx, _, _ = w.mesh_arrays()
+    P = pos.astype(np.float64)
+    v0, v1, v2 = P[idx[:, 0]], P[idx[:, 1]], P[idx[:, 2]]
+    sph = [(np.asarray(f.center, np.float64), float(f.radius)) for f in w.surfaces if f.kind == W.SURF_SPHERE]
+    eps = 1e-4 * s.extent
+    sel = np.nonzero(np.isin(r["status"], (0, 5)))[0]
+    n_occ = 0
+    for q in sel:
+        k = int(r["k"][q])
+        pts = [w.xD[q // w.spp].astype(np.float64)] + [r["pos"][q][i] for i in range(k)] + [r["xL"][q]]
+        occ = any(CF.any_hit_brute_force(pts[j], pts[j + 1], v0, v1, v2, sph, eps) for j in range(k + 1))
+        assert occ == (r["status"][q] == 5), q
+        n_occ += occ
+    print(len(sel), n_occ)
+    assert len(sel) > 100 and n_occ > 5

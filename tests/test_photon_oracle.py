@@ -66,3 +66,52 @@ def test_photon_chains_satisfy_the_constraints(cfg):
         assert ok
         worst = max(worst, np.abs(Cv).max())
     assert worst < 1e-4, worst
+
+
+def _mirror_over_glass():
+    """A downward-facing plane mirror (conductor) at y = 5 over a horizontal glass
+    interface (eta 1.5 below) at y = 0, point light at (0, 4, 0): photons emitted
+    upwards hit the conductor first, then the dielectric."""
+    mirror = W.Surface(W.SURF_QUAD, W.MAT_CONDUCTOR, reflectance=1.0, origin=(-10.0, 5.0, -10.0),
+                       edge_u=(20.0, 0.0, 0.0), edge_v=(0.0, 0.0, 20.0))
+    glass = W.Surface(W.SURF_QUAD, W.MAT_DIELECTRIC, eta_in=1.5, eta_out=1.0, origin=(-10.0, 0.0, -10.0),
+                      edge_u=(0.0, 0.0, 20.0), edge_v=(20.0, 0.0, 0.0))
+    light = W.Light(W.LIGHT_POINT, 1.0, position=(0.0, 4.0, 0.0))
+    xD, nD = W.receiver_grid(-1.0, 1.0, 2, -1.0)
+    return W.Workload("mirror_over_glass", [mirror, glass], [light], xD, nD, 1, W.SeedSpec(W.SEED_CAP), W.WalkOpts())
+
+
+def test_photon_RT_choice_after_a_conductor_vertex_follows_fresnel():
+    """R33 / P:398: at every dielectric vertex a photon refracts with probability
+    1 - F (exact Fresnel), also when an earlier vertex was a conductor (the R/T
+    uniform of vertex v is word v&3 of draw (10, v>>2), whatever the materials).
+    Count of landed light-order chains (conductor R, dielectric T) = N E[1 - F(cos)]
+    over the upward emission directions that reach the glass, expectation by an
+    independent numpy Monte Carlo of the same geometry."""
+    w = _mirror_over_glass()
+    s = O.OracleScene(w)
+    n = 40000
+    rec, nv, verts, prims, surfs = s.trace_photons(n, (0, -1.0, 0), (0, 1, 0))
+    # type in x_D order: vertex 0 = the glass (T, bit 0), vertex 1 = the mirror (R): (1 << 2) - 2 + 0b01
+    got = int(((nv == 2) & (rec["type"] == (1 << 2) - 2 + 1)).sum())
+    rng = np.random.default_rng(123)
+    m = 2_000_000
+    z = rng.uniform(-1, 1, m)
+    ph = rng.uniform(0, 2 * np.pi, m)
+    st = np.sqrt(1 - z * z)
+    d = np.stack([st * np.cos(ph), z, st * np.sin(ph)], 1)
+    up = d[:, 1] > 0
+    t1 = (5.0 - 4.0) / np.where(up, d[:, 1], 1.0)
+    p1 = np.array([0.0, 4.0, 0.0]) + t1[:, None] * d                    # mirror hit
+    t2 = 5.0 / np.where(up, d[:, 1], 1.0)                               # down to y = 0 after reflection
+    p2 = p1 + t2[:, None] * d * np.array([1.0, -1.0, 1.0])
+    ok = up & (np.abs(p1[:, 0]) < 10) & (np.abs(p1[:, 2]) < 10) & (np.abs(p2[:, 0]) < 10) & (np.abs(p2[:, 2]) < 10)
+    cos = d[ok, 1]
+    sint = np.sqrt(1 - cos ** 2) / 1.5
+    ct = np.sqrt(1 - sint ** 2)
+    rs = (cos - 1.5 * ct) / (cos + 1.5 * ct)
+    rp = (1.5 * cos - ct) / (1.5 * cos + ct)
+    p_T = (1 - 0.5 * (rs ** 2 + rp ** 2)).sum() / m
+    exp = n * p_T
+    print(got, exp)
+    assert exp > 1000 and abs(got - exp) < 4 * np.sqrt(exp)

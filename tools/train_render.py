@@ -26,7 +26,7 @@ def main():
     for name, guide, frac, photons, kmax in runs:
         w = W.config4(guide=guide)
         iters, _ = mpg.training_schedule(budget, frac)
-        ds = mpg.DeviceScene(w, stree_capacity=max([1] + iters) * w.n_walks, stree_kappa_max=kmax)
+        ds = mpg.DeviceScene(w, stree_capacity=max([1] + iters) * w.n_walks, stree_kappa=(1.0 if kmax < 3e38 else 0.0, kmax))
         b = mpg.Batch(w.xD, w.nD, w.spp, w.seed.k)
         opts = ds.opts(flags=w.opts.flags | 8)
         mpg.run_train_render(ds, b, opts, 4, train_frac=frac, photons=photons)     # warm-up (allocations)
