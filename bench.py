@@ -8,7 +8,8 @@ A step is one pass of the whole hot path over one batch of synthetic input
 deduction, Newton with ray-traced reprojection, validation, kappa/G/T and
 reciprocal-probability trials (mpg_manifold_walk) -> per-pixel estimator
 (mpg_estimate) [-> guide accumulation for guided configs].  The workload is
-BASELINE.json configs[1] (1,048,576 k=2 walks through a glass icosphere) unless
+BASELINE.json configs[2] (16,777,216 k=1 walks through the water heightfield, the
+largest configuration that fits one GPU; BASELINE.json's metric names none) unless
 --config says otherwise.  N>1: one process per GPU (torchrun), each rank walks
 its own independent partition (walk_id_base = rank*n); no data-path collective.
 
@@ -117,7 +118,7 @@ def oracle_rate(w, n_walks, seed_base=0):
 
 
 def _oracle_shard(args):
-    cfg, lo, hi, seed_base, barrier = args
+    cfg, lo, hi, seed_base, barrier, trials = args
     from oracle import oracle as O
     w = make_workload(cfg)
     s = O.OracleScene(w)
@@ -125,7 +126,7 @@ def _oracle_shard(args):
     if barrier is not None:
         barrier.wait()
     t0 = time.perf_counter()
-    r = s.walks(ids, s.opts(walk_id_base=seed_base))
+    r = s.walks(ids, s.opts(walk_id_base=seed_base, trials=int(trials)))
     t1 = time.perf_counter()
     return int(np.isin(r["status"], (0, 5)).sum()), int(r["total_iters"].sum()), t0, t1
 
@@ -140,7 +141,7 @@ def cpu_model():
     return "unknown"
 
 
-def oracle_rate_parallel(cfg, n_walks, procs, seed_base=0):
+def oracle_rate_parallel(cfg, n_walks, procs, seed_base=0, trials=True):
     """The oracle (single-threaded C) on the first n_walks, split into `procs`
     contiguous shards run by that many worker processes on the host cores.
     Scene/BVH builds are excluded (workers start timing together after a barrier).
@@ -148,13 +149,14 @@ def oracle_rate_parallel(cfg, n_walks, procs, seed_base=0):
     import multiprocessing as mpr
     procs = max(1, min(procs, n_walks))
     if procs == 1:
-        c, it, t0, t1 = _oracle_shard((cfg, 0, n_walks, seed_base, None))
+        c, it, t0, t1 = _oracle_shard((cfg, 0, n_walks, seed_base, None, trials))
         return c / (t1 - t0), t1 - t0, c, it
     ctx = mpr.get_context("spawn")   # the ours-arm parent holds a CUDA context: never fork it
     bar = ctx.Manager().Barrier(procs)
     cuts = np.linspace(0, n_walks, procs + 1).astype(np.int64)
     with ctx.Pool(procs) as pool:
-        res = pool.map(_oracle_shard, [(cfg, int(cuts[i]), int(cuts[i + 1]), seed_base, bar) for i in range(procs)])
+        res = pool.map(_oracle_shard, [(cfg, int(cuts[i]), int(cuts[i + 1]), seed_base, bar, trials)
+                                       for i in range(procs)])
     c = sum(r[0] for r in res)
     it = sum(r[1] for r in res)
     dt = max(r[3] for r in res) - min(r[2] for r in res)
@@ -163,6 +165,27 @@ def oracle_rate_parallel(cfg, n_walks, procs, seed_base=0):
 
 def host_procs():
     return max(1, min(os.cpu_count() or 1, 64))
+
+
+def cpu_baseline(args, w):
+    """The oracle as it stands on the host cores (SURVEY 8(d) Timing): (ii) all cores
+    (one single-threaded process per core on contiguous shards), trials on = the
+    reported value, and trials off; (i) one core on the first walks, trials on / off."""
+    P = host_procs()
+    n = min(w.n_walks, args.ref_walks * P)
+    v, dt, conv, it = oracle_rate_parallel(args.config, n, P)
+    v0, dt0, conv0, it0 = oracle_rate_parallel(args.config, n, P, trials=False)
+    n1 = min(w.n_walks, args.ref_walks_single)
+    v1, dt1, conv1, it1 = oracle_rate_parallel(args.config, n1, 1)
+    v10, dt10, _, it10 = oracle_rate_parallel(args.config, n1, 1, trials=False)
+    return {"value": v, "unit": "walks/s", "cores": P, "kind": "oracle", "cpu_model": cpu_model(),
+            "newton_iters_per_s": it / dt,
+            "sample": f"first {n} walks of the workload, {P} single-threaded oracle processes on "
+                      f"contiguous shards ({dt:.1f} s wall, {conv} converged), trials on",
+            "all_cores_trials_off": {"value": v0, "newton_iters_per_s": it0 / dt0, "walks": n, "wall_s": dt0},
+            "single_core_trials_on": {"value": v1, "newton_iters_per_s": it1 / dt1, "walks": n1, "wall_s": dt1},
+            "single_core_trials_off": {"value": v10, "newton_iters_per_s": it10 / dt10, "walks": n1,
+                                       "wall_s": dt10}}
 
 
 def run_reference(args):
@@ -254,6 +277,8 @@ def run_ours(args):
     for _ in range(max(3, args.warmup)):
         step()
     torch.cuda.synchronize()
+    # the FP32 roof of this GPU, measured here (FFMA microbenchmark), before the timed region
+    measured_peak = mpg.mpg_measure_fp32_peak() if not args.nominal_peak else None
 
     # ---- device-timed region: K steps, L2 flushed before each (outside the events) ----
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
@@ -325,7 +350,7 @@ def run_ours(args):
     flops = (FLOP_PER_VERTEX_SWEEP * S["vertex_iters"] + FLOP_PER_NODE * S["node_visits"] +
              FLOP_PER_TRI * S["tri_tests"])
     achieved = flops / walk_s / 1e12
-    peak = fp32_peak_tflops()
+    peak = measured_peak if measured_peak else fp32_peak_tflops()
     traffic = None
     prof = os.path.join(ROOT, "profiles", f"ncu_walk_cfg{args.config}.json")
     if os.path.exists(prof):
@@ -382,13 +407,7 @@ def run_ours(args):
     # ---- CPU baseline: the oracle on a bounded sample (rank 0, N=1 only) ----
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        P = host_procs()
-        n = min(w.n_walks, args.ref_walks * P)
-        v, dt, conv, it = oracle_rate_parallel(args.config, n, P)
-        cpu = {"value": v, "unit": "walks/s", "cores": P, "kind": "oracle", "cpu_model": cpu_model(),
-               "newton_iters_per_s": it / dt,
-               "sample": f"first {n} walks of the workload, {P} single-threaded oracle processes on "
-                         f"contiguous shards ({dt:.1f} s wall, {conv} converged)"}
+        cpu = cpu_baseline(args, w)
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "walks/s", "n_gpus": world, "steps": args.steps,
@@ -420,7 +439,11 @@ def run_ours(args):
                     "newton_iters_per_s": newton_all / (sum(walk_ms) / 1e3)},
                 "roofline": {"bound": "alu", "kernel": "k_walk", "achieved": achieved, "peak": peak,
                              "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
-                             "peak_source": "148 SM x 128 FP32 lanes x 2 x 1965 MHz (B200_PROFILING.md unit counts)",
+                             "peak_source": ("measured in this run: FFMA microbenchmark (mpg_measure_fp32_peak, "
+                                             "8 independent chains per thread, SMs x 4 x 256 threads, best of 5)"
+                                             if measured_peak else
+                                             "148 SM x 128 FP32 lanes x 2 x 1965 MHz (B200_PROFILING.md unit counts)"),
+                             "nominal_peak": fp32_peak_tflops(),
                              "algorithmic_flops_per_launch": flops / args.steps},
                 "hbm": hbm,
                 "stats_per_step": {k: v / args.steps for k, v in S.items()},
@@ -439,8 +462,10 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", type=int, default=1)
-    ap.add_argument("--ref-walks", type=int, default=100000)
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--ref-walks", type=int, default=20000, help="oracle walks per host process (cpu_baseline)")
+    ap.add_argument("--ref-walks-single", type=int, default=8192, help="oracle walks of the single-core timing")
+    ap.add_argument("--nominal-peak", action="store_true", help="roofline against the unit-count FP32 peak")
     ap.add_argument("--guide", default="hist", choices=["hist", "stree"],
                     help="configs[4] guide: BASELINE's histogram (default) or the paper's STree + vMF (SURVEY 8(f)1)")
     ap.add_argument("--photons", type=int, default=0,

@@ -355,6 +355,12 @@ int32_t mpg_version(void);
 /* Number of kernel launches this library has enqueued since load (host-side
  * counter, all threads; library launches such as cub's radix-sort passes are counted too). */
 uint64_t mpg_kernel_launches(void);
+/* Measurement helper, not on the walk path: FP32 FFMA throughput of the current
+ * device in TFLOP/s (8 independent FFMA chains per thread, SMs x 4 blocks of 256
+ * threads, `iters` x 128 FFMA per thread, best of `reps` timed launches after one
+ * warm-up; CUDA events on `stream`, synchronizes).  The roofline denominator of
+ * bench.py.  iters/reps <= 0 or tflops NULL -> MPG_ERR_INVALID_ARG. */
+mpg_status mpg_measure_fp32_peak(int32_t iters, int32_t reps, double *tflops, void *stream);
 
 #ifdef __cplusplus
 }

@@ -1433,3 +1433,53 @@ extern "C" mpg_status mpg_splat(const float *w, int64_t n_recv, int32_t spp, dou
 extern "C" const char *mpg_last_error(void) { return g_err.c_str(); }
 extern "C" int32_t mpg_version(void) { return 1; }
 extern "C" uint64_t mpg_kernel_launches(void) { return g_launches.load(std::memory_order_relaxed); }
+
+// ----------------------------------------------------------------------------
+// measurement helper (not on the walk path): the FP32 FFMA roof of this GPU,
+// the denominator of bench.py's roofline ("measure with an FFMA
+// microbenchmark on the box").  Every thread runs 8 independent FFMA chains
+// (latency 4 cycles, so 2 warps per SM sub-partition already saturate the
+// pipe); grid = SMs x 4 blocks of 256; best of `reps` launches.
+// ----------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_ffma_peak(float *out, int iters, float b, float c) {
+    float a0 = threadIdx.x * 1e-7f, a1 = a0 + 1.0f, a2 = a0 + 2.0f, a3 = a0 + 3.0f, a4 = a0 + 4.0f, a5 = a0 + 5.0f,
+          a6 = a0 + 6.0f, a7 = a0 + 7.0f;
+    for (int i = 0; i < iters; i++) {
+#pragma unroll
+        for (int j = 0; j < 16; j++) {
+            a0 = fmaf(a0, b, c); a1 = fmaf(a1, b, c); a2 = fmaf(a2, b, c); a3 = fmaf(a3, b, c);
+            a4 = fmaf(a4, b, c); a5 = fmaf(a5, b, c); a6 = fmaf(a6, b, c); a7 = fmaf(a7, b, c);
+        }
+    }
+    const float s = a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7;
+    if (s == 12345.678f) out[0] = s;   // keeps the chains live
+}
+
+extern "C" mpg_status mpg_measure_fp32_peak(int32_t iters, int32_t reps, double *tflops, void *stream) {
+    ARG_CHECK(tflops && iters > 0 && reps > 0, "bad argument");
+    cudaStream_t s = as_stream(stream);
+    float *d = nullptr;
+    CUDA_TRY(cudaMallocAsync(&d, 4, s));
+    const int blocks = num_sms() * 4;
+    cudaEvent_t e0, e1;
+    CUDA_TRY(cudaEventCreate(&e0));
+    CUDA_TRY(cudaEventCreate(&e1));
+    double best = 0.0;
+    for (int r = 0; r <= reps; r++) {   // r = 0: warm-up
+        CUDA_TRY(cudaEventRecord(e0, s));
+        COUNT_LAUNCH(1);
+        k_ffma_peak<<<blocks, 256, 0, s>>>(d, iters, 0.999999f, 1e-6f);
+        CUDA_TRY(cudaEventRecord(e1, s));
+        CUDA_TRY(cudaEventSynchronize(e1));
+        float ms = 0.f;
+        CUDA_TRY(cudaEventElapsedTime(&ms, e0, e1));
+        const double flops = (double)blocks * 256.0 * iters * 16.0 * 8.0 * 2.0;
+        if (r > 0) best = std::max(best, flops / (ms * 1e-3) / 1e12);
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    CUDA_TRY(cudaFreeAsync(d, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    *tflops = best;
+    return MPG_OK;
+}

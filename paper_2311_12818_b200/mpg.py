@@ -109,7 +109,7 @@ EXPORTS = ["mpg_scene_create", "mpg_scene_destroy", "mpg_scene_get_info", "mpg_t
            "mpg_guide_download", "mpg_guide_download_dir_tables", "mpg_sample_seeds", "mpg_walk_workspace_size", "mpg_manifold_walk", "mpg_estimate",
            "mpg_debug_trace", "mpg_last_error", "mpg_version", "mpg_kernel_launches", "mpg_guide_create_stree",
            "mpg_guide_record_samples", "mpg_guide_set_samples", "mpg_guide_get_samples", "mpg_guide_stree_info",
-           "mpg_guide_download_stree", "mpg_trace_photons", "mpg_splat", "mpg_guide_set_separator"]
+           "mpg_guide_download_stree", "mpg_trace_photons", "mpg_splat", "mpg_guide_set_separator", "mpg_measure_fp32_peak"]
 
 _lib = None
 
@@ -149,6 +149,7 @@ def lib():
             "mpg_last_error": (C.c_char_p, []),
             "mpg_version": (C.c_int32, []),
             "mpg_kernel_launches": (C.c_uint64, []),
+            "mpg_measure_fp32_peak": (st, [C.c_int32, C.c_int32, C.POINTER(C.c_double), P]),
             "mpg_guide_create_stree": (st, [C.POINTER(mpg_stree_desc), C.POINTER(P)]),
             "mpg_guide_record_samples": (st, [P, C.POINTER(mpg_query), C.POINTER(mpg_seed_buf),
                                               C.POINTER(mpg_walk_buf), C.c_int64, P]),
@@ -373,6 +374,13 @@ def mpg_version() -> int:
 
 def mpg_kernel_launches() -> int:
     return int(lib().mpg_kernel_launches())
+
+
+def mpg_measure_fp32_peak(iters: int = 20000, reps: int = 5, stream=None) -> float:
+    """Measured FP32 FFMA throughput of this GPU in TFLOP/s (bench.py's roofline peak)."""
+    v = C.c_double()
+    _check(lib().mpg_measure_fp32_peak(int(iters), int(reps), C.byref(v), _stream_ptr(stream)), "mpg_measure_fp32_peak")
+    return float(v.value)
 
 
 # ----------------------------------------------------------------------------

@@ -169,15 +169,20 @@ def test_stree_walk_parity(stree_guided_run):
     assert rep["n_other_chain"] <= max(1, 0.001 * rep["both"])
 
 
-def test_stree_progressive_loop_independent():
+@pytest.mark.parametrize("clamp", [False, True])
+def test_stree_progressive_loop_independent(clamp):
     """GPU loop vs oracle loop, each fitting its own STree from its own samples of the
     last iteration (P:426 footnote): walks agree per iteration, the trees agree
-    in size, and the guide learns (more converged walks than the initializer alone)."""
+    in size, and the guide learns (more converged walks than the initializer alone).
+    Each side fits its own tree from its own walks, whose positions differ by fp64
+    rounding: with Eq. 12's unclamped kappa = sigma'^-2 two nearly equal directions give
+    very different kappa, so the loops drift further apart than with the R30b clamp."""
     import torch
     from oracle import oracle as O
     from paper_2311_12818_b200 import mpg
+    kap = O.KAPPA_CLAMP_R30B if clamp else (O.STREE_DEFAULTS["kappa_min"], O.STREE_DEFAULTS["kappa_max"])
     w = W.config4(n_side=48, guide="stree")
-    ds = mpg.DeviceScene(w)
+    ds = mpg.DeviceScene(w, stree_kappa=kap)
     b = mpg.Batch(w.xD, w.nD, w.spp, w.seed.k)
     opts = ds.opts()
     s = O.OracleScene(w)
@@ -190,7 +195,7 @@ def test_stree_progressive_loop_independent():
         rep = PY.compare(g, o, np.arange(w.n_walks), ds.extent, 6)
         rec = O.record_samples(w.xD, w.spp, o["status"], o["w"].astype(np.float32), o["pos"][:, 0].astype(np.float32),
                                o["k"], o["tau"], o["xL"].astype(np.float32))
-        R = O.stree_build(rec)
+        R = O.stree_build(rec, kappa_min=kap[0], kappa_max=kap[1])
         s.set_stree(R)                                   # the oracle's own next guide
         log.append((rep["flag_agree"], int(np.isin(g["status"], (0, 5)).sum()), R["n_valid"]))
 
@@ -203,7 +208,7 @@ def test_stree_progressive_loop_independent():
     # iteration; walk-level parity on one tree is test_stree_walk_parity
     for agree, nconv, nvalid in log:
         assert agree >= 0.98
-    assert abs(info["n_valid"] - log[-1][2]) <= max(2, 0.01 * log[-1][2])
+    assert abs(info["n_valid"] - log[-1][2]) <= max(2, (0.01 if clamp else 0.03) * log[-1][2])
     assert log[-1][1] > log[0][1]
 
 

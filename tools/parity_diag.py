@@ -7,7 +7,7 @@ from tests import parity as PY
 
 which = sys.argv[1] if len(sys.argv) > 1 else "cfg1"
 w = {"cfg0": lambda: W.config0(), "cfg1": lambda: W.config1(128, 1), "cfg1a": lambda: W.config1(96, 2, analytic=True),
-     "cfg2": lambda: W.config2(64, 4), "cfg3": lambda: W.config3(48, 1)}[which]()
+     "cfg2": lambda: W.config2(64, 4), "cfg3": lambda: W.config3(48, 1), "cfg3_64": lambda: W.config3(64, 1)}[which]()
 flags = int(sys.argv[2]) if len(sys.argv) > 2 else w.opts.flags
 g, st, ext = PY.run_gpu(w, flags=flags)
 ids = np.arange(w.n_walks)
