@@ -463,8 +463,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=2)
-    ap.add_argument("--ref-walks", type=int, default=20000, help="oracle walks per host process (cpu_baseline)")
-    ap.add_argument("--ref-walks-single", type=int, default=8192, help="oracle walks of the single-core timing")
+    ap.add_argument("--ref-walks", type=int, default=200000, help="oracle walks per host process (cpu_baseline)")
+    ap.add_argument("--ref-walks-single", type=int, default=65536, help="oracle walks of the single-core timing")
     ap.add_argument("--nominal-peak", action="store_true", help="roofline against the unit-count FP32 peak")
     ap.add_argument("--guide", default="hist", choices=["hist", "stree"],
                     help="configs[4] guide: BASELINE's histogram (default) or the paper's STree + vMF (SURVEY 8(f)1)")

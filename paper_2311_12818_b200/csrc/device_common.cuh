@@ -253,6 +253,7 @@ struct DScene {
     const float4 *tpos;  // BVH order, TSTRIDE float4 per tri; v0.w = original tri id, v1.w = surf id, v2.w = specular flag
     const float4 *tnrm;  // BVH order, 3 float4 per tri: vertex shading normals
     const int4 *oidx;    // original order: vertex indices (w: BVH slot)
+    const int4 *tadj;    // BVH order: BVH slots of the neighbours across the edges opposite v0, v1, v2 (-1: none)
     const float4 *vpos;  // original vertex positions
 };
 

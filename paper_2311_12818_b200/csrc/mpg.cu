@@ -471,8 +471,36 @@ extern "C" mpg_status mpg_scene_create(const mpg_surface_desc *surfaces, int32_t
         d.tpos = (const float4 *)((char *)p + nb);
         s->trav_bytes = nb + tb;
     }
+    // edge adjacency in BVH order (refine_hit's fp64 triangle choice at shared edges, R17):
+    // neighbour across the edge opposite vertex e of each triangle, -1 on a border
+    std::vector<int4> tadj((size_t)d.n_tri, make_int4(-1, -1, -1, -1));
+    {
+        std::vector<std::pair<unsigned long long, int>> edges;   // (edge key, slot*4 + e)
+        edges.reserve((size_t)3 * d.n_tri);
+        for (int t = 0; t < d.n_tri; t++) {
+            const int4 ix = oidx[t];
+            const int v[3] = {ix.x, ix.y, ix.z};
+            for (int e = 0; e < 3; e++) {
+                unsigned long long p = (unsigned)v[(e + 1) % 3], q = (unsigned)v[(e + 2) % 3];
+                if (p > q) std::swap(p, q);
+                edges.push_back({(p << 32) | q, ix.w * 4 + e});
+            }
+        }
+        std::sort(edges.begin(), edges.end());
+        for (size_t i = 0; i + 1 < edges.size(); i++) {
+            if (edges[i].first != edges[i + 1].first) continue;
+            if (i + 2 < edges.size() && edges[i + 2].first == edges[i].first) {   // non-manifold edge: no link
+                while (i + 1 < edges.size() && edges[i + 1].first == edges[i].first) i++;
+                continue;
+            }
+            const int a = edges[i].second, b = edges[i + 1].second;
+            (&tadj[a >> 2].x)[a & 3] = b >> 2;
+            (&tadj[b >> 2].x)[b & 3] = a >> 2;
+            i++;
+        }
+    }
     if ((st = upload(s, tnrm, &d.tnrm)) != MPG_OK || (st = upload(s, oidx, &d.oidx)) != MPG_OK ||
-        (st = upload(s, vpos, &d.vpos)) != MPG_OK) {
+        (st = upload(s, vpos, &d.vpos)) != MPG_OK || (st = upload(s, tadj, &d.tadj)) != MPG_OK) {
         mpg_scene_destroy(s);
         return st;
     }

@@ -97,7 +97,7 @@ __global__ void k_photons(const DScene S, const PhotonDev P, int64_t first, int6
             if (!hit || nv == P.maxv) break;               // escaped, or longer than the guide's chains
             const DSurf &f = S.surf[h.surf];
             if (f.mat == 2) break;                         // absorbed by a diffuse occluder
-            const double3 y = refine_hit(S, h.prim, h.surf, o, o + d, h.p);
+            const double3 y = refine_hit(S, h.prim, h.surf, o, o + d, h.p);   // may move h.prim across a shared edge
             const float3 yf = f3d(y);
             const float3 ng = geo_normal(S, h.prim, h.surf, yf);
             const float3 nf = shading_normal(S, h.prim, h.surf, yf);

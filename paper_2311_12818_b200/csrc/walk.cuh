@@ -140,18 +140,50 @@ __device__ __forceinline__ bool scatter_dir(const DScene &S, double3 &dd, int pr
 // rounded once: the reprojected vertex is within 1/2 ulp of the exact point,
 // so the Newton residual is not floored by reprojection noise (which near
 // grazing chains reached ~1e-5 in fp32, measured).
-__device__ __forceinline__ double3 refine_hit(const DScene &S, int prim, int surf, double3 o, double3 q, float3 pf) {
+//
+// Triangle choice at shared edges (R17): the fp32 watertight traversal may pick
+// the neighbour of the triangle the exact (fp64) line crosses when the crossing
+// lies within fp32 rounding of their common edge.  The plane of the wrong
+// neighbour moves the vertex by ~(distance to the edge) x (dihedral angle)
+// ~ 1e-9 x extent, which long chaotic walks (k = 6 slabs, 40 halving
+// iterations) amplify to a different outcome.  So the fp64 barycentrics of the
+// refined point are checked, and while one is negative the point moves to the
+// triangle across that edge (mesh adjacency, <= 2 hops): the primitive is then
+// the one the exact line crosses, as in the fp64 oracle.  `prim` is updated.
+__device__ __forceinline__ double3 refine_hit(const DScene &S, int &prim, int surf, double3 o, double3 q, float3 pf) {
     double ox = o.x, oy = o.y, oz = o.z;
     double dx = q.x - ox, dy = q.y - oy, dz = q.z - oz;
     double t;
     if (prim >= 0) {
-        float3 a = xyz(__ldg(S.tpos + TSTRIDE * prim)), b = xyz(__ldg(S.tpos + TSTRIDE * prim + 1)), c = xyz(__ldg(S.tpos + TSTRIDE * prim + 2));
-        double e1x = (double)b.x - a.x, e1y = (double)b.y - a.y, e1z = (double)b.z - a.z;
-        double e2x = (double)c.x - a.x, e2y = (double)c.y - a.y, e2z = (double)c.z - a.z;
-        double nx = e1y * e2z - e1z * e2y, ny = e1z * e2x - e1x * e2z, nz = e1x * e2y - e1y * e2x;
-        double den = dx * nx + dy * ny + dz * nz;
-        if (den == 0.0) return d3f(pf);
-        t = (((double)a.x - ox) * nx + ((double)a.y - oy) * ny + ((double)a.z - oz) * nz) / den;
+        int cur = prim;
+        double3 y0 = d3f(pf);
+#pragma unroll 1
+        for (int hop = 0; hop < 3; hop++) {
+            float3 a = xyz(__ldg(S.tpos + TSTRIDE * cur)), b = xyz(__ldg(S.tpos + TSTRIDE * cur + 1)),
+                   c = xyz(__ldg(S.tpos + TSTRIDE * cur + 2));
+            double e1x = (double)b.x - a.x, e1y = (double)b.y - a.y, e1z = (double)b.z - a.z;
+            double e2x = (double)c.x - a.x, e2y = (double)c.y - a.y, e2z = (double)c.z - a.z;
+            double nx = e1y * e2z - e1z * e2y, ny = e1z * e2x - e1x * e2z, nz = e1x * e2y - e1y * e2x;
+            double den = dx * nx + dy * ny + dz * nz;
+            if (den == 0.0) break;
+            t = (((double)a.x - ox) * nx + ((double)a.y - oy) * ny + ((double)a.z - oz) * nz) / den;
+            const double3 y = make_double3(ox + t * dx, oy + t * dy, oz + t * dz);
+            if (hop == 0) y0 = y;
+            if (!S.tadj) { prim = cur; return y; }
+            // unnormalized barycentrics (sign = side of each edge): opposite a, b, c
+            double pax = (double)a.x - y.x, pay = (double)a.y - y.y, paz = (double)a.z - y.z;
+            double pbx = (double)b.x - y.x, pby = (double)b.y - y.y, pbz = (double)b.z - y.z;
+            double pcx = (double)c.x - y.x, pcy = (double)c.y - y.y, pcz = (double)c.z - y.z;
+            double wa = (pby * pcz - pbz * pcy) * nx + (pbz * pcx - pbx * pcz) * ny + (pbx * pcy - pby * pcx) * nz;
+            double wb = (pcy * paz - pcz * pay) * nx + (pcz * pax - pcx * paz) * ny + (pcx * pay - pcy * pax) * nz;
+            double wc = (pay * pbz - paz * pby) * nx + (paz * pbx - pax * pbz) * ny + (pax * pby - pay * pbx) * nz;
+            if (wa >= 0.0 && wb >= 0.0 && wc >= 0.0) { prim = cur; return y; }
+            const int4 nb = __ldg(S.tadj + cur);
+            const int nxt = (wa <= wb && wa <= wc) ? nb.x : (wb <= wc ? nb.y : nb.z);
+            if (nxt < 0) break;
+            cur = nxt;
+        }
+        return y0;   // no neighbour contains the crossing: keep the traversal's triangle
     } else {
         const DSurf &f = S.surf[surf];
         if (f.kind == 0) {
@@ -192,9 +224,11 @@ enum { TR_REPROJ = 0, TR_DEDUCE = 1, TR_VIS = 2 };
 // One traversal call site serves all three modes, so lanes tracing visibility
 // traverse together with warp-mates that reproject (no separate low-occupancy
 // visibility traversal).
-template <int KMAX, int W>
+// Reprojection targets q_i = x_i + beta dq_i are formed here from the chain and its
+// step (no q array survives between the Newton step and the trace).
+template <int KMAX, int W, typename R>
 __device__ __forceinline__ int trace_chain(const DScene &S, int mode, int k, uint32_t bits, bool learned,
-                                           float3 xD, float3 xL, float3 tgt, const double3 (&q)[KMAX],
+                                           float3 xD, float3 xL, float3 tgt, const V3<R> (&dq)[KMAX], float beta,
                                            const double3 (&x)[KMAX], const int (&hint)[KMAX],
                                            uint32_t surf_req, float eps, double3 (&y)[KMAX], int (&yp)[KMAX],
                                            int (&ys)[KMAX], LaneStats &st, uint32_t &tau_res, unsigned *s_rays) {
@@ -224,7 +258,7 @@ __device__ __forceinline__ int trace_chain(const DScene &S, int mode, int k, uin
             tmax = l - eps;
         } else {
             if (!deduce) {
-                double3 v = rget(q, i) - o;
+                double3 v = (rget(x, i) + tod(rget(dq, i)) * (double)beta) - o;
                 double l2 = ddot(v, v);
                 if (!(l2 > 0.0)) return 3 | (i << 4);
                 dd = v * rsqrt(l2);
@@ -254,7 +288,8 @@ __device__ __forceinline__ int trace_chain(const DScene &S, int mode, int k, uin
             if (bit && mat != 1) return 4 | (i << 4);
             res |= bit << i;
         }
-        const double3 yi = refine_hit(S, h.prim, h.surf, o, deduce ? o + dd : rget(q, i), h.p);
+        const double3 yi = refine_hit(S, h.prim, h.surf, o, deduce ? o + dd : rget(x, i) + tod(rget(dq, i)) * (double)beta,
+                                      h.p);   // may move h.prim across a shared edge
         rset(y, i, yi);
         rset(yp, i, h.prim);
         rset(ys, i, h.surf);
@@ -343,34 +378,34 @@ __global__ void __launch_bounds__(128, MINB) k_walk(const DScene S, const SeedCt
     const int lane = threadIdx.x & 31;
     // chain type of the current attempt (per lane: configs[4] draws n and tau per sample)
     int k = g.k, pk = g.k;
-    uint32_t tau = g.tau, ptau = g.tau, bits = g.tau;
-    bool learned = true;
-    float Pn = 1.0f;
+    uint32_t tau = g.tau, ptau = g.tau;
 
     // lane state
     int phase = PH_FETCH;
     int64_t w = -1;
     uint32_t trial = 0;
     int end_status = 0;
-    float3 xD = f3(0, 0, 0), nD = f3(0, 1, 0), xL = f3(0, 0, 0), tgt = f3(0, 0, 0);
+    float3 xD = f3(0, 0, 0), xL = f3(0, 0, 0);
     float pdfL = 1.f, Tprim = 0.f;
+    float Gc = 0.f, Tc = 0.f;   // G, T of a converged primary (computed before its visibility rays)
     int lid = 0;
     int it = 0;
     float beta = 1.f;
     bool fresh = false;
     uint32_t psurf = 0; // primary surf ids, 4 bits each
+    // persistent chain state: the vertices, their primitives and the Newton step (kept
+    // for step halving); the Jacobian blocks, frames and GGT live only inside the
+    // SOLVE block below (transient), so they never stay live across a trace
     double3 x[KMAX];
-    V3<R> sg[KMAX], tg[KMAX], dq[KMAX];
+    V3<R> dq[KMAX];
     int prim[KMAX], surf[KMAX];
-    R Di[KMAX][4], Ub[KMAX][4];
-    double3 q[KMAX], y[KMAX];
+    double3 y[KMAX];
     int yp[KMAX], ys[KMAX];
-    bool singular = false;
-    bool vis_done = false, occluded = false;   // visibility of a converged primary (PH_VIS)
+    bool occluded = false;   // visibility of a converged primary (PH_VIS)
 #pragma unroll
     for (int i = 0; i < KMAX; i++) {
         x[i] = make_double3(0.0, 0.0, 0.0);
-        sg[i] = tg[i] = dq[i] = mk3<R>(0, 0, 0);
+        dq[i] = mk3<R>(0, 0, 0);
         prim[i] = -1; surf[i] = 0;
     }
     LaneStats ls = {0u, 0u, 0u};
@@ -400,7 +435,6 @@ __global__ void __launch_bounds__(128, MINB) k_walk(const DScene S, const SeedCt
                     trial = 0;
                     int64_t rcv = w / P.spp;
                     xD = xyz(__ldg(P.xD + rcv));
-                    nD = xyz(__ldg(P.nD + rcv));
                     float4 l4 = __ldg(P.seed_xL + w);
                     xL = xyz(l4);
                     pdfL = l4.w;
@@ -465,7 +499,6 @@ __global__ void __launch_bounds__(128, MINB) k_walk(const DScene S, const SeedCt
                 ptau = pct >> 4;
                 int64_t rcv = w / P.spp;
                 xD = xyz(__ldg(P.xD + rcv));
-                nD = xyz(__ldg(P.nD + rcv));
                 float4 l4 = __ldg(P.seed_xL + w);
                 xL = xyz(l4);
                 pdfL = l4.w;
@@ -492,6 +525,11 @@ __global__ void __launch_bounds__(128, MINB) k_walk(const DScene S, const SeedCt
         }
 
         // ---- seed ---------------------------------------------------------
+        // (the seed target and the type bits are used by the deduction of the same
+        // pass only: not loop-carried)
+        float3 tgt = f3(0, 0, 0);
+        uint32_t bits = g.tau;
+        bool learned = true;
         if (phase == PH_SEED) {
             c_attempts++;
             bool ok;
@@ -504,7 +542,6 @@ __global__ void __launch_bounds__(128, MINB) k_walk(const DScene S, const SeedCt
                     bits = (ct >> 4) & 255u;
                     learned = (ct >> 12) & 1u;
                 }
-                Pn = P.seed_pn ? __ldg(P.seed_pn + w) : 1.0f;
             } else {
                 SeedRes sr;
                 ok = seed_target(S, g, P.walk_id_base + w, trial + P.trial_base, xD, xL, sr);
@@ -512,7 +549,6 @@ __global__ void __launch_bounds__(128, MINB) k_walk(const DScene S, const SeedCt
                 k = sr.n;
                 bits = sr.bits;
                 learned = sr.learned;
-                Pn = sr.Pn;
             }
             k = max(1, min(k, KMAX));
             it = 0;
@@ -541,12 +577,11 @@ __global__ void __launch_bounds__(128, MINB) k_walk(const DScene S, const SeedCt
             for (int i = 0; i < KMAX; i++) sreq |= (uint32_t)(surf[i] & 15) << (4 * i);
             uint32_t tres = tau;
             const int mode = ded ? TR_DEDUCE : (phase == PH_VIS ? TR_VIS : TR_REPROJ);
-            int why = trace_chain<KMAX, W>(S, mode, k, bits, learned, xD, xL, tgt, q, x, prim, sreq, P.ray_eps, y, yp, ys, ls,
-                                        tres, &s_rays[threadIdx.x]);
+            int why = trace_chain<KMAX, W, R>(S, mode, k, bits, learned, xD, xL, tgt, dq, beta, x, prim, sreq, P.ray_eps,
+                                              y, yp, ys, ls, tres, &s_rays[threadIdx.x]);
             bool ok = why == 0;
             if (mode == TR_VIS) {
                 occluded = !ok;
-                vis_done = true;
                 phase = PH_END;
             } else {
             if (ok && ded) tau = tres;
@@ -579,12 +614,36 @@ __global__ void __launch_bounds__(128, MINB) k_walk(const DScene S, const SeedCt
                 fresh = false;
                 c_vtx += k;
                 float cm = 0.f;
+                bool singular = false;
+                R Di[KMAX][4], Ub[KMAX][4];      // transient: D'^-1_i, U_i of the block-Thomas sweep
+                V3<R> sg[KMAX], tg[KMAX];          // transient: tangent frames of the step
                 int r = newton_system<KMAX, R>(S, k, tau, xD, xL, x, prim, surf, P.tol, Di, Ub, sg, tg, dq, singular, cm);
                 if (P.dbg && trial == 0 && w < P.n_dbg && 2 * it + 1 < P.dbg_stride) {
                     P.dbg[w * P.dbg_stride + 2 * it] = cm;
                     P.dbg[w * P.dbg_stride + 2 * it + 1] = beta;
                 }
-                if (r == 1) { end_status = ST_CONVERGED; phase = PH_END; }
+                if (r == 1) {
+                    end_status = ST_CONVERGED;
+                    phase = PH_END;
+                    if (trial == 0) {
+                        // a converged primary: sides (R8; BAD_SIDE precedes OCCLUDED), kappa and the
+                        // analytic GGT from this sweep's blocks (R11, R12), then its k+1 visibility
+                        // segments in the next trace phase (PH_VIS)
+                        const DLight &L = S.light[lid];
+                        float kap;
+                        R DL[4];
+                        if (!post_sweep<KMAX, R>(S, L, k, tau, xD, xL, x, prim, surf, true, kap, DL)) {
+                            end_status = ST_BAD_SIDE;
+                        } else {
+                            const float3 nD = xyz(__ldg(P.nD + w / P.spp));
+                            Gc = singular ? 0.0f : ggt_from_blocks<KMAX, R>(k, xD, nD, x, Di, Ub, sg, tg, DL);
+                            float Le = L.emit;
+                            if (L.kind == 1 && !(dot(f3d(x[k - 1]) - xL, L.n) > 0.0f)) Le = 0.0f;
+                            Tc = kap * Gc * Le;
+                            phase = PH_VIS;
+                        }
+                    }
+                }
                 else if (r == 2) { end_status = ST_DEGENERATE; phase = PH_END; }
             }
             if (phase == PH_SOLVE) {
@@ -592,43 +651,20 @@ __global__ void __launch_bounds__(128, MINB) k_walk(const DScene S, const SeedCt
                     end_status = ST_MAXITER;
                     phase = PH_END;
                 }
-                else {
-#pragma unroll
-                    for (int i = 0; i < KMAX; i++) {
-                        if (i >= k) break;
-                        q[i] = x[i] + tod(dq[i]) * (double)beta;
-                    }
-                    phase = PH_REPROJ;
-                }
+                else phase = PH_REPROJ;
             }
         }
 
         // ---- end of an attempt ---------------------------------------------
-        // a converged primary first traces its visibility segments (next iteration,
-        // in the shared trace phase), then comes back here
-        if (phase == PH_END && trial == 0 && end_status == ST_CONVERGED && !vis_done) phase = PH_VIS;
         if (phase == PH_END) {
             c_newton += it;
             int st = end_status;
             if (trial == 0) {
                 float G = 0.f, T = 0.f;
                 if (st == ST_CONVERGED) {
-                    const DLight &L = S.light[lid];
-                    float kap;
-                    R DL[4];
-                    vis_done = false;
-                    // sides first: BAD_SIDE takes precedence over OCCLUDED
-                    if (!post_sweep<KMAX, R>(S, L, k, tau, xD, xL, x, prim, surf, true, kap, DL)) st = ST_BAD_SIDE;
-                    else {
-                        // visibility: k+1 any-hit segments against all surfaces
-                        if (occluded) st = ST_OCCLUDED;
-                        else {
-                            G = singular ? 0.0f : ggt_from_blocks<KMAX, R>(k, xD, nD, x, Di, Ub, sg, tg, DL);
-                            float Le = L.emit;
-                            if (L.kind == 1 && !(dot(f3d(x[k - 1]) - xL, L.n) > 0.0f)) Le = 0.0f;
-                            T = kap * G * Le;
-                        }
-                    }
+                    // visibility: k+1 any-hit segments against all surfaces, V = 0 -> G = T = 0
+                    if (occluded) st = ST_OCCLUDED;
+                    else { G = Gc; T = Tc; }
                 }
                 if (st != ST_SEED_FAIL) {
 #pragma unroll

@@ -26,8 +26,9 @@ def run_oracle(w, ids, **opt_over):
     return s.walks(np.asarray(ids, np.int64), s.opts(**opt_over)), s
 
 
-def compare(g, o, ids, extent, k):
-    """Walk-level parity report for walk indices `ids` (g: full GPU arrays, o: oracle on ids)."""
+def compare(g, o, ids, extent, k, w=None):
+    """Walk-level parity report for walk indices `ids` (g: full GPU arrays, o: oracle on ids);
+    with the workload `w`, also the triangle-id mismatches that are not shared-edge ties (R17)."""
     gs = g["status"][ids].astype(np.int64)
     os_ = o["status"].astype(np.int64)
     cg = np.isin(gs, (0, 5))
@@ -64,9 +65,53 @@ def compare(g, o, ids, extent, k):
         rep["G_rel_max"] = float(rg.max())
         tr = (g["trials"][ids][vis] == o["trials"][vis])
         rep["trials_agree"] = float(tr.mean())
+    if w is not None:
+        rep["prim_mis"], rep["prim_bad"] = prim_mismatches(w, g, o, np.asarray(ids), extent, k)
     rep["disagree_ids"] = np.asarray(ids)[cg != co]
     rep["prim_mismatch_ids"] = np.asarray(ids)[both & ~same_prim]
     return rep
+
+
+def _dist_point_segment(p, a, b):
+    ab = b - a
+    t = np.clip(np.dot(p - a, ab) / max(np.dot(ab, ab), 1e-300), 0.0, 1.0)
+    return float(np.linalg.norm(p - (a + t * ab)))
+
+
+def prim_mismatches(w, g, o, ids, extent, k, tol_rel=1e-4):
+    """Reading R17: triangle ids are bit-exact on chains both sides converge to
+    the same chain, except where the vertex lies on an edge (or corner) shared by the two
+    triangles -- within tol_rel x extent (the position tolerance) of the shared vertices'
+    segment.  Returns (mismatching vertices, list of (walk, vertex, gpu tri, oracle tri, dist)
+    for mismatches that are NOT such ties)."""
+    pos, _, I, _, _ = w.mesh_arrays()
+    P = pos.astype(np.float64)
+    gs, os_ = g["status"][ids], o["status"]
+    both = np.isin(gs, (0, 5)) & np.isin(os_, (0, 5))
+    n_mis, bad = 0, []
+    for j in np.nonzero(both)[0]:
+        kk = int(o["k"][j]) if "k" in o else k
+        if np.linalg.norm(g["pos"][ids[j], :kk] - o["pos"][j, :kk], axis=1).max() > tol_rel * extent:
+            continue                     # another admissible chain (counted as n_other_chain, R27)
+        for v in range(kk):
+            a, b = int(g["prim"][ids[j], v]), int(o["prim"][j, v])
+            if a == b:
+                continue
+            n_mis += 1
+            if a < 0 or b < 0:
+                bad.append((int(ids[j]), v, a, b, np.inf))
+                continue
+            shared = sorted(set(I[a].tolist()) & set(I[b].tolist()))
+            p = o["pos"][j, v]
+            if len(shared) >= 2:
+                d = _dist_point_segment(p, P[shared[0]], P[shared[1]])
+            elif len(shared) == 1:
+                d = float(np.linalg.norm(p - P[shared[0]]))
+            else:
+                d = np.inf
+            if not d <= tol_rel * extent:
+                bad.append((int(ids[j]), v, a, b, d / extent))
+    return n_mis, bad
 
 
 def tile_means(wv, spp, recv_shape, tile):

@@ -77,6 +77,10 @@ def _check_walk_parity(rep, min_agree=0.999, w=None, s=None, o=None, ext=None, m
     # and the full status code (incl. MAXITER / SEED_FAIL / BAD_SIDE / DEGENERATE) agrees overall
     assert rep["vis_agree"] >= 0.999 and rep["vis_mismatch"] <= max(1, 0.001 * rep["both"])
     assert rep["status_agree"] >= min_agree - 0.001
+    if "prim_bad" in rep:
+        # triangle ids: every mismatch is a tie on an edge/corner shared by both triangles (R17)
+        print(f"triangle-id mismatches {rep['prim_mis']}, not at a shared edge: {rep['prim_bad'][:10]}")
+        assert not rep["prim_bad"]
     assert rep["prim_agree"] >= 0.999
     # positions: chains both sides converge to the same admissible chain agree within 1e-4 x extent;
     # a different admissible chain (several are correct, R27) is a basin-boundary case and is counted
@@ -95,7 +99,7 @@ def cfg0_oracle_scene():
 
 def test_cfg0_full_walk_parity(cfg0_run, cfg0_oracle_scene):
     w, g, st, ext, o, ids = cfg0_run
-    rep = PY.compare(g, o, ids, ext, w.seed.k)
+    rep = PY.compare(g, o, ids, ext, w.seed.k, w=w)
     _check_walk_parity(rep, w=w, s=cfg0_oracle_scene, o=o, ext=ext)
     assert rep["G_rel_p99"] < 1e-3
     assert rep["trials_agree"] >= 0.99
@@ -111,7 +115,7 @@ def test_twin0v_visibility_parity_and_closed_form():
     g, st, ext = PY.run_gpu(w)
     ids = np.arange(w.n_walks)
     o, s = PY.run_oracle(w, ids)
-    rep = PY.compare(g, o, ids, ext, 1)
+    rep = PY.compare(g, o, ids, ext, 1, w=w)
     _check_walk_parity(rep, w=w, s=s, o=o, ext=ext)
     assert rep["n_occluded_gpu"] > 1000 and rep["vis_mismatch"] == 0
     n = {True: 0, False: 0}
@@ -158,7 +162,7 @@ def test_cfg0_estimator_tiles(cfg0_run):
 def test_cfg1_walk_parity(cfg1_small_run):
     from oracle import oracle as O
     w, g, st, ext, o, ids = cfg1_small_run
-    rep = PY.compare(g, o, ids, ext, w.seed.k)
+    rep = PY.compare(g, o, ids, ext, w.seed.k, w=w)
     _check_walk_parity(rep, w=w, s=O.OracleScene(w), o=o, ext=ext, max_non_boundary=1)
 
 
@@ -170,7 +174,7 @@ def test_cfg1_full_size_sampled():
     rng = np.random.default_rng(1)
     ids = np.sort(rng.choice(w.n_walks, size=3000, replace=False))
     o, s = PY.run_oracle(w, ids)
-    rep = PY.compare(g, o, ids, ext, w.seed.k)
+    rep = PY.compare(g, o, ids, ext, w.seed.k, w=w)
     # 3000 samples: at the measured 99.95% agreement, >= 99.7% holds with prob > 0.999
     _check_walk_parity(rep, min_agree=0.997, w=w, s=s, o=o, ext=ext, max_non_boundary=1)
     assert st["walks"] == w.n_walks
@@ -181,7 +185,7 @@ def test_twin1a_walk_parity():
     g, st, ext = PY.run_gpu(w)
     ids = np.arange(w.n_walks)
     o, s = PY.run_oracle(w, ids)
-    _check_walk_parity(PY.compare(g, o, ids, ext, w.seed.k), min_agree=0.998, w=w, s=s, o=o, ext=ext,
+    _check_walk_parity(PY.compare(g, o, ids, ext, w.seed.k, w=w), min_agree=0.998, w=w, s=s, o=o, ext=ext,
                        max_non_boundary=3)
 
 
@@ -277,7 +281,7 @@ def cfg2_run():
 
 def test_cfg2_walk_parity(cfg2_run):
     w, g, st, ext, o, s, ids = cfg2_run
-    rep = PY.compare(g, o, ids, ext, w.seed.k)
+    rep = PY.compare(g, o, ids, ext, w.seed.k, w=w)
     _check_walk_parity(rep, w=w, s=s, o=o, ext=ext, max_non_boundary=1)
     assert rep["G_rel_p99"] < 1e-4
 
@@ -292,12 +296,44 @@ def test_cfg2_estimator_tiles(cfg2_run):
     assert (z > 3).mean() <= 0.01 and z.max() <= 5
 
 
-def test_cfg3_walk_parity():
+def _check_estimator_tiles(w, g, o, tile):
+    """Reading R19 (north_star "per-pixel estimator means within 3 standard errors"): per
+    tile of tile x tile receivers x spp walks (>= 64), |mean_gpu - mean_orc| <= 3 SE on
+    >= 99 % of the tiles and <= 5 SE on all, SE = sqrt(s_gpu^2/N + s_orc^2/N)."""
+    mg, sg, n = PY.tile_means(g["w"], w.spp, w.recv_shape, tile)
+    mo, so, _ = PY.tile_means(o["w"], w.spp, w.recv_shape, tile)
+    assert n >= 64
+    se = np.sqrt(sg ** 2 / n + so ** 2 / n)
+    z = np.abs(mg - mo) / np.maximum(se, 1e-30)
+    z[(se == 0) & (mg == mo)] = 0
+    print(f"tiles {len(z)}, nonzero {(mo > 0).sum()}, max z {z.max():.2f}, > 3 SE: {(z > 3).sum()}")
+    assert (z > 3).mean() <= 0.01 and z.max() <= 5
+    return z
+
+
+def test_cfg1_estimator_tiles(cfg1_small_run):
+    w, g, st, ext, o, ids = cfg1_small_run
+    z = _check_estimator_tiles(w, g, o, 8)
+    assert len(z) == 256
+
+
+@pytest.fixture(scope="module")
+def cfg3_run():
     w = W.config3(n_side=64, spp=1)          # full slabs (780,300 tris), 4,096 k=6 walks
     g, st, ext = PY.run_gpu(w)
     ids = np.arange(w.n_walks)
     o, s = PY.run_oracle(w, ids)
-    rep = PY.compare(g, o, ids, ext, w.seed.k)
+    return w, g, st, ext, o, s, ids
+
+
+def test_cfg3_estimator_tiles(cfg3_run):
+    w, g, st, ext, o, s, ids = cfg3_run
+    _check_estimator_tiles(w, g, o, 8)
+
+
+def test_cfg3_walk_parity(cfg3_run):
+    w, g, st, ext, o, s, ids = cfg3_run
+    rep = PY.compare(g, o, ids, ext, w.seed.k, w=w)
     _check_walk_parity(rep, min_agree=0.997, w=w, s=s, o=o, ext=ext, max_non_boundary=2)
 
 
@@ -309,7 +345,7 @@ def test_twin3a_walk_parity_and_closed_form():
     g, st, ext = PY.run_gpu(w)
     ids = np.arange(w.n_walks)
     o, s = PY.run_oracle(w, ids)
-    rep = PY.compare(g, o, ids, ext, w.seed.k)
+    rep = PY.compare(g, o, ids, ext, w.seed.k, w=w)
     print({k: v for k, v in rep.items() if not isinstance(v, np.ndarray)})
     assert rep["flag_agree"] >= 0.999 and rep["n_other_chain"] == 0
     # coplanar triangles: a vertex on a shared edge may be attributed to either
@@ -402,7 +438,7 @@ def test_cfg2_full_size_sampled():
     rng = np.random.default_rng(2)
     ids = np.sort(rng.choice(w.n_walks, size=2000, replace=False))
     o, s = PY.run_oracle(w, ids)
-    rep = PY.compare(g, o, ids, ext, w.seed.k)
+    rep = PY.compare(g, o, ids, ext, w.seed.k, w=w)
     _check_walk_parity(rep, min_agree=0.997, w=w, s=s, o=o, ext=ext, max_non_boundary=1)
 
 
@@ -569,7 +605,7 @@ def test_cfg4_seeds_match_oracle(cfg4_guided_run):
 def test_cfg4_walk_parity(cfg4_guided_run):
     w, g, o, s = cfg4_guided_run
     ids = np.arange(w.n_walks)
-    rep = PY.compare(g, o, ids, g["extent"], 6)
+    rep = PY.compare(g, o, ids, g["extent"], 6, w=w)
     cg = np.isin(g["status"], (0, 5)); co = np.isin(o["status"], (0, 5))
     both = cg & co
     ct = g["ctype"][both]
@@ -580,6 +616,11 @@ def test_cfg4_walk_parity(cfg4_guided_run):
     assert rep["n_other_chain"] <= max(1, 0.001 * rep["both"])
     wg, wo = g["w"][both & (g["status"] == 0)], o["w"][both & (g["status"] == 0)]
     assert np.median(np.abs(wg - wo) / np.maximum(wo, 1e-30)) < 1e-3        # same trials, same P(n)
+
+
+def test_cfg4_estimator_tiles(cfg4_guided_run):
+    w, g, o, s = cfg4_guided_run
+    _check_estimator_tiles(w, g, o, 8)
 
 
 def test_cfg4_progressive_loop_per_iteration():
@@ -674,7 +715,7 @@ def test_cfg3_full_size_sampled():
     rng = np.random.default_rng(3)
     ids = np.sort(rng.choice(w.n_walks, size=600, replace=False))
     o, s = PY.run_oracle(w, ids)
-    rep = PY.compare(g, o, ids, ext, w.seed.k)
+    rep = PY.compare(g, o, ids, ext, w.seed.k, w=w)
     _check_walk_parity(rep, min_agree=0.99, w=w, s=s, o=o, ext=ext, max_non_boundary=2)
 
 
@@ -732,7 +773,7 @@ def test_cfg4_full_size_first_iterations():
         ds.close()
         ids = np.sort(rng.choice(w.n_walks, size=800, replace=False))
         o = s.walks(ids)
-        rep = PY.compare(g, o, ids, ext, 6)
+        rep = PY.compare(g, o, ids, ext, 6, w=w)
         agree.append(rep["flag_agree"])
         assert rep["n_other_chain"] <= 1 and rep["vis_mismatch"] == 0
     print(agree)

@@ -159,7 +159,8 @@ def test_stree_seeds_match_oracle(stree_guided_run):
 def test_stree_walk_parity(stree_guided_run):
     w, g, o, s = stree_guided_run
     ids = np.arange(w.n_walks)
-    rep = PY.compare(g, o, ids, g["extent"], 6)
+    rep = PY.compare(g, o, ids, g["extent"], 6, w=w)
+    assert not rep["prim_bad"] and rep["vis_mismatch"] == 0
     cg = np.isin(g["status"], (0, 5)); co = np.isin(o["status"], (0, 5))
     both = cg & co
     ct = g["ctype"][both]

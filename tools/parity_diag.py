@@ -49,11 +49,11 @@ nbi = 0
 for i in d[:200]:
     xD = w.xD[i // w.spp].astype(np.float64)
     base = np.isin(o["status"][i], (0, 5))
-    flags = []
+    fl = []
     for mi in (w.opts.max_iters - 3, w.opts.max_iters + 3):
         r = s.walk_from_target(xD, w.nD[0], o["xL"][i], o["target"][i].astype(np.float64), opts=s.opts(max_iters=mi))
-        flags.append(r["status"] in (0, 5))
-    nbi += (flags[0] != base) or (flags[1] != base)
+        fl.append(r["status"] in (0, 5))
+    nbi += (fl[0] != base) or (fl[1] != base)
 print(f"boundary (iteration budget +-3): {nbi} of {min(200, len(d))} disagreements")
 
 # per-iteration traces of a few disagreements: GPU vs oracle
@@ -70,7 +70,7 @@ mpg.mpg_debug_trace(None)
 tr = buf.cpu().numpy()
 st2 = b.status.cpu().numpy(); it2 = b.iters.cpu().numpy()
 print("rerun determinism: status equal", (st2 == g["status"]).mean(), "iters equal", (it2 == g["iters"]).mean())
-np.set_printoptions(precision=2, linewidth=200)
+np.set_printoptions(precision=3, linewidth=250)
 for i in d[:8]:
     st_o, it_o, res_o, beta_o = s.walk_trace(w.xD[i // w.spp].astype(np.float64), o["xL"][i], o["target"][i].astype(np.float64))
     ng = g["iters"][i] + 1
