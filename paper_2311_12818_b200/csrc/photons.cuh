@@ -98,12 +98,14 @@ __global__ void k_photons(const DScene S, const PhotonDev P, int64_t first, int6
             const DSurf &f = S.surf[h.surf];
             if (f.mat == 2) break;                         // absorbed by a diffuse occluder
             const double3 y = refine_hit(S, h.prim, h.surf, o, o + d, h.p);   // may move h.prim across a shared edge
-            const float3 yf = f3d(y);
-            const float3 ng = geo_normal(S, h.prim, h.surf, yf);
-            const float3 nf = shading_normal(S, h.prim, h.surf, yf);
-            double3 n = d3f(nf);
+            // normals in fp64 at the fp64 vertex (as the deduction, scatter_dir)
+            const V3<double> ngd = geo_normalR<double>(S, h.prim, h.surf, y);
+            V3<double> dna, dnb;
+            const V3<double> z0 = mk3<double>(0.0, 0.0, 0.0);
+            const V3<double> nsd = shadingR<double>(S, h.prim, h.surf, y, z0, z0, dna, dnb);
+            double3 n = make_double3(nsd.x, nsd.y, nsd.z);
             n = n * rsqrt(ddot(n, n));
-            const bool outside = ddot(d, d3f(ng)) < 0.0;
+            const bool outside = ddot(d, make_double3(ngd.x, ngd.y, ngd.z)) < 0.0;
             if (ddot(d, n) > 0.0) n = n * -1.0;
             const double ci = -ddot(d, n);
             if (!(ci > 0.0)) break;

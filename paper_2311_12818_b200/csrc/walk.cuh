@@ -104,12 +104,17 @@ enum { SS_WALKS = 0, SS_CONV, SS_NEWTON, SS_PRIM_IT, SS_ATTEMPTS, SS_RAYS, SS_TR
        SS_VTX, SS_STATUS0, SS_N = SS_STATUS0 + 8 };
 
 // reflect / refract the propagation direction d at a vertex (deduction, Eq. 6);
-// media from the side of d w.r.t. the geometric normal (R9, R14).  fp64: the
-// deduced seed chain then matches the oracle's to fp32 rounding of positions.
-__device__ __forceinline__ bool scatter_dir(const DScene &S, double3 &dd, int prim, int surf, float3 p, bool isT) {
+// media from the side of d w.r.t. the geometric normal (R9, R14).  Everything in
+// fp64 at the fp64 vertex, normals included (an fp32 shading normal at the
+// fp32-rounded point tilted the deduced chain by ~1e-7 relative, which the long
+// halving sequences of configs[3] amplified into different outcomes, measured):
+// the deduced seed chain matches the oracle's to fp64 rounding.
+__device__ __forceinline__ bool scatter_dir(const DScene &S, double3 &dd, int prim, int surf, double3 p, bool isT) {
     const DSurf &f = S.surf[surf];
-    float3 ng = geo_normal(S, prim, surf, p);
-    float3 nf = shading_normal(S, prim, surf, p);
+    const V3<double> ng = geo_normalR<double>(S, prim, surf, p);
+    V3<double> dna, dnb;
+    const V3<double> z0 = mk3<double>(0.0, 0.0, 0.0);
+    const V3<double> nf = shadingR<double>(S, prim, surf, p, z0, z0, dna, dnb);
     double dx = dd.x, dy = dd.y, dz = dd.z, nx = nf.x, ny = nf.y, nz = nf.z;
     double il = rsqrt(nx * nx + ny * ny + nz * nz);
     nx *= il; ny *= il; nz *= il;
@@ -263,7 +268,7 @@ __device__ __forceinline__ int trace_chain(const DScene &S, int mode, int k, uin
                 if (!(l2 > 0.0)) return 3 | (i << 4);
                 dd = v * rsqrt(l2);
             } else if (i > 0) {
-                if (!scatter_dir(S, dd, pprim, psurf, f3d(o), (res >> (i - 1)) & 1u)) return 4 | (i << 4);
+                if (!scatter_dir(S, dd, pprim, psurf, o, (res >> (i - 1)) & 1u)) return 4 | (i << 4);
             }
             of = f3d(o);
             d = nrmz(f3d(dd));

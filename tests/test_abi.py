@@ -90,3 +90,51 @@ def test_new_struct_layouts():
     assert C.sizeof(mpg.mpg_stree_info) == 48
     assert C.sizeof(mpg.mpg_photon_desc) == 56
     assert mpg.GUIDE_SAMPLE_BYTES == 48
+
+
+def test_trace_loop_head_yields_in_every_walk_kernel(L, tmp_path):
+    """DESIGN.md §4 item 1: the per-ray loop of trace_chain starts with a YIELD (emitted
+    because of the shared-memory ray counter in that loop), which lets lanes that are done
+    with ray i go on while warp-mates still traverse (measured -7..-17 % k_walk time).
+    ptxas decides this, so the built SASS is checked: every k_walk instantiation has a
+    YIELD directly before the code of the trace_chain loop."""
+    import shutil
+    import subprocess
+    cuobjdump = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    nvdisasm = shutil.which("nvdisasm") or "/usr/local/cuda/bin/nvdisasm"
+    if not (os.path.exists(cuobjdump) and os.path.exists(nvdisasm)):
+        pytest.skip("CUDA binary utilities not available")
+    src = open(os.path.join(ROOT, "paper_2311_12818_b200", "csrc", "walk.cuh")).read().splitlines()
+    start = next(i for i, l in enumerate(src) if "int trace_chain(" in l) + 1
+    end = next(i for i, l in enumerate(src) if i > start and "tau_res = res;" in l) + 1
+    subprocess.run([cuobjdump, "-xelf", "all", mpg.LIB_PATH], cwd=tmp_path, check=True, capture_output=True)
+    cub = [f for f in os.listdir(tmp_path) if f.endswith(".cubin")]
+    assert cub
+    sass = subprocess.run([nvdisasm, "-g", "-c", str(tmp_path / cub[0])], capture_output=True, text=True).stdout
+    kernels, fn, cur = {}, None, None
+    for line in sass.splitlines():
+        if ".section\t.text." in line:
+            name = line.split(".text.")[1].split(",")[0]
+            fn = name if name.startswith("_Z6k_walk") else None
+            if fn:
+                kernels[fn] = []
+            continue
+        if fn is None:
+            continue
+        m = re.search(r'//## File "([^"]+)", line (\d+)', line)
+        if m:
+            cur = (os.path.basename(m.group(1)), int(m.group(2)))
+            continue
+        if re.search(r"/\*[0-9a-f]{4,}\*/", line):
+            kernels[fn].append((cur, line))
+    assert len(kernels) >= 8
+    for fn, ins in kernels.items():
+        ok = False
+        for j, (c, l) in enumerate(ins):
+            if "YIELD" not in l:
+                continue
+            nxt = [x for x, _ in ins[j + 1:j + 6] if x]
+            if any(f == "walk.cuh" and start <= n <= end for f, n in nxt):
+                ok = True
+                break
+        assert ok, f"no YIELD at the trace_chain loop head in {fn}"

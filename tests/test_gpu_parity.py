@@ -163,7 +163,7 @@ def test_cfg1_walk_parity(cfg1_small_run):
     from oracle import oracle as O
     w, g, st, ext, o, ids = cfg1_small_run
     rep = PY.compare(g, o, ids, ext, w.seed.k, w=w)
-    _check_walk_parity(rep, w=w, s=O.OracleScene(w), o=o, ext=ext, max_non_boundary=1)
+    _check_walk_parity(rep, w=w, s=O.OracleScene(w), o=o, ext=ext)
 
 
 def test_cfg1_full_size_sampled():
@@ -175,8 +175,7 @@ def test_cfg1_full_size_sampled():
     ids = np.sort(rng.choice(w.n_walks, size=3000, replace=False))
     o, s = PY.run_oracle(w, ids)
     rep = PY.compare(g, o, ids, ext, w.seed.k, w=w)
-    # 3000 samples: at the measured 99.95% agreement, >= 99.7% holds with prob > 0.999
-    _check_walk_parity(rep, min_agree=0.997, w=w, s=s, o=o, ext=ext, max_non_boundary=1)
+    _check_walk_parity(rep, w=w, s=s, o=o, ext=ext)
     assert st["walks"] == w.n_walks
 
 
@@ -185,8 +184,7 @@ def test_twin1a_walk_parity():
     g, st, ext = PY.run_gpu(w)
     ids = np.arange(w.n_walks)
     o, s = PY.run_oracle(w, ids)
-    _check_walk_parity(PY.compare(g, o, ids, ext, w.seed.k, w=w), min_agree=0.998, w=w, s=s, o=o, ext=ext,
-                       max_non_boundary=3)
+    _check_walk_parity(PY.compare(g, o, ids, ext, w.seed.k, w=w), w=w, s=s, o=o, ext=ext)
 
 
 def test_twin1a_full_size_closed_form():
@@ -213,7 +211,7 @@ def test_ragged_and_empty_batches():
     g, st, ext = PY.run_gpu(w)
     o, s = PY.run_oracle(w, np.arange(w.n_walks))
     rep = PY.compare(g, o, np.arange(w.n_walks), ext, 1)
-    assert rep["flag_agree"] >= 0.99 and st["walks"] == 832
+    assert (np.isin(g["status"], (0, 5)) != np.isin(o["status"], (0, 5))).sum() <= 1 and st["walks"] == 832
     import dataclasses
     w0 = dataclasses.replace(w, xD=w.xD[:0], nD=w.nD[:0])
     g0, st0, _ = PY.run_gpu(w0)
@@ -282,7 +280,7 @@ def cfg2_run():
 def test_cfg2_walk_parity(cfg2_run):
     w, g, st, ext, o, s, ids = cfg2_run
     rep = PY.compare(g, o, ids, ext, w.seed.k, w=w)
-    _check_walk_parity(rep, w=w, s=s, o=o, ext=ext, max_non_boundary=1)
+    _check_walk_parity(rep, w=w, s=s, o=o, ext=ext)
     assert rep["G_rel_p99"] < 1e-4
 
 
@@ -334,7 +332,7 @@ def test_cfg3_estimator_tiles(cfg3_run):
 def test_cfg3_walk_parity(cfg3_run):
     w, g, st, ext, o, s, ids = cfg3_run
     rep = PY.compare(g, o, ids, ext, w.seed.k, w=w)
-    _check_walk_parity(rep, min_agree=0.997, w=w, s=s, o=o, ext=ext, max_non_boundary=2)
+    _check_walk_parity(rep, w=w, s=s, o=o, ext=ext)
 
 
 def test_twin3a_walk_parity_and_closed_form():
@@ -439,7 +437,7 @@ def test_cfg2_full_size_sampled():
     ids = np.sort(rng.choice(w.n_walks, size=2000, replace=False))
     o, s = PY.run_oracle(w, ids)
     rep = PY.compare(g, o, ids, ext, w.seed.k, w=w)
-    _check_walk_parity(rep, min_agree=0.997, w=w, s=s, o=o, ext=ext, max_non_boundary=1)
+    _check_walk_parity(rep, w=w, s=s, o=o, ext=ext)
 
 
 def _guide_tables_gpu(w, E):
@@ -708,15 +706,15 @@ def test_sorted_order_gives_identical_walks(which):
 
 
 def test_cfg3_full_size_sampled():
-    """configs[3] at full size (1,048,576 k=6 walks, bench launch configuration) vs 600 sampled oracle walks."""
+    """configs[3] at full size (1,048,576 k=6 walks, bench launch configuration) vs 3,000 sampled oracle walks."""
     w = W.config3()
     g, st, ext = PY.run_gpu(w, flags=w.opts.flags | BENCH_FLAGS)
     assert st["walks"] == w.n_walks
     rng = np.random.default_rng(3)
-    ids = np.sort(rng.choice(w.n_walks, size=600, replace=False))
+    ids = np.sort(rng.choice(w.n_walks, size=3000, replace=False))
     o, s = PY.run_oracle(w, ids)
     rep = PY.compare(g, o, ids, ext, w.seed.k, w=w)
-    _check_walk_parity(rep, min_agree=0.99, w=w, s=s, o=o, ext=ext, max_non_boundary=2)
+    _check_walk_parity(rep, w=w, s=s, o=o, ext=ext)
 
 
 def test_cfg4_mirror_sphere_chains_closed_form():
@@ -751,7 +749,7 @@ def test_cfg4_mirror_sphere_chains_closed_form():
 def test_cfg4_full_size_first_iterations():
     """configs[4] at full size (1,048,576 walks, the bench's flags): the initial iteration
     (empty guide) and a guided iteration (the seeded typed histogram uploaded to both
-    sides) vs 800 sampled oracle walks each."""
+    sides) vs 3,000 sampled oracle walks each."""
     from paper_2311_12818_b200 import mpg
     from oracle import oracle as O
     import torch
@@ -771,13 +769,14 @@ def test_cfg4_full_size_first_iterations():
         g = b.results()
         ext = ds.extent
         ds.close()
-        ids = np.sort(rng.choice(w.n_walks, size=800, replace=False))
+        ids = np.sort(rng.choice(w.n_walks, size=3000, replace=False))
         o = s.walks(ids)
         rep = PY.compare(g, o, ids, ext, 6, w=w)
         agree.append(rep["flag_agree"])
+        assert not rep["prim_bad"]
         assert rep["n_other_chain"] <= 1 and rep["vis_mismatch"] == 0
     print(agree)
-    assert min(agree) >= 0.995
+    assert min(agree) >= 0.999
 
 
 @pytest.mark.parametrize("caps", [("16", None), (None, "40"), ("3", "7")])
