@@ -237,7 +237,8 @@ def run_ours(args):
     w.opts.walk_id_base = D.walk_id_base(rank, w.n_walks * iters)
     ds = mpg.DeviceScene(w, stree_capacity=max(w.n_walks, args.photons) * world)
     b = mpg.Batch(w.xD, w.nD, w.spp, w.seed.k)
-    opts = ds.opts(flags=w.opts.flags | (4 if args.f64 else 0) | (0 if args.no_sort else 8))
+    fl = (w.opts.flags | (4 if args.f64 else 0) | (0 if args.no_sort else 8)) & ~(4 if args.f32 else 0)
+    opts = ds.opts(flags=fl)
     stream = torch.cuda.current_stream()
     guided = ds.guide is not None
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)   # > 126 MB L2
@@ -475,6 +476,7 @@ def main():
     ap.add_argument("--no-sort", action="store_true",
                     help="walk-order primaries (default: coherence-sorted order, MPG_FLAG_SORT; same results)")
     ap.add_argument("--f64", action="store_true", help="MPG_FLAG_NEWTON_F64")
+    ap.add_argument("--f32", action="store_true", help="clear MPG_FLAG_NEWTON_F64 (fp32 Jacobian/step)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -66,7 +66,10 @@ enum {
     MPG_WALK_SEED_FAIL = 2,  /* no seed, deduction missed, TIR or type mismatch   */
     MPG_WALK_BAD_SIDE = 3,   /* spurious constraint zero (R8)                     */
     MPG_WALK_DEGENERATE = 4, /* singular block, zero-length segment or NaN        */
-    MPG_WALK_OCCLUDED = 5    /* admissible but V = 0                      */
+    MPG_WALK_OCCLUDED = 5,   /* admissible but V = 0                      */
+    MPG_WALK_INACTIVE = 6    /* selective activation (MPG_FLAG_SELECTIVE, R36): the STree
+                                leaf of (x_D, x_L) holds no own (non-copy) sample, so specular chain
+                                sampling is not activated; the caller path-traces instead.  w = 0 */
 };
 
 /* One specular (or diffuse occluder) surface.  Outward normal (R9):
@@ -123,6 +126,10 @@ typedef struct {
 #define MPG_FLAG_SORT 8u      /* persistent kernel: process the primaries in the order of a key built from
                                   (receiver cell, seed direction) for ray coherence; every walk's result is
                                   unchanged (it depends only on its own walk id) */
+#define MPG_FLAG_SELECTIVE 16u /* selective activation (R36), MPG_SEED_GUIDE_STREE only (ignored
+                                  otherwise): mpg_sample_seeds marks a walk whose STree leaf has no own
+                                  sample (bin = -3) and mpg_manifold_walk returns MPG_WALK_INACTIVE for it
+                                  (the rendering stage's switch to path tracing) */
 
 typedef struct {
     int32_t max_iters;     /* Newton cap (BASELINE configs: 20, or 40 for k=6)       */
@@ -264,10 +271,13 @@ mpg_status mpg_guide_stree_info(const mpg_guide *guide, mpg_stree_info *info);
  * nodes int4 [n_nodes] (split bits, axis, child0, child1; child < 0 = ~leaf), leaf_begin /
  * leaf_count int64 [n_leaves] into leaf_ids int32 [n_lobes] (record indices, leaf order),
  * grp_off int32 [n_leaves][127], lobe_sample int32 [n_lobes], lobe_prefix u64 [n_lobes],
- * lobe_mu float4 [n_lobes] (mu, kappa), n_prefix u64 [n_leaves][6], type_prefix u64 [n_leaves][126]. */
+ * lobe_mu float4 [n_lobes] (mu, kappa), n_prefix u64 [n_leaves][6], type_prefix u64 [n_leaves][126],
+ * leaf_own int32 [n_leaves]: samples whose own key descends to the leaf, i.e. the leaf's samples
+ * without the overlap copies (selective activation, R36). */
 mpg_status mpg_guide_download_stree(const mpg_guide *guide, int32_t *nodes, int64_t *leaf_begin, int64_t *leaf_count,
                                     int32_t *leaf_ids, int32_t *grp_off, int32_t *lobe_sample, uint64_t *lobe_prefix,
-                                    float *lobe_mu, uint64_t *n_prefix, uint64_t *type_prefix, void *stream);
+                                    float *lobe_mu, uint64_t *n_prefix, uint64_t *type_prefix, int32_t *leaf_own,
+                                    void *stream);
 
 /* ---- photon-based initial distribution (R33) ----
  * Trace n_photons photons from the emitters (uniform light choice, cosine-weighted area

@@ -18,6 +18,7 @@
  *   repeated reciprocal est.    PAPER.md:906-915 (R x M)                            [R32]
  *   photon-based p_0            PAPER.md:398, :883                                   [R33]
  *   glossy separator weighting  PAPER.md:550-556 (Eq. 14)                            [R35]
+ *   selective activation        PAPER.md:604-608                                     [R36]
  * Every choice the paper leaves open is a numbered reading (R1..R35) in
  * DESIGN.md §3; the code cites them as [Rn].
  *
@@ -41,6 +42,7 @@
 #define ST_BAD_SIDE 3
 #define ST_DEGENERATE 4
 #define ST_OCCLUDED 5
+#define ST_INACTIVE 6 /* selective activation: no own sample in the STree leaf [R36] */
 
 /* ------------------------------------------------------------------------ */
 /* input records (mirrored by oracle/oracle.py ctypes)                       */
@@ -77,6 +79,7 @@ typedef struct {
     const int32_t *grp_off;      /* [leaves][127] lobe offsets of the (leaf, type) groups */
     const uint64_t *lobe_prefix; /* [lobes] inclusive per-group prefix of lobe weights   */
     const float *lobe_mu;        /* [lobes][4] vMF mean direction (xyz), kappa (w)       */
+    const int64_t *leaf_own;     /* [leaves] samples whose own key lies in the leaf (no copies) */
 } orc_seed_cfg;
 
 typedef struct {
@@ -87,7 +90,8 @@ typedef struct {
     double tol, beta0, same_chain_eps, ray_eps;
     uint64_t seed, walk_id_base;
     int32_t recip_repeats;  /* M >= 2: M independent reciprocal estimates averaged [R32] */
-    int32_t pad_;
+    int32_t selective;      /* selective activation [R36]: with the STree guide, a walk whose
+                               leaf holds no own (non-copy) sample is INACTIVE (left to path tracing) */
 } orc_opts;
 
 typedef struct {
@@ -914,6 +918,8 @@ static int seed_target(const orc_scene *sc, const orc_seed_cfg *cfg, const orc_o
             int ref = cfg->root_ref;
             while (ref >= 0) ref = p[nodes[ref].axis] < nodes[ref].split ? nodes[ref].child[0] : nodes[ref].child[1];
             c = ~ref;
+            /* selective activation: no own sample in the leaf -> path tracing [R36] */
+            if (o->selective && cfg->leaf_own && cfg->leaf_own[c] == 0) return -1;
         }
         const uint64_t *npf = cfg->n_prefix + (size_t)c * 6;
         draw(o, walk, 1u, 0u, r); /* n reused by every trial */
@@ -1051,7 +1057,9 @@ static int attempt(const orc_scene *sc, const orc_seed_cfg *cfg, const orc_opts 
     *k = cfg->k;
     *tau = cfg->tau;
     float xLf[3] = {(float)xL.x, (float)xL.y, (float)xL.z}; /* exact: x_L was drawn in fp32 */
-    if (!seed_target(sc, cfg, o, walk, trial, xD, xLf, sr)) return ST_SEED_FAIL;
+    const int sok = seed_target(sc, cfg, o, walk, trial, xD, xLf, sr);
+    if (sok < 0) return ST_INACTIVE;
+    if (!sok) return ST_SEED_FAIL;
     *k = sr->n;
     v3 xd = vf(xD);
     double eps = eps_ray(sc, o);
@@ -1467,6 +1475,7 @@ typedef struct {
     uint64_t *lobe_prefix;            /* [lobes] */
     float *lobe_mu;                   /* [lobes][4] */
     uint64_t *n_prefix, *type_prefix; /* [leaves][6], [leaves][126] */
+    int64_t *leaf_own;                /* [leaves] samples whose own key descends to the leaf [R36] */
 } orc_stree;
 
 static float skey(const orc_gsample *r, int a) { return canon0(a < 3 ? r->xD[a] : r->xL[a - 3]); }
@@ -1492,6 +1501,7 @@ void orc_stree_free(void *h) {
     if (!t) return;
     free(t->nodes); free(t->leaf_begin); free(t->leaf_count); free(t->leaf_ids); free(t->grp_off);
     free(t->lobe_sample); free(t->lobe_prefix); free(t->lobe_mu); free(t->n_prefix); free(t->type_prefix);
+    free(t->leaf_own);
     free(t);
 }
 
@@ -1664,6 +1674,16 @@ void *orc_stree_build(const orc_gsample *rec, int64_t n, float eps, float c_thr,
         t->grp_off[(size_t)l * 127 + 126] = (int32_t)pos;
         typed_tables(E, t->n_prefix + (size_t)l * 6, t->type_prefix + (size_t)l * 126);
     }
+    /* selective activation [R36]: "samples (excluding those used for filtering)",
+     * i.e. without the overlap copies, are the samples whose own key descends to the leaf */
+    t->leaf_own = (int64_t *)calloc(t->n_leaves > 0 ? t->n_leaves : 1, sizeof(int64_t));
+    for (int64_t i = 0; i < n; i++) {
+        if (!(rec[i].w > 0.0f && rec[i].type >= 0 && rec[i].type < 126)) continue;
+        int ref = t->root_ref;
+        while (ref >= 0) ref = skey(rec + i, t->nodes[ref].axis) < t->nodes[ref].split ? t->nodes[ref].child[0]
+                                                                                      : t->nodes[ref].child[1];
+        t->leaf_own[~ref]++;
+    }
     return t;
 }
 
@@ -1677,7 +1697,7 @@ void orc_stree_info(const void *h, int64_t out[6]) {
 /* copy out (caller sizes from orc_stree_info); any pointer may be NULL */
 void orc_stree_get(const void *h, orc_snode *nodes, int64_t *leaf_begin, int64_t *leaf_count, int64_t *leaf_ids,
                    int32_t *grp_off, int64_t *lobe_sample, uint64_t *lobe_prefix, float *lobe_mu, uint64_t *n_prefix,
-                   uint64_t *type_prefix) {
+                   uint64_t *type_prefix, int64_t *leaf_own) {
     const orc_stree *t = (const orc_stree *)h;
     int64_t L = t->n_leaves, nl = t->n_lobes;
     if (nodes) memcpy(nodes, t->nodes, sizeof(orc_snode) * t->n_nodes);
@@ -1690,6 +1710,7 @@ void orc_stree_get(const void *h, orc_snode *nodes, int64_t *leaf_begin, int64_t
     if (lobe_mu) memcpy(lobe_mu, t->lobe_mu, sizeof(float) * 4 * nl);
     if (n_prefix) memcpy(n_prefix, t->n_prefix, sizeof(uint64_t) * 6 * L);
     if (type_prefix) memcpy(type_prefix, t->type_prefix, sizeof(uint64_t) * 126 * L);
+    if (leaf_own) memcpy(leaf_own, t->leaf_own, sizeof(int64_t) * L);
 }
 
 /* sample records from walk outputs (Eq. 9 samples of one iteration): x_D of the walk's receiver,

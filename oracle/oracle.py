@@ -19,7 +19,7 @@ SRC = os.path.join(HERE, "mpg_oracle.c")
 LIB = os.path.join(HERE, "libmpg_oracle.so")
 KMAX = 8
 
-STATUS = {0: "CONVERGED", 1: "MAXITER", 2: "SEED_FAIL", 3: "BAD_SIDE", 4: "DEGENERATE", 5: "OCCLUDED"}
+STATUS = {0: "CONVERGED", 1: "MAXITER", 2: "SEED_FAIL", 3: "BAD_SIDE", 4: "DEGENERATE", 5: "OCCLUDED", 6: "INACTIVE"}
 
 
 def build(force: bool = False) -> str:
@@ -49,7 +49,7 @@ class SeedCfg(C.Structure):
                 ("uv_scale", C.c_float * 2), ("uv_plane_y", C.c_float), ("prefix", C.POINTER(C.c_uint64)),
                 ("n_prefix", C.c_void_p), ("type_prefix", C.c_void_p), ("dir_prefix", C.c_void_p),
                 ("root_ref", C.c_int32), ("pad_", C.c_int32), ("nodes", C.c_void_p), ("grp_off", C.c_void_p),
-                ("lobe_prefix", C.c_void_p), ("lobe_mu", C.c_void_p)]
+                ("lobe_prefix", C.c_void_p), ("lobe_mu", C.c_void_p), ("leaf_own", C.c_void_p)]
 
 
 # STree + vMF guide: 48-byte sample record and tree node, as in mpg_oracle.c
@@ -68,7 +68,7 @@ class Opts(C.Structure):
     _fields_ = [("max_iters", C.c_int32), ("trials", C.c_int32), ("k_max", C.c_uint32), ("max_iters_long", C.c_int32),
                 ("tol", C.c_double), ("beta0", C.c_double), ("same_chain_eps", C.c_double), ("ray_eps", C.c_double),
                 ("seed", C.c_uint64), ("walk_id_base", C.c_uint64), ("recip_repeats", C.c_int32),
-                ("pad_", C.c_int32)]
+                ("selective", C.c_int32)]
 
 
 class WalkOut(C.Structure):
@@ -135,7 +135,7 @@ def lib():
         _lib.orc_stree_build.argtypes = [P, C.c_int64, C.c_float, C.c_float, C.c_int32, C.c_float, C.c_float]
         _lib.orc_stree_free.argtypes = [P]
         _lib.orc_stree_info.argtypes = [P, P]
-        _lib.orc_stree_get.argtypes = [P] + [P] * 10
+        _lib.orc_stree_get.argtypes = [P] + [P] * 11
         _lib.orc_record_samples.argtypes = [P, C.c_int32, C.c_int64, P, P, P, P, P, P, P, P, C.c_float, P]
         _lib.orc_vmf_sample.argtypes = [P, C.c_float, C.c_float, C.c_float, P]
         _lib.orc_trace_photons.argtypes = [P, C.POINTER(PhotonDesc), C.c_int64, C.c_int64, P, P, P, P, P]
@@ -211,9 +211,10 @@ def stree_build(records: np.ndarray, eps=0.1, c_thr=1.0, max_depth=32, kappa_min
                leaf_ids=np.zeros(max(nlobe, 1), np.int64), grp_off=np.zeros((nl, 127), np.int32),
                lobe_sample=np.zeros(max(nlobe, 1), np.int64), lobe_prefix=np.zeros(max(nlobe, 1), np.uint64),
                lobe_mu=np.zeros((max(nlobe, 1), 4), np.float32), n_prefix=np.zeros((nl, 6), np.uint64),
-               type_prefix=np.zeros((nl, 126), np.uint64))
+               type_prefix=np.zeros((nl, 126), np.uint64), leaf_own=np.zeros(max(nl, 1), np.int64))
     L.orc_stree_get(h, *(_ptr(out[k]) for k in ("nodes", "leaf_begin", "leaf_count", "leaf_ids", "grp_off",
-                                                "lobe_sample", "lobe_prefix", "lobe_mu", "n_prefix", "type_prefix")))
+                                                "lobe_sample", "lobe_prefix", "lobe_mu", "n_prefix", "type_prefix",
+                                                "leaf_own")))
     L.orc_stree_free(h)
     out["nodes"] = out["nodes"][:nn]
     for k in ("leaf_ids", "lobe_sample", "lobe_prefix", "lobe_mu"):
@@ -247,7 +248,8 @@ def make_opts(w, **over) -> Opts:
     o = w.opts
     d = dict(max_iters=o.max_iters, trials=o.trials, k_max=o.k_max, tol=o.tol, beta0=o.beta0, seed=o.seed,
              walk_id_base=o.walk_id_base, same_chain_eps=0.0, ray_eps=0.0,
-             max_iters_long=getattr(o, "max_iters_long", 0), recip_repeats=getattr(o, "recip_repeats", 1))
+             max_iters_long=getattr(o, "max_iters_long", 0), recip_repeats=getattr(o, "recip_repeats", 1),
+             selective=int(bool(o.flags & 16)))
     d.update(over)
     r = Opts()
     for k, v in d.items():
@@ -326,6 +328,7 @@ class OracleScene:
         c.nodes, c.grp_off = _ptr(G["nodes"]), _ptr(G["grp_off"])
         c.lobe_prefix, c.lobe_mu = _ptr(G["lobe_prefix"]), _ptr(G["lobe_mu"])
         c.n_prefix, c.type_prefix = _ptr(G["n_prefix"]), _ptr(G["type_prefix"])
+        c.leaf_own = _ptr(G["leaf_own"])
 
     def trace_photons(self, n_photons, plane_point, plane_normal, first=0, count=None, seed=0, base=0,
                       max_vertices=6):

@@ -63,8 +63,17 @@ __device__ __forceinline__ void onb(float3 n, float3 &b1, float3 &b2) {
 // Philox4x32-10 (Salmon et al. 2011): key (seed_lo, seed_hi), counter
 // (walk_lo, walk_hi, purpose, trial) (R2)
 // ----------------------------------------------------------------------------
+// MPG_ROLL_PHILOX: rolled rounds (the kernel inlines it at ~10 sites, ~500 SASS
+// instructions unrolled); measured slower on configs[2] (A/B in DESIGN.md §4)
+#ifndef MPG_ROLL_PHILOX
+#define MPG_ROLL_PHILOX 0
+#endif
 __device__ __forceinline__ uint4 philox10(uint4 c, uint2 k) {
+#if MPG_ROLL_PHILOX
+#pragma unroll 1
+#else
 #pragma unroll
+#endif
     for (int r = 0; r < 10; r++) {
         unsigned hi0 = __umulhi(0xD2511F53u, c.x), lo0 = 0xD2511F53u * c.x;
         unsigned hi1 = __umulhi(0xCD9E8D57u, c.z), lo1 = 0xCD9E8D57u * c.z;

@@ -962,6 +962,8 @@ static mpg_status make_seed_ctx(const mpg_scene *scene, const mpg_guide *guide, 
         g.lobe_mu = T->lobe_mu.p;
         g.n_prefix = T->n_prefix.p;
         g.type_prefix = T->type_prefix.p;
+        g.leaf_own = T->leaf_own.p;
+        g.selective = (o->flags & MPG_FLAG_SELECTIVE) != 0;
         return MPG_OK;
     }
     if (sd->mode >= 2) {
@@ -991,7 +993,7 @@ __global__ void k_seeds(const DScene S, const SeedCtx g, const float4 *xD, int64
         SeedRes sr;
         bool ok = seed_target(S, g, wid, 0u, xyz(xD[i / spp]), l, sr);
         tgt[i] = make_float4(sr.tgt.x, sr.tgt.y, sr.tgt.z, 0.f);
-        bin[i] = ok ? sr.bin : -2;
+        bin[i] = ok ? sr.bin : (sr.bin == -3 ? -3 : -2);   // -3: inactive (R36), -2: seed failed
         if (ctype) ctype[i] = (uint32_t)sr.n | ((sr.bits & 255u) << 4) | ((sr.learned ? 1u : 0u) << 12);
         if (pn) pn[i] = sr.Pn;
     }
@@ -1313,7 +1315,7 @@ extern "C" mpg_status mpg_manifold_walk(const mpg_scene *scene, const mpg_guide 
     ARG_CHECK(q->n_recv * (int64_t)q->spp < (int64_t)1 << 31, "at most 2^31-1 walks per call");
     ARG_CHECK(o->max_iters >= 0 && o->max_iters < 65536 && o->tol > 0.f && o->beta0 > 0.f, "bad walk options");
     ARG_CHECK(!o->trials || o->k_max >= 1, "k_max must be >= 1");
-    ARG_CHECK((o->flags & ~(MPG_FLAG_NEWTON_F64 | MPG_FLAG_SORT)) == 0, "unknown walk flag");
+    ARG_CHECK((o->flags & ~(MPG_FLAG_NEWTON_F64 | MPG_FLAG_SORT | MPG_FLAG_SELECTIVE)) == 0, "unknown walk flag");
     SeedCtx g;
     mpg_status st = make_seed_ctx(scene, guide, sd, o, g);
     if (st != MPG_OK) return st;

@@ -14,6 +14,9 @@
 #pragma once
 #include "device_common.cuh"
 
+#ifndef MPG_ROLL_DC
+#define MPG_ROLL_DC 0
+#endif
 template <typename R> struct V3 {
     R x, y, z;
 };
@@ -200,15 +203,34 @@ __device__ __forceinline__ int newton_system(const DScene &S, int k, uint32_t ta
         VTermR<R> v;
         if (!vtermR<R>(a, xi, b, crossR(sgi, tgi), n, f, (tau >> i) & 1u, v)) { degen = true; break; }
         cmax = fmax(cmax, fmax(fabs(v.c0), fabs(v.c1)));
+        // the two tangent directions (MPG_ROLL_DC: in a rolled loop, one copy of the block
+        // code; A/B in DESIGN.md §4)
         R D00, D10, D01, D11;
-        dC_selfR(v, sgi, dna, D00, D10);
-        dC_selfR(v, tgi, dnb, D01, D11);
+#if MPG_ROLL_DC
+#pragma unroll 1
+#else
+#pragma unroll
+#endif
+        for (int c = 0; c < 2; c++) {
+            R o0, o1;
+            dC_selfR(v, c ? tgi : sgi, c ? dnb : dna, o0, o1);
+            if (c == 0) { D00 = o0; D10 = o1; } else { D01 = o0; D11 = o1; }
+        }
         R r0 = (R)(-v.c0), r1 = (R)(-v.c1);
         if (i > 0) {
             const int j = i > 0 ? i - 1 : 0;
             R l00, l10, l01, l11;
-            dC_nbR(v, v.wi, v.li, v.ei, rget(sg, j), l00, l10);
-            dC_nbR(v, v.wi, v.li, v.ei, rget(tg, j), l01, l11);
+            const V3<R> sgj = rget(sg, j), tgj = rget(tg, j);
+#if MPG_ROLL_DC
+#pragma unroll 1
+#else
+#pragma unroll
+#endif
+            for (int c = 0; c < 2; c++) {
+                R o0, o1;
+                dC_nbR(v, v.wi, v.li, v.ei, c ? tgj : sgj, o0, o1);
+                if (c == 0) { l00 = o0; l10 = o1; } else { l01 = o0; l11 = o1; }
+            }
             const R d0 = rget2(Di, j, 0), d1 = rget2(Di, j, 1), d2 = rget2(Di, j, 2), d3 = rget2(Di, j, 3);
             const R u0 = rget2(Ub, j, 0), u1 = rget2(Ub, j, 1), u2 = rget2(Ub, j, 2), u3 = rget2(Ub, j, 3);
             R M00 = l00 * d0 + l01 * d2, M01 = l00 * d1 + l01 * d3;
@@ -224,8 +246,17 @@ __device__ __forceinline__ int newton_system(const DScene &S, int k, uint32_t ta
         if (i < k - 1) {
             const int j = i + 1 < KMAX ? i + 1 : i;
             R u00, u10, u01, u11;
-            dC_nbR(v, v.wo, v.lo, v.eo, rget(sg, j), u00, u10);
-            dC_nbR(v, v.wo, v.lo, v.eo, rget(tg, j), u01, u11);
+            const V3<R> sgj = rget(sg, j), tgj = rget(tg, j);
+#if MPG_ROLL_DC
+#pragma unroll 1
+#else
+#pragma unroll
+#endif
+            for (int c = 0; c < 2; c++) {
+                R o0, o1;
+                dC_nbR(v, v.wo, v.lo, v.eo, c ? tgj : sgj, o0, o1);
+                if (c == 0) { u00 = o0; u10 = o1; } else { u01 = o0; u11 = o1; }
+            }
             rset2(Ub, i, 0, u00); rset2(Ub, i, 1, u01); rset2(Ub, i, 2, u10); rset2(Ub, i, 3, u11);
         }
         R det = D00 * D11 - D01 * D10;

@@ -29,6 +29,8 @@ struct SeedCtx {
     const int *grp_off;                     // [leaves][127] lobe offsets of (leaf, type) groups
     const unsigned long long *lobe_prefix;  // [lobes] inclusive per-group prefix of W_i
     const float4 *lobe_mu;                  // [lobes] mu (xyz), kappa (w)
+    const int *leaf_own;                    // [leaves] own (non-copy) samples per leaf (R36)
+    int selective;                          // MPG_FLAG_SELECTIVE: empty leaf -> INACTIVE
 };
 
 // one seed draw: the deduction ray x_D -> tgt gives x_1 (Eq. 6); n = chain
@@ -80,7 +82,8 @@ __device__ __forceinline__ void onb_exact(float3 n, float3 &b1, float3 &b2) {
 }
 
 // Seed target for (walk, trial): the deduction ray x_D -> target gives x_1
-// (Eq. 6).  Returns false if no seed could be drawn (SEED_FAIL).
+// (Eq. 6).  Returns false if no seed could be drawn (SEED_FAIL), with bin = -3 if
+// the walk is inactive (selective activation, R36).
 // w_D ~ vMF(mu, kappa) (Eq. 12) by the inverse CDF of cos(theta) (R31)
 __device__ __forceinline__ float3 vmf_dir(float4 m, float u1, float u2) {
     float kap = m.w;
@@ -220,6 +223,8 @@ __device__ MPG_COLD bool seed_target(const DScene &S, const SeedCtx &g, uint64_t
     if (g.mode == 3 || g.mode == 4) { // configs[4]: n ~ 1/2 P_0 + 1/2 P_e, then one-sample MIS for (w_D, tau)
         // (R22); mode 4: P_e from the STree leaf of (x_D, x_L), w_D from its vMF mixture (R28-R31)
         int c = g.mode == 3 ? seed_cell(g, xD) : stree_leaf(g, xD, xL);
+        // selective activation (R36): no own sample in the leaf -> path tracing
+        if (g.mode == 4 && g.selective && __ldg(g.leaf_own + c) == 0) { bin = -3; return false; }
         const unsigned long long *npf = (const unsigned long long *)g.n_prefix + (size_t)c * 6;
         uint4 r0 = rng_draw(g.seed, wid, 1u, 0u); // n is reused by every trial
         uint64_t S6 = __ldg(npf + 5);

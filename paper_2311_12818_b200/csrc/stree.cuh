@@ -92,6 +92,7 @@ struct StreeState {
     DBuf<unsigned long long> lobe_prefix;
     DBuf<float4> lobe_mu;
     DBuf<uint64_t> n_prefix, type_prefix;
+    DBuf<int> leaf_own;                  // [leaves] own (non-copy) samples (selective activation, R36)
     DBuf<double> E;
     // scratch
     DBuf<unsigned char> flags;
@@ -109,7 +110,7 @@ static void stree_state_free(StreeState *t) {
     if (!t) return;
     t->rec.release(); t->nodes.release(); t->leaf_begin.release(); t->leaf_count.release();
     t->leaf_ids.release(); t->grp_off.release(); t->lobe_sample.release(); t->lobe_prefix.release();
-    t->lobe_mu.release(); t->n_prefix.release(); t->type_prefix.release(); t->E.release();
+    t->lobe_mu.release(); t->n_prefix.release(); t->type_prefix.release(); t->leaf_own.release(); t->E.release();
     t->flags.release(); t->ids_a.release(); t->ids_b.release(); t->ids_c.release();
     t->nv.release(); t->keys_a.release(); t->keys_b.release(); t->temp.release(); t->bbox.release();
     t->split_out.release();
@@ -273,6 +274,21 @@ __global__ void k_lobe_kappa(const mpg_guide_sample *rec, const unsigned long lo
         float kap = ghi - glo == 1 ? 1.0f : (d2min > 0.0f ? FD(1.0f, d2min) : kmax);
         kap = fminf(fmaxf(kap, kmin), kmax);
         lobe_mu[j] = make_float4(ox, oy, oz, kap);
+    }
+}
+
+// selective activation (R36): a leaf's own samples -- "excluding those used for
+// filtering", the overlap copies -- are the samples whose own key descends to it
+__global__ void k_leaf_own(const mpg_guide_sample *rec, int64_t n, const int4 *nodes, int root_ref, int *leaf_own) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const mpg_guide_sample r = rec[i];
+        if (!gs_valid(r)) continue;
+        int ref = root_ref;
+        while (ref >= 0) {
+            const int4 nd = __ldg(nodes + ref);
+            ref = gs_key(r, nd.y) < __int_as_float(nd.x) ? nd.z : nd.w;
+        }
+        atomicAdd(leaf_own + ~ref, 1);
     }
 }
 
@@ -653,6 +669,14 @@ static mpg_status stree_build(StreeState *T, cudaStream_t st) {
     COUNT_LAUNCH(1);
     k_dir_cell_tables<<<(n_leaves + 127) / 128, 128, 0, st>>>(T->E.p, n_leaves, T->n_prefix.p, T->type_prefix.p);
     ST_TRY(cudaPeekAtLastError());
+    ST_TRY(T->leaf_own.reserve(std::max(n_leaves, 1)));
+    ST_TRY(cudaMemsetAsync(T->leaf_own.p, 0, sizeof(int) * std::max(n_leaves, 1), st));
+    if (T->n_rec > 0) {
+        COUNT_LAUNCH(1);
+        k_leaf_own<<<(int)std::min<int64_t>((T->n_rec + 255) / 256, nsm * 8), 256, 0, st>>>(
+            T->rec.p, T->n_rec, T->nodes.p, T->root_ref, T->leaf_own.p);
+        ST_TRY(cudaPeekAtLastError());
+    }
     ST_TRY(cudaStreamSynchronize(st));
     prof.mark("tables", st);
     if (!T->d.keep_all) T->n_rec = 0; // "last iteration only" (P:426 footnote) unless keep_all
@@ -761,7 +785,8 @@ extern "C" mpg_status mpg_guide_stree_info(const mpg_guide *g, mpg_stree_info *i
 extern "C" mpg_status mpg_guide_download_stree(const mpg_guide *g, int32_t *nodes, int64_t *leaf_begin,
                                                int64_t *leaf_count, int32_t *leaf_ids, int32_t *grp_off,
                                                int32_t *lobe_sample, uint64_t *lobe_prefix, float *lobe_mu,
-                                               uint64_t *n_prefix, uint64_t *type_prefix, void *stream) {
+                                               uint64_t *n_prefix, uint64_t *type_prefix, int32_t *leaf_own,
+                                               void *stream) {
     ARG_CHECK(g && g->stree, "needs an STree guide");
     const StreeState *T = g->stree;
     cudaStream_t s = as_stream(stream);
@@ -777,6 +802,7 @@ extern "C" mpg_status mpg_guide_download_stree(const mpg_guide *g, int32_t *node
     if (lobe_mu && NL) CUDA_TRY(cudaMemcpyAsync(lobe_mu, T->lobe_mu.p, NL * 16, K, s));
     if (n_prefix) CUDA_TRY(cudaMemcpyAsync(n_prefix, T->n_prefix.p, L * 6 * 8, K, s));
     if (type_prefix) CUDA_TRY(cudaMemcpyAsync(type_prefix, T->type_prefix.p, L * 126 * 8, K, s));
+    if (leaf_own && L) CUDA_TRY(cudaMemcpyAsync(leaf_own, T->leaf_own.p, L * 4, K, s));
     return MPG_OK;
 }
 

@@ -39,7 +39,8 @@
 enum { PH_FETCH = 0, PH_SEED = 1, PH_DEDUCE = 2, PH_SOLVE = 3, PH_REPROJ = 4, PH_END = 5, PH_IDLE = 6, PH_WAIT = 7,
        PH_VIS = 8 };
 #define HARD_NONE 0xffffffffu
-enum { ST_CONVERGED = 0, ST_MAXITER = 1, ST_SEED_FAIL = 2, ST_BAD_SIDE = 3, ST_DEGENERATE = 4, ST_OCCLUDED = 5 };
+enum { ST_CONVERGED = 0, ST_MAXITER = 1, ST_SEED_FAIL = 2, ST_BAD_SIDE = 3, ST_DEGENERATE = 4, ST_OCCLUDED = 5,
+       ST_INACTIVE = 6 };
 
 struct TrialHdr {
     unsigned long long queue;   // next primary walk
@@ -310,12 +311,12 @@ __device__ __forceinline__ int trace_chain(const DScene &S, int mode, int k, uin
 // final output of a walk with trial count kk (Eq. 15: w = T k / (P(n) pdf_L),
 // P(n) and pdf_L of the primary sample)
 __device__ __forceinline__ void trial_finalize(const WalkParams &P, int64_t w, uint32_t kk, bool truncated,
-                                               unsigned long long *s_stats) {
+                                               unsigned *s_stats) {
     P.trials[w] = kk;
     const float pn = P.seed_pn ? __ldg(P.seed_pn + w) : 1.0f;
     P.w[w] = __ldcg(P.T + w) * (float)kk / (pn * __ldg(P.seed_xL + w).w);
-    atomicAdd(&s_stats[SS_TRIALS], (unsigned long long)kk);
-    if (truncated) atomicAdd(&s_stats[SS_TRUNC], 1ull);
+    atomicAdd(&s_stats[SS_TRIALS], kk);
+    if (truncated) atomicAdd(&s_stats[SS_TRUNC], 1u);
 }
 // walks a lane has made final are counted in a register and published when the
 // lane runs out of primaries (PH_WAIT): one atomic per lane, not per walk
@@ -374,9 +375,11 @@ __device__ __forceinline__ unsigned long long gtimer() {
 
 template <int KMAX, typename R, int W, int MINB>
 __global__ void __launch_bounds__(128, MINB) k_walk(const DScene S, const SeedCtx g, const WalkParams P) {
-    __shared__ unsigned long long s_stats[SS_N];
+    // per-block walk counters in 32 bits (native shared atomics; 64-bit shared atomicAdd
+    // compiles to a CAS loop): a block makes at most ~2^25 walks final per launch
+    __shared__ unsigned s_stats[SS_N];
     __shared__ unsigned s_rays[128];   // chain rays per thread (see trace_chain)
-    for (int i = threadIdx.x; i < SS_N; i += blockDim.x) s_stats[i] = 0ull;
+    for (int i = threadIdx.x; i < SS_N; i += blockDim.x) s_stats[i] = 0u;
     s_rays[threadIdx.x] = 0u;
     __syncthreads();
 
@@ -538,8 +541,11 @@ __global__ void __launch_bounds__(128, MINB) k_walk(const DScene S, const SeedCt
         if (phase == PH_SEED) {
             c_attempts++;
             bool ok;
+            bool inactive = false;
             if (trial == 0) {
-                ok = __ldg(P.seed_bin + w) != -2;
+                const int sb = __ldg(P.seed_bin + w);
+                ok = sb >= -1;
+                inactive = sb == -3;   // selective activation (R36): left to path tracing
                 tgt = xyz(__ldg(P.seed_tgt + w));
                 if (P.seed_ctype) {
                     uint32_t ct = __ldg(P.seed_ctype + w);
@@ -558,7 +564,7 @@ __global__ void __launch_bounds__(128, MINB) k_walk(const DScene S, const SeedCt
             k = max(1, min(k, KMAX));
             it = 0;
             if (ok) phase = PH_DEDUCE;
-            else { end_status = ST_SEED_FAIL; phase = PH_END; }
+            else { end_status = inactive ? ST_INACTIVE : ST_SEED_FAIL; phase = PH_END; }
         }
 
 #ifdef MPG_TIMELINE
@@ -671,7 +677,7 @@ __global__ void __launch_bounds__(128, MINB) k_walk(const DScene S, const SeedCt
                     if (occluded) st = ST_OCCLUDED;
                     else { G = Gc; T = Tc; }
                 }
-                if (st != ST_SEED_FAIL) {
+                if (st != ST_SEED_FAIL && st != ST_INACTIVE) {
 #pragma unroll
                     for (int i = 0; i < KMAX; i++) {
                         if (i >= k) break;
@@ -684,10 +690,10 @@ __global__ void __launch_bounds__(128, MINB) k_walk(const DScene S, const SeedCt
                 P.G[w] = G;
                 P.T[w] = T;
                 if (P.out_ctype) P.out_ctype[w] = (uint16_t)((uint32_t)k | (tau << 4));
-                atomicAdd(&s_stats[SS_STATUS0 + st], 1ull);
-                atomicAdd(&s_stats[SS_PRIM_IT], (unsigned long long)it);
-                atomicAdd(&s_stats[SS_WALKS], 1ull);
-                if (st == ST_CONVERGED || st == ST_OCCLUDED) atomicAdd(&s_stats[SS_CONV], 1ull);
+                atomicAdd(&s_stats[SS_STATUS0 + st], 1u);
+                atomicAdd(&s_stats[SS_PRIM_IT], (unsigned)it);
+                atomicAdd(&s_stats[SS_WALKS], 1u);
+                if (st == ST_CONVERGED || st == ST_OCCLUDED) atomicAdd(&s_stats[SS_CONV], 1u);
                 if (st == ST_CONVERGED && T > 0.0f && P.trials_on) {
                     Tprim = T;
                     pk = k;
@@ -792,15 +798,18 @@ __global__ void __launch_bounds__(128, MINB) k_walk(const DScene S, const SeedCt
         for (int o = 16; o > 0; o >>= 1) v[j] += __shfl_down_sync(MPG_FULL, v[j], o);
     }
     if (lane == 0) {
-        atomicAdd(&s_stats[SS_NEWTON], v[0]);
-        atomicAdd(&s_stats[SS_ATTEMPTS], v[1]);
-        atomicAdd(&s_stats[SS_RAYS], v[2]);
-        atomicAdd(&s_stats[SS_NODES], v[3]);
-        atomicAdd(&s_stats[SS_TRIS], v[4]);
-        atomicAdd(&s_stats[SS_VTX], v[5]);
+        // work counters per warp straight into the 64-bit global stats
+        if (P.stats) {
+            atomicAdd(P.stats + SS_NEWTON, v[0]);
+            atomicAdd(P.stats + SS_ATTEMPTS, v[1]);
+            atomicAdd(P.stats + SS_RAYS, v[2]);
+            atomicAdd(P.stats + SS_NODES, v[3]);
+            atomicAdd(P.stats + SS_TRIS, v[4]);
+            atomicAdd(P.stats + SS_VTX, v[5]);
+        }
     }
     __syncthreads();
     if (P.stats)
         for (int i = threadIdx.x; i < SS_N; i += blockDim.x)
-            if (s_stats[i]) atomicAdd(P.stats + i, s_stats[i]);
+            if (s_stats[i]) atomicAdd(P.stats + i, (unsigned long long)s_stats[i]);
 }

@@ -19,7 +19,7 @@ LIB_PATH = os.environ.get("MPG_LIB", os.path.join(HERE, "libmpg.so"))   # MPG_LI
 KMAX = 8
 FLT_MAX = float(np.finfo(np.float32).max)   # unclamped vMF concentration (Eq. 12, R30)
 KAPPA_CLAMP_R30B = (1.0, 300.0)             # the measured product option (R30b)
-STATUS_NAMES = ["CONVERGED", "MAXITER", "SEED_FAIL", "BAD_SIDE", "DEGENERATE", "OCCLUDED"]
+STATUS_NAMES = ["CONVERGED", "MAXITER", "SEED_FAIL", "BAD_SIDE", "DEGENERATE", "OCCLUDED", "INACTIVE"]
 
 
 class MPGError(RuntimeError):
@@ -159,7 +159,7 @@ def lib():
             "mpg_trace_photons": (st, [P, C.POINTER(mpg_photon_desc), P, P]),
             "mpg_splat": (st, [P, C.c_int64, C.c_int32, P, P, P]),
             "mpg_guide_set_separator": (st, [P, P, P, C.c_float]),
-            "mpg_guide_download_stree": (st, [P] + [P] * 10 + [P]),
+            "mpg_guide_download_stree": (st, [P] + [P] * 11 + [P]),
         }
         for name, (res, args) in sig.items():
             if "MPG_LIB" in os.environ and not hasattr(L, name):
@@ -296,11 +296,12 @@ def mpg_guide_download_stree(h, stream=None) -> dict:
                leaf_count=torch.zeros(L, dtype=torch.int64), leaf_ids=torch.zeros(max(NL, 1), dtype=torch.int32),
                grp_off=torch.zeros(L, 127, dtype=torch.int32), lobe_sample=torch.zeros(max(NL, 1), dtype=torch.int32),
                lobe_prefix=torch.zeros(max(NL, 1), dtype=torch.int64), lobe_mu=torch.zeros(max(NL, 1), 4),
-               n_prefix=torch.zeros(L, 6, dtype=torch.int64), type_prefix=torch.zeros(L, 126, dtype=torch.int64))
+               n_prefix=torch.zeros(L, 6, dtype=torch.int64), type_prefix=torch.zeros(L, 126, dtype=torch.int64),
+               leaf_own=torch.zeros(max(L, 1), dtype=torch.int32))
     dev = {k: v.cuda() for k, v in dev.items()}
     _check(lib().mpg_guide_download_stree(h, *(_ptr(dev[k]) for k in (
         "nodes", "leaf_begin", "leaf_count", "leaf_ids", "grp_off", "lobe_sample", "lobe_prefix", "lobe_mu",
-        "n_prefix", "type_prefix")), _stream_ptr(stream)), "mpg_guide_download_stree")
+        "n_prefix", "type_prefix", "leaf_own")), _stream_ptr(stream)), "mpg_guide_download_stree")
     torch.cuda.synchronize()
     out = dict(inf)
     for k, v in dev.items():
@@ -309,6 +310,7 @@ def mpg_guide_download_stree(h, stream=None) -> dict:
             a = a.view(np.uint64)
         out[k] = a
     out["nodes"] = out["nodes"][:NN]
+    out["leaf_own"] = out["leaf_own"][:L]
     for k in ("leaf_ids", "lobe_sample", "lobe_prefix", "lobe_mu"):
         out[k] = out[k][:NL]
     return out

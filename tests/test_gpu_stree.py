@@ -56,6 +56,7 @@ def _assert_same_tree(G, R):
     assert np.array_equal(G["lobe_mu"].view(np.uint32), R["lobe_mu"].view(np.uint32)), "mu, kappa"
     assert np.array_equal(G["n_prefix"], R["n_prefix"]), "P(n) tables"
     assert np.array_equal(G["type_prefix"], R["type_prefix"]), "P(tau|n) tables"
+    assert np.array_equal(G["leaf_own"], R["leaf_own"][:R["n_leaves"]]), "own samples per leaf (R36)"
 
 
 @pytest.mark.parametrize("n,eps,c_thr", [(0, 0.1, 1.0), (1, 0.1, 1.0), (700, 0.1, 1.0), (20000, 0.1, 1.0),
@@ -269,3 +270,36 @@ def test_record_samples_glossy_separator_bit_exact():
                              o["ctype"] >> 4, o["xL"])
     assert (got["w"] > 0).sum() > 100 and not np.array_equal(got["w"], plain["w"])
     ds.close()
+
+
+def test_selective_activation_parity():
+    """MPG_FLAG_SELECTIVE (R36): the same tree on both sides (records with a gap
+    over the receivers, so some leaves hold no own sample); the GPU marks exactly the
+    oracle's INACTIVE walks, and every walk's status agrees."""
+    import torch
+    from oracle import oracle as O
+    from paper_2311_12818_b200 import mpg
+    w = W.config4(n_side=64, guide="stree")
+    r = W.synthetic_guide_samples(40000, seed=5)
+    keep = (r["xD"][:, 0] < -3.0) | (r["xD"][:, 0] > 6.0)
+    r["w"][~keep] = 0.0
+    ds = mpg.DeviceScene(w, stree_capacity=len(r))
+    t = torch.from_numpy(np.frombuffer(r.tobytes(), np.uint8).copy()).cuda()
+    mpg.mpg_guide_set_samples(ds.guide, t, len(r))
+    mpg.mpg_guide_rebuild(ds.guide)
+    b = mpg.Batch(w.xD, w.nD, w.spp, w.seed.k)
+    mpg.run_step(ds, b, ds.opts(flags=w.opts.flags | W.FLAG_SELECTIVE | BENCH_FLAGS))
+    torch.cuda.synchronize()
+    g = b.results()
+    st = b.stats_dict()
+    ext = ds.extent
+    ds.close()
+    s = O.OracleScene(w)
+    s.set_stree(O.stree_build(_oracle_records(r)))
+    o = s.walks(np.arange(w.n_walks), s.opts(selective=1))
+    gi, oi = g["status"] == 6, o["status"] == 6
+    print(int(gi.sum()), int(oi.sum()), st["by_status"])
+    assert oi.sum() > 100 and np.array_equal(gi, oi)
+    assert (g["w"][gi] == 0).all() and st["by_status"][6] == int(gi.sum())
+    rep = PY.compare(g, o, np.arange(w.n_walks), ext, 6, w=w)
+    assert rep["flag_agree"] >= 0.999 and rep["status_agree"] >= 0.998 and not rep["prim_bad"]

@@ -292,3 +292,88 @@ def test_ggx_separator_reciprocal_and_one_sided():
     assert np.allclose(a, b, rtol=2e-6)                                  # rho(v, l) = rho(l, v)
     below = l[:5] * np.array([1, -1, 1])
     assert (_rho(v[0], below, 0.3) == 0).all()                          # no weight below the separator
+
+
+# ---------------------------------------------------------------------------
+# Selective activation (reading R36)
+# ---------------------------------------------------------------------------
+def _leaf_boxes(G, K, valid):
+    """Leaf boxes from the split planes (left: x < c, right: x >= c), root = the data box."""
+    lo0, hi0 = K[valid].min(0), K[valid].max(0)
+    boxes = {}
+    stack = [(G["root_ref"], lo0.copy(), hi0.copy(), np.zeros(6, bool))]
+    while stack:
+        ref, lo, hi, cut = stack.pop()          # cut[a]: hi[a] is a split plane (strict <)
+        if ref < 0:
+            boxes[~ref] = (lo, hi, cut)
+            continue
+        nd = G["nodes"][ref]
+        a, c = int(nd["axis"]), np.float32(nd["split"])
+        h2, c2 = hi.copy(), cut.copy()
+        h2[a], c2[a] = c, True
+        stack.append((int(nd["child"][0]), lo.copy(), h2, c2))
+        l2 = lo.copy()
+        l2[a] = c
+        stack.append((int(nd["child"][1]), l2, hi.copy(), cut.copy()))
+    return boxes
+
+
+def _inside(P, box):
+    lo, hi, cut = box
+    return np.all(P >= lo, axis=-1) & np.all(np.where(cut, P < hi, P <= hi), axis=-1)
+
+
+@pytest.mark.parametrize("eps", [0.1, 0.0])
+def test_leaf_own_samples_are_the_leaf_list_without_copies(eps):
+    """P:606 "samples (excluding those used for filtering)": a leaf's own samples are the
+    members of its list that lie inside its box (the rest are the overlap copies of P:523);
+    they partition S, and with eps = 0 (no copies) they are the whole list."""
+    r = _records(8000, seed=3)
+    G = O.stree_build(r, eps=eps)
+    K = _key(r)
+    valid = (r["w"] > 0) & (r["type"] >= 0)
+    boxes = _leaf_boxes(G, K, valid)
+    start = 0
+    own = np.zeros(G["n_leaves"], np.int64)
+    for l in range(G["n_leaves"]):
+        cnt = G["leaf_count"][l]
+        ids = G["leaf_ids"][start:start + cnt]
+        start += cnt
+        own[l] = int(_inside(K[ids], boxes[l]).sum())
+    assert np.array_equal(G["leaf_own"], own)
+    assert own.sum() == valid.sum()                    # every sample is own in exactly one leaf
+    if eps == 0.0:
+        assert np.array_equal(own, G["leaf_count"])
+    else:
+        assert (own < G["leaf_count"]).any()           # copies exist and are excluded
+
+
+def test_selective_activation_marks_walks_in_empty_leaves():
+    """With MPG_FLAG_SELECTIVE a walk is INACTIVE (w = 0, left to path tracing) exactly when
+    the leaf whose box holds its (x_D, x_L) has no own sample; every other walk is unchanged."""
+    w = W.config4(n_side=32, grid_n=32, guide="stree")
+    r = _records(20000, seed=5)
+    keep = (r["xD"][:, 0] < -3.0) | (r["xD"][:, 0] > 6.0)   # a gap without samples between two regions
+    r["w"][~keep] = 0.0
+    G = O.stree_build(r)
+    s = O.OracleScene(w)
+    s.set_stree(G)
+    ids = np.arange(w.n_walks)
+    on = s.walks(ids, s.opts(selective=1))
+    off = s.walks(ids, s.opts(selective=0))
+    inact = on["status"] == 6
+    assert 50 < inact.sum() < w.n_walks - 50
+    act = ~inact
+    for f in ("status", "iters", "trials", "G", "T", "w", "pos"):
+        assert np.array_equal(on[f][act], off[f][act]), f
+    assert (on["w"][inact] == 0).all() and (on["trials"][inact] == 0).all()
+    K = _key(r)
+    valid = (r["w"] > 0) & (r["type"] >= 0)
+    boxes = _leaf_boxes(G, K, valid)
+    own = G["leaf_own"]
+    key = np.concatenate([w.xD[ids // w.spp], on["xL"].astype(np.float32)], axis=1) + np.float32(0.0)
+    for q in range(len(ids)):
+        leaves = [l for l in range(G["n_leaves"]) if _inside(key[q], boxes[l])]
+        if len(leaves) != 1:                           # outside the root box: the boundary leaf decides
+            continue
+        assert inact[q] == (own[leaves[0]] == 0), q
