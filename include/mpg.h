@@ -365,6 +365,17 @@ int32_t mpg_version(void);
 /* Number of kernel launches this library has enqueued since load (host-side
  * counter, all threads; library launches such as cub's radix-sort passes are counted too). */
 uint64_t mpg_kernel_launches(void);
+/* The paper's online training schedule (R34), host logic of the
+ * progressive train/render loop, in passes of one walk per receiver: the training budget
+ * is T = floor(train_frac * budget_passes) (0.3); training iterations of 1, 2, 4, ...
+ * passes (doubling); after an iteration a new round starts only while less than
+ * T/2 is used, otherwise the current iteration continues to T; the remaining
+ * budget_passes - T passes render with the final guide and only they are splatted.
+ * iters (host, max_iters entries) receives the passes of each training iteration, n_iters
+ * their number, render_passes the rest.  Synchronous, no device work.  A budget < 0,
+ * train_frac outside [0, 1], NULL outputs or too short an iters array -> MPG_ERR_INVALID_ARG. */
+mpg_status mpg_training_schedule(int64_t budget_passes, double train_frac, int64_t *iters, int32_t max_iters,
+                                 int32_t *n_iters, int64_t *render_passes);
 /* Measurement helper, not on the walk path: FP32 FFMA throughput of the current
  * device in TFLOP/s (8 independent FFMA chains per thread, SMs x 4 blocks of 256
  * threads, `iters` x 128 FFMA per thread, best of `reps` timed launches after one

@@ -1894,3 +1894,31 @@ void orc_trace_photons(const void *h, const orc_photon_desc *pd, int64_t first, 
         if (surfs) memcpy(surfs + KMAX * i, su, sizeof(su));
     }
 }
+
+/* ------------------------------------------------------------------------ */
+/* online training schedule [R34], in passes:            */
+/*   "We separate the training stage into several iterations with          */
+/*    increasing budgets. Specifically, we double the sample count in each  */
+/*    iteration. We stop the training stage immediately when 30% of the     */
+/*    budget is already used. Besides, when a training iteration is         */
+/*    finished, we start a new round if less than half of the training      */
+/*    budget is used. Otherwise, we continue the current iteration until    */
+/*    the rendering stage starts."                                          */
+/* Simulated pass by pass: each pass belongs to the current iteration.      */
+/* ------------------------------------------------------------------------ */
+int orc_training_schedule(int64_t budget, double train_frac, int64_t *iters, int32_t max_iters, int64_t *render) {
+    int64_t T = (int64_t)floor(train_frac * (double)budget); /* the training budget */
+    int32_t m = 0;
+    int64_t size = 1, in_cur = 0, used = 0;
+    int extend = 0; /* the current iteration continues until training ends */
+    while (used < T) {
+        if (in_cur == 0) { if (m >= max_iters) return -1; iters[m++] = 0; }
+        iters[m - 1]++; in_cur++; used++;
+        if (!extend && in_cur == size && used < T) {      /* iteration finished */
+            if (2 * used < T) { size *= 2; in_cur = 0; }   /* a new round */
+            else extend = 1;                               /* continue the current one */
+        }
+    }
+    *render = budget - T;
+    return m;
+}

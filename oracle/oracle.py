@@ -139,6 +139,8 @@ def lib():
         _lib.orc_record_samples.argtypes = [P, C.c_int32, C.c_int64, P, P, P, P, P, P, P, P, C.c_float, P]
         _lib.orc_vmf_sample.argtypes = [P, C.c_float, C.c_float, C.c_float, P]
         _lib.orc_trace_photons.argtypes = [P, C.POINTER(PhotonDesc), C.c_int64, C.c_int64, P, P, P, P, P]
+        _lib.orc_training_schedule.restype = C.c_int
+        _lib.orc_training_schedule.argtypes = [C.c_int64, C.c_double, P, C.c_int32, P]
         _lib.orc_scatter.restype = C.c_int
         _lib.orc_scatter.argtypes = [C.c_int, C.c_double, C.c_double, dp, dp, dp]
     return _lib
@@ -160,6 +162,15 @@ def philox(ctr: np.ndarray, key) -> np.ndarray:
     k = np.asarray(key, np.uint32)
     L.orc_philox_batch(_ptr(ctr), C.c_int64(ctr.shape[0]), _ptr(k), _ptr(out))
     return out
+
+
+def training_schedule(budget, train_frac=0.3):
+    """The paper's training schedule, simulated pass by pass: (iterations, render)."""
+    it = np.zeros(64, np.int64)
+    r = np.zeros(1, np.int64)
+    m = lib().orc_training_schedule(int(budget), float(train_frac), _ptr(it), 64, _ptr(r))
+    assert m >= 0
+    return [int(x) for x in it[:m]], int(r[0])
 
 
 def fresnel(cos_i, eta1, eta2) -> float:

@@ -64,9 +64,9 @@ __device__ __forceinline__ void onb(float3 n, float3 &b1, float3 &b2) {
 // (walk_lo, walk_hi, purpose, trial) (R2)
 // ----------------------------------------------------------------------------
 // MPG_ROLL_PHILOX: rolled rounds (the kernel inlines it at ~10 sites, ~500 SASS
-// instructions unrolled); measured slower on configs[2] (A/B in DESIGN.md §4)
+// instructions unrolled): measured -2 % (configs[2]) / -3.5 % ([4]) walk time
 #ifndef MPG_ROLL_PHILOX
-#define MPG_ROLL_PHILOX 0
+#define MPG_ROLL_PHILOX 1
 #endif
 __device__ __forceinline__ uint4 philox10(uint4 c, uint2 k) {
 #if MPG_ROLL_PHILOX

@@ -1513,3 +1513,32 @@ extern "C" mpg_status mpg_measure_fp32_peak(int32_t iters, int32_t reps, double 
     *tflops = best;
     return MPG_OK;
 }
+
+// ----------------------------------------------------------------------------
+// online training schedule (reading R34): host logic of the
+// progressive train/render loop, in passes of one walk per receiver
+// ----------------------------------------------------------------------------
+extern "C" mpg_status mpg_training_schedule(int64_t budget_passes, double train_frac, int64_t *iters,
+                                            int32_t max_iters, int32_t *n_iters, int64_t *render_passes) {
+    ARG_CHECK(budget_passes >= 0 && train_frac >= 0.0 && train_frac <= 1.0, "bad budget / training fraction");
+    ARG_CHECK(n_iters && render_passes && (iters || max_iters == 0) && max_iters >= 0, "NULL argument");
+    // "We stop the training stage immediately when 30% of the budget is already used"
+    const int64_t T = (int64_t)std::floor(train_frac * (double)budget_passes);
+    int32_t m = 0;
+    int64_t used = 0, size = 1;   // "we double the sample count in each iteration"
+    while (used < T) {
+        ARG_CHECK(m < max_iters, "iters array too short");
+        int64_t n = std::min(size, T - used);
+        iters[m++] = n;
+        used += n;
+        if (used >= T) break;
+        // "when a training iteration is finished, we start a new round if less than half of
+        // the training budget is used.  Otherwise, we continue the current iteration until the
+        // rendering stage starts"
+        if (2 * used < T) size *= 2;
+        else { iters[m - 1] += T - used; used = T; }
+    }
+    *n_iters = m;
+    *render_passes = budget_passes - T;
+    return MPG_OK;
+}

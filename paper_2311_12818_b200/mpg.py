@@ -109,7 +109,8 @@ EXPORTS = ["mpg_scene_create", "mpg_scene_destroy", "mpg_scene_get_info", "mpg_t
            "mpg_guide_download", "mpg_guide_download_dir_tables", "mpg_sample_seeds", "mpg_walk_workspace_size", "mpg_manifold_walk", "mpg_estimate",
            "mpg_debug_trace", "mpg_last_error", "mpg_version", "mpg_kernel_launches", "mpg_guide_create_stree",
            "mpg_guide_record_samples", "mpg_guide_set_samples", "mpg_guide_get_samples", "mpg_guide_stree_info",
-           "mpg_guide_download_stree", "mpg_trace_photons", "mpg_splat", "mpg_guide_set_separator", "mpg_measure_fp32_peak"]
+           "mpg_guide_download_stree", "mpg_trace_photons", "mpg_splat", "mpg_guide_set_separator", "mpg_measure_fp32_peak",
+           "mpg_training_schedule"]
 
 _lib = None
 
@@ -150,6 +151,8 @@ def lib():
             "mpg_version": (C.c_int32, []),
             "mpg_kernel_launches": (C.c_uint64, []),
             "mpg_measure_fp32_peak": (st, [C.c_int32, C.c_int32, C.POINTER(C.c_double), P]),
+            "mpg_training_schedule": (st, [C.c_int64, C.c_double, P, C.c_int32, C.POINTER(C.c_int32),
+                                           C.POINTER(C.c_int64)]),
             "mpg_guide_create_stree": (st, [C.POINTER(mpg_stree_desc), C.POINTER(P)]),
             "mpg_guide_record_samples": (st, [P, C.POINTER(mpg_query), C.POINTER(mpg_seed_buf),
                                               C.POINTER(mpg_walk_buf), C.c_int64, P]),
@@ -594,21 +597,13 @@ def training_schedule(budget_passes: int, train_frac: float = 0.3):
     iteration, a new (doubled) one starts only while less than half of the training budget
     floor(train_frac * budget) is used, otherwise the current iteration continues until the
     training budget is used up; training stops at that budget.  Returns (passes per training
-    iteration, render passes)."""
-    T = int(train_frac * budget_passes)
-    iters, used, i = [], 0, 0
-    while used < T:
-        n = min(1 << i, T - used)
-        iters.append(n)
-        used += n
-        if used >= T:
-            break
-        if 2 * used < T:
-            i += 1
-        else:                       # continue the current iteration to the end of training
-            iters[-1] += T - used
-            used = T
-    return iters, budget_passes - T
+    iteration, render passes).  The schedule is computed by the library (mpg_training_schedule)."""
+    buf = (C.c_int64 * 64)()
+    n = C.c_int32()
+    r = C.c_int64()
+    _check(lib().mpg_training_schedule(int(budget_passes), float(train_frac), buf, 64, C.byref(n), C.byref(r)),
+           "mpg_training_schedule")
+    return [int(buf[i]) for i in range(n.value)], int(r.value)
 
 
 def run_train_render(ds: DeviceScene, b: Batch, opts: mpg_walk_opts, budget_passes: int, stream=None,

@@ -20,7 +20,7 @@ def L():
 def declared_symbols():
     src = open(os.path.join(ROOT, "include", "mpg.h")).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\b(mpg_[a-z_]+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b(mpg_[a-z0-9_]+)\s*\(", src)))
 
 
 def test_header_declares_the_boundary():
