@@ -8,6 +8,25 @@
 #include <cuda_runtime.h>
 
 #define MPG_FULL 0xffffffffu
+// MPG_CHECKS=1: a bounds-checked build (device-side traps on out-of-range indices in the
+// traversal stack, the trial ring / entry table, chain outputs and STree lookups).  It is
+// the memory-error check of this repo: compute-sanitizer is closed on the GPU pool
+// (profiles/r2_bounds_checks.log).  Off in the product build.
+#ifndef MPG_CHECKS
+#define MPG_CHECKS 0
+#endif
+#if MPG_CHECKS
+#include <cstdio>
+#define MPG_CHECK(cond)                                                                        \
+    do {                                                                                       \
+        if (!(cond)) {                                                                         \
+            printf("MPG_CHECK failed %s:%d: %s\n", __FILE__, __LINE__, #cond);                 \
+            __trap();                                                                          \
+        }                                                                                      \
+    } while (0)
+#else
+#define MPG_CHECK(cond) ((void)0)
+#endif
 // end-of-attempt / seeding helpers (__noinline__ measured slower than inlined:
 // 3.3 KB stack frame, configs[1,3])
 #ifndef MPG_COLD
@@ -221,6 +240,7 @@ __device__ __forceinline__ int bvh_visit(const float4 *nodes, int node, float3 o
     }
     MPG_CAS(0, 1) MPG_CAS(2, 3) MPG_CAS(0, 2) MPG_CAS(1, 3) MPG_CAS(1, 2)
 #undef MPG_CAS
+    MPG_CHECK(sp >= 1 && sp + 3 <= TRAV_STACK(4));
     if (t[0] == INF) return stack[--sp];
     if (t[3] != INF) stack[sp++] = c[3];
     if (t[2] != INF) stack[sp++] = c[2];
@@ -241,6 +261,7 @@ __device__ __forceinline__ int bvh_visit(const float4 *nodes, int node, float3 o
     float n1 = fmaxf(fmaxf(fminf(sx0, sx1), fminf(sy0, sy1)), fmaxf(fminf(sz0, sz1), tmin));
     float f1 = fminf(fminf(fmaxf(sx0, sx1), fmaxf(sy0, sy1)), fminf(fmaxf(sz0, sz1), tmax));
     bool h0 = n0 <= f0, h1 = n1 <= f1;
+    MPG_CHECK(sp >= 1 && sp + 1 <= TRAV_STACK(2));
     if (h0 && h1) {
         bool swp = n1 < n0;
         stack[sp++] = swp ? ch.x : ch.y;
@@ -435,6 +456,7 @@ __device__ __forceinline__ bool trace(const DScene &S, float3 o, float3 d, float
         while (node != SENT || leaf != NONE) {
             while (node >= 0 && node != SENT) {
                 st.nodes++;
+                MPG_CHECK(node < S.n_nodes);
                 node = bvh_visit<W>(S.nodes, node, oi, r.idir, tmin, best, stack, sp);
                 if (node < 0 && leaf == NONE) { // postpone the leaf, keep traversing
                     leaf = node;
@@ -445,6 +467,7 @@ __device__ __forceinline__ bool trace(const DScene &S, float3 o, float3 d, float
             while (leaf != NONE) {
                 int v = ~leaf;
                 int start = v >> 3, cnt = (v & 7) + 1;
+                MPG_CHECK(start >= 0 && start + cnt <= S.n_tri);
                 for (int j = start; j < start + cnt; j++) {
                     st.tris++;
                     float4 p0 = MPG_LDN(S.tpos + TSTRIDE * j), p1 = MPG_LDN(S.tpos + TSTRIDE * j + 1),

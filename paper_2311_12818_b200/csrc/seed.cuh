@@ -111,7 +111,9 @@ __device__ __forceinline__ float canon0(float x) { return __fadd_rn(x, 0.0f); } 
 __device__ __noinline__ int stree_leaf(const SeedCtx &g, float3 xD, float3 xL) {
     float p[6] = {canon0(xD.x), canon0(xD.y), canon0(xD.z), canon0(xL.x), canon0(xL.y), canon0(xL.z)};
     int ref = g.root_ref;
+    int guard = 0;
     while (ref >= 0) {
+        MPG_CHECK(++guard <= 64);
         int4 nd = __ldg(g.nodes + ref);
         float v = p[0];
 #pragma unroll
@@ -127,6 +129,7 @@ __device__ __noinline__ float3 stree_lobe_target(const SeedCtx &g, int grp, uint
                                                  float3 xD, int &bin) {
     const int *go = g.grp_off + grp;
     int glo = __ldg(go), ghi = __ldg(go + 1);
+    MPG_CHECK(glo < ghi);
     uint64_t Sl = __ldg(g.lobe_prefix + ghi - 1);
     uint64_t tl = mulhi_u64(rw, Sl);
     int lo2 = glo, hi2 = ghi - 1; // upper_bound over the group

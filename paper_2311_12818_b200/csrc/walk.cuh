@@ -325,6 +325,7 @@ __device__ __forceinline__ void trial_finalize(const WalkParams &P, int64_t w, u
 __device__ __forceinline__ bool items_push(const WalkParams &P, uint32_t e, uint32_t t0, uint32_t B) {
     unsigned base = atomicAdd(&P.th->item_tail, B);
     if ((unsigned long long)base + B > P.item_cap) return false;
+    MPG_CHECK((unsigned long long)base + B <= P.item_cap);
     for (uint32_t j = 0; j < B; j++)
         *(volatile unsigned long long *)(P.items + base + j) = ((unsigned long long)e << 32) | (t0 + j);
     return true;
@@ -347,6 +348,7 @@ __device__ __forceinline__ bool hard_publish(const WalkParams &P, int64_t w, uin
     const unsigned backlog = *(volatile unsigned *)&P.th->item_tail - *(volatile unsigned *)&P.th->item_head;
     const bool idle = (int)backlog < (int)P.idle_backlog && __ldcg(&P.th->queue) >= (unsigned long long)P.n;
     const uint32_t B = min(idle ? P.item_b0_idle : P.item_b0, P.k_max - last);
+    MPG_CHECK(e < P.hard_cap && w >= 0 && w < P.n);
     P.e_walk[e] = w;
     P.e_psurf[e] = psurf;
     P.e_pct[e] = (uint32_t)pk | (ptau << 4);
@@ -500,7 +502,9 @@ __global__ void __launch_bounds__(128, MINB) k_walk(const DScene S, const SeedCt
                 trial = (uint32_t)wd;
                 // entries and primary chains are written by other SMs during this launch:
                 // read them through L2 (ld.global.cg), never from a possibly stale L1 line
+                MPG_CHECK(item_e >= 0 && (uint32_t)item_e < P.hard_cap);
                 w = __ldcg(P.e_walk + item_e);
+                MPG_CHECK(w >= 0 && w < P.n);
                 psurf = __ldcg(P.e_psurf + item_e);
                 uint32_t pct = __ldcg(P.e_pct + item_e);
                 pk = (int)(pct & 15u);
@@ -682,6 +686,7 @@ __global__ void __launch_bounds__(128, MINB) k_walk(const DScene S, const SeedCt
                     for (int i = 0; i < KMAX; i++) {
                         if (i >= k) break;
                         int pid = prim[i] >= 0 ? __float_as_int(__ldg(S.tpos + TSTRIDE * prim[i]).w) : -1;
+                        MPG_CHECK(w >= 0 && w < P.n && i < KMAX);
                         P.chain[(int64_t)i * P.n + w] = make_float4((float)x[i].x, (float)x[i].y, (float)x[i].z, __int_as_float(pid));
                     }
                 }
