@@ -85,6 +85,12 @@ typedef struct {
     const float *normals;                     /* mesh: host [n_vertices*3] shading normals (outward) */
     const int32_t *indices;                   /* mesh: host [n_triangles*3] */
     int32_t n_vertices, n_triangles;
+    float roughness;                          /* GGX alpha of a glossy specular surface (0: pure specular).
+                                                 Glossy chains (R37): each walk draws one offset
+                                                 normal per chain vertex from D(m) cos(theta_m) (Philox
+                                                 purpose 11 + i/2, trial 0; reused by all trials) and the
+                                                 chain satisfies h || m in the shading frame.  < 0 ->
+                                                 MPG_ERR_INVALID_ARG */
 } mpg_surface_desc;
 
 /* Emitter (R15): point (intensity emit) or one-sided parallelogram

@@ -19,6 +19,7 @@
  *   photon-based p_0            PAPER.md:398, :883                                   [R33]
  *   glossy separator weighting  PAPER.md:550-556 (Eq. 14)                            [R35]
  *   selective activation        PAPER.md:604-608                                     [R36]
+ *   glossy chains (offsets)     PAPER.md:562-565                                     [R37]
  * Every choice the paper leaves open is a numbered reading (R1..R35) in
  * DESIGN.md §3; the code cites them as [Rn].
  *
@@ -51,6 +52,7 @@ typedef struct {
     int32_t kind, mat, tri_begin, tri_count; /* kind 0 sphere 1 quad 2 mesh; mat 0 conductor 1 dielectric 2 diffuse */
     float eta_in, eta_out, reflectance, radius;
     float center[3], origin[3], edge_u[3], edge_v[3];
+    float roughness; /* GGX alpha of a glossy specular surface (0: pure specular) [R37] */
 } orc_surface;
 
 typedef struct {
@@ -135,6 +137,18 @@ static void onb(v3 n, v3 *b1, v3 *b2) {
     double b = n.x * n.y * a;
     *b1 = V(1.0 + sign * n.x * n.x * a, sign * b, -sign * n.x);
     *b2 = V(b, sign + n.y * n.y * a, -n.y);
+}
+
+/* the derivative of that basis for a change dn of n (differentiating the formulas above);
+ * glossy vertices need it: with an offset normal the frame's twist no longer drops out of
+ * the constraint at the solution [R37] */
+static void onb_d(v3 n, v3 dn, v3 *d1, v3 *d2) {
+    double sign = copysign(1.0, n.z);
+    double a = -1.0 / (sign + n.z);
+    double da = a * a * dn.z;
+    double db = (dn.x * n.y + n.x * dn.y) * a + n.x * n.y * da;
+    *d1 = V(sign * (2.0 * n.x * dn.x * a + n.x * n.x * da), sign * db, -sign * dn.x);
+    *d2 = V(db, 2.0 * n.y * dn.y * a + n.y * n.y * da, -dn.y);
 }
 
 /* ------------------------------------------------------------------------ */
@@ -391,7 +405,20 @@ static hit_t closest(const orc_scene *s, v3 o, v3 d, double tmin, double tmax, i
 /* ------------------------------------------------------------------------ */
 /* local geometry at a vertex                                                 */
 /* ------------------------------------------------------------------------ */
-typedef struct { v3 p; int prim, surf; } cvtx;
+/* a chain vertex; (oa, ob): the offset normal's slopes in the vertex's shading frame
+ * (s, t, n) for a glossy surface, 0 for a pure specular one [R37] */
+typedef struct { v3 p; int prim, surf; double oa, ob; } cvtx;
+
+/* glossy chains: "we sample the offset normal from the microfacet distribution
+ * before manifold sampling" -- GGX(alpha) normals m by D(m) cos(theta_m):
+ * tan(theta_m) = alpha sqrt(u1 / (1 - u1)), phi_m = 2 pi u2; slopes m_x/m_z, m_y/m_z [R37] */
+static void ggx_slopes(double alpha, double u1, double u2, double *a, double *b) {
+    if (!(alpha > 0.0)) { *a = *b = 0.0; return; }
+    double tt = alpha * sqrt(u1 / (1.0 - u1));
+    double ph = 6.28318530717958647692 * u2;
+    *a = tt * cos(ph);
+    *b = tt * sin(ph);
+}
 
 /* geometric normal (outward [R9]) */
 static v3 geo_normal(const orc_scene *s, const cvtx *x) {
@@ -445,6 +472,8 @@ typedef struct {
     v3 wi, wo, h, n, s, t, ng, sg, tg;
     double li, lo, eta_i, eta_o, hlen;
     v3 dn[2]; /* d n_s along sg, tg */
+    double oa, ob; /* offset slopes [R37] */
+    int glossy;
 } cterm;
 
 /* returns 0 on a degenerate configuration */
@@ -471,10 +500,19 @@ static int cterm_eval(const orc_scene *sc, v3 a, const cvtx *x, v3 b, int isT, c
     c->hlen = len(ht);
     if (!(c->hlen > 0.0) || !isfinite(c->hlen)) return 0;
     c->h = mul(ht, 1.0 / c->hlen);
+    c->oa = x->oa;
+    c->ob = x->ob;
+    c->glossy = f->roughness > 0.0f;
     return 1;
 }
 
-static void cterm_C(const cterm *c, double C[2]) { C[0] = dot(c->s, c->h); C[1] = dot(c->t, c->h); }
+/* C_i = (s.h, t.h) (R1); with an offset normal m = (oa, ob, 1) in the frame (s, t, n), h must
+ * be parallel to m: C_i = (s.h - oa n.h, t.h - ob n.h) [R37] */
+static void cterm_C(const cterm *c, double C[2]) {
+    double hn = dot(c->n, c->h);
+    C[0] = dot(c->s, c->h) - c->oa * hn;
+    C[1] = dot(c->t, c->h) - c->ob * hn;
+}
 
 /* dh for a change u of h~ : P_h u = (u - h(h.u))/|h~| */
 static v3 dh_of(const cterm *c, v3 u) { return mul(sub(u, mul(c->h, dot(c->h, u))), 1.0 / c->hlen); }
@@ -485,12 +523,12 @@ static v3 Po(const cterm *c, v3 v) { return mul(sub(v, mul(c->wo, dot(c->wo, v))
 /* dC/d(x_{i-1}) along v  (block L) */
 static void dC_da(const cterm *c, v3 v, double out[2]) {
     v3 dh = dh_of(c, mul(Pi(c, v), c->eta_i));
-    out[0] = dot(c->s, dh); out[1] = dot(c->t, dh);
+    out[0] = dot(c->s, dh) - c->oa * dot(c->n, dh); out[1] = dot(c->t, dh) - c->ob * dot(c->n, dh);
 }
 /* dC/d(x_{i+1}) along v  (block U, and D_L for the light) */
 static void dC_db(const cterm *c, v3 v, double out[2]) {
     v3 dh = dh_of(c, mul(Po(c, v), c->eta_o));
-    out[0] = dot(c->s, dh); out[1] = dot(c->t, dh);
+    out[0] = dot(c->s, dh) - c->oa * dot(c->n, dh); out[1] = dot(c->t, dh) - c->ob * dot(c->n, dh);
 }
 /* dC/d(x_i) along basis vector j (block D); frame moves by minimal rotation [R3] */
 static void dC_dp(const cterm *c, int j, double out[2]) {
@@ -498,6 +536,14 @@ static void dC_dp(const cterm *c, int j, double out[2]) {
     v3 u = sub(mul(Pi(c, v), -c->eta_i), mul(Po(c, v), c->eta_o));
     v3 dh = dh_of(c, u);
     double hn = dot(c->h, c->n);
+    if (c->glossy) { /* exact frame derivative (onb_d) and the offset terms [R37] */
+        v3 ds, dt;
+        onb_d(c->n, c->dn[j], &ds, &dt);
+        double dhn = dot(c->dn[j], c->h) + dot(c->n, dh);
+        out[0] = dot(ds, c->h) + dot(c->s, dh) - c->oa * dhn;
+        out[1] = dot(dt, c->h) + dot(c->t, dh) - c->ob * dhn;
+        return;
+    }
     out[0] = dot(c->s, dh) - hn * dot(c->s, c->dn[j]);
     out[1] = dot(c->t, dh) - hn * dot(c->t, c->dn[j]);
 }
@@ -603,6 +649,7 @@ static int newton(const orc_scene *sc, const orc_opts *o, int k, uint32_t tau, v
             hit_t h = closest(sc, prev, dir, eps, 1e300, 1, 1);
             if (h.surf < 0 || h.surf != x[i].surf) { ok = 0; break; }
             y[i].p = h.p; y[i].prim = h.prim; y[i].surf = h.surf;
+            y[i].oa = x[i].oa; y[i].ob = x[i].ob; /* the offsets stay (same surface) [R37] */
             prev = h.p;
         }
         if (ok) { for (int i = 0; i < k; i++) x[i] = y[i]; beta = beta * 2.0 < 1.0 ? beta * 2.0 : 1.0; }
@@ -656,6 +703,11 @@ static double kappa_of(const orc_scene *sc, int k, uint32_t tau, v3 xD, v3 xL, c
         v3 ng = geo_normal(sc, &x[i]);
         v3 dummy[1];
         v3 ns = shading_normal(sc, &x[i], 0, NULL, dummy);
+        if (f->roughness > 0.0f) { /* Fresnel at the micro-normal (offset normal) [R37] */
+            v3 s, t;
+            onb(ns, &s, &t);
+            ns = nrmz(add(ns, add(mul(s, x[i].oa), mul(t, x[i].ob))));
+        }
         int out_i = dot(wi, ng) > 0.0, out_o = dot(wo, ng) > 0.0;
         double eta_wi = out_i ? f->eta_out : f->eta_in;
         double eta_wo = out_o ? f->eta_out : f->eta_in;
@@ -993,8 +1045,35 @@ static int seed_target(const orc_scene *sc, const orc_seed_cfg *cfg, const orc_o
  * learned = 0 (initializer, "generated by ray tracing, deciding the
  * scattering type"): vertex i on a dielectric takes bit i of tau as T/R, a
  * conductor always R; the resolved string is returned in *tau_out [R22]. */
+/* test hook: offset uniforms (u1, u2 per vertex) for the explicit-chain entry points
+ * (orc_constraint, orc_newton_chain, orc_walk_from_target, orc_ggt, orc_kappa); NULL = 0 */
+static const double *g_test_uv = NULL;
+static double g_test_uv_buf[2 * KMAX];
+void orc_set_offset_uv(const double *uv, int k) {
+    if (!uv) { g_test_uv = NULL; return; }
+    for (int i = 0; i < 2 * k && i < 2 * KMAX; i++) g_test_uv_buf[i] = uv[i];
+    g_test_uv = g_test_uv_buf;
+}
+static void set_offsets(const orc_scene *sc, cvtx *x, int k, const double *uv) {
+    for (int i = 0; i < k; i++) {
+        if (uv) ggx_slopes(sc->surf[x[i].surf].roughness, uv[2 * i], uv[2 * i + 1], &x[i].oa, &x[i].ob);
+        else x[i].oa = x[i].ob = 0.0;
+    }
+}
+/* the walk's offset uniforms: vertex i takes words 2(i&1), 2(i&1)+1 of draw (11 + i/2, trial 0):
+ * drawn once per walk and reused by every trial (the chains are "constrained to
+ * this offset normal") [R37] */
+static void walk_offset_uv(const orc_opts *o, uint64_t walk, int k, double *uv) {
+    uint32_t r[4];
+    for (int i = 0; i < k; i++) {
+        if ((i & 1) == 0) draw(o, walk, 11u + (uint32_t)(i >> 1), 0u, r);
+        uv[2 * i] = (double)u01(r[2 * (i & 1)]);
+        uv[2 * i + 1] = (double)u01(r[2 * (i & 1) + 1]);
+    }
+}
+
 static int deduce_ex(const orc_scene *sc, int k, uint32_t tau, int learned, v3 xD, v3 target, double eps, cvtx *x,
-                     uint32_t *tau_out) {
+                     uint32_t *tau_out, const double *ouv) {
     uint32_t res = 0;
     v3 d = sub(target, xD);
     double dl = len(d);
@@ -1005,6 +1084,8 @@ static int deduce_ex(const orc_scene *sc, int k, uint32_t tau, int learned, v3 x
         hit_t h = closest(sc, o, d, eps, 1e300, 1, 1);
         if (h.surf < 0) return 0;
         x[i].p = h.p; x[i].prim = h.prim; x[i].surf = h.surf;
+        x[i].oa = x[i].ob = 0.0;
+        if (ouv) ggx_slopes(sc->surf[h.surf].roughness, ouv[2 * i], ouv[2 * i + 1], &x[i].oa, &x[i].ob);
         uint32_t bit = (tau >> i) & 1u;
         if (!learned && sc->surf[h.surf].mat == 0) bit = 0u;
         if (bit && sc->surf[h.surf].mat != 1) return 0; /* T on a conductor */
@@ -1014,6 +1095,11 @@ static int deduce_ex(const orc_scene *sc, int k, uint32_t tau, int learned, v3 x
             v3 ng = geo_normal(sc, &x[i]);
             v3 dummy[1];
             v3 n = shading_normal(sc, &x[i], 0, NULL, dummy);
+            if (f->roughness > 0.0f) { /* scatter about the offset normal [R37] */
+                v3 s, t;
+                onb(n, &s, &t);
+                n = nrmz(add(n, add(mul(s, x[i].oa), mul(t, x[i].ob))));
+            }
             int outside = dot(d, ng) < 0.0;
             if (dot(d, n) > 0.0) n = mul(n, -1.0);
             double ci = -dot(d, n);
@@ -1036,7 +1122,7 @@ static int deduce_ex(const orc_scene *sc, int k, uint32_t tau, int learned, v3 x
 
 static int deduce(const orc_scene *sc, int k, uint32_t tau, v3 xD, v3 target, double eps, cvtx *x) {
     uint32_t t2;
-    return deduce_ex(sc, k, tau, 1, xD, target, eps, x, &t2);
+    return deduce_ex(sc, k, tau, 1, xD, target, eps, x, &t2, g_test_uv);
 }
 
 static int same_chain(int k, const cvtx *a, const cvtx *b, double eps) {
@@ -1063,7 +1149,9 @@ static int attempt(const orc_scene *sc, const orc_seed_cfg *cfg, const orc_opts 
     *k = sr->n;
     v3 xd = vf(xD);
     double eps = eps_ray(sc, o);
-    if (!deduce_ex(sc, sr->n, sr->learned ? sr->tau : sr->init_bits, sr->learned, xd, vf(sr->tgt), eps, x, tau))
+    double ouv[2 * KMAX];
+    walk_offset_uv(o, walk, sr->n, ouv);
+    if (!deduce_ex(sc, sr->n, sr->learned ? sr->tau : sr->init_bits, sr->learned, xd, vf(sr->tgt), eps, x, tau, ouv))
         return ST_SEED_FAIL;
     int st = newton(sc, o, *k, *tau, xd, xL, x, iters, eps, NULL);
     if (st == ST_CONVERGED && !sides_ok(sc, *k, *tau, xd, xL, x)) st = ST_BAD_SIDE;
@@ -1171,6 +1259,7 @@ int orc_constraint(const void *h, int k, uint32_t tau, const double xD[3], const
     cvtx x[KMAX];
     cterm terms[KMAX];
     for (int i = 0; i < k; i++) { x[i].p = V(pos[3 * i], pos[3 * i + 1], pos[3 * i + 2]); x[i].prim = prim[i]; x[i].surf = surf[i]; }
+    set_offsets((const orc_scene *)h, x, k, g_test_uv);
     return chain_system((const orc_scene *)h, k, tau, V(xD[0], xD[1], xD[2]), V(xL[0], xL[1], xL[2]), x, C, J, terms);
 }
 
@@ -1181,6 +1270,7 @@ int orc_newton_chain(const void *h, const orc_opts *o, int k, uint32_t tau, cons
     const orc_scene *sc = (const orc_scene *)h;
     cvtx x[KMAX];
     for (int i = 0; i < k; i++) { x[i].p = V(pos[3 * i], pos[3 * i + 1], pos[3 * i + 2]); x[i].prim = prim[i]; x[i].surf = surf[i]; }
+    set_offsets((const orc_scene *)h, x, k, g_test_uv);
     int it;
     int st = newton(sc, o, k, tau, V(xD[0], xD[1], xD[2]), V(xL[0], xL[1], xL[2]), x, &it, eps_ray(sc, o), res_hist);
     for (int i = 0; i < k; i++) { pos[3 * i] = x[i].p.x; pos[3 * i + 1] = x[i].p.y; pos[3 * i + 2] = x[i].p.z; prim[i] = x[i].prim; surf[i] = x[i].surf; }
@@ -1214,6 +1304,7 @@ double orc_ggt(const void *h, const orc_opts *o, int method, double delta, int k
     const orc_scene *sc = (const orc_scene *)h;
     cvtx x[KMAX];
     for (int i = 0; i < k; i++) { x[i].p = V(pos[3 * i], pos[3 * i + 1], pos[3 * i + 2]); x[i].prim = prim[i]; x[i].surf = surf[i]; }
+    set_offsets((const orc_scene *)h, x, k, g_test_uv);
     v3 xd = V(xD[0], xD[1], xD[2]), nd = V(nD[0], nD[1], nD[2]), xl = V(xL[0], xL[1], xL[2]);
     const orc_light *L = &sc->light[light_id];
     if (method == 0) return ggt_analytic(sc, k, tau, xd, nd, xl, L, x);
@@ -1247,6 +1338,7 @@ double orc_kappa(const void *h, int k, uint32_t tau, const double xD[3], const d
                  const int32_t *prim, const int32_t *surf) {
     cvtx x[KMAX];
     for (int i = 0; i < k; i++) { x[i].p = V(pos[3 * i], pos[3 * i + 1], pos[3 * i + 2]); x[i].prim = prim[i]; x[i].surf = surf[i]; }
+    set_offsets((const orc_scene *)h, x, k, g_test_uv);
     return kappa_of((const orc_scene *)h, k, tau, V(xD[0], xD[1], xD[2]), V(xL[0], xL[1], xL[2]), x);
 }
 

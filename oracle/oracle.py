@@ -34,7 +34,7 @@ class Surface(C.Structure):
     _fields_ = [("kind", C.c_int32), ("mat", C.c_int32), ("tri_begin", C.c_int32), ("tri_count", C.c_int32),
                 ("eta_in", C.c_float), ("eta_out", C.c_float), ("reflectance", C.c_float), ("radius", C.c_float),
                 ("center", C.c_float * 3), ("origin", C.c_float * 3), ("edge_u", C.c_float * 3),
-                ("edge_v", C.c_float * 3)]
+                ("edge_v", C.c_float * 3), ("roughness", C.c_float)]
 
 
 class Light(C.Structure):
@@ -141,6 +141,7 @@ def lib():
         _lib.orc_trace_photons.argtypes = [P, C.POINTER(PhotonDesc), C.c_int64, C.c_int64, P, P, P, P, P]
         _lib.orc_training_schedule.restype = C.c_int
         _lib.orc_training_schedule.argtypes = [C.c_int64, C.c_double, P, C.c_int32, P]
+        _lib.orc_set_offset_uv.argtypes = [P, C.c_int]
         _lib.orc_scatter.restype = C.c_int
         _lib.orc_scatter.argtypes = [C.c_int, C.c_double, C.c_double, dp, dp, dp]
     return _lib
@@ -171,6 +172,16 @@ def training_schedule(budget, train_frac=0.3):
     m = lib().orc_training_schedule(int(budget), float(train_frac), _ptr(it), 64, _ptr(r))
     assert m >= 0
     return [int(x) for x in it[:m]], int(r[0])
+
+
+def set_offset_uv(uv=None):
+    """Offset-normal uniforms (u1, u2 per vertex, [k, 2]) used by the explicit-chain entry points
+    (constraint, newton_chain, walk_from_target, ggt, kappa) on glossy surfaces [R37]; None = 0."""
+    if uv is None:
+        lib().orc_set_offset_uv(None, 0)
+        return
+    a = np.ascontiguousarray(uv, np.float64).reshape(-1)
+    lib().orc_set_offset_uv(a.ctypes.data_as(C.c_void_p), a.size // 2)
 
 
 def fresnel(cos_i, eta1, eta2) -> float:
@@ -285,6 +296,7 @@ class OracleScene:
             S[i].origin[:] = list(s.origin)
             S[i].edge_u[:] = list(s.edge_u)
             S[i].edge_v[:] = list(s.edge_v)
+            S[i].roughness = float(getattr(s, "roughness", 0.0))
         Ls = (Light * max(1, len(w.lights)))()
         for i, l in enumerate(w.lights):
             Ls[i].kind, Ls[i].emit = l.kind, l.emit

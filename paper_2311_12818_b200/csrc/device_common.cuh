@@ -119,6 +119,7 @@ __device__ __forceinline__ uint32_t uidx(uint32_t x, uint32_t m) { return __umul
 struct DSurf {
     int kind, mat, tri_begin, tri_count;
     float eta_in, eta_out, refl, radius;
+    float rough;   // GGX alpha of a glossy surface (0: pure specular, R37)
     float3 center, origin, eu, ev, nq; // nq: unit quad normal
 };
 

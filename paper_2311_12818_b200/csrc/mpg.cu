@@ -264,6 +264,8 @@ extern "C" mpg_status mpg_scene_create(const mpg_surface_desc *surfaces, int32_t
         f.eta_in = sd.eta_in > 0.f ? sd.eta_in : 1.f;
         f.eta_out = sd.eta_out > 0.f ? sd.eta_out : 1.f;
         f.refl = sd.reflectance;
+        if (!(sd.roughness >= 0.f)) { mpg_scene_destroy(s); return fail(MPG_ERR_INVALID_ARG, "roughness must be >= 0"); }
+        f.rough = sd.roughness;
         f.radius = sd.radius;
         f.center = F3(H(sd.center));
         f.origin = F3(H(sd.origin));

@@ -45,6 +45,33 @@ template <typename R> __device__ __forceinline__ void onbR(V3<R> n, V3<R> &b1, V
     b1 = {(R)1 + sign * n.x * n.x * a, sign * b, -sign * n.x};
     b2 = {b, sign + n.y * n.y * a, -n.y};
 }
+// derivative of that basis for a change dn of n (glossy vertices: with an offset normal the
+// frame's twist does not drop out of the constraint at the solution, R37)
+template <typename R> __device__ __forceinline__ void onb_dR(V3<R> n, V3<R> dn, V3<R> &d1, V3<R> &d2) {
+    R sign = copysign((R)1, n.z);
+    R a = (R)-1 / (sign + n.z);
+    R da = a * a * dn.z;
+    R db = (dn.x * n.y + n.x * dn.y) * a + n.x * n.y * da;
+    d1 = {sign * ((R)2 * n.x * dn.x * a + n.x * n.x * da), sign * db, -sign * dn.x};
+    d2 = {db, (R)2 * n.y * dn.y * a + n.y * n.y * da, -dn.y};
+}
+
+// Glossy chains (R37): offset slopes (a, b) of chain vertex i, i.e. the offset
+// normal m = (a, b, 1) in the vertex's shading frame, GGX(alpha) by D(m) cos(theta_m):
+// tan(theta_m) = alpha sqrt(u1 / (1 - u1)), phi = 2 pi u2, with (u1, u2) = words 2(i&1),
+// 2(i&1)+1 of Philox (walk, purpose 11 + i/2, trial 0) -- once per walk, reused by trials
+__device__ __forceinline__ void glossy_slopes(const DScene &S, int surf, uint64_t seed, uint64_t wid, int i,
+                                              double &a, double &b) {
+    a = b = 0.0;
+    const float al = S.surf[surf].rough;
+    if (!(al > 0.0f)) return;
+    const uint4 r = rng_draw(seed, wid, 11u + (uint32_t)(i >> 1), 0u);
+    const double u1 = (double)u01((i & 1) ? r.z : r.x), u2 = (double)u01((i & 1) ? r.w : r.y);
+    const double tt = (double)al * sqrt(u1 / (1.0 - u1));
+    const double ph = 6.28318530717958647692 * u2;
+    a = tt * cos(ph);
+    b = tt * sin(ph);
+}
 
 // geometric normal (outward, R9)
 template <typename R> __device__ __forceinline__ V3<R> geo_normalR(const DScene &S, int prim, int surf, double3 p) {
@@ -110,15 +137,17 @@ template <typename R> __device__ __forceinline__ R fresnelR(R ci, R eta1, R eta2
 }
 
 template <typename R> struct VTermR {
-    V3<R> wi, wo, h, s, t;
+    V3<R> wi, wo, h, s, t, n;
     R li, lo, ei, eo, hl, hn;
+    R oa, ob;        // offset slopes (glossy, R37)
+    bool glossy;
     double c0, c1;
 };
 
 // residual always fp64 from fp64 positions (R24); the rest in R
 template <typename R>
 __device__ __forceinline__ bool vtermR(double3 a, double3 p, double3 b, V3<R> ng, V3<R> n, const DSurf &f, bool isT,
-                                       VTermR<R> &v) {
+                                       VTermR<R> &v, double oa = 0.0, double ob = 0.0) {
     double ax = a.x - p.x, ay = a.y - p.y, az = a.z - p.z;
     double bx = b.x - p.x, by = b.y - p.y, bz = b.z - p.z;
     double la2 = ax * ax + ay * ay + az * az, lb2 = bx * bx + by * by + bz * bz;
@@ -146,9 +175,18 @@ __device__ __forceinline__ bool vtermR(double3 a, double3 p, double3 b, V3<R> ng
     v.hl = (R)(hl2 * ih);
     v.h = mk3<R>((R)hx, (R)hy, (R)hz);
     onbR(n, v.s, v.t);
+    v.n = n;
     v.c0 = (double)v.s.x * hx + (double)v.s.y * hy + (double)v.s.z * hz;
     v.c1 = (double)v.t.x * hx + (double)v.t.y * hy + (double)v.t.z * hz;
     v.hn = dotR(v.h, n);
+    v.glossy = f.rough > 0.0f;
+    v.oa = (R)oa;
+    v.ob = (R)ob;
+    if (v.glossy) {  // h || m = (a, b, 1) in (s, t, n): C = (s.h - a n.h, t.h - b n.h) (R37)
+        const double hn = (double)n.x * hx + (double)n.y * hy + (double)n.z * hz;
+        v.c0 -= oa * hn;
+        v.c1 -= ob * hn;
+    }
     return true;
 }
 
@@ -159,12 +197,25 @@ __device__ __forceinline__ void dC_nbR(const VTermR<R> &v, V3<R> w, R l, R eta, 
     V3<R> dh = (u - v.h * dotR(v.h, u)) * ((R)1 / v.hl);
     o0 = dotR(v.s, dh);
     o1 = dotR(v.t, dh);
+    if (v.glossy) {
+        const R ndh = dotR(v.n, dh);
+        o0 -= v.oa * ndh;
+        o1 -= v.ob * ndh;
+    }
 }
 // dC along the vertex's own displacement (D block; minimal-rotation frame, R3)
 template <typename R>
 __device__ __forceinline__ void dC_selfR(const VTermR<R> &v, V3<R> dir, V3<R> dn, R &o0, R &o1) {
     V3<R> u = (dir - v.wi * dotR(v.wi, dir)) * (-v.ei / v.li) - (dir - v.wo * dotR(v.wo, dir)) * (v.eo / v.lo);
     V3<R> dh = (u - v.h * dotR(v.h, u)) * ((R)1 / v.hl);
+    if (v.glossy) {  // exact frame derivative and the offset terms (R37)
+        V3<R> ds, dt;
+        onb_dR(v.n, dn, ds, dt);
+        const R dhn = dotR(dn, v.h) + dotR(v.n, dh);
+        o0 = dotR(ds, v.h) + dotR(v.s, dh) - v.oa * dhn;
+        o1 = dotR(dt, v.h) + dotR(v.t, dh) - v.ob * dhn;
+        return;
+    }
     o0 = dotR(v.s, dh) - v.hn * dotR(v.s, dn);
     o1 = dotR(v.t, dh) - v.hn * dotR(v.t, dn);
 }
@@ -173,7 +224,8 @@ __device__ __forceinline__ void dC_selfR(const VTermR<R> &v, V3<R> dir, V3<R> dn
 // back substitution into world-space steps dq.  Returns 0 step, 1 converged,
 // 2 degenerate; `singular` flags a singular pivot (G is then 0 at convergence).
 template <int KMAX, typename R>
-__device__ __forceinline__ int newton_system(const DScene &S, int k, uint32_t tau, float3 xD, float3 xL,
+__device__ __forceinline__ int newton_system(const DScene &S, uint64_t seed, uint64_t wid, int k, uint32_t tau,
+                                             float3 xD, float3 xL,
                                              const double3 (&x)[KMAX], const int (&prim)[KMAX],
                                              const int (&surf)[KMAX], float tol, R (&Di)[KMAX][4], R (&Ub)[KMAX][4],
                                              V3<R> (&sg)[KMAX], V3<R> (&tg)[KMAX], V3<R> (&dq)[KMAX],
@@ -201,7 +253,9 @@ __device__ __forceinline__ int newton_system(const DScene &S, int k, uint32_t ta
         V3<R> dna, dnb;
         V3<R> n = shadingR<R>(S, pi, si, xi, sgi, tgi, dna, dnb);
         VTermR<R> v;
-        if (!vtermR<R>(a, xi, b, crossR(sgi, tgi), n, f, (tau >> i) & 1u, v)) { degen = true; break; }
+        double oa, ob;
+        glossy_slopes(S, si, seed, wid, i, oa, ob);
+        if (!vtermR<R>(a, xi, b, crossR(sgi, tgi), n, f, (tau >> i) & 1u, v, oa, ob)) { degen = true; break; }
         cmax = fmax(cmax, fmax(fabs(v.c0), fabs(v.c1)));
         // the two tangent directions (MPG_ROLL_DC: in a rolled loop, one copy of the block
         // code; A/B in DESIGN.md §4)
@@ -289,7 +343,8 @@ __device__ __forceinline__ int newton_system(const DScene &S, int k, uint32_t ta
 
 // sides (R8), kappa (R12) and the light-side block D_L at a converged chain
 template <int KMAX, typename R>
-__device__ MPG_COLD bool post_sweep(const DScene &S, const DLight &L, int k, uint32_t tau, float3 xD,
+__device__ MPG_COLD bool post_sweep(const DScene &S, uint64_t seed, uint64_t wid, const DLight &L, int k, uint32_t tau,
+                                           float3 xD,
                                            float3 xL, const double3 (&x)[KMAX], const int (&prim)[KMAX],
                                            const int (&surf)[KMAX], bool want_kappa, float &kappa, R (&DL)[4]) {
     R kap = 1, etaD = 1, etaL = 1;
@@ -308,13 +363,15 @@ __device__ MPG_COLD bool post_sweep(const DScene &S, const DLight &L, int k, uin
         if (!want_kappa) continue;
         V3<R> z = mk3<R>(0, 0, 0), dna, dnb;
         V3<R> n = shadingR<R>(S, pi, si, xi, z, z, dna, dnb);
+        double oa, ob;
+        glossy_slopes(S, si, seed, wid, i, oa, ob);
         bool oi = di > (R)0, oo = dd > (R)0;
         R e_wi = oi ? (R)f.eta_out : (R)f.eta_in, e_wo = oo ? (R)f.eta_out : (R)f.eta_in;
         if (i == 0) etaD = e_wi;
         if (i == k - 1) {
             etaL = e_wo;
             VTermR<R> v;
-            if (!vtermR<R>(a, xi, b, ng, n, f, isT, v)) { DL[0] = DL[1] = DL[2] = DL[3] = 0; }
+            if (!vtermR<R>(a, xi, b, ng, n, f, isT, v, oa, ob)) { DL[0] = DL[1] = DL[2] = DL[3] = 0; }
             else {
                 V3<R> l1, l2;
                 if (L.kind == 1) { l1 = fromf<R>(L.l1); l2 = fromf<R>(L.l2); }
@@ -327,7 +384,13 @@ __device__ MPG_COLD bool post_sweep(const DScene &S, const DLight &L, int k, uin
         else {
             R e_other = oi ? (R)f.eta_in : (R)f.eta_out;
             V3<R> wi = nrmR(fromd<R>(a - xi));
-            R F = fresnelR<R>(dotR(wi, n), e_wi, e_other);
+            V3<R> nm = n;
+            if (f.rough > 0.0f) {  // Fresnel at the micro-normal (offset normal, R37)
+                V3<R> s, t;
+                onbR(n, s, t);
+                nm = nrmR(n + s * (R)oa + t * (R)ob);
+            }
+            R F = fresnelR<R>(dotR(wi, nm), e_wi, e_other);
             kap *= isT ? ((R)1 - F) : F;
         }
     }

@@ -110,12 +110,20 @@ enum { SS_WALKS = 0, SS_CONV, SS_NEWTON, SS_PRIM_IT, SS_ATTEMPTS, SS_RAYS, SS_TR
 // fp32-rounded point tilted the deduced chain by ~1e-7 relative, which the long
 // halving sequences of configs[3] amplified into different outcomes, measured):
 // the deduced seed chain matches the oracle's to fp64 rounding.
-__device__ __forceinline__ bool scatter_dir(const DScene &S, double3 &dd, int prim, int surf, double3 p, bool isT) {
+__device__ __forceinline__ bool scatter_dir(const DScene &S, double3 &dd, int prim, int surf, double3 p, bool isT,
+                                            uint64_t seed, uint64_t wid, int vi) {
     const DSurf &f = S.surf[surf];
     const V3<double> ng = geo_normalR<double>(S, prim, surf, p);
     V3<double> dna, dnb;
     const V3<double> z0 = mk3<double>(0.0, 0.0, 0.0);
-    const V3<double> nf = shadingR<double>(S, prim, surf, p, z0, z0, dna, dnb);
+    V3<double> nf = shadingR<double>(S, prim, surf, p, z0, z0, dna, dnb);
+    if (f.rough > 0.0f) {  // scatter about the offset normal of vertex vi (R37)
+        double oa, ob;
+        glossy_slopes(S, surf, seed, wid, vi, oa, ob);
+        V3<double> s, t;
+        onbR(nf, s, t);
+        nf = nrmR(nf + s * oa + t * ob);
+    }
     double dx = dd.x, dy = dd.y, dz = dd.z, nx = nf.x, ny = nf.y, nz = nf.z;
     double il = rsqrt(nx * nx + ny * ny + nz * nz);
     nx *= il; ny *= il; nz *= il;
@@ -237,7 +245,8 @@ __device__ __forceinline__ int trace_chain(const DScene &S, int mode, int k, uin
                                            float3 xD, float3 xL, float3 tgt, const V3<R> (&dq)[KMAX], float beta,
                                            const double3 (&x)[KMAX], const int (&hint)[KMAX],
                                            uint32_t surf_req, float eps, double3 (&y)[KMAX], int (&yp)[KMAX],
-                                           int (&ys)[KMAX], LaneStats &st, uint32_t &tau_res, unsigned *s_rays) {
+                                           int (&ys)[KMAX], LaneStats &st, uint32_t &tau_res, unsigned *s_rays,
+                                           uint64_t seed, uint64_t wid) {
     const bool deduce = mode == TR_DEDUCE, vis = mode == TR_VIS;
     uint32_t res = 0;
     double3 o = d3f(xD);
@@ -269,7 +278,7 @@ __device__ __forceinline__ int trace_chain(const DScene &S, int mode, int k, uin
                 if (!(l2 > 0.0)) return 3 | (i << 4);
                 dd = v * rsqrt(l2);
             } else if (i > 0) {
-                if (!scatter_dir(S, dd, pprim, psurf, o, (res >> (i - 1)) & 1u)) return 4 | (i << 4);
+                if (!scatter_dir(S, dd, pprim, psurf, o, (res >> (i - 1)) & 1u, seed, wid, i - 1)) return 4 | (i << 4);
             }
             of = f3d(o);
             d = nrmz(f3d(dd));
@@ -593,7 +602,7 @@ __global__ void __launch_bounds__(128, MINB) k_walk(const DScene S, const SeedCt
             uint32_t tres = tau;
             const int mode = ded ? TR_DEDUCE : (phase == PH_VIS ? TR_VIS : TR_REPROJ);
             int why = trace_chain<KMAX, W, R>(S, mode, k, bits, learned, xD, xL, tgt, dq, beta, x, prim, sreq, P.ray_eps,
-                                              y, yp, ys, ls, tres, &s_rays[threadIdx.x]);
+                                              y, yp, ys, ls, tres, &s_rays[threadIdx.x], g.seed, P.walk_id_base + w);
             bool ok = why == 0;
             if (mode == TR_VIS) {
                 occluded = !ok;
@@ -632,7 +641,8 @@ __global__ void __launch_bounds__(128, MINB) k_walk(const DScene S, const SeedCt
                 bool singular = false;
                 R Di[KMAX][4], Ub[KMAX][4];      // transient: D'^-1_i, U_i of the block-Thomas sweep
                 V3<R> sg[KMAX], tg[KMAX];          // transient: tangent frames of the step
-                int r = newton_system<KMAX, R>(S, k, tau, xD, xL, x, prim, surf, P.tol, Di, Ub, sg, tg, dq, singular, cm);
+                int r = newton_system<KMAX, R>(S, g.seed, P.walk_id_base + w, k, tau, xD, xL, x, prim, surf, P.tol, Di, Ub,
+                                               sg, tg, dq, singular, cm);
                 if (P.dbg && trial == 0 && w < P.n_dbg && 2 * it + 1 < P.dbg_stride) {
                     P.dbg[w * P.dbg_stride + 2 * it] = cm;
                     P.dbg[w * P.dbg_stride + 2 * it + 1] = beta;
@@ -647,7 +657,8 @@ __global__ void __launch_bounds__(128, MINB) k_walk(const DScene S, const SeedCt
                         const DLight &L = S.light[lid];
                         float kap;
                         R DL[4];
-                        if (!post_sweep<KMAX, R>(S, L, k, tau, xD, xL, x, prim, surf, true, kap, DL)) {
+                        if (!post_sweep<KMAX, R>(S, g.seed, P.walk_id_base + w, L, k, tau, xD, xL, x, prim, surf, true, kap,
+                                                 DL)) {
                             end_status = ST_BAD_SIDE;
                         } else {
                             const float3 nD = xyz(__ldg(P.nD + w / P.spp));
@@ -727,7 +738,8 @@ __global__ void __launch_bounds__(128, MINB) k_walk(const DScene S, const SeedCt
                 float kdummy;
                 R DLdummy[4];
                 if (st == ST_CONVERGED && k == pk && tau == ptau &&
-                    post_sweep<KMAX, R>(S, S.light[lid], k, tau, xD, xL, x, prim, surf, false, kdummy, DLdummy)) {
+                    post_sweep<KMAX, R>(S, g.seed, P.walk_id_base + w, S.light[lid], k, tau, xD, xL, x, prim, surf, false,
+                                        kdummy, DLdummy)) {
                     same = true;
 #pragma unroll
                     for (int i = 0; i < KMAX; i++) {

@@ -34,7 +34,7 @@ class mpg_surface_desc(C.Structure):
                 ("reflectance", C.c_float), ("center", C.c_float * 3), ("radius", C.c_float),
                 ("origin", C.c_float * 3), ("edge_u", C.c_float * 3), ("edge_v", C.c_float * 3),
                 ("positions", C.c_void_p), ("normals", C.c_void_p), ("indices", C.c_void_p),
-                ("n_vertices", C.c_int32), ("n_triangles", C.c_int32)]
+                ("n_vertices", C.c_int32), ("n_triangles", C.c_int32), ("roughness", C.c_float)]
 
 
 class mpg_light_desc(C.Structure):
@@ -409,6 +409,7 @@ class DeviceScene:
             d = mpg_surface_desc()
             d.kind, d.mat = s.kind, s.mat
             d.eta_in, d.eta_out, d.reflectance, d.radius = s.eta_in, s.eta_out, s.reflectance, s.radius
+            d.roughness = float(getattr(s, "roughness", 0.0))
             d.center, d.origin, d.edge_u, d.edge_v = _f3(s.center), _f3(s.origin), _f3(s.edge_u), _f3(s.edge_v)
             if s.kind == W.SURF_MESH:
                 P = np.ascontiguousarray(s.positions, np.float32)

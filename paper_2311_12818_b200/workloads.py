@@ -47,6 +47,7 @@ class Surface:
     positions: Optional[np.ndarray] = None   # float32 [nv,3]
     normals: Optional[np.ndarray] = None     # float32 [nv,3] shading normals (outward)
     indices: Optional[np.ndarray] = None     # int32 [nt,3]
+    roughness: float = 0.0                   # GGX alpha of a glossy specular surface (0: pure specular, R37)
 
 
 @dataclasses.dataclass
@@ -349,41 +350,47 @@ OCCLUDERS_0V = (((-0.2, 2.5, -1.0), (1.6, 0.0, 0.0), (0.0, 0.0, 1.4)),
                 ((1.0, -1.25, 0.5), (1.5, 0.0, 0.0), (0.0, 0.0, 1.5)))
 
 
-def config0(n_side: int = 64, spp: int = 16, occluders: bool = False) -> Workload:
+def config0(n_side: int = 64, spp: int = 16, occluders: bool = False, roughness: float = 0.0) -> Workload:
     """configs[0]: k=1 R off an analytic mirror sphere r=1 at the origin, point
     light (0,4,0), 64x64 receivers on y=-1.5 over [-3,3]^2, 16 cap seeds each.
     `occluders=True` is twin 0v: the same scene plus the two opaque diffuse
     rectangles OCCLUDERS_0V, where visibility has a closed form (an
-    Alhazen chain is occluded iff one of its two segments crosses a rectangle)."""
-    sph = Surface(SURF_SPHERE, MAT_CONDUCTOR, reflectance=1.0, center=(0.0, 0.0, 0.0), radius=1.0)
+    Alhazen chain is occluded iff one of its two segments crosses a rectangle).
+    `roughness` > 0 is the glossy twin 0g (GGX alpha; offset normals, R37)."""
+    sph = Surface(SURF_SPHERE, MAT_CONDUCTOR, reflectance=1.0, center=(0.0, 0.0, 0.0), radius=1.0,
+                  roughness=roughness)
     surfs = [sph]
     if occluders:
         surfs += [Surface(SURF_QUAD, MAT_DIFFUSE, origin=o, edge_u=u, edge_v=v) for o, u, v in OCCLUDERS_0V]
     light = Light(LIGHT_POINT, 1.0, position=(0.0, 4.0, 0.0))
     xD, nD = receiver_grid(-3.0, 3.0, n_side, -1.5)
-    return Workload("cfg0_sphere_mirror_k1" + ("_occluded" if occluders else ""), surfs, [light], xD, nD, spp,
+    return Workload("cfg0_sphere_mirror_k1" + ("_occluded" if occluders else "") + ("_glossy" if roughness else ""),
+                    surfs, [light], xD, nD, spp,
                     SeedSpec(SEED_CAP, surf_id=0, k=1, tau=0b0),
                     WalkOpts(max_iters=20), recv_shape=(n_side, n_side))
 
 
-def config1(n_side: int = 1024, spp: int = 1, analytic: bool = False) -> Workload:
+def config1(n_side: int = 1024, spp: int = 1, analytic: bool = False, roughness: float = 0.0) -> Workload:
     """configs[1]: k=2 TT through a glass icosphere (L4, Phong normals, eta 1.5),
     unit square area light at y=5, 1024^2 receivers on y=-1.2 over [-2,2]^2,
     1 seed per receiver, uniform over front-facing triangles.
     `analytic=True` is twin 1a (analytic glass sphere, cap seeds) for closed-form pins."""
     if analytic:
-        s = Surface(SURF_SPHERE, MAT_DIELECTRIC, eta_in=1.5, eta_out=1.0, center=(0.0, 0.0, 0.0), radius=1.0)
+        s = Surface(SURF_SPHERE, MAT_DIELECTRIC, eta_in=1.5, eta_out=1.0, center=(0.0, 0.0, 0.0), radius=1.0,
+                    roughness=roughness)
         seed = SeedSpec(SEED_CAP, surf_id=0, k=2, tau=0b11)
     else:
         P, N, F = icosphere(4)
-        s = Surface(SURF_MESH, MAT_DIELECTRIC, eta_in=1.5, eta_out=1.0, positions=P, normals=N, indices=F)
+        s = Surface(SURF_MESH, MAT_DIELECTRIC, eta_in=1.5, eta_out=1.0, positions=P, normals=N, indices=F,
+                    roughness=roughness)
         seed = SeedSpec(SEED_TRIANGLE, surf_id=0, k=2, tau=0b11)
     light = Light(LIGHT_QUAD, 1.0, position=(0.0, 5.0, 0.0), edge_u=(1.0, 0.0, 0.0), edge_v=(0.0, 0.0, 1.0))
     xD, nD = receiver_grid(-2.0, 2.0, n_side, -1.2)
     # fp64 Jacobian / step (R24): with fp32 steps 4 of 3,000 sampled full-size walks (99.87 %)
     # and 1 of 16,384 at 128^2 ended differently from the fp64 oracle without a basin boundary
     # (chaotic halving sequences amplify the fp32 step's rounding); fp64 steps: 100 %
-    return Workload("cfg1_glass_icosphere_k2" + ("_analytic" if analytic else ""), [s], [light], xD, nD,
+    return Workload("cfg1_glass_icosphere_k2" + ("_analytic" if analytic else "") + ("_glossy" if roughness else ""),
+                    [s], [light], xD, nD,
                     spp, seed, WalkOpts(max_iters=20, flags=FLAG_NEWTON_F64), recv_shape=(n_side, n_side))
 
 

@@ -123,15 +123,18 @@ def tile_means(wv, spp, recv_shape, tile):
     return a.mean(1), a.std(1, ddof=1), a.shape[1]
 
 
-def classify_boundary(s, w, o, ids, extent, max_n=300, seed=0):
+def classify_boundary(s, w, o, ids, extent, max_n=300, seed=0, offsets=None):
     """Reading R18: a flag disagreement is a basin/budget boundary case if the
     oracle's own outcome changes under one of 8 seed-target perturbations of
-    1e-4 x extent, or under max_iters +- 3.  Returns (n_boundary, n_checked, non_boundary_ids)."""
+    1e-4 x extent, or under max_iters +- 3.  Returns (n_boundary, n_checked, non_boundary_ids).
+    offsets(walk) -> [k, 2] offset uniforms of a glossy walk (R37), set for its re-runs."""
     rng = np.random.default_rng(seed)
     pos = {int(x): j for j, x in enumerate(o["walk"])}
     nb, bad = 0, []
     for i in list(ids)[:max_n]:
         j = pos[int(i)]
+        if offsets is not None:
+            O.set_offset_uv(offsets(int(i)))
         xD = w.xD[int(i) // w.spp].astype(np.float64)
         base = o["status"][j] in (0, 5)
         tgt = o["target"][j].astype(np.float64)
@@ -152,4 +155,6 @@ def classify_boundary(s, w, o, ids, extent, max_n=300, seed=0):
         nb += changed
         if not changed:
             bad.append(int(i))
+    if offsets is not None:
+        O.set_offset_uv(None)
     return nb, min(len(ids), max_n), bad

@@ -823,3 +823,29 @@ def test_repeated_reciprocal_estimates(which, flags):
     assert rep["flag_agree"] >= 0.999 and agree >= 0.98
     same = both & (g4["trials"] == o["trials"])
     assert np.median(np.abs(g4["w"][same] - o["w"][same]) / np.maximum(o["w"][same], 1e-30)) < 1e-4
+
+
+@pytest.mark.parametrize("which", ["sphere", "glass_sphere", "icosphere"])
+def test_glossy_chain_parity(which):
+    """Glossy chains via sampled offset normals (R37): GPU == oracle on glossy twins
+    (same per-walk offsets from Philox purpose 11 + i/2), at the north_star bar."""
+    from tests.test_glossy_oracle import walk_uv
+    w = {"sphere": lambda: W.config0(n_side=48, spp=8, roughness=0.3),
+         "glass_sphere": lambda: W.config1(n_side=64, spp=2, analytic=True, roughness=0.15),
+         "icosphere": lambda: W.config1(n_side=96, spp=1, roughness=0.1)}[which]()
+    g, st, ext = PY.run_gpu(w, flags=w.opts.flags | BENCH_FLAGS)
+    ids = np.arange(w.n_walks)
+    o, s = PY.run_oracle(w, ids)
+    rep = PY.compare(g, o, ids, ext, w.seed.k, w=w)
+    print({k: v for k, v in rep.items() if not isinstance(v, np.ndarray)})
+    assert rep["conv_orc"] > 500
+    assert rep["flag_agree"] >= 0.999 and rep["vis_agree"] >= 0.999 and not rep["prim_bad"]
+    assert rep["n_other_chain"] <= max(1, 0.001 * rep["both"])
+    if len(rep["disagree_ids"]):
+        nb, nc, bad = PY.classify_boundary(s, w, o, rep["disagree_ids"], ext,
+                                           offsets=lambda i: walk_uv(w, [i], w.seed.k)[0])
+        print(f"boundary {nb}/{nc}; non-boundary walks: {bad}")
+        assert not bad
+    both = (g["status"] == 0) & (o["status"] == 0)
+    rg = np.abs(g["G"][both] - o["G"][both]) / np.maximum(o["G"][both], 1e-30)
+    assert np.quantile(rg, 0.99) < 1e-3
