@@ -831,8 +831,8 @@ def test_glossy_chain_parity(which):
     (same per-walk offsets from Philox purpose 11 + i/2), at the north_star bar."""
     from tests.test_glossy_oracle import walk_uv
     w = {"sphere": lambda: W.config0(n_side=48, spp=8, roughness=0.3),
-         "glass_sphere": lambda: W.config1(n_side=64, spp=2, analytic=True, roughness=0.15),
-         "icosphere": lambda: W.config1(n_side=96, spp=1, roughness=0.1)}[which]()
+         "glass_sphere": lambda: W.config1(n_side=96, spp=2, analytic=True, roughness=0.15),
+         "icosphere": lambda: W.config1(n_side=128, spp=1, roughness=0.1)}[which]()
     g, st, ext = PY.run_gpu(w, flags=w.opts.flags | BENCH_FLAGS)
     ids = np.arange(w.n_walks)
     o, s = PY.run_oracle(w, ids)
