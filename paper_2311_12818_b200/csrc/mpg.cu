@@ -54,6 +54,7 @@ struct mpg_scene {
     size_t bytes = 0;
     size_t trav_bytes = 0;  // nodes + triangle positions, contiguous from d.nodes
     int n_vert = 0;
+    bool glossy = false;    // a surface has roughness > 0: the walk runs the glossy kernels (R37)
 };
 
 struct StreeState;
@@ -266,6 +267,7 @@ extern "C" mpg_status mpg_scene_create(const mpg_surface_desc *surfaces, int32_t
         f.refl = sd.reflectance;
         if (!(sd.roughness >= 0.f)) { mpg_scene_destroy(s); return fail(MPG_ERR_INVALID_ARG, "roughness must be >= 0"); }
         f.rough = sd.roughness;
+        if (sd.roughness > 0.f) s->glossy = true;
         f.radius = sd.radius;
         f.center = F3(H(sd.center));
         f.origin = F3(H(sd.origin));
@@ -1200,7 +1202,8 @@ static size_t l2_persist_bytes() {
     return (size_t)v;
 }
 
-template <int KMAX, typename R, int MINB = (KMAX <= 2 ? MPG_WALK_MINB2 : MPG_WALK_MINB_LONG)>
+template <int KMAX, typename R, int MINB = (KMAX <= 2 ? MPG_WALK_MINB2 : MPG_WALK_MINB_LONG), bool GL = false,
+          bool CMP = false>
 static mpg_status launch_walk(const DScene &S, const SeedCtx &g, WalkParams P, cudaStream_t st, void *ws,
                               bool sort) {
     const bool wide = S.bvh_w == 4;
@@ -1212,11 +1215,11 @@ static mpg_status launch_walk(const DScene &S, const SeedCtx &g, WalkParams P, c
         // L1/shared array can cache nodes and the lanes' local memory
         if (const char *e = getenv("MPG_CARVEOUT")) {
             int pc = atoi(e);
-            CUDA_TRY(cudaFuncSetAttribute(k_walk<KMAX, R, 4, MINB>, cudaFuncAttributePreferredSharedMemoryCarveout, pc));
-            CUDA_TRY(cudaFuncSetAttribute(k_walk<KMAX, R, 2, MINB>, cudaFuncAttributePreferredSharedMemoryCarveout, pc));
+            CUDA_TRY(cudaFuncSetAttribute(k_walk<KMAX, R, 4, MINB, GL, CMP>, cudaFuncAttributePreferredSharedMemoryCarveout, pc));
+            CUDA_TRY(cudaFuncSetAttribute(k_walk<KMAX, R, 2, MINB, GL, CMP>, cudaFuncAttributePreferredSharedMemoryCarveout, pc));
         }
         CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-            &occ, wide ? k_walk<KMAX, R, 4, MINB> : k_walk<KMAX, R, 2, MINB>, 128, 0));
+            &occ, wide ? k_walk<KMAX, R, 4, MINB, GL, CMP> : k_walk<KMAX, R, 2, MINB, GL, CMP>, 128, 0));
         if (occ <= 0) occ = 1;
     }
     MKLayout L = mk_layout(P.n);
@@ -1296,8 +1299,8 @@ static mpg_status launch_walk(const DScene &S, const SeedCtx &g, WalkParams P, c
         attr[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
         cfg.numAttrs = 1;
     }
-    if (wide) CUDA_TRY(cudaLaunchKernelEx(&cfg, k_walk<KMAX, R, 4, MINB>, S, g, P));
-    else CUDA_TRY(cudaLaunchKernelEx(&cfg, k_walk<KMAX, R, 2, MINB>, S, g, P));
+    if (wide) CUDA_TRY(cudaLaunchKernelEx(&cfg, k_walk<KMAX, R, 4, MINB, GL, CMP>, S, g, P));
+    else CUDA_TRY(cudaLaunchKernelEx(&cfg, k_walk<KMAX, R, 2, MINB, GL, CMP>, S, g, P));
     CUDA_TRY(cudaPeekAtLastError());
     return MPG_OK;
 }
@@ -1396,23 +1399,35 @@ static mpg_status walk_dispatch(const mpg_scene *scene, const SeedCtx &g, const 
                                 const mpg_walk_opts *o, const WalkParams &P, void *workspace, size_t workspace_bytes,
                                 cudaStream_t s) {
     const int k = g.k;
-    if (o->flags & MPG_FLAG_NEWTON_F64) {
-        if (k <= 1) return launch_walk<1, double>(scene->d, g, P, s, workspace, (o->flags & MPG_FLAG_SORT) != 0);
-        if (k <= 2) return launch_walk<2, double>(scene->d, g, P, s, workspace, (o->flags & MPG_FLAG_SORT) != 0);
-        if (k <= 4) return launch_walk<4, double>(scene->d, g, P, s, workspace, (o->flags & MPG_FLAG_SORT) != 0);
-        if (k <= 6) {
-            if (sd->mode >= MPG_SEED_GUIDE_DIR)   // mixed chain lengths: see MPG_WALK_MINB_MIXED
-                return launch_walk<6, double, MPG_WALK_MINB_MIXED>(scene->d, g, P, s, workspace,
-                                                                   (o->flags & MPG_FLAG_SORT) != 0);
-            return launch_walk<6, double>(scene->d, g, P, s, workspace, (o->flags & MPG_FLAG_SORT) != 0);
+    const bool sort = (o->flags & MPG_FLAG_SORT) != 0, f64 = (o->flags & MPG_FLAG_NEWTON_F64) != 0;
+    if (scene->glossy) {   // glossy chains (R37): kernels with the offset-normal code, k <= 6
+        if (k > 6) return fail(MPG_ERR_UNSUPPORTED, "glossy chains support k <= 6");
+        if (f64) {
+            if (k <= 2) return launch_walk<2, double, MPG_WALK_MINB2, true>(scene->d, g, P, s, workspace, sort);
+            return launch_walk<6, double, MPG_WALK_MINB_LONG, true>(scene->d, g, P, s, workspace, sort);
         }
-        return launch_walk<8, double>(scene->d, g, P, s, workspace, (o->flags & MPG_FLAG_SORT) != 0);
+        if (k <= 2) return launch_walk<2, float, MPG_WALK_MINB2, true>(scene->d, g, P, s, workspace, sort);
+        return launch_walk<6, float, MPG_WALK_MINB_LONG, true>(scene->d, g, P, s, workspace, sort);
     }
-    if (k <= 1) return launch_walk<1, float>(scene->d, g, P, s, workspace, (o->flags & MPG_FLAG_SORT) != 0);
-    if (k <= 2) return launch_walk<2, float>(scene->d, g, P, s, workspace, (o->flags & MPG_FLAG_SORT) != 0);
-    if (k <= 4) return launch_walk<4, float>(scene->d, g, P, s, workspace, (o->flags & MPG_FLAG_SORT) != 0);
-    if (k <= 6) return launch_walk<6, float>(scene->d, g, P, s, workspace, (o->flags & MPG_FLAG_SORT) != 0);
-    return launch_walk<8, float>(scene->d, g, P, s, workspace, (o->flags & MPG_FLAG_SORT) != 0);
+    if (f64) {
+        if (k <= 1) return launch_walk<1, double>(scene->d, g, P, s, workspace, sort);
+        if (k <= 2) return launch_walk<2, double>(scene->d, g, P, s, workspace, sort);
+        if (k <= 4) return launch_walk<4, double>(scene->d, g, P, s, workspace, sort);
+        if (k <= 6) {
+            // mixed chain lengths (configs[4]): see MPG_WALK_MINB_MIXED; compacted trace rounds
+            // (MPG_COMPACT) measured faster there only
+            if (sd->mode >= MPG_SEED_GUIDE_DIR)
+                return launch_walk<6, double, MPG_WALK_MINB_MIXED, false, MPG_COMPACT != 0>(scene->d, g, P, s,
+                                                                                          workspace, sort);
+            return launch_walk<6, double>(scene->d, g, P, s, workspace, sort);
+        }
+        return launch_walk<8, double>(scene->d, g, P, s, workspace, sort);
+    }
+    if (k <= 1) return launch_walk<1, float>(scene->d, g, P, s, workspace, sort);
+    if (k <= 2) return launch_walk<2, float>(scene->d, g, P, s, workspace, sort);
+    if (k <= 4) return launch_walk<4, float>(scene->d, g, P, s, workspace, sort);
+    if (k <= 6) return launch_walk<6, float>(scene->d, g, P, s, workspace, sort);
+    return launch_walk<8, float>(scene->d, g, P, s, workspace, sort);
 }
 
 // ----------------------------------------------------------------------------

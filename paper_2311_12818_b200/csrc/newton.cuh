@@ -136,7 +136,7 @@ template <typename R> __device__ __forceinline__ R fresnelR(R ci, R eta1, R eta2
     return (R)0.5 * (rs * rs + rp * rp);
 }
 
-template <typename R> struct VTermR {
+template <typename R, bool GL> struct VTermR {
     V3<R> wi, wo, h, s, t, n;
     R li, lo, ei, eo, hl, hn;
     R oa, ob;        // offset slopes (glossy, R37)
@@ -145,9 +145,9 @@ template <typename R> struct VTermR {
 };
 
 // residual always fp64 from fp64 positions (R24); the rest in R
-template <typename R>
+template <typename R, bool GL>
 __device__ __forceinline__ bool vtermR(double3 a, double3 p, double3 b, V3<R> ng, V3<R> n, const DSurf &f, bool isT,
-                                       VTermR<R> &v, double oa = 0.0, double ob = 0.0) {
+                                       VTermR<R, GL> &v, double oa = 0.0, double ob = 0.0) {
     double ax = a.x - p.x, ay = a.y - p.y, az = a.z - p.z;
     double bx = b.x - p.x, by = b.y - p.y, bz = b.z - p.z;
     double la2 = ax * ax + ay * ay + az * az, lb2 = bx * bx + by * by + bz * bz;
@@ -175,10 +175,11 @@ __device__ __forceinline__ bool vtermR(double3 a, double3 p, double3 b, V3<R> ng
     v.hl = (R)(hl2 * ih);
     v.h = mk3<R>((R)hx, (R)hy, (R)hz);
     onbR(n, v.s, v.t);
-    v.n = n;
     v.c0 = (double)v.s.x * hx + (double)v.s.y * hy + (double)v.s.z * hz;
     v.c1 = (double)v.t.x * hx + (double)v.t.y * hy + (double)v.t.z * hz;
     v.hn = dotR(v.h, n);
+    if constexpr (GL) {
+    v.n = n;
     v.glossy = f.rough > 0.0f;
     v.oa = (R)oa;
     v.ob = (R)ob;
@@ -187,34 +188,39 @@ __device__ __forceinline__ bool vtermR(double3 a, double3 p, double3 b, V3<R> ng
         v.c0 -= oa * hn;
         v.c1 -= ob * hn;
     }
+    }
     return true;
 }
 
 // dC along a neighbour displacement (L, U, D_L blocks)
-template <typename R>
-__device__ __forceinline__ void dC_nbR(const VTermR<R> &v, V3<R> w, R l, R eta, V3<R> dir, R &o0, R &o1) {
+template <typename R, bool GL>
+__device__ __forceinline__ void dC_nbR(const VTermR<R, GL> &v, V3<R> w, R l, R eta, V3<R> dir, R &o0, R &o1) {
     V3<R> u = (dir - w * dotR(w, dir)) * (eta / l);
     V3<R> dh = (u - v.h * dotR(v.h, u)) * ((R)1 / v.hl);
     o0 = dotR(v.s, dh);
     o1 = dotR(v.t, dh);
-    if (v.glossy) {
-        const R ndh = dotR(v.n, dh);
-        o0 -= v.oa * ndh;
-        o1 -= v.ob * ndh;
+    if constexpr (GL) {
+        if (v.glossy) {
+            const R ndh = dotR(v.n, dh);
+            o0 -= v.oa * ndh;
+            o1 -= v.ob * ndh;
+        }
     }
 }
 // dC along the vertex's own displacement (D block; minimal-rotation frame, R3)
-template <typename R>
-__device__ __forceinline__ void dC_selfR(const VTermR<R> &v, V3<R> dir, V3<R> dn, R &o0, R &o1) {
+template <typename R, bool GL>
+__device__ __forceinline__ void dC_selfR(const VTermR<R, GL> &v, V3<R> dir, V3<R> dn, R &o0, R &o1) {
     V3<R> u = (dir - v.wi * dotR(v.wi, dir)) * (-v.ei / v.li) - (dir - v.wo * dotR(v.wo, dir)) * (v.eo / v.lo);
     V3<R> dh = (u - v.h * dotR(v.h, u)) * ((R)1 / v.hl);
-    if (v.glossy) {  // exact frame derivative and the offset terms (R37)
-        V3<R> ds, dt;
-        onb_dR(v.n, dn, ds, dt);
-        const R dhn = dotR(dn, v.h) + dotR(v.n, dh);
-        o0 = dotR(ds, v.h) + dotR(v.s, dh) - v.oa * dhn;
-        o1 = dotR(dt, v.h) + dotR(v.t, dh) - v.ob * dhn;
-        return;
+    if constexpr (GL) {
+        if (v.glossy) {  // exact frame derivative and the offset terms (R37)
+            V3<R> ds, dt;
+            onb_dR(v.n, dn, ds, dt);
+            const R dhn = dotR(dn, v.h) + dotR(v.n, dh);
+            o0 = dotR(ds, v.h) + dotR(v.s, dh) - v.oa * dhn;
+            o1 = dotR(dt, v.h) + dotR(v.t, dh) - v.ob * dhn;
+            return;
+        }
     }
     o0 = dotR(v.s, dh) - v.hn * dotR(v.s, dn);
     o1 = dotR(v.t, dh) - v.hn * dotR(v.t, dn);
@@ -223,7 +229,7 @@ __device__ __forceinline__ void dC_selfR(const VTermR<R> &v, V3<R> dir, V3<R> dn
 // Forward sweep (constraint + blocks + block-Thomas) and, if not converged,
 // back substitution into world-space steps dq.  Returns 0 step, 1 converged,
 // 2 degenerate; `singular` flags a singular pivot (G is then 0 at convergence).
-template <int KMAX, typename R>
+template <int KMAX, typename R, bool GL>
 __device__ __forceinline__ int newton_system(const DScene &S, uint64_t seed, uint64_t wid, int k, uint32_t tau,
                                              float3 xD, float3 xL,
                                              const double3 (&x)[KMAX], const int (&prim)[KMAX],
@@ -252,10 +258,10 @@ __device__ __forceinline__ int newton_system(const DScene &S, uint64_t seed, uin
         const DSurf &f = S.surf[si];
         V3<R> dna, dnb;
         V3<R> n = shadingR<R>(S, pi, si, xi, sgi, tgi, dna, dnb);
-        VTermR<R> v;
-        double oa, ob;
-        glossy_slopes(S, si, seed, wid, i, oa, ob);
-        if (!vtermR<R>(a, xi, b, crossR(sgi, tgi), n, f, (tau >> i) & 1u, v, oa, ob)) { degen = true; break; }
+        VTermR<R, GL> v;
+        double oa = 0.0, ob = 0.0;
+        if constexpr (GL) glossy_slopes(S, si, seed, wid, i, oa, ob);
+        if (!vtermR<R, GL>(a, xi, b, crossR(sgi, tgi), n, f, (tau >> i) & 1u, v, oa, ob)) { degen = true; break; }
         cmax = fmax(cmax, fmax(fabs(v.c0), fabs(v.c1)));
         // the two tangent directions (MPG_ROLL_DC: in a rolled loop, one copy of the block
         // code; A/B in DESIGN.md §4)
@@ -342,7 +348,7 @@ __device__ __forceinline__ int newton_system(const DScene &S, uint64_t seed, uin
 }
 
 // sides (R8), kappa (R12) and the light-side block D_L at a converged chain
-template <int KMAX, typename R>
+template <int KMAX, typename R, bool GL>
 __device__ MPG_COLD bool post_sweep(const DScene &S, uint64_t seed, uint64_t wid, const DLight &L, int k, uint32_t tau,
                                            float3 xD,
                                            float3 xL, const double3 (&x)[KMAX], const int (&prim)[KMAX],
@@ -363,15 +369,15 @@ __device__ MPG_COLD bool post_sweep(const DScene &S, uint64_t seed, uint64_t wid
         if (!want_kappa) continue;
         V3<R> z = mk3<R>(0, 0, 0), dna, dnb;
         V3<R> n = shadingR<R>(S, pi, si, xi, z, z, dna, dnb);
-        double oa, ob;
-        glossy_slopes(S, si, seed, wid, i, oa, ob);
+        double oa = 0.0, ob = 0.0;
+        if constexpr (GL) glossy_slopes(S, si, seed, wid, i, oa, ob);
         bool oi = di > (R)0, oo = dd > (R)0;
         R e_wi = oi ? (R)f.eta_out : (R)f.eta_in, e_wo = oo ? (R)f.eta_out : (R)f.eta_in;
         if (i == 0) etaD = e_wi;
         if (i == k - 1) {
             etaL = e_wo;
-            VTermR<R> v;
-            if (!vtermR<R>(a, xi, b, ng, n, f, isT, v, oa, ob)) { DL[0] = DL[1] = DL[2] = DL[3] = 0; }
+            VTermR<R, GL> v;
+            if (!vtermR<R, GL>(a, xi, b, ng, n, f, isT, v, oa, ob)) { DL[0] = DL[1] = DL[2] = DL[3] = 0; }
             else {
                 V3<R> l1, l2;
                 if (L.kind == 1) { l1 = fromf<R>(L.l1); l2 = fromf<R>(L.l2); }
@@ -385,7 +391,7 @@ __device__ MPG_COLD bool post_sweep(const DScene &S, uint64_t seed, uint64_t wid
             R e_other = oi ? (R)f.eta_in : (R)f.eta_out;
             V3<R> wi = nrmR(fromd<R>(a - xi));
             V3<R> nm = n;
-            if (f.rough > 0.0f) {  // Fresnel at the micro-normal (offset normal, R37)
+            if (GL && f.rough > 0.0f) {  // Fresnel at the micro-normal (offset normal, R37)
                 V3<R> s, t;
                 onbR(n, s, t);
                 nm = nrmR(n + s * (R)oa + t * (R)ob);

@@ -32,6 +32,13 @@
 #ifndef MPG_WALK_MINB_MIXED
 #define MPG_WALK_MINB_MIXED 3  // per-sample chain length (configs[4]; 2/3/4: 261/255/271 ms)
 #endif
+// MPG_COMPACT: block-synchronous passes whose chain rays are traced in compacted
+// rounds -- every lane that needs a ray writes it to a shared-memory slot, the
+// block's threads trace the slots in order (full warps), and the lanes read their
+// hits back -- instead of each lane tracing its own ray inside its warp
+#ifndef MPG_COMPACT
+#define MPG_COMPACT 1
+#endif
 #include "device_common.cuh"
 #include "seed.cuh"
 #include "newton.cuh"
@@ -110,6 +117,7 @@ enum { SS_WALKS = 0, SS_CONV, SS_NEWTON, SS_PRIM_IT, SS_ATTEMPTS, SS_RAYS, SS_TR
 // fp32-rounded point tilted the deduced chain by ~1e-7 relative, which the long
 // halving sequences of configs[3] amplified into different outcomes, measured):
 // the deduced seed chain matches the oracle's to fp64 rounding.
+template <bool GL>
 __device__ __forceinline__ bool scatter_dir(const DScene &S, double3 &dd, int prim, int surf, double3 p, bool isT,
                                             uint64_t seed, uint64_t wid, int vi) {
     const DSurf &f = S.surf[surf];
@@ -117,7 +125,7 @@ __device__ __forceinline__ bool scatter_dir(const DScene &S, double3 &dd, int pr
     V3<double> dna, dnb;
     const V3<double> z0 = mk3<double>(0.0, 0.0, 0.0);
     V3<double> nf = shadingR<double>(S, prim, surf, p, z0, z0, dna, dnb);
-    if (f.rough > 0.0f) {  // scatter about the offset normal of vertex vi (R37)
+    if (GL && f.rough > 0.0f) {  // scatter about the offset normal of vertex vi (R37)
         double oa, ob;
         glossy_slopes(S, surf, seed, wid, vi, oa, ob);
         V3<double> s, t;
@@ -240,7 +248,7 @@ enum { TR_REPROJ = 0, TR_DEDUCE = 1, TR_VIS = 2 };
 // visibility traversal).
 // Reprojection targets q_i = x_i + beta dq_i are formed here from the chain and its
 // step (no q array survives between the Newton step and the trace).
-template <int KMAX, int W, typename R>
+template <int KMAX, int W, typename R, bool GL>
 __device__ __forceinline__ int trace_chain(const DScene &S, int mode, int k, uint32_t bits, bool learned,
                                            float3 xD, float3 xL, float3 tgt, const V3<R> (&dq)[KMAX], float beta,
                                            const double3 (&x)[KMAX], const int (&hint)[KMAX],
@@ -278,7 +286,7 @@ __device__ __forceinline__ int trace_chain(const DScene &S, int mode, int k, uin
                 if (!(l2 > 0.0)) return 3 | (i << 4);
                 dd = v * rsqrt(l2);
             } else if (i > 0) {
-                if (!scatter_dir(S, dd, pprim, psurf, o, (res >> (i - 1)) & 1u, seed, wid, i - 1)) return 4 | (i << 4);
+                if (!scatter_dir<GL>(S, dd, pprim, psurf, o, (res >> (i - 1)) & 1u, seed, wid, i - 1)) return 4 | (i << 4);
             }
             of = f3d(o);
             d = nrmz(f3d(dd));
@@ -384,8 +392,18 @@ __device__ __forceinline__ unsigned long long gtimer() {
 }
 #endif
 
-template <int KMAX, typename R, int W, int MINB>
+// GL: glossy scenes (offset normals, R37) -- the glossy code is compiled only into the kernels
+// for scenes with a rough surface; CMP: compacted trace rounds (MPG_COMPACT above)
+template <int KMAX, typename R, int W, int MINB, bool GL, bool CMP>
 __global__ void __launch_bounds__(128, MINB) k_walk(const DScene S, const SeedCtx g, const WalkParams P) {
+    // ray slots of the compacted trace rounds (CMP): origin + tmax, direction + mode, hint;
+    // hits: point, primitive + surface
+    constexpr int NS = CMP ? 128 : 1;
+    __shared__ float4 s_ro[NS], s_rd[NS], s_hp[NS];
+    __shared__ int2 s_hs[NS];
+    __shared__ int s_rh[NS];
+    __shared__ int s_wcnt[4];
+    const int warp = threadIdx.x >> 5;
     // per-block walk counters in 32 bits (native shared atomics; 64-bit shared atomicAdd
     // compiles to a CAS loop): a block makes at most ~2^25 walks final per launch
     __shared__ unsigned s_stats[SS_N];
@@ -532,12 +550,25 @@ __global__ void __launch_bounds__(128, MINB) k_walk(const DScene S, const SeedCt
                 phase = PH_IDLE;
             }
         }
+        if constexpr (!CMP) {
         const unsigned wst = __reduce_and_sync(MPG_FULL, (phase == PH_IDLE ? 1u : 0u) |
                                                           (phase == PH_IDLE || phase == PH_WAIT ? 2u : 0u));
         if (wst & 1u) break;
         if (wst & 2u) {
             // the whole warp waits for trial items: back off (polling lanes would
             // otherwise flood L2 while the remaining lanes finish their walks)
+            __nanosleep(backoff);
+            backoff = min(2u * backoff, P.backoff_max);
+            continue;
+        }
+        backoff = 256u;
+        }
+        }
+        if constexpr (CMP) {
+        // block-synchronous passes: the block stops when every lane is idle and backs off
+        // while every lane waits for trial items
+        if (__syncthreads_and(phase == PH_IDLE)) break;
+        if (__syncthreads_and(phase == PH_IDLE || phase == PH_WAIT)) {
             __nanosleep(backoff);
             backoff = min(2u * backoff, P.backoff_max);
             continue;
@@ -594,16 +625,147 @@ __global__ void __launch_bounds__(128, MINB) k_walk(const DScene S, const SeedCt
         }
 #endif
         // ---- trace: deduction (Eq. 6) or reprojection --------------------
-        if (phase == PH_DEDUCE || phase == PH_REPROJ || phase == PH_VIS) {
-            bool ded = phase == PH_DEDUCE;
+        const bool tracing = phase == PH_DEDUCE || phase == PH_REPROJ || phase == PH_VIS;
+        const int tmode = phase == PH_DEDUCE ? TR_DEDUCE : (phase == PH_VIS ? TR_VIS : TR_REPROJ);
+        int why = 0;
+        uint32_t tres = tau;
+        if constexpr (CMP) {
+        // The lane's k (or k+1 visibility) rays are traced in rounds: ray i of every
+        // tracing lane of the block goes to a shared slot, the block's first M threads
+        // trace the M slots (warps start full), and each lane consumes its hit (the
+        // body of trace_chain split at the traversal call).  Same rays, same results.
+        int ti = -1, tcode = 0, tpp = -1, tps = 0;
+        uint32_t sreq = 0;
+        tres = 0;
+        double3 to = d3f(xD), tdd = make_double3(0.0, 0.0, 0.0);
+        if (tracing) {
+            ti = 0;
+#pragma unroll
+            for (int i = 0; i < KMAX; i++) sreq |= (uint32_t)(surf[i] & 15) << (4 * i);
+            if (tmode == TR_DEDUCE) {
+                const double3 v = d3f(tgt) - to;
+                const double l2 = ddot(v, v);
+                if (!(l2 > 0.0)) { tcode = 3; ti = -1; }
+                else tdd = v * rsqrt(l2);
+            }
+        }
+        const int tnr = tmode == TR_VIS ? k + 1 : k;
+        while (__syncthreads_or(ti >= 0)) {
+            // 1. this lane's ray ti (top of the trace_chain loop body)
+            bool has = ti >= 0;
+            float3 of = f3(0.f, 0.f, 0.f), d = f3(0.f, 0.f, 1.f);
+            float tmax = 3.0e38f;
+            int hint = -1;
+            if (has) {
+                if (tmode == TR_VIS) {
+                    const float3 a = ti == 0 ? xD : f3d(rget(x, ti - 1));
+                    const float3 b = ti == k ? xL : f3d(rget(x, ti));
+                    const float3 ab = b - a;
+                    const float l = len(ab);
+                    of = a;
+                    d = ab * (1.0f / l);
+                    tmax = l - P.ray_eps;
+                } else {
+                    if (tmode == TR_REPROJ) {
+                        const double3 v = (rget(x, ti) + tod(rget(dq, ti)) * (double)beta) - to;
+                        const double l2 = ddot(v, v);
+                        if (!(l2 > 0.0)) { tcode = 3 | (ti << 4); has = false; }
+                        else tdd = v * rsqrt(l2);
+                        hint = rget(prim, ti);
+                    } else if (ti > 0) {
+                        if (!scatter_dir<GL>(S, tdd, tpp, tps, to, (tres >> (ti - 1)) & 1u, g.seed, P.walk_id_base + w,
+                                         ti - 1)) {
+                            tcode = 4 | (ti << 4);
+                            has = false;
+                        }
+                    }
+                    of = f3d(to);
+                    d = nrmz(f3d(tdd));
+                }
+                if (!has) ti = -1;
+            }
+            // 2. slot = rank among the block's rays
+            const unsigned bal = __ballot_sync(MPG_FULL, has);
+            if (lane == 0) s_wcnt[warp] = __popc(bal);
+            __syncthreads();
+            int rbase = 0, M = 0;
+#pragma unroll
+            for (int q = 0; q < 4; q++) {
+                const int c = s_wcnt[q];
+                rbase += q < warp ? c : 0;
+                M += c;
+            }
+            const int slot = rbase + __popc(bal & ((1u << lane) - 1u));
+            if (has) {
+                s_ro[slot] = make_float4(of.x, of.y, of.z, tmax);
+                s_rd[slot] = make_float4(d.x, d.y, d.z, __int_as_float(tmode == TR_VIS ? 1 : 0));
+                s_rh[slot] = hint;
+            }
+            __syncthreads();
+            // 3. the first M threads trace the M rays
+            if ((int)threadIdx.x < M) {
+                const float4 ro = s_ro[threadIdx.x], rd = s_rd[threadIdx.x];
+                const bool vis = __float_as_int(rd.w) != 0;
+                Hit h;
+                ls.rays++;
+                const bool hit = trace<W>(S, xyz(ro), xyz(rd), P.ray_eps, ro.w, !vis, vis, h, ls,
+                                          vis ? -1 : s_rh[threadIdx.x]);
+                s_hp[threadIdx.x] = make_float4(h.p.x, h.p.y, h.p.z, 0.f);
+                s_hs[threadIdx.x] = make_int2(hit ? h.prim : -3, h.surf);
+            }
+            __syncthreads();
+            // 4. consume the hit (bottom of the trace_chain loop body)
+            if (has) {
+                const int2 hs = s_hs[slot];
+                const bool hit = hs.x != -3;
+                if (tmode == TR_VIS) {
+                    if (hit) { tcode = 5; ti = -1; }
+                    else if (++ti >= tnr) ti = -1;
+                } else if (!hit) {
+                    tcode = 1 | (ti << 4);
+                    ti = -1;
+                } else if (tmode == TR_REPROJ && hs.y != (int)((sreq >> (4 * ti)) & 15u)) {
+                    tcode = 2 | (ti << 4);
+                    ti = -1;
+                } else {
+                    if (tmode == TR_DEDUCE) {
+                        uint32_t bit = (bits >> ti) & 1u;
+                        const int mat = S.surf[hs.y].mat;
+                        if (!learned && mat == 0) bit = 0u;
+                        if (bit && mat != 1) { tcode = 4 | (ti << 4); ti = -1; }
+                        else tres |= bit << ti;
+                    }
+                    if (ti >= 0) {
+                        const float4 hp = s_hp[slot];
+                        int hprim = hs.x;
+                        const double3 yi = refine_hit(S, hprim, hs.y, to,
+                                                      tmode == TR_DEDUCE ? to + tdd
+                                                                         : rget(x, ti) + tod(rget(dq, ti)) * (double)beta,
+                                                      f3(hp.x, hp.y, hp.z));
+                        rset(y, ti, yi);
+                        rset(yp, ti, hprim);
+                        rset(ys, ti, hs.y);
+                        tpp = hprim;
+                        tps = hs.y;
+                        to = yi;
+                        if (++ti >= tnr) ti = -1;
+                    }
+                }
+            }
+        }
+        why = tcode;
+        } else if (tracing) {
             uint32_t sreq = 0;
 #pragma unroll
             for (int i = 0; i < KMAX; i++) sreq |= (uint32_t)(surf[i] & 15) << (4 * i);
-            uint32_t tres = tau;
-            const int mode = ded ? TR_DEDUCE : (phase == PH_VIS ? TR_VIS : TR_REPROJ);
-            int why = trace_chain<KMAX, W, R>(S, mode, k, bits, learned, xD, xL, tgt, dq, beta, x, prim, sreq, P.ray_eps,
+            why = trace_chain<KMAX, W, R, GL>(S, tmode, k, bits, learned, xD, xL, tgt, dq, beta, x, prim, sreq, P.ray_eps,
                                               y, yp, ys, ls, tres, &s_rays[threadIdx.x], g.seed, P.walk_id_base + w);
+        }
+        if (tracing) {
+            const bool ded = tmode == TR_DEDUCE;
+            const int mode = tmode;
             bool ok = why == 0;
+
             if (mode == TR_VIS) {
                 occluded = !ok;
                 phase = PH_END;
@@ -641,7 +803,7 @@ __global__ void __launch_bounds__(128, MINB) k_walk(const DScene S, const SeedCt
                 bool singular = false;
                 R Di[KMAX][4], Ub[KMAX][4];      // transient: D'^-1_i, U_i of the block-Thomas sweep
                 V3<R> sg[KMAX], tg[KMAX];          // transient: tangent frames of the step
-                int r = newton_system<KMAX, R>(S, g.seed, P.walk_id_base + w, k, tau, xD, xL, x, prim, surf, P.tol, Di, Ub,
+                int r = newton_system<KMAX, R, GL>(S, g.seed, P.walk_id_base + w, k, tau, xD, xL, x, prim, surf, P.tol, Di, Ub,
                                                sg, tg, dq, singular, cm);
                 if (P.dbg && trial == 0 && w < P.n_dbg && 2 * it + 1 < P.dbg_stride) {
                     P.dbg[w * P.dbg_stride + 2 * it] = cm;
@@ -657,7 +819,7 @@ __global__ void __launch_bounds__(128, MINB) k_walk(const DScene S, const SeedCt
                         const DLight &L = S.light[lid];
                         float kap;
                         R DL[4];
-                        if (!post_sweep<KMAX, R>(S, g.seed, P.walk_id_base + w, L, k, tau, xD, xL, x, prim, surf, true, kap,
+                        if (!post_sweep<KMAX, R, GL>(S, g.seed, P.walk_id_base + w, L, k, tau, xD, xL, x, prim, surf, true, kap,
                                                  DL)) {
                             end_status = ST_BAD_SIDE;
                         } else {
@@ -738,7 +900,7 @@ __global__ void __launch_bounds__(128, MINB) k_walk(const DScene S, const SeedCt
                 float kdummy;
                 R DLdummy[4];
                 if (st == ST_CONVERGED && k == pk && tau == ptau &&
-                    post_sweep<KMAX, R>(S, g.seed, P.walk_id_base + w, S.light[lid], k, tau, xD, xL, x, prim, surf, false,
+                    post_sweep<KMAX, R, GL>(S, g.seed, P.walk_id_base + w, S.light[lid], k, tau, xD, xL, x, prim, surf, false,
                                         kdummy, DLdummy)) {
                     same = true;
 #pragma unroll
