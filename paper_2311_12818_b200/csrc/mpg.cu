@@ -986,16 +986,36 @@ static mpg_status make_seed_ctx(const mpg_scene *scene, const mpg_guide *guide, 
     return MPG_OK;
 }
 
+// The guided (u,v) sampler (mode 2) stages the prefix table of a cell in shared memory when all
+// of a block's walks fall in that one cell (consecutive walks are consecutive receivers along a
+// cell row: for configs[2] a 256-walk block spans 64 receivers of a 128-receiver-wide cell); the
+// binary search then reads shared memory instead of L1/L2 (north_star).
 __global__ void k_seeds(const DScene S, const SeedCtx g, const float4 *xD, int64_t n, int spp, uint64_t base,
-                        float4 *xL, float4 *tgt, int *bin, uint32_t *ctype, float *pn) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+                        float4 *xL, float4 *tgt, int *bin, uint32_t *ctype, float *pn, int stage_bins) {
+    extern __shared__ unsigned long long s_pf[];
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x; i0 < n; i0 += stride) {   // block-uniform chunks
+        const int64_t i = i0 + threadIdx.x;
+        int stage_cell = -1;
+        if (stage_bins) {
+            const int c0 = seed_cell(g, xyz(xD[i0 / spp]));
+            const int c = i < n ? seed_cell(g, xyz(xD[i / spp])) : c0;
+            __syncthreads();                                   // previous chunk done with s_pf
+            if (__syncthreads_and(c == c0)) {
+                const unsigned long long *src = (const unsigned long long *)g.prefix + (size_t)c0 * stage_bins;
+                for (int b = threadIdx.x; b < stage_bins; b += blockDim.x) s_pf[b] = __ldg(src + b);
+                stage_cell = c0;
+            }
+            __syncthreads();
+        }
+        if (i >= n) continue;
         uint64_t wid = base + (uint64_t)i;
         float3 l;
         int lid;
         float pdf = sample_light(S, g.seed, wid, l, lid);
         xL[i] = make_float4(l.x, l.y, l.z, pdf);
         SeedRes sr;
-        bool ok = seed_target(S, g, wid, 0u, xyz(xD[i / spp]), l, sr);
+        bool ok = seed_target(S, g, wid, 0u, xyz(xD[i / spp]), l, sr, stage_bins ? s_pf : nullptr, stage_cell);
         tgt[i] = make_float4(sr.tgt.x, sr.tgt.y, sr.tgt.z, 0.f);
         bin[i] = ok ? sr.bin : (sr.bin == -3 ? -3 : -2);   // -3: inactive (R36), -2: seed failed
         if (ctype) ctype[i] = (uint32_t)sr.n | ((sr.bits & 255u) << 4) | ((sr.learned ? 1u : 0u) << 12);
@@ -1025,10 +1045,13 @@ extern "C" mpg_status mpg_sample_seeds(const mpg_scene *scene, const mpg_guide *
     if (n == 0) return MPG_OK;
     ARG_CHECK(q->xD && sb->xL && sb->target && sb->bin, "NULL query/seed array");
     int blocks = (int)std::min<int64_t>((n + 255) / 256, (int64_t)num_sms() * 8);
+    const int nb = g.bins_x * g.bins_y;
+    const int stage = (g.mode == MPG_SEED_GUIDE_UV && nb > 0 && nb <= 6144 && !getenv("MPG_NO_STAGE")) ? nb : 0;
     COUNT_LAUNCH(1);
-    k_seeds<<<blocks, 256, 0, as_stream(stream)>>>(scene->d, g, (const float4 *)q->xD, n, q->spp, o->walk_id_base,
-                                                   (float4 *)sb->xL, (float4 *)sb->target, sb->bin, sb->ctype,
-                                                   sb->pn);
+    k_seeds<<<blocks, 256, (size_t)stage * 8, as_stream(stream)>>>(scene->d, g, (const float4 *)q->xD, n, q->spp,
+                                                                   o->walk_id_base, (float4 *)sb->xL,
+                                                                   (float4 *)sb->target, sb->bin, sb->ctype, sb->pn,
+                                                                   stage);
     CUDA_TRY(cudaPeekAtLastError());
     return MPG_OK;
 }

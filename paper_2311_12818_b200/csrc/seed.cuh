@@ -144,8 +144,11 @@ __device__ __noinline__ float3 stree_lobe_target(const SeedCtx &g, int grp, uint
     return f3(FA(xD.x, om.x), FA(xD.y, om.y), FA(xD.z, om.z));
 }
 
+// stage / stage_cell: the seed kernel's copy of one cell's prefix table in shared memory
+// (north_star: "CDF tables staged in shared memory"), used when the walk's cell is that cell
 __device__ MPG_COLD bool seed_target(const DScene &S, const SeedCtx &g, uint64_t wid, uint32_t trial,
-                                            float3 xD, float3 xL, SeedRes &sr) {
+                                            float3 xD, float3 xL, SeedRes &sr,
+                                            const unsigned long long *stage = nullptr, int stage_cell = -1) {
     float3 &tgt = sr.tgt;
     int &bin = sr.bin;
     bin = -1;
@@ -204,16 +207,27 @@ __device__ MPG_COLD bool seed_target(const DScene &S, const SeedCtx &g, uint64_t
     }
     if (g.mode == 2) { // guided bin over the surface (u,v): integer CDF of W' (R20)
         int nb = g.bins_x * g.bins_y;
-        const uint64_t *pf = g.prefix + (size_t)seed_cell(g, xD) * nb;
-        uint64_t S_ = __ldg((const unsigned long long *)pf + nb - 1);
+        const int cell = seed_cell(g, xD);
+        const uint64_t *pf = g.prefix + (size_t)cell * nb;
         uint4 r = rng_draw(g.seed, wid, 1u, trial);
         uint64_t x = r.x;
-        uint64_t t = x * (S_ >> 32) + ((x * (S_ & 0xffffffffull)) >> 32); // floor(x*S/2^32)
         int lo = 0, hi = nb - 1; // upper_bound: first b with prefix[b] > t
-        while (lo < hi) {
-            int mid = (lo + hi) >> 1;
-            if ((uint64_t)__ldg((const unsigned long long *)pf + mid) > t) hi = mid;
-            else lo = mid + 1;
+        if (stage && cell == stage_cell) {   // the table staged in shared memory
+            const uint64_t S_ = stage[nb - 1];
+            const uint64_t t = x * (S_ >> 32) + ((x * (S_ & 0xffffffffull)) >> 32); // floor(x*S/2^32)
+            while (lo < hi) {
+                int mid = (lo + hi) >> 1;
+                if ((uint64_t)stage[mid] > t) hi = mid;
+                else lo = mid + 1;
+            }
+        } else {
+            const uint64_t S_ = __ldg((const unsigned long long *)pf + nb - 1);
+            const uint64_t t = x * (S_ >> 32) + ((x * (S_ & 0xffffffffull)) >> 32);
+            while (lo < hi) {
+                int mid = (lo + hi) >> 1;
+                if ((uint64_t)__ldg((const unsigned long long *)pf + mid) > t) hi = mid;
+                else lo = mid + 1;
+            }
         }
         bin = lo;
         int bx = lo % g.bins_x, by = lo / g.bins_x;

@@ -392,6 +392,36 @@ __device__ __forceinline__ unsigned long long gtimer() {
 }
 #endif
 
+// the end of a trace: the lane consumes its trace result (deduced / reprojected chain, or
+// the visibility of a converged primary)
+#define MPG_TRACE_TAIL \
+            if (mode == TR_VIS) { \
+                occluded = !ok; \
+                phase = PH_END; \
+            } else { \
+            if (ok && ded) tau = tres; \
+            if (!ok && !ded && P.dbg && trial == 0 && w < P.n_dbg && 2 * it + 3 < P.dbg_stride) \
+                P.dbg[w * P.dbg_stride + 2 * (it + 1)] = -(float)(why + 1); \
+            if (ok) { \
+_Pragma("unroll") \
+                for (int i = 0; i < KMAX; i++) { \
+                    if (i >= k) break; \
+                    x[i] = y[i]; prim[i] = yp[i]; surf[i] = ys[i]; \
+                } \
+                fresh = true; \
+                if (ded) { beta = P.beta0; it = 0; } \
+                else { beta = fminf(1.0f, 2.0f * beta); it++; } \
+                phase = PH_SOLVE; \
+            } else if (ded) { \
+                end_status = ST_SEED_FAIL; \
+                phase = PH_END; \
+            } else { \
+                beta *= 0.5f; \
+                it++; \
+                phase = PH_SOLVE; \
+            } \
+            } \
+
 // GL: glossy scenes (offset normals, R37) -- the glossy code is compiled only into the kernels
 // for scenes with a rough surface; CMP: compacted trace rounds (MPG_COMPACT above)
 template <int KMAX, typename R, int W, int MINB, bool GL, bool CMP>
@@ -625,11 +655,26 @@ __global__ void __launch_bounds__(128, MINB) k_walk(const DScene S, const SeedCt
         }
 #endif
         // ---- trace: deduction (Eq. 6) or reprojection --------------------
+        // (the two variants share the tail MPG_TRACE_TAIL; each instantiation sees only its own
+        // code: the non-compact one is exactly the round-1 structure, A/B-measured)
+        if constexpr (!CMP) {
+        if (phase == PH_DEDUCE || phase == PH_REPROJ || phase == PH_VIS) {
+            bool ded = phase == PH_DEDUCE;
+            uint32_t sreq = 0;
+#pragma unroll
+            for (int i = 0; i < KMAX; i++) sreq |= (uint32_t)(surf[i] & 15) << (4 * i);
+            uint32_t tres = tau;
+            const int mode = ded ? TR_DEDUCE : (phase == PH_VIS ? TR_VIS : TR_REPROJ);
+            int why = trace_chain<KMAX, W, R, GL>(S, mode, k, bits, learned, xD, xL, tgt, dq, beta, x, prim, sreq,
+                                                  P.ray_eps, y, yp, ys, ls, tres, &s_rays[threadIdx.x], g.seed,
+                                                  P.walk_id_base + w);
+            bool ok = why == 0;
+            MPG_TRACE_TAIL
+        }
+        } else {
         const bool tracing = phase == PH_DEDUCE || phase == PH_REPROJ || phase == PH_VIS;
         const int tmode = phase == PH_DEDUCE ? TR_DEDUCE : (phase == PH_VIS ? TR_VIS : TR_REPROJ);
-        int why = 0;
-        uint32_t tres = tau;
-        if constexpr (CMP) {
+        uint32_t tres = 0;
         // The lane's k (or k+1 visibility) rays are traced in rounds: ray i of every
         // tracing lane of the block goes to a shared slot, the block's first M threads
         // trace the M slots (warps start full), and each lane consumes its hit (the
@@ -753,45 +798,13 @@ __global__ void __launch_bounds__(128, MINB) k_walk(const DScene S, const SeedCt
                 }
             }
         }
-        why = tcode;
-        } else if (tracing) {
-            uint32_t sreq = 0;
-#pragma unroll
-            for (int i = 0; i < KMAX; i++) sreq |= (uint32_t)(surf[i] & 15) << (4 * i);
-            why = trace_chain<KMAX, W, R, GL>(S, tmode, k, bits, learned, xD, xL, tgt, dq, beta, x, prim, sreq, P.ray_eps,
-                                              y, yp, ys, ls, tres, &s_rays[threadIdx.x], g.seed, P.walk_id_base + w);
-        }
         if (tracing) {
             const bool ded = tmode == TR_DEDUCE;
             const int mode = tmode;
+            const int why = tcode;
             bool ok = why == 0;
-
-            if (mode == TR_VIS) {
-                occluded = !ok;
-                phase = PH_END;
-            } else {
-            if (ok && ded) tau = tres;
-            if (!ok && !ded && P.dbg && trial == 0 && w < P.n_dbg && 2 * it + 3 < P.dbg_stride)
-                P.dbg[w * P.dbg_stride + 2 * (it + 1)] = -(float)(why + 1);
-            if (ok) {
-#pragma unroll
-                for (int i = 0; i < KMAX; i++) {
-                    if (i >= k) break;
-                    x[i] = y[i]; prim[i] = yp[i]; surf[i] = ys[i];
-                }
-                fresh = true;
-                if (ded) { beta = P.beta0; it = 0; }
-                else { beta = fminf(1.0f, 2.0f * beta); it++; }
-                phase = PH_SOLVE;
-            } else if (ded) {
-                end_status = ST_SEED_FAIL;
-                phase = PH_END;
-            } else {
-                beta *= 0.5f;
-                it++;
-                phase = PH_SOLVE;
-            }
-            }
+            MPG_TRACE_TAIL
+        }
         }
 
         // ---- Newton system / step ------------------------------------------
@@ -992,3 +1005,4 @@ __global__ void __launch_bounds__(128, MINB) k_walk(const DScene S, const SeedCt
         for (int i = threadIdx.x; i < SS_N; i += blockDim.x)
             if (s_stats[i]) atomicAdd(P.stats + i, (unsigned long long)s_stats[i]);
 }
+#undef MPG_TRACE_TAIL
