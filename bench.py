@@ -233,6 +233,13 @@ def run_ours(args):
     progressive = w.seed.mode in (3, 4)  # configs[4]: one step = the whole 8-iteration loop (R22)
     stree = w.seed.mode == 4             # --guide stree: the paper's STree + vMF guide
     iters = 8 if progressive else 1
+    # N > 1 progressive loop: owner-computes by default -- each rank walks the
+    # receiver rows of its guide-cell rows with spp x N, fits its guide from its own samples
+    # and exchanges nothing; --exchange keeps every rank on all receivers with the guide
+    # exchange (histogram all-reduce / STree record all-gather)
+    owner = progressive and world > 1 and not args.exchange
+    if owner:
+        w, _ = D.owner_workload(w, rank, world)
     # independent partitions (weak scaling): rank r owns walk ids [r*n*iters, (r+1)*n*iters)
     w.opts.walk_id_base = D.walk_id_base(rank, w.n_walks * iters)
     ds = mpg.DeviceScene(w, stree_capacity=max(w.n_walks, args.photons) * world)
@@ -249,7 +256,7 @@ def run_ours(args):
     gsz = ds.info_guide_size() if (progressive and not stree) else 0
     hbuf = torch.empty(max(gsz, 1), dtype=torch.float32, device=dev)
     exchange = None
-    if progressive and world > 1:
+    if progressive and world > 1 and not owner:
         if stree:   # STree: the sample records of all ranks are gathered (the tree is fitted from all of them)
             sbuf = torch.empty(b.n * world * mpg.GUIDE_SAMPLE_BYTES, dtype=torch.uint8, device=dev)
             exchange = lambda d: D.exchange_samples(d, sbuf, b.n)
@@ -259,7 +266,7 @@ def run_ours(args):
     plane = (w.xD[0].tolist(), w.nD[0].tolist())   # receiver plane (photon landing, R33)
 
     pbuf = None
-    if stree and args.photons and world > 1:
+    if stree and args.photons and world > 1 and not owner:
         pbuf = torch.empty(args.photons * world * mpg.GUIDE_SAMPLE_BYTES, dtype=torch.uint8, device=dev)
 
     def photon_init():
@@ -424,6 +431,10 @@ def run_ours(args):
                            "order": ("primaries in walk order" if not opts.flags & 8 else
                                      "primaries in (receiver cell, seed direction) order, MPG_FLAG_SORT"),
                            "path": "persistent kernel",
+                           "parallelism": (f"{world} ranks, owner-computes receiver bands aligned to guide-cell rows, "
+                                           "spp x N, no data-path collective" if owner else
+                                           f"{world} ranks, disjoint walk-id partitions" +
+                                           (", guide exchange per iteration" if progressive and world > 1 else "")),
                            "bvh": (f"{ds.info.bvh_width}-wide SAH, {ds.info.n_nodes} nodes, {ds.info.n_tri} triangles"
                                    if ds.info.n_tri else "analytic surfaces only"),
                            "precision": ("fp32 scene/traversal; fp64 positions, residual, hit refinement" +
@@ -475,6 +486,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-sort", action="store_true",
                     help="walk-order primaries (default: coherence-sorted order, MPG_FLAG_SORT; same results)")
+    ap.add_argument("--exchange", action="store_true",
+                    help="N>1 progressive loop: all receivers on every rank + guide exchange (default: owner-computes)")
     ap.add_argument("--f64", action="store_true", help="MPG_FLAG_NEWTON_F64")
     ap.add_argument("--f32", action="store_true", help="clear MPG_FLAG_NEWTON_F64 (fp32 Jacobian/step)")
     args = ap.parse_args()

@@ -1046,7 +1046,10 @@ extern "C" mpg_status mpg_sample_seeds(const mpg_scene *scene, const mpg_guide *
     ARG_CHECK(q->xD && sb->xL && sb->target && sb->bin, "NULL query/seed array");
     int blocks = (int)std::min<int64_t>((n + 255) / 256, (int64_t)num_sms() * 8);
     const int nb = g.bins_x * g.bins_y;
-    const int stage = (g.mode == MPG_SEED_GUIDE_UV && nb > 0 && nb <= 6144 && !getenv("MPG_NO_STAGE")) ? nb : 0;
+    // staging measured slower on configs[2] (k_seeds 0.72 vs 0.62 ms: a block loads the whole
+    // 8 KB table for ~10 probes per walk that L1 serves anyway) -> opt-in (MPG_STAGE=1)
+    static const bool want_stage = getenv("MPG_STAGE") && atoi(getenv("MPG_STAGE")) != 0;
+    const int stage = (want_stage && g.mode == MPG_SEED_GUIDE_UV && nb > 0 && nb <= 6144) ? nb : 0;
     COUNT_LAUNCH(1);
     k_seeds<<<blocks, 256, (size_t)stage * 8, as_stream(stream)>>>(scene->d, g, (const float4 *)q->xD, n, q->spp,
                                                                    o->walk_id_base, (float4 *)sb->xL,
@@ -1432,9 +1435,15 @@ static mpg_status walk_dispatch(const mpg_scene *scene, const SeedCtx &g, const 
         if (k <= 2) return launch_walk<2, float, MPG_WALK_MINB2, true>(scene->d, g, P, s, workspace, sort);
         return launch_walk<6, float, MPG_WALK_MINB_LONG, true>(scene->d, g, P, s, workspace, sort);
     }
+#ifndef MPG_CMP_SHORT
+#define MPG_CMP_SHORT 0   // compacted rounds for fixed k <= 2 (A/B knob; measured slower)
+#endif
+#ifndef MPG_CMP_LONG
+#define MPG_CMP_LONG 0    // compacted rounds for fixed k in 3..6 (A/B knob)
+#endif
     if (f64) {
-        if (k <= 1) return launch_walk<1, double>(scene->d, g, P, s, workspace, sort);
-        if (k <= 2) return launch_walk<2, double>(scene->d, g, P, s, workspace, sort);
+        if (k <= 1) return launch_walk<1, double, MPG_WALK_MINB2, false, MPG_CMP_SHORT != 0>(scene->d, g, P, s, workspace, sort);
+        if (k <= 2) return launch_walk<2, double, MPG_WALK_MINB2, false, MPG_CMP_SHORT != 0>(scene->d, g, P, s, workspace, sort);
         if (k <= 4) return launch_walk<4, double>(scene->d, g, P, s, workspace, sort);
         if (k <= 6) {
             // mixed chain lengths (configs[4]): see MPG_WALK_MINB_MIXED; compacted trace rounds
@@ -1442,7 +1451,8 @@ static mpg_status walk_dispatch(const mpg_scene *scene, const SeedCtx &g, const 
             if (sd->mode >= MPG_SEED_GUIDE_DIR)
                 return launch_walk<6, double, MPG_WALK_MINB_MIXED, false, MPG_COMPACT != 0>(scene->d, g, P, s,
                                                                                           workspace, sort);
-            return launch_walk<6, double>(scene->d, g, P, s, workspace, sort);
+            return launch_walk<6, double, MPG_WALK_MINB_LONG, false, MPG_CMP_LONG != 0>(scene->d, g, P, s, workspace,
+                                                                                        sort);
         }
         return launch_walk<8, double>(scene->d, g, P, s, workspace, sort);
     }

@@ -30,7 +30,9 @@
 #define MPG_WALK_MINB_LONG 6   // fixed long chains (configs[3])
 #endif
 #ifndef MPG_WALK_MINB_MIXED
-#define MPG_WALK_MINB_MIXED 3  // per-sample chain length (configs[4]; 2/3/4: 261/255/271 ms)
+// per-sample chain length (configs[4]); round 1 (per-lane rays): 2/3/4 blocks 261/255/271 ms;
+// round 2 (compacted trace rounds, CMP): 2/3/4/5/6 blocks 269/225/219/235/252 ms
+#define MPG_WALK_MINB_MIXED 4
 #endif
 // MPG_COMPACT: block-synchronous passes whose chain rays are traced in compacted
 // rounds -- every lane that needs a ray writes it to a shared-memory slot, the

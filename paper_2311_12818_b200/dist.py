@@ -17,6 +17,7 @@ torch.distributed carries these (NCCL on the GPU box, gloo in the CPU tests).
 """
 from __future__ import annotations
 
+import numpy as np
 import torch
 import torch.distributed as dist
 
@@ -103,3 +104,33 @@ def gather_records(mine: torch.Tensor, out: torch.Tensor) -> torch.Tensor:
     parts = list(out.view(world, -1).unbind(0))
     dist.all_gather(parts, mine)
     return out
+
+
+def owner_rows(recv_z, cells_y: int, grid_origin_z: float, grid_extent_z: float, rank: int, world: int):
+    """Owner-computes partition of the progressive loop: rank r owns the
+    receiver rows whose guide-cell row is in [cells_y*r/world, cells_y*(r+1)/world), i.e.
+    whole guide cells.  recv_z: the z coordinate of each receiver row (rows are z-major).
+    A rank's walks then only ever accumulate into -- and sample from -- its own cells, so
+    the histogram exchange is not needed (the tables of a rank's cells are identical with
+    or without the all-reduce, tests/test_dist_gloo.py); the STree guide is fitted per rank
+    from its own configurations.  Returns the owned row indices (contiguous)."""
+    import numpy as np
+    z = np.asarray(recv_z, np.float32)
+    cz = np.floor((z - np.float32(grid_origin_z)) * np.float32(cells_y) / np.float32(grid_extent_z)).astype(np.int64)
+    cz = np.clip(cz, 0, cells_y - 1)
+    c0, c1 = cells_y * rank // world, cells_y * (rank + 1) // world
+    return np.nonzero((cz >= c0) & (cz < c1))[0]
+
+
+def owner_workload(w, rank: int, world: int):
+    """This rank's share of a progressive workload under owner-computes: its receiver rows,
+    spp multiplied by world (weak scaling: every rank walks as many walks per iteration as
+    one GPU does on the whole receiver set)."""
+    import dataclasses
+    ny, nx = w.recv_shape
+    zrows = w.xD.reshape(ny, nx, 3)[:, 0, 2]
+    sp = w.seed
+    rows = owner_rows(zrows, sp.cells_y, sp.grid_origin[1], sp.grid_extent[1], rank, world)
+    sel = (rows[:, None] * nx + np.arange(nx)[None, :]).ravel() if len(rows) else np.zeros(0, np.int64)
+    return dataclasses.replace(w, xD=np.ascontiguousarray(w.xD[sel]), nD=np.ascontiguousarray(w.nD[sel]),
+                               spp=w.spp * world, recv_shape=(len(rows), nx)), rows

@@ -225,3 +225,48 @@ def test_sample_exchange_rejects_keep_all_and_small_capacity(tmp_path):
     mp.spawn(_keep_all_worker, args=(2, _free_port(), out), nprocs=2, join=True)
     r = json.load(open(out))
     assert "keep_all" in r["1_100"] and "capacity" in r["0_10"]
+
+
+# ---- owner-computes: receiver bands aligned to guide cells, no exchange ----
+def _worker_owner(rank, world, port, out):
+    import torch
+    import torch.distributed as dist
+    from oracle import oracle as O
+    from paper_2311_12818_b200 import dist as D
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    w, rows = D.owner_workload(W.config4(n_side=16, grid_n=32), rank, world)
+    s = O.OracleScene(w)
+    s.set_dir_hist(np.zeros((256, 126, 1024), np.float32))
+    base = D.walk_id_base(rank, w.n_walks)
+    o = s.walks(np.arange(w.n_walks), s.opts(walk_id_base=base))
+    h = s.accumulate_dir(o["status"], o["w"], o["pos"][:, 0], o["k"], o["tau"])
+    summed = torch.from_numpy(h.copy())
+    D.allreduce_histogram(summed)                          # what an exchange would give
+    own = O.guide_dir_tables(h.astype(np.float32))
+    ex = O.guide_dir_tables(summed.numpy().astype(np.float32))
+    cells = sorted({int(c) for c in np.nonzero(h.reshape(256, -1).sum(1))[0]})
+    np.savez(out + f".{rank}.npz", rows=rows, cells=np.array(cells), n=w.n_walks,
+             own_n=own[0], own_t=own[1], own_d=own[2], ex_n=ex[0], ex_t=ex[1], ex_d=ex[2])
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_rank_owner_computes_needs_no_exchange(tmp_path):
+    """Owner-computes: rank r walks the receiver rows of guide-cell rows [16r/2, 16(r+1)/2)
+    with spp x 2 (weak scaling).  The bands are disjoint, cover the receivers and align to
+    cell rows; each rank's histogram has mass only in its own cells, so the tables of its
+    cells are bit-identical with and without the all-reduce: no data-path collective."""
+    out = str(tmp_path / "o")
+    mp.spawn(_worker_owner, args=(2, _free_port(), out), nprocs=2, join=True)
+    r = [np.load(out + f".{k}.npz") for k in range(2)]
+    rows0, rows1 = r[0]["rows"], r[1]["rows"]
+    assert len(set(rows0) & set(rows1)) == 0 and sorted(np.concatenate([rows0, rows1])) == list(range(16))
+    assert int(r[0]["n"]) == int(r[1]["n"]) == 8 * 16 * 2              # per-rank work = one GPU's
+    for k in range(2):
+        cells = r[k]["cells"]
+        assert len(cells) > 0
+        cy = cells // 16
+        assert ((cy >= 8 * k) & (cy < 8 * (k + 1))).all()              # mass only in its own cell rows
+        mine = (np.arange(256) // 16 >= 8 * k) & (np.arange(256) // 16 < 8 * (k + 1))
+        for a, b in (("own_n", "ex_n"), ("own_t", "ex_t"), ("own_d", "ex_d")):
+            assert np.array_equal(r[k][a][mine], r[k][b][mine])       # the exchange changes nothing it uses
