@@ -1,0 +1,921 @@
+// walk_pool.cuh -- the warp-specialized manifold-walk kernel (sm_100a), round 2.
+//
+// Same method and same per-walk arithmetic as walk.cuh (it calls the same device
+// functions: trace<W>, refine_hit, scatter_dir, newton_system, post_sweep,
+// ggt_from_blocks, seed_target and the trial bookkeeping), different execution model.
+//
+// walk.cuh binds one walk to one lane for the walk's whole life, so a warp
+// instruction of the traversal, of the Newton sweep or of the end-of-attempt logic
+// runs on the 8-12 lanes that happen to be in that phase (ncu), all
+// phases share one register budget (64: ~1 KB of spills per lane, 0.5 TB of
+// local-memory DRAM traffic per configs[2] launch) and every warp walks through the
+// whole 60 KB of code (41 % instruction-fetch stalls).
+//
+// Here a block (one per SM) owns a pool of NV walk *slots* whose state lives in
+// shared memory, and its warps are specialized:
+//   * trace warps pop slots that need rays from the ray queue and run only the
+//     chain-ray loop (deduction, reprojection with its step-halving retries, or the
+//     k+1 visibility segments): every lane with a slot traces a ray in every
+//     iteration, finished lanes refill from the queue at once (north_star's
+//     "compaction to regroup still-iterating chains"), few registers;
+//   * compute warps pop slots with a fresh chain from the solve queue and run the
+//     Newton sweep on 32 of them at once (many registers: setmaxnreg hands them the
+//     trace warps' surplus), and pop slots whose attempt ended from the control queue
+//     (end-of-attempt bookkeeping, reciprocal-probability trials, fetch of the next
+//     primary, trial seeds), or poll the trial-item ring for slots that wait.
+// Queues are rings of slot ids in shared memory.  The global work distribution
+// (primary queue, hard entries, trial items by ticket, `resolved` count) is
+// walk.cuh's, with a slot in the place of a lane, so the trial count k of every walk
+// is the same sequential count (Eq. 15, R13) and outputs are bit-identical.
+#pragma once
+#include "walk.cuh"
+
+enum { PQ_RAY = 0, PQ_SOLVE = 1, PQ_CTL = 2, PQ_WAIT = 3, PQ_N = 4 };
+
+// MPG_POOL_PROF: diagnostic build (tools/pool_prof.py): per-role cycle and batch counters
+#ifdef MPG_POOL_PROF
+// trace: 0 rounds, 1 lanes with a ray, 2 busy cycles, 3 idle cycles, 4 idle rounds
+// compute: 5 solve batches, 6 solve slots, 7 solve cycles, 8 ctl batches, 9 ctl slots, 10 ctl cycles,
+//          11 wait batches, 12 wait cycles, 13 idle cycles, 14 idle rounds
+__device__ unsigned long long g_pool_prof[16];
+#define PROF_DECL unsigned long long pf_[16] = {0}; long long pf_t = clock64();
+#define PROF_ADD(i, v) (pf_[i] += (unsigned long long)(v))
+#define PROF_LAP(i) { const long long t_ = clock64(); pf_[i] += (unsigned long long)(t_ - pf_t); pf_t = t_; }
+#define PROF_FLUSH if (lane == 0) { for (int i_ = 0; i_ < 16; i_++) if (pf_[i_]) atomicAdd(&g_pool_prof[i_], pf_[i_]); }
+#else
+#define PROF_DECL
+#define PROF_ADD(i, v)
+#define PROF_LAP(i)
+#define PROF_FLUSH
+#endif
+
+struct PoolShared {
+    unsigned head[PQ_N], tail[PQ_N];
+    unsigned done, drained;
+    unsigned stats[SS_N];
+};
+
+// slot word `st`: it (16) | end_status (3) << 16 | occluded << 19 | seq_only << 20 | phase (4) << 24 | lid (3) << 28
+// slot word `ct`: k (4) | tau (8) << 4 | bits (8) << 12 | learned << 20 | cur << 21
+#define ST_IT(s) ((int)((s)&0xffffu))
+#define ST_END(s) ((int)(((s) >> 16) & 7u))
+#define ST_OCC(s) ((((s) >> 19) & 1u) != 0u)
+#define ST_SEQ(s) ((((s) >> 20) & 1u) != 0u)
+#define ST_PH(s) ((int)(((s) >> 24) & 15u))
+#define ST_LID(s) ((int)(((s) >> 28) & 7u))
+__device__ __forceinline__ uint32_t st_pack(int it, int end_status, bool occ, bool seq, int phase, int lid) {
+    return (uint32_t)(it & 0xffff) | ((uint32_t)(end_status & 7) << 16) | ((occ ? 1u : 0u) << 19) |
+           ((seq ? 1u : 0u) << 20) | ((uint32_t)(phase & 15) << 24) | ((uint32_t)(lid & 7) << 28);
+}
+__device__ __forceinline__ uint32_t ct_pack(int k, uint32_t tau, uint32_t bits, bool learned, int cur) {
+    return (uint32_t)(k & 15) | ((tau & 255u) << 4) | ((bits & 255u) << 12) | ((learned ? 1u : 0u) << 20) |
+           ((uint32_t)(cur & 1) << 21);
+}
+
+template <int KMAX, typename R> struct Pool {
+    int nv, nvq;
+    double *xb;            // [2][KMAX][3][nv] chain vertices: buffer cur = the chain, cur^1 = the chain being traced
+    R *dq;                 // [KMAX][3][nv] Newton step (world space); [0] doubles as the seed target during deduction
+    int *pr;               // [2][KMAX][nv] primitives
+    uint32_t *sf;          // [2][nv] surface ids, 4 bits per vertex
+    uint32_t *w, *trial, *ct, *pct, *psurf, *st, *ticket;
+    int *item_e;
+    float *beta, *Tprim, *Gc, *Tc, *xD;   // xD [3][nv]
+    unsigned short *ring;  // [PQ_N][nvq] slot + 1 (0: empty)
+    static __host__ __device__ size_t slot_bytes() {
+        return (size_t)KMAX * (48 + 3 * sizeof(R) + 8) + 8 + 7 * 4 + 4 + 4 * 4 + 12;
+    }
+    static __host__ __device__ size_t bytes(int nv, int nvq) { return slot_bytes() * nv + (size_t)PQ_N * nvq * 2 + 64; }
+    __device__ void carve(unsigned char *base, int nv_, int nvq_) {
+        nv = nv_; nvq = nvq_;
+        unsigned char *p = base;
+        xb = (double *)p; p += (size_t)2 * KMAX * 3 * nv * 8;
+        dq = (R *)p; p += (size_t)KMAX * 3 * nv * sizeof(R);
+        pr = (int *)p; p += (size_t)2 * KMAX * nv * 4;
+        sf = (uint32_t *)p; p += (size_t)2 * nv * 4;
+        w = (uint32_t *)p; p += (size_t)nv * 4;
+        trial = (uint32_t *)p; p += (size_t)nv * 4;
+        ct = (uint32_t *)p; p += (size_t)nv * 4;
+        pct = (uint32_t *)p; p += (size_t)nv * 4;
+        psurf = (uint32_t *)p; p += (size_t)nv * 4;
+        st = (uint32_t *)p; p += (size_t)nv * 4;
+        ticket = (uint32_t *)p; p += (size_t)nv * 4;
+        item_e = (int *)p; p += (size_t)nv * 4;
+        beta = (float *)p; p += (size_t)nv * 4;
+        Tprim = (float *)p; p += (size_t)nv * 4;
+        Gc = (float *)p; p += (size_t)nv * 4;
+        Tc = (float *)p; p += (size_t)nv * 4;
+        xD = (float *)p; p += (size_t)3 * nv * 4;
+        ring = (unsigned short *)p;
+    }
+    __device__ __forceinline__ double3 getx(int buf, int i, int s) const {
+        const double *p = xb + (size_t)((buf * KMAX + i) * 3) * nv + s;
+        return make_double3(p[0], p[nv], p[2 * nv]);
+    }
+    __device__ __forceinline__ void setx(int buf, int i, int s, double3 v) {
+        double *p = xb + (size_t)((buf * KMAX + i) * 3) * nv + s;
+        p[0] = v.x; p[nv] = v.y; p[2 * nv] = v.z;
+    }
+    __device__ __forceinline__ V3<R> getdq(int i, int s) const {
+        const R *p = dq + (size_t)(i * 3) * nv + s;
+        return mk3<R>(p[0], p[nv], p[2 * nv]);
+    }
+    __device__ __forceinline__ void setdq(int i, int s, V3<R> v) {
+        R *p = dq + (size_t)(i * 3) * nv + s;
+        p[0] = v.x; p[nv] = v.y; p[2 * nv] = v.z;
+    }
+    // the seed target of a deduction pass, in the (then unused) step storage of vertex 0
+    // (float -> R -> float is exact)
+    __device__ __forceinline__ float3 gettgt(int s) const { return tof(getdq(0, s)); }
+    __device__ __forceinline__ void settgt(int s, float3 v) { setdq(0, s, fromf<R>(v)); }
+    __device__ __forceinline__ float3 getxD(int s) const { return f3(xD[s], xD[nv + s], xD[2 * nv + s]); }
+    __device__ __forceinline__ void setxD(int s, float3 v) { xD[s] = v.x; xD[nv + s] = v.y; xD[2 * nv + s] = v.z; }
+    __device__ __forceinline__ int getpr(int buf, int i, int s) const { return pr[(size_t)(buf * KMAX + i) * nv + s]; }
+    __device__ __forceinline__ void setpr(int buf, int i, int s, int v) { pr[(size_t)(buf * KMAX + i) * nv + s] = v; }
+};
+
+// ---- queues: rings of slot ids; a slot is in at most one queue, so a ring of >= nv entries never
+// overflows.  Producers reserve positions with one atomicAdd per warp and then write the entries;
+// consumers reserve [head, head + take) below the reserved tail with a CAS and wait (briefly: the
+// producer is between its atomicAdd and its store) for each entry to appear.
+__device__ __forceinline__ int q_reserve(PoolShared *sh, int q, int want, unsigned &base) {
+    while (true) {
+        const unsigned h = *(volatile unsigned *)&sh->head[q];
+        const unsigned t = *(volatile unsigned *)&sh->tail[q];
+        const int avail = (int)(t - h);
+        const int take = min(want, avail);
+        if (take <= 0) return 0;
+        if (atomicCAS(&sh->head[q], h, h + (unsigned)take) == h) { base = h; return take; }
+    }
+}
+template <int KMAX, typename R>
+__device__ __forceinline__ int q_take(const Pool<KMAX, R> &pl, int q, unsigned pos) {
+    volatile unsigned short *e = pl.ring + (size_t)q * pl.nvq + (pos & (unsigned)(pl.nvq - 1));
+    unsigned short v;
+    while ((v = *e) == 0) {}
+    *e = 0;
+    __threadfence_block();
+    return (int)v - 1;
+}
+// push the slots of the lanes with `flag` (whole warp calls it)
+template <int KMAX, typename R>
+__device__ __forceinline__ void q_push(const Pool<KMAX, R> &pl, PoolShared *sh, int q, bool flag, int slot, int lane) {
+    const unsigned m = __ballot_sync(MPG_FULL, flag);
+    if (!m) return;
+    const int leader = __ffs(m) - 1;
+    unsigned base = 0;
+    __threadfence_block();   // the slot's state before its id
+    if (lane == leader) base = atomicAdd(&sh->tail[q], (unsigned)__popc(m));
+    base = __shfl_sync(MPG_FULL, base, leader);
+    if (flag) {
+        const unsigned pos = base + (unsigned)__popc(m & ((1u << lane) - 1u));
+        volatile unsigned short *e = pl.ring + (size_t)q * pl.nvq + (pos & (unsigned)(pl.nvq - 1));
+        while (*e != 0) {}   // the consumer of the previous lap is clearing it
+        *e = (unsigned short)(slot + 1);
+    }
+    __syncwarp();
+}
+
+template <int REGS> __device__ __forceinline__ void reg_inc() {
+    if constexpr (REGS > 0) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(REGS));
+}
+template <int REGS> __device__ __forceinline__ void reg_dec() {
+    if constexpr (REGS > 0) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(REGS));
+}
+
+// ============================================================================
+// trace warps: the chain-ray loop of one pass per slot (body of walk.cuh's trace_chain,
+// one ray per iteration, lanes refilled from the ray queue between rays)
+// ============================================================================
+template <int KMAX, typename R, int W, bool GL>
+__device__ __forceinline__ void pool_trace_role(const DScene &S, const SeedCtx &g, const WalkParams &P,
+                                                Pool<KMAX, R> &pl, PoolShared *sh, const int lane,
+                                                unsigned long long *rays_out, LaneStats &ls, const int dbgm) {
+    int slot = -1;
+    int mode = TR_REPROJ, k = 1, ti = -1, it = 0, cur = 0, tpp = -1, tps = 0, tcode = 0;
+    uint32_t bits = 0, tres = 0, sreq = 0, ysf = 0, stw = 0, ctw = 0, wi = 0;
+    float beta = 1.f;
+    float3 xD = f3(0.f, 0.f, 0.f);
+    double3 to = make_double3(0.0, 0.0, 0.0), tdd = make_double3(0.0, 0.0, 1.0);
+    unsigned idle_ns = 32u;
+    unsigned long long rays = 0;
+    PROF_DECL
+    while (true) {
+        // ---- refill the lanes without a slot ---------------------------------
+        const unsigned need = __ballot_sync(MPG_FULL, slot < 0);
+        if (need) {
+            int got = 0;
+            unsigned base = 0;
+            if (lane == 0) {
+                got = q_reserve(sh, PQ_RAY, __popc(need), base);
+                // (read by one lane and broadcast: the decision to leave must be warp-uniform)
+                if (!got && need == MPG_FULL && *(volatile unsigned *)&sh->done) got = -1;
+            }
+            got = __shfl_sync(MPG_FULL, got, 0);
+            base = __shfl_sync(MPG_FULL, base, 0);
+            if (got < 0) break;
+            const int rank = __popc(need & ((1u << lane) - 1u));
+            if (slot < 0 && rank < got) {
+                slot = q_take(pl, PQ_RAY, base + (unsigned)rank);
+                // begin the pass
+                ctw = pl.ct[slot];
+                stw = pl.st[slot];
+                k = (int)(ctw & 15u);
+                bits = (ctw >> 12) & 255u;
+                cur = (int)((ctw >> 21) & 1u);
+                const int ph = ST_PH(stw);
+                mode = ph == PH_DEDUCE ? TR_DEDUCE : (ph == PH_VIS ? TR_VIS : TR_REPROJ);
+                it = ST_IT(stw);
+                beta = pl.beta[slot];
+                xD = pl.getxD(slot);
+                wi = pl.w[slot];
+                sreq = pl.sf[cur * pl.nv + slot];
+                ti = 0; tres = 0; tcode = 0; ysf = 0; tpp = -1; tps = 0;
+                to = d3f(xD);
+                if (mode == TR_DEDUCE) {
+                    const double3 v = d3f(pl.gettgt(slot)) - to;
+                    const double l2 = ddot(v, v);
+                    if (!(l2 > 0.0)) { tcode = 3; ti = -1; }
+                    else tdd = v * rsqrt(l2);
+                }
+            }
+            if (need == MPG_FULL && got == 0) {   // the whole warp is idle
+                PROF_ADD(4, 1);
+                PROF_LAP(3)
+                __nanosleep(idle_ns);
+                idle_ns = min(2u * idle_ns, 512u);
+                continue;
+            }
+        }
+        idle_ns = 32u;
+        // ---- this lane's ray ti (top of the trace_chain loop body) -----------
+        bool has = slot >= 0 && ti >= 0;
+        float3 of = f3(0.f, 0.f, 0.f), d = f3(0.f, 0.f, 1.f);
+        float tmax = 3.0e38f;
+        int hint = -1;
+        if (has) {
+            if (mode == TR_VIS) {
+                const float3 a = ti == 0 ? xD : f3d(pl.getx(cur, ti - 1, slot));
+                const float3 b = ti == k ? xyz(__ldg(P.seed_xL + wi)) : f3d(pl.getx(cur, min(ti, KMAX - 1), slot));
+                const float3 ab = b - a;
+                const float l = len(ab);
+                of = a;
+                d = ab * (1.0f / l);
+                tmax = l - P.ray_eps;
+            } else {
+                if (mode == TR_REPROJ) {
+                    const double3 v = (pl.getx(cur, ti, slot) + tod(pl.getdq(ti, slot)) * (double)beta) - to;
+                    const double l2 = ddot(v, v);
+                    if (!(l2 > 0.0)) { tcode = 3 | (ti << 4); has = false; }
+                    else tdd = v * rsqrt(l2);
+                    hint = pl.getpr(cur, ti, slot);
+                } else if (ti > 0) {
+                    if (!scatter_dir<GL>(S, tdd, tpp, tps, to, (tres >> (ti - 1)) & 1u, g.seed, P.walk_id_base + wi,
+                                         ti - 1)) {
+                        tcode = 4 | (ti << 4);
+                        has = false;
+                    }
+                }
+                of = f3d(to);
+                d = nrmz(f3d(tdd));
+            }
+            if (!has) ti = -1;
+        }
+        // ---- traverse ----------------------------------------------------------
+        if (has) {
+            const bool vis = mode == TR_VIS;
+            Hit h;
+            rays++;
+            bool hit = false;
+            if (dbgm != 3) hit = trace<W>(S, of, d, P.ray_eps, tmax, !vis, vis, h, ls, vis ? -1 : hint);
+            // ---- consume the hit (bottom of the trace_chain loop body) ---------
+            if (vis) {
+                if (hit) { tcode = 5; ti = -1; }
+                else if (++ti >= k + 1) ti = -1;
+            } else if (!hit) {
+                tcode = 1 | (ti << 4);
+                ti = -1;
+            } else if (mode == TR_REPROJ && h.surf != (int)((sreq >> (4 * ti)) & 15u)) {
+                tcode = 2 | (ti << 4);
+                ti = -1;
+            } else {
+                if (mode == TR_DEDUCE) {
+                    uint32_t bit = (bits >> ti) & 1u;
+                    const int mat = S.surf[h.surf].mat;
+                    if (!((ctw >> 20) & 1u) && mat == 0) bit = 0u;
+                    if (bit && mat != 1) { tcode = 4 | (ti << 4); ti = -1; }
+                    else tres |= bit << ti;
+                }
+                if (ti >= 0) {
+                    int hprim = h.prim;
+                    const double3 yi = refine_hit(S, hprim, h.surf, to,
+                                                  mode == TR_DEDUCE
+                                                      ? to + tdd
+                                                      : pl.getx(cur, ti, slot) + tod(pl.getdq(ti, slot)) * (double)beta,
+                                                  h.p);
+                    pl.setx(cur ^ 1, ti, slot, yi);
+                    pl.setpr(cur ^ 1, ti, slot, hprim);
+                    ysf |= (uint32_t)(h.surf & 15) << (4 * ti);
+                    tpp = hprim;
+                    tps = h.surf;
+                    to = yi;
+                    if (++ti >= k) ti = -1;
+                }
+            }
+        }
+        // ---- end of a pass (walk.cuh MPG_TRACE_TAIL) -------------------------
+        bool to_solve = false, to_ctl = false;
+        if (slot >= 0 && ti < 0) {
+            const bool ok = tcode == 0, ded = mode == TR_DEDUCE;
+            uint32_t tau = (ctw >> 4) & 255u;
+            int phase = PH_END, end_status = ST_END(stw);
+            bool occ = false;
+            if (mode == TR_VIS) {
+                occ = !ok;
+                to_ctl = true;
+            } else {
+                if (!ok && !ded && P.dbg && pl.trial[slot] == 0 && (int64_t)wi < P.n_dbg && 2 * it + 3 < P.dbg_stride)
+                    P.dbg[(int64_t)wi * P.dbg_stride + 2 * (it + 1)] = -(float)(tcode + 1);
+                if (ok) {
+                    cur ^= 1;
+                    pl.sf[cur * pl.nv + slot] = ysf;
+                    if (ded) { tau = tres; beta = P.beta0; it = 0; }
+                    else { beta = fminf(1.0f, 2.0f * beta); it++; }
+                    phase = PH_SOLVE;
+                    to_solve = true;
+                } else if (ded) {
+                    end_status = ST_SEED_FAIL;
+                    to_ctl = true;
+                } else {
+                    beta *= 0.5f;
+                    it++;
+                    if (it >= ((k >= 3 && P.max_iters_long > 0) ? P.max_iters_long : P.max_iters)) {
+                        end_status = ST_MAXITER;
+                        to_ctl = true;
+                    } else {   // step halving: retrace the same chain with the shorter step
+                        ti = 0; tres = 0; tcode = 0; ysf = 0; tpp = -1; tps = 0;
+                        to = d3f(xD);
+                    }
+                }
+            }
+            if (to_solve || to_ctl) {
+                pl.ct[slot] = ct_pack(k, tau, bits, (ctw >> 20) & 1u, cur);
+                pl.st[slot] = st_pack(it, end_status, occ, ST_SEQ(stw), phase, ST_LID(stw));
+                pl.beta[slot] = beta;
+            }
+        }
+        q_push(pl, sh, PQ_SOLVE, to_solve, slot, lane);
+        q_push(pl, sh, PQ_CTL, to_ctl, slot, lane);
+        if (to_solve || to_ctl) slot = -1;
+        PROF_ADD(0, 1);
+        PROF_ADD(1, __popc(__ballot_sync(MPG_FULL, has)));
+        PROF_LAP(2)
+    }
+    PROF_FLUSH
+    *rays_out = rays;
+}
+
+// ============================================================================
+// compute warps
+// ============================================================================
+template <int KMAX, typename R>
+__device__ __forceinline__ void pool_load_chain(const Pool<KMAX, R> &pl, int slot, int cur, int k, double3 (&x)[KMAX],
+                                                int (&prim)[KMAX], int (&surf)[KMAX]) {
+    const uint32_t sfw = pl.sf[cur * pl.nv + slot];
+#pragma unroll
+    for (int i = 0; i < KMAX; i++) {
+        if (i < k) {
+            x[i] = pl.getx(cur, i, slot);
+            prim[i] = pl.getpr(cur, i, slot);
+        } else {
+            x[i] = make_double3(0.0, 0.0, 0.0);
+            prim[i] = -1;
+        }
+        surf[i] = (int)((sfw >> (4 * i)) & 15u);
+    }
+}
+
+// Newton sweep on fresh chains (walk.cuh PH_SOLVE)
+template <int KMAX, typename R, bool GL>
+__device__ __forceinline__ void pool_solve(const DScene &S, const SeedCtx &g, const WalkParams &P, Pool<KMAX, R> &pl,
+                                           PoolShared *sh, const int lane, int slot, uint32_t &c_vtx) {
+    bool to_ray = false, to_ctl = false;
+    if (slot >= 0) {
+        const uint32_t ctw = pl.ct[slot], stw = pl.st[slot];
+        const int k = (int)(ctw & 15u), cur = (int)((ctw >> 21) & 1u);
+        const uint32_t tau = (ctw >> 4) & 255u;
+        const int it = ST_IT(stw), lid = ST_LID(stw);
+        const uint32_t wi = pl.w[slot], trial = pl.trial[slot];
+        const float3 xD = pl.getxD(slot);
+        const float3 xL = xyz(__ldg(P.seed_xL + wi));
+        double3 x[KMAX];
+        int prim[KMAX], surf[KMAX];
+        pool_load_chain(pl, slot, cur, k, x, prim, surf);
+        c_vtx += k;
+        float cm = 0.f;
+        bool singular = false;
+        R Di[KMAX][4], Ub[KMAX][4];
+        V3<R> sg[KMAX], tg[KMAX], dq[KMAX];
+        int phase = PH_REPROJ, end_status = 0;
+        const int r = newton_system<KMAX, R, GL>(S, g.seed, P.walk_id_base + wi, k, tau, xD, xL, x, prim, surf, P.tol, Di,
+                                                 Ub, sg, tg, dq, singular, cm);
+        if (P.dbg && trial == 0 && (int64_t)wi < P.n_dbg && 2 * it + 1 < P.dbg_stride) {
+            P.dbg[(int64_t)wi * P.dbg_stride + 2 * it] = cm;
+            P.dbg[(int64_t)wi * P.dbg_stride + 2 * it + 1] = pl.beta[slot];
+        }
+        if (r == 1) {
+            end_status = ST_CONVERGED;
+            phase = PH_END;
+            if (trial == 0) {
+                const DLight &L = S.light[lid];
+                float kap;
+                R DL[4];
+                if (!post_sweep<KMAX, R, GL>(S, g.seed, P.walk_id_base + wi, L, k, tau, xD, xL, x, prim, surf, true, kap,
+                                             DL)) {
+                    end_status = ST_BAD_SIDE;
+                } else {
+                    const float3 nD = xyz(__ldg(P.nD + wi / (uint32_t)P.spp));
+                    const float Gc = singular ? 0.0f : ggt_from_blocks<KMAX, R>(k, xD, nD, x, Di, Ub, sg, tg, DL);
+                    float Le = L.emit;
+                    if (L.kind == 1 && !(dot(f3d(x[k - 1]) - xL, L.n) > 0.0f)) Le = 0.0f;
+                    pl.Gc[slot] = Gc;
+                    pl.Tc[slot] = kap * Gc * Le;
+                    phase = PH_VIS;
+                }
+            }
+        } else if (r == 2) {
+            end_status = ST_DEGENERATE;
+            phase = PH_END;
+        } else {
+            if (it >= ((k >= 3 && P.max_iters_long > 0) ? P.max_iters_long : P.max_iters)) {
+                end_status = ST_MAXITER;
+                phase = PH_END;
+            } else {
+#pragma unroll
+                for (int i = 0; i < KMAX; i++)
+                    if (i < k) pl.setdq(i, slot, dq[i]);
+            }
+        }
+        pl.st[slot] = st_pack(it, end_status, false, ST_SEQ(stw), phase, lid);
+        to_ctl = phase == PH_END;
+        to_ray = !to_ctl;
+    }
+    q_push(pl, sh, PQ_RAY, to_ray, slot, lane);
+    q_push(pl, sh, PQ_CTL, to_ctl, slot, lane);
+}
+
+// End-of-attempt bookkeeping, trials, fetch, seeds (walk.cuh PH_END / PH_FETCH / PH_WAIT / PH_SEED)
+// for the slots of one control or wait batch.  Returns true if any lane made progress.
+template <int KMAX, typename R, bool GL>
+__device__ __forceinline__ bool pool_control(const DScene &S, const SeedCtx &g, const WalkParams &P, Pool<KMAX, R> &pl,
+                                             PoolShared *sh, const int lane, int slot, uint32_t &c_newton,
+                                             uint32_t &c_attempts) {
+    unsigned *s_stats = sh->stats;
+    // slot state in registers for the batch
+    int phase = PH_IDLE;
+    int64_t w = -1;
+    uint32_t trial = 0, psurf = 0, ptau = 0, tau = g.tau, ticket = 0xffffffffu;
+    int k = g.k, pk = g.k, cur = 0, it = 0, end_status = 0, lid = 0, item_e = -1;
+    bool occluded = false, seq_only = false;
+    float Tprim = 0.f, pdfL = 1.f;
+    float3 xD = f3(0.f, 0.f, 0.f), xL = f3(0.f, 0.f, 0.f);
+    uint32_t my_resolved = 0;
+    bool progress = false;
+    if (slot >= 0) {
+        const uint32_t ctw = pl.ct[slot], stw = pl.st[slot];
+        phase = ST_PH(stw);
+        it = ST_IT(stw);
+        end_status = ST_END(stw);
+        occluded = ST_OCC(stw);
+        seq_only = ST_SEQ(stw);
+        lid = ST_LID(stw);
+        k = (int)(ctw & 15u);
+        tau = (ctw >> 4) & 255u;
+        cur = (int)((ctw >> 21) & 1u);
+        trial = pl.trial[slot];
+        item_e = pl.item_e[slot];
+        ticket = pl.ticket[slot];
+        if (phase == PH_END) {
+            w = (int64_t)pl.w[slot];
+            const uint32_t pct = pl.pct[slot];
+            pk = (int)(pct & 15u);
+            ptau = pct >> 4;
+            psurf = pl.psurf[slot];
+            Tprim = pl.Tprim[slot];
+            xD = pl.getxD(slot);
+            const float4 l4 = __ldg(P.seed_xL + w);
+            xL = xyz(l4);
+            pdfL = l4.w;
+        }
+    }
+    float3 tgt = f3(0.f, 0.f, 0.f);
+    uint32_t bits = g.tau;
+    bool learned = true;
+    bool to_ray = false, to_wait = false;
+    while (true) {
+        // ---- end of an attempt -------------------------------------------------
+        if (phase == PH_END) {
+            progress = true;
+            c_newton += (uint32_t)it;
+            int st = end_status;
+            if (trial == 0) {
+                float G = 0.f, T = 0.f;
+                if (st == ST_CONVERGED) {
+                    if (occluded) st = ST_OCCLUDED;
+                    else { G = pl.Gc[slot]; T = pl.Tc[slot]; }
+                }
+                uint32_t sfw = 0;
+                if (st != ST_SEED_FAIL && st != ST_INACTIVE) {
+                    sfw = pl.sf[cur * pl.nv + slot];
+#pragma unroll
+                    for (int i = 0; i < KMAX; i++) {
+                        if (i >= k) break;
+                        const int pi = pl.getpr(cur, i, slot);
+                        const double3 xi = pl.getx(cur, i, slot);
+                        int pid = pi >= 0 ? __float_as_int(__ldg(S.tpos + TSTRIDE * pi).w) : -1;
+                        MPG_CHECK(w >= 0 && w < P.n && i < KMAX);
+                        P.chain[(int64_t)i * P.n + w] = make_float4((float)xi.x, (float)xi.y, (float)xi.z, __int_as_float(pid));
+                    }
+                }
+                P.status[w] = (uint8_t)st;
+                P.iters[w] = (uint16_t)it;
+                P.G[w] = G;
+                P.T[w] = T;
+                if (P.out_ctype) P.out_ctype[w] = (uint16_t)((uint32_t)k | (tau << 4));
+                atomicAdd(&s_stats[SS_STATUS0 + st], 1u);
+                atomicAdd(&s_stats[SS_PRIM_IT], (unsigned)it);
+                atomicAdd(&s_stats[SS_WALKS], 1u);
+                if (st == ST_CONVERGED || st == ST_OCCLUDED) atomicAdd(&s_stats[SS_CONV], 1u);
+                if (st == ST_CONVERGED && T > 0.0f && P.trials_on) {
+                    Tprim = T;
+                    pk = k;
+                    ptau = tau;
+                    psurf = 0;
+#pragma unroll
+                    for (int i = 0; i < KMAX; i++) {
+                        if (i >= k) break;
+                        psurf |= ((sfw >> (4 * i)) & 15u) << (4 * i);
+                    }
+                    if (P.psurf_out) P.psurf_out[w] = psurf;
+                    const bool dr = *(volatile unsigned *)&sh->drained != 0u;
+                    if (queue_drained(P, dr) && P.items && hard_publish(P, w, psurf, pk, ptau, 0u, seq_only))
+                        phase = PH_FETCH;
+                    else {
+                        trial = 1;
+                        phase = PH_SEED;
+                    }
+                } else {
+                    P.trials[w] = 0;
+                    P.w[w] = 0.0f;
+                    my_resolved++;
+                    phase = PH_FETCH;
+                }
+            } else {
+                bool same = false;
+                if (st == ST_CONVERGED && k == pk && tau == ptau) {
+                    double3 x[KMAX];
+                    int prim[KMAX], surf[KMAX];
+                    pool_load_chain(pl, slot, cur, k, x, prim, surf);
+                    float kdummy;
+                    R DLdummy[4];
+                    if (post_sweep<KMAX, R, GL>(S, g.seed, P.walk_id_base + w, S.light[lid], k, tau, xD, xL, x, prim, surf,
+                                                false, kdummy, DLdummy)) {
+                        same = true;
+#pragma unroll
+                        for (int i = 0; i < KMAX; i++) {
+                            if (i >= k) break;
+                            float4 c = __ldcg(P.chain + (int64_t)i * P.n + w);
+                            float3 dd = f3d(x[i]) - xyz(c);
+                            if ((int)((psurf >> (4 * i)) & 15u) != (surf[i] & 15) || !(len(dd) < P.same_eps)) same = false;
+                        }
+                    }
+                }
+                const bool dr = *(volatile unsigned *)&sh->drained != 0u;
+                if (item_e >= 0) {
+                    const uint32_t e = (uint32_t)item_e;
+                    if (same) atomicMin(P.e_best + e, trial);
+                    __threadfence();
+                    unsigned left = atomicSub(P.e_pending + e, 1u) - 1u;
+                    phase = PH_FETCH;
+                    if (left == 0) {
+                        __threadfence();
+                        const uint32_t b = *(volatile uint32_t *)(P.e_best + e);
+                        const uint32_t issued = __ldcg(P.e_issued + e);
+                        if (b != HARD_NONE) {
+                            trial_finalize(P, w, b, false, s_stats);
+                            my_resolved++;
+                        } else if (issued >= P.k_max) {
+                            trial_finalize(P, w, P.k_max, true, s_stats);
+                            my_resolved++;
+                        } else {
+                            const unsigned backlog = *(volatile unsigned *)&P.th->item_tail -
+                                                     *(volatile unsigned *)&P.th->item_head;
+                            const uint32_t gr = (int)backlog < (int)P.idle_backlog && queue_drained(P, dr) ? P.item_grow_idle
+                                                                                                          : P.item_grow;
+                            const uint32_t B = min(__ldcg(P.e_batch + e) << gr, P.k_max - issued);
+                            P.e_batch[e] = B;
+                            P.e_pending[e] = B;
+                            P.e_issued[e] = issued + B;
+                            __threadfence();
+                            if (!items_push(P, e, issued + 1, B)) {
+                                P.e_pending[e] = 0;
+                                item_e = -1;
+                                seq_only = true;
+                                trial = issued + 1;
+                                phase = PH_SEED;
+                            }
+                        }
+                    }
+                } else if (same || trial >= P.k_max) {
+                    trial_finalize(P, w, trial, !same, s_stats);
+                    my_resolved++;
+                    phase = PH_FETCH;
+                } else {
+                    if ((trial >= P.local_trials || queue_drained(P, dr)) && !seq_only && P.items &&
+                        hard_publish(P, w, psurf, pk, ptau, trial, seq_only))
+                        phase = PH_FETCH;
+                    else {
+                        trial++;
+                        phase = PH_SEED;
+                    }
+                }
+            }
+        }
+        // ---- fetch a primary walk (warp-aggregated) ------------------------------
+        const unsigned need = __ballot_sync(MPG_FULL, phase == PH_FETCH);
+        if (need) {
+            progress = true;
+            const int leader = __ffs(need) - 1;
+            unsigned long long base = 0;
+            if (lane == leader) {
+                base = atomicAdd(&P.th->queue, (unsigned long long)__popc(need));
+                if (base + __popc(need) >= (unsigned long long)P.n) *(volatile unsigned *)&sh->drained = 1u;
+            }
+            base = __shfl_sync(MPG_FULL, base, leader);
+            if (phase == PH_FETCH) {
+                const int64_t idx = (int64_t)base + __popc(need & ((1u << lane) - 1u));
+                item_e = -1;
+                seq_only = false;
+                if (idx < P.n) {
+                    w = P.perm ? (int64_t)__ldg(P.perm + idx) : idx;
+                    trial = 0;
+                    xD = xyz(__ldg(P.xD + w / P.spp));
+                    const float4 l4 = __ldg(P.seed_xL + w);
+                    xL = xyz(l4);
+                    pdfL = l4.w;
+                    lid = 0;
+                    if (S.n_light > 1) lid = (int)uidx(rng_draw(g.seed, P.walk_id_base + w, 0u, 0u).z, (uint32_t)S.n_light);
+                    phase = PH_SEED;
+                    if (P.trials_only) {
+                        const float T0 = P.T[w];
+                        if (P.status[w] == ST_CONVERGED && T0 > 0.0f && P.trials_on) {
+                            const uint32_t c2 = P.out_ctype ? (uint32_t)P.out_ctype[w] : ((uint32_t)g.k | (g.tau << 4));
+                            pk = (int)(c2 & 15u);
+                            ptau = c2 >> 4;
+                            psurf = P.psurf_out[w];
+                            Tprim = T0;
+                            trial = 1;
+                        } else {
+                            P.trials[w] = 0;
+                            P.w[w] = 0.0f;
+                            my_resolved++;
+                            phase = PH_FETCH;
+                        }
+                    }
+                } else {
+                    phase = PH_WAIT;
+                    ticket = 0xffffffffu;
+                }
+            }
+        }
+        // ---- trial items by ticket ------------------------------------------------
+        {
+            const unsigned needt = __ballot_sync(MPG_FULL, phase == PH_WAIT && ticket == 0xffffffffu);
+            if (needt) {
+                const int leader = __ffs(needt) - 1;
+                unsigned base = 0;
+                if (lane == leader) base = atomicAdd(&P.th->item_head, (unsigned)__popc(needt));
+                base = __shfl_sync(MPG_FULL, base, leader);
+                if (phase == PH_WAIT && ticket == 0xffffffffu) ticket = base + (unsigned)__popc(needt & ((1u << lane) - 1u));
+            }
+        }
+        if (phase == PH_WAIT) {
+            const unsigned long long wd =
+                ticket < P.item_cap ? *(volatile unsigned long long *)(P.items + ticket) : ITEM_EMPTY;
+            if (wd != ITEM_EMPTY) {
+                progress = true;
+                ticket = 0xffffffffu;
+                item_e = (int)(wd >> 32);
+                trial = (uint32_t)wd;
+                MPG_CHECK(item_e >= 0 && (uint32_t)item_e < P.hard_cap);
+                w = __ldcg(P.e_walk + item_e);
+                MPG_CHECK(w >= 0 && w < P.n);
+                psurf = __ldcg(P.e_psurf + item_e);
+                const uint32_t pct = __ldcg(P.e_pct + item_e);
+                pk = (int)(pct & 15u);
+                ptau = pct >> 4;
+                xD = xyz(__ldg(P.xD + w / P.spp));
+                const float4 l4 = __ldg(P.seed_xL + w);
+                xL = xyz(l4);
+                pdfL = l4.w;
+                lid = 0;
+                if (S.n_light > 1) lid = (int)uidx(rng_draw(g.seed, P.walk_id_base + w, 0u, 0u).z, (uint32_t)S.n_light);
+                if (*(volatile uint32_t *)(P.e_best + item_e) < trial) { end_status = ST_SEED_FAIL; it = 0; phase = PH_END; }
+                else phase = PH_SEED;
+            } else {
+                if (*(volatile unsigned int *)&P.th->resolved >= (unsigned int)P.n) *(volatile unsigned *)&sh->done = 1u;
+                to_wait = true;   // park the slot again
+            }
+        }
+        // ---- seed -------------------------------------------------------------------
+        if (phase == PH_SEED) {
+            c_attempts++;
+            bool ok;
+            bool inactive = false;
+            if (trial == 0) {
+                const int sb = __ldg(P.seed_bin + w);
+                ok = sb >= -1;
+                inactive = sb == -3;
+                tgt = xyz(__ldg(P.seed_tgt + w));
+                k = g.k;
+                bits = g.tau;
+                learned = true;
+                if (P.seed_ctype) {
+                    const uint32_t c2 = __ldg(P.seed_ctype + w);
+                    k = (int)(c2 & 15u);
+                    bits = (c2 >> 4) & 255u;
+                    learned = (c2 >> 12) & 1u;
+                }
+            } else {
+                SeedRes sr;
+                ok = seed_target(S, g, P.walk_id_base + w, trial + P.trial_base, xD, xL, sr);
+                tgt = sr.tgt;
+                k = sr.n;
+                bits = sr.bits;
+                learned = sr.learned;
+            }
+            k = max(1, min(k, KMAX));
+            it = 0;
+            if (ok) {
+                phase = PH_DEDUCE;
+                to_ray = true;
+            } else {
+                end_status = inactive ? ST_INACTIVE : ST_SEED_FAIL;
+                phase = PH_END;
+            }
+        }
+        if (!__any_sync(MPG_FULL, phase == PH_END || phase == PH_FETCH || phase == PH_SEED)) break;
+    }
+    // ---- store the slots and hand them on --------------------------------------------
+    if (slot >= 0) {
+        if (to_ray) {
+            pl.w[slot] = (uint32_t)w;
+            pl.trial[slot] = trial;
+            pl.ct[slot] = ct_pack(k, g.tau, bits, learned, 0);
+            pl.pct[slot] = (uint32_t)pk | (ptau << 4);
+            pl.psurf[slot] = psurf;
+            pl.Tprim[slot] = Tprim;
+            pl.item_e[slot] = item_e;
+            pl.beta[slot] = P.beta0;
+            pl.setxD(slot, xD);
+            pl.settgt(slot, tgt);
+            pl.sf[slot] = 0u;
+            pl.st[slot] = st_pack(0, 0, false, seq_only, PH_DEDUCE, lid);
+        } else {
+            pl.ticket[slot] = ticket;
+            pl.st[slot] = st_pack(0, 0, false, false, PH_WAIT, 0);
+        }
+    }
+    // walks made final by this batch: one atomic per warp, after their outputs
+    const unsigned tot = __reduce_add_sync(MPG_FULL, my_resolved);
+    if (tot) {
+        __threadfence();
+        if (lane == 0) atomicAdd(&P.th->resolved, tot);
+    }
+    q_push(pl, sh, PQ_RAY, to_ray, slot, lane);
+    q_push(pl, sh, PQ_WAIT, slot >= 0 && !to_ray, slot, lane);
+    (void)pdfL;
+    (void)to_wait;
+    return progress;
+}
+
+template <int KMAX, typename R, bool GL>
+__device__ __forceinline__ void pool_compute_role(const DScene &S, const SeedCtx &g, const WalkParams &P,
+                                                  Pool<KMAX, R> &pl, PoolShared *sh, const int lane,
+                                                  uint32_t &c_newton, uint32_t &c_attempts, uint32_t &c_vtx,
+                                                  const int dbgm) {
+    unsigned idle_ns = 32u, backoff = 256u;
+    int idle_loops = 0;
+    PROF_DECL
+    while (true) {
+        int kind = -1, got = 0;
+        unsigned base = 0;
+        if (lane == 0) {
+            // (read by one lane and broadcast: the decision to leave must be warp-uniform)
+            if (*(volatile unsigned *)&sh->done) got = -1;
+            else {
+                got = q_reserve(sh, PQ_SOLVE, 32, base);
+                kind = PQ_SOLVE;
+                if (!got) { got = q_reserve(sh, PQ_CTL, 32, base); kind = PQ_CTL; }
+                if (!got) { got = q_reserve(sh, PQ_WAIT, 32, base); kind = PQ_WAIT; }
+            }
+        }
+        got = __shfl_sync(MPG_FULL, got, 0);
+        kind = __shfl_sync(MPG_FULL, kind, 0);
+        base = __shfl_sync(MPG_FULL, base, 0);
+        if (got < 0) break;
+        if (!got) {
+            PROF_ADD(14, 1);
+            PROF_LAP(13)
+            if (dbgm == 2 && ++idle_loops > 1000) break;
+            __nanosleep(idle_ns);
+            idle_ns = min(2u * idle_ns, 512u);
+            continue;
+        }
+        idle_ns = 32u;
+        const int slot = lane < got ? q_take(pl, kind, base + (unsigned)lane) : -1;
+        if (kind == PQ_SOLVE) {
+            pool_solve<KMAX, R, GL>(S, g, P, pl, sh, lane, slot, c_vtx);
+            backoff = 256u;
+            PROF_ADD(5, 1);
+            PROF_ADD(6, got);
+            PROF_LAP(7)
+        } else {
+            const bool progress = pool_control<KMAX, R, GL>(S, g, P, pl, sh, lane, slot, c_newton, c_attempts);
+#ifdef MPG_POOL_PROF
+            if (kind == PQ_CTL) { PROF_ADD(8, 1); PROF_ADD(9, got); PROF_LAP(10) }
+            else { PROF_ADD(11, 1); PROF_LAP(12) }
+#endif
+            if (kind == PQ_WAIT && !__any_sync(MPG_FULL, progress)) {
+                // nothing but waiting slots, and no item for them yet: back off
+                __nanosleep(backoff);
+                backoff = min(2u * backoff, P.backoff_max);
+            } else {
+                backoff = 256u;
+            }
+        }
+    }
+    PROF_FLUSH
+}
+
+// NTW trace warpgroups + NCW compute warpgroups (4 warps each); RT / RC: registers per
+// thread of the two roles after setmaxnreg (0: no redistribution)
+template <int KMAX, typename R, int W, bool GL, int NTW, int NCW, int RT, int RC>
+__global__ void __launch_bounds__((NTW + NCW) * 128, 1)
+    k_walk_pool(const DScene S, const SeedCtx g, const WalkParams P, const int nv, const int nvq, const int dbgm) {
+    extern __shared__ __align__(16) unsigned char pool_smem[];
+    __shared__ PoolShared sh;
+    Pool<KMAX, R> pl;
+    pl.carve(pool_smem, nv, nvq);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (threadIdx.x < PQ_N) { sh.head[threadIdx.x] = 0u; sh.tail[threadIdx.x] = 0u; }
+    if (threadIdx.x == 0) { sh.done = 0u; sh.drained = 0u; }
+    for (int i = threadIdx.x; i < SS_N; i += blockDim.x) sh.stats[i] = 0u;
+    for (int i = threadIdx.x; i < PQ_N * nvq; i += blockDim.x) pl.ring[i] = 0;
+    __syncthreads();
+    // every slot starts in the control queue, asking for a primary walk
+    for (int i = threadIdx.x; i < nv; i += blockDim.x) {
+        pl.st[i] = st_pack(0, 0, false, false, PH_FETCH, 0);
+        pl.ct[i] = ct_pack(g.k, g.tau, g.tau, true, 0);
+        pl.trial[i] = 0u;
+        pl.item_e[i] = -1;
+        pl.ticket[i] = 0xffffffffu;
+        pl.ring[(size_t)PQ_CTL * nvq + i] = (unsigned short)(i + 1);
+    }
+    if (threadIdx.x == 0) sh.tail[PQ_CTL] = (unsigned)nv;
+    __syncthreads();
+
+    unsigned long long v[6] = {0ull, 0ull, 0ull, 0ull, 0ull, 0ull};
+    if (dbgm == 1) return;
+    if (warp < NTW * 4) {
+        if (dbgm == 2) return;
+        reg_dec<RT>();
+        LaneStats ls = {0u, 0u, 0u};
+        unsigned long long rays = 0;
+        pool_trace_role<KMAX, R, W, GL>(S, g, P, pl, &sh, lane, &rays, ls, dbgm);
+        v[2] = rays; v[3] = ls.nodes; v[4] = ls.tris;
+    } else {
+        reg_inc<RC>();
+        uint32_t c_newton = 0, c_attempts = 0, c_vtx = 0;
+        pool_compute_role<KMAX, R, GL>(S, g, P, pl, &sh, lane, c_newton, c_attempts, c_vtx, dbgm);
+        v[0] = c_newton; v[1] = c_attempts; v[5] = c_vtx;
+    }
+    // ---- stats reduction ----------------------------------------------------
+#pragma unroll
+    for (int j = 0; j < 6; j++) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v[j] += __shfl_down_sync(MPG_FULL, v[j], o);
+    }
+    if (lane == 0 && P.stats) {
+        if (v[0]) atomicAdd(P.stats + SS_NEWTON, v[0]);
+        if (v[1]) atomicAdd(P.stats + SS_ATTEMPTS, v[1]);
+        if (v[2]) atomicAdd(P.stats + SS_RAYS, v[2]);
+        if (v[3]) atomicAdd(P.stats + SS_NODES, v[3]);
+        if (v[4]) atomicAdd(P.stats + SS_TRIS, v[4]);
+        if (v[5]) atomicAdd(P.stats + SS_VTX, v[5]);
+    }
+    __syncthreads();
+    if (P.stats)
+        for (int i = threadIdx.x; i < SS_N; i += blockDim.x)
+            if (sh.stats[i]) atomicAdd(P.stats + i, (unsigned long long)sh.stats[i]);
+}
