@@ -1238,11 +1238,11 @@ static bool pool_enabled() {
     const char *e = getenv("MPG_POOL");
     return e ? atoi(e) != 0 : MPG_POOL_DEFAULT != 0;
 }
-template <int KMAX, typename R, bool GL, int NTW, int NCW, int RT, int RC>
+template <int KMAX, typename R, bool GL, int NW>
 static mpg_status launch_pool(const DScene &S, const SeedCtx &g, WalkParams P, cudaStream_t st) {
     const bool wide = S.bvh_w == 4;
-    auto k4 = k_walk_pool<KMAX, R, 4, GL, NTW, NCW, RT, RC>;
-    auto k2 = k_walk_pool<KMAX, R, 2, GL, NTW, NCW, RT, RC>;
+    auto k4 = k_walk_pool<KMAX, R, 4, GL, NW>;
+    auto k2 = k_walk_pool<KMAX, R, 2, GL, NW>;
     auto kern = wide ? k4 : k2;
     int smem_kb = 160, nv_want = 1024;
     if (const char *e = getenv("MPG_POOL_SMEM_KB")) smem_kb = std::max(16, std::min(226, atoi(e)));
@@ -1269,24 +1269,18 @@ static mpg_status launch_pool(const DScene &S, const SeedCtx &g, WalkParams P, c
         P.idle_backlog = div ? (uint32_t)((int64_t)blocks * nv / div) : 0x7fffffffu;
     }
     COUNT_LAUNCH(1);
-    int dbgm = 0;
-    if (const char *e = getenv("MPG_POOL_DBG")) dbgm = atoi(e);
-    kern<<<blocks, (NTW + NCW) * 128, bytes, st>>>(S, g, P, nv, nvq, dbgm);
+    // phase scheduling: a Newton phase once s_min fresh chains wait, a control phase once c_min ended
+    // attempts wait (or when nothing else is left)
+    int s_min = NW * 32 * 7 / 10, c_min = nv / 4;
+    if (const char *e = getenv("MPG_POOL_SMIN")) s_min = atoi(e);
+    if (const char *e = getenv("MPG_POOL_CMIN")) c_min = atoi(e);
+    kern<<<blocks, NW * 32, bytes, st>>>(S, g, P, nv, nvq, std::max(1, s_min), std::max(1, c_min));
     CUDA_TRY(cudaPeekAtLastError());
     return MPG_OK;
 }
-// role split per chain length (warpgroups of 4 warps; registers after setmaxnreg)
-#ifndef MPG_POOL_NTW
-#define MPG_POOL_NTW 3
-#endif
-#ifndef MPG_POOL_NCW
-#define MPG_POOL_NCW 2
-#endif
-#ifndef MPG_POOL_RT
-#define MPG_POOL_RT 0
-#endif
-#ifndef MPG_POOL_RC
-#define MPG_POOL_RC 0
+// warps per block (one block per SM; registers per thread = 65536 / (32 NW), rounded down to 8)
+#ifndef MPG_POOL_NW
+#define MPG_POOL_NW 20
 #endif
 #ifdef MPG_POOL_PROF
 extern "C" int mpg_debug_pool_prof(unsigned long long *out16) {
@@ -1368,7 +1362,7 @@ static mpg_status launch_walk(const DScene &S, const SeedCtx &g, WalkParams P, c
     }
     if constexpr (PoolBuilt<KMAX>::value && !CMP) {
         if (pool_enabled())
-            return launch_pool<KMAX, R, GL, MPG_POOL_NTW, MPG_POOL_NCW, MPG_POOL_RT, MPG_POOL_RC>(S, g, P, st);
+            return launch_pool<KMAX, R, GL, MPG_POOL_NW>(S, g, P, st);
     }
     int64_t want = (P.n + 127) / 128;
     int blocks = (int)std::min<int64_t>(want, (int64_t)num_sms() * occ);

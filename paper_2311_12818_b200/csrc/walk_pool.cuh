@@ -31,12 +31,12 @@
 #include "walk.cuh"
 
 enum { PQ_RAY = 0, PQ_SOLVE = 1, PQ_CTL = 2, PQ_WAIT = 3, PQ_N = 4 };
+enum { PS_TRACE = 0, PS_SOLVE = 1, PS_CTL = 2, PS_SLEEP = 3, PS_EXIT = 4 };
 
 // MPG_POOL_PROF: diagnostic build (tools/pool_prof.py): per-role cycle and batch counters
 #ifdef MPG_POOL_PROF
-// trace: 0 rounds, 1 lanes with a ray, 2 busy cycles, 3 idle cycles, 4 idle rounds
-// compute: 5 solve batches, 6 solve slots, 7 solve cycles, 8 ctl batches, 9 ctl slots, 10 ctl cycles,
-//          11 wait batches, 12 wait cycles, 13 idle cycles, 14 idle rounds
+// per warp: 0 T phases, 1 S phases, 4 C phases, 2 T cycles, 7 S cycles, 10 C cycles, 11 scheduler + barrier
+// cycles, 5 solve batches, 6 solve slots, 8 control batches, 9 control slots
 __device__ unsigned long long g_pool_prof[16];
 #define PROF_DECL unsigned long long pf_[16] = {0}; long long pf_t = clock64();
 #define PROF_ADD(i, v) (pf_[i] += (unsigned long long)(v))
@@ -51,6 +51,9 @@ __device__ unsigned long long g_pool_prof[16];
 
 struct PoolShared {
     unsigned head[PQ_N], tail[PQ_N];
+    unsigned end[PQ_N];     // phase snapshot of the tails (entries present when the phase began)
+    unsigned sel;           // phase chosen by the scheduler thread
+    unsigned progress;      // a control phase moved some slot on
     unsigned done, drained;
     unsigned stats[SS_N];
 };
@@ -138,16 +141,14 @@ template <int KMAX, typename R> struct Pool {
 // overflows.  Producers reserve positions with one atomicAdd per warp and then write the entries;
 // consumers reserve [head, head + take) below the reserved tail with a CAS and wait (briefly: the
 // producer is between its atomicAdd and its store) for each entry to appear.
-__device__ __forceinline__ int q_reserve(PoolShared *sh, int q, int want, unsigned &base) {
-    while (true) {
-        const unsigned h = *(volatile unsigned *)&sh->head[q];
-        const unsigned t = *(volatile unsigned *)&sh->tail[q];
-        const int avail = (int)(t - h);
-        const int take = min(want, avail);
-        if (take <= 0) return 0;
-        if (atomicCAS(&sh->head[q], h, h + (unsigned)take) == h) { base = h; return take; }
-    }
+// (one atomicAdd per reservation; a reservation that reaches past `end` is cut there and the
+// overshoot of `head` is undone by the scheduler thread after the phase, when no one reserves)
+__device__ __forceinline__ int q_reserve(PoolShared *sh, int q, int want, unsigned &base, unsigned end) {
+    if ((int)(end - *(volatile unsigned *)&sh->head[q]) <= 0) return 0;
+    base = atomicAdd(&sh->head[q], (unsigned)want);
+    return max(0, min(want, (int)(end - base)));
 }
+__device__ __forceinline__ unsigned q_tail(PoolShared *sh, int q) { return *(volatile unsigned *)&sh->tail[q]; }
 template <int KMAX, typename R>
 __device__ __forceinline__ int q_take(const Pool<KMAX, R> &pl, int q, unsigned pos) {
     volatile unsigned short *e = pl.ring + (size_t)q * pl.nvq + (pos & (unsigned)(pl.nvq - 1));
@@ -176,44 +177,31 @@ __device__ __forceinline__ void q_push(const Pool<KMAX, R> &pl, PoolShared *sh, 
     __syncwarp();
 }
 
-template <int REGS> __device__ __forceinline__ void reg_inc() {
-    if constexpr (REGS > 0) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(REGS));
-}
-template <int REGS> __device__ __forceinline__ void reg_dec() {
-    if constexpr (REGS > 0) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(REGS));
-}
-
 // ============================================================================
-// trace warps: the chain-ray loop of one pass per slot (body of walk.cuh's trace_chain,
-// one ray per iteration, lanes refilled from the ray queue between rays)
+// trace phase: the chain-ray loop of one pass per slot (body of walk.cuh's trace_chain,
+// one ray per round); lanes take slots from the ray queue below t_end (the entries
+// present when the phase began) until none is left
 // ============================================================================
 template <int KMAX, typename R, int W, bool GL>
-__device__ __forceinline__ void pool_trace_role(const DScene &S, const SeedCtx &g, const WalkParams &P,
-                                                Pool<KMAX, R> &pl, PoolShared *sh, const int lane,
-                                                unsigned long long *rays_out, LaneStats &ls, const int dbgm) {
+__device__ __forceinline__ void pool_trace_phase(const DScene &S, const SeedCtx &g, const WalkParams &P,
+                                                 Pool<KMAX, R> &pl, PoolShared *sh, const int lane, const unsigned t_end,
+                                                 unsigned long long &rays, LaneStats &ls) {
     int slot = -1;
     int mode = TR_REPROJ, k = 1, ti = -1, it = 0, cur = 0, tpp = -1, tps = 0, tcode = 0;
     uint32_t bits = 0, tres = 0, sreq = 0, ysf = 0, stw = 0, ctw = 0, wi = 0;
     float beta = 1.f;
     float3 xD = f3(0.f, 0.f, 0.f);
     double3 to = make_double3(0.0, 0.0, 0.0), tdd = make_double3(0.0, 0.0, 1.0);
-    unsigned idle_ns = 32u;
-    unsigned long long rays = 0;
-    PROF_DECL
     while (true) {
         // ---- refill the lanes without a slot ---------------------------------
         const unsigned need = __ballot_sync(MPG_FULL, slot < 0);
         if (need) {
             int got = 0;
             unsigned base = 0;
-            if (lane == 0) {
-                got = q_reserve(sh, PQ_RAY, __popc(need), base);
-                // (read by one lane and broadcast: the decision to leave must be warp-uniform)
-                if (!got && need == MPG_FULL && *(volatile unsigned *)&sh->done) got = -1;
-            }
+            if (lane == 0) got = q_reserve(sh, PQ_RAY, __popc(need), base, t_end);
             got = __shfl_sync(MPG_FULL, got, 0);
             base = __shfl_sync(MPG_FULL, base, 0);
-            if (got < 0) break;
+            if (need == MPG_FULL && got == 0) break;   // nothing held, nothing left
             const int rank = __popc(need & ((1u << lane) - 1u));
             if (slot < 0 && rank < got) {
                 slot = q_take(pl, PQ_RAY, base + (unsigned)rank);
@@ -239,15 +227,7 @@ __device__ __forceinline__ void pool_trace_role(const DScene &S, const SeedCtx &
                     else tdd = v * rsqrt(l2);
                 }
             }
-            if (need == MPG_FULL && got == 0) {   // the whole warp is idle
-                PROF_ADD(4, 1);
-                PROF_LAP(3)
-                __nanosleep(idle_ns);
-                idle_ns = min(2u * idle_ns, 512u);
-                continue;
-            }
         }
-        idle_ns = 32u;
         // ---- this lane's ray ti (top of the trace_chain loop body) -----------
         bool has = slot >= 0 && ti >= 0;
         float3 of = f3(0.f, 0.f, 0.f), d = f3(0.f, 0.f, 1.f);
@@ -286,8 +266,7 @@ __device__ __forceinline__ void pool_trace_role(const DScene &S, const SeedCtx &
             const bool vis = mode == TR_VIS;
             Hit h;
             rays++;
-            bool hit = false;
-            if (dbgm != 3) hit = trace<W>(S, of, d, P.ray_eps, tmax, !vis, vis, h, ls, vis ? -1 : hint);
+            const bool hit = trace<W>(S, of, d, P.ray_eps, tmax, !vis, vis, h, ls, vis ? -1 : hint);
             // ---- consume the hit (bottom of the trace_chain loop body) ---------
             if (vis) {
                 if (hit) { tcode = 5; ti = -1; }
@@ -324,7 +303,7 @@ __device__ __forceinline__ void pool_trace_role(const DScene &S, const SeedCtx &
             }
         }
         // ---- end of a pass (walk.cuh MPG_TRACE_TAIL) -------------------------
-        bool to_solve = false, to_ctl = false;
+        bool to_solve = false, to_ctl = false, to_ray = false;
         if (slot >= 0 && ti < 0) {
             const bool ok = tcode == 0, ded = mode == TR_DEDUCE;
             uint32_t tau = (ctw >> 4) & 255u;
@@ -352,27 +331,21 @@ __device__ __forceinline__ void pool_trace_role(const DScene &S, const SeedCtx &
                     if (it >= ((k >= 3 && P.max_iters_long > 0) ? P.max_iters_long : P.max_iters)) {
                         end_status = ST_MAXITER;
                         to_ctl = true;
-                    } else {   // step halving: retrace the same chain with the shorter step
-                        ti = 0; tres = 0; tcode = 0; ysf = 0; tpp = -1; tps = 0;
-                        to = d3f(xD);
+                    } else {   // step halving: the same chain with the shorter step, in the next trace phase
+                        phase = PH_REPROJ;
+                        to_ray = true;
                     }
                 }
             }
-            if (to_solve || to_ctl) {
-                pl.ct[slot] = ct_pack(k, tau, bits, (ctw >> 20) & 1u, cur);
-                pl.st[slot] = st_pack(it, end_status, occ, ST_SEQ(stw), phase, ST_LID(stw));
-                pl.beta[slot] = beta;
-            }
+            pl.ct[slot] = ct_pack(k, tau, bits, (ctw >> 20) & 1u, cur);
+            pl.st[slot] = st_pack(it, end_status, occ, ST_SEQ(stw), phase, ST_LID(stw));
+            pl.beta[slot] = beta;
         }
         q_push(pl, sh, PQ_SOLVE, to_solve, slot, lane);
         q_push(pl, sh, PQ_CTL, to_ctl, slot, lane);
-        if (to_solve || to_ctl) slot = -1;
-        PROF_ADD(0, 1);
-        PROF_ADD(1, __popc(__ballot_sync(MPG_FULL, has)));
-        PROF_LAP(2)
+        q_push(pl, sh, PQ_RAY, to_ray, slot, lane);
+        if (to_solve || to_ctl || to_ray) slot = -1;
     }
-    PROF_FLUSH
-    *rays_out = rays;
 }
 
 // ============================================================================
@@ -799,75 +772,21 @@ __device__ __forceinline__ bool pool_control(const DScene &S, const SeedCtx &g, 
     return progress;
 }
 
-template <int KMAX, typename R, bool GL>
-__device__ __forceinline__ void pool_compute_role(const DScene &S, const SeedCtx &g, const WalkParams &P,
-                                                  Pool<KMAX, R> &pl, PoolShared *sh, const int lane,
-                                                  uint32_t &c_newton, uint32_t &c_attempts, uint32_t &c_vtx,
-                                                  const int dbgm) {
-    unsigned idle_ns = 32u, backoff = 256u;
-    int idle_loops = 0;
-    PROF_DECL
-    while (true) {
-        int kind = -1, got = 0;
-        unsigned base = 0;
-        if (lane == 0) {
-            // (read by one lane and broadcast: the decision to leave must be warp-uniform)
-            if (*(volatile unsigned *)&sh->done) got = -1;
-            else {
-                got = q_reserve(sh, PQ_SOLVE, 32, base);
-                kind = PQ_SOLVE;
-                if (!got) { got = q_reserve(sh, PQ_CTL, 32, base); kind = PQ_CTL; }
-                if (!got) { got = q_reserve(sh, PQ_WAIT, 32, base); kind = PQ_WAIT; }
-            }
-        }
-        got = __shfl_sync(MPG_FULL, got, 0);
-        kind = __shfl_sync(MPG_FULL, kind, 0);
-        base = __shfl_sync(MPG_FULL, base, 0);
-        if (got < 0) break;
-        if (!got) {
-            PROF_ADD(14, 1);
-            PROF_LAP(13)
-            if (dbgm == 2 && ++idle_loops > 1000) break;
-            __nanosleep(idle_ns);
-            idle_ns = min(2u * idle_ns, 512u);
-            continue;
-        }
-        idle_ns = 32u;
-        const int slot = lane < got ? q_take(pl, kind, base + (unsigned)lane) : -1;
-        if (kind == PQ_SOLVE) {
-            pool_solve<KMAX, R, GL>(S, g, P, pl, sh, lane, slot, c_vtx);
-            backoff = 256u;
-            PROF_ADD(5, 1);
-            PROF_ADD(6, got);
-            PROF_LAP(7)
-        } else {
-            const bool progress = pool_control<KMAX, R, GL>(S, g, P, pl, sh, lane, slot, c_newton, c_attempts);
-#ifdef MPG_POOL_PROF
-            if (kind == PQ_CTL) { PROF_ADD(8, 1); PROF_ADD(9, got); PROF_LAP(10) }
-            else { PROF_ADD(11, 1); PROF_LAP(12) }
-#endif
-            if (kind == PQ_WAIT && !__any_sync(MPG_FULL, progress)) {
-                // nothing but waiting slots, and no item for them yet: back off
-                __nanosleep(backoff);
-                backoff = min(2u * backoff, P.backoff_max);
-            } else {
-                backoff = 256u;
-            }
-        }
-    }
-    PROF_FLUSH
-}
-
-// NTW trace warpgroups + NCW compute warpgroups (4 warps each); RT / RC: registers per
-// thread of the two roles after setmaxnreg (0: no redistribution)
-template <int KMAX, typename R, int W, bool GL, int NTW, int NCW, int RT, int RC>
-__global__ void __launch_bounds__((NTW + NCW) * 128, 1)
-    k_walk_pool(const DScene S, const SeedCtx g, const WalkParams P, const int nv, const int nvq, const int dbgm) {
+// One block per SM, NW universal warps.  The block cycles through three phases separated by
+// barriers, so that at any time all its warps execute the same (instruction-cache-sized) code:
+//   T  trace one pass of every slot in the ray queue,
+//   S  Newton sweep of every slot with a fresh chain,
+//   C  end-of-attempt bookkeeping / trials / fetch / seeds of every slot in the control queue,
+//      and one poll of the trial-item ring for the waiting slots.
+template <int KMAX, typename R, int W, bool GL, int NW>
+__global__ void __launch_bounds__(NW * 32, 1)
+    k_walk_pool(const DScene S, const SeedCtx g, const WalkParams P, const int nv, const int nvq, const int s_min,
+                const int c_min) {
     extern __shared__ __align__(16) unsigned char pool_smem[];
     __shared__ PoolShared sh;
     Pool<KMAX, R> pl;
     pl.carve(pool_smem, nv, nvq);
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
     if (threadIdx.x < PQ_N) { sh.head[threadIdx.x] = 0u; sh.tail[threadIdx.x] = 0u; }
     if (threadIdx.x == 0) { sh.done = 0u; sh.drained = 0u; }
     for (int i = threadIdx.x; i < SS_N; i += blockDim.x) sh.stats[i] = 0u;
@@ -885,22 +804,94 @@ __global__ void __launch_bounds__((NTW + NCW) * 128, 1)
     if (threadIdx.x == 0) sh.tail[PQ_CTL] = (unsigned)nv;
     __syncthreads();
 
-    unsigned long long v[6] = {0ull, 0ull, 0ull, 0ull, 0ull, 0ull};
-    if (dbgm == 1) return;
-    if (warp < NTW * 4) {
-        if (dbgm == 2) return;
-        reg_dec<RT>();
-        LaneStats ls = {0u, 0u, 0u};
-        unsigned long long rays = 0;
-        pool_trace_role<KMAX, R, W, GL>(S, g, P, pl, &sh, lane, &rays, ls, dbgm);
-        v[2] = rays; v[3] = ls.nodes; v[4] = ls.tris;
-    } else {
-        reg_inc<RC>();
-        uint32_t c_newton = 0, c_attempts = 0, c_vtx = 0;
-        pool_compute_role<KMAX, R, GL>(S, g, P, pl, &sh, lane, c_newton, c_attempts, c_vtx, dbgm);
-        v[0] = c_newton; v[1] = c_attempts; v[5] = c_vtx;
+    LaneStats ls = {0u, 0u, 0u};
+    unsigned long long rays = 0;
+    uint32_t c_newton = 0, c_attempts = 0, c_vtx = 0;
+    unsigned backoff = 256u;
+    if (threadIdx.x == 0) { sh.sel = PS_CTL; sh.progress = 1u; }
+    for (int q = threadIdx.x; q < PQ_N; q += blockDim.x) sh.end[q] = 0u;
+    PROF_DECL
+    while (true) {
+        // ---- scheduler: thread 0 picks the next phase from the queue lengths ---------------
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            for (int q = 0; q < PQ_N; q++)   // undo reservation overshoots of the last phase
+                if ((int)(sh.head[q] - sh.end[q]) > 0) sh.head[q] = sh.end[q];
+            const int nR = (int)(sh.tail[PQ_RAY] - sh.head[PQ_RAY]), nS = (int)(sh.tail[PQ_SOLVE] - sh.head[PQ_SOLVE]),
+                      nC = (int)(sh.tail[PQ_CTL] - sh.head[PQ_CTL]);
+            unsigned sel;
+            if (sh.done) sel = PS_EXIT;
+            else if (nS >= s_min) sel = PS_SOLVE;
+            else if (nC >= c_min) sel = PS_CTL;
+            else if (nR > 0) sel = PS_TRACE;
+            else if (nS > 0) sel = PS_SOLVE;
+            else if (nC > 0) sel = PS_CTL;
+            else sel = sh.progress ? PS_CTL : PS_SLEEP;   // only waiting slots: poll (with back-off)
+            for (int q = 0; q < PQ_N; q++) sh.end[q] = sh.tail[q];
+            if (sel != PS_CTL && sel != PS_SLEEP) { sh.end[PQ_CTL] = sh.head[PQ_CTL]; sh.end[PQ_WAIT] = sh.head[PQ_WAIT]; }
+            if (sel != PS_TRACE) sh.end[PQ_RAY] = sh.head[PQ_RAY];
+            if (sel != PS_SOLVE) sh.end[PQ_SOLVE] = sh.head[PQ_SOLVE];
+            sh.progress = 0u;
+            sh.sel = sel;
+        }
+        __syncthreads();
+        const unsigned sel = sh.sel;
+        PROF_LAP(11)
+        if (sel == PS_EXIT) break;
+        if (sel == PS_TRACE) {
+            // ---- T: one pass of every slot in the ray queue -------------------------------
+            pool_trace_phase<KMAX, R, W, GL>(S, g, P, pl, &sh, lane, sh.end[PQ_RAY], rays, ls);
+            PROF_LAP(2)
+            PROF_ADD(0, 1);
+        } else if (sel == PS_SOLVE) {
+            // ---- S: Newton sweep of the fresh chains --------------------------------------
+            const unsigned s_end = sh.end[PQ_SOLVE];
+            while (true) {
+                int got = 0;
+                unsigned base = 0;
+                if (lane == 0) got = q_reserve(&sh, PQ_SOLVE, 32, base, s_end);
+                got = __shfl_sync(MPG_FULL, got, 0);
+                base = __shfl_sync(MPG_FULL, base, 0);
+                if (!got) break;
+                const int slot = lane < got ? q_take(pl, PQ_SOLVE, base + (unsigned)lane) : -1;
+                pool_solve<KMAX, R, GL>(S, g, P, pl, &sh, lane, slot, c_vtx);
+                PROF_ADD(5, 1);
+                PROF_ADD(6, got);
+            }
+            PROF_LAP(7)
+            PROF_ADD(1, 1);
+        } else {
+            // ---- C: control queue, then one poll of the waiting slots ---------------------
+            if (sel == PS_SLEEP) {
+                __nanosleep(backoff);
+                backoff = min(2u * backoff, P.backoff_max);
+            } else {
+                backoff = 256u;
+            }
+            bool progress = false;
+            for (int q = PQ_CTL; q <= PQ_WAIT; q++) {
+                const unsigned q_end = sh.end[q];   // slots re-parked in this phase wait for the next
+                while (true) {
+                    int got = 0;
+                    unsigned base = 0;
+                    if (lane == 0) got = q_reserve(&sh, q, 32, base, q_end);
+                    got = __shfl_sync(MPG_FULL, got, 0);
+                    base = __shfl_sync(MPG_FULL, base, 0);
+                    if (!got) break;
+                    const int slot = lane < got ? q_take(pl, q, base + (unsigned)lane) : -1;
+                    progress |= pool_control<KMAX, R, GL>(S, g, P, pl, &sh, lane, slot, c_newton, c_attempts);
+                    PROF_ADD(8, 1);
+                    PROF_ADD(9, got);
+                }
+            }
+            if (__any_sync(MPG_FULL, progress) && lane == 0) *(volatile unsigned *)&sh.progress = 1u;
+            PROF_LAP(10)
+            PROF_ADD(4, 1);
+        }
     }
+    PROF_FLUSH
     // ---- stats reduction ----------------------------------------------------
+    unsigned long long v[6] = {c_newton, c_attempts, rays, ls.nodes, ls.tris, c_vtx};
 #pragma unroll
     for (int j = 0; j < 6; j++) {
 #pragma unroll
