@@ -1244,25 +1244,41 @@ static mpg_status launch_pool(const DScene &S, const SeedCtx &g, WalkParams P, c
     auto k4 = k_walk_pool<KMAX, R, 4, GL, NW>;
     auto k2 = k_walk_pool<KMAX, R, 2, GL, NW>;
     auto kern = wide ? k4 : k2;
-    int smem_kb = 160, nv_want = 1024;
+    int smem_kb = 160 / MPG_POOL_BPS, nv_want = 1024;
     if (const char *e = getenv("MPG_POOL_SMEM_KB")) smem_kb = std::max(16, std::min(226, atoi(e)));
-    if (const char *e = getenv("MPG_POOL_NV")) nv_want = std::max(32, std::min(8192, atoi(e)));
+    if (const char *e = getenv("MPG_POOL_NV")) nv_want = std::max(32, std::min(32768, atoi(e)));
+    bool global_state = false;
+    if (const char *e = getenv("MPG_POOL_GLOBAL")) global_state = atoi(e) != 0;
     const size_t slot = Pool<KMAX, R>::slot_bytes();
     int nv = nv_want;
     auto nvq_of = [](int v) { int q = 32; while (q < v) q <<= 1; return q; };
-    while (nv > 32 && Pool<KMAX, R>::bytes(nv, nvq_of(nv)) > (size_t)smem_kb * 1024) nv -= 32;
+    if (!global_state)
+        while (nv > 32 && Pool<KMAX, R>::bytes(nv, nvq_of(nv)) > (size_t)smem_kb * 1024) nv -= 32;
     // no more slots than walks to share out over the SMs
-    const int64_t per_sm = (P.n + num_sms() - 1) / num_sms();
+    const int64_t n_blk = (int64_t)num_sms() * MPG_POOL_BPS;
+    const int64_t per_sm = (P.n + n_blk - 1) / n_blk;
     nv = (int)std::max<int64_t>(32, std::min<int64_t>(nv, (per_sm + 31) / 32 * 32));
     const int nvq = nvq_of(nv);
-    const size_t bytes = Pool<KMAX, R>::bytes(nv, nvq);
+    const size_t bytes = global_state ? (size_t)PQ_N * nvq * 2 + 64 : Pool<KMAX, R>::bytes(nv, nvq);
     static size_t set2 = 0, set4 = 0;
     size_t &set = wide ? set4 : set2;
     if (bytes > set) {
         CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
         set = bytes;
     }
-    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(num_sms(), (P.n + nv - 1) / nv));
+    unsigned char *gstate = nullptr;
+    if (global_state) {
+        static unsigned char *gbuf = nullptr;
+        static size_t gcap = 0;
+        const size_t need = (((size_t)slot * nv + 255) & ~(size_t)255) * n_blk;
+        if (need > gcap) {
+            if (gbuf) cudaFree(gbuf);
+            CUDA_TRY(cudaMalloc(&gbuf, need));
+            gcap = need;
+        }
+        gstate = gbuf;
+    }
+    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(n_blk, (P.n + nv - 1) / nv));
     {
         int div = 8;
         if (const char *v = getenv("MPG_IDLE_DIV")) div = std::max(0, atoi(v));
@@ -1274,7 +1290,9 @@ static mpg_status launch_pool(const DScene &S, const SeedCtx &g, WalkParams P, c
     int s_min = NW * 32 * 7 / 10, c_min = nv / 4;
     if (const char *e = getenv("MPG_POOL_SMIN")) s_min = atoi(e);
     if (const char *e = getenv("MPG_POOL_CMIN")) c_min = atoi(e);
-    kern<<<blocks, NW * 32, bytes, st>>>(S, g, P, nv, nvq, std::max(1, s_min), std::max(1, c_min));
+    int refill = 8;   // idle lanes of a warp that make it fetch new rays (ray phase)
+    if (const char *e = getenv("MPG_POOL_REFILL")) refill = std::max(1, std::min(32, atoi(e)));
+    kern<<<blocks, NW * 32, bytes, st>>>(S, g, P, nv, nvq, std::max(1, s_min), std::max(1, c_min), refill, gstate);
     CUDA_TRY(cudaPeekAtLastError());
     return MPG_OK;
 }

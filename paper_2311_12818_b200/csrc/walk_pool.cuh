@@ -30,13 +30,13 @@
 #pragma once
 #include "walk.cuh"
 
-enum { PQ_RAY = 0, PQ_SOLVE = 1, PQ_CTL = 2, PQ_WAIT = 3, PQ_N = 4 };
-enum { PS_TRACE = 0, PS_SOLVE = 1, PS_CTL = 2, PS_SLEEP = 3, PS_EXIT = 4 };
+enum { PQ_RAY = 0, PQ_HIT = 1, PQ_SOLVE = 2, PQ_CTL = 3, PQ_WAIT = 4, PQ_N = 5 };
+enum { PS_TRACE = 0, PS_HIT = 1, PS_SOLVE = 2, PS_CTL = 3, PS_SLEEP = 4, PS_EXIT = 5 };
 
 // MPG_POOL_PROF: diagnostic build (tools/pool_prof.py): per-role cycle and batch counters
 #ifdef MPG_POOL_PROF
-// per warp: 0 T phases, 1 S phases, 4 C phases, 2 T cycles, 7 S cycles, 10 C cycles, 11 scheduler + barrier
-// cycles, 5 solve batches, 6 solve slots, 8 control batches, 9 control slots
+// per warp: 0 R phases, 12 H phases, 1 S phases, 4 C phases, 2 R cycles, 3 H cycles, 7 S cycles, 10 C cycles,
+// 11 scheduler + barrier cycles, 5 solve batches, 6 solve slots, 8 control batches, 9 control slots
 __device__ unsigned long long g_pool_prof[16];
 #define PROF_DECL unsigned long long pf_[16] = {0}; long long pf_t = clock64();
 #define PROF_ADD(i, v) (pf_[i] += (unsigned long long)(v))
@@ -59,7 +59,8 @@ struct PoolShared {
 };
 
 // slot word `st`: it (16) | end_status (3) << 16 | occluded << 19 | seq_only << 20 | phase (4) << 24 | lid (3) << 28
-// slot word `ct`: k (4) | tau (8) << 4 | bits (8) << 12 | learned << 20 | cur << 21
+// slot word `ct`: k (4) | tau (8) << 4 | bits (8) << 12 | learned << 20 | cur << 21 | ti (3) << 22
+// (tau holds the types resolved so far while a deduction is being traced; ti = the chain ray in flight)
 #define ST_IT(s) ((int)((s)&0xffffu))
 #define ST_END(s) ((int)(((s) >> 16) & 7u))
 #define ST_OCC(s) ((((s) >> 19) & 1u) != 0u)
@@ -70,10 +71,11 @@ __device__ __forceinline__ uint32_t st_pack(int it, int end_status, bool occ, bo
     return (uint32_t)(it & 0xffff) | ((uint32_t)(end_status & 7) << 16) | ((occ ? 1u : 0u) << 19) |
            ((seq ? 1u : 0u) << 20) | ((uint32_t)(phase & 15) << 24) | ((uint32_t)(lid & 7) << 28);
 }
-__device__ __forceinline__ uint32_t ct_pack(int k, uint32_t tau, uint32_t bits, bool learned, int cur) {
+__device__ __forceinline__ uint32_t ct_pack(int k, uint32_t tau, uint32_t bits, bool learned, int cur, int ti = 0) {
     return (uint32_t)(k & 15) | ((tau & 255u) << 4) | ((bits & 255u) << 12) | ((learned ? 1u : 0u) << 20) |
-           ((uint32_t)(cur & 1) << 21);
+           ((uint32_t)(cur & 1) << 21) | ((uint32_t)(ti & 7) << 22);
 }
+#define CT_TI(c) ((int)(((c) >> 22) & 7u))
 
 template <int KMAX, typename R> struct Pool {
     int nv, nvq;
@@ -84,12 +86,15 @@ template <int KMAX, typename R> struct Pool {
     uint32_t *w, *trial, *ct, *pct, *psurf, *st, *ticket;
     int *item_e;
     float *beta, *Tprim, *Gc, *Tc, *xD;   // xD [3][nv]
+    float *ray;            // [8][nv] the ray in flight: o, d, tmax, hint (-1 none, -2 any-hit over all surfaces);
+                           // then its hit: point, -, -, -, surface, primitive (-1 analytic, -3 miss, <= -16 no ray: -16 - code)
     unsigned short *ring;  // [PQ_N][nvq] slot + 1 (0: empty)
     static __host__ __device__ size_t slot_bytes() {
-        return (size_t)KMAX * (48 + 3 * sizeof(R) + 8) + 8 + 7 * 4 + 4 + 4 * 4 + 12;
+        return (size_t)KMAX * (48 + 3 * sizeof(R) + 8) + 8 + 7 * 4 + 4 + 4 * 4 + 12 + 32;
     }
     static __host__ __device__ size_t bytes(int nv, int nvq) { return slot_bytes() * nv + (size_t)PQ_N * nvq * 2 + 64; }
-    __device__ void carve(unsigned char *base, int nv_, int nvq_) {
+    // slot arrays at `base`, queue rings at `rings` (shared memory)
+    __device__ void carve(unsigned char *base, unsigned char *rings, int nv_, int nvq_) {
         nv = nv_; nvq = nvq_;
         unsigned char *p = base;
         xb = (double *)p; p += (size_t)2 * KMAX * 3 * nv * 8;
@@ -109,7 +114,8 @@ template <int KMAX, typename R> struct Pool {
         Gc = (float *)p; p += (size_t)nv * 4;
         Tc = (float *)p; p += (size_t)nv * 4;
         xD = (float *)p; p += (size_t)3 * nv * 4;
-        ring = (unsigned short *)p;
+        ray = (float *)p; p += (size_t)8 * nv * 4;
+        ring = rings ? (unsigned short *)rings : (unsigned short *)p;
     }
     __device__ __forceinline__ double3 getx(int buf, int i, int s) const {
         const double *p = xb + (size_t)((buf * KMAX + i) * 3) * nv + s;
@@ -127,10 +133,17 @@ template <int KMAX, typename R> struct Pool {
         R *p = dq + (size_t)(i * 3) * nv + s;
         p[0] = v.x; p[nv] = v.y; p[2 * nv] = v.z;
     }
-    // the seed target of a deduction pass, in the (then unused) step storage of vertex 0
-    // (float -> R -> float is exact)
-    __device__ __forceinline__ float3 gettgt(int s) const { return tof(getdq(0, s)); }
-    __device__ __forceinline__ void settgt(int s, float3 v) { setdq(0, s, fromf<R>(v)); }
+    __device__ __forceinline__ void set_ray(int s, float3 o, float3 d, float tmax, int hint) {
+        ray[s] = o.x; ray[nv + s] = o.y; ray[2 * nv + s] = o.z;
+        ray[3 * nv + s] = d.x; ray[4 * nv + s] = d.y; ray[5 * nv + s] = d.z;
+        ray[6 * nv + s] = tmax; ray[7 * nv + s] = __int_as_float(hint);
+    }
+    // no ray could be formed (zero length, failed scatter): the pass ends with `code` in the hit phase
+    __device__ __forceinline__ void set_noray(int s, int code) { ray[7 * nv + s] = __int_as_float(-16 - code); }
+    __device__ __forceinline__ void set_hit(int s, float3 p, int surf, int prim) {
+        ray[s] = p.x; ray[nv + s] = p.y; ray[2 * nv + s] = p.z;
+        ray[6 * nv + s] = __int_as_float(surf); ray[7 * nv + s] = __int_as_float(prim);
+    }
     __device__ __forceinline__ float3 getxD(int s) const { return f3(xD[s], xD[nv + s], xD[2 * nv + s]); }
     __device__ __forceinline__ void setxD(int s, float3 v) { xD[s] = v.x; xD[nv + s] = v.y; xD[2 * nv + s] = v.z; }
     __device__ __forceinline__ int getpr(int buf, int i, int s) const { return pr[(size_t)(buf * KMAX + i) * nv + s]; }
@@ -178,174 +191,318 @@ __device__ __forceinline__ void q_push(const Pool<KMAX, R> &pl, PoolShared *sh, 
 }
 
 // ============================================================================
-// trace phase: the chain-ray loop of one pass per slot (body of walk.cuh's trace_chain,
-// one ray per round); lanes take slots from the ray queue below t_end (the entries
-// present when the phase began) until none is left
+// ray phase: nothing but BVH traversal.  A lane takes the ray of a slot from the ray queue,
+// traverses, writes the hit into the slot and hands the slot to the hit queue.  Lanes whose
+// ray ends take the next one as soon as `refill` lanes of the warp are idle (persistent
+// while-while traversal with dynamic fetch, Aila & Laine 2009), so the traversal loop runs
+// on nearly full warps although ray lengths differ widely.  Same closest / any hit as
+// trace<W> (device_common.cuh): same node order, same tests, same tie rules.
 // ============================================================================
-template <int KMAX, typename R, int W, bool GL>
-__device__ __forceinline__ void pool_trace_phase(const DScene &S, const SeedCtx &g, const WalkParams &P,
-                                                 Pool<KMAX, R> &pl, PoolShared *sh, const int lane, const unsigned t_end,
-                                                 unsigned long long &rays, LaneStats &ls) {
+template <int KMAX, typename R, int W>
+__device__ __forceinline__ void pool_ray_phase(const DScene &S, const WalkParams &P, Pool<KMAX, R> &pl, PoolShared *sh,
+                                               const int lane, const unsigned r_end, const int refill,
+                                               unsigned long long &rays, LaneStats &st) {
+    const int SENT = 0x7fffffff, NONE = 0;
+    const float eps = P.ray_eps;
     int slot = -1;
-    int mode = TR_REPROJ, k = 1, ti = -1, it = 0, cur = 0, tpp = -1, tps = 0, tcode = 0;
-    uint32_t bits = 0, tres = 0, sreq = 0, ysf = 0, stw = 0, ctw = 0, wi = 0;
-    float beta = 1.f;
-    float3 xD = f3(0.f, 0.f, 0.f);
-    double3 to = make_double3(0.0, 0.0, 0.0), tdd = make_double3(0.0, 0.0, 1.0);
+    bool active = false, fin = false, more = true;
+    bool any = false, spec_only = true;
+    float best = 0.f, bb0 = 0.f, bb1 = 0.f, bb2 = 0.f;
+    int bprim = -2, bsurf = -1;
+    float3 bp = f3(0.f, 0.f, 0.f), oi = f3(0.f, 0.f, 0.f);
+    RayW r;
+    r.o = r.d = r.idir = f3(0.f, 0.f, 1.f);
+    r.kx = 0; r.ky = 1; r.kz = 2; r.Sx = r.Sy = 0.f; r.Sz = 1.f;
+    int stack[TRAV_STACK(W)];
+    int sp = 1, node = SENT, leaf = NONE;
     while (true) {
-        // ---- refill the lanes without a slot ---------------------------------
-        const unsigned need = __ballot_sync(MPG_FULL, slot < 0);
-        if (need) {
+        // ---- finished rays: the hit goes to the slot, the slot to the hit queue --------------
+        if (fin) {
+            float3 hp = bp;
+            int hprim = bprim;
+            if (bsurf < 0) hprim = -3;
+            else if (bprim >= 0 && !any) {
+                const float3 v0 = xyz(__ldg(S.tpos + TSTRIDE * bprim)), v1 = xyz(__ldg(S.tpos + TSTRIDE * bprim + 1)),
+                             v2 = xyz(__ldg(S.tpos + TSTRIDE * bprim + 2));
+                hp = v0 * bb0 + v1 * bb1 + v2 * bb2;
+            }
+            pl.set_hit(slot, hp, bsurf, hprim);
+        }
+        q_push(pl, sh, PQ_HIT, fin, slot, lane);
+        if (fin) { fin = false; slot = -1; }
+        // ---- fetch ----------------------------------------------------------------------------
+        const unsigned idle = __ballot_sync(MPG_FULL, !active);
+        if (idle && more) {
             int got = 0;
             unsigned base = 0;
-            if (lane == 0) got = q_reserve(sh, PQ_RAY, __popc(need), base, t_end);
+            const int want = __popc(idle);
+            if (lane == 0) got = q_reserve(sh, PQ_RAY, want, base, r_end);
             got = __shfl_sync(MPG_FULL, got, 0);
             base = __shfl_sync(MPG_FULL, base, 0);
-            if (need == MPG_FULL && got == 0) break;   // nothing held, nothing left
-            const int rank = __popc(need & ((1u << lane) - 1u));
-            if (slot < 0 && rank < got) {
+            if (got < want) more = false;   // the queue is exhausted: no more early exits from the traversal
+            const int rank = __popc(idle & ((1u << lane) - 1u));
+            if (!active && rank < got) {
                 slot = q_take(pl, PQ_RAY, base + (unsigned)rank);
-                // begin the pass
-                ctw = pl.ct[slot];
-                stw = pl.st[slot];
-                k = (int)(ctw & 15u);
-                bits = (ctw >> 12) & 255u;
-                cur = (int)((ctw >> 21) & 1u);
-                const int ph = ST_PH(stw);
-                mode = ph == PH_DEDUCE ? TR_DEDUCE : (ph == PH_VIS ? TR_VIS : TR_REPROJ);
-                it = ST_IT(stw);
-                beta = pl.beta[slot];
-                xD = pl.getxD(slot);
-                wi = pl.w[slot];
-                sreq = pl.sf[cur * pl.nv + slot];
-                ti = 0; tres = 0; tcode = 0; ysf = 0; tpp = -1; tps = 0;
-                to = d3f(xD);
-                if (mode == TR_DEDUCE) {
-                    const double3 v = d3f(pl.gettgt(slot)) - to;
-                    const double l2 = ddot(v, v);
-                    if (!(l2 > 0.0)) { tcode = 3; ti = -1; }
-                    else tdd = v * rsqrt(l2);
-                }
-            }
-        }
-        // ---- this lane's ray ti (top of the trace_chain loop body) -----------
-        bool has = slot >= 0 && ti >= 0;
-        float3 of = f3(0.f, 0.f, 0.f), d = f3(0.f, 0.f, 1.f);
-        float tmax = 3.0e38f;
-        int hint = -1;
-        if (has) {
-            if (mode == TR_VIS) {
-                const float3 a = ti == 0 ? xD : f3d(pl.getx(cur, ti - 1, slot));
-                const float3 b = ti == k ? xyz(__ldg(P.seed_xL + wi)) : f3d(pl.getx(cur, min(ti, KMAX - 1), slot));
-                const float3 ab = b - a;
-                const float l = len(ab);
-                of = a;
-                d = ab * (1.0f / l);
-                tmax = l - P.ray_eps;
-            } else {
-                if (mode == TR_REPROJ) {
-                    const double3 v = (pl.getx(cur, ti, slot) + tod(pl.getdq(ti, slot)) * (double)beta) - to;
-                    const double l2 = ddot(v, v);
-                    if (!(l2 > 0.0)) { tcode = 3 | (ti << 4); has = false; }
-                    else tdd = v * rsqrt(l2);
-                    hint = pl.getpr(cur, ti, slot);
-                } else if (ti > 0) {
-                    if (!scatter_dir<GL>(S, tdd, tpp, tps, to, (tres >> (ti - 1)) & 1u, g.seed, P.walk_id_base + wi,
-                                         ti - 1)) {
-                        tcode = 4 | (ti << 4);
-                        has = false;
+                const float *ry = pl.ray + slot;
+                const int nv = pl.nv;
+                const float3 o = f3(ry[0], ry[nv], ry[2 * nv]), d = f3(ry[3 * nv], ry[4 * nv], ry[5 * nv]);
+                const float tmax = ry[6 * nv];
+                const int hint = __float_as_int(ry[7 * nv]);
+                any = hint == -2;
+                spec_only = !any;
+                rays++;
+                best = tmax;
+                bprim = -2; bsurf = -1;
+                bb0 = bb1 = bb2 = 0.f;
+                active = true;
+                // analytic surfaces (as trace<W>)
+                for (int i = 0; i < S.n_surf; i++) {
+                    const DSurf &f = S.surf[i];
+                    if (f.kind == 2 || (spec_only && f.mat == 2)) continue;
+                    float t;
+                    float3 p;
+                    bool hit;
+                    if (f.kind == 0) hit = sphere_hit(o, d, f.center, f.radius, eps, best, t, p);
+                    else {
+                        hit = quad_hit(o, d, f.origin, f.eu, f.ev, eps, best, t);
+                        p = o + d * t;
+                    }
+                    if (hit) {
+                        best = t; bprim = -1; bsurf = i; bp = p;
+                        if (any) { active = false; break; }
                     }
                 }
-                of = f3d(to);
-                d = nrmz(f3d(tdd));
+                node = SENT; leaf = NONE; sp = 1;
+                if (active && S.n_tri > 0) {
+                    ray_setup(r, o, d);
+                    if (!any && hint >= 0) {   // bound the search by the hinted triangle (see trace<W>)
+                        st.tris++;
+                        const float4 p0 = __ldg(S.tpos + TSTRIDE * hint), p1 = __ldg(S.tpos + TSTRIDE * hint + 1),
+                                     p2 = __ldg(S.tpos + TSTRIDE * hint + 2);
+                        float t, c0, c1, c2;
+                        if (!(spec_only && __float_as_int(p2.w) == 0) &&
+                            tri_hit(r, xyz(p0), xyz(p1), xyz(p2), eps, best, t, c0, c1, c2)) {
+                            best = t; bprim = hint; bsurf = __float_as_int(p1.w);
+                            bb0 = c0; bb1 = c1; bb2 = c2;
+                        }
+                    }
+                    oi = f3(o.x * r.idir.x, o.y * r.idir.y, o.z * r.idir.z);
+                    stack[0] = SENT;
+                    node = 0;
+                } else {
+                    active = false;
+                }
+                if (!active) fin = true;   // decided without the BVH
             }
-            if (!has) ti = -1;
         }
-        // ---- traverse ----------------------------------------------------------
-        if (has) {
-            const bool vis = mode == TR_VIS;
-            Hit h;
-            rays++;
-            const bool hit = trace<W>(S, of, d, P.ray_eps, tmax, !vis, vis, h, ls, vis ? -1 : hint);
-            // ---- consume the hit (bottom of the trace_chain loop body) ---------
-            if (vis) {
-                if (hit) { tcode = 5; ti = -1; }
-                else if (++ti >= k + 1) ti = -1;
+        if (!__any_sync(MPG_FULL, active)) {
+            if (__any_sync(MPG_FULL, fin)) continue;   // flush the rays decided at fetch
+            if (!more) break;
+            continue;
+        }
+        // ---- traverse (while-while with postponed leaves) until `refill` lanes are idle -----
+        while (true) {
+            if (active) {
+                while (node >= 0 && node != SENT) {
+                    st.nodes++;
+                    MPG_CHECK(node < S.n_nodes);
+                    node = bvh_visit<W>(S.nodes, node, oi, r.idir, eps, best, stack, sp);
+                    if (node < 0 && leaf == NONE) {
+                        leaf = node;
+                        node = stack[--sp];
+                    }
+                    if (!__any_sync(__activemask(), leaf == NONE)) break;
+                }
+                while (leaf != NONE) {
+                    const int v = ~leaf;
+                    const int start = v >> 3, cnt = (v & 7) + 1;
+                    MPG_CHECK(start >= 0 && start + cnt <= S.n_tri);
+                    for (int j = start; j < start + cnt; j++) {
+                        st.tris++;
+                        const float4 p0 = MPG_LDN(S.tpos + TSTRIDE * j), p1 = MPG_LDN(S.tpos + TSTRIDE * j + 1),
+                                     p2 = MPG_LDN(S.tpos + TSTRIDE * j + 2);
+                        if (spec_only && __float_as_int(p2.w) == 0) continue;
+                        float t, c0, c1, c2;
+                        if (tri_hit(r, xyz(p0), xyz(p1), xyz(p2), eps, best, t, c0, c1, c2)) {
+                            best = t; bprim = j; bsurf = __float_as_int(p1.w);
+                            bb0 = c0; bb1 = c1; bb2 = c2;
+                            if (any) { node = SENT; break; }
+                        }
+                    }
+                    leaf = NONE;
+                    if (node < 0) {
+                        leaf = node;
+                        node = stack[--sp];
+                    }
+                    if (any && bsurf >= 0) { leaf = NONE; node = SENT; }
+                }
+                if (node == SENT && leaf == NONE) { active = false; fin = true; }
+            }
+            const unsigned act = __ballot_sync(MPG_FULL, active);
+            if (act == 0u) break;
+            if (more && 32 - __popc(act) >= refill) break;
+        }
+    }
+}
+
+// ---- rays of the three pass kinds (top of walk.cuh's trace_chain loop body) ----------------------
+// reprojection ray ti of the chain in buffer cur, from `to` (x_D or the vertex just placed)
+template <int KMAX, typename R>
+__device__ __forceinline__ bool pool_build_reproj(Pool<KMAX, R> &pl, int slot, int cur, int ti, float beta, double3 to) {
+    const double3 v = (pl.getx(cur, ti, slot) + tod(pl.getdq(ti, slot)) * (double)beta) - to;
+    const double l2 = ddot(v, v);
+    if (!(l2 > 0.0)) { pl.set_noray(slot, 3 | (ti << 4)); return false; }
+    const double3 dd = v * rsqrt(l2);
+    pl.set_ray(slot, f3d(to), nrmz(f3d(dd)), 3.0e38f, pl.getpr(cur, ti, slot));
+    return true;
+}
+// visibility segment ti of the converged chain in buffer cur
+template <int KMAX, typename R>
+__device__ __forceinline__ void pool_build_vis(const WalkParams &P, Pool<KMAX, R> &pl, int slot, int cur, int k, int ti,
+                                               float3 xD, uint32_t wi) {
+    const float3 a = ti == 0 ? xD : f3d(pl.getx(cur, ti - 1, slot));
+    const float3 b = ti == k ? xyz(__ldg(P.seed_xL + wi)) : f3d(pl.getx(cur, min(ti, KMAX - 1), slot));
+    const float3 ab = b - a;
+    const float l = len(ab);
+    pl.set_ray(slot, a, ab * (1.0f / l), l - P.ray_eps, -2);
+}
+// deduction ray ti along dd (kept in the vertex's place of the chain being traced until its hit replaces it)
+template <int KMAX, typename R>
+__device__ __forceinline__ void pool_build_deduce(Pool<KMAX, R> &pl, int slot, int cur, int ti, double3 to, double3 dd) {
+    pl.setx(cur ^ 1, ti, slot, dd);
+    pl.set_ray(slot, f3d(to), nrmz(f3d(dd)), 3.0e38f, -1);
+}
+
+// ============================================================================
+// hit phase: consume the hit of every slot in the hit queue (bottom of walk.cuh's trace_chain
+// loop body), then either form the chain's next ray or end the pass (MPG_TRACE_TAIL): a
+// complete chain goes to the Newton phase, a failed reprojection halves its step and
+// re-enters the ray queue, everything else goes to the control phase
+// ============================================================================
+template <int KMAX, typename R, bool GL>
+__device__ __forceinline__ void pool_hit(const DScene &S, const SeedCtx &g, const WalkParams &P, Pool<KMAX, R> &pl,
+                                         PoolShared *sh, const int lane, int slot) {
+    bool to_ray = false, to_hit = false, to_solve = false, to_ctl = false;
+    if (slot >= 0) {
+        const uint32_t ctw = pl.ct[slot], stw = pl.st[slot];
+        const int k = (int)(ctw & 15u);
+        const uint32_t bits = (ctw >> 12) & 255u;
+        const bool learned = (ctw >> 20) & 1u;
+        int cur = (int)((ctw >> 21) & 1u);
+        int ti = CT_TI(ctw);
+        uint32_t tau = (ctw >> 4) & 255u;   // deduction: the types resolved so far
+        const int ph = ST_PH(stw);
+        const int mode = ph == PH_DEDUCE ? TR_DEDUCE : (ph == PH_VIS ? TR_VIS : TR_REPROJ);
+        int it = ST_IT(stw);
+        float beta = pl.beta[slot];
+        const float3 xD = pl.getxD(slot);
+        const uint32_t wi = pl.w[slot];
+        const int nv = pl.nv;
+        const int hprim0 = __float_as_int(pl.ray[7 * nv + slot]);
+        int tcode = 0;
+        bool pass_end = false;
+        if (hprim0 <= -16) {   // the ray could not be formed
+            tcode = -(hprim0 + 16);
+            pass_end = true;
+        } else {
+            const bool hit = hprim0 != -3;
+            const int hsurf = __float_as_int(pl.ray[6 * nv + slot]);
+            if (mode == TR_VIS) {
+                if (hit) { tcode = 5; pass_end = true; }
+                else if (++ti >= k + 1) pass_end = true;
+                else { pool_build_vis(P, pl, slot, cur, k, ti, xD, wi); to_ray = true; }
             } else if (!hit) {
                 tcode = 1 | (ti << 4);
-                ti = -1;
-            } else if (mode == TR_REPROJ && h.surf != (int)((sreq >> (4 * ti)) & 15u)) {
+                pass_end = true;
+            } else if (mode == TR_REPROJ && hsurf != (int)((pl.sf[cur * nv + slot] >> (4 * ti)) & 15u)) {
                 tcode = 2 | (ti << 4);
-                ti = -1;
+                pass_end = true;
             } else {
                 if (mode == TR_DEDUCE) {
                     uint32_t bit = (bits >> ti) & 1u;
-                    const int mat = S.surf[h.surf].mat;
-                    if (!((ctw >> 20) & 1u) && mat == 0) bit = 0u;
-                    if (bit && mat != 1) { tcode = 4 | (ti << 4); ti = -1; }
-                    else tres |= bit << ti;
+                    const int mat = S.surf[hsurf].mat;
+                    if (!learned && mat == 0) bit = 0u;
+                    if (bit && mat != 1) { tcode = 4 | (ti << 4); pass_end = true; }
+                    else tau = (ti == 0 ? 0u : tau) | (bit << ti);
                 }
-                if (ti >= 0) {
-                    int hprim = h.prim;
-                    const double3 yi = refine_hit(S, hprim, h.surf, to,
+                if (!pass_end) {
+                    const double3 to = ti == 0 ? d3f(xD) : pl.getx(cur ^ 1, ti - 1, slot);
+                    const double3 tdd = mode == TR_DEDUCE ? pl.getx(cur ^ 1, ti, slot) : make_double3(0.0, 0.0, 0.0);
+                    int hprim = hprim0;
+                    const float3 hp = f3(pl.ray[slot], pl.ray[nv + slot], pl.ray[2 * nv + slot]);
+                    const double3 yi = refine_hit(S, hprim, hsurf, to,
                                                   mode == TR_DEDUCE
                                                       ? to + tdd
                                                       : pl.getx(cur, ti, slot) + tod(pl.getdq(ti, slot)) * (double)beta,
-                                                  h.p);
+                                                  hp);
                     pl.setx(cur ^ 1, ti, slot, yi);
                     pl.setpr(cur ^ 1, ti, slot, hprim);
-                    ysf |= (uint32_t)(h.surf & 15) << (4 * ti);
-                    tpp = hprim;
-                    tps = h.surf;
-                    to = yi;
-                    if (++ti >= k) ti = -1;
-                }
-            }
-        }
-        // ---- end of a pass (walk.cuh MPG_TRACE_TAIL) -------------------------
-        bool to_solve = false, to_ctl = false, to_ray = false;
-        if (slot >= 0 && ti < 0) {
-            const bool ok = tcode == 0, ded = mode == TR_DEDUCE;
-            uint32_t tau = (ctw >> 4) & 255u;
-            int phase = PH_END, end_status = ST_END(stw);
-            bool occ = false;
-            if (mode == TR_VIS) {
-                occ = !ok;
-                to_ctl = true;
-            } else {
-                if (!ok && !ded && P.dbg && pl.trial[slot] == 0 && (int64_t)wi < P.n_dbg && 2 * it + 3 < P.dbg_stride)
-                    P.dbg[(int64_t)wi * P.dbg_stride + 2 * (it + 1)] = -(float)(tcode + 1);
-                if (ok) {
-                    cur ^= 1;
-                    pl.sf[cur * pl.nv + slot] = ysf;
-                    if (ded) { tau = tres; beta = P.beta0; it = 0; }
-                    else { beta = fminf(1.0f, 2.0f * beta); it++; }
-                    phase = PH_SOLVE;
-                    to_solve = true;
-                } else if (ded) {
-                    end_status = ST_SEED_FAIL;
-                    to_ctl = true;
-                } else {
-                    beta *= 0.5f;
-                    it++;
-                    if (it >= ((k >= 3 && P.max_iters_long > 0) ? P.max_iters_long : P.max_iters)) {
-                        end_status = ST_MAXITER;
-                        to_ctl = true;
-                    } else {   // step halving: the same chain with the shorter step, in the next trace phase
-                        phase = PH_REPROJ;
-                        to_ray = true;
+                    const uint32_t ysf = (ti == 0 ? 0u : pl.sf[(cur ^ 1) * nv + slot]) | ((uint32_t)(hsurf & 15) << (4 * ti));
+                    pl.sf[(cur ^ 1) * nv + slot] = ysf;
+                    if (++ti >= k) pass_end = true;
+                    else if (mode == TR_REPROJ) {
+                        if (pool_build_reproj(pl, slot, cur, ti, beta, yi)) to_ray = true;
+                        else { tcode = 3 | (ti << 4); pass_end = true; }
+                    } else {
+                        double3 dd = tdd;
+                        if (scatter_dir<GL>(S, dd, hprim, hsurf, yi, (tau >> (ti - 1)) & 1u, g.seed, P.walk_id_base + wi, ti - 1)) {
+                            pool_build_deduce(pl, slot, cur, ti, yi, dd);
+                            to_ray = true;
+                        } else {
+                            tcode = 4 | (ti << 4);
+                            pass_end = true;
+                        }
                     }
                 }
             }
-            pl.ct[slot] = ct_pack(k, tau, bits, (ctw >> 20) & 1u, cur);
-            pl.st[slot] = st_pack(it, end_status, occ, ST_SEQ(stw), phase, ST_LID(stw));
-            pl.beta[slot] = beta;
         }
-        q_push(pl, sh, PQ_SOLVE, to_solve, slot, lane);
-        q_push(pl, sh, PQ_CTL, to_ctl, slot, lane);
-        q_push(pl, sh, PQ_RAY, to_ray, slot, lane);
-        if (to_solve || to_ctl || to_ray) slot = -1;
+        int phase = ph, end_status = ST_END(stw);
+        bool occ = false;
+        // ---- end of a pass (walk.cuh MPG_TRACE_TAIL) -------------------------
+        while (pass_end) {
+            pass_end = false;
+            const bool ok = tcode == 0, ded = mode == TR_DEDUCE;
+            if (mode == TR_VIS) {
+                occ = !ok;
+                phase = PH_END;
+                to_ctl = true;
+                break;
+            }
+            if (!ok && !ded && P.dbg && pl.trial[slot] == 0 && (int64_t)wi < P.n_dbg && 2 * it + 3 < P.dbg_stride)
+                P.dbg[(int64_t)wi * P.dbg_stride + 2 * (it + 1)] = -(float)(tcode + 1);
+            if (ok) {
+                cur ^= 1;
+                if (ded) { beta = P.beta0; it = 0; }   // tau = the resolved types
+                else { beta = fminf(1.0f, 2.0f * beta); it++; }
+                phase = PH_SOLVE;
+                to_solve = true;
+            } else if (ded) {
+                end_status = ST_SEED_FAIL;
+                phase = PH_END;
+                to_ctl = true;
+            } else {
+                beta *= 0.5f;
+                it++;
+                if (it >= ((k >= 3 && P.max_iters_long > 0) ? P.max_iters_long : P.max_iters)) {
+                    end_status = ST_MAXITER;
+                    phase = PH_END;
+                    to_ctl = true;
+                } else {   // step halving: the same chain with the shorter step
+                    ti = 0;
+                    if (pool_build_reproj(pl, slot, cur, 0, beta, d3f(xD))) to_ray = true;
+                    else { tcode = 3; pass_end = true; }
+                }
+            }
+        }
+        if (mode != TR_DEDUCE) tau = (ctw >> 4) & 255u;
+        pl.ct[slot] = ct_pack(k, tau, bits, learned, cur, to_ray ? ti : 0);
+        pl.st[slot] = st_pack(it, end_status, occ, ST_SEQ(stw), phase, ST_LID(stw));
+        pl.beta[slot] = beta;
     }
+    q_push(pl, sh, PQ_RAY, to_ray, slot, lane);
+    q_push(pl, sh, PQ_SOLVE, to_solve, slot, lane);
+    q_push(pl, sh, PQ_CTL, to_ctl, slot, lane);
+    (void)to_hit;
 }
 
 // ============================================================================
@@ -372,7 +529,7 @@ __device__ __forceinline__ void pool_load_chain(const Pool<KMAX, R> &pl, int slo
 template <int KMAX, typename R, bool GL>
 __device__ __forceinline__ void pool_solve(const DScene &S, const SeedCtx &g, const WalkParams &P, Pool<KMAX, R> &pl,
                                            PoolShared *sh, const int lane, int slot, uint32_t &c_vtx) {
-    bool to_ray = false, to_ctl = false;
+    bool to_ray = false, to_ctl = false, to_hit = false;
     if (slot >= 0) {
         const uint32_t ctw = pl.ct[slot], stw = pl.st[slot];
         const int k = (int)(ctw & 15u), cur = (int)((ctw >> 21) & 1u);
@@ -431,9 +588,17 @@ __device__ __forceinline__ void pool_solve(const DScene &S, const SeedCtx &g, co
         }
         pl.st[slot] = st_pack(it, end_status, false, ST_SEQ(stw), phase, lid);
         to_ctl = phase == PH_END;
-        to_ray = !to_ctl;
+        // the first ray of the next pass: reprojection ray 0, or visibility segment 0
+        if (phase == PH_VIS) {
+            pool_build_vis(P, pl, slot, cur, k, 0, xD, wi);
+            to_ray = true;
+        } else if (phase == PH_REPROJ) {
+            if (pool_build_reproj(pl, slot, cur, 0, pl.beta[slot], d3f(xD))) to_ray = true;
+            else to_hit = true;   // no ray: the hit phase ends the pass (step halving)
+        }
     }
     q_push(pl, sh, PQ_RAY, to_ray, slot, lane);
+    q_push(pl, sh, PQ_HIT, to_hit, slot, lane);
     q_push(pl, sh, PQ_CTL, to_ctl, slot, lane);
 }
 
@@ -484,7 +649,7 @@ __device__ __forceinline__ bool pool_control(const DScene &S, const SeedCtx &g, 
     float3 tgt = f3(0.f, 0.f, 0.f);
     uint32_t bits = g.tau;
     bool learned = true;
-    bool to_ray = false, to_wait = false;
+    bool to_ray = false, to_wait = false, to_hit = false;
     while (true) {
         // ---- end of an attempt -------------------------------------------------
         if (phase == PH_END) {
@@ -751,9 +916,13 @@ __device__ __forceinline__ bool pool_control(const DScene &S, const SeedCtx &g, 
             pl.item_e[slot] = item_e;
             pl.beta[slot] = P.beta0;
             pl.setxD(slot, xD);
-            pl.settgt(slot, tgt);
             pl.sf[slot] = 0u;
             pl.st[slot] = st_pack(0, 0, false, seq_only, PH_DEDUCE, lid);
+            // deduction ray 0: x_D towards the seed target (Eq. 6)
+            const double3 v = d3f(tgt) - d3f(xD);
+            const double l2 = ddot(v, v);
+            if (!(l2 > 0.0)) { pl.set_noray(slot, 3); to_hit = true; }
+            else pool_build_deduce(pl, slot, 0, 0, d3f(xD), v * rsqrt(l2));
         } else {
             pl.ticket[slot] = ticket;
             pl.st[slot] = st_pack(0, 0, false, false, PH_WAIT, 0);
@@ -765,7 +934,8 @@ __device__ __forceinline__ bool pool_control(const DScene &S, const SeedCtx &g, 
         __threadfence();
         if (lane == 0) atomicAdd(&P.th->resolved, tot);
     }
-    q_push(pl, sh, PQ_RAY, to_ray, slot, lane);
+    q_push(pl, sh, PQ_RAY, to_ray && !to_hit, slot, lane);
+    q_push(pl, sh, PQ_HIT, to_ray && to_hit, slot, lane);
     q_push(pl, sh, PQ_WAIT, slot >= 0 && !to_ray, slot, lane);
     (void)pdfL;
     (void)to_wait;
@@ -778,14 +948,19 @@ __device__ __forceinline__ bool pool_control(const DScene &S, const SeedCtx &g, 
 //   S  Newton sweep of every slot with a fresh chain,
 //   C  end-of-attempt bookkeeping / trials / fetch / seeds of every slot in the control queue,
 //      and one poll of the trial-item ring for the waiting slots.
+#ifndef MPG_POOL_BPS
+#define MPG_POOL_BPS 1   // blocks per SM
+#endif
 template <int KMAX, typename R, int W, bool GL, int NW>
-__global__ void __launch_bounds__(NW * 32, 1)
+__global__ void __launch_bounds__(NW * 32, MPG_POOL_BPS)
     k_walk_pool(const DScene S, const SeedCtx g, const WalkParams P, const int nv, const int nvq, const int s_min,
-                const int c_min) {
+                const int c_min, const int refill, unsigned char *gstate) {
     extern __shared__ __align__(16) unsigned char pool_smem[];
     __shared__ PoolShared sh;
     Pool<KMAX, R> pl;
-    pl.carve(pool_smem, nv, nvq);
+    // slot state in shared memory, or (gstate) in this block's region of a global buffer (L2-resident)
+    if (gstate) pl.carve(gstate + (size_t)blockIdx.x * (((size_t)Pool<KMAX, R>::slot_bytes() * nv + 255) & ~(size_t)255), pool_smem, nv, nvq);
+    else pl.carve(pool_smem, nullptr, nv, nvq);
     const int lane = threadIdx.x & 31;
     if (threadIdx.x < PQ_N) { sh.head[threadIdx.x] = 0u; sh.tail[threadIdx.x] = 0u; }
     if (threadIdx.x == 0) { sh.done = 0u; sh.drained = 0u; }
@@ -817,20 +992,22 @@ __global__ void __launch_bounds__(NW * 32, 1)
         if (threadIdx.x == 0) {
             for (int q = 0; q < PQ_N; q++)   // undo reservation overshoots of the last phase
                 if ((int)(sh.head[q] - sh.end[q]) > 0) sh.head[q] = sh.end[q];
-            const int nR = (int)(sh.tail[PQ_RAY] - sh.head[PQ_RAY]), nS = (int)(sh.tail[PQ_SOLVE] - sh.head[PQ_SOLVE]),
-                      nC = (int)(sh.tail[PQ_CTL] - sh.head[PQ_CTL]);
+            const int nR = (int)(sh.tail[PQ_RAY] - sh.head[PQ_RAY]), nH = (int)(sh.tail[PQ_HIT] - sh.head[PQ_HIT]),
+                      nS = (int)(sh.tail[PQ_SOLVE] - sh.head[PQ_SOLVE]), nC = (int)(sh.tail[PQ_CTL] - sh.head[PQ_CTL]);
             unsigned sel;
             if (sh.done) sel = PS_EXIT;
+            else if (nH > 0) sel = PS_HIT;
             else if (nS >= s_min) sel = PS_SOLVE;
             else if (nC >= c_min) sel = PS_CTL;
             else if (nR > 0) sel = PS_TRACE;
             else if (nS > 0) sel = PS_SOLVE;
             else if (nC > 0) sel = PS_CTL;
             else sel = sh.progress ? PS_CTL : PS_SLEEP;   // only waiting slots: poll (with back-off)
-            for (int q = 0; q < PQ_N; q++) sh.end[q] = sh.tail[q];
-            if (sel != PS_CTL && sel != PS_SLEEP) { sh.end[PQ_CTL] = sh.head[PQ_CTL]; sh.end[PQ_WAIT] = sh.head[PQ_WAIT]; }
-            if (sel != PS_TRACE) sh.end[PQ_RAY] = sh.head[PQ_RAY];
-            if (sel != PS_SOLVE) sh.end[PQ_SOLVE] = sh.head[PQ_SOLVE];
+            for (int q = 0; q < PQ_N; q++) sh.end[q] = sh.head[q];
+            if (sel == PS_TRACE) sh.end[PQ_RAY] = sh.tail[PQ_RAY];
+            if (sel == PS_HIT) sh.end[PQ_HIT] = sh.tail[PQ_HIT];
+            if (sel == PS_SOLVE) sh.end[PQ_SOLVE] = sh.tail[PQ_SOLVE];
+            if (sel == PS_CTL || sel == PS_SLEEP) { sh.end[PQ_CTL] = sh.tail[PQ_CTL]; sh.end[PQ_WAIT] = sh.tail[PQ_WAIT]; }
             sh.progress = 0u;
             sh.sel = sel;
         }
@@ -839,10 +1016,25 @@ __global__ void __launch_bounds__(NW * 32, 1)
         PROF_LAP(11)
         if (sel == PS_EXIT) break;
         if (sel == PS_TRACE) {
-            // ---- T: one pass of every slot in the ray queue -------------------------------
-            pool_trace_phase<KMAX, R, W, GL>(S, g, P, pl, &sh, lane, sh.end[PQ_RAY], rays, ls);
+            // ---- R: the ray of every slot in the ray queue ----------------------------------
+            pool_ray_phase<KMAX, R, W>(S, P, pl, &sh, lane, sh.end[PQ_RAY], refill, rays, ls);
             PROF_LAP(2)
             PROF_ADD(0, 1);
+        } else if (sel == PS_HIT) {
+            // ---- H: consume the hits, form the next rays or end the passes ---------------
+            const unsigned h_end = sh.end[PQ_HIT];
+            while (true) {
+                int got = 0;
+                unsigned base = 0;
+                if (lane == 0) got = q_reserve(&sh, PQ_HIT, 32, base, h_end);
+                got = __shfl_sync(MPG_FULL, got, 0);
+                base = __shfl_sync(MPG_FULL, base, 0);
+                if (!got) break;
+                const int slot = lane < got ? q_take(pl, PQ_HIT, base + (unsigned)lane) : -1;
+                pool_hit<KMAX, R, GL>(S, g, P, pl, &sh, lane, slot);
+            }
+            PROF_LAP(3)
+            PROF_ADD(12, 1);
         } else if (sel == PS_SOLVE) {
             // ---- S: Newton sweep of the fresh chains --------------------------------------
             const unsigned s_end = sh.end[PQ_SOLVE];

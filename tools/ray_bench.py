@@ -44,6 +44,16 @@ def main():
         # random directions from receivers (mostly misses)
         "recv_random": (xD[ri], torch.randn(n, 3, device="cuda", generator=g)),
     }
+    if cfg == 2:
+        # walk-like rays of configs[2]: every receiver (in order: coherent) towards a point of the
+        # water plane within +-0.5 of straight above it
+        m = min(n, xD.shape[0])
+        tgt = xD[:m].clone()
+        tgt[:, 1] = 0.0
+        tgt[:, 0] += torch.rand(m, device="cuda", generator=g) - 0.5
+        tgt[:, 2] += torch.rand(m, device="cuda", generator=g) - 0.5
+        pad = lambda a: torch.cat([a, a[: n - m]], 0) if m < n else a
+        cases = {"recv_up_coherent": (pad(xD[:m]), pad(tgt - xD[:m])), **cases}
     t = torch.empty(n, device="cuda")
     prim = torch.empty(n, dtype=torch.int32, device="cuda")
     surf = torch.empty(n, dtype=torch.int32, device="cuda")
