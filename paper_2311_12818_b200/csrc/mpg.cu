@@ -20,7 +20,6 @@
 #include "device_common.cuh"
 #include "seed.cuh"
 #include "walk.cuh"
-#include "walk_pool.cuh"
 
 // ----------------------------------------------------------------------------
 // error plumbing
@@ -1229,88 +1228,6 @@ static size_t l2_persist_bytes() {
     return (size_t)v;
 }
 
-// ---- the warp-specialized pool kernel (walk_pool.cuh) ------------------------------------------
-// MPG_POOL=0|1 (env) selects walk.cuh's lane-per-walk kernel or the pool kernel where one is built.
-#ifndef MPG_POOL_DEFAULT
-#define MPG_POOL_DEFAULT 0
-#endif
-static bool pool_enabled() {
-    const char *e = getenv("MPG_POOL");
-    return e ? atoi(e) != 0 : MPG_POOL_DEFAULT != 0;
-}
-template <int KMAX, typename R, bool GL, int NW>
-static mpg_status launch_pool(const DScene &S, const SeedCtx &g, WalkParams P, cudaStream_t st) {
-    const bool wide = S.bvh_w == 4;
-    auto k4 = k_walk_pool<KMAX, R, 4, GL, NW>;
-    auto k2 = k_walk_pool<KMAX, R, 2, GL, NW>;
-    auto kern = wide ? k4 : k2;
-    int smem_kb = 160 / MPG_POOL_BPS, nv_want = 1024;
-    if (const char *e = getenv("MPG_POOL_SMEM_KB")) smem_kb = std::max(16, std::min(226, atoi(e)));
-    if (const char *e = getenv("MPG_POOL_NV")) nv_want = std::max(32, std::min(32768, atoi(e)));
-    bool global_state = false;
-    if (const char *e = getenv("MPG_POOL_GLOBAL")) global_state = atoi(e) != 0;
-    const size_t slot = Pool<KMAX, R>::slot_bytes();
-    int nv = nv_want;
-    auto nvq_of = [](int v) { int q = 32; while (q < v) q <<= 1; return q; };
-    if (!global_state)
-        while (nv > 32 && Pool<KMAX, R>::bytes(nv, nvq_of(nv)) > (size_t)smem_kb * 1024) nv -= 32;
-    // no more slots than walks to share out over the SMs
-    const int64_t n_blk = (int64_t)num_sms() * MPG_POOL_BPS;
-    const int64_t per_sm = (P.n + n_blk - 1) / n_blk;
-    nv = (int)std::max<int64_t>(32, std::min<int64_t>(nv, (per_sm + 31) / 32 * 32));
-    const int nvq = nvq_of(nv);
-    const size_t bytes = global_state ? (size_t)PQ_N * nvq * 2 + 64 : Pool<KMAX, R>::bytes(nv, nvq);
-    static size_t set2 = 0, set4 = 0;
-    size_t &set = wide ? set4 : set2;
-    if (bytes > set) {
-        CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-        set = bytes;
-    }
-    unsigned char *gstate = nullptr;
-    if (global_state) {
-        static unsigned char *gbuf = nullptr;
-        static size_t gcap = 0;
-        const size_t need = (((size_t)slot * nv + 255) & ~(size_t)255) * n_blk;
-        if (need > gcap) {
-            if (gbuf) cudaFree(gbuf);
-            CUDA_TRY(cudaMalloc(&gbuf, need));
-            gcap = need;
-        }
-        gstate = gbuf;
-    }
-    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(n_blk, (P.n + nv - 1) / nv));
-    {
-        int div = 8;
-        if (const char *v = getenv("MPG_IDLE_DIV")) div = std::max(0, atoi(v));
-        P.idle_backlog = div ? (uint32_t)((int64_t)blocks * nv / div) : 0x7fffffffu;
-    }
-    COUNT_LAUNCH(1);
-    // phase scheduling: a Newton phase once s_min fresh chains wait, a control phase once c_min ended
-    // attempts wait (or when nothing else is left)
-    int s_min = NW * 32 * 7 / 10, c_min = nv / 4;
-    if (const char *e = getenv("MPG_POOL_SMIN")) s_min = atoi(e);
-    if (const char *e = getenv("MPG_POOL_CMIN")) c_min = atoi(e);
-    int refill = 8;   // idle lanes of a warp that make it fetch new rays (ray phase)
-    if (const char *e = getenv("MPG_POOL_REFILL")) refill = std::max(1, std::min(32, atoi(e)));
-    kern<<<blocks, NW * 32, bytes, st>>>(S, g, P, nv, nvq, std::max(1, s_min), std::max(1, c_min), refill, gstate);
-    CUDA_TRY(cudaPeekAtLastError());
-    return MPG_OK;
-}
-// warps per block (one block per SM; registers per thread = 65536 / (32 NW), rounded down to 8)
-#ifndef MPG_POOL_NW
-#define MPG_POOL_NW 20
-#endif
-#ifdef MPG_POOL_PROF
-extern "C" int mpg_debug_pool_prof(unsigned long long *out16) {
-    cudaDeviceSynchronize();
-    cudaMemcpyFromSymbol(out16, g_pool_prof, 16 * sizeof(unsigned long long));
-    unsigned long long z[16] = {0};
-    cudaMemcpyToSymbol(g_pool_prof, z, sizeof(z));
-    return 0;
-}
-#endif
-template <int KMAX> struct PoolBuilt { static constexpr bool value = KMAX <= 2; };
-
 template <int KMAX, typename R, int MINB = (KMAX <= 2 ? MPG_WALK_MINB2 : MPG_WALK_MINB_LONG), bool GL = false,
           bool CMP = false>
 static mpg_status launch_walk(const DScene &S, const SeedCtx &g, WalkParams P, cudaStream_t st, void *ws,
@@ -1377,10 +1294,6 @@ static mpg_status launch_walk(const DScene &S, const SeedCtx &g, WalkParams P, c
         COUNT_LAUNCH(4);   // cub onesweep: histogram + 3 passes of 10 bits (library launches, counted)
         CUDA_TRY(cub::DeviceRadixSort::SortPairs(b + L.stemp, tb, k0, k1, v0, v1, (int)P.n, 0, kbits, st));
         P.perm = v1;
-    }
-    if constexpr (PoolBuilt<KMAX>::value && !CMP) {
-        if (pool_enabled())
-            return launch_pool<KMAX, R, GL, MPG_POOL_NW>(S, g, P, st);
     }
     int64_t want = (P.n + 127) / 128;
     int blocks = (int)std::min<int64_t>(want, (int64_t)num_sms() * occ);
@@ -1513,15 +1426,6 @@ static mpg_status walk_dispatch(const mpg_scene *scene, const SeedCtx &g, const 
                                 cudaStream_t s) {
     const int k = g.k;
     const bool sort = (o->flags & MPG_FLAG_SORT) != 0, f64 = (o->flags & MPG_FLAG_NEWTON_F64) != 0;
-#ifdef MPG_DEV_FAST   // development builds: only the short-chain kernels (fast compile)
-    if (scene->glossy || k > 2) return fail(MPG_ERR_UNSUPPORTED, "MPG_DEV_FAST build: k <= 2, no glossy");
-    if (f64) {
-        if (k <= 1) return launch_walk<1, double>(scene->d, g, P, s, workspace, sort);
-        return launch_walk<2, double>(scene->d, g, P, s, workspace, sort);
-    }
-    if (k <= 1) return launch_walk<1, float>(scene->d, g, P, s, workspace, sort);
-    return launch_walk<2, float>(scene->d, g, P, s, workspace, sort);
-#else
     if (scene->glossy) {   // glossy chains (R37): kernels with the offset-normal code, k <= 6
         if (k > 6) return fail(MPG_ERR_UNSUPPORTED, "glossy chains support k <= 6");
         if (f64) {
@@ -1557,7 +1461,6 @@ static mpg_status walk_dispatch(const mpg_scene *scene, const SeedCtx &g, const 
     if (k <= 4) return launch_walk<4, float>(scene->d, g, P, s, workspace, sort);
     if (k <= 6) return launch_walk<6, float>(scene->d, g, P, s, workspace, sort);
     return launch_walk<8, float>(scene->d, g, P, s, workspace, sort);
-#endif
 }
 
 // ----------------------------------------------------------------------------

@@ -17,18 +17,9 @@ def region(f, ln):
     if f == "walk.cuh":
         if ln < 162: return "wk:scatter_dir"
         if ln < 236: return "wk:refine_hit"
+        if ln < 330: return "wk:trace_chain"
         if ln < 400: return "wk:trial helpers"
         return "wk:kernel"
-    if f == "walk_pool.cuh":
-        src = open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "paper_2311_12818_b200", "csrc", "walk_pool.cuh")).read().split("\n")
-        marks = [(i + 1, l) for i, l in enumerate(src) if l.startswith("__device__") or l.startswith("__global__") or l.startswith("template")]
-        name = "pool:?"
-        for i, l in marks:
-            if i <= ln + 1:
-                nxt = src[i] if l.startswith("template") and i < len(src) else l
-                m = __import__("re").search(r"(\w+)\(", nxt if "(" in nxt else l)
-                if m: name = "pool:" + m.group(1)
-        return name
     if f == "seed.cuh": return "seed"
     return "intrinsics/" + f.split(".")[0][:12]
 
