@@ -400,7 +400,10 @@ __device__ __forceinline__ bool quad_hit(float3 o, float3 d, float3 q0, float3 e
 #ifdef MPG_NH
 __device__ unsigned long long g_nh[256];   // diagnostic: closest-hit rays by node visits
 #endif
-template <int W>
+// WANT_P = false: for a triangle hit h.p holds the hit's barycentrics instead of the fp32 point
+// (the walk recomputes the point in fp64 from the vertices anyway, refine_hit: three 16-byte
+// loads per ray less on the L1 data pipe, the unit that bounds the traversal)
+template <int W, bool WANT_P = true>
 __device__ __forceinline__ bool trace(const DScene &S, float3 o, float3 d, float tmin, float tmax, bool spec_only,
                                       const bool ANY, Hit &h, LaneStats &st, int hint = -1) {   // callers count rays
 #ifdef MPG_NH
@@ -496,10 +499,14 @@ __device__ __forceinline__ bool trace(const DScene &S, float3 o, float3 d, float
     h.t = best; h.prim = bprim; h.surf = bsurf;
     if (bsurf < 0) return false;
     if (bprim >= 0) {
-        // hit point from barycentrics: lies on the triangle plane up to rounding
-        float3 v0 = xyz(__ldg(S.tpos + TSTRIDE * bprim)), v1 = xyz(__ldg(S.tpos + TSTRIDE * bprim + 1)),
-               v2 = xyz(__ldg(S.tpos + TSTRIDE * bprim + 2));
-        h.p = v0 * bb0 + v1 * bb1 + v2 * bb2;
+        if constexpr (WANT_P) {
+            // hit point from barycentrics: lies on the triangle plane up to rounding
+            float3 v0 = xyz(__ldg(S.tpos + TSTRIDE * bprim)), v1 = xyz(__ldg(S.tpos + TSTRIDE * bprim + 1)),
+                   v2 = xyz(__ldg(S.tpos + TSTRIDE * bprim + 2));
+            h.p = v0 * bb0 + v1 * bb1 + v2 * bb2;
+        } else {
+            h.p = f3(bb0, bb1, bb2);
+        }
     } else {
         h.p = bp;
     }

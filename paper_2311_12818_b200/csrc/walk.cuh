@@ -41,6 +41,11 @@
 #ifndef MPG_COMPACT
 #define MPG_COMPACT 1
 #endif
+// MPG_TRACE_P = 1: the traversal also forms the fp32 hit point of a triangle hit (A/B knob; 0: three
+// loads per chain ray less, the walk refines the hit in fp64 from the vertices anyway)
+#ifndef MPG_TRACE_P
+#define MPG_TRACE_P 0
+#endif
 #include "device_common.cuh"
 #include "seed.cuh"
 #include "newton.cuh"
@@ -174,7 +179,10 @@ __device__ __forceinline__ bool scatter_dir(const DScene &S, double3 &dd, int pr
 // refined point are checked, and while one is negative the point moves to the
 // triangle across that edge (mesh adjacency, <= 2 hops): the primitive is then
 // the one the exact line crosses, as in the fp64 oracle.  `prim` is updated.
-__device__ __forceinline__ double3 refine_hit(const DScene &S, int &prim, int surf, double3 o, double3 q, float3 pf) {
+// pf: the traversal's fp32 hit point, or (pf_bary, triangles only) its barycentrics: the fp32 point
+// is only the fallback of a line parallel to the triangle's plane
+__device__ __forceinline__ double3 refine_hit(const DScene &S, int &prim, int surf, double3 o, double3 q, float3 pf,
+                                              const bool pf_bary = false) {
     double ox = o.x, oy = o.y, oz = o.z;
     double dx = q.x - ox, dy = q.y - oy, dz = q.z - oz;
     double t;
@@ -189,7 +197,10 @@ __device__ __forceinline__ double3 refine_hit(const DScene &S, int &prim, int su
             double e2x = (double)c.x - a.x, e2y = (double)c.y - a.y, e2z = (double)c.z - a.z;
             double nx = e1y * e2z - e1z * e2y, ny = e1z * e2x - e1x * e2z, nz = e1x * e2y - e1y * e2x;
             double den = dx * nx + dy * ny + dz * nz;
-            if (den == 0.0) break;
+            if (den == 0.0) {
+                if (hop == 0 && pf_bary) y0 = d3f(a * pf.x + b * pf.y + c * pf.z);
+                break;
+            }
             t = (((double)a.x - ox) * nx + ((double)a.y - oy) * ny + ((double)a.z - oz) * nz) / den;
             const double3 y = make_double3(ox + t * dx, oy + t * dy, oz + t * dz);
             if (hop == 0) y0 = y;
@@ -299,7 +310,7 @@ __device__ __forceinline__ int trace_chain(const DScene &S, int mode, int k, uin
         // k_walk -17 % configs[1], -7 % [2], -13 % [3] against a register counter)
         atomicAdd(s_rays, 1u);
         Hit h;
-        const bool hit = trace<W>(S, of, d, eps, tmax, !vis, vis, h, st, mode == TR_REPROJ ? rget(hint, i) : -1);
+        const bool hit = trace<W, MPG_TRACE_P != 0>(S, of, d, eps, tmax, !vis, vis, h, st, mode == TR_REPROJ ? rget(hint, i) : -1);
         if (vis) {
             if (hit) return 5;
             continue;
@@ -314,7 +325,7 @@ __device__ __forceinline__ int trace_chain(const DScene &S, int mode, int k, uin
             res |= bit << i;
         }
         const double3 yi = refine_hit(S, h.prim, h.surf, o, deduce ? o + dd : rget(x, i) + tod(rget(dq, i)) * (double)beta,
-                                      h.p);   // may move h.prim across a shared edge
+                                      h.p, MPG_TRACE_P == 0);   // may move h.prim across a shared edge
         rset(y, i, yi);
         rset(yp, i, h.prim);
         rset(ys, i, h.surf);
