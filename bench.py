@@ -360,10 +360,18 @@ def run_ours(args):
     achieved = flops / walk_s / 1e12
     peak = measured_peak if measured_peak else fp32_peak_tflops()
     traffic = None
+    ncu_units = None     # what the committed ncu capture of this config's k_walk says limits it
     prof = os.path.join(ROOT, "profiles", f"ncu_walk_cfg{args.config}.json")
     if os.path.exists(prof):
         try:
-            traffic = json.load(open(prof)).get("dram_bytes_per_launch")
+            pj = json.load(open(prof))
+            traffic = pj.get("dram_bytes_per_launch")
+            ncu_units = {"source": f"profiles/ncu_walk_cfg{args.config}.json (ncu --set full, one k_walk launch)",
+                         "l1_data_pipe_lsu_wavefronts_pct_of_peak": pj.get("l1_data_pipe_lsu_wavefronts_pct_of_peak"),
+                         "issue_active_pct": pj.get("issue_active_pct"),
+                         "active_threads_per_warp_instruction": pj.get("simt_threads_per_inst"),
+                         "dram_throughput_pct": pj.get("dram_throughput_pct"),
+                         "top_stalls_pct": pj.get("top_stalls_pct")}
         except Exception:
             traffic = None
 
@@ -456,7 +464,8 @@ def run_ours(args):
                                              if measured_peak else
                                              "148 SM x 128 FP32 lanes x 2 x 1965 MHz (B200_PROFILING.md unit counts)"),
                              "nominal_peak": fp32_peak_tflops(),
-                             "algorithmic_flops_per_launch": flops / args.steps},
+                             "algorithmic_flops_per_launch": flops / args.steps,
+                             "ncu_units": ncu_units},
                 "hbm": hbm,
                 "stats_per_step": {k: v / args.steps for k, v in S.items()},
                 "gpu_launches": launches,

@@ -48,6 +48,11 @@ def summarize(d):
         "dram_bytes_per_launch": g("dram__bytes_read.sum", 0.0) + g("dram__bytes_write.sum", 0.0),
         "dram_gbs": (g("dram__bytes_read.sum", 0.0) + g("dram__bytes_write.sum", 0.0)) / dur if dur else None,
         "l1_hit_pct": g("l1tex__t_sector_hit_rate.pct"), "l2_hit_pct": g("lts__t_sector_hit_rate.pct"),
+        # the most utilized unit of this kernel: the L1 data pipe (LSU wavefronts of divergent 16-byte loads)
+        "l1_data_pipe_lsu_wavefronts_pct_of_peak": g("l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed"),
+        "compute_memory_throughput_pct": g("gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed"),
+        "dram_throughput_pct": g("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"),
+        "sm_throughput_pct": g("sm__throughput.avg.pct_of_peak_sustained_elapsed"),
         "warp_instructions": g("smsp__inst_executed.sum"),
         "top_stalls_pct": {k: round(100 * v / tot, 1) for k, v in top},
     }
