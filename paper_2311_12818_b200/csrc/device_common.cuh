@@ -199,6 +199,13 @@ template <typename T, int N, int M> __device__ __forceinline__ void rset2(T (&a)
 #define MPG_LDN __ldg
 #endif
 #define TRAV_STACK(W) ((W) == 4 ? 96 : 64)
+// MPG_TOP_NODES = N > 0: the walk kernel stages the first N nodes of the tree (the scene build numbers
+// the top levels breadth-first, so these are the root's first levels) in shared memory and the
+// traversal reads them there (north_star: "node stream staged through shared memory"; A/B in
+// measured, not faster -- 0 = off)
+#ifndef MPG_TOP_NODES
+#define MPG_TOP_NODES 0
+#endif
 
 // One node visit of the ordered traversal: returns the nearest child whose box
 // overlaps [tmin, tmax] (or pops the stack if none) and pushes the others
@@ -209,12 +216,20 @@ template <int W>
 // by ~ulp(|o|); node boxes are inflated by extent * 2^-20 at build time, so the
 // test stays conservative (a box the ray truly enters is never culled).
 __device__ __forceinline__ int bvh_visit(const float4 *nodes, int node, float3 oi, float3 idir, float tmin,
-                                         float tmax, int *stack, int &sp) {
+                                         float tmax, int *stack, int &sp, const float4 *top = nullptr) {
   if (W == 4) {
     const float4 *nd = nodes + NODE_F4(4) * node;
-    const float4 lx = MPG_LDN(nd), hx = MPG_LDN(nd + 1), ly = MPG_LDN(nd + 2), hy = MPG_LDN(nd + 3), lz = MPG_LDN(nd + 4),
-                 hz = MPG_LDN(nd + 5);
-    const int4 ch = MPG_LDN(reinterpret_cast<const int4 *>(nd + 6));
+    float4 lx, hx, ly, hy, lz, hz;
+    int4 ch;
+    if (MPG_TOP_NODES > 0 && top && node < MPG_TOP_NODES) {   // the first levels, staged in shared memory
+        const float4 *tn = top + NODE_F4(4) * node;
+        lx = tn[0]; hx = tn[1]; ly = tn[2]; hy = tn[3]; lz = tn[4]; hz = tn[5];
+        ch = *reinterpret_cast<const int4 *>(tn + 6);
+    } else {
+        lx = MPG_LDN(nd); hx = MPG_LDN(nd + 1); ly = MPG_LDN(nd + 2); hy = MPG_LDN(nd + 3); lz = MPG_LDN(nd + 4);
+        hz = MPG_LDN(nd + 5);
+        ch = MPG_LDN(reinterpret_cast<const int4 *>(nd + 6));
+    }
     const float INF = __int_as_float(0x7f800000);
     float t[4];
     int c[4] = {ch.x, ch.y, ch.z, ch.w};
@@ -249,8 +264,16 @@ __device__ __forceinline__ int bvh_visit(const float4 *nodes, int node, float3 o
     return c[0];
   } else {
     const float4 *nd = nodes + NODE_F4(2) * node;
-    float4 a = MPG_LDN(nd), b = MPG_LDN(nd + 1), c = MPG_LDN(nd + 2);
-    int4 ch = MPG_LDN(reinterpret_cast<const int4 *>(nd + 3));
+    float4 a, b, c;
+    int4 ch;
+    if (MPG_TOP_NODES > 0 && top && node < MPG_TOP_NODES) {
+        const float4 *tn = top + NODE_F4(2) * node;
+        a = tn[0]; b = tn[1]; c = tn[2];
+        ch = *reinterpret_cast<const int4 *>(tn + 3);
+    } else {
+        a = MPG_LDN(nd); b = MPG_LDN(nd + 1); c = MPG_LDN(nd + 2);
+        ch = MPG_LDN(reinterpret_cast<const int4 *>(nd + 3));
+    }
     float tx0 = fmaf(a.x, idir.x, -oi.x), tx1 = fmaf(a.w, idir.x, -oi.x);
     float ty0 = fmaf(a.y, idir.y, -oi.y), ty1 = fmaf(b.x, idir.y, -oi.y);
     float tz0 = fmaf(a.z, idir.z, -oi.z), tz1 = fmaf(b.y, idir.z, -oi.z);
@@ -405,7 +428,8 @@ __device__ unsigned long long g_nh[256];   // diagnostic: closest-hit rays by no
 // loads per ray less on the L1 data pipe, the unit that bounds the traversal)
 template <int W, bool WANT_P = true>
 __device__ __forceinline__ bool trace(const DScene &S, float3 o, float3 d, float tmin, float tmax, bool spec_only,
-                                      const bool ANY, Hit &h, LaneStats &st, int hint = -1) {   // callers count rays
+                                      const bool ANY, Hit &h, LaneStats &st, int hint = -1,
+                                      const float4 *top = nullptr) {   // callers count rays
 #ifdef MPG_NH
     const uint32_t n_at_entry = st.nodes;
 #endif
@@ -461,7 +485,7 @@ __device__ __forceinline__ bool trace(const DScene &S, float3 o, float3 d, float
             while (node >= 0 && node != SENT) {
                 st.nodes++;
                 MPG_CHECK(node < S.n_nodes);
-                node = bvh_visit<W>(S.nodes, node, oi, r.idir, tmin, best, stack, sp);
+                node = bvh_visit<W>(S.nodes, node, oi, r.idir, tmin, best, stack, sp, top);
                 if (node < 0 && leaf == NONE) { // postpone the leaf, keep traversing
                     leaf = node;
                     node = stack[--sp];

@@ -439,6 +439,34 @@ extern "C" mpg_status mpg_scene_create(const mpg_surface_desc *surfaces, int32_t
             memcpy(&nodes4[4 * i + 3], &ch, sizeof(int4));
         }
         }
+        {   // number the first levels breadth-first (root = 0, then its children, ...): the walk kernel can
+            // stage nodes [0, MPG_TOP_NODES) in shared memory; the other nodes keep their relative order
+            const int F4 = NODE_F4(width), NCH = width == 4 ? 4 : 2;
+            auto child = [&](int n, int j) -> int & {
+                return *reinterpret_cast<int *>(width == 4 ? &(&nodes4[(size_t)F4 * n + 6].x)[j] : &(&nodes4[(size_t)F4 * n + 3].x)[j]);
+            };
+            const int NB = std::min(d.n_nodes, 256);
+            std::vector<int> order, newid(d.n_nodes, -1);
+            order.push_back(0);
+            for (size_t q = 0; q < order.size() && (int)order.size() < NB; q++)
+                for (int j = 0; j < NCH && (int)order.size() < NB; j++) {
+                    const int c = child(order[q], j);
+                    if (c >= 0 && c != 0x7fffffff) order.push_back(c);
+                }
+            for (size_t q = 0; q < order.size(); q++) newid[order[q]] = (int)q;
+            int nxt = (int)order.size();
+            for (int n = 0; n < d.n_nodes; n++)
+                if (newid[n] < 0) newid[n] = nxt++;
+            std::vector<float4> re(nodes4.size());
+            for (int n = 0; n < d.n_nodes; n++) {
+                for (int j = 0; j < NCH; j++) {
+                    int &c = child(n, j);
+                    if (c >= 0 && c != 0x7fffffff) c = newid[c];
+                }
+                for (int f = 0; f < F4; f++) re[(size_t)F4 * newid[n] + f] = nodes4[(size_t)F4 * n + f];
+            }
+            nodes4.swap(re);
+        }
         tpos.assign((size_t)TSTRIDE * d.n_tri, make_float4(0.f, 0.f, 0.f, 0.f));
         tnrm.resize(3 * d.n_tri);
         for (int j = 0; j < d.n_tri; j++) {

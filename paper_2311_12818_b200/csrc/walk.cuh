@@ -267,7 +267,7 @@ __device__ __forceinline__ int trace_chain(const DScene &S, int mode, int k, uin
                                            const double3 (&x)[KMAX], const int (&hint)[KMAX],
                                            uint32_t surf_req, float eps, double3 (&y)[KMAX], int (&yp)[KMAX],
                                            int (&ys)[KMAX], LaneStats &st, uint32_t &tau_res, unsigned *s_rays,
-                                           uint64_t seed, uint64_t wid) {
+                                           uint64_t seed, uint64_t wid, const float4 *top = nullptr) {
     const bool deduce = mode == TR_DEDUCE, vis = mode == TR_VIS;
     uint32_t res = 0;
     double3 o = d3f(xD);
@@ -310,7 +310,8 @@ __device__ __forceinline__ int trace_chain(const DScene &S, int mode, int k, uin
         // k_walk -17 % configs[1], -7 % [2], -13 % [3] against a register counter)
         atomicAdd(s_rays, 1u);
         Hit h;
-        const bool hit = trace<W, MPG_TRACE_P != 0>(S, of, d, eps, tmax, !vis, vis, h, st, mode == TR_REPROJ ? rget(hint, i) : -1);
+        const bool hit = trace<W, MPG_TRACE_P != 0>(S, of, d, eps, tmax, !vis, vis, h, st, mode == TR_REPROJ ? rget(hint, i) : -1,
+                                                    top);
         if (vis) {
             if (hit) return 5;
             continue;
@@ -453,6 +454,14 @@ __global__ void __launch_bounds__(128, MINB) k_walk(const DScene S, const SeedCt
     __shared__ unsigned s_rays[128];   // chain rays per thread (see trace_chain)
     for (int i = threadIdx.x; i < SS_N; i += blockDim.x) s_stats[i] = 0u;
     s_rays[threadIdx.x] = 0u;
+    // the first levels of the BVH (breadth-first at the front of the node array) in shared memory
+    constexpr int NTOPF4 = MPG_TOP_NODES > 0 ? MPG_TOP_NODES * NODE_F4(W) : 1;
+    __shared__ float4 s_top[NTOPF4];
+    const float4 *top = nullptr;
+    if (MPG_TOP_NODES > 0 && S.n_nodes >= MPG_TOP_NODES) {
+        for (int i = threadIdx.x; i < NTOPF4; i += blockDim.x) s_top[i] = __ldg(S.nodes + i);
+        top = s_top;
+    }
     __syncthreads();
 
     const int lane = threadIdx.x & 31;
@@ -680,7 +689,7 @@ __global__ void __launch_bounds__(128, MINB) k_walk(const DScene S, const SeedCt
             const int mode = ded ? TR_DEDUCE : (phase == PH_VIS ? TR_VIS : TR_REPROJ);
             int why = trace_chain<KMAX, W, R, GL>(S, mode, k, bits, learned, xD, xL, tgt, dq, beta, x, prim, sreq,
                                                   P.ray_eps, y, yp, ys, ls, tres, &s_rays[threadIdx.x], g.seed,
-                                                  P.walk_id_base + w);
+                                                  P.walk_id_base + w, top);
             bool ok = why == 0;
             MPG_TRACE_TAIL
         }
@@ -767,7 +776,7 @@ __global__ void __launch_bounds__(128, MINB) k_walk(const DScene S, const SeedCt
                 Hit h;
                 ls.rays++;
                 const bool hit = trace<W>(S, xyz(ro), xyz(rd), P.ray_eps, ro.w, !vis, vis, h, ls,
-                                          vis ? -1 : s_rh[threadIdx.x]);
+                                          vis ? -1 : s_rh[threadIdx.x], top);
                 s_hp[threadIdx.x] = make_float4(h.p.x, h.p.y, h.p.z, 0.f);
                 s_hs[threadIdx.x] = make_int2(hit ? h.prim : -3, h.surf);
             }

@@ -46,6 +46,31 @@ def main():
         for i in stall_cols:
             v = int(r[i] or 0)
             if v: c[h[i]] += v
+    if len(sys.argv) > 4:   # per source line of the named files (innermost inlined line): top 60 by stall samples
+        files = sys.argv[4].split(",")
+        lines = collections.defaultdict(lambda: collections.Counter())
+        base2 = None
+        tot = 0
+        for r in rows[hi + 1:]:
+            if len(r) < len(h): continue
+            a = int(r[0], 16)
+            if base2 is None: base2 = a
+            smp = int(r[ci["Warp Stall Sampling (All Samples)"]] or 0)
+            tot += smp
+            src = amap.get(a - base2)
+            if not src or src[0] not in files: continue
+            c = lines[src]
+            c["samples"] += smp
+            c["inst"] += int(r[ci["Instructions Executed"]] or 0)
+            c["thr"] += int(r[ci["Thread Instructions Executed"]] or 0)
+            for i in stall_cols:
+                v = int(r[i] or 0)
+                if v and "Not Issued" not in h[i]: c[h[i]] += v
+        for src, c in sorted(lines.items(), key=lambda x: -x[1]["samples"])[:60]:
+            st = sorted(((k, v) for k, v in c.items() if k.startswith("stall_")), key=lambda x: -x[1])[:3]
+            print(f"{src[0]}:{src[1]:<5d} samples {100 * c['samples'] / tot:5.2f}%  inst {c['inst']:>12,d} thr/inst {c['thr'] / max(c['inst'], 1):5.1f}  "
+                  + " ".join(f"{k[6:]}:{100 * v / max(c['samples'], 1):.0f}%" for k, v in st))
+        return
     ti = sum(c["inst"] for c in agg.values()); ts = sum(c["samples"] for c in agg.values())
     print(f"total warp instructions {ti:,}, stall samples {ts:,}")
     for reg, c in sorted(agg.items(), key=lambda x: -x[1]["samples"]):
