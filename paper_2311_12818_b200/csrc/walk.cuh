@@ -522,7 +522,7 @@ __global__ void __launch_bounds__(128, MINB) k_walk(const DScene S, const SeedCt
                 if (idx < P.n) {
                     w = P.perm ? (int64_t)__ldg(P.perm + idx) : idx;
                     trial = 0;
-                    int64_t rcv = w / P.spp;
+                    const uint32_t rcv = (uint32_t)w / (uint32_t)P.spp;   // n < 2^31 (mpg_manifold_walk): no 64-bit division
                     xD = xyz(__ldg(P.xD + rcv));
                     float4 l4 = __ldg(P.seed_xL + w);
                     xL = xyz(l4);
@@ -588,7 +588,7 @@ __global__ void __launch_bounds__(128, MINB) k_walk(const DScene S, const SeedCt
                 uint32_t pct = __ldcg(P.e_pct + item_e);
                 pk = (int)(pct & 15u);
                 ptau = pct >> 4;
-                int64_t rcv = w / P.spp;
+                const uint32_t rcv = (uint32_t)w / (uint32_t)P.spp;
                 xD = xyz(__ldg(P.xD + rcv));
                 float4 l4 = __ldg(P.seed_xL + w);
                 xL = xyz(l4);
@@ -858,7 +858,7 @@ __global__ void __launch_bounds__(128, MINB) k_walk(const DScene S, const SeedCt
                                                  DL)) {
                             end_status = ST_BAD_SIDE;
                         } else {
-                            const float3 nD = xyz(__ldg(P.nD + w / P.spp));
+                            const float3 nD = xyz(__ldg(P.nD + (uint32_t)w / (uint32_t)P.spp));
                             Gc = singular ? 0.0f : ggt_from_blocks<KMAX, R>(k, xD, nD, x, Di, Ub, sg, tg, DL);
                             float Le = L.emit;
                             if (L.kind == 1 && !(dot(f3d(x[k - 1]) - xL, L.n) > 0.0f)) Le = 0.0f;
