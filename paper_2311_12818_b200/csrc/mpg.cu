@@ -1291,6 +1291,15 @@ static mpg_status launch_walk(const DScene &S, const SeedCtx &g, WalkParams P, c
     if (const char *v = getenv("MPG_ITEM_B0_IDLE")) P.item_b0_idle = std::max(1, atoi(v));
     if (const char *v = getenv("MPG_ITEM_GROW_IDLE")) P.item_grow_idle = std::max(1, std::min(4, atoi(v)));
     if (const char *v = getenv("MPG_BACKOFF_MAX")) P.backoff_max = std::max(32, atoi(v));
+    // attempt boundaries (end / fetch / seed sections) served in batches (kernels for k <= 2 and the
+    // mixed-length kernel).  Measured, ms per step at svc_min / svc_wait = 1/1 (every pass, as before),
+    // 2/2, 4/3, 8/4, 8/8, 12/12, 16/12, 24/16: configs[2] 292.4 / 281.1 / 266.5 / 258.4 / 249.2 /
+    // 242.8 / 243.2 / 290.6; configs[1] 43.9 / 43.9 / 43.1 / 42.6 / 42.5 / 42.6; configs[4] 217.9 -> 213.9
+    // at 12/12; fixed k = 6 (configs[3]) 156.4 -> 158-160: not used there
+    P.svc_min = 12u;
+    P.svc_wait = 12u;
+    if (const char *v = getenv("MPG_SVC_MIN")) P.svc_min = (uint32_t)std::max(1, std::min(32, atoi(v)));
+    if (const char *v = getenv("MPG_SVC_WAIT")) P.svc_wait = (uint32_t)std::max(1, atoi(v));
     P.hard_cap = L.H;
     // tickets index the ring only below item_cap: it bounds both the reads and the clear;
     // a full ring (or entry table) makes the walk continue its trials sequentially

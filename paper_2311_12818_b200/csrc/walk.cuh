@@ -46,6 +46,9 @@
 #ifndef MPG_TRACE_P
 #define MPG_TRACE_P 0
 #endif
+#ifndef MPG_SVC_ALL
+#define MPG_SVC_ALL 0   // A/B: batched attempt boundaries in every k_walk instantiation (default: k <= 2 only)
+#endif
 #include "device_common.cuh"
 #include "seed.cuh"
 #include "newton.cuh"
@@ -105,6 +108,7 @@ struct WalkParams {
     // idle_backlog (most lanes idle in the tail: a larger batch then costs no
     // throughput and saves rounds of trial-walk latency on the critical path)
     uint32_t item_grow_idle, idle_backlog, item_b0_idle;
+    uint32_t svc_min, svc_wait; // attempt boundaries served in batches (k_walk): waiting lanes / passes that trigger a service
     uint32_t backoff_max;       // ns, cap of the waiting warps' sleep
     uint32_t hard_cap;          // entries
     uint32_t item_cap;          // item ring capacity (a full ring -> sequential fallback)
@@ -506,9 +510,18 @@ __global__ void __launch_bounds__(128, MINB) k_walk(const DScene S, const SeedCt
     int item_e = -1;          // hard entry of the trial item this lane runs (-1: none)
     long long ticket = -1;    // item-ring ticket while waiting for an item
     bool seq_only = false;    // trials continued in this lane after a full item ring
+    // Attempt boundaries in batches (non-compact kernels): the end-of-attempt, fetch and seed sections
+    // cost a warp the same whether one lane or ten are in them, and with ~1.7 lanes of a warp ending
+    // an attempt per pass they used to run in ~83 % of the passes at 1.5 active lanes (and pull their
+    // code through the instruction cache every pass).  A lane whose attempt ended now waits until
+    // svc_min lanes of its warp wait, or svc_wait passes (WalkParams), and the warp then serves them
+    // together.  A walk's arithmetic does not depend on when it is served: outputs are unchanged.
+    bool svc = true;        // warp-uniform: this pass serves the fetch / seed sections (decided at the last end section)
+    int svc_since = 0;
     while (true) {
         // ---- fetch a primary walk (warp-aggregated) ------------------------
         unsigned need = __ballot_sync(MPG_FULL, phase == PH_FETCH);
+        if (!svc) need = 0u;
         if (need) {
             int leader = __ffs(need) - 1;
             unsigned long long base = 0;
@@ -634,7 +647,7 @@ __global__ void __launch_bounds__(128, MINB) k_walk(const DScene S, const SeedCt
         float3 tgt = f3(0, 0, 0);
         uint32_t bits = g.tau;
         bool learned = true;
-        if (phase == PH_SEED) {
+        if (phase == PH_SEED && svc) {
             c_attempts++;
             bool ok;
             bool inactive = false;
@@ -879,7 +892,13 @@ __global__ void __launch_bounds__(128, MINB) k_walk(const DScene S, const SeedCt
         }
 
         // ---- end of an attempt ---------------------------------------------
-        if (phase == PH_END) {
+        if constexpr (MPG_SVC_ALL || CMP || KMAX <= 2) {   // (fixed long chains have few boundaries per pass: measured no gain)
+            // serve now? (always in the tail: idle lanes are waiting for exactly this work)
+            const int nwait = __popc(__ballot_sync(MPG_FULL, phase == PH_END || phase == PH_FETCH || phase == PH_SEED));
+            svc = nwait >= (int)P.svc_min || ++svc_since >= (int)P.svc_wait || drained || nwait == 0;
+            if (svc) svc_since = 0;
+        }
+        if (phase == PH_END && svc) {
             c_newton += it;
             int st = end_status;
             if (trial == 0) {
