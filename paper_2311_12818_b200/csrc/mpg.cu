@@ -1119,11 +1119,13 @@ extern "C" mpg_status mpg_debug_trace(float *buf, int64_t n_walks, int32_t strid
 // (ms/step, configs 1/2/3/4): 1 -> 66/508/337/391, 2 -> 62/497/337/386,
 // 4 -> 61.5/474/335/377, 8 -> 62.6/451/335/377: with many walks per launch the
 // primaries keep every lane busy and in-lane trials are cheaper than items, with
-// few the parallel items shorten the tail.
+// few the parallel items shorten the tail.  Re-measured in round 2 with the batched attempt
+// boundaries (configs[2], 16.8 M walks): 2 -> 292, 4 -> 268, 8 -> 243, 16 -> 229, 32 -> 225,
+// 64..1024 -> 225 ms; configs[1] (1 M walks) flat from 4 to 1024; configs[3]/[4] flat or +1 %.
 #ifdef MPG_LOCAL_TRIALS
 #define LOCAL_TRIALS(n) ((uint32_t)MPG_LOCAL_TRIALS)
 #else
-#define LOCAL_TRIALS(n) ((n) >= (int64_t)4 << 20 ? 8u : 4u)
+#define LOCAL_TRIALS(n) ((n) >= (int64_t)4 << 20 ? 32u : 4u)
 #endif
 struct MKLayout {
     uint32_t H, C;
