@@ -23,8 +23,10 @@
 // blocks (200+ regs) / 4 (128) / 6 (80) / 8 (64): configs[3] 232 / 170 / 163 /
 // 180 ms, but the mixed-length loop of configs[4] 256 / 264 / 279 / 292 ms per
 // step -> two instantiations, chosen by the sampler (MINB below).
+// (re-measured with the batched attempt boundaries of round 2: 6 / 7 / 8 blocks: configs[2] 226.4 /
+// 224.3 / 225.3 ms, configs[1] 42.8 / 42.0 / 42.7 -> 7 blocks, 72 registers)
 #ifndef MPG_WALK_MINB2
-#define MPG_WALK_MINB2 8
+#define MPG_WALK_MINB2 7
 #endif
 #ifndef MPG_WALK_MINB_LONG
 #define MPG_WALK_MINB_LONG 6   // fixed long chains (configs[3])
