@@ -25,8 +25,8 @@ for c in 2 1 4; do
   ncu -i $O/walk_cfg$c.ncu-rep --page source --csv --print-source sass > $O/walk_cfg${c}_sass.csv 2>/dev/null
   # summaries here (gpurun brings back at most 64 MiB): the report and its SASS page stay on the box
   python tools/ncu_summary.py $O/walk_cfg$c.ncu-rep $O/ncu_walk_cfg$c.json > /dev/null 2>&1
-  K=_Z6k_walkILi1EdLi4ELi8ELb0ELb0EEv6DScene7SeedCtx10WalkParams
-  [ "$c" = 1 ] && K=_Z6k_walkILi2EdLi2ELi8ELb0ELb0EEv6DScene7SeedCtx10WalkParams
+  K=_Z6k_walkILi1EdLi4ELi7ELb0ELb0EEv6DScene7SeedCtx10WalkParams
+  [ "$c" = 1 ] && K=_Z6k_walkILi2EdLi2ELi7ELb0ELb0EEv6DScene7SeedCtx10WalkParams
   [ "$c" = 4 ] && K=_Z6k_walkILi6EdLi4ELi4ELb0ELb1EEv6DScene7SeedCtx10WalkParams
   python tools/ncu_regions.py $O/walk_cfg${c}_sass.csv paper_2311_12818_b200/libmpg.so $K > $O/ncu_walk_cfg${c}_regions.txt 2>&1
   rm -f $O/walk_cfg$c.ncu-rep $O/walk_cfg${c}_sass.csv
