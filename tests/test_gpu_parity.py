@@ -800,6 +800,33 @@ def test_trial_fallbacks_give_identical_walks(caps, monkeypatch):
         assert sa["trials"] == sb["trials"] and sa["truncated"] == sb["truncated"]
 
 
+@pytest.mark.parametrize("svc", [("1", "1"), ("32", "64")])
+def test_batched_attempt_boundaries_give_identical_walks(svc, monkeypatch):
+    """k_walk serves the lanes whose attempt ended in batches (svc_min waiting lanes or
+    svc_wait passes): a scheduling choice only.  Served every pass (1/1) or
+    as late as possible (32 lanes / 64 passes), every output equals the default's bit for
+    bit (a walk's arithmetic depends on its counter-based draws alone, R13)."""
+    for mk in (lambda: W.config2(n_side=96, spp=4), lambda: W.config1(n_side=128, spp=2),
+               lambda: W.config0(n_side=32, spp=8), lambda: W.config4(n_side=64)):
+        w = mk()
+        fl = w.opts.flags | 8
+        a, sa, _ = PY.run_gpu(w, flags=fl)
+        monkeypatch.setenv("MPG_SVC_MIN", svc[0])
+        monkeypatch.setenv("MPG_SVC_WAIT", svc[1])
+        b, sb, _ = PY.run_gpu(w, flags=fl)
+        monkeypatch.delenv("MPG_SVC_MIN", raising=False)
+        monkeypatch.delenv("MPG_SVC_WAIT", raising=False)
+        for k in ("status", "iters", "trials", "G", "T", "w"):
+            assert np.array_equal(a[k], b[k]), (w.name, k)
+        conv = np.isin(a["status"], (0, 5))
+        n = a["ctype"][conv] & 15 if w.seed.mode >= 3 else np.full(int(conv.sum()), w.seed.k)
+        used = np.arange(a["pos"].shape[1])[None, :] < n[:, None]
+        assert np.array_equal(a["pos"][conv][used], b["pos"][conv][used]), w.name
+        assert np.array_equal(a["prim"][conv][used], b["prim"][conv][used]), w.name
+        for k in ("walks", "converged", "trials", "truncated", "primary_iters"):
+            assert sa[k] == sb[k], (w.name, k)
+
+
 @pytest.mark.parametrize("which,flags", [("cfg0", 0), ("cfg1", BENCH_FLAGS)])
 def test_repeated_reciprocal_estimates(which, flags):
     """recip_repeats = 4 (R x 4, R32): the summed trial counts equal the oracle's
